@@ -1,0 +1,251 @@
+/*
+ * tsb.h -- C ABI of the B200-native implicit-FEM solve path (libtsb.so).
+ *
+ * The reference (tetsim, /root/reference/pkg/src/tetsim) is pure Python +
+ * NumPy and has no native interface; each entry point below replaces one
+ * reference function on the hot path named by BASELINE.json's north_star and
+ * is cited with the reference file:line it replaces.  The Python host layer
+ * (paper_2306_05893_b200/) keeps the reference's API and calls these through
+ * ctypes; INTEGRATION.md shows the binding a tetsim maintainer would add.
+ *
+ * Conventions
+ *   - every pointer named d_* is a DEVICE pointer (cudaMalloc / torch CUDA
+ *     storage); plain pointers are host memory;
+ *   - indices are int32 (CSR row_ptr/col_ind, element connectivity), offsets
+ *     into factor storage are int64;
+ *   - every call is ordered on the caller's stream (`stream` is a
+ *     cudaStream_t passed as void*, NULL = legacy default stream) and never
+ *     synchronises unless documented (tsb_pcg_solve reads back one report);
+ *   - return value: 0 = ok, otherwise a TSB_E_* code; the message is kept
+ *     per thread and read with tsb_last_error().  Codes map to the reference
+ *     exceptions (see paper_2306_05893_b200/_lib.py).
+ *   - handles are opaque, bound to one stream at a time, not thread-safe.
+ */
+#ifndef TSB_H
+#define TSB_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TSB_ABI_VERSION 1
+
+enum tsb_status {
+    TSB_OK = 0,
+    TSB_E_ASSEMBLY = 1,       /* assembly.AssemblyError        assembly.py:42-43   */
+    TSB_E_STALE_MAPPING = 2,  /* assembly.StaleMappingError    assembly.py:46-47   */
+    TSB_E_SOLVER = 3,         /* krylov.SolverError            krylov.py:34-35     */
+    TSB_E_LIFECYCLE = 4,      /* ndprecond.LifecycleError      ndprecond.py:65-66  */
+    TSB_E_CUDA = 5,           /* CUDA runtime failure (RuntimeError)               */
+    TSB_E_MODEL = 6,          /* models.ModelError             models.py:37-38     */
+    TSB_E_ARG = 7,            /* bad argument (ValueError)                         */
+    TSB_E_PRECOND = 8         /* ndprecond.PrecondError        ndprecond.py:57-58  */
+};
+
+int tsb_abi_version(void);
+/* Copies the calling thread's last error message into buf (NUL-terminated). */
+int tsb_last_error(char *buf, size_t len);
+/* Number of kernels libtsb launched in this process (for bench evidence). */
+int64_t tsb_launch_count(void);
+
+/* ------------------------------------------------------------------------
+ * CSR SpMV  y = A x                        replaces krylov.spmv  krylov.py:73-96
+ * Bit-identical to the reference: per row y_i = p_0 + pairwise(p_1..p_{L-1})
+ * with p_k = a_k * x[col_k], i.e. np.add.reduceat's summation order
+ * (krylov.py:63-70).
+ * ---------------------------------------------------------------------- */
+int tsb_spmv(int64_t nrows, const int32_t *d_row_ptr, const int32_t *d_col_ind,
+             const double *d_values, const double *d_x, double *d_y, void *stream);
+
+/* Diagonal of a CSR matrix        replaces CsrMatrix.diagonal  assembly.py:154-159 */
+int tsb_csr_diagonal(int64_t nrows, int64_t ncols, const int32_t *d_row_ptr,
+                     const int32_t *d_col_ind, const double *d_values, double *d_diag,
+                     void *stream);
+
+/* ------------------------------------------------------------------------
+ * Triplet merge through a compression mapping
+ *                       replaces assembly.compress / compress_parallel
+ *                       assembly.py:322-376
+ * values[s] = sum over kept triplets t with slot s, ascending t, of
+ *             coeffs[t]*vals[t]   (coeffs may be NULL), starting from 0.0,
+ * which is np.bincount's order (assembly.py:341); pinned diagonal slots := 1.0.
+ * d_slot_ptr (nnz+1) / d_slot_trip: kept triplet ids grouped by slot.
+ * ---------------------------------------------------------------------- */
+int tsb_compress(int64_t nnz, const int64_t *d_slot_ptr, const int32_t *d_slot_trip,
+                 const double *d_vals, const double *d_coeffs,
+                 const int32_t *d_fixed_diag_slots, int64_t nfixed, double *d_values,
+                 void *stream);
+
+/* ------------------------------------------------------------------------
+ * Fused corotational assembly         replaces
+ *   BackwardEulerIntegrator.assemble_system  integrator.py:145-169
+ *   corotational_forces_and_stiffness        models.py:200-238
+ *   MatrixAssembler.finish / compress        assembly.py:407-419, 332-343
+ * One element pass (F, polar R, rotated gradients, f_e = R Ke (R^T x - x0),
+ * K v) followed by deterministic gathers into the fixed CSR pattern (slot
+ * sums in ascending triplet order, mass triplets first) and into the nodal
+ * vectors (ascending element order, np.bincount's order, models.py:192-193).
+ * All arrays are SoA on the device and owned by the caller.
+ * ---------------------------------------------------------------------- */
+typedef struct tsb_asm_plan {
+    int64_t n_nodes;            /* N                                         */
+    int64_t n_elems;            /* m                                         */
+    int64_t n_blocks;           /* CSR 3x3 node blocks with >=1 contribution  */
+    int64_t nnz;                /* CSR nnz                                   */
+    int64_t n_fixed_slots;      /* pinned diagonal slots                     */
+    const int32_t *d_conn;      /* [4][m] element node ids                   */
+    const double *d_grads;      /* [12][m] rest shape gradients (a*3+i)      */
+    const double *d_vol;        /* [m] rest volumes                          */
+    const double *d_mass_share; /* [m] rho*V/4 (integrator._mass_vals)       */
+    const double *d_rest;       /* [3N] rest positions                       */
+    const double *d_mass_diag;  /* [3N] lumped mass diagonal                 */
+    const double *d_gravity;    /* [3N] gravity force M g                    */
+    const uint8_t *d_fixed_dof; /* [3N] 1 = pinned                           */
+    const int32_t *d_blk;       /* [nb][4] slot0, rowlen, list_begin, list_end */
+    const int32_t *d_blk_list;  /* contributions e*16 + a*4 + b, sorted by (block, e) */
+    const int32_t *d_node_ptr;  /* [N+1] incidence offsets                   */
+    const int32_t *d_node_list; /* e*4 + a, ascending e per node             */
+    const int32_t *d_fixed_slots; /* [n_fixed_slots]                         */
+    double *d_work;             /* [36][m] scratch: rotated grads, f_e, K v_e */
+    int32_t *d_flags;           /* [4] device status words                   */
+} tsb_asm_plan;
+
+typedef struct tsb_asm_coeffs {
+    double lam, mu;             /* Lame constants (models.py:57-64)          */
+    double h;                   /* dt                                        */
+    double rayleigh_stiffness;  /* beta                                      */
+    double rayleigh_mass;       /* alpha                                     */
+    double cm, ck;              /* per-triplet coefficients (integrator.py:135-143) */
+    int32_t linear;             /* 1: R := I (linear elastic)                */
+    int32_t want_matrix;        /* 0: forces only (model.internal_forces)    */
+} tsb_asm_coeffs;
+
+/* x, v: [3N] positions/velocities; f_ext_state: [3N] state.f_ext.
+ * Outputs: d_values [nnz], d_b, d_f_int, d_kv, d_f_ext [3N] (NULL allowed for
+ * d_values when want_matrix == 0, and for d_b/d_f_ext).  d_flags[0] is set
+ * to 1 when a position or deformation gradient is non-finite (ModelError);
+ * the caller reads it back when it reads the solve report. */
+int tsb_assemble_corot(const tsb_asm_plan *plan, const tsb_asm_coeffs *coeffs,
+                       const double *d_x, const double *d_v, const double *d_f_ext_state,
+                       double *d_values, double *d_b, double *d_f_int, double *d_kv,
+                       double *d_f_ext, void *stream);
+
+/* Kinematic update of one implicit step   replaces integrator.py:192-208
+ * d_flags[1] := 1 if an acceleration is non-finite (StepError); pinned DOFs
+ * get accel 0 and keep v, x; v' = v + h a, x' = x + h v' (NumPy rounding). */
+int tsb_advance(int64_t n_dof, const double *d_accel, const double *d_v, const double *d_x,
+                const uint8_t *d_fixed_dof, double h, double *d_acc_out, double *d_v_out,
+                double *d_x_out, int32_t *d_flags, void *stream);
+
+/* Element stiffness blocks R Ke R^T as the reference emits them
+ * (models.py:231, 196-197): d_kblocks [m][144], row-major per element.
+ * Used only by the API-compatibility path that fills a TripletStream. */
+int tsb_element_blocks(const tsb_asm_plan *plan, const tsb_asm_coeffs *coeffs,
+                       const double *d_x, double *d_kblocks, void *stream);
+
+/* ------------------------------------------------------------------------
+ * Nested-dissection LDL^T preconditioner apply
+ *   replaces solve_lower  ndprecond.py:647-671 (+ _forward_block 623-631)
+ *            solve_upper  ndprecond.py:674-691 (+ _backward_block 634-644)
+ *            apply        ndprecond.py:694-700, LdlFactors.apply 497-498
+ * Factor values come from the host factorisation (ldlt_factor,
+ * ndprecond.py:501-572) and are packed by the host into the layout below.
+ * ---------------------------------------------------------------------- */
+typedef struct tsb_ldlt_desc {
+    int64_t n;
+    int64_t n_blocks;
+    int64_t n_levels;
+    int32_t tile;               /* diagonal tile width t (<= 32)                  */
+    int32_t max_block;          /* largest block size m                          */
+    /* per block, in factor order (ascending start; levels are contiguous runs) */
+    const int32_t *d_blk_start;   /* [nb] */
+    const int32_t *d_blk_size;    /* [nb] */
+    const int32_t *d_blk_nanc;    /* [nb] */
+    const int64_t *d_blk_l11;     /* [nb] offset of the packed column panels      */
+    const int64_t *d_blk_l21;     /* [nb] offset of the |anc| x m row-major panel  */
+    const int64_t *d_blk_tinv;    /* [nb] offset of the t x t tile inverses        */
+    const int64_t *d_blk_anc;     /* [nb] offset into d_anc / contribution buffer  */
+    const int32_t *h_level_ptr;   /* HOST [n_levels+1] block ranges per level      */
+    const double *d_l11;          /* column panels: tile it -> rows [t1,m) x t     */
+    const double *d_l21;
+    const double *d_tinv;
+    const int32_t *d_anc;         /* permuted ancestor row ids                     */
+    const int64_t *d_cin_ptr;     /* [n+1] contributions into permuted row k       */
+    const int32_t *d_cin_idx;     /* indices into the contribution buffer          */
+    const double *d_d;            /* [n] D                                          */
+    const int32_t *d_perm;        /* [n] perm[k] = original index at position k    */
+    double *d_cbuf;               /* scratch [sum |anc|]                           */
+    double *d_y;                  /* scratch [n]                                   */
+} tsb_ldlt_desc;
+
+typedef struct tsb_ldlt *tsb_ldlt_t;
+
+int tsb_ldlt_create(const tsb_ldlt_desc *desc, tsb_ldlt_t *out);
+int tsb_ldlt_destroy(tsb_ldlt_t h);
+/* y = L^{-1} r, both in permuted order                 (solve_lower) */
+int tsb_ldlt_lower(tsb_ldlt_t h, const double *d_r, double *d_y, void *stream);
+/* z = L^{-T} w, both in permuted order                 (solve_upper) */
+int tsb_ldlt_upper(tsb_ldlt_t h, const double *d_w, double *d_z, void *stream);
+/* z = P^T L^{-T} D^{-1} L^{-1} P r, original order     (apply)       */
+int tsb_ldlt_apply(tsb_ldlt_t h, const double *d_r, double *d_z, void *stream);
+
+/* ------------------------------------------------------------------------
+ * Device-resident preconditioned CG      replaces krylov.pcg / krylov.cg
+ *                                        krylov.py:120-163
+ * The iteration loop runs inside one CUDA graph with a conditional WHILE
+ * node: alpha, beta and the convergence test live on the device, no host
+ * round-trip per iteration; one report is read back per solve.
+ * ---------------------------------------------------------------------- */
+enum tsb_precond_kind {
+    TSB_PRECOND_IDENTITY = 0,   /* IdentityPreconditioner  krylov.py:99-101  */
+    TSB_PRECOND_JACOBI = 1,     /* jacobi_precond           krylov.py:104-117 */
+    TSB_PRECOND_LDLT = 2        /* LdlFactors.apply         ndprecond.py:497  */
+};
+
+typedef struct tsb_report {     /* krylov.SolveReport  krylov.py:55-60       */
+    int64_t iterations;
+    double final_residual;
+    int32_t converged;
+    int32_t status;             /* 0 ok, 3 zero diagonal (SolverError)        */
+    int64_t zero_diag_row;
+} tsb_report;
+
+typedef struct tsb_pcg *tsb_pcg_t;
+
+int tsb_pcg_create(int64_t n, tsb_pcg_t *out);
+int tsb_pcg_destroy(tsb_pcg_t h);
+/* Solve A x = b.  d_x0 may be NULL (x0 = 0).  precond_kind selects the
+ * preconditioner; ldlt is required for TSB_PRECOND_LDLT.  For Jacobi,
+ * d_inv_diag (may be NULL) supplies 1/diag, otherwise the diagonal is
+ * extracted from the matrix and inverted on the device.  d_x receives the
+ * solution.  When `report` is non-NULL the call synchronises the stream
+ * once and fills it; otherwise the report stays on the device
+ * (tsb_pcg_report reads it later). */
+int tsb_pcg_solve(tsb_pcg_t h, int64_t nrows, const int32_t *d_row_ptr,
+                  const int32_t *d_col_ind, const double *d_values, const double *d_b,
+                  const double *d_x0, double *d_x, int32_t precond_kind, tsb_ldlt_t ldlt,
+                  const double *d_inv_diag, double tol, int64_t max_iterations,
+                  tsb_report *report, void *stream);
+int tsb_pcg_report(tsb_pcg_t h, tsb_report *report, void *stream);
+
+/* ------------------------------------------------------------------------
+ * Host setup (not on the per-iteration path): nested-dissection ordering
+ *   replaces nested_dissection / _dissect / _greedy_cover / _pseudo_peripheral
+ *   ndprecond.py:107-267  (same algorithm and tie-breaking, so the
+ *   permutation and block tree are identical to the reference's)
+ * Graph: CSR adjacency (sorted neighbour lists, no self loops).
+ * Outputs (host, caller-allocated with capacity n for the per-block arrays
+ * and n for children): perm[n], blocks in creation order.
+ * ---------------------------------------------------------------------- */
+int tsb_nested_dissection(int64_t n, const int64_t *indptr, const int64_t *indices,
+                          int64_t leaf_threshold, int64_t *perm, int64_t *n_blocks,
+                          int64_t *blk_start, int64_t *blk_stop, int64_t *blk_tree_start,
+                          int32_t *blk_is_sep, int64_t *blk_child_ptr, int64_t *blk_child);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TSB_H */

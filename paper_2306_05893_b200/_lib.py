@@ -1,0 +1,219 @@
+"""ctypes binding of libtsb.so (include/tsb.h) plus the device-buffer helpers.
+
+The CUDA path is the product: if the library or a GPU is missing, every
+device entry point raises instead of falling back to a CPU implementation.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+from pathlib import Path
+
+import numpy as np
+
+_PKG = Path(__file__).resolve().parent
+LIB_PATH = _PKG / "libtsb.so"
+
+TSB_OK = 0
+TSB_E_ASSEMBLY = 1
+TSB_E_STALE_MAPPING = 2
+TSB_E_SOLVER = 3
+TSB_E_LIFECYCLE = 4
+TSB_E_CUDA = 5
+TSB_E_MODEL = 6
+TSB_E_ARG = 7
+TSB_E_PRECOND = 8
+
+PRECOND_IDENTITY = 0
+PRECOND_JACOBI = 1
+PRECOND_LDLT = 2
+
+c_i64 = C.c_int64
+c_i32 = C.c_int32
+c_vp = C.c_void_p
+
+
+class AsmPlan(C.Structure):
+    _fields_ = [
+        ("n_nodes", c_i64), ("n_elems", c_i64), ("n_blocks", c_i64), ("nnz", c_i64),
+        ("n_fixed_slots", c_i64),
+        ("d_conn", c_vp), ("d_grads", c_vp), ("d_vol", c_vp), ("d_mass_share", c_vp),
+        ("d_rest", c_vp), ("d_mass_diag", c_vp), ("d_gravity", c_vp), ("d_fixed_dof", c_vp),
+        ("d_blk", c_vp), ("d_blk_list", c_vp), ("d_node_ptr", c_vp), ("d_node_list", c_vp),
+        ("d_fixed_slots", c_vp), ("d_work", c_vp), ("d_flags", c_vp),
+    ]
+
+
+class AsmCoeffs(C.Structure):
+    _fields_ = [
+        ("lam", C.c_double), ("mu", C.c_double), ("h", C.c_double),
+        ("rayleigh_stiffness", C.c_double), ("rayleigh_mass", C.c_double),
+        ("cm", C.c_double), ("ck", C.c_double), ("linear", c_i32), ("want_matrix", c_i32),
+    ]
+
+
+class LdltDesc(C.Structure):
+    _fields_ = [
+        ("n", c_i64), ("n_blocks", c_i64), ("n_levels", c_i64), ("tile", c_i32), ("max_block", c_i32),
+        ("d_blk_start", c_vp), ("d_blk_size", c_vp), ("d_blk_nanc", c_vp),
+        ("d_blk_l11", c_vp), ("d_blk_l21", c_vp), ("d_blk_tinv", c_vp), ("d_blk_anc", c_vp),
+        ("h_level_ptr", c_vp),
+        ("d_l11", c_vp), ("d_l21", c_vp), ("d_tinv", c_vp), ("d_anc", c_vp),
+        ("d_cin_ptr", c_vp), ("d_cin_idx", c_vp), ("d_d", c_vp), ("d_perm", c_vp),
+        ("d_cbuf", c_vp), ("d_y", c_vp),
+    ]
+
+
+class Report(C.Structure):
+    _fields_ = [
+        ("iterations", c_i64), ("final_residual", C.c_double), ("converged", c_i32),
+        ("status", c_i32), ("zero_diag_row", c_i64),
+    ]
+
+
+# every symbol include/tsb.h declares, with its ctypes signature
+_SIGNATURES = {
+    "tsb_abi_version": (C.c_int, []),
+    "tsb_last_error": (C.c_int, [C.c_char_p, C.c_size_t]),
+    "tsb_launch_count": (c_i64, []),
+    "tsb_spmv": (C.c_int, [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "tsb_csr_diagonal": (C.c_int, [c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "tsb_compress": (C.c_int, [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp]),
+    "tsb_assemble_corot": (C.c_int, [C.POINTER(AsmPlan), C.POINTER(AsmCoeffs), c_vp, c_vp, c_vp,
+                                     c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "tsb_element_blocks": (C.c_int, [C.POINTER(AsmPlan), C.POINTER(AsmCoeffs), c_vp, c_vp, c_vp]),
+    "tsb_advance": (C.c_int, [c_i64, c_vp, c_vp, c_vp, c_vp, C.c_double, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "tsb_ldlt_create": (C.c_int, [C.POINTER(LdltDesc), C.POINTER(c_vp)]),
+    "tsb_ldlt_destroy": (C.c_int, [c_vp]),
+    "tsb_ldlt_lower": (C.c_int, [c_vp, c_vp, c_vp, c_vp]),
+    "tsb_ldlt_upper": (C.c_int, [c_vp, c_vp, c_vp, c_vp]),
+    "tsb_ldlt_apply": (C.c_int, [c_vp, c_vp, c_vp, c_vp]),
+    "tsb_pcg_create": (C.c_int, [c_i64, C.POINTER(c_vp)]),
+    "tsb_pcg_destroy": (C.c_int, [c_vp]),
+    "tsb_pcg_solve": (C.c_int, [c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, c_vp,
+                                c_vp, C.c_double, c_i64, C.POINTER(Report), c_vp]),
+    "tsb_pcg_report": (C.c_int, [c_vp, C.POINTER(Report), c_vp]),
+    "tsb_nested_dissection": (C.c_int, [c_i64, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp,
+                                        c_vp, c_vp, c_vp]),
+}
+
+_lib = None
+_lock = threading.Lock()
+
+
+class NativeLibraryError(RuntimeError):
+    """libtsb.so is missing or incompatible (build it with __graft_entry__.build())."""
+
+
+def load() -> C.CDLL:
+    """Load libtsb.so (raises NativeLibraryError; there is no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        path = Path(os.environ.get("TSB_LIB", LIB_PATH))
+        if not path.exists():
+            raise NativeLibraryError(
+                f"{path} not found: build it with `python -m paper_2306_05893_b200.build`"
+            )
+        lib = C.CDLL(str(path))
+        for name, (res, args) in _SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        if lib.tsb_abi_version() != 1:
+            raise NativeLibraryError("libtsb ABI version mismatch")
+        _lib = lib
+    return _lib
+
+
+def exported_symbols():
+    return list(_SIGNATURES)
+
+
+def last_error() -> str:
+    buf = C.create_string_buffer(4096)
+    load().tsb_last_error(buf, len(buf))
+    return buf.value.decode(errors="replace")
+
+
+def check(status: int, what: str = ""):
+    """Map a tsb status code to the reference's exception types."""
+    if status == TSB_OK:
+        return
+    msg = last_error() or what
+    from . import assembly, krylov, models, ndprecond  # local: avoid import cycles
+
+    exc = {
+        TSB_E_ASSEMBLY: assembly.AssemblyError,
+        TSB_E_STALE_MAPPING: assembly.StaleMappingError,
+        TSB_E_SOLVER: krylov.SolverError,
+        TSB_E_LIFECYCLE: ndprecond.LifecycleError,
+        TSB_E_MODEL: models.ModelError,
+        TSB_E_PRECOND: ndprecond.PrecondError,
+        TSB_E_ARG: ValueError,
+    }.get(status, RuntimeError)
+    raise exc(f"{what}: {msg}" if what else msg)
+
+
+def launch_count() -> int:
+    return int(load().tsb_launch_count())
+
+
+# ---------------------------------------------------------------------------
+# torch buffer helpers (torch is used for device memory and streams only)
+# ---------------------------------------------------------------------------
+
+def torch():
+    import torch as _t
+
+    return _t
+
+
+def require_cuda():
+    t = torch()
+    if not t.cuda.is_available():
+        raise NativeLibraryError("the B200 path needs a CUDA device; no CPU fallback exists")
+    load()
+    return t
+
+
+def is_cuda_ready() -> bool:
+    try:
+        return bool(torch().cuda.is_available()) and load() is not None
+    except Exception:
+        return False
+
+
+def stream_ptr(stream=None) -> int:
+    t = torch()
+    s = stream if stream is not None else t.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+def ptr(tensor) -> int | None:
+    return None if tensor is None else int(tensor.data_ptr())
+
+
+def to_device(a, dtype=None, device="cuda"):
+    """numpy/torch -> contiguous CUDA tensor (no copy if already there)."""
+    t = torch()
+    if isinstance(a, t.Tensor):
+        out = a.to(device=device, dtype=dtype) if dtype is not None else a.to(device=device)
+        return out.contiguous()
+    arr = np.ascontiguousarray(a)
+    if dtype is not None:
+        arr = arr.astype(np.dtype(str(dtype).replace("torch.", "")), copy=False)
+    return t.from_numpy(arr).to(device=device, non_blocking=False)
+
+
+def is_tensor(a) -> bool:
+    try:
+        import torch as _t
+    except Exception:  # pragma: no cover
+        return False
+    return isinstance(a, _t.Tensor)

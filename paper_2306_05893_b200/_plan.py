@@ -1,0 +1,201 @@
+"""Device-side assembly plan: HBM layout of the mesh, the fixed CSR pattern and
+the deterministic gather lists (host setup, built once per mesh/BC).
+
+Pattern contract (bit-exact with the reference's build_pattern,
+assembly.py:235-312): with whole pinned nodes the pattern is an exact 3x3
+block pattern over free nodes -- row 3I+c holds columns 3J+d for every free
+node J sharing an element with free node I (J ascending, d inner); pinned
+DOFs keep one diagonal slot.  It is derived here straight from the element
+topology (no 156 m-entry triplet sort), and `tests/` check it equals the
+reference's triplet-built pattern.
+
+HBM layout (all int32 indices):
+  conn      [4][m]      element node ids (SoA -> coalesced per node slot)
+  grads     [m][12]     rest gradients, 96 B per tet (6 x 16 B loads)
+  vol, share [m]        rest volume, rho V / 4
+  blk       [nb][4]     slot0, row length, list begin, list end per 3x3 block
+  blk_list  [16 m']     e*16 + a*4 + b, grouped by block, ascending e
+  node_ptr/node_list    e*4 + a per node, ascending e
+  work      [m][36]     rotated gradients, f_e, (K v)_e (element pass output)
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _lib
+
+
+def topology_pattern(mesh):
+    """-> dict with row_ptr, col_ind, fixed_diag_slots, block arrays, node lists."""
+    N = mesh.node_count
+    el = mesh.elements
+    m = len(el)
+    pinned = np.zeros(N, dtype=bool)
+    pinned[mesh.fixed_nodes] = True
+
+    a_idx = np.repeat(np.arange(4), 4)
+    b_idx = np.tile(np.arange(4), 4)
+    I = el[:, a_idx].ravel()
+    J = el[:, b_idx].ravel()
+    code = (np.arange(m, dtype=np.int64)[:, None] * 16 + a_idx * 4 + b_idx).ravel()
+    keep = ~(pinned[I] | pinned[J])
+    I, J, code = I[keep], J[keep], code[keep]
+    key = I * N + J
+    order = np.argsort(key, kind="stable")
+    key = key[order]
+    code = code[order]
+    first = np.ones(len(key), dtype=bool)
+    first[1:] = key[1:] != key[:-1]
+    starts = np.flatnonzero(first)
+    ends = np.append(starts[1:], len(key))
+    bkey = key[starts]
+    bI, bJ = bkey // N, bkey % N
+    nb_row = np.bincount(bI, minlength=N)
+    nblk = len(bkey)
+
+    rowlen = np.where(pinned, 1, 3 * nb_row)           # per node, each of its 3 rows
+    row_len_dof = np.repeat(rowlen, 3)
+    row_ptr = np.zeros(3 * N + 1, dtype=np.int64)
+    np.cumsum(row_len_dof, out=row_ptr[1:])
+    nnz = int(row_ptr[-1])
+
+    first_blk_of_row = np.zeros(N + 1, dtype=np.int64)
+    np.cumsum(nb_row, out=first_blk_of_row[1:])
+    k_in_row = np.arange(nblk) - first_blk_of_row[bI]
+    slot0 = row_ptr[3 * bI] + 3 * k_in_row
+    brow = 3 * nb_row[bI]
+
+    col_ind = np.empty(nnz, dtype=np.int64)
+    for c in range(3):
+        for d in range(3):
+            col_ind[slot0 + c * brow + d] = 3 * bJ + d
+    fixed_dofs = mesh.fixed_dofs()
+    fixed_slots = row_ptr[fixed_dofs]
+    col_ind[fixed_slots] = fixed_dofs
+
+    node_flat = el.ravel()
+    norder = np.argsort(node_flat, kind="stable")
+    node_ptr = np.zeros(N + 1, dtype=np.int64)
+    np.cumsum(np.bincount(node_flat, minlength=N), out=node_ptr[1:])
+
+    for a in (row_ptr, col_ind, fixed_slots):
+        a.setflags(write=False)
+    return {
+        "row_ptr": row_ptr, "col_ind": col_ind, "fixed_diag_slots": fixed_slots,
+        "blk": np.stack([slot0, brow, starts, ends], axis=1),
+        "blk_list": code, "node_ptr": node_ptr, "node_list": norder,
+    }
+
+
+def _i32(a):
+    a = np.asarray(a)
+    if a.size and (a.max() >= 2**31 or a.min() < -(2**31)):
+        raise OverflowError("index exceeds int32 range of the device layout")
+    return np.ascontiguousarray(a, dtype=np.int32)
+
+
+class AssemblyPlan:
+    """Device buffers + the C struct handed to tsb_assemble_corot."""
+
+    def __init__(self, precomp, pattern=None, mass_share=None, mass_diag=None, gravity=None,
+                 fixed_dof=None, n_nodes=None):
+        t = _lib.require_cuda()
+        dev = "cuda"
+        el = precomp.elements
+        m = len(el)
+        N = len(precomp.rest_positions) if n_nodes is None else n_nodes
+        self.m, self.N = m, N
+
+        def up(a, dtype):
+            return t.from_numpy(np.ascontiguousarray(a, dtype=dtype)).to(dev)
+
+        self.conn = t.from_numpy(_i32(el.T)).to(dev)
+        self.grads = up(precomp.grads.reshape(m, 12), np.float64)
+        self.vol = up(precomp.volume, np.float64)
+        self.rest = up(precomp.rest_positions.reshape(-1), np.float64)
+        self.share = up(mass_share if mass_share is not None else np.zeros(m), np.float64)
+        self.mass_diag = up(mass_diag if mass_diag is not None else np.zeros(3 * N), np.float64)
+        self.gravity = up(gravity if gravity is not None else np.zeros(3 * N), np.float64)
+        fd = np.zeros(3 * N, dtype=np.uint8)
+        if fixed_dof is not None:
+            fd[fixed_dof] = 1
+        self.fixed_dof = up(fd, np.uint8)
+        self.work = t.empty(max(m, 1) * 36, dtype=t.float64, device=dev)
+        self.flags = t.zeros(4, dtype=t.int32, device=dev)
+        self.pattern = pattern
+        if pattern is not None:
+            self.blk = t.from_numpy(_i32(pattern["blk"])).to(dev)
+            self.blk_list = t.from_numpy(_i32(pattern["blk_list"])).to(dev)
+            self.fixed_slots = t.from_numpy(_i32(pattern["fixed_diag_slots"])).to(dev)
+            node_ptr, node_list = pattern["node_ptr"], pattern["node_list"]
+            nb, nnz, nfix = len(pattern["blk"]), len(pattern["col_ind"]), len(pattern["fixed_diag_slots"])
+        else:
+            self.blk = self.blk_list = self.fixed_slots = None
+            flat = el.ravel()
+            node_list = np.argsort(flat, kind="stable")
+            node_ptr = np.zeros(N + 1, dtype=np.int64)
+            np.cumsum(np.bincount(flat, minlength=N), out=node_ptr[1:])
+            nb = nnz = nfix = 0
+        self.node_ptr = t.from_numpy(_i32(node_ptr)).to(dev)
+        self.node_list = t.from_numpy(_i32(node_list)).to(dev)
+        P = _lib.ptr
+        self.c = _lib.AsmPlan(
+            n_nodes=N, n_elems=m, n_blocks=nb, nnz=nnz, n_fixed_slots=nfix,
+            d_conn=P(self.conn), d_grads=P(self.grads), d_vol=P(self.vol), d_mass_share=P(self.share),
+            d_rest=P(self.rest), d_mass_diag=P(self.mass_diag), d_gravity=P(self.gravity),
+            d_fixed_dof=P(self.fixed_dof), d_blk=P(self.blk), d_blk_list=P(self.blk_list),
+            d_node_ptr=P(self.node_ptr), d_node_list=P(self.node_list),
+            d_fixed_slots=P(self.fixed_slots), d_work=P(self.work), d_flags=P(self.flags),
+        )
+        self.lame = precomp.lame
+
+    @classmethod
+    def for_model(cls, precomp):
+        return cls(precomp)
+
+    def coeffs(self, h=0.0, beta=0.0, alpha=0.0, cm=1.0, ck=1.0, linear=False, want_matrix=True):
+        lam, mu = self.lame
+        return _lib.AsmCoeffs(lam=lam, mu=mu, h=h, rayleigh_stiffness=beta, rayleigh_mass=alpha,
+                              cm=cm, ck=ck, linear=int(linear), want_matrix=int(want_matrix))
+
+    def run(self, coeffs, x, v, f_ext_state, values, b, f_int, kv, f_ext):
+        import ctypes as C
+
+        P = _lib.ptr
+        _lib.check(_lib.load().tsb_assemble_corot(
+            C.byref(self.c), C.byref(coeffs), P(x), P(v), P(f_ext_state), P(values), P(b),
+            P(f_int), P(kv), P(f_ext), _lib.stream_ptr()), "assemble")
+
+    def element_pass(self, positions, velocities, want_blocks=False, linear=False):
+        """Model-level pass (no matrix): (f, kv, kblocks|None) in the caller's array kind."""
+        import ctypes as C
+
+        t = _lib.torch()
+        host = not _lib.is_tensor(positions)
+        x = _lib.to_device(np.asarray(positions, dtype=np.float64).reshape(-1) if host
+                           else positions.reshape(-1), t.float64)
+        v = None
+        if velocities is not None:
+            v = _lib.to_device(np.asarray(velocities, dtype=np.float64).reshape(-1)
+                               if not _lib.is_tensor(velocities) else velocities.reshape(-1), t.float64)
+        n = 3 * self.N
+        f = t.empty(n, dtype=t.float64, device="cuda")
+        kv = t.empty(n, dtype=t.float64, device="cuda")
+        co = self.coeffs(linear=linear, want_matrix=False)
+        self.flags.zero_()
+        vz = v if v is not None else t.zeros(n, dtype=t.float64, device="cuda")
+        self.run(co, x, vz, None, None, None, f, kv, None)
+        kb = None
+        if want_blocks:
+            kb = t.empty(self.m * 144, dtype=t.float64, device="cuda")
+            _lib.check(_lib.load().tsb_element_blocks(C.byref(self.c), C.byref(co), _lib.ptr(x),
+                                                      _lib.ptr(kb), _lib.stream_ptr()), "element_blocks")
+        if int(self.flags[0].item()):
+            from .models import ModelError
+
+            raise ModelError("non-finite positions")
+        if host:
+            return (f.cpu().numpy(), kv.cpu().numpy() if v is not None else None,
+                    kb.cpu().numpy().reshape(self.m, 12, 12) if kb is not None else None)
+        return f, (kv if v is not None else None), (kb.view(self.m, 12, 12) if kb is not None else None)

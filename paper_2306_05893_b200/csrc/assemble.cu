@@ -1,0 +1,391 @@
+// Fused corotational assembly into a fixed CSR pattern.
+//
+// Replaces, on the device, the per-step work of
+//   BackwardEulerIntegrator.assemble_system     integrator.py:145-169
+//   corotational_forces_and_stiffness           models.py:200-238
+//   polar_rotations                             models.py:174-189
+//   MatrixAssembler.finish -> compress          assembly.py:407-419, 332-343
+//
+// Three kernels, no atomics, fixed summation order:
+//   1. elem_kernel   one thread per tetrahedron: F = sum_a x_a g_a^T, Newton
+//                    polar R <- (R + R^-T)/2, rotated gradients g^_a = R g_a,
+//                    f_e = R Ke (R^T x - x0) and (K v)_e = R Ke R^T v in
+//                    stress form (no 12x12 Ke is ever read: 104 B of rest data
+//                    per tet instead of 1,152 B).
+//   2. block_kernel  one thread per 3x3 node block of the CSR pattern: sums
+//                    cm*mass (diagonal blocks) then ck*(R Ke R^T)_ab over the
+//                    contributing elements in ascending element order -- the
+//                    ascending-triplet order np.bincount uses
+//                    (assembly.py:341), so slot sums follow the reference's
+//                    association exactly.  Block entry (i,j) of element e:
+//                    V (lam g^_a,i g^_b,j + mu g^_a,j g^_b,i + mu (g_a.g_b) d_ij)
+//   3. node_kernel   one thread per node: f_int and K v gathered over incident
+//                    elements in ascending order (np.bincount order,
+//                    models.py:192-193), then
+//                    b = f_ext - f_int - (h+beta) K v - alpha M v, b[pinned]=0
+//                    (integrator.py:158-162), every operation rounded as NumPy
+//                    rounds it.
+#include "tsb_common.cuh"
+
+namespace tsb {
+
+constexpr int kWork = 36;  // per-element scratch: g^[12], f_e[12], (Kv)_e[12]
+
+__device__ __forceinline__ bool finite3(double a, double b, double c) {
+    return isfinite(a) && isfinite(b) && isfinite(c);
+}
+
+// R <- (R + R^{-T}) / 2 until max |dR| < tol (models.py:174-189), per element.
+__device__ __forceinline__ void polar(const double F[9], double R[9]) {
+#pragma unroll
+    for (int k = 0; k < 9; ++k) R[k] = F[k];
+    for (int it = 0; it < 50; ++it) {
+        // cofactor matrix C: inv(R)^T = C / det
+        double c00 = R[4] * R[8] - R[5] * R[7];
+        double c01 = R[5] * R[6] - R[3] * R[8];
+        double c02 = R[3] * R[7] - R[4] * R[6];
+        double c10 = R[2] * R[7] - R[1] * R[8];
+        double c11 = R[0] * R[8] - R[2] * R[6];
+        double c12 = R[1] * R[6] - R[0] * R[7];
+        double c20 = R[1] * R[5] - R[2] * R[4];
+        double c21 = R[2] * R[3] - R[0] * R[5];
+        double c22 = R[0] * R[4] - R[1] * R[3];
+        double det = R[0] * c00 + R[1] * c01 + R[2] * c02;
+        double id = 1.0 / det;
+        double C[9] = {c00, c01, c02, c10, c11, c12, c20, c21, c22};
+        double delta = 0.0;
+#pragma unroll
+        for (int k = 0; k < 9; ++k) {
+            double nr = 0.5 * (R[k] + C[k] * id);
+            delta = fmax(delta, fabs(nr - R[k]));
+            R[k] = nr;
+        }
+        if (delta < 1e-12) break;
+    }
+}
+
+// (Ke u)_a = V sigma g_a with sigma = lam tr(H) I + mu (H + H^T), H = sum_b u_b g_b^T.
+__device__ __forceinline__ void ke_apply(const double u[12], const double g[12], double V,
+                                         double lam, double mu, double out[12]) {
+    double H[9];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+            H[3 * i + j] = u[i] * g[j] + u[3 + i] * g[3 + j] + u[6 + i] * g[6 + j] + u[9 + i] * g[9 + j];
+    const double tr = H[0] + H[4] + H[8];
+    double S[9];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) S[3 * i + j] = mu * (H[3 * i + j] + H[3 * j + i]) + (i == j ? lam * tr : 0.0);
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+            out[3 * a + i] = V * (S[3 * i] * g[3 * a] + S[3 * i + 1] * g[3 * a + 1] + S[3 * i + 2] * g[3 * a + 2]);
+}
+
+__global__ void __launch_bounds__(128)
+elem_kernel(int64_t m, const int32_t *__restrict__ conn, const double *__restrict__ grads,
+            const double *__restrict__ vol, const double *__restrict__ rest,
+            const double *__restrict__ x, const double *__restrict__ v, double lam, double mu,
+            int linear, double *__restrict__ work, int32_t *__restrict__ flags) {
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e >= m) return;
+    int nd[4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) nd[a] = __ldg(conn + a * m + e);
+    double g[12], xe[12], ve[12], x0[12];
+    const double2 *g2 = reinterpret_cast<const double2 *>(grads + e * 12);
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+        double2 t = __ldg(g2 + k);
+        g[2 * k] = t.x;
+        g[2 * k + 1] = t.y;
+    }
+    bool ok = true;
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            xe[3 * a + i] = __ldg(x + 3 * nd[a] + i);
+            ve[3 * a + i] = v ? __ldg(v + 3 * nd[a] + i) : 0.0;
+            x0[3 * a + i] = __ldg(rest + 3 * nd[a] + i);
+        }
+        ok = ok && finite3(xe[3 * a], xe[3 * a + 1], xe[3 * a + 2]);
+    }
+    if (!ok) atomicOr(flags, 1);
+    const double V = __ldg(vol + e);
+
+    double R[9];
+    if (linear) {
+#pragma unroll
+        for (int k = 0; k < 9; ++k) R[k] = (k % 4 == 0) ? 1.0 : 0.0;
+    } else {
+        double F[9];
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+            for (int j = 0; j < 3; ++j)
+                F[3 * i + j] = xe[i] * g[j] + xe[3 + i] * g[3 + j] + xe[6 + i] * g[6 + j] + xe[9 + i] * g[9 + j];
+        polar(F, R);
+    }
+
+    // u_a = R^T x_a - x0_a  (models.py:227, same order as the reference)
+    double u[12], w[12], t[12];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            u[3 * a + i] = (R[i] * xe[3 * a] + R[3 + i] * xe[3 * a + 1] + R[6 + i] * xe[3 * a + 2]) - x0[3 * a + i];
+            w[3 * a + i] = R[i] * ve[3 * a] + R[3 + i] * ve[3 * a + 1] + R[6 + i] * ve[3 * a + 2];
+        }
+    double2 *out = reinterpret_cast<double2 *>(work + e * kWork);
+    // rotated gradients
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+            t[3 * a + i] = R[3 * i] * g[3 * a] + R[3 * i + 1] * g[3 * a + 1] + R[3 * i + 2] * g[3 * a + 2];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) out[k] = make_double2(t[2 * k], t[2 * k + 1]);
+    // f_e = R (Ke u)
+    double ku[12];
+    ke_apply(u, g, V, lam, mu, ku);
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+            t[3 * a + i] = R[3 * i] * ku[3 * a] + R[3 * i + 1] * ku[3 * a + 1] + R[3 * i + 2] * ku[3 * a + 2];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) out[6 + k] = make_double2(t[2 * k], t[2 * k + 1]);
+    // (K v)_e = R (Ke (R^T v))
+    ke_apply(w, g, V, lam, mu, ku);
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+            t[3 * a + i] = R[3 * i] * ku[3 * a] + R[3 * i + 1] * ku[3 * a + 1] + R[3 * i + 2] * ku[3 * a + 2];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) out[12 + k] = make_double2(t[2 * k], t[2 * k + 1]);
+}
+
+// Rotated element block entry (R Ke_ab R^T)_ij.
+__device__ __forceinline__ void rot_block(const double *ga, const double *gb, double G, double V,
+                                          double lam, double mu, double k[9]) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+            k[3 * i + j] = V * (lam * ga[i] * gb[j] + mu * ga[j] * gb[i] + (i == j ? mu * G : 0.0));
+}
+
+__global__ void __launch_bounds__(256)
+block_kernel(int64_t nb, const int4 *__restrict__ blk, const int32_t *__restrict__ list,
+             const double *__restrict__ work, const double *__restrict__ grads,
+             const double *__restrict__ vol, const double *__restrict__ share, double lam,
+             double mu, double cm, double ck, double *__restrict__ values) {
+    const int64_t bi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (bi >= nb) return;
+    const int4 info = __ldg(blk + bi);  // slot0, rowlen, begin, end
+    double acc[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) acc[k] = 0.0;
+    const int c0 = __ldg(list + info.z);
+    const bool diag = ((c0 >> 2) & 3) == (c0 & 3);
+    if (diag) {
+        // mass triplets first (indices < 12 m), ascending element
+        for (int k = info.z; k < info.w; ++k) {
+            const double mv = mul(cm, __ldg(share + (__ldg(list + k) >> 4)));
+            acc[0] = add(acc[0], mv);
+            acc[4] = add(acc[4], mv);
+            acc[8] = add(acc[8], mv);
+        }
+    }
+    for (int k = info.z; k < info.w; ++k) {
+        const int c = __ldg(list + k);
+        const int64_t e = c >> 4;
+        const int a = (c >> 2) & 3, b = c & 3;
+        const double *we = work + e * kWork;
+        double ga[3], gb[3], ra[3], rb[3];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            ga[i] = __ldg(we + 3 * a + i);
+            gb[i] = __ldg(we + 3 * b + i);
+            ra[i] = __ldg(grads + e * 12 + 3 * a + i);
+            rb[i] = __ldg(grads + e * 12 + 3 * b + i);
+        }
+        const double G = ra[0] * rb[0] + ra[1] * rb[1] + ra[2] * rb[2];
+        double kb[9];
+        rot_block(ga, gb, G, __ldg(vol + e), lam, mu, kb);
+#pragma unroll
+        for (int q = 0; q < 9; ++q) acc[q] = add(acc[q], mul(ck, kb[q]));
+    }
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) values[info.x + i * info.y + j] = acc[3 * i + j];
+}
+
+__global__ void __launch_bounds__(256)
+node_kernel(int64_t N, const int32_t *__restrict__ node_ptr, const int32_t *__restrict__ node_list,
+            const double *__restrict__ work, const double *__restrict__ x,
+            const double *__restrict__ v, const double *__restrict__ fext_state,
+            const double *__restrict__ gravity, const double *__restrict__ mass_diag,
+            const uint8_t *__restrict__ fixed, double hb, double alpha,
+            double *__restrict__ f_int, double *__restrict__ kv, double *__restrict__ b,
+            double *__restrict__ f_ext, int32_t *__restrict__ flags) {
+    const int64_t I = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (I >= N) return;
+    if (!finite3(x[3 * I], x[3 * I + 1], x[3 * I + 2])) atomicOr(flags, 1);
+    double f[3] = {0.0, 0.0, 0.0}, k[3] = {0.0, 0.0, 0.0};
+    const int lo = __ldg(node_ptr + I), hi = __ldg(node_ptr + I + 1);
+    for (int q = lo; q < hi; ++q) {
+        const int c = __ldg(node_list + q);
+        const double *we = work + (int64_t)(c >> 2) * kWork + 3 * (c & 3);
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            f[i] = add(f[i], __ldg(we + 12 + i));
+            k[i] = add(k[i], __ldg(we + 24 + i));
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        const int64_t d = 3 * I + i;
+        f_int[d] = f[i];
+        kv[d] = k[i];
+        if (b != nullptr) {
+            const double fe = add(fext_state[d], gravity[d]);
+            double r = sub(sub(fe, f[i]), mul(hb, k[i]));
+            if (alpha != 0.0) r = sub(r, mul(alpha, mul(mass_diag[d], v[d])));
+            if (fixed[d]) r = 0.0;
+            b[d] = r;
+            if (f_ext != nullptr) f_ext[d] = fe;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(128)
+kblock_kernel(int64_t m, const double *__restrict__ work, const double *__restrict__ grads,
+              const double *__restrict__ vol, double lam, double mu, double *__restrict__ out) {
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e >= m) return;
+    const double *we = work + e * kWork;
+    const double V = vol[e];
+    for (int a = 0; a < 4; ++a)
+        for (int b = 0; b < 4; ++b) {
+            const double *ra = grads + e * 12 + 3 * a, *rb = grads + e * 12 + 3 * b;
+            double kb[9];
+            rot_block(we + 3 * a, we + 3 * b, ra[0] * rb[0] + ra[1] * rb[1] + ra[2] * rb[2], V, lam, mu, kb);
+            for (int i = 0; i < 3; ++i)
+                for (int j = 0; j < 3; ++j) out[e * 144 + (3 * a + i) * 12 + 3 * b + j] = kb[3 * i + j];
+        }
+}
+
+// Kinematic update of one implicit step (integrator.py:192-208):
+// non-finite accel -> flag (StepError); accel[pinned] = 0; v' = v + h a;
+// x' = x + h v'; pinned DOFs keep v and x.
+__global__ void advance_kernel(int64_t n, const double *__restrict__ acc, const double *__restrict__ v,
+                               const double *__restrict__ x, const uint8_t *__restrict__ fixed, double h,
+                               double *__restrict__ acc_out, double *__restrict__ v_out,
+                               double *__restrict__ x_out, int32_t *__restrict__ flags) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        double a = acc[i];
+        if (!isfinite(a)) atomicOr(flags + 1, 1);
+        const bool pin = fixed[i] != 0;
+        if (pin) a = 0.0;
+        double vv = add(v[i], mul(h, a));
+        double xx = add(x[i], mul(h, vv));
+        if (pin) {
+            vv = v[i];
+            xx = x[i];
+        }
+        acc_out[i] = a;
+        v_out[i] = vv;
+        x_out[i] = xx;
+    }
+}
+
+__global__ void set_ones_kernel(int64_t n, const int32_t *__restrict__ slots, double *__restrict__ out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        out[slots[i]] = 1.0;
+}
+
+static inline int grid_for(int64_t n, int block) {
+    int64_t g = (n + block - 1) / block;
+    return (int)(g > 0 ? g : 1);
+}
+
+void launch_elem(const tsb_asm_plan *p, const tsb_asm_coeffs *c, const double *x, const double *v,
+                 cudaStream_t s) {
+    if (p->n_elems <= 0) return;
+    elem_kernel<<<grid_for(p->n_elems, 128), 128, 0, s>>>(p->n_elems, p->d_conn, p->d_grads, p->d_vol,
+                                                          p->d_rest, x, v, c->lam, c->mu, c->linear,
+                                                          p->d_work, p->d_flags);
+    TSB_LAUNCHED();
+}
+
+}  // namespace tsb
+
+extern "C" int tsb_assemble_corot(const tsb_asm_plan *p, const tsb_asm_coeffs *c, const double *d_x,
+                                  const double *d_v, const double *d_f_ext_state, double *d_values,
+                                  double *d_b, double *d_f_int, double *d_kv, double *d_f_ext,
+                                  void *stream) {
+    using namespace tsb;
+    return guard([&] {
+        if (p == nullptr || c == nullptr) throw Error(TSB_E_ARG, "null plan/coeffs");
+        cudaStream_t s = as_stream(stream);
+        launch_elem(p, c, d_x, d_v, s);
+        if (c->want_matrix && d_values != nullptr) {
+            if (p->n_blocks > 0) {
+                block_kernel<<<grid_for(p->n_blocks, 256), 256, 0, s>>>(
+                    p->n_blocks, reinterpret_cast<const int4 *>(p->d_blk), p->d_blk_list, p->d_work,
+                    p->d_grads, p->d_vol, p->d_mass_share, c->lam, c->mu, c->cm, c->ck, d_values);
+                TSB_LAUNCHED();
+            }
+            if (p->n_fixed_slots > 0) {
+                set_ones_kernel<<<grid_for(p->n_fixed_slots, 256), 256, 0, s>>>(p->n_fixed_slots,
+                                                                                p->d_fixed_slots, d_values);
+                TSB_LAUNCHED();
+            }
+        }
+        if (p->n_nodes > 0) {
+            node_kernel<<<grid_for(p->n_nodes, 256), 256, 0, s>>>(
+                p->n_nodes, p->d_node_ptr, p->d_node_list, p->d_work, d_x, d_v, d_f_ext_state,
+                p->d_gravity, p->d_mass_diag, p->d_fixed_dof, c->h + c->rayleigh_stiffness,
+                c->rayleigh_mass, d_f_int, d_kv, d_b, d_f_ext, p->d_flags);
+            TSB_LAUNCHED();
+        }
+    });
+}
+
+extern "C" int tsb_element_blocks(const tsb_asm_plan *p, const tsb_asm_coeffs *c, const double *d_x,
+                                  double *d_kblocks, void *stream) {
+    using namespace tsb;
+    return guard([&] {
+        cudaStream_t s = as_stream(stream);
+        launch_elem(p, c, d_x, nullptr, s);
+        if (p->n_elems > 0) {
+            kblock_kernel<<<grid_for(p->n_elems, 128), 128, 0, s>>>(p->n_elems, p->d_work, p->d_grads,
+                                                                    p->d_vol, c->lam, c->mu, d_kblocks);
+            TSB_LAUNCHED();
+        }
+    });
+}
+
+extern "C" int tsb_advance(int64_t n_dof, const double *d_accel, const double *d_v, const double *d_x,
+                           const uint8_t *d_fixed_dof, double h, double *d_acc_out, double *d_v_out,
+                           double *d_x_out, int32_t *d_flags, void *stream) {
+    using namespace tsb;
+    return guard([&] {
+        if (n_dof <= 0) return;
+        int g = grid_for(n_dof, 256);
+        if (g > kNumSM * 8) g = kNumSM * 8;
+        advance_kernel<<<g, 256, 0, as_stream(stream)>>>(n_dof, d_accel, d_v, d_x, d_fixed_dof, h,
+                                                         d_acc_out, d_v_out, d_x_out, d_flags);
+        TSB_LAUNCHED();
+    });
+}

@@ -1,0 +1,29 @@
+// Error reporting and launch accounting shared by every libtsb entry point.
+#include <atomic>
+#include <cstring>
+#include <string>
+
+#include "tsb_common.cuh"
+
+namespace tsb {
+
+static thread_local std::string g_last_error;
+static std::atomic<int64_t> g_launches{0};
+
+void set_last_error(const std::string &msg) { g_last_error = msg; }
+void count_launch(int64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+}  // namespace tsb
+
+extern "C" int tsb_abi_version(void) { return TSB_ABI_VERSION; }
+
+extern "C" int tsb_last_error(char *buf, size_t len) {
+    if (buf == nullptr || len == 0) return TSB_E_ARG;
+    const std::string &m = tsb::g_last_error;
+    size_t k = m.size() < len - 1 ? m.size() : len - 1;
+    std::memcpy(buf, m.data(), k);
+    buf[k] = '\0';
+    return TSB_OK;
+}
+
+extern "C" int64_t tsb_launch_count(void) { return tsb::g_launches.load(); }

@@ -1,0 +1,77 @@
+// Bit-exact CSR row reduction shared by tsb_spmv and the fused PCG SpMV.
+//
+// The reference computes y = A x as
+//     prod = values * x[col_ind]; y[rows] = np.add.reduceat(prod, starts)
+// (krylov.py:63-70).  For float64, reduceat seeds each row with its first
+// product and adds NumPy's pairwise sum of the remaining L-1 products:
+//   n < 8      : sequential from -0.0
+//   8<=n<=128  : 8 strided partial sums r_j, combined ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)),
+//                then the n%8 tail sequentially
+//   n > 128    : split at n/2 rounded down to a multiple of 8, recurse.
+// One row is owned by a group of 8 lanes; lane j carries partial sum r_j and
+// the xor-1/2/4 butterfly reproduces the combine tree exactly (IEEE addition
+// is commutative), so the result equals the reference bit for bit.
+#pragma once
+
+#include "tsb_common.cuh"
+
+namespace tsb {
+
+// Plain x[j] accessor.
+struct XPlain {
+    const double *__restrict__ x;
+    __device__ __forceinline__ double operator()(int j) const { return __ldg(x + j); }
+};
+
+// p_j = z_j + beta * p_old_j computed on the fly (PCG direction update
+// fused into the SpMV, krylov.py:156); every reader rounds identically.
+struct XDirection {
+    const double *__restrict__ z;
+    const double *__restrict__ pold;
+    double beta;
+    __device__ __forceinline__ double operator()(int j) const {
+        return add(__ldcg(z + j), mul(beta, __ldcg(pold + j)));
+    }
+};
+
+// Returns the exact row sum in every lane of the 8-lane group.
+// `lane8` in [0,8), `gmask` = the group's lanes in the warp.
+template <class XAcc>
+__device__ __forceinline__ double row_sum_exact(int lo, int len, const int32_t *__restrict__ col,
+                                                const double *__restrict__ val, const XAcc &xa,
+                                                int lane8, unsigned gmask) {
+    if (len <= 0) return 0.0;
+    auto term = [&](int64_t k) -> double { return mul(__ldg(val + k), xa(__ldg(col + k))); };
+    const int n = len - 1;  // terms handled by the pairwise sum
+    double res;
+    if (n > 128) {
+        double r = 0.0;
+        if (lane8 == 0) r = pairwise_serial(term, (int64_t)lo + 1, (int64_t)n);
+        res = __shfl_sync(gmask, r, 0, 8);
+    } else if (n >= 8) {
+        const int full = n - (n % 8);
+        double r = term(lo + 1 + lane8);
+        for (int i = 8; i < full; i += 8) r = add(r, term(lo + 1 + i + lane8));
+        r = add(r, __shfl_xor_sync(gmask, r, 1, 8));
+        r = add(r, __shfl_xor_sync(gmask, r, 2, 8));
+        r = add(r, __shfl_xor_sync(gmask, r, 4, 8));
+        // tail: n%8 < 8 terms, loaded in parallel, added in order
+        const int tail = n - full;
+        double t = 0.0;
+        if (lane8 < tail) t = term(lo + 1 + full + lane8);
+        for (int k = 0; k < tail; ++k) r = add(r, __shfl_sync(gmask, t, k, 8));
+        res = r;
+    } else {
+        double t = 0.0;
+        if (lane8 < n) t = term(lo + 1 + lane8);
+        double r = -0.0;
+        for (int k = 0; k < n; ++k) r = add(r, __shfl_sync(gmask, t, k, 8));
+        res = r;
+    }
+    double p0 = 0.0;
+    if (lane8 == 0) p0 = term(lo);
+    p0 = __shfl_sync(gmask, p0, 0, 8);
+    return add(p0, res);
+}
+
+}  // namespace tsb

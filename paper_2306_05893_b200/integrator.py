@@ -1,0 +1,319 @@
+"""Backward-Euler step on the B200 (drop-in for tetsim.integrator, integrator.py:1-236).
+
+`assemble_system` is one fused device pass (element kernel -> CSR block
+gather -> nodal gather + rhs) into a fixed pattern built once from the mesh
+topology; `compute_step` keeps A, b, the solve and the kinematic update on
+the device.  States may hold NumPy arrays (host buffers: uploaded at the
+start of the step, results downloaded at the end -- the reference-facing
+path) or CUDA tensors (fully device-resident).
+
+System: A = (1 + h alpha) M + h (h + beta) K,
+        b = f_ext - f(x_t) - (h + beta) K v_t - alpha M v_t,  pinned rows identity / zero.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from ._plan import AssemblyPlan, topology_pattern
+from .assembly import CsrMatrix, build_pattern, TripletStream
+from .krylov import SolveReport
+from .mesh import Mesh
+from .models import lumped_mass
+
+__all__ = [
+    "IntegratorError",
+    "StepError",
+    "IntegratorConfig",
+    "SimState",
+    "StepResult",
+    "BackwardEulerIntegrator",
+]
+
+
+class IntegratorError(ValueError):
+    pass
+
+
+class StepError(RuntimeError):
+    """Linear solve failed during a step; carries the solver report."""
+
+    def __init__(self, message: str, report: SolveReport):
+        super().__init__(message)
+        self.report = report
+
+
+@dataclass
+class IntegratorConfig:
+    dt: float
+    rayleigh_mass: float = 0.0
+    rayleigh_stiffness: float = 0.0
+    gravity: tuple = (0.0, 0.0, -9.81)
+    newton_iterations: int = 1
+
+    def __post_init__(self):
+        if not self.dt > 0:
+            raise IntegratorError(f"dt must be positive, got {self.dt}")
+        if self.rayleigh_mass < 0 or self.rayleigh_stiffness < 0:
+            raise IntegratorError("Rayleigh coefficients must be non-negative")
+        if self.newton_iterations < 1:
+            raise IntegratorError("newton_iterations must be >= 1")
+
+
+def _copy(a):
+    return a.clone() if _lib.is_tensor(a) else a.copy()
+
+
+@dataclass
+class SimState:
+    """Nodal kinematics (NumPy arrays or CUDA tensors) plus last step's forces."""
+
+    positions: object      # (n, 3)
+    velocities: object     # (n, 3)
+    accelerations: object  # (n, 3)
+    f_int: object          # (3n,)
+    f_ext: object          # (3n,)
+    time: float = 0.0
+
+    @classmethod
+    def rest(cls, mesh: Mesh, device: bool = False) -> "SimState":
+        n = mesh.node_count
+        st = cls(mesh.nodes.copy(), np.zeros((n, 3)), np.zeros((n, 3)), np.zeros(3 * n), np.zeros(3 * n))
+        return st.to_device() if device else st
+
+    @property
+    def on_device(self) -> bool:
+        return _lib.is_tensor(self.positions)
+
+    def to_device(self) -> "SimState":
+        t = _lib.require_cuda()
+        cv = lambda a: t.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).cuda()  # noqa: E731
+        if self.on_device:
+            return self
+        return SimState(cv(self.positions), cv(self.velocities), cv(self.accelerations),
+                        cv(self.f_int), cv(self.f_ext), self.time)
+
+    def to_host(self) -> "SimState":
+        if not self.on_device:
+            return self
+        cv = lambda a: a.detach().cpu().numpy()  # noqa: E731
+        return SimState(cv(self.positions), cv(self.velocities), cv(self.accelerations),
+                        cv(self.f_int), cv(self.f_ext), self.time)
+
+    def copy(self) -> "SimState":
+        return SimState(_copy(self.positions), _copy(self.velocities), _copy(self.accelerations),
+                        _copy(self.f_int), _copy(self.f_ext), self.time)
+
+
+@dataclass
+class StepResult:
+    positions: object
+    velocities: object
+    accelerations: object
+    f_int: object
+    f_ext: object
+    matrix: CsrMatrix
+    rhs: object
+    report: SolveReport
+    pattern_rebuilt: bool
+    assembly_time: float
+    solve_time: float
+
+
+class _DeviceAssembler:
+    """Pattern owner of the device path (stands in for MatrixAssembler on the
+    integrator: `pattern_rebuilds`, `force_rebuild`, lazily a `mapping`)."""
+
+    def __init__(self, mesh: Mesh):
+        self.mesh = mesh
+        self.n = mesh.ndof
+        self.fixed_dofs = mesh.fixed_dofs()
+        self.pattern = None
+        self.pattern_rebuilds = 0
+        self.force_rebuild = False
+        self._mapping = None
+
+    def ensure(self) -> bool:
+        if self.pattern is None or self.force_rebuild:
+            self.pattern = topology_pattern(self.mesh)
+            self.pattern_rebuilds += 1
+            self._mapping = None
+            return True
+        return False
+
+    @property
+    def mapping(self):
+        """Reference CompressionMapping of the fused mass+stiffness stream (built on demand)."""
+        if self._mapping is None and self.pattern is not None:
+            el = self.mesh.elements
+            gdof = (3 * el[:, :, None] + np.arange(3)).reshape(len(el), 12)
+            st = TripletStream()
+            st.begin_pass()
+            st.add_block(gdof.ravel(), gdof.ravel(), np.zeros(gdof.size))
+            st.add_block(np.repeat(gdof, 12, axis=1).ravel(), np.tile(gdof, (1, 12)).ravel(),
+                         np.zeros(144 * len(el)))
+            st.end_pass()
+            _, self._mapping = build_pattern(st, self.n, self.fixed_dofs)
+        return self._mapping
+
+
+class BackwardEulerIntegrator:
+    """Owns the device plan (mesh layout, pattern, gather lists) and the mass data."""
+
+    def __init__(self, mesh: Mesh, model, config: IntegratorConfig, workers: int = 1):
+        self.mesh = mesh
+        self.model = model
+        self.config = config
+        self.workers = workers
+        self.fixed_dofs = mesh.fixed_dofs()
+        self.assembler = _DeviceAssembler(mesh)
+        self.mass_diag = lumped_mass(mesh, model.params)
+        share = model.params.density * mesh.signed_volumes() / 4.0
+        self._mass_share = share
+        self._gravity_force = (self.mass_diag.reshape(-1, 3) * np.asarray(config.gravity)).ravel()
+        self._plan: AssemblyPlan | None = None
+        self._linear = bool(getattr(model, "linear", False))
+
+    @property
+    def _mass_vals(self) -> np.ndarray:
+        return np.repeat(self._mass_share, 12)
+
+    def _coefficients(self):
+        h = self.config.dt
+        return 1.0 + h * self.config.rayleigh_mass, h * (h + self.config.rayleigh_stiffness)
+
+    def _ensure_plan(self) -> bool:
+        rebuilt = self.assembler.ensure()
+        if rebuilt or self._plan is None:
+            self._plan = AssemblyPlan(
+                self.model.precomp, pattern=self.assembler.pattern, mass_share=self._mass_share,
+                mass_diag=self.mass_diag, gravity=self._gravity_force, fixed_dof=self.fixed_dofs,
+                n_nodes=self.mesh.node_count,
+            )
+        return rebuilt
+
+    # -- device core ------------------------------------------------------
+    def _assemble_device(self, x, v, f_ext_state):
+        """Enqueue the fused assembly; returns (A, b, f_int, f_ext, rebuilt) as device objects."""
+        t = _lib.torch()
+        rebuilt = self._ensure_plan()
+        plan = self._plan
+        pat = self.assembler.pattern
+        n = self.mesh.ndof
+        cfg = self.config
+        cm, ck = self._coefficients()
+        co = plan.coeffs(h=cfg.dt, beta=cfg.rayleigh_stiffness, alpha=cfg.rayleigh_mass, cm=cm, ck=ck,
+                         linear=self._linear, want_matrix=True)
+        values = t.empty(len(pat["col_ind"]), dtype=t.float64, device="cuda")
+        b = t.empty(n, dtype=t.float64, device="cuda")
+        f_int = t.empty(n, dtype=t.float64, device="cuda")
+        kv = t.empty(n, dtype=t.float64, device="cuda")
+        f_ext = t.empty(n, dtype=t.float64, device="cuda")
+        plan.flags.zero_()
+        plan.run(co, x, v, f_ext_state, values, b, f_int, kv, f_ext)
+        a = CsrMatrix(n, n, pat["row_ptr"], pat["col_ind"], values)
+        return a, b, f_int, f_ext, rebuilt
+
+    @staticmethod
+    def _flat_dev(a):
+        t = _lib.torch()
+        if _lib.is_tensor(a):
+            return a.reshape(-1).to(dtype=t.float64).contiguous()
+        return t.from_numpy(np.ascontiguousarray(np.asarray(a, dtype=np.float64).reshape(-1))).cuda()
+
+    def _raise_model_flags(self, flags):
+        from .models import ModelError
+
+        if int(flags[0]):
+            raise ModelError("non-finite positions")
+
+    # -- reference API ----------------------------------------------------
+    def assemble_system(self, state: SimState):
+        """One fused mass-and-stiffness pass on the device; returns (A, b, info)."""
+        t0 = time.perf_counter()
+        host = not state.on_device
+        x = self._flat_dev(state.positions)
+        v = self._flat_dev(state.velocities)
+        fe = self._flat_dev(state.f_ext)
+        a, b, f_int, f_ext, rebuilt = self._assemble_device(x, v, fe)
+        flags = self._plan.flags.cpu()
+        self._raise_model_flags(flags)
+        if host:
+            b, f_int, f_ext = b.cpu().numpy(), f_int.cpu().numpy(), f_ext.cpu().numpy()
+        info = {"pattern_rebuilt": rebuilt, "assembly_time": time.perf_counter() - t0,
+                "f_int": f_int, "f_ext": f_ext}
+        return a, b, info
+
+    def compute_step(self, state: SimState, solve) -> StepResult:
+        """One implicit step without committing it (integrator.py:171-221).
+
+        `solve(A, b) -> (x, SolveReport)`.  Solvers marked `accepts_device`
+        receive b as a CUDA tensor; others get a NumPy array as in the reference.
+        """
+        t = _lib.torch()
+        cfg = self.config
+        h = cfg.dt
+        host = not state.on_device
+        x0 = self._flat_dev(state.positions)
+        v0 = self._flat_dev(state.velocities)
+        fe_state = self._flat_dev(state.f_ext)
+        n = self.mesh.ndof
+        dev_solve = bool(getattr(solve, "accepts_device", False))
+        ev = [t.cuda.Event(enable_timing=True) for _ in range(3)]
+        assembly_time = solve_time = 0.0
+        rebuilt_any = False
+        x_tr, v_tr = x0, v0
+        fixed = self._plan.fixed_dof if self._plan is not None else None
+        for _ in range(cfg.newton_iterations):
+            ev[0].record()
+            a, b, f_int, f_ext, rebuilt = self._assemble_device(x_tr, v_tr, fe_state)
+            fixed = self._plan.fixed_dof
+            ev[1].record()
+            rebuilt_any = rebuilt_any or rebuilt
+            accel, report = solve(a, b if dev_solve else b.cpu().numpy())
+            ev[2].record()
+            d_acc = self._flat_dev(accel)
+            acc = t.empty(n, dtype=t.float64, device="cuda")
+            v1 = t.empty(n, dtype=t.float64, device="cuda")
+            x1 = t.empty(n, dtype=t.float64, device="cuda")
+            P = _lib.ptr
+            _lib.check(_lib.load().tsb_advance(n, P(d_acc), P(v0), P(x0), P(fixed), h, P(acc), P(v1),
+                                               P(x1), P(self._plan.flags), _lib.stream_ptr()), "advance")
+            flags = self._plan.flags.cpu()  # one readback: model + accel flags
+            ev[2].synchronize()
+            assembly_time += ev[0].elapsed_time(ev[1]) * 1e-3
+            solve_time += ev[1].elapsed_time(ev[2]) * 1e-3
+            self._raise_model_flags(flags)
+            if not report.converged:
+                raise StepError(
+                    f"linear solve did not converge: residual {report.final_residual:g} "
+                    f"after {report.iterations} iterations", report)
+            if int(flags[1]):
+                raise StepError("solver produced non-finite accelerations", report)
+            x_tr, v_tr = x1, v1
+        if host:
+            out = lambda a_: a_.cpu().numpy()  # noqa: E731
+            pos, vel, acc_o = out(x_tr).reshape(-1, 3), out(v_tr).reshape(-1, 3), out(acc).reshape(-1, 3)
+            f_int_o, f_ext_o = out(f_int), out(f_ext)
+            rhs = out(b)
+        else:
+            pos, vel, acc_o = x_tr.view(-1, 3), v_tr.view(-1, 3), acc.view(-1, 3)
+            f_int_o, f_ext_o, rhs = f_int, f_ext, b
+        return StepResult(pos, vel, acc_o, f_int_o, f_ext_o, a, rhs, report, rebuilt_any,
+                          assembly_time, solve_time)
+
+    def commit(self, state: SimState, result: StepResult):
+        state.positions = result.positions
+        state.velocities = result.velocities
+        state.accelerations = result.accelerations
+        state.f_int = result.f_int
+        state.time += self.config.dt
+
+    def step(self, state: SimState, solve) -> StepResult:
+        result = self.compute_step(state, solve)
+        self.commit(state, result)
+        return result

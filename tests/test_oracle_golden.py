@@ -1,0 +1,115 @@
+"""Pin the CPU oracle against the reference's own outputs (tests/golden, made by
+tests/golden/make_golden.py from /root/reference).  CPU only."""
+
+import numpy as np
+import pytest
+
+from conftest import GoldenFactors
+from oracle import tetsim_oracle as O
+
+G = 9.81
+
+
+@pytest.mark.parametrize("name", ["beam_small", "beam_cfg1"])
+def test_spmv_bit_exact(golden, name):
+    g = golden(name)
+    y = O.spmv(g["row_ptr"], g["col_ind"], g["values"], g["spmv_x"])
+    assert np.array_equal(y, g["spmv_y"])
+
+
+def test_compress_bit_exact(golden):
+    g = golden("beam_small")
+    vals = O.compress(g["trip_vals"], g["kept"], g["kept_slots"], len(g["col_ind"]),
+                      g["fixed_diag_slots"], g["coeffs"])
+    assert np.array_equal(vals, g["values"])
+
+
+def test_sort_merge_pattern_matches_reference_mapping(golden):
+    g = golden("beam_small")
+    n = 3 * len(g["nodes"])
+    fixed = (3 * g["fixed_nodes"][:, None] + np.arange(3)).ravel()
+    rp, ci, slot, fs = O.sort_merge_pattern(g["trip_rows"], g["trip_cols"], n, fixed)
+    assert np.array_equal(rp, g["row_ptr"])
+    assert np.array_equal(ci, g["col_ind"])
+    assert np.array_equal(slot, g["slot_of_triplet"])
+    assert np.array_equal(fs, g["fixed_diag_slots"])
+
+
+@pytest.mark.parametrize("name", ["beam_small", "beam_cfg1"])
+def test_rest_data_matches_reference(golden, name):
+    g = golden(name)
+    rest = O.rest_data(g["nodes"], g["elements"], 1e5, 0.3, 1000.0)
+    assert np.array_equal(rest["grads"], g["grads"])
+    assert np.array_equal(rest["vol"], g["volume"])
+    assert np.array_equal(rest["ke"], g["ke"])
+
+
+@pytest.mark.parametrize("name", ["beam_small", "beam_cfg1"])
+def test_assemble_system_matches_reference(golden, name):
+    g = golden(name)
+    rest = O.rest_data(g["nodes"], g["elements"], 1e5, 0.3, 1000.0)
+    out = O.assemble_system(g["nodes"], g["elements"], g["fixed_nodes"], rest, g["positions"],
+                            g["velocities"], g["f_ext_state"], 0.01, (0.0, -G, 0.0))
+    assert np.array_equal(out["row_ptr"], g["row_ptr"])
+    assert np.array_equal(out["col_ind"], g["col_ind"])
+    # same NumPy/BLAS calls in the same order: bit-identical in this container
+    assert np.array_equal(out["values"], g["values"])
+    assert np.array_equal(out["b"], g["b"])
+    assert np.array_equal(out["f_int"], g["f_int"])
+    assert np.array_equal(out["f_ext"], g["f_ext"])
+
+
+@pytest.mark.parametrize("name", ["beam_small", "beam_cfg1"])
+def test_pcg_matches_reference(golden, name):
+    g = golden(name)
+    n = len(g["b"])
+    inv = O.jacobi_inv_diag(g["row_ptr"], g["col_ind"], g["values"], n)
+    x, it, res, conv = O.pcg(g["row_ptr"], g["col_ind"], g["values"], g["b"], lambda r: r * inv,
+                             tol=1e-9, max_it=8000)
+    assert conv and it == int(g["it_jacobi"])
+    assert np.array_equal(x, g["x_jacobi"])
+    x, it, res, conv = O.pcg(g["row_ptr"], g["col_ind"], g["values"], g["b"], None, tol=1e-9, max_it=8000)
+    assert it == int(g["it_cg"]) and res == float(g["res_cg"])
+    assert np.array_equal(x, g["x_cg"])
+
+
+def test_ldlt_solves_match_reference(golden):
+    g = golden("ldlt_small")
+    f = GoldenFactors(g)
+    assert np.array_equal(O.solve_lower(f, g["r"]), g["lower"])
+    assert np.array_equal(O.solve_upper(f, g["r"]), g["upper"])
+    assert np.array_equal(O.apply(f, g["r"]), g["apply"])
+    x, it, res, conv = O.pcg(g["row_ptr"], g["col_ind"], g["values"], g["b"], lambda r: O.apply(f, r),
+                             tol=1e-9, max_it=8000)
+    assert conv and it == int(g["it_ldlt"])
+    assert np.array_equal(x, g["x_ldlt"])
+
+
+def test_textbook_substitution_agrees_with_level_solves(golden):
+    g = golden("ldlt_small")
+    f = GoldenFactors(g)
+    n = len(g["r"])
+    rows, cols, vals = [], [], []
+    for b in f.blocks:
+        m = b.stop - b.start
+        ir, ic = np.tril_indices(m, -1)
+        rows.append(b.start + ir), cols.append(b.start + ic), vals.append(b.l11[ir, ic])
+        if len(b.anc):
+            rows.append(np.repeat(b.anc, m)), cols.append(np.tile(np.arange(b.start, b.stop), len(b.anc)))
+            vals.append(b.l21.ravel())
+    rows, cols, vals = map(np.concatenate, (rows, cols, vals))
+    o = np.lexsort((cols, rows))
+    rp = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(np.bincount(rows, minlength=n), out=rp[1:])
+    y = O.forward_substitution(rp, cols[o], vals[o], g["r"])
+    assert np.abs(y - g["lower"]).max() <= 1e-12 * np.abs(y).max()
+    z = O.backward_substitution(rp, cols[o], vals[o], g["r"])
+    assert np.abs(z - g["upper"]).max() <= 1e-12 * np.abs(z).max()
+
+
+def test_corotational_kv_matches_reference(golden):
+    g = golden("beam_cfg1")
+    rest = O.rest_data(g["nodes"], g["elements"], 1e5, 0.3, 1000.0)
+    f, kv, _ = O.corotational(g["nodes"], g["elements"], rest, g["positions"], g["velocities"])
+    assert np.array_equal(kv, g["kv"])
+    assert np.array_equal(f, g["f_int"])
