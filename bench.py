@@ -1,0 +1,435 @@
+"""Benchmark of the B200 implicit-FEM solve path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg2|cfg1|cfg3]
+                    [--precond ldlt|jacobi] [--impl reference]
+
+A step = one implicit time step of the scenario (assemble A, b on the device
++ device PCG + kinematic update) at scenario step 7 of a clamped corotational
+beam under transverse gravity, LDL^T factors replayed at a fixed staleness of
+3 steps (SURVEY.md 8d / BASELINE.md section 2).  Every timed step repeats the
+same step from the same state (nothing committed), L2 flushed between steps.
+N > 1: one independent simulation per GPU (replicas, weak scaling).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "PCG ms/time step + tri-solve GB/s vs HBM roofline per mesh size"
+WORKLOADS = {
+    "cfg1": dict(dims=(6, 6, 28), law="linear", desc="config 1: ~1k-node beam, linear elastic"),
+    "cfg2": dict(dims=(10, 10, 100), law="corotational", desc="config 2: ~10k-node corotational beam"),
+    "cfg3": dict(dims=(20, 20, 250), law="corotational", desc="config 3: ~100k-node corotational beam"),
+}
+STALE_FROM, AT_STEP = 4, 7
+TOL, MAX_IT, LEAF, TILE = 1e-9, 8000, 64, 16
+
+
+def peaks():
+    try:
+        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text()), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0}, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# workload
+# ---------------------------------------------------------------------------
+
+def build_workload(name, device=True):
+    import paper_2306_05893_b200 as P
+    from paper_2306_05893_b200 import krylov, ndprecond as ND
+    from paper_2306_05893_b200.integrator import BackwardEulerIntegrator, IntegratorConfig, SimState
+
+    w = WORKLOADS[name]
+    mesh = P.generate_beam(*w["dims"], 0.1)
+    mesh = mesh.with_fixed_nodes(np.flatnonzero(mesh.nodes[:, 2] == 0.0))
+    params = P.MaterialParams(1e5, 0.3, 1000.0)
+    integ = BackwardEulerIntegrator(mesh, P.make_model(w["law"], mesh, params),
+                                    IntegratorConfig(dt=0.01, gravity=(0.0, -9.81, 0.0)))
+    cfg = krylov.SolverConfig(TOL, MAX_IT)
+
+    def jacobi(a, b):
+        return krylov.pcg(a, b, krylov.jacobi_precond(a), cfg)
+
+    jacobi.accepts_device = True
+    t0 = time.perf_counter()
+    plan = ND.expand_plan(ND.nested_dissection(P.vertex_adjacency(mesh), LEAF))
+    t_nd = time.perf_counter() - t0
+    st = SimState.rest(mesh, device=True)
+    factors = None
+    t_factor = 0.0
+    for k in range(1, AT_STEP):
+        res = integ.step(st, jacobi)
+        if k == STALE_FROM:
+            t0 = time.perf_counter()
+            factors = ND.ldlt_factor(res.matrix, plan, tile=TILE, source_step=k)
+            t_factor = time.perf_counter() - t0
+    factors.device()
+
+    def ldlt(a, b):
+        return krylov.pcg(a, b, factors, cfg)
+
+    ldlt.accepts_device = True
+    return dict(name=name, mesh=mesh, integ=integ, state=st, factors=factors, plan=plan,
+                solvers={"jacobi": jacobi, "ldlt": ldlt}, t_nd=t_nd, t_factor=t_factor, cfg=cfg)
+
+
+class L2Flush:
+    def __init__(self):
+        import torch
+
+        self.buf = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MB > L2
+
+    def __call__(self):
+        self.buf.zero_()
+
+
+def body_kernels(factors, mode):
+    return 2 if mode == "jacobi" else 3 + 2 * len(factors.levels)
+
+
+def time_steps(W, mode, steps, warmup, flush):
+    import torch
+    from paper_2306_05893_b200 import _lib
+
+    integ, st, solve = W["integ"], W["state"], W["solvers"][mode]
+    for _ in range(warmup):
+        integ.compute_step(st, solve)
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    iters, asm, slv = [], [], []
+    launches = 0
+    for k in range(steps):
+        flush()
+        l0 = _lib.launch_count()
+        ev[k][0].record()
+        res = integ.compute_step(st, solve)
+        ev[k][1].record()
+        launches += _lib.launch_count() - l0 + (res.report.iterations or 1) * body_kernels(W["factors"], mode)
+        iters.append(res.report.iterations)
+        asm.append(res.assembly_time * 1e3)
+        slv.append(res.solve_time * 1e3)
+    torch.cuda.synchronize()
+    per = [a.elapsed_time(b) for a, b in ev]
+    return dict(total_ms=sum(per), ms=statistics.median(per), iterations=statistics.median(iters),
+                assembly_ms=statistics.median(asm), solve_ms=statistics.median(slv), launches=launches,
+                per_step=per)
+
+
+def time_apply(W, reps, flush):
+    """Isolated LDL^T apply (both sweeps + perm/D), CUDA events on the launching stream."""
+    import torch
+
+    f = W["factors"]
+    dev = f.device()
+    r = torch.randn(f.plan.n, dtype=torch.float64, device="cuda")
+    z = torch.empty_like(r)
+    for _ in range(3):
+        dev.run("apply", r, z)
+    ts = []
+    for _ in range(reps):
+        flush()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        dev.run("apply", r, z)
+        b.record()
+        b.synchronize()
+        ts.append(a.elapsed_time(b))
+    nnzL = f.fill_in
+    n = f.plan.n
+    bytes_apply = 16 * nnzL + 48 * n  # two sweeps + perm gather + D + iperm
+    ms = statistics.median(ts)
+    return dict(ms=ms, bytes=bytes_apply, gbs=bytes_apply / (ms * 1e-3) / 1e9, nnzL=nnzL,
+                stored_bytes=sum(dev.bytes.values()))
+
+
+def time_spmv(W, reps, flush):
+    import torch
+    from paper_2306_05893_b200 import krylov
+
+    integ, st = W["integ"], W["state"]
+    a, b, _ = integ.assemble_system(st)
+    x = torch.randn(a.ncols, dtype=torch.float64, device="cuda")
+    for _ in range(3):
+        krylov.spmv(a, x)
+    ts = []
+    for _ in range(reps):
+        flush()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        krylov.spmv(a, x)
+        e1.record()
+        e1.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    ms = statistics.median(ts)
+    byts = 12 * a.nnz + 20 * a.nrows
+    return dict(ms=ms, bytes=byts, gbs=byts / (ms * 1e-3) / 1e9, nnz=a.nnz)
+
+
+def time_e2e(W, mode, steps):
+    """Same step through the reference-facing API with HOST (NumPy) state:
+    H2D of x, v, f_ext and D2H of the step's results inside the timed region."""
+    import torch
+    from paper_2306_05893_b200.integrator import SimState
+
+    st = W["state"].to_host()
+    host = SimState(st.positions, st.velocities, st.accelerations, st.f_int, st.f_ext, st.time)
+    solve = W["solvers"][mode]
+    for _ in range(2):
+        W["integ"].compute_step(host, solve)
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        res = W["integ"].compute_step(host, solve)
+        _ = res.positions.sum()  # results are host arrays
+        ts.append((time.perf_counter() - t0) * 1e3)
+    n = 3 * W["mesh"].node_count
+    return dict(ms=statistics.median(ts), h2d=3 * 8 * n, d2h=6 * 8 * n)
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the oracle port of the reference on the host cores
+# ---------------------------------------------------------------------------
+
+def oracle_step(W, mode, rest, host_state):
+    from oracle import tetsim_oracle as O
+
+    mesh = W["mesh"]
+    x, v, fe = host_state
+    out = O.assemble_system(mesh.nodes, mesh.elements, mesh.fixed_nodes, rest, x, v, fe, 0.01,
+                            (0.0, -9.81, 0.0), linear=WORKLOADS[W["name"]]["law"] == "linear")
+    if mode == "ldlt":
+        f = W["factors"]
+        pre = lambda r: O.apply(f, r)  # noqa: E731
+    else:
+        inv = O.jacobi_inv_diag(out["row_ptr"], out["col_ind"], out["values"], len(out["b"]))
+        pre = lambda r: r * inv  # noqa: E731
+    return O.pcg(out["row_ptr"], out["col_ind"], out["values"], out["b"], pre, TOL, MAX_IT)
+
+
+def cpu_baseline(W, mode, budget_s=20.0, max_steps=10, threads=1):
+    from oracle import tetsim_oracle as O
+    from threadpoolctl import threadpool_limits
+
+    st = W["state"].to_host()
+    host_state = (st.positions, st.velocities, st.f_ext)
+    with threadpool_limits(limits=threads):
+        rest = O.rest_data(W["mesh"].nodes, W["mesh"].elements, 1e5, 0.3, 1000.0)
+        ts = []
+        t_start = time.perf_counter()
+        while len(ts) < max_steps and (time.perf_counter() - t_start) < budget_s:
+            t0 = time.perf_counter()
+            _, it, _, _ = oracle_step(W, mode, rest, host_state)
+            ts.append((time.perf_counter() - t0) * 1e3)
+    return dict(ms=statistics.median(ts), steps=len(ts), iterations=it)
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region
+# ---------------------------------------------------------------------------
+
+class ClockSampler:
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,utilization.gpu")
+
+    def __init__(self, gpu):
+        self.gpu = gpu
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-lms", "50", "-i", str(self.gpu)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        return False
+
+    def summary(self):
+        rows = []
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) >= 7:
+                try:
+                    rows.append((float(p[0]), float(p[1]), p[2:6], float(p[6])))
+                except ValueError:
+                    pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i, v in enumerate(r[2]) if v.lower() == "active"})
+        loaded = [r for r in rows if r[3] > 0] or rows
+        return {"sm_mhz": statistics.median(r[0] for r in loaded), "sm_max_mhz": max(r[1] for r in rows),
+                "reasons": reasons, "samples": len(rows), "samples_under_load": len(loaded)}
+
+
+def traffic_from_profiles(workload):
+    p = ROOT / "profiles" / "ncu_traffic.json"
+    try:
+        return json.loads(p.read_text()).get(workload)
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------------------
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    W = build_workload(args.workload)
+    ncores = os.cpu_count()
+    from oracle import tetsim_oracle as O
+
+    st = W["state"].to_host()
+    rest = O.rest_data(W["mesh"].nodes, W["mesh"].elements, 1e5, 0.3, 1000.0)
+    hs = (st.positions, st.velocities, st.f_ext)
+    for _ in range(args.warmup):
+        oracle_step(W, args.precond, rest, hs)
+    ts = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        _, it, _, _ = oracle_step(W, args.precond, rest, hs)
+        ts.append((time.perf_counter() - t0) * 1e3)
+    ms = statistics.mean(ts)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOADS[args.workload]["desc"], "precond": args.precond,
+                   "staleness": AT_STEP - STALE_FROM, "iterations": it},
+        "cpu_baseline": {"value": ms, "unit": "ms", "cores": ncores, "kind": "port",
+                         "sample": f"{args.steps} full steps (assembly + PCG) of {args.workload} with the "
+                                   "NumPy oracle port of the reference, all host BLAS threads"},
+        "e2e": {"value": ms, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
+    ap.add_argument("--precond", default="ldlt", choices=["ldlt", "jacobi"])
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2306_05893_b200 import _lib
+
+    W = build_workload(args.workload)
+    flush = L2Flush()
+    pk, pk_kind = peaks()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        main_r = time_steps(W, args.precond, args.steps, args.warmup, flush)
+    other = "jacobi" if args.precond == "ldlt" else "ldlt"
+    other_r = time_steps(W, other, max(10, args.steps // 4), 3, flush)
+    torch.cuda.synchronize()
+    t_local = torch.tensor([main_r["total_ms"]], dtype=torch.float64, device="cuda")
+    if dist:
+        dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
+        dist.barrier()
+    total_ms = float(t_local.item())
+    apply_r = time_apply(W, 20, flush)
+    spmv_r = time_spmv(W, 20, flush)
+    e2e_r = time_e2e(W, args.precond, max(5, min(args.steps, 30)))
+    ms = total_ms / args.steps
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return 0
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(W, args.precond)
+    hbm = pk.get("hbm_gbs", 6650.0)
+    traffic = traffic_from_profiles(args.workload)
+    mesh, f = W["mesh"], W["factors"]
+    line = {
+        "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {
+            "workload": WORKLOADS[args.workload]["desc"], "mesh": "x".join(map(str, WORKLOADS[args.workload]["dims"])),
+            "nodes": mesh.node_count, "tets": mesh.element_count, "dofs": mesh.ndof, "nnz": spmv_r["nnz"],
+            "nnz_L": apply_r["nnzL"], "precond": args.precond, "staleness": AT_STEP - STALE_FROM,
+            "scenario_step": AT_STEP, "tol": TOL, "leaf": LEAF, "tile": TILE,
+            "l2": "flushed (256 MB write) before every timed step", "parallelism": f"replicas x{world}",
+        },
+        "iterations": main_r["iterations"], "assembly_ms": main_r["assembly_ms"], "pcg_ms": main_r["solve_ms"],
+        other: {"ms_per_step": other_r["ms"], "iterations": other_r["iterations"],
+                "assembly_ms": other_r["assembly_ms"], "pcg_ms": other_r["solve_ms"]},
+        "trisolve": {"apply_ms": apply_r["ms"], "gbs": apply_r["gbs"], "frac": apply_r["gbs"] / hbm,
+                     "algorithmic_bytes": apply_r["bytes"], "stored_bytes": apply_r["stored_bytes"]},
+        "spmv": {"ms": spmv_r["ms"], "gbs": spmv_r["gbs"], "frac": spmv_r["gbs"] / hbm},
+        "roofline": {"bound": "hbm", "kernel": "ldlt apply (level-scheduled L and L^T sweeps)",
+                     "achieved": apply_r["gbs"], "peak": hbm, "peak_kind": pk_kind, "unit": "GB/s",
+                     "frac": apply_r["gbs"] / hbm, "traffic": traffic},
+        "e2e": {"value": e2e_r["ms"], "unit": "ms", "h2d_bytes_per_step": e2e_r["h2d"],
+                "d2h_bytes_per_step": e2e_r["d2h"]},
+        "gpu_launches": main_r["launches"],
+        "clocks": clk.summary(),
+        "setup_s": {"nested_dissection": W["t_nd"], "host_factor": W["t_factor"]},
+    }
+    if cpu is not None:
+        line["cpu_baseline"] = {"value": cpu["ms"], "unit": "ms", "cores": 1, "kind": "port",
+                                "sample": f"median of {cpu['steps']} oracle steps (assembly + {args.precond}-PCG, "
+                                          f"{cpu['iterations']} it) of the same {args.workload} state, 1 BLAS thread"}
+    print(json.dumps(line))
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

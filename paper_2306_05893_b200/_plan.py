@@ -108,7 +108,7 @@ class AssemblyPlan:
         self.m, self.N = m, N
 
         def up(a, dtype):
-            return t.from_numpy(np.ascontiguousarray(a, dtype=dtype)).to(dev)
+            return t.from_numpy(np.array(a, dtype=dtype, copy=True)).to(dev)
 
         self.conn = t.from_numpy(_i32(el.T)).to(dev)
         self.grads = up(precomp.grads.reshape(m, 12), np.float64)
