@@ -154,31 +154,51 @@ int tsb_element_blocks(const tsb_asm_plan *plan, const tsb_asm_coeffs *coeffs,
  * Factor values come from the host factorisation (ldlt_factor,
  * ndprecond.py:501-572) and are packed by the host into the layout below.
  * ---------------------------------------------------------------------- */
+/* Panel layout (built by the host from LdlFactors): every dissection block
+ * is cut into column panels of <= panel_width (128) columns.  Panel p owns
+ * permuted rows [p_start, p_start + p_w) and stores
+ *   tri  (p_tri, p_tri_len doubles): 16-wide tile-column panels of its strict
+ *        lower triangle (tile t: rows [t1, w) x 16) followed by the 16x16
+ *        tile inverses -- contiguous for one TMA bulk copy;
+ *   pan  (p_pan): its below panel, rows `below` (p_below: later rows of the
+ *        block, then the block's ancestors) x w columns, row-major;
+ *   cb   (p_cb): its slice of the contribution buffer (one per below row).
+ * Items are 8 x int32: type, panel, r0, r1, dep_off, dep_cnt, out_off, pad. */
 typedef struct tsb_ldlt_desc {
     int64_t n;
-    int64_t n_blocks;
-    int64_t n_levels;
-    int32_t tile;               /* diagonal tile width t (<= 32)                  */
-    int32_t max_block;          /* largest block size m                          */
-    /* per block, in factor order (ascending start; levels are contiguous runs) */
-    const int32_t *d_blk_start;   /* [nb] */
-    const int32_t *d_blk_size;    /* [nb] */
-    const int32_t *d_blk_nanc;    /* [nb] */
-    const int64_t *d_blk_l11;     /* [nb] offset of the packed column panels      */
-    const int64_t *d_blk_l21;     /* [nb] offset of the |anc| x m row-major panel  */
-    const int64_t *d_blk_tinv;    /* [nb] offset of the t x t tile inverses        */
-    const int64_t *d_blk_anc;     /* [nb] offset into d_anc / contribution buffer  */
-    const int32_t *h_level_ptr;   /* HOST [n_levels+1] block ranges per level      */
-    const double *d_l11;          /* column panels: tile it -> rows [t1,m) x t     */
-    const double *d_l21;
-    const double *d_tinv;
-    const int32_t *d_anc;         /* permuted ancestor row ids                     */
-    const int64_t *d_cin_ptr;     /* [n+1] contributions into permuted row k       */
-    const int32_t *d_cin_idx;     /* indices into the contribution buffer          */
+    int64_t n_panels;
+    int64_t n_items_lower;
+    int64_t n_items_upper;
+    int32_t tile;                 /* 16                                            */
+    int32_t panel_width;          /* <= 128                                        */
+    int32_t tri_smem_doubles;     /* max p_tri_len                                 */
+    int32_t max_chunk_rows;       /* max rows of an upper item                     */
+    int32_t grid;                 /* persistent CTAs (0 = fill the GPU)            */
+    int32_t pad_;
+    const int32_t *d_items_lower; /* dispatch order, topological                   */
+    const int32_t *d_items_upper;
+    const int32_t *d_p_start;
+    const int32_t *d_p_w;
+    const int64_t *d_p_tri;
+    const int64_t *d_p_tri_len;
+    const int64_t *d_p_pan;
+    const int64_t *d_p_cb;
+    const int64_t *d_p_below;
+    const double *d_tri;
+    const double *d_pan;
+    const int32_t *d_below;       /* permuted row ids                               */
+    const int32_t *d_deps;        /* panel ids: lower targets / upper owners        */
+    const int64_t *d_cin_ptr;     /* [n+1] contribution slots per permuted row      */
+    const int32_t *d_cin_idx;
     const double *d_d;            /* [n] D                                          */
     const int32_t *d_perm;        /* [n] perm[k] = original index at position k    */
-    double *d_cbuf;               /* scratch [sum |anc|]                           */
+    double *d_cbuf;               /* scratch: lower contributions                  */
+    double *d_part;               /* scratch: upper partial sums                   */
     double *d_y;                  /* scratch [n]                                   */
+    int32_t *d_cnt0, *d_cnt1, *d_cnt2, *d_cnt3; /* [n_panels] counters (zeroed)    */
+    int32_t *d_ctl;               /* [4] tickets / exit counters (zeroed)          */
+    int64_t *d_trace_lower;       /* optional [n_items_lower][4] item timeline     */
+    int64_t *d_trace_upper;       /* optional [n_items_upper][4]                   */
 } tsb_ldlt_desc;
 
 typedef struct tsb_ldlt *tsb_ldlt_t;

@@ -405,113 +405,7 @@ def _blocks_to_csr(n, blocks) -> CsrMatrix:
 # device image of the factors + level-scheduled solves
 # ---------------------------------------------------------------------------
 
-DEVICE_TILE = 16
-
-
-class DeviceFactors:
-    """Factor panels packed level-major into HBM (layout in csrc/ldlt.cu)."""
-
-    def __init__(self, factors: LdlFactors, stream=None):
-        t = _lib.require_cuda()
-        tile = factors.blocks[0].tile if factors.blocks else DEVICE_TILE
-        own_tiles = 4 <= tile <= 32 and tile % 4 == 0
-        dt = tile if own_tiles else DEVICE_TILE
-        order = [bf for lvl in factors.levels for bf in lvl]
-        level_ptr = np.zeros(len(factors.levels) + 1, dtype=np.int32)
-        np.cumsum([len(lvl) for lvl in factors.levels], out=level_ptr[1:])
-        nb = len(order)
-        start = np.empty(nb, dtype=np.int32)
-        size = np.empty(nb, dtype=np.int32)
-        nanc = np.empty(nb, dtype=np.int32)
-        o11 = np.empty(nb, dtype=np.int64)
-        o21 = np.empty(nb, dtype=np.int64)
-        otv = np.empty(nb, dtype=np.int64)
-        oan = np.empty(nb, dtype=np.int64)
-        p11, p21, ptv, pan = [], [], [], []
-        c11 = c21 = ctv = can = 0
-        for i, bf in enumerate(order):
-            m = bf.stop - bf.start
-            start[i], size[i], nanc[i] = bf.start, m, len(bf.anc)
-            o11[i], o21[i], otv[i], oan[i] = c11, c21, ctv, can
-            inv = bf.tile_inv if own_tiles else _tile_inverses(bf.l11, dt)
-            for it, t0 in enumerate(range(0, m, dt)):
-                t1 = min(t0 + dt, m)
-                if t1 < m:
-                    pnl = bf.l11[t1:, t0:t1]
-                    p11.append(pnl.ravel())
-                    c11 += pnl.size
-                tv = np.zeros((dt, dt))
-                tv[: t1 - t0, : t1 - t0] = inv[it]
-                ptv.append(tv.ravel())
-                ctv += dt * dt
-            if len(bf.anc):
-                p21.append(bf.l21.ravel())
-                c21 += bf.l21.size
-                pan.append(bf.anc)
-                can += len(bf.anc)
-        cat = lambda parts, dtype: (np.concatenate(parts).astype(dtype, copy=False)  # noqa: E731
-                                    if parts else np.zeros(1, dtype=dtype))
-        anc_all = cat(pan, np.int64)
-        n = factors.plan.n
-        if can:
-            corder = np.argsort(anc_all, kind="stable")
-            cin_ptr = np.zeros(n + 1, dtype=np.int64)
-            np.cumsum(np.bincount(anc_all, minlength=n), out=cin_ptr[1:])
-        else:
-            corder = np.zeros(1, dtype=np.int64)
-            cin_ptr = np.zeros(n + 1, dtype=np.int64)
-        s = stream
-        ctx = t.cuda.stream(s) if s is not None else _nullctx()
-        with ctx:
-            up = lambda a: t.from_numpy(np.ascontiguousarray(a)).pin_memory().to("cuda", non_blocking=True)  # noqa: E731
-            self.t = {
-                "start": up(start), "size": up(size), "nanc": up(nanc), "o11": up(o11), "o21": up(o21),
-                "otv": up(otv), "oan": up(oan), "l11": up(cat(p11, np.float64)),
-                "l21": up(cat(p21, np.float64)), "tinv": up(cat(ptv, np.float64)),
-                "anc": up(anc_all.astype(np.int32)), "cin_ptr": up(cin_ptr),
-                "cin_idx": up(corder.astype(np.int32)), "d": up(np.asarray(factors.d, dtype=np.float64)),
-                "perm": up(np.asarray(factors.plan.perm, dtype=np.int32)),
-            }
-            self.t["cbuf"] = t.empty(max(can, 1), dtype=t.float64, device="cuda")
-            self.t["y"] = t.empty(max(n, 1), dtype=t.float64, device="cuda")
-        self.level_ptr = level_ptr
-        self.n = n
-        self.tile = dt
-        self.bytes = {"l11": c11 * 8, "l21": c21 * 8, "tinv": ctv * 8}
-        P = lambda k: _lib.ptr(self.t[k])  # noqa: E731
-        self.desc = _lib.LdltDesc(
-            n=n, n_blocks=nb, n_levels=len(factors.levels), tile=dt,
-            max_block=int(size.max()) if nb else 0,
-            d_blk_start=P("start"), d_blk_size=P("size"), d_blk_nanc=P("nanc"), d_blk_l11=P("o11"),
-            d_blk_l21=P("o21"), d_blk_tinv=P("otv"), d_blk_anc=P("oan"),
-            h_level_ptr=level_ptr.ctypes.data, d_l11=P("l11"), d_l21=P("l21"), d_tinv=P("tinv"),
-            d_anc=P("anc"), d_cin_ptr=P("cin_ptr"), d_cin_idx=P("cin_idx"), d_d=P("d"), d_perm=P("perm"),
-            d_cbuf=P("cbuf"), d_y=P("y"),
-        )
-        h = C.c_void_p()
-        _lib.check(_lib.load().tsb_ldlt_create(C.byref(self.desc), C.byref(h)), "ldlt_create")
-        self.h = h
-        self._lib = _lib.load()
-
-    def __del__(self):
-        try:
-            if self.h:
-                self._lib.tsb_ldlt_destroy(self.h)
-        except Exception:
-            pass
-
-    def run(self, mode: str, r, out):
-        fn = {"lower": self._lib.tsb_ldlt_lower, "upper": self._lib.tsb_ldlt_upper,
-              "apply": self._lib.tsb_ldlt_apply}[mode]
-        _lib.check(fn(self.h, _lib.ptr(r), _lib.ptr(out), _lib.stream_ptr()), f"ldlt_{mode}")
-
-
-class _nullctx:
-    def __enter__(self):
-        return self
-
-    def __exit__(self, *a):
-        return False
+from ._ldlt_pack import DevicePanels as DeviceFactors  # noqa: E402  (device image of the factors)
 
 
 def as_factors(obj):
