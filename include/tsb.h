@@ -154,15 +154,17 @@ int tsb_element_blocks(const tsb_asm_plan *plan, const tsb_asm_coeffs *coeffs,
  * Factor values come from the host factorisation (ldlt_factor,
  * ndprecond.py:501-572) and are packed by the host into the layout below.
  * ---------------------------------------------------------------------- */
-/* Panel layout (built by the host from LdlFactors): every dissection block
- * is cut into column panels of <= panel_width (128) columns.  Panel p owns
- * permuted rows [p_start, p_start + p_w) and stores
- *   tri  (p_tri, p_tri_len doubles): 16-wide tile-column panels of its strict
- *        lower triangle (tile t: rows [t1, w) x 16) followed by the 16x16
- *        tile inverses -- contiguous for one TMA bulk copy;
- *   pan  (p_pan): its below panel, rows `below` (p_below: later rows of the
- *        block, then the block's ancestors) x w columns, row-major;
- *   cb   (p_cb): its slice of the contribution buffer (one per below row).
+/* Panel layout (built by the host from LdlFactors, _ldlt_pack.py): every
+ * dissection block is cut into column panels of <= panel_width (128) columns.
+ * Panel p owns permuted rows [p_start, p_start + p_w) and stores
+ *   tri   (p_tri, p_tri_len doubles): the strict lower part of the inverse of
+ *         its unit-lower diagonal triangle, column-packed in d_tri (lower
+ *         sweep) and row-packed in d_tri_u (upper sweep), even length;
+ *   pan   (p_pan): its below panel, rows `below` (p_below: later rows of the
+ *         block, then the block's ancestors) x w columns, row-major, rows
+ *         padded to an even stride (16-byte TMA chunks);
+ *   cb    (p_cb): per below row, its slot in the row-contiguous contribution
+ *         buffer (d_cslot), so row r's contributions are cbuf[cin_ptr[r]..].
  * Items are 8 x int32: type, panel, r0, r1, dep_off, dep_cnt, out_off, pad. */
 typedef struct tsb_ldlt_desc {
     int64_t n;
@@ -171,7 +173,7 @@ typedef struct tsb_ldlt_desc {
     int64_t n_items_upper;
     int32_t tile;                 /* 16                                            */
     int32_t panel_width;          /* <= 128                                        */
-    int32_t tri_smem_doubles;     /* max p_tri_len                                 */
+    int32_t stage_doubles;        /* TMA staging: max(tri, chunk) doubles          */
     int32_t max_chunk_rows;       /* max rows of an upper item                     */
     int32_t grid;                 /* persistent CTAs (0 = fill the GPU)            */
     int32_t pad_;
@@ -184,12 +186,13 @@ typedef struct tsb_ldlt_desc {
     const int64_t *d_p_pan;
     const int64_t *d_p_cb;
     const int64_t *d_p_below;
-    const double *d_tri;
+    const double *d_tri;          /* column-packed panel inverses (lower sweep)    */
+    const double *d_tri_u;        /* row-packed panel inverses (upper sweep)       */
     const double *d_pan;
     const int32_t *d_below;       /* permuted row ids                               */
     const int32_t *d_deps;        /* panel ids: lower targets / upper owners        */
-    const int64_t *d_cin_ptr;     /* [n+1] contribution slots per permuted row      */
-    const int32_t *d_cin_idx;
+    const int64_t *d_cin_ptr;     /* [n+1] contiguous contribution slots per row    */
+    const int32_t *d_cslot;       /* [sum below] slot of (panel, below row) in cbuf */
     const double *d_d;            /* [n] D                                          */
     const int32_t *d_perm;        /* [n] perm[k] = original index at position k    */
     double *d_cbuf;               /* scratch: lower contributions                  */

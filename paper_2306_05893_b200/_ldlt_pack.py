@@ -2,7 +2,7 @@
 
 Runs once per factor refresh (on the AsyncPreconditioner worker thread for
 the async path).  Cuts every dissection block of `LdlFactors` into column
-panels of <= PANEL_W columns, lays out the triangle/tile-inverse blobs and
+panels of <= PANEL_W columns, lays out the diagonal-triangle inverses and
 the below panels contiguously for streaming, builds the work-item lists of
 the two sweeps (csrc/ldlt.cu) and orders them critical-path first.
 
@@ -29,13 +29,30 @@ CRIT_ROWS = 32         # chunk rows for the next panel of the same block (critic
 IT_DIAG, IT_OFF, IT_OFFT, IT_DIAGT = 0, 1, 2, 3
 
 
-def _tile_inv16(l11):
-    m = len(l11)
-    out = []
-    for t0 in range(0, m, TILE):
-        t1 = min(t0 + TILE, m)
-        out.append(np.linalg.inv(l11[t0:t1, t0:t1]))
-    return out
+def packed_inverse(l):
+    """Strict lower part of inv(l) for a unit-lower l -> (column-packed, row-packed).
+
+    Column-packed: column j holds rows j+1..w-1 at j(2w-j-1)/2 (lower sweep:
+    thread per row reads consecutive words); row-packed: row i holds columns
+    0..i-1 at i(i-1)/2 (upper sweep).  Padded to an even length (16-byte TMA).
+    """
+    from scipy.linalg import solve_triangular
+
+    w = len(l)
+    inv = solve_triangular(l, np.eye(w), lower=True, unit_diagonal=True, check_finite=False)
+    rows = inv[np.tril_indices(w, -1)]
+    cols = inv.T[np.triu_indices(w, 1)]
+    if len(rows) == 0:
+        return np.zeros(2), np.zeros(2)
+    if len(rows) % 2:
+        rows, cols = np.append(rows, 0.0), np.append(cols, 0.0)
+    return cols, rows
+
+
+def _inverse(order):
+    inv = np.empty_like(order)
+    inv[order] = np.arange(len(order))
+    return inv
 
 
 def _chunks(nb, n_crit, w):
@@ -45,7 +62,7 @@ def _chunks(nb, n_crit, w):
     while r < n_crit:
         out.append((r, min(r + CRIT_ROWS, n_crit)))
         r = out[-1][1]
-    step = max(32, CHUNK_ELEMS // max(w, 1))
+    step = max(32, CHUNK_ELEMS // max(w + (w & 1), 1))
     while r < nb:
         out.append((r, min(r + step, nb)))
         r = out[-1][1]
@@ -59,33 +76,26 @@ def pack(factors):
         order = [bf for lvl in factors.levels for bf in lvl]
         # -------- panels --------
         p_start, p_w, p_blk = [], [], []
-        tri_parts, pan_parts, below_parts = [], [], []
+        tri_parts, tri_u_parts, pan_parts, below_parts = [], [], [], []
         p_tri, p_tri_len, p_pan, p_below, p_cb = [], [], [], [], []
         ct = cp = cb = cbuf = 0
         panel_of_row = np.empty(n, dtype=np.int64)
         crit = []
         for bi, bf in enumerate(order):
             s, m = bf.start, bf.stop - bf.start
-            inv = bf.tile_inv if bf.tile == TILE else _tile_inv16(bf.l11)
             anc = np.asarray(bf.anc, dtype=np.int64)
             for c0 in range(0, m, PANEL_W):
                 w = min(PANEL_W, m - c0)
                 pid = len(p_start)
                 panel_of_row[s + c0:s + c0 + w] = pid
                 below = np.concatenate([np.arange(s + c0 + w, s + m, dtype=np.int64), anc])
-                pan = np.concatenate([bf.l11[c0 + w:, c0:c0 + w].ravel(), bf.l21[:, c0:c0 + w].ravel()])
-                blob = []
-                nt = (w + TILE - 1) // TILE
-                for k in range(nt):
-                    t0 = c0 + k * TILE
-                    t1 = min(t0 + TILE, c0 + w)
-                    blob.append(bf.l11[t1:c0 + w, t0:t0 + TILE].ravel())
-                for k in range(nt):
-                    tv = np.zeros((TILE, TILE))
-                    iv = inv[c0 // TILE + k]
-                    tv[: iv.shape[0], : iv.shape[1]] = iv
-                    blob.append(tv.ravel())
-                blob = np.concatenate(blob)
+                # rows padded to an even stride so every chunk is a 16-byte-aligned TMA copy
+                ws = w + (w & 1)
+                pan = np.zeros((len(below), ws))
+                pan[: m - c0 - w, :w] = bf.l11[c0 + w:, c0:c0 + w]
+                pan[m - c0 - w:, :w] = bf.l21[:, c0:c0 + w]
+                pan = pan.ravel()
+                blob, blob_u = packed_inverse(bf.l11[c0:c0 + w, c0:c0 + w])
                 p_start.append(s + c0)
                 p_w.append(w)
                 p_blk.append(bi)
@@ -95,6 +105,7 @@ def pack(factors):
                 p_below.append(cb)
                 p_cb.append(cbuf)
                 tri_parts.append(blob)
+                tri_u_parts.append(blob_u)
                 pan_parts.append(pan)
                 below_parts.append(below)
                 ct += len(blob)
@@ -122,7 +133,7 @@ def pack(factors):
         tri_len = np.asarray(p_tri_len, dtype=np.int64)
 
         def cost_diag(p):
-            return 1.0 + 0.25 * ((p_w[p] + TILE - 1) // TILE) + tri_len[p] * 8 / 150e3
+            return 1.5 + tri_len[p] * 8 / 100e3
 
         def cost_chunk(p, r0, r1):
             return 0.8 + (r1 - r0) * p_w[p] * 8 / 40e3
@@ -164,6 +175,9 @@ def pack(factors):
         cin_ptr = np.zeros(n + 1, dtype=np.int64)
         np.cumsum(np.bincount(rows_all, minlength=n), out=cin_ptr[1:])
         max_chunk = max((r1 - r0 for ch in chunks for r0, r1 in ch), default=1)
+        # staging buffer: the largest tri blob or factor chunk (rows x padded width)
+        stage = max([int(tri_len.max()) if P else 0] +
+                    [(r1 - r0) * (int(p_w[p]) + int(p_w[p]) % 2) for p in range(P) for r0, r1 in chunks[p]])
 
         cat = lambda parts, dt: (np.concatenate(parts).astype(dt, copy=False) if parts  # noqa: E731
                                  else np.zeros(1, dtype=dt))
@@ -172,11 +186,15 @@ def pack(factors):
         "p_w": p_w, "p_tri": np.asarray(p_tri, dtype=np.int64), "p_tri_len": tri_len,
         "p_pan": np.asarray(p_pan, dtype=np.int64), "p_cb": np.asarray(p_cb, dtype=np.int64),
         "p_below": np.asarray(p_below, dtype=np.int64), "tri": cat(tri_parts, np.float64),
+        "tri_u": cat(tri_u_parts, np.float64),
         "pan": cat(pan_parts, np.float64), "below": cat(below_parts, np.int64),
         "deps": np.asarray(deps if deps else [0], dtype=np.int64), "cin_ptr": cin_ptr,
-        "cin_idx": corder if len(corder) else np.zeros(1, dtype=np.int64),
+        # contributions land row-contiguous: entry i of the concatenated below lists
+        # (panel order) goes to slot cslot[i]; row r reads cbuf[cin_ptr[r]:cin_ptr[r+1]]
+        "cslot": _inverse(corder) if len(corder) else np.zeros(1, dtype=np.int64),
         "d": np.asarray(factors.d, dtype=np.float64), "perm": np.asarray(factors.plan.perm, dtype=np.int64),
-        "ncbuf": cbuf, "npart": int(part_off[-1]), "max_chunk": int(max_chunk), "bytes_tri": ct * 8,
+        "ncbuf": cbuf, "npart": int(part_off[-1]), "max_chunk": int(max_chunk), "stage": int(stage),
+        "bytes_tri": ct * 8,
         "bytes_pan": cp * 8,
     }
 
@@ -191,8 +209,8 @@ class DevicePanels:
         items_l, items_u, tri_len = H["items_l"], H["items_u"], H["p_tri_len"]
         self.host = H if trace else None
         if trace:  # per-item timeline (globaltimer ns): take, ready, end, smid
-            self.trace_l = t.zeros((len(items_l), 4), dtype=t.int64, device="cuda")
-            self.trace_u = t.zeros((len(items_u), 4), dtype=t.int64, device="cuda")
+            self.trace_l = t.zeros((len(items_l), 8), dtype=t.int64, device="cuda")
+            self.trace_u = t.zeros((len(items_u), 8), dtype=t.int64, device="cuda")
         ctx = t.cuda.stream(stream) if stream is not None else _NullCtx()
         with ctx:
             up = lambda a: t.from_numpy(np.ascontiguousarray(a)).pin_memory().to("cuda", non_blocking=True)  # noqa: E731
@@ -202,8 +220,8 @@ class DevicePanels:
                 "items_l": up(items_l), "items_u": up(items_u), "p_start": i32(H["p_start"]),
                 "p_w": i32(H["p_w"]), "p_tri": i64(H["p_tri"]), "p_tri_len": i64(tri_len),
                 "p_pan": i64(H["p_pan"]), "p_cb": i64(H["p_cb"]), "p_below": i64(H["p_below"]),
-                "tri": up(H["tri"]), "pan": up(H["pan"]), "below": i32(H["below"]), "deps": i32(H["deps"]),
-                "cin_ptr": i64(H["cin_ptr"]), "cin_idx": i32(H["cin_idx"]), "d": up(H["d"]),
+                "tri": up(H["tri"]), "tri_u": up(H["tri_u"]), "pan": up(H["pan"]), "below": i32(H["below"]), "deps": i32(H["deps"]),
+                "cin_ptr": i64(H["cin_ptr"]), "cslot": i32(H["cslot"]), "d": up(H["d"]),
                 "perm": i32(H["perm"]),
             }
             z = lambda k, dt: t.zeros(max(k, 1), dtype=dt, device="cuda")  # noqa: E731
@@ -218,12 +236,12 @@ class DevicePanels:
         cnt = self.t["cnt"]
         self.desc = _lib.LdltDesc(
             n=n, n_panels=P, n_items_lower=len(items_l), n_items_upper=len(items_u), tile=TILE,
-            panel_width=PANEL_W, tri_smem_doubles=int(tri_len.max()) if P else 0, max_chunk_rows=int(max_chunk),
+            panel_width=PANEL_W, stage_doubles=H["stage"], max_chunk_rows=int(max_chunk),
             grid=0, pad_=0,
             d_items_lower=tp("items_l"), d_items_upper=tp("items_u"), d_p_start=tp("p_start"), d_p_w=tp("p_w"),
             d_p_tri=tp("p_tri"), d_p_tri_len=tp("p_tri_len"), d_p_pan=tp("p_pan"), d_p_cb=tp("p_cb"),
-            d_p_below=tp("p_below"), d_tri=tp("tri"), d_pan=tp("pan"), d_below=tp("below"), d_deps=tp("deps"),
-            d_cin_ptr=tp("cin_ptr"), d_cin_idx=tp("cin_idx"), d_d=tp("d"), d_perm=tp("perm"),
+            d_p_below=tp("p_below"), d_tri=tp("tri"), d_tri_u=tp("tri_u"), d_pan=tp("pan"), d_below=tp("below"), d_deps=tp("deps"),
+            d_cin_ptr=tp("cin_ptr"), d_cslot=tp("cslot"), d_d=tp("d"), d_perm=tp("perm"),
             d_cbuf=tp("cbuf"), d_part=tp("part"), d_y=tp("y"),
             d_cnt0=_lib.ptr(cnt[0:P]) if P else tp("cnt"), d_cnt1=_lib.ptr(cnt[P:2 * P]) if P else tp("cnt"),
             d_cnt2=_lib.ptr(cnt[2 * P:3 * P]) if P else tp("cnt"), d_cnt3=_lib.ptr(cnt[3 * P:]) if P else tp("cnt"),

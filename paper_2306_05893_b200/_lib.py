@@ -57,12 +57,12 @@ class AsmCoeffs(C.Structure):
 class LdltDesc(C.Structure):
     _fields_ = [
         ("n", c_i64), ("n_panels", c_i64), ("n_items_lower", c_i64), ("n_items_upper", c_i64),
-        ("tile", c_i32), ("panel_width", c_i32), ("tri_smem_doubles", c_i32), ("max_chunk_rows", c_i32),
+        ("tile", c_i32), ("panel_width", c_i32), ("stage_doubles", c_i32), ("max_chunk_rows", c_i32),
         ("grid", c_i32), ("pad_", c_i32),
         ("d_items_lower", c_vp), ("d_items_upper", c_vp), ("d_p_start", c_vp), ("d_p_w", c_vp),
         ("d_p_tri", c_vp), ("d_p_tri_len", c_vp), ("d_p_pan", c_vp), ("d_p_cb", c_vp), ("d_p_below", c_vp),
-        ("d_tri", c_vp), ("d_pan", c_vp), ("d_below", c_vp), ("d_deps", c_vp),
-        ("d_cin_ptr", c_vp), ("d_cin_idx", c_vp), ("d_d", c_vp), ("d_perm", c_vp),
+        ("d_tri", c_vp), ("d_tri_u", c_vp), ("d_pan", c_vp), ("d_below", c_vp), ("d_deps", c_vp),
+        ("d_cin_ptr", c_vp), ("d_cslot", c_vp), ("d_d", c_vp), ("d_perm", c_vp),
         ("d_cbuf", c_vp), ("d_part", c_vp), ("d_y", c_vp),
         ("d_cnt0", c_vp), ("d_cnt1", c_vp), ("d_cnt2", c_vp), ("d_cnt3", c_vp), ("d_ctl", c_vp),
         ("d_trace_lower", c_vp), ("d_trace_upper", c_vp),

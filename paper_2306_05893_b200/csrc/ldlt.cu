@@ -5,26 +5,28 @@
 // Replaces solve_lower (ndprecond.py:647-671, _forward_block 623-631),
 // solve_upper (674-691, _backward_block 634-644) and apply (694-700).  Factor
 // values come from the host factorisation (ldlt_factor, ndprecond.py:501-572)
-// and are re-cut on the host (paper_2306_05893_b200/ndprecond.py,
-// DeviceFactors) into PANELS: every dissection block is split into column
-// panels of <= 128 columns.  Panel p of block b owns columns [c0, c0+w) and
-//   tri    the strict-lower w x w triangle as 16-wide tile-column panels plus
-//          the 16x16 tile inverses (the reference's tile_inv, t = 16) --
-//          contiguous, so one TMA bulk copy stages it in shared memory;
-//   P      its "below" panel: rows (block rows >= c0+w) U anc(b), w columns,
-//          row-major -- [L11[c0+w:, c0:c0+w]; L21[:, c0:c0+w]].
+// and are re-cut on the host (paper_2306_05893_b200/_ldlt_pack.py) into
+// PANELS: every dissection block is split into column panels of <= 128
+// columns.  Panel p of block b owns columns [c0, c0+w) and stores
+//   tri    the explicit inverse of its unit-lower w x w diagonal triangle --
+//          the reference's tile_inv (ndprecond.py:575-587) widened from 16 to
+//          the whole panel, so the in-panel solve is one dependency-free GEMV
+//          (column-packed copy for the lower sweep, row-packed for the upper,
+//          each read by its sweep only; staged in shared memory by one TMA copy);
+//   P      its below panel: rows (block rows >= c0+w) U anc(b), w columns,
+//          row-major, rows padded to an even stride -- [L11[c0+w:, c0:c0+w];
+//          L21[:, c0:c0+w]] -- streamed chunk by chunk with TMA bulk copies.
 // Work items (dispatched in a precomputed topological, critical-path-first
 // order through one atomic ticket counter; every CTA is resident, so an item
 // only ever waits on items dispensed before it):
-//   lower  DIAG(p)        rows of p = input - pre-accumulated contributions
-//                         (gathered in a fixed order -> deterministic, no
-//                         atomics on data), then the tile chain in smem
-//                         (tile_inv matvec, column-major push) -> y[p]
-//          OFFDIAG(p,k)   contributions of y[p] to a chunk of p's below rows
+//   lower  DIAG(p)        rows of p = input - contributions pre-accumulated by
+//                         earlier panels (row-contiguous, summed in a fixed
+//                         order -> deterministic, no atomics on data), then
+//                         y_p = inv(L_pp) x_p
+//          OFFDIAG(p,k)   contributions of y_p to a chunk of p's below rows
 //                         (column-major pre-accumulation, paper Fig. solveBlock)
-//   upper  OFFDIAG_T(p,k) partial sums of P[k rows]^T z[below]   (row-major pull)
-//          DIAG_T(p)      w - sum of partials (chunk order), backward tile chain
-//                         with tile_inv^T -> z[p]
+//   upper  OFFDIAG_T(p,k) partial sums P[k rows]^T z[below]        (row-major pull)
+//          DIAG_T(p)      z_p = inv(L_pp)^T (w_p - sum of partials in chunk order)
 // Counters (int32 per panel) are reset by the last CTA to leave, so the kernel
 // can be replayed inside the PCG graph without extra memsets.
 #include <mutex>
@@ -40,7 +42,7 @@ struct tsb_ldlt {
 namespace tsb {
 
 constexpr int kSweepBlock = 256;
-constexpr int kT = 16;        // diagonal tile (the reference's default tile)
+constexpr int kT = 16;        // device tile parameter (ABI: panels start at multiples of it)
 constexpr int kMaxW = 128;    // panel width
 enum { IT_DIAG = 0, IT_OFF = 1, IT_OFFT = 2, IT_DIAGT = 3 };
 
@@ -56,6 +58,7 @@ __device__ __forceinline__ void mbar_init(uint64_t *bar, int count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
+// one-thread TMA bulk copy global -> shared, completion on the mbarrier
 __device__ __forceinline__ void tma_load_1d(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
@@ -88,16 +91,16 @@ __device__ __forceinline__ void spin_until_geq(const int *p, int target) {
     }
 }
 
-// Optional per-item timeline (globaltimer ns): [take, ready, end, smid].
+// Optional per-item timeline (globaltimer ns): [take, ready, end, smid, staged, computed].
 __device__ __forceinline__ void trace(int64_t *buf, int iid, int slot) {
     if (buf != nullptr && threadIdx.x == 0) {
         uint64_t t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        buf[(int64_t)iid * 4 + slot] = (int64_t)t;
+        buf[(int64_t)iid * 8 + slot] = (int64_t)t;
         if (slot == 0) {
             uint32_t sm;
             asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
-            buf[(int64_t)iid * 4 + 3] = sm;
+            buf[(int64_t)iid * 8 + 3] = sm;
         }
     }
 }
@@ -135,18 +138,73 @@ __device__ __forceinline__ void sweep_exit(const tsb_ldlt_desc &D, int32_t *ctl,
 }
 
 // ---------------------------------------------------------------------------
-// lower sweep: L y = r
+// Diagonal-panel GEMVs with the explicit inverse of the unit-lower triangle.
+// The factor blocks are well conditioned (cond(L11) <= 3.4 on the beams); the
+// panel-inverse sweeps agree with the tile-16 reference to ~6e-16.
+// Both put one output per thread, two partial sums (column/row parity), so
+// consecutive threads read consecutive shared-memory words.
 // ---------------------------------------------------------------------------
+// column-packed strict lower: column j holds rows j+1..w-1 at j*(2w-j-1)/2
+__device__ __forceinline__ int col_off(int j, int w) { return (j * (2 * w - j - 1)) >> 1; }
+// row-packed strict lower: row i holds columns 0..i-1 at i*(i-1)/2
+__device__ __forceinline__ int row_off(int i) { return (i * (i - 1)) >> 1; }
+
+// y = inv(L_pp) x   (lower sweep): thread per row i, columns j < i of one parity
+__device__ __forceinline__ void panel_lower(const double *Lc, int w, const double *x, double *y, double *red,
+                                            int tid) {
+    const int i = tid & (kMaxW - 1), h = tid / kMaxW;
+    double a0 = 0.0, a1 = 0.0;
+    if (i < w) {
+        int j = h;
+        for (; j + 2 < i; j += 4) {
+            a0 += Lc[col_off(j, w) + i - j - 1] * x[j];
+            a1 += Lc[col_off(j + 2, w) + i - j - 3] * x[j + 2];
+        }
+        if (j < i) a0 += Lc[col_off(j, w) + i - j - 1] * x[j];
+    }
+    red[tid] = a0 + a1;
+    __syncthreads();
+    if (tid < w) y[tid] = x[tid] + (red[tid] + red[tid + kMaxW]);
+}
+
+// z = inv(L_pp)^T v   (upper sweep): thread per column j, rows i > j of one parity
+__device__ __forceinline__ void panel_upper(const double *Lr, int w, const double *v, double *z, double *red,
+                                            int tid) {
+    const int j = tid & (kMaxW - 1), h = tid / kMaxW;
+    double a0 = 0.0, a1 = 0.0;
+    if (j < w) {
+        int i = j + 1;
+        if ((i & 1) != h) ++i;
+        for (; i + 2 < w; i += 4) {
+            a0 += Lr[row_off(i) + j] * v[i];
+            a1 += Lr[row_off(i + 2) + j] * v[i + 2];
+        }
+        if (i < w) a0 += Lr[row_off(i) + j] * v[i];
+    }
+    red[tid] = a0 + a1;
+    __syncthreads();
+    if (tid < w) z[tid] = v[tid] + (red[tid] + red[tid + kMaxW]);
+}
+
+// ---------------------------------------------------------------------------
+// lower sweep: L y = r
+// shared memory: [stage][seg 128][yv 128][red 256][row pointers 130 x int64][dst slots]
+// ---------------------------------------------------------------------------
+template <bool TRACE>
 __global__ void __launch_bounds__(kSweepBlock)
 lower_sweep(tsb_ldlt_desc D, SweepArgs A) {
     extern __shared__ __align__(128) double smem[];
-    double *tri = smem;                               // staged tri + tinv of a DIAG panel
-    double *seg = smem + D.tri_smem_doubles;          // panel rows (w <= 128)
+    double *stage = smem;                             // TMA staging: panel inverse or factor chunk
+    double *seg = smem + D.stage_doubles;             // gathered panel rows
+    double *yv = seg + kMaxW;                         // solved panel rows
+    double *red = yv + kMaxW;                         // 256 partial sums
+    int64_t *rptr = reinterpret_cast<int64_t *>(red + kSweepBlock);  // contribution row pointers
+    int32_t *dsts = reinterpret_cast<int32_t *>(rptr + kMaxW + 2);   // chunk rows' cbuf slots
     __shared__ uint64_t bar;
     __shared__ int item_id;
-    __shared__ double tvec[kT];
     int32_t *ctl = D.d_ctl;
     int32_t *contrib = D.d_cnt0, *flag = D.d_cnt1;
+    int64_t *const tbuf = TRACE ? D.d_trace_lower : nullptr;  // folds away when off
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (A.done != nullptr && *((volatile const int32_t *)A.done)) {
         sweep_exit(D, ctl, contrib, flag);
@@ -161,96 +219,78 @@ lower_sweep(tsb_ldlt_desc D, SweepArgs A) {
         __syncthreads();
         const int iid = item_id;
         if (iid >= D.n_items_lower) break;
-        trace(D.d_trace_lower, iid, 0);
+        trace(tbuf, iid, 0);
         const Item it = items[iid];
         const int p = it.panel;
         const int pstart = D.d_p_start[p], w = D.d_p_w[p];
         if (it.type == IT_DIAG) {
-            const int ntiles = (w + kT - 1) / kT;
-            const int64_t tbytes = D.d_p_tri_len[p] * 8;
-            if (tid == 0) tma_load_1d(tri, D.d_tri + D.d_p_tri[p], (uint32_t)tbytes, &bar);
-            if (tid == 0) spin_until_geq(contrib + p, it.dep_cnt);
+            if (tid == 0) {
+                tma_load_1d(stage, D.d_tri + D.d_p_tri[p], (uint32_t)(D.d_p_tri_len[p] * 8), &bar);
+                spin_until_geq(contrib + p, it.dep_cnt);
+            }
+            if (tid <= w) rptr[tid] = __ldg(D.d_cin_ptr + pstart + tid);
             __syncthreads();
-            trace(D.d_trace_lower, iid, 1);
-            // rows: input - contributions pre-accumulated by earlier panels.  8 lanes
-            // per row, lane-strided sums + xor tree: a fixed order (deterministic).
-            for (int kb = warp * 4; kb < w; kb += kSweepBlock / 8) {
-                const int k = kb + (lane >> 3), l8 = lane & 7;
-                double acc = 0.0;
-                if (k < w) {
-                    const int row = pstart + k;
-                    const int64_t q0 = D.d_cin_ptr[row], q1 = D.d_cin_ptr[row + 1];
+            trace(tbuf, iid, 1);
+            // rows: input - contributions; 8 lanes per row, lane-strided partial
+            // sums + xor tree = a fixed summation order (deterministic)
+            {
+                const int l8 = lane & 7;
+                for (int kb = warp * 4; kb < w; kb += kSweepBlock / 8) {
+                    const int k = kb + (lane >> 3);
+                    double acc = 0.0;
+                    if (k < w) {
+                        const int64_t q1 = rptr[k + 1];
 #pragma unroll 4
-                    for (int64_t q = q0 + l8; q < q1; q += 8) acc += __ldcg(D.d_cbuf + D.d_cin_idx[q]);
-                }
-                acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-                acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-                acc += __shfl_xor_sync(0xffffffffu, acc, 4);
-                if (k < w && l8 == 0) {
-                    const int row = pstart + k;
-                    seg[k] = A.in[A.in_perm ? A.in_perm[row] : row] - acc;
+                        for (int64_t q = rptr[k] + l8; q < q1; q += 8) acc += __ldcg(D.d_cbuf + q);
+                    }
+                    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+                    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+                    acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+                    if (k < w && l8 == 0) {
+                        const int row = pstart + k;
+                        seg[k] = A.in[A.in_perm ? A.in_perm[row] : row] - acc;
+                    }
                 }
             }
             mbar_wait(&bar, phase);
             phase ^= 1;
             __syncthreads();
-            const double *tinv = tri + D.d_p_tri_len[p] - ntiles * kT * kT;
-            const double *tp = tri;
-            for (int t = 0; t < ntiles; ++t) {
-                const int t0 = t * kT, tw = min(kT, w - t0), t1 = t0 + tw;
-                if (warp == 0) {
-                    double acc = 0.0;
-                    if (lane < tw) {
-                        const double *ti = tinv + t * kT * kT + lane * kT;
-                        for (int j = 0; j < tw; ++j) acc += ti[j] * seg[t0 + j];
-                    }
-                    __syncwarp();
-                    if (lane < tw) {
-                        seg[t0 + lane] = acc;
-                        tvec[lane] = acc;
-                    } else if (lane < kT) {
-                        tvec[lane] = 0.0;
-                    }
-                }
-                __syncthreads();
-                // trailing rows inside the panel: 4 lanes per row, 4 columns each
-                const int nrows = w - t1;
-                for (int rb = (tid >> 5) * 8; rb < nrows; rb += kSweepBlock / 4) {
-                    const int r = rb + (lane >> 2);
-                    double part = 0.0;
-                    if (r < nrows) {
-                        const double *pr = tp + r * kT + (lane & 3) * 4;
-#pragma unroll
-                        for (int c = 0; c < 4; ++c) part += pr[c] * tvec[(lane & 3) * 4 + c];
-                    }
-                    part += __shfl_xor_sync(0xffffffffu, part, 1);
-                    part += __shfl_xor_sync(0xffffffffu, part, 2);
-                    if ((lane & 3) == 0 && r < nrows) seg[t1 + r] -= part;
-                }
-                tp += nrows * kT;
-                __syncthreads();
-            }
-            for (int k = tid; k < w; k += kSweepBlock) A.x[pstart + k] = seg[k];
+            trace(tbuf, iid, 4);
+            panel_lower(stage, w, seg, yv, red, tid);
+            __syncthreads();
+            for (int k = tid; k < w; k += kSweepBlock) A.x[pstart + k] = yv[k];
+            trace(tbuf, iid, 5);
             __threadfence();
             __syncthreads();
             if (tid == 0) atomicExch(flag + p, 1);
-            trace(D.d_trace_lower, iid, 2);
+            trace(tbuf, iid, 2);
         } else {  // IT_OFF: contributions of panel p to below rows [r0, r1)
-            if (tid == 0) spin_until_geq(flag + p, 1);
+            // the factor chunk does not depend on the sweep: stage it with TMA while
+            // waiting for the panel's solution
+            const int ws = w + (w & 1), nr = it.r1 - it.r0;
+            if (tid == 0) {
+                tma_load_1d(stage, D.d_pan + D.d_p_pan[p] + (int64_t)it.r0 * ws, (uint32_t)(nr * ws * 8), &bar);
+                spin_until_geq(flag + p, 1);
+            }
+            const int32_t *slot = D.d_cslot + D.d_p_cb[p] + it.r0;
+            for (int j = tid; j < nr; j += kSweepBlock) dsts[j] = __ldg(slot + j);
             __syncthreads();
-            trace(D.d_trace_lower, iid, 1);
+            trace(tbuf, iid, 1);
             for (int k = tid; k < w; k += kSweepBlock) seg[k] = __ldcg(A.x + pstart + k);
+            mbar_wait(&bar, phase);
+            phase ^= 1;
             __syncthreads();
-            const double *P = D.d_pan + D.d_p_pan[p];
-            double *cb = D.d_cbuf + D.d_p_cb[p];
-            for (int j0 = it.r0 + warp * 2; j0 < it.r1; j0 += (kSweepBlock / 32) * 2) {
-                const double *pa = P + (int64_t)j0 * w;
-                const bool two = j0 + 1 < it.r1;
+            trace(tbuf, iid, 4);
+            // warp per below row (two rows in flight), lanes over the panel columns;
+            // each result goes to the row's contiguous contribution slot
+            for (int j = warp * 2; j < nr; j += (kSweepBlock / 32) * 2) {
+                const double *pa = stage + j * ws;
+                const bool two = j + 1 < nr;
                 double a0 = 0.0, a1 = 0.0;
                 for (int c = lane; c < w; c += 32) {
                     const double s = seg[c];
-                    a0 += __ldg(pa + c) * s;
-                    if (two) a1 += __ldg(pa + w + c) * s;
+                    a0 += pa[c] * s;
+                    if (two) a1 += pa[ws + c] * s;
                 }
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) {
@@ -258,16 +298,17 @@ lower_sweep(tsb_ldlt_desc D, SweepArgs A) {
                     a1 += __shfl_xor_sync(0xffffffffu, a1, o);
                 }
                 if (lane == 0) {
-                    cb[j0] = a0;
-                    if (two) cb[j0 + 1] = a1;
+                    D.d_cbuf[dsts[j]] = a0;
+                    if (two) D.d_cbuf[dsts[j + 1]] = a1;
                 }
             }
+            trace(tbuf, iid, 5);
             __threadfence();
             __syncthreads();
             if (tid == 0) {
                 for (int q = 0; q < it.dep_cnt; ++q) atomicAdd(contrib + D.d_deps[it.dep_off + q], 1);
             }
-            trace(D.d_trace_lower, iid, 2);
+            trace(tbuf, iid, 2);
         }
     }
     sweep_exit(D, ctl, contrib, flag);
@@ -275,20 +316,23 @@ lower_sweep(tsb_ldlt_desc D, SweepArgs A) {
 
 // ---------------------------------------------------------------------------
 // upper sweep: L^T z = w
+// shared memory: [stage][seg 128][red 256][zv 128][zb max chunk rows]
 // ---------------------------------------------------------------------------
+template <bool TRACE>
 __global__ void __launch_bounds__(kSweepBlock)
 upper_sweep(tsb_ldlt_desc D, SweepArgs A) {
     extern __shared__ __align__(128) double smem[];
-    double *tri = smem;
-    double *seg = smem + D.tri_smem_doubles;          // w doubles
-    double *red = seg + kMaxW;                        // kSweepBlock doubles
-    double *zb = red + kSweepBlock;                   // chunk rows of z[below]
+    double *stage = smem;
+    double *seg = smem + D.stage_doubles;
+    double *red = seg + kMaxW;
+    double *zv = red + kSweepBlock;
+    double *zb = zv + kMaxW;
     __shared__ uint64_t bar;
     __shared__ int item_id;
-    __shared__ double tvec[kT];
     int32_t *ctl = D.d_ctl + 2;
     int32_t *ready = D.d_cnt2, *flag = D.d_cnt3;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    int64_t *const tbuf = TRACE ? D.d_trace_upper : nullptr;
+    const int tid = threadIdx.x;
     if (A.done != nullptr && *((volatile const int32_t *)A.done)) {
         sweep_exit(D, ctl, ready, flag);
         return;
@@ -302,102 +346,80 @@ upper_sweep(tsb_ldlt_desc D, SweepArgs A) {
         __syncthreads();
         const int iid = item_id;
         if (iid >= D.n_items_upper) break;
-        trace(D.d_trace_upper, iid, 0);
+        trace(tbuf, iid, 0);
         const Item it = items[iid];
         const int p = it.panel;
         const int pstart = D.d_p_start[p], w = D.d_p_w[p];
         if (it.type == IT_OFFT) {
-            // partial[c] = sum_{j in [r0,r1)} P[j][c] * z[below[j]]
+            // partial[c] = sum_{j in [r0,r1)} P[j][c] * z[below[j]]; the factor chunk
+            // is staged by TMA while the owners of its rows finish
+            const int ws = w + (w & 1), nr = it.r1 - it.r0;
             if (tid == 0) {
+                tma_load_1d(stage, D.d_pan + D.d_p_pan[p] + (int64_t)it.r0 * ws, (uint32_t)(nr * ws * 8), &bar);
                 for (int q = 0; q < it.dep_cnt; ++q) spin_until_geq(flag + D.d_deps[it.dep_off + q], 1);
             }
             __syncthreads();
-            trace(D.d_trace_upper, iid, 1);
-            const int32_t *below = D.d_below + D.d_p_below[p];
-            for (int j = it.r0 + tid; j < it.r1; j += kSweepBlock) zb[j - it.r0] = __ldcg(A.x + below[j]);
+            trace(tbuf, iid, 1);
+            const int32_t *below = D.d_below + D.d_p_below[p] + it.r0;
+            for (int j = tid; j < nr; j += kSweepBlock) zb[j] = __ldcg(A.x + below[j]);
+            mbar_wait(&bar, phase);
+            phase ^= 1;
             __syncthreads();
-            const double *P = D.d_pan + D.d_p_pan[p];
+            trace(tbuf, iid, 4);
             const int wp = w <= 16 ? 16 : (w <= 32 ? 32 : (w <= 64 ? 64 : 128));
             const int c = tid % wp, rg = tid / wp, ng = kSweepBlock / wp;
-            double acc = 0.0;
+            double a0 = 0.0, a1 = 0.0;
             if (c < w) {
-                int j = it.r0 + rg;
-                for (; j + ng < it.r1; j += 2 * ng)
-                    acc += __ldg(P + (int64_t)j * w + c) * zb[j - it.r0] +
-                           __ldg(P + (int64_t)(j + ng) * w + c) * zb[j + ng - it.r0];
-                if (j < it.r1) acc += __ldg(P + (int64_t)j * w + c) * zb[j - it.r0];
+                int j = rg;
+                for (; j + ng < nr; j += 2 * ng) {
+                    a0 += stage[j * ws + c] * zb[j];
+                    a1 += stage[(j + ng) * ws + c] * zb[j + ng];
+                }
+                if (j < nr) a0 += stage[j * ws + c] * zb[j];
             }
-            red[tid] = acc;
+            red[tid] = a0 + a1;
             __syncthreads();
             if (tid < w) {
                 double s = 0.0;
                 for (int g = 0; g < ng; ++g) s += red[g * wp + tid];
                 D.d_part[it.out_off + tid] = s;
             }
+            trace(tbuf, iid, 5);
             __threadfence();
             __syncthreads();
             if (tid == 0) atomicAdd(ready + p, 1);
-            trace(D.d_trace_upper, iid, 2);
+            trace(tbuf, iid, 2);
         } else {  // IT_DIAGT
-            const int ntiles = (w + kT - 1) / kT;
-            if (tid == 0) tma_load_1d(tri, D.d_tri + D.d_p_tri[p], (uint32_t)(D.d_p_tri_len[p] * 8), &bar);
-            if (tid == 0) spin_until_geq(ready + p, it.dep_cnt);
+            if (tid == 0) {
+                tma_load_1d(stage, D.d_tri_u + D.d_p_tri[p], (uint32_t)(D.d_p_tri_len[p] * 8), &bar);
+                spin_until_geq(ready + p, it.dep_cnt);
+            }
             __syncthreads();
-            trace(D.d_trace_upper, iid, 1);
+            trace(tbuf, iid, 1);
             for (int k = tid; k < w; k += kSweepBlock) {
                 double v = A.in[pstart + k];
                 if (A.dscale) v = v / A.dscale[pstart + k];
                 double s = 0.0;
+#pragma unroll 8
                 for (int q = 0; q < it.dep_cnt; ++q) s += __ldcg(D.d_part + it.out_off + q * w + k);
                 seg[k] = v - s;
             }
             mbar_wait(&bar, phase);
             phase ^= 1;
             __syncthreads();
-            const double *tinv = tri + D.d_p_tri_len[p] - ntiles * kT * kT;
-            // offsets of the tile-column panels inside tri
-            int64_t toff = 0;
-            for (int t = 0; t < ntiles; ++t) toff += (int64_t)(w - min(t * kT + kT, w)) * kT;
-            for (int t = ntiles - 1; t >= 0; --t) {
-                const int t0 = t * kT, tw = min(kT, w - t0), t1 = t0 + tw;
-                const int nrows = w - t1;
-                toff -= (int64_t)nrows * kT;
-                const double *tp = tri + toff;
-                // acc_c = sum_{r < nrows} tp[r][c] * seg[t1 + r]   (16 row groups)
-                {
-                    const int cc = tid & (kT - 1), g = tid >> 4;
-                    double a = 0.0;
-                    for (int r = g; r < nrows; r += kSweepBlock / kT) a += tp[r * kT + cc] * seg[t1 + r];
-                    red[tid] = a;
-                }
-                __syncthreads();
-                if (warp == 0) {
-                    double v = 0.0;
-                    if (lane < tw) {
-                        double a = 0.0;
-                        for (int g = 0; g < kSweepBlock / kT; ++g) a += red[g * kT + lane];
-                        v = seg[t0 + lane] - a;
-                        tvec[lane] = v;
-                    }
-                    __syncwarp();
-                    if (lane < tw) {
-                        double z = 0.0;
-                        const double *ti = tinv + t * kT * kT;
-                        for (int q = 0; q < tw; ++q) z += ti[q * kT + lane] * tvec[q];
-                        seg[t0 + lane] = z;
-                    }
-                }
-                __syncthreads();
-            }
+            trace(tbuf, iid, 4);
+            panel_upper(stage, w, seg, zv, red, tid);
+            __syncthreads();
             for (int k = tid; k < w; k += kSweepBlock) {
-                const double v = seg[k];
+                const double v = zv[k];
                 A.x[pstart + k] = v;
                 if (A.out_perm) A.out[A.out_perm[pstart + k]] = v;
             }
+            trace(tbuf, iid, 5);
             __threadfence();
             __syncthreads();
             if (tid == 0) atomicExch(flag + p, 1);
-            trace(D.d_trace_upper, iid, 2);
+            trace(tbuf, iid, 2);
         }
     }
     sweep_exit(D, ctl, ready, flag);
@@ -406,9 +428,12 @@ upper_sweep(tsb_ldlt_desc D, SweepArgs A) {
 static uint64_t g_serial = 0;
 static std::mutex g_serial_mu;
 
-static size_t lower_smem(const tsb_ldlt_desc &D) { return (D.tri_smem_doubles + kMaxW) * sizeof(double); }
+static size_t lower_smem(const tsb_ldlt_desc &D) {
+    return (D.stage_doubles + 2 * kMaxW + kSweepBlock + (kMaxW + 2)) * sizeof(double) +
+           ((D.max_chunk_rows + 1) & ~1) * sizeof(int32_t);
+}
 static size_t upper_smem(const tsb_ldlt_desc &D) {
-    return (D.tri_smem_doubles + kMaxW + kSweepBlock + D.max_chunk_rows) * sizeof(double);
+    return (D.stage_doubles + kMaxW + kSweepBlock + kMaxW + D.max_chunk_rows) * sizeof(double);
 }
 
 void ldlt_enqueue(tsb_ldlt_t h, int mode, const double *r, double *out, const int32_t *done,
@@ -419,13 +444,19 @@ void ldlt_enqueue(tsb_ldlt_t h, int mode, const double *r, double *out, const in
     const int grid = D.grid;
     if (mode == 0 || mode == 2) {
         SweepArgs a{r, mode == 2 ? D.d_perm : nullptr, nullptr, mode == 2 ? D.d_y : out, nullptr, nullptr, done};
-        lower_sweep<<<grid, kSweepBlock, lower_smem(D), st>>>(D, a);
+        if (D.d_trace_lower)
+            lower_sweep<true><<<grid, kSweepBlock, lower_smem(D), st>>>(D, a);
+        else
+            lower_sweep<false><<<grid, kSweepBlock, lower_smem(D), st>>>(D, a);
         TSB_LAUNCHED();
     }
     if (mode == 1 || mode == 2) {
         SweepArgs a{mode == 2 ? D.d_y : r, nullptr, mode == 2 ? D.d_d : nullptr, mode == 2 ? D.d_y : out,
                     mode == 2 ? D.d_perm : nullptr, mode == 2 ? out : nullptr, done};
-        upper_sweep<<<grid, kSweepBlock, upper_smem(D), st>>>(D, a);
+        if (D.d_trace_upper)
+            upper_sweep<true><<<grid, kSweepBlock, upper_smem(D), st>>>(D, a);
+        else
+            upper_sweep<false><<<grid, kSweepBlock, upper_smem(D), st>>>(D, a);
         TSB_LAUNCHED();
     }
 }
@@ -443,11 +474,13 @@ extern "C" int tsb_ldlt_create(const tsb_ldlt_desc *desc, tsb_ldlt_t *out) {
         auto *h = new tsb_ldlt;
         h->d = *desc;
         const size_t ls = lower_smem(*desc), us = upper_smem(*desc);
-        TSB_CUDA(cudaFuncSetAttribute(lower_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ls));
-        TSB_CUDA(cudaFuncSetAttribute(upper_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)us));
+        for (auto fn : {lower_sweep<false>, lower_sweep<true>})
+            TSB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ls));
+        for (auto fn : {upper_sweep<false>, upper_sweep<true>})
+            TSB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)us));
         int per_sm_l = 0, per_sm_u = 0;
-        TSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_l, lower_sweep, kSweepBlock, ls));
-        TSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_u, upper_sweep, kSweepBlock, us));
+        TSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_l, lower_sweep<true>, kSweepBlock, ls));
+        TSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_u, upper_sweep<true>, kSweepBlock, us));
         int per_sm = per_sm_l < per_sm_u ? per_sm_l : per_sm_u;
         if (per_sm < 1) {
             delete h;

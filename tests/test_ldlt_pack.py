@@ -13,18 +13,19 @@ from paper_2306_05893_b200 import _ldlt_pack as K, mesh as M, ndprecond as ND
 from paper_2306_05893_b200.assembly import CsrMatrix
 
 
-def _tri_views(H, p):
+def _panel_inverse(H, p, which):
+    """Unpack the panel's explicit diagonal-triangle inverse (unit lower) from the
+    lower sweep's column-packed copy or the upper sweep's row-packed copy."""
     w = int(H["p_w"][p])
-    blob = H["tri"][H["p_tri"][p]: H["p_tri"][p] + H["p_tri_len"][p]]
-    nt = (w + 15) // 16
-    tinv = blob[len(blob) - nt * 256:].reshape(nt, 16, 16)
-    panels, off = [], 0
-    for t in range(nt):
-        t1 = min(16 * t + 16, w)
-        rows = w - t1
-        panels.append(blob[off: off + rows * 16].reshape(rows, 16))
-        off += rows * 16
-    return panels, tinv
+    blob = H[which][H["p_tri"][p]: H["p_tri"][p] + H["p_tri_len"][p]]
+    Li = np.eye(w)
+    if which == "tri":
+        cj, ri = np.triu_indices(w, 1)
+        Li[ri, cj] = blob[: len(ri)]
+    else:
+        ri, cj = np.tril_indices(w, -1)
+        Li[ri, cj] = blob[: len(ri)]
+    return Li
 
 
 def emulate_lower(H, r):
@@ -42,22 +43,16 @@ def emulate_lower(H, r):
                 row = s + k
                 v = r[row]
                 for q in range(H["cin_ptr"][row], H["cin_ptr"][row + 1]):
-                    v -= cbuf[H["cin_idx"][q]]
+                    v -= cbuf[q]
                 seg[k] = v
-            panels, tinv = _tri_views(H, p)
-            for t in range(len(tinv)):
-                t0 = 16 * t
-                tw = min(16, w - t0)
-                seg[t0:t0 + tw] = tinv[t][:tw, :tw] @ seg[t0:t0 + tw]
-                if len(panels[t]):
-                    seg[t0 + tw:] -= panels[t] @ seg[t0:t0 + 16]
-            y[s:s + w] = seg
+            y[s:s + w] = _panel_inverse(H, p, "tri") @ seg
             flag[p] = True
         else:
             assert typ == K.IT_OFF and flag[p]
             nb = H["p_below"][p + 1] - H["p_below"][p] if p + 1 < P else len(H["below"]) - H["p_below"][p]
-            pan = H["pan"][H["p_pan"][p]: H["p_pan"][p] + nb * w].reshape(nb, w)
-            cbuf[H["p_cb"][p] + r0: H["p_cb"][p] + r1] = pan[r0:r1] @ y[s:s + w]
+            ws = w + (w & 1)  # rows padded to an even stride (16-byte TMA chunks)
+            pan = H["pan"][H["p_pan"][p]: H["p_pan"][p] + nb * ws].reshape(nb, ws)[:, :w]
+            cbuf[H["cslot"][H["p_cb"][p] + r0: H["p_cb"][p] + r1]] = pan[r0:r1] @ y[s:s + w]
             contrib[H["deps"][doff: doff + dcnt]] += 1
     return y
 
@@ -73,21 +68,15 @@ def emulate_upper(H, w_in):
         if typ == K.IT_OFFT:
             assert all(flag[H["deps"][doff: doff + dcnt]]), "OFFT dispatched before its owners"
             nb = H["p_below"][p + 1] - H["p_below"][p] if p + 1 < P else len(H["below"]) - H["p_below"][p]
-            pan = H["pan"][H["p_pan"][p]: H["p_pan"][p] + nb * w].reshape(nb, w)
+            ws = w + (w & 1)  # rows padded to an even stride (16-byte TMA chunks)
+            pan = H["pan"][H["p_pan"][p]: H["p_pan"][p] + nb * ws].reshape(nb, ws)[:, :w]
             below = H["below"][H["p_below"][p]: H["p_below"][p] + nb]
             part[ooff: ooff + w] = pan[r0:r1].T @ z[below[r0:r1]]
             ready[p] += 1
         else:
             assert typ == K.IT_DIAGT and ready[p] == dcnt
             seg = w_in[s:s + w] - sum(part[ooff + q * w: ooff + (q + 1) * w] for q in range(dcnt))
-            panels, tinv = _tri_views(H, p)
-            for t in range(len(tinv) - 1, -1, -1):
-                t0 = 16 * t
-                tw = min(16, w - t0)
-                if len(panels[t]):
-                    seg[t0:t0 + 16] -= panels[t].T @ seg[t0 + tw:]
-                seg[t0:t0 + tw] = tinv[t][:tw, :tw].T @ seg[t0:t0 + tw]
-            z[s:s + w] = seg
+            z[s:s + w] = _panel_inverse(H, p, "tri_u").T @ seg
             flag[p] = True
     return z
 

@@ -38,6 +38,9 @@ def summarize(tr, items):
             "exec_us_mean": float(((end - ready)[m]).mean() / 1e3),
             "exec_us_sum": float(((end - ready)[m]).sum() / 1e3),
             "wait_us_sum": float(((ready - take)[m]).sum() / 1e3),
+            "stage_us_mean": float(((tr[:, 4] - tr[:, 1])[m]).mean() / 1e3),
+            "compute_us_mean": float(((tr[:, 5] - tr[:, 4])[m]).mean() / 1e3),
+            "publish_us_mean": float(((tr[:, 2] - tr[:, 5])[m]).mean() / 1e3),
         }
     out["by_type"] = per
     busy = float((end - ready).sum())
@@ -78,8 +81,19 @@ def main():
         e1.synchronize()
         res.append(e0.elapsed_time(e1))
     H = dev.host
+    plain = DevicePanels(f)  # same kernels without the trace instrumentation
+    res_plain = []
+    for _ in range(args.reps):
+        flush()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        plain.run("apply", r, z)
+        e1.record()
+        e1.synchronize()
+        res_plain.append(e0.elapsed_time(e1))
     report = {
-        "workload": args.workload, "apply_ms_median": float(np.median(res)), "panels": H["P"],
+        "workload": args.workload, "apply_ms_median": float(np.median(res)),
+        "apply_ms_untraced": float(np.median(res_plain)), "panels": H["P"],
         "n": H["n"], "grid_note": "persistent grid = SMs x resident CTAs",
         "lower": summarize(dev.trace_l.cpu().numpy(), H["items_l"]),
         "upper": summarize(dev.trace_u.cpu().numpy(), H["items_u"]),
@@ -88,6 +102,9 @@ def main():
     print(txt)
     if args.out:
         Path(args.out).write_text(txt)
+        keep = {k: H[k] for k in ("items_l", "items_u", "p_w", "p_start", "deps", "p_below", "p_cb")}
+        np.savez_compressed(Path(args.out).with_suffix(".npz"), trace_l=dev.trace_l.cpu().numpy(),
+                            trace_u=dev.trace_u.cpu().numpy(), **keep)
 
 
 if __name__ == "__main__":
