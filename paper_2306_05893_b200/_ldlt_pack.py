@@ -23,7 +23,7 @@ from . import _lib
 
 PANEL_W = 128          # panel width (columns), multiple of the 16-wide tile
 TILE = 16
-CHUNK_ELEMS = 12288    # ~96 KB of factor per off-diagonal item
+CHUNK_ELEMS = 6144     # ~48 KB of factor per off-diagonal item
 CRIT_ROWS = 32         # chunk rows for the next panel of the same block (critical path)
 
 IT_DIAG, IT_OFF, IT_OFFT, IT_DIAGT = 0, 1, 2, 3

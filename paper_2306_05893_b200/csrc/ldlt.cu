@@ -153,16 +153,18 @@ __device__ __forceinline__ int row_off(int i) { return (i * (i - 1)) >> 1; }
 __device__ __forceinline__ void panel_lower(const double *Lc, int w, const double *x, double *y, double *red,
                                             int tid) {
     const int i = tid & (kMaxW - 1), h = tid / kMaxW;
-    double a0 = 0.0, a1 = 0.0;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
     if (i < w) {
         int j = h;
-        for (; j + 2 < i; j += 4) {
+        for (; j + 6 < i; j += 8) {  // four independent chains hide the LDS latency
             a0 += Lc[col_off(j, w) + i - j - 1] * x[j];
             a1 += Lc[col_off(j + 2, w) + i - j - 3] * x[j + 2];
+            a2 += Lc[col_off(j + 4, w) + i - j - 5] * x[j + 4];
+            a3 += Lc[col_off(j + 6, w) + i - j - 7] * x[j + 6];
         }
-        if (j < i) a0 += Lc[col_off(j, w) + i - j - 1] * x[j];
+        for (; j < i; j += 2) a0 += Lc[col_off(j, w) + i - j - 1] * x[j];
     }
-    red[tid] = a0 + a1;
+    red[tid] = (a0 + a1) + (a2 + a3);
     __syncthreads();
     if (tid < w) y[tid] = x[tid] + (red[tid] + red[tid + kMaxW]);
 }
@@ -171,17 +173,19 @@ __device__ __forceinline__ void panel_lower(const double *Lc, int w, const doubl
 __device__ __forceinline__ void panel_upper(const double *Lr, int w, const double *v, double *z, double *red,
                                             int tid) {
     const int j = tid & (kMaxW - 1), h = tid / kMaxW;
-    double a0 = 0.0, a1 = 0.0;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
     if (j < w) {
         int i = j + 1;
         if ((i & 1) != h) ++i;
-        for (; i + 2 < w; i += 4) {
+        for (; i + 6 < w; i += 8) {
             a0 += Lr[row_off(i) + j] * v[i];
             a1 += Lr[row_off(i + 2) + j] * v[i + 2];
+            a2 += Lr[row_off(i + 4) + j] * v[i + 4];
+            a3 += Lr[row_off(i + 6) + j] * v[i + 6];
         }
-        if (i < w) a0 += Lr[row_off(i) + j] * v[i];
+        for (; i < w; i += 2) a0 += Lr[row_off(i) + j] * v[i];
     }
-    red[tid] = a0 + a1;
+    red[tid] = (a0 + a1) + (a2 + a3);
     __syncthreads();
     if (tid < w) z[tid] = v[tid] + (red[tid] + red[tid + kMaxW]);
 }
@@ -224,33 +228,35 @@ lower_sweep(tsb_ldlt_desc D, SweepArgs A) {
         const int p = it.panel;
         const int pstart = D.d_p_start[p], w = D.d_p_w[p];
         if (it.type == IT_DIAG) {
-            if (tid == 0) {
-                tma_load_1d(stage, D.d_tri + D.d_p_tri[p], (uint32_t)(D.d_p_tri_len[p] * 8), &bar);
-                spin_until_geq(contrib + p, it.dep_cnt);
+            // everything that does not depend on the contributions is fetched
+            // before the wait: the panel inverse (TMA), row pointers, the input
+            const int k = tid >> 1, h = tid & 1;
+            double xin = 0.0;
+            int64_t q0 = 0, q1 = 0;
+            if (tid == 0) tma_load_1d(stage, D.d_tri + D.d_p_tri[p], (uint32_t)(D.d_p_tri_len[p] * 8), &bar);
+            if (k < w) {
+                const int row = pstart + k;
+                q0 = __ldg(D.d_cin_ptr + row) + h;
+                q1 = __ldg(D.d_cin_ptr + row + 1);
+                if (h == 0) xin = A.in[A.in_perm ? A.in_perm[row] : row];
             }
-            if (tid <= w) rptr[tid] = __ldg(D.d_cin_ptr + pstart + tid);
+            if (tid == 0) spin_until_geq(contrib + p, it.dep_cnt);
             __syncthreads();
             trace(tbuf, iid, 1);
-            // rows: input - contributions; 8 lanes per row, lane-strided partial
-            // sums + xor tree = a fixed summation order (deterministic)
+            // rows: input - contributions.  Two threads per row (w <= 128), each
+            // summing every other contribution with its loads in flight, then one
+            // xor step: a fixed summation order (deterministic)
             {
-                const int l8 = lane & 7;
-                for (int kb = warp * 4; kb < w; kb += kSweepBlock / 8) {
-                    const int k = kb + (lane >> 3);
-                    double acc = 0.0;
-                    if (k < w) {
-                        const int64_t q1 = rptr[k + 1];
-#pragma unroll 4
-                        for (int64_t q = rptr[k] + l8; q < q1; q += 8) acc += __ldcg(D.d_cbuf + q);
-                    }
-                    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-                    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-                    acc += __shfl_xor_sync(0xffffffffu, acc, 4);
-                    if (k < w && l8 == 0) {
-                        const int row = pstart + k;
-                        seg[k] = A.in[A.in_perm ? A.in_perm[row] : row] - acc;
-                    }
+                double acc0 = 0.0, acc1 = 0.0;
+                int64_t q = q0;
+                for (; q + 2 < q1; q += 4) {
+                    acc0 += __ldcg(D.d_cbuf + q);
+                    acc1 += __ldcg(D.d_cbuf + q + 2);
                 }
+                if (q < q1) acc0 += __ldcg(D.d_cbuf + q);
+                double acc = acc0 + acc1;
+                acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+                if (k < w && h == 0) seg[k] = xin - acc;
             }
             mbar_wait(&bar, phase);
             phase ^= 1;
@@ -281,25 +287,31 @@ lower_sweep(tsb_ldlt_desc D, SweepArgs A) {
             phase ^= 1;
             __syncthreads();
             trace(tbuf, iid, 4);
-            // warp per below row (two rows in flight), lanes over the panel columns;
-            // each result goes to the row's contiguous contribution slot
-            for (int j = warp * 2; j < nr; j += (kSweepBlock / 32) * 2) {
-                const double *pa = stage + j * ws;
-                const bool two = j + 1 < nr;
-                double a0 = 0.0, a1 = 0.0;
-                for (int c = lane; c < w; c += 32) {
-                    const double s = seg[c];
-                    a0 += pa[c] * s;
-                    if (two) a1 += pa[ws + c] * s;
-                }
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-                    a0 += __shfl_xor_sync(0xffffffffu, a0, o);
-                    a1 += __shfl_xor_sync(0xffffffffu, a1, o);
-                }
-                if (lane == 0) {
-                    D.d_cbuf[dsts[j]] = a0;
-                    if (two) D.d_cbuf[dsts[j + 1]] = a1;
+            // G lanes per below row (G = 32/16/8 for wide/medium/narrow panels),
+            // two rows in flight per group, lanes over the panel columns; each
+            // result goes to the row's contiguous contribution slot
+            {
+                const int G = w > 64 ? 32 : (w > 32 ? 16 : 8);
+                const int gl = lane & (G - 1), gpw = 32 / G;
+                // warp-uniform trip count: the xor shuffles need every lane
+                for (int jb = warp * gpw * 2; jb < nr; jb += (kSweepBlock / 32) * gpw * 2) {
+                    const int j = jb + (lane / G) * 2;
+                    const bool one = j < nr, two = j + 1 < nr;
+                    const double *pa = stage + j * ws;
+                    double a0 = 0.0, a1 = 0.0;
+                    for (int c = gl; c < w; c += G) {
+                        const double s = seg[c];
+                        if (one) a0 += pa[c] * s;
+                        if (two) a1 += pa[ws + c] * s;
+                    }
+                    for (int o = G >> 1; o > 0; o >>= 1) {
+                        a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+                        a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+                    }
+                    if (gl == 0 && one) {
+                        D.d_cbuf[dsts[j]] = a0;
+                        if (two) D.d_cbuf[dsts[j + 1]] = a1;
+                    }
                 }
             }
             trace(tbuf, iid, 5);
@@ -390,19 +402,30 @@ upper_sweep(tsb_ldlt_desc D, SweepArgs A) {
             if (tid == 0) atomicAdd(ready + p, 1);
             trace(tbuf, iid, 2);
         } else {  // IT_DIAGT
-            if (tid == 0) {
-                tma_load_1d(stage, D.d_tri_u + D.d_p_tri[p], (uint32_t)(D.d_p_tri_len[p] * 8), &bar);
-                spin_until_geq(ready + p, it.dep_cnt);
+            const int k = tid >> 1, h = tid & 1;
+            double vin = 0.0;
+            if (tid == 0) tma_load_1d(stage, D.d_tri_u + D.d_p_tri[p], (uint32_t)(D.d_p_tri_len[p] * 8), &bar);
+            if (k < w && h == 0) {  // input (and D scaling) does not depend on the wait
+                vin = A.in[pstart + k];
+                if (A.dscale) vin = vin / A.dscale[pstart + k];
             }
+            if (tid == 0) spin_until_geq(ready + p, it.dep_cnt);
             __syncthreads();
             trace(tbuf, iid, 1);
-            for (int k = tid; k < w; k += kSweepBlock) {
-                double v = A.in[pstart + k];
-                if (A.dscale) v = v / A.dscale[pstart + k];
-                double s = 0.0;
-#pragma unroll 8
-                for (int q = 0; q < it.dep_cnt; ++q) s += __ldcg(D.d_part + it.out_off + q * w + k);
-                seg[k] = v - s;
+            {
+                // two threads per row sum the chunk partials of one parity (fixed order)
+                double s0 = 0.0, s1 = 0.0;
+                if (k < w) {
+                    int q = h;
+                    for (; q + 2 < it.dep_cnt; q += 4) {
+                        s0 += __ldcg(D.d_part + it.out_off + q * w + k);
+                        s1 += __ldcg(D.d_part + it.out_off + (q + 2) * w + k);
+                    }
+                    if (q < it.dep_cnt) s0 += __ldcg(D.d_part + it.out_off + q * w + k);
+                }
+                double s = s0 + s1;
+                s += __shfl_xor_sync(0xffffffffu, s, 1);
+                if (k < w && h == 0) seg[k] = vin - s;
             }
             mbar_wait(&bar, phase);
             phase ^= 1;
