@@ -253,6 +253,9 @@ int tsb_pcg_solve(tsb_pcg_t h, int64_t nrows, const int32_t *d_row_ptr,
                   const double *d_inv_diag, double tol, int64_t max_iterations,
                   tsb_report *report, void *stream);
 int tsb_pcg_report(tsb_pcg_t h, tsb_report *report, void *stream);
+/* Diagnostics of the last solve: CTA 0's device time (ns) in SpMV, barrier +
+ * alpha, vector update, barrier + beta, preconditioner, whole loop. */
+int tsb_pcg_phase_times(tsb_pcg_t h, int64_t *out6, void *stream);
 
 /* ------------------------------------------------------------------------
  * Host setup (not on the per-iteration path): nested-dissection ordering

@@ -98,6 +98,7 @@ _SIGNATURES = {
     "tsb_pcg_solve": (C.c_int, [c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, c_vp,
                                 c_vp, C.c_double, c_i64, C.POINTER(Report), c_vp]),
     "tsb_pcg_report": (C.c_int, [c_vp, C.POINTER(Report), c_vp]),
+    "tsb_pcg_phase_times": (C.c_int, [c_vp, c_vp, c_vp]),
     "tsb_nested_dissection": (C.c_int, [c_i64, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp,
                                         c_vp, c_vp, c_vp]),
 }

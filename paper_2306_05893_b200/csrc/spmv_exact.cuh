@@ -43,8 +43,41 @@ __device__ __forceinline__ double row_sum_exact(int lo, int len, const int32_t *
     if (len <= 0) return 0.0;
     auto term = [&](int64_t k) -> double { return mul(__ldg(val + k), xa(__ldg(col + k))); };
     const int n = len - 1;  // terms handled by the pairwise sum
+    double p0 = 0.0;        // first product seeds the row (issued with the other loads)
+    if (lane8 == 0) p0 = term(lo);
     double res;
-    if (n > 128) {
+    if (n <= 64) {
+        // common case (FEM rows <= 45 entries): every lane fetches its <= 8 terms
+        // up front -- all index, value and gather loads in flight together --
+        // then the same summation order as below, in registers
+        double t[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int idx = 8 * u + lane8;
+            t[u] = idx < n ? term(lo + 1 + idx) : 0.0;
+        }
+        if (n >= 8) {
+            const int nfull = (n - (n % 8)) / 8;  // complete groups of 8 terms
+            double r = t[0];
+#pragma unroll
+            for (int u = 1; u < 8; ++u)
+                if (u < nfull) r = add(r, t[u]);
+            r = add(r, __shfl_xor_sync(gmask, r, 1, 8));
+            r = add(r, __shfl_xor_sync(gmask, r, 2, 8));
+            r = add(r, __shfl_xor_sync(gmask, r, 4, 8));
+            const int tail = n % 8;
+            double tv = 0.0;
+#pragma unroll
+            for (int u = 1; u < 8; ++u)
+                if (u == nfull) tv = t[u];
+            for (int k = 0; k < tail; ++k) r = add(r, __shfl_sync(gmask, tv, k, 8));
+            res = r;
+        } else {
+            double r = -0.0;
+            for (int k = 0; k < n; ++k) r = add(r, __shfl_sync(gmask, t[0], k, 8));
+            res = r;
+        }
+    } else if (n > 128) {
         double r = 0.0;
         if (lane8 == 0) r = pairwise_serial(term, (int64_t)lo + 1, (int64_t)n);
         res = __shfl_sync(gmask, r, 0, 8);
@@ -68,8 +101,6 @@ __device__ __forceinline__ double row_sum_exact(int lo, int len, const int32_t *
         for (int k = 0; k < n; ++k) r = add(r, __shfl_sync(gmask, t, k, 8));
         res = r;
     }
-    double p0 = 0.0;
-    if (lane8 == 0) p0 = term(lo);
     p0 = __shfl_sync(gmask, p0, 0, 8);
     return add(p0, res);
 }

@@ -80,7 +80,39 @@ __global__ void k_ldg(const double *src, int64_t stride_doubles, uint32_t bytes,
     if (acc == 12345.678) sink[0] = acc;
 }
 
+__device__ __forceinline__ void gsync(unsigned *bar) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned *gen = bar + 1;
+        const unsigned g = *gen;
+        __threadfence();
+        if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+            atomicExch(bar, 0u);
+            __threadfence();
+            atomicAdd(bar + 1, 1u);
+        } else {
+            while (*gen == g) __nanosleep(32);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+__global__ void k_barrier(unsigned *bar, int iters, long long *ns) {
+    uint64_t t0, t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (int i = 0; i < iters; ++i) gsync(bar);
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    if (threadIdx.x == 0 && blockIdx.x == 0) ns[0] = (long long)(t1 - t0);
+}
+
 }  // namespace ub
+
+extern "C" int ub_barrier(unsigned *bar, int iters, int grid, long long *ns) {
+    void *args[] = {&bar, &iters, &ns};
+    cudaLaunchCooperativeKernel((const void *)ub::k_barrier, dim3(grid), dim3(256), args, 0, 0);
+    return (int)cudaDeviceSynchronize();
+}
 
 extern "C" int ub_forward(const double *blob, int64_t tri_len, int w, int iters, long long *cycles, double *out) {
     size_t smem = (tri_len + 256 + 512) * sizeof(double);

@@ -66,6 +66,10 @@ def main():
             t = ns[:grid].cpu().numpy().max() / 1e9
             res[f"ldg_{kb}KB_grid{grid}"] = {"GBps_total": byts * iters * grid / t / 1e9,
                                              "us_per_copy": t / iters * 1e6}
+    bar = torch.zeros(64, dtype=torch.int32, device="cuda")
+    for grid in (148, 296, 592):
+        lib.ub_barrier(vp(bar.data_ptr()), 1000, grid, vp(ns.data_ptr()))
+        res[f"grid_barrier_us_grid{grid}"] = float(ns[0].item()) / 1000 / 1e3
     print(json.dumps(res, indent=1))
     (ROOT / "gpurun_out").mkdir(exist_ok=True)
     (ROOT / "gpurun_out" / "ubench.json").write_text(json.dumps(res, indent=1))
