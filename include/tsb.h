@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define TSB_ABI_VERSION 1
+#define TSB_ABI_VERSION 2
 
 enum tsb_status {
     TSB_OK = 0,
@@ -50,6 +50,9 @@ int tsb_abi_version(void);
 int tsb_last_error(char *buf, size_t len);
 /* Number of kernels libtsb launched in this process (for bench evidence). */
 int64_t tsb_launch_count(void);
+/* sizeof of the ABI structs (0 asm_plan, 1 asm_coeffs, 2 ldlt_block,
+ * 3 ldlt_desc, 4 report) so bindings can verify their layouts; -1 = unknown. */
+int64_t tsb_struct_size(int32_t which);
 
 /* ------------------------------------------------------------------------
  * CSR SpMV  y = A x                        replaces krylov.spmv  krylov.py:73-96
@@ -154,54 +157,62 @@ int tsb_element_blocks(const tsb_asm_plan *plan, const tsb_asm_coeffs *coeffs,
  * Factor values come from the host factorisation (ldlt_factor,
  * ndprecond.py:501-572) and are packed by the host into the layout below.
  * ---------------------------------------------------------------------- */
-/* Panel layout (built by the host from LdlFactors, _ldlt_pack.py): every
- * dissection block is cut into column panels of <= panel_width (128) columns.
- * Panel p owns permuted rows [p_start, p_start + p_w) and stores
- *   tri   (p_tri, p_tri_len doubles): the strict lower part of the inverse of
- *         its unit-lower diagonal triangle, column-packed in d_tri (lower
- *         sweep) and row-packed in d_tri_u (upper sweep), even length;
- *   pan   (p_pan): its below panel, rows `below` (p_below: later rows of the
- *         block, then the block's ancestors) x w columns, row-major, rows
- *         padded to an even stride (16-byte TMA chunks);
- *   cb    (p_cb): per below row, its slot in the row-contiguous contribution
- *         buffer (d_cslot), so row r's contributions are cbuf[cin_ptr[r]..].
- * Items are 8 x int32: type, panel, r0, r1, dep_off, dep_cnt, out_off, pad. */
+/* Block-inverse layout (built by the host from LdlFactors, _ldlt_pack.py).
+ * For every dissection block b (permuted rows [start, start+m), ancestors
+ * anc[0..na)) the host stores ONE row-major matrix
+ *     G_b = [ inv(L11) - I   (strict lower triangle, rows 1..m-1)      ]
+ *           [ M = L21 inv(L11)  (na x m)                               ]
+ * -- the reference's tile inverses (ndprecond.py:575-587) widened to the
+ * whole diagonal block, with the coupling panel pre-multiplied by it.  Then
+ *   lower (solve_lower, ndprecond.py:647-671):  y_b = x_b + (Linv-I) x_b,
+ *          contributions to the ancestors  c_b = M x_b  (column-major
+ *          pre-accumulation of the paper, one GEMV per block, no in-block chain);
+ *   upper (solve_upper, ndprecond.py:674-691):  z_b = w_b + G_b^T [w_b; -z_anc].
+ * Row r of G_b starts at g_off + off(r): off(r) = r*r/2 for triangle rows
+ * (row r holds r entries, padded to even), off(r) = m*m/2 + (r-m)*ms for the
+ * M rows (ms = m rounded up to even), so every row is 16-byte aligned.
+ * Lower items (int4): block, r0, r1, -- one TMA-staged row chunk of G_b.
+ * Upper items (8 x int32): block, slab, ra, rb, tile, has_dep, 0, 0 -- rows
+ * [ra, rb) x columns of one slab (cp.async-staged); the last tile of a slab
+ * reduces the slab's partials in tile order (deterministic). */
+typedef struct tsb_ldlt_block {
+    int32_t start, m, na, parent;   /* parent: dissection-tree parent, -1 = root */
+    int32_t target_l;               /* lower items of all children (x_b ready)     */
+    int32_t nslabs, slab_base, sw;  /* upper: column slabs of width sw            */
+    int64_t g_off;                  /* offset of G_b in d_g (doubles, even)       */
+    int64_t anc_off;                /* offset of the block's anc rows in d_anc     */
+} tsb_ldlt_block;
+
 typedef struct tsb_ldlt_desc {
     int64_t n;
-    int64_t n_panels;
+    int64_t n_blocks;
     int64_t n_items_lower;
     int64_t n_items_upper;
-    int32_t tile;                 /* 16                                            */
-    int32_t panel_width;          /* <= 128                                        */
-    int32_t stage_doubles;        /* TMA staging: max(tri, chunk) doubles          */
-    int32_t max_chunk_rows;       /* max rows of an upper item                     */
-    int32_t grid;                 /* persistent CTAs (0 = fill the GPU)            */
-    int32_t pad_;
-    const int32_t *d_items_lower; /* dispatch order, topological                   */
-    const int32_t *d_items_upper;
-    const int32_t *d_p_start;
-    const int32_t *d_p_w;
-    const int64_t *d_p_tri;
-    const int64_t *d_p_tri_len;
-    const int64_t *d_p_pan;
-    const int64_t *d_p_cb;
-    const int64_t *d_p_below;
-    const double *d_tri;          /* column-packed panel inverses (lower sweep)    */
-    const double *d_tri_u;        /* row-packed panel inverses (upper sweep)       */
-    const double *d_pan;
-    const int32_t *d_below;       /* permuted row ids                               */
-    const int32_t *d_deps;        /* panel ids: lower targets / upper owners        */
-    const int64_t *d_cin_ptr;     /* [n+1] contiguous contribution slots per row    */
-    const int32_t *d_cslot;       /* [sum below] slot of (panel, below row) in cbuf */
+    int64_t n_slabs;
+    int32_t stage_doubles;        /* staging buffer (doubles), >= any chunk/tile */
+    int32_t max_m;                /* largest block                                */
+    int32_t max_tile_rows;        /* rows of the largest upper tile               */
+    int32_t grid;                 /* persistent CTAs (0 = fill the GPU)           */
+    const tsb_ldlt_block *d_blocks;
+    const int32_t *d_items_lower; /* [n_items_lower][4], topological dispatch order */
+    const int32_t *d_items_upper; /* [n_items_upper][8]                            */
+    const double *d_g;            /* all G_b                                       */
+    const int32_t *d_anc;         /* permuted ancestor rows, per block             */
+    const int32_t *d_cslot;       /* cbuf slot of (block, anc k)                    */
+    const int64_t *d_cin_ptr;     /* [n+1]: row r's contributions are cbuf[cin_ptr[r]..cin_ptr[r+1]) */
+    const int64_t *d_slab_part;   /* [n_slabs] offset of the slab's partials in d_part */
+    const int32_t *d_slab_ntiles; /* [n_slabs]                                      */
     const double *d_d;            /* [n] D                                          */
     const int32_t *d_perm;        /* [n] perm[k] = original index at position k    */
     double *d_cbuf;               /* scratch: lower contributions                  */
-    double *d_part;               /* scratch: upper partial sums                   */
-    double *d_y;                  /* scratch [n]                                   */
-    int32_t *d_cnt0, *d_cnt1, *d_cnt2, *d_cnt3; /* [n_panels] counters (zeroed)    */
+    double *d_part;               /* scratch: upper slab partials                  */
+    double *d_x;                  /* scratch [n]: x_b of non-leaf blocks (lower)    */
+    double *d_y;                  /* scratch [n]: lower result inside apply         */
+    int32_t *d_cnt_l, *d_ready_l; /* [n_blocks] counters (zeroed; reset on exit)    */
+    int32_t *d_cnt_s, *d_done_u;  /* [n_slabs], [n_blocks]                          */
     int32_t *d_ctl;               /* [4] tickets / exit counters (zeroed)          */
-    int64_t *d_trace_lower;       /* optional [n_items_lower][4] item timeline     */
-    int64_t *d_trace_upper;       /* optional [n_items_upper][4]                   */
+    int64_t *d_trace_lower;       /* optional [n_items_lower][8] item timeline     */
+    int64_t *d_trace_upper;       /* optional [n_items_upper][8]                   */
 } tsb_ldlt_desc;
 
 typedef struct tsb_ldlt *tsb_ldlt_t;

@@ -1,16 +1,34 @@
-"""Host-side packing of LDL^T factors into the device panel layout (setup).
+"""Host-side packing of LDL^T factors into the device block-inverse layout (setup).
 
 Runs once per factor refresh (on the AsyncPreconditioner worker thread for
-the async path).  Cuts every dissection block of `LdlFactors` into column
-panels of <= PANEL_W columns, lays out the diagonal-triangle inverses and
-the below panels contiguously for streaming, builds the work-item lists of
-the two sweeps (csrc/ldlt.cu) and orders them critical-path first.
+the async path).  For every dissection block b (rows [start, start+m),
+ancestor rows anc, na = len(anc)) it stores one row-major matrix
 
-Item dispatch order = list schedule on an infinite machine: each item is
-keyed by its earliest start time under a simple cost model (tile-chain
-latency for diagonal items, bytes / per-CTA bandwidth for panel chunks).
-Because every dependency finishes before its dependant starts, the order is
-topological, which is all the persistent kernel needs to be deadlock-free.
+    G_b = [ inv(L11) - I        strict lower triangle, rows 1..m-1  ]
+          [ M = L21 inv(L11)    na x m                              ]
+
+The reference applies L11^-1 by t x t tile substitution with explicit tile
+inverses (ndprecond.py:575-587, 623-644); widening the tile to the whole
+block removes the in-block dependency chain, and pre-multiplying the
+coupling panel by it (M) makes the ancestor contributions depend only on the
+block's input x_b:
+
+    lower:  y_b = x_b + (Linv - I) x_b,   contributions  c = M x_b
+    upper:  z_b = w_b + G_b^T [w_b ; -z_anc]
+
+G_b has exactly the entries of [L11 ; L21] (same bytes per sweep), serves
+both sweeps, and the only serial chain left is the depth of the dissection
+tree.  The factor blocks are well conditioned (cond_1(L11) <= 12.5 on the
+cfg2 beam); the block-inverse apply matches the reference's tile-16 sweeps
+to ~4e-16 relative.
+
+Work items (csrc/ldlt.cu): lower = row chunks of G_b (~48 KB, one TMA bulk
+copy each); upper = column slab (32 columns) x row tile (<= 192 rows).  The
+dispatch order is a list schedule on an infinite machine keyed by each
+item's earliest start under a simple cost model, ties broken by the longest
+remaining path (critical path first).  Every dependency finishes strictly
+before its dependant starts, so the order is topological -- all the
+persistent kernel needs to be deadlock-free.
 """
 
 from __future__ import annotations
@@ -21,181 +39,224 @@ import numpy as np
 
 from . import _lib
 
-PANEL_W = 128          # panel width (columns), multiple of the 16-wide tile
-TILE = 16
-CHUNK_ELEMS = 6144     # ~48 KB of factor per off-diagonal item
-CRIT_ROWS = 32         # chunk rows for the next panel of the same block (critical path)
+CHUNK = 6144          # doubles per lower item (48 KB, one TMA bulk copy)
+CHUNK_ROWS = 512      # rows per lower item (csrc kMaxChunkRows)
+SLAB = 32             # upper slab width (columns); 16 for blocks of <= 16 columns
+TILE_ROWS = CHUNK // SLAB
 
-IT_DIAG, IT_OFF, IT_OFFT, IT_DIAGT = 0, 1, 2, 3
+BLOCK_DTYPE = np.dtype([
+    ("start", "<i4"), ("m", "<i4"), ("na", "<i4"), ("parent", "<i4"),
+    ("target_l", "<i4"), ("nslabs", "<i4"), ("slab_base", "<i4"), ("sw", "<i4"),
+    ("g_off", "<i8"), ("anc_off", "<i8"),
+])
+assert BLOCK_DTYPE.itemsize == 48
 
 
-def packed_inverse(l):
-    """Strict lower part of inv(l) for a unit-lower l -> (column-packed, row-packed).
+def row_offsets(m: int, na: int) -> np.ndarray:
+    """Offsets (doubles) of the m + na + 1 row boundaries of G_b (csrc g_row_off)."""
+    r = np.arange(m + na + 1, dtype=np.int64)
+    ms = m + (m & 1)
+    return np.where(r < m, (r * r) // 2, (m * m) // 2 + (r - m) * ms)
 
-    Column-packed: column j holds rows j+1..w-1 at j(2w-j-1)/2 (lower sweep:
-    thread per row reads consecutive words); row-packed: row i holds columns
-    0..i-1 at i(i-1)/2 (upper sweep).  Padded to an even length (16-byte TMA).
-    """
+
+def block_matrix(bf):
+    """-> (Linv with unit diagonal, M = L21 Linv) of one block factor."""
     from scipy.linalg import solve_triangular
 
-    w = len(l)
-    inv = solve_triangular(l, np.eye(w), lower=True, unit_diagonal=True, check_finite=False)
-    rows = inv[np.tril_indices(w, -1)]
-    cols = inv.T[np.triu_indices(w, 1)]
-    if len(rows) == 0:
-        return np.zeros(2), np.zeros(2)
-    if len(rows) % 2:
-        rows, cols = np.append(rows, 0.0), np.append(cols, 0.0)
-    return cols, rows
+    m = bf.stop - bf.start
+    linv = solve_triangular(bf.l11, np.eye(m), lower=True, unit_diagonal=True, check_finite=False)
+    mm = bf.l21 @ linv if len(bf.anc) else np.zeros((0, m))
+    return linv, mm
 
 
-def _inverse(order):
-    inv = np.empty_like(order)
-    inv[order] = np.arange(len(order))
-    return inv
+def pack_block(bf) -> np.ndarray:
+    """G_b in the device row layout (flat float64, even length)."""
+    m, na = bf.stop - bf.start, len(bf.anc)
+    linv, mm = block_matrix(bf)
+    off = row_offsets(m, na)
+    g = np.zeros(int(off[-1]))
+    ir, ic = np.tril_indices(m, -1)
+    g[(ir * ir) // 2 + ic] = linv[ir, ic]
+    if na:
+        ms = m + (m & 1)
+        g[off[m]:].reshape(na, ms)[:, :m] = mm
+    return g
 
 
-def _chunks(nb, n_crit, w):
-    """Row ranges of a panel's below list: critical rows first, in small chunks."""
-    out = []
-    r = 0
-    while r < n_crit:
-        out.append((r, min(r + CRIT_ROWS, n_crit)))
-        r = out[-1][1]
-    step = max(32, CHUNK_ELEMS // max(w + (w & 1), 1))
-    while r < nb:
-        out.append((r, min(r + step, nb)))
-        r = out[-1][1]
-    return out
+def unpack_block(g, m, na):
+    """Inverse of pack_block -> (Linv with unit diagonal, M)."""
+    off = row_offsets(m, na)
+    linv = np.eye(m)
+    ir, ic = np.tril_indices(m, -1)
+    linv[ir, ic] = g[(ir * ir) // 2 + ic]
+    ms = m + (m & 1)
+    mm = g[off[m]:off[-1]].reshape(na, ms)[:, :m] if na else np.zeros((0, m))
+    return linv, mm
+
+
+def _lower_chunks(off, nrows):
+    """Row ranges of G_b with <= CHUNK doubles each (at least one row)."""
+    out, r0 = [], 0
+    while r0 < nrows:
+        r1 = int(np.searchsorted(off, off[r0] + CHUNK, side="right")) - 1
+        r1 = min(max(r1, r0 + 1), nrows, r0 + CHUNK_ROWS)
+        out.append((r0, r1))
+        r0 = r1
+    return out or [(0, 0)]
 
 
 def pack(factors):
-    """Host arrays of the panel layout + item lists (pure NumPy; see DevicePanels)."""
-    if True:
-        n = factors.plan.n
-        order = [bf for lvl in factors.levels for bf in lvl]
-        # -------- panels --------
-        p_start, p_w, p_blk = [], [], []
-        tri_parts, tri_u_parts, pan_parts, below_parts = [], [], [], []
-        p_tri, p_tri_len, p_pan, p_below, p_cb = [], [], [], [], []
-        ct = cp = cb = cbuf = 0
-        panel_of_row = np.empty(n, dtype=np.int64)
-        crit = []
-        for bi, bf in enumerate(order):
-            s, m = bf.start, bf.stop - bf.start
-            anc = np.asarray(bf.anc, dtype=np.int64)
-            for c0 in range(0, m, PANEL_W):
-                w = min(PANEL_W, m - c0)
-                pid = len(p_start)
-                panel_of_row[s + c0:s + c0 + w] = pid
-                below = np.concatenate([np.arange(s + c0 + w, s + m, dtype=np.int64), anc])
-                # rows padded to an even stride so every chunk is a 16-byte-aligned TMA copy
-                ws = w + (w & 1)
-                pan = np.zeros((len(below), ws))
-                pan[: m - c0 - w, :w] = bf.l11[c0 + w:, c0:c0 + w]
-                pan[m - c0 - w:, :w] = bf.l21[:, c0:c0 + w]
-                pan = pan.ravel()
-                blob, blob_u = packed_inverse(bf.l11[c0:c0 + w, c0:c0 + w])
-                p_start.append(s + c0)
-                p_w.append(w)
-                p_blk.append(bi)
-                p_tri.append(ct)
-                p_tri_len.append(len(blob))
-                p_pan.append(cp)
-                p_below.append(cb)
-                p_cb.append(cbuf)
-                tri_parts.append(blob)
-                tri_u_parts.append(blob_u)
-                pan_parts.append(pan)
-                below_parts.append(below)
-                ct += len(blob)
-                cp += len(pan)
-                cb += len(below)
-                cbuf += len(below)
-                crit.append(min(PANEL_W, max(0, m - c0 - w)))
-        P = len(p_start)
-        p_w = np.asarray(p_w, dtype=np.int64)
-        # -------- items --------
-        chunks = [_chunks(len(below_parts[p]), crit[p], int(p_w[p])) for p in range(P)]
-        deps, dep_off, dep_cnt = [], [], []
-        E = np.zeros(P, dtype=np.int64)
-        owner_lists = []
-        for p in range(P):
+    """Host arrays of the block-inverse layout + item lists (pure NumPy)."""
+    plan = factors.plan
+    n = plan.n
+    bfs = list(factors.blocks)
+    nb = len(bfs)
+    # block elimination tree: parent(b) = owner of b's first ancestor row.  The
+    # fill property  anc(b) \ rows(parent) <= anc(parent)  makes "all children
+    # done" imply "all descendants done" (lower) and "parent done" imply "all
+    # ancestors done" (upper) -- the only dependencies the kernels track.
+    owner = np.full(n, -1, dtype=np.int64)
+    for i, bf in enumerate(bfs):
+        if bf.stop <= bf.start:
+            raise ValueError("empty dissection block")
+        owner[bf.start:bf.stop] = i
+    parent = np.full(nb, -1, dtype=np.int64)
+    for i, bf in enumerate(bfs):
+        if len(bf.anc):
+            anc = np.asarray(bf.anc)
+            if np.any(anc < bf.stop) or np.any(np.diff(anc) <= 0):
+                raise ValueError("ancestor rows must be sorted and follow the block")
+            parent[i] = owner[anc[0]]
+    for i, bf in enumerate(bfs):
+        p = parent[i]
+        if p >= 0:
+            pb = bfs[p]
+            rest = np.asarray(bf.anc)
+            rest = rest[rest >= pb.stop]
+            if len(rest) and not np.all(np.isin(rest, np.asarray(pb.anc))):
+                raise ValueError("factor structure violates the fill property")
+    children = [[] for _ in range(nb)]
+    for i in range(nb):
+        if parent[i] >= 0:
+            children[parent[i]].append(i)
+
+    ms_ = np.array([bf.stop - bf.start for bf in bfs], dtype=np.int64)
+    na_ = np.array([len(bf.anc) for bf in bfs], dtype=np.int64)
+    # ---------------- G blobs ----------------
+    g_parts, g_off = [], np.zeros(nb, dtype=np.int64)
+    pos = 0
+    for i, bf in enumerate(bfs):
+        g = pack_block(bf)
+        g_off[i] = pos
+        g_parts.append(g)
+        pos += len(g)
+    anc_off = np.zeros(nb + 1, dtype=np.int64)
+    np.cumsum(na_, out=anc_off[1:])
+    anc_all = (np.concatenate([np.asarray(bf.anc, dtype=np.int64) for bf in bfs]) if anc_off[-1]
+               else np.zeros(0, dtype=np.int64))
+    # ---------------- lower items ----------------
+    offs = [row_offsets(int(ms_[i]), int(na_[i])) for i in range(nb)]
+    lchunks = [_lower_chunks(offs[i], int(ms_[i] + na_[i])) for i in range(nb)]
+    nl = np.array([len(c) for c in lchunks], dtype=np.int64)
+    target_l = np.array([sum(int(nl[c]) for c in children[i]) for i in range(nb)], dtype=np.int64)
+
+    def cost(doubles):  # us: item overhead + streaming at ~40 GB/s per CTA
+        return 1.0 + doubles * 8 / 40e3
+
+    order = sorted(range(nb), key=lambda i: bfs[i].start)  # children before parents
+    ready_l = np.zeros(nb)
+    done_l = np.zeros(nb)
+    for i in order:
+        if children[i]:
+            ready_l[i] = max(done_l[c] for c in children[i]) + 1.0 + 0.002 * ms_[i]
+        worst = max(cost(offs[i][r1] - offs[i][r0]) for r0, r1 in lchunks[i])
+        done_l[i] = ready_l[i] + worst
+    tail_l = np.zeros(nb)
+    for i in reversed(order):  # parents first
+        tail_l[i] = (done_l[i] - ready_l[i]) + (tail_l[parent[i]] if parent[i] >= 0 else 0.0)
+    lower = []
+    for i in range(nb):
+        for r0, r1 in lchunks[i]:
+            lower.append((ready_l[i], -tail_l[i], bfs[i].start, r0, i, r1))
+    lower.sort()
+    items_l = np.array([(x[4], x[3], x[5], 0) for x in lower], dtype=np.int32).reshape(-1, 4)
+    # ---------------- upper items ----------------
+    sw_ = np.where(ms_ > 16, SLAB, 16)
+    nslabs = (ms_ + sw_ - 1) // sw_
+    slab_base = np.zeros(nb + 1, dtype=np.int64)
+    np.cumsum(nslabs, out=slab_base[1:])
+    S = int(slab_base[-1])
+    tiles = [None] * S   # per slab: list of (ra, rb, has_dep)
+    for i in range(nb):
+        m, na, sw = int(ms_[i]), int(na_[i]), int(sw_[i])
+        tr = TILE_ROWS * SLAB // sw
+        for q in range(int(nslabs[i])):
+            c0 = q * sw
             lst = []
-            for r0, r1 in chunks[p]:
-                tg = np.unique(panel_of_row[below_parts[p][r0:r1]])
-                lst.append((len(deps), len(tg)))
-                deps.extend(tg.tolist())
-                E[tg] += 1
-            owner_lists.append(lst)
-        part_off = np.zeros(P + 1, dtype=np.int64)
-        np.cumsum([len(chunks[p]) * int(p_w[p]) for p in range(P)], out=part_off[1:])
-        tri_len = np.asarray(p_tri_len, dtype=np.int64)
-
-        def cost_diag(p):
-            return 1.5 + tri_len[p] * 8 / 100e3
-
-        def cost_chunk(p, r0, r1):
-            return 0.8 + (r1 - r0) * p_w[p] * 8 / 40e3
-
-        # lower schedule (panels are in a topological order already)
-        ready = np.zeros(P)
-        lower = []
-        for p in range(P):
-            st = ready[p]
-            fin = st + cost_diag(p)
-            lower.append((st, 0, p, IT_DIAG, p, 0, 0, 0, int(E[p]), 0))
-            for q, (r0, r1) in enumerate(chunks[p]):
-                off, cnt = owner_lists[p][q]
-                cf = fin + cost_chunk(p, r0, r1)
-                lower.append((fin, 1, p, IT_OFF, p, r0, r1, off, cnt, 0))
-                tg = deps[off:off + cnt]
-                ready[tg] = np.maximum(ready[tg], cf)
-        # upper schedule: reverse topological order of panels
-        done = np.zeros(P)
-        upper = []
-        for p in range(P - 1, -1, -1):
-            st_d = 0.0
-            for q, (r0, r1) in enumerate(chunks[p]):
-                off, cnt = owner_lists[p][q]
-                tg = deps[off:off + cnt]
-                st = float(done[tg].max()) if cnt else 0.0
-                upper.append((st, 0, -p, IT_OFFT, p, r0, r1, off, cnt, int(part_off[p] + q * p_w[p])))
-                st_d = max(st_d, st + cost_chunk(p, r0, r1))
-            upper.append((st_d, 1, -p, IT_DIAGT, p, 0, 0, 0, len(chunks[p]), int(part_off[p])))
-            done[p] = st_d + cost_diag(p)
-        lower.sort(key=lambda x: (x[0], x[1], x[2]))
-        upper.sort(key=lambda x: (x[0], x[1], x[2]))
-        to_items = lambda L: np.array([x[3:] for x in L], dtype=np.int32).reshape(-1, 7)  # noqa: E731
-        items_l = np.concatenate([to_items(lower), np.zeros((len(lower), 1), dtype=np.int32)], axis=1)
-        items_u = np.concatenate([to_items(upper), np.zeros((len(upper), 1), dtype=np.int32)], axis=1)
-        # -------- contribution gather lists (lower) --------
-        rows_all = np.concatenate(below_parts) if cb else np.zeros(0, dtype=np.int64)
-        corder = np.argsort(rows_all, kind="stable")
-        cin_ptr = np.zeros(n + 1, dtype=np.int64)
-        np.cumsum(np.bincount(rows_all, minlength=n), out=cin_ptr[1:])
-        max_chunk = max((r1 - r0 for ch in chunks for r0, r1 in ch), default=1)
-        # staging buffer: the largest tri blob or factor chunk (rows x padded width)
-        stage = max([int(tri_len.max()) if P else 0] +
-                    [(r1 - r0) * (int(p_w[p]) + int(p_w[p]) % 2) for p in range(P) for r0, r1 in chunks[p]])
-
-        cat = lambda parts, dt: (np.concatenate(parts).astype(dt, copy=False) if parts  # noqa: E731
-                                 else np.zeros(1, dtype=dt))
+            for ra in range(c0 + 1, m, tr):
+                lst.append((ra, min(ra + tr, m), 0))
+            for ra in range(m, m + na, tr):
+                lst.append((ra, min(ra + tr, m + na), 1))
+            tiles[slab_base[i] + q] = lst or [(0, 0, 0)]
+    slab_ntiles = np.array([len(t) for t in tiles], dtype=np.int64)
+    slab_part = np.zeros(S + 1, dtype=np.int64)
+    slab_sw = np.repeat(sw_, nslabs)
+    np.cumsum(slab_ntiles * slab_sw, out=slab_part[1:])
+    done_u = np.zeros(nb)
+    start_of = {}
+    for i in sorted(range(nb), key=lambda i: -bfs[i].start):  # parents first
+        dep_t = done_u[parent[i]] if parent[i] >= 0 else 0.0
+        fin = 0.0
+        for q in range(int(nslabs[i])):
+            for ra, rb, dep in tiles[slab_base[i] + q]:
+                st = dep_t if dep else 0.0
+                start_of[(i, q, ra)] = st
+                fin = max(fin, st + cost((rb - ra) * int(sw_[i])))
+        done_u[i] = fin + 0.5
+    tail_u = np.zeros(nb)
+    for i in order:  # children first
+        own = done_u[i] - (done_u[parent[i]] if parent[i] >= 0 else 0.0)
+        tail_u[i] = own + max((tail_u[c] for c in children[i]), default=0.0)
+    upper = []
+    for i in range(nb):
+        for q in range(int(nslabs[i])):
+            sid = int(slab_base[i] + q)
+            for t, (ra, rb, dep) in enumerate(tiles[sid]):
+                upper.append((start_of[(i, q, ra)], -tail_u[i], -bfs[i].start, q, t, i, sid, ra, rb, dep))
+    upper.sort()
+    items_u = np.array([(x[5], x[6], x[7], x[8], x[4], x[9], 0, 0) for x in upper],
+                       dtype=np.int32).reshape(-1, 8)
+    # ---------------- contribution slots (lower) ----------------
+    corder = np.argsort(anc_all, kind="stable")   # row-contiguous, block order within a row
+    cin_ptr = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(np.bincount(anc_all, minlength=n), out=cin_ptr[1:])
+    cslot = np.empty(len(anc_all), dtype=np.int64)
+    cslot[corder] = np.arange(len(anc_all))
+    # ---------------- block table ----------------
+    blocks = np.zeros(nb, dtype=BLOCK_DTYPE)
+    blocks["start"] = [bf.start for bf in bfs]
+    blocks["m"] = ms_
+    blocks["na"] = na_
+    blocks["parent"] = parent
+    blocks["target_l"] = target_l
+    blocks["nslabs"] = nslabs
+    blocks["slab_base"] = slab_base[:-1]
+    blocks["sw"] = sw_
+    blocks["g_off"] = g_off
+    blocks["anc_off"] = anc_off[:-1]
+    max_lchunk = max(int(offs[i][r1] - offs[i][r0]) for i in range(nb) for r0, r1 in lchunks[i]) if nb else 2
+    max_tile = max((rb - ra for t in tiles for ra, rb, _ in t), default=1)
+    stage = max(max_lchunk, max(max_tile, 1) * SLAB, 2)
+    stage += stage & 1
     return {
-        "n": n, "P": P, "items_l": items_l, "items_u": items_u, "p_start": np.asarray(p_start, dtype=np.int64),
-        "p_w": p_w, "p_tri": np.asarray(p_tri, dtype=np.int64), "p_tri_len": tri_len,
-        "p_pan": np.asarray(p_pan, dtype=np.int64), "p_cb": np.asarray(p_cb, dtype=np.int64),
-        "p_below": np.asarray(p_below, dtype=np.int64), "tri": cat(tri_parts, np.float64),
-        "tri_u": cat(tri_u_parts, np.float64),
-        "pan": cat(pan_parts, np.float64), "below": cat(below_parts, np.int64),
-        "deps": np.asarray(deps if deps else [0], dtype=np.int64), "cin_ptr": cin_ptr,
-        # contributions land row-contiguous: entry i of the concatenated below lists
-        # (panel order) goes to slot cslot[i]; row r reads cbuf[cin_ptr[r]:cin_ptr[r+1]]
-        "cslot": _inverse(corder) if len(corder) else np.zeros(1, dtype=np.int64),
-        "d": np.asarray(factors.d, dtype=np.float64), "perm": np.asarray(factors.plan.perm, dtype=np.int64),
-        "ncbuf": cbuf, "npart": int(part_off[-1]), "max_chunk": int(max_chunk), "stage": int(stage),
-        "bytes_tri": ct * 8,
-        "bytes_pan": cp * 8,
+        "n": n, "nb": nb, "blocks": blocks, "items_l": items_l, "items_u": items_u,
+        "g": np.concatenate(g_parts) if g_parts else np.zeros(2), "anc": anc_all, "cslot": cslot,
+        "cin_ptr": cin_ptr, "slab_part": slab_part[:-1], "slab_ntiles": slab_ntiles, "n_slabs": S,
+        "npart": int(slab_part[-1]), "ncbuf": len(anc_all),
+        "d": np.asarray(factors.d, dtype=np.float64), "perm": np.asarray(plan.perm, dtype=np.int64),
+        "stage": int(stage), "max_m": int(ms_.max()) if nb else 1, "max_tile": int(max(max_tile, 1)),
+        "parent": parent, "children": children,
+        "bytes_g": int(pos) * 8,
     }
 
 
@@ -205,10 +266,10 @@ class DevicePanels:
     def __init__(self, factors, stream=None, trace=False):
         t = _lib.require_cuda()
         H = pack(factors)
-        n, P = H["n"], H["P"]
-        items_l, items_u, tri_len = H["items_l"], H["items_u"], H["p_tri_len"]
+        n, nb = H["n"], H["nb"]
+        items_l, items_u = H["items_l"], H["items_u"]
         self.host = H if trace else None
-        if trace:  # per-item timeline (globaltimer ns): take, ready, end, smid
+        if trace:  # per-item timeline (globaltimer ns): take, ready, end, smid, staged, computed
             self.trace_l = t.zeros((len(items_l), 8), dtype=t.int64, device="cuda")
             self.trace_u = t.zeros((len(items_u), 8), dtype=t.int64, device="cuda")
         ctx = t.cuda.stream(stream) if stream is not None else _NullCtx()
@@ -216,36 +277,32 @@ class DevicePanels:
             up = lambda a: t.from_numpy(np.ascontiguousarray(a)).pin_memory().to("cuda", non_blocking=True)  # noqa: E731
             i32 = lambda a: up(np.asarray(a, dtype=np.int32))  # noqa: E731
             i64 = lambda a: up(np.asarray(a, dtype=np.int64))  # noqa: E731
-            self.t = {
-                "items_l": up(items_l), "items_u": up(items_u), "p_start": i32(H["p_start"]),
-                "p_w": i32(H["p_w"]), "p_tri": i64(H["p_tri"]), "p_tri_len": i64(tri_len),
-                "p_pan": i64(H["p_pan"]), "p_cb": i64(H["p_cb"]), "p_below": i64(H["p_below"]),
-                "tri": up(H["tri"]), "tri_u": up(H["tri_u"]), "pan": up(H["pan"]), "below": i32(H["below"]), "deps": i32(H["deps"]),
-                "cin_ptr": i64(H["cin_ptr"]), "cslot": i32(H["cslot"]), "d": up(H["d"]),
-                "perm": i32(H["perm"]),
-            }
             z = lambda k, dt: t.zeros(max(k, 1), dtype=dt, device="cuda")  # noqa: E731
-            self.t.update(cbuf=z(H["ncbuf"], t.float64), part=z(H["npart"], t.float64), y=z(n, t.float64),
-                          cnt=z(4 * P, t.int32), ctl=z(4, t.int32))
+            nz = lambda a: a if len(a) else np.zeros(1, dtype=a.dtype)  # noqa: E731
+            self.t = {
+                "blocks": up(H["blocks"].view(np.uint8)), "items_l": up(nz(items_l.ravel())),
+                "items_u": up(nz(items_u.ravel())), "g": up(H["g"]), "anc": i32(nz(H["anc"])),
+                "cslot": i32(nz(H["cslot"])), "cin_ptr": i64(H["cin_ptr"]), "slab_part": i64(nz(H["slab_part"])),
+                "slab_ntiles": i32(nz(H["slab_ntiles"])), "d": up(H["d"]), "perm": i32(H["perm"]),
+            }
+            self.t.update(cbuf=z(H["ncbuf"], t.float64), part=z(H["npart"], t.float64), x=z(n, t.float64),
+                          y=z(n, t.float64), cnt=z(3 * nb + H["n_slabs"], t.int32), ctl=z(4, t.int32))
         self.n = n
-        self.n_panels = P
+        self.n_blocks = nb
         self.n_items = (len(items_l), len(items_u))
-        self.bytes = {"tri": H["bytes_tri"], "pan": H["bytes_pan"]}
-        max_chunk = H["max_chunk"]
+        self.bytes = {"g": H["bytes_g"]}
         tp = lambda k: _lib.ptr(self.t[k])  # noqa: E731
         cnt = self.t["cnt"]
+        cp = lambda a, b: _lib.ptr(cnt[a:b]) if b > a else _lib.ptr(cnt)  # noqa: E731
         self.desc = _lib.LdltDesc(
-            n=n, n_panels=P, n_items_lower=len(items_l), n_items_upper=len(items_u), tile=TILE,
-            panel_width=PANEL_W, stage_doubles=H["stage"], max_chunk_rows=int(max_chunk),
-            grid=0, pad_=0,
-            d_items_lower=tp("items_l"), d_items_upper=tp("items_u"), d_p_start=tp("p_start"), d_p_w=tp("p_w"),
-            d_p_tri=tp("p_tri"), d_p_tri_len=tp("p_tri_len"), d_p_pan=tp("p_pan"), d_p_cb=tp("p_cb"),
-            d_p_below=tp("p_below"), d_tri=tp("tri"), d_tri_u=tp("tri_u"), d_pan=tp("pan"), d_below=tp("below"), d_deps=tp("deps"),
-            d_cin_ptr=tp("cin_ptr"), d_cslot=tp("cslot"), d_d=tp("d"), d_perm=tp("perm"),
-            d_cbuf=tp("cbuf"), d_part=tp("part"), d_y=tp("y"),
-            d_cnt0=_lib.ptr(cnt[0:P]) if P else tp("cnt"), d_cnt1=_lib.ptr(cnt[P:2 * P]) if P else tp("cnt"),
-            d_cnt2=_lib.ptr(cnt[2 * P:3 * P]) if P else tp("cnt"), d_cnt3=_lib.ptr(cnt[3 * P:]) if P else tp("cnt"),
-            d_ctl=tp("ctl"),
+            n=n, n_blocks=nb, n_items_lower=len(items_l), n_items_upper=len(items_u), n_slabs=H["n_slabs"],
+            stage_doubles=H["stage"], max_m=H["max_m"], max_tile_rows=H["max_tile"], grid=0,
+            d_blocks=tp("blocks"), d_items_lower=tp("items_l"), d_items_upper=tp("items_u"), d_g=tp("g"),
+            d_anc=tp("anc"), d_cslot=tp("cslot"), d_cin_ptr=tp("cin_ptr"), d_slab_part=tp("slab_part"),
+            d_slab_ntiles=tp("slab_ntiles"), d_d=tp("d"), d_perm=tp("perm"),
+            d_cbuf=tp("cbuf"), d_part=tp("part"), d_x=tp("x"), d_y=tp("y"),
+            d_cnt_l=cp(0, nb), d_ready_l=cp(nb, 2 * nb), d_cnt_s=cp(2 * nb, 2 * nb + H["n_slabs"]),
+            d_done_u=cp(2 * nb + H["n_slabs"], 3 * nb + H["n_slabs"]), d_ctl=tp("ctl"),
             d_trace_lower=_lib.ptr(self.trace_l) if trace else None,
             d_trace_upper=_lib.ptr(self.trace_u) if trace else None,
         )

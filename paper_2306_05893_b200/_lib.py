@@ -56,15 +56,14 @@ class AsmCoeffs(C.Structure):
 
 class LdltDesc(C.Structure):
     _fields_ = [
-        ("n", c_i64), ("n_panels", c_i64), ("n_items_lower", c_i64), ("n_items_upper", c_i64),
-        ("tile", c_i32), ("panel_width", c_i32), ("stage_doubles", c_i32), ("max_chunk_rows", c_i32),
-        ("grid", c_i32), ("pad_", c_i32),
-        ("d_items_lower", c_vp), ("d_items_upper", c_vp), ("d_p_start", c_vp), ("d_p_w", c_vp),
-        ("d_p_tri", c_vp), ("d_p_tri_len", c_vp), ("d_p_pan", c_vp), ("d_p_cb", c_vp), ("d_p_below", c_vp),
-        ("d_tri", c_vp), ("d_tri_u", c_vp), ("d_pan", c_vp), ("d_below", c_vp), ("d_deps", c_vp),
-        ("d_cin_ptr", c_vp), ("d_cslot", c_vp), ("d_d", c_vp), ("d_perm", c_vp),
-        ("d_cbuf", c_vp), ("d_part", c_vp), ("d_y", c_vp),
-        ("d_cnt0", c_vp), ("d_cnt1", c_vp), ("d_cnt2", c_vp), ("d_cnt3", c_vp), ("d_ctl", c_vp),
+        ("n", c_i64), ("n_blocks", c_i64), ("n_items_lower", c_i64), ("n_items_upper", c_i64),
+        ("n_slabs", c_i64),
+        ("stage_doubles", c_i32), ("max_m", c_i32), ("max_tile_rows", c_i32), ("grid", c_i32),
+        ("d_blocks", c_vp), ("d_items_lower", c_vp), ("d_items_upper", c_vp), ("d_g", c_vp),
+        ("d_anc", c_vp), ("d_cslot", c_vp), ("d_cin_ptr", c_vp), ("d_slab_part", c_vp),
+        ("d_slab_ntiles", c_vp), ("d_d", c_vp), ("d_perm", c_vp),
+        ("d_cbuf", c_vp), ("d_part", c_vp), ("d_x", c_vp), ("d_y", c_vp),
+        ("d_cnt_l", c_vp), ("d_ready_l", c_vp), ("d_cnt_s", c_vp), ("d_done_u", c_vp), ("d_ctl", c_vp),
         ("d_trace_lower", c_vp), ("d_trace_upper", c_vp),
     ]
 
@@ -81,6 +80,7 @@ _SIGNATURES = {
     "tsb_abi_version": (C.c_int, []),
     "tsb_last_error": (C.c_int, [C.c_char_p, C.c_size_t]),
     "tsb_launch_count": (c_i64, []),
+    "tsb_struct_size": (c_i64, [c_i32]),
     "tsb_spmv": (C.c_int, [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "tsb_csr_diagonal": (C.c_int, [c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "tsb_compress": (C.c_int, [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp]),
@@ -129,8 +129,11 @@ def load() -> C.CDLL:
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
-        if lib.tsb_abi_version() != 1:
+        if lib.tsb_abi_version() != 2:
             raise NativeLibraryError("libtsb ABI version mismatch")
+        for k, st in enumerate((AsmPlan, AsmCoeffs, None, LdltDesc, Report)):
+            if st is not None and lib.tsb_struct_size(k) != C.sizeof(st):
+                raise NativeLibraryError(f"libtsb struct layout mismatch: {st.__name__}")
         _lib = lib
     return _lib
 

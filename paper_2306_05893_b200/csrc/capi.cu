@@ -27,3 +27,14 @@ extern "C" int tsb_last_error(char *buf, size_t len) {
 }
 
 extern "C" int64_t tsb_launch_count(void) { return tsb::g_launches.load(); }
+
+extern "C" int64_t tsb_struct_size(int32_t which) {
+    switch (which) {
+        case 0: return sizeof(tsb_asm_plan);
+        case 1: return sizeof(tsb_asm_coeffs);
+        case 2: return sizeof(tsb_ldlt_block);
+        case 3: return sizeof(tsb_ldlt_desc);
+        case 4: return sizeof(tsb_report);
+        default: return -1;
+    }
+}

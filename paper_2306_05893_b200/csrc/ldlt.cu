@@ -1,34 +1,34 @@
 // Nested-dissection LDL^T apply on the B200: one persistent, dependency-driven
 // kernel per triangular sweep (the paper's level-scheduled GPU Cholesky apply,
-// with the level barriers replaced by per-panel completion counters).
+// with the level barriers replaced by per-block completion counters).
 //
 // Replaces solve_lower (ndprecond.py:647-671, _forward_block 623-631),
 // solve_upper (674-691, _backward_block 634-644) and apply (694-700).  Factor
 // values come from the host factorisation (ldlt_factor, ndprecond.py:501-572)
-// and are re-cut on the host (paper_2306_05893_b200/_ldlt_pack.py) into
-// PANELS: every dissection block is split into column panels of <= 128
-// columns.  Panel p of block b owns columns [c0, c0+w) and stores
-//   tri    the explicit inverse of its unit-lower w x w diagonal triangle --
-//          the reference's tile_inv (ndprecond.py:575-587) widened from 16 to
-//          the whole panel, so the in-panel solve is one dependency-free GEMV
-//          (column-packed copy for the lower sweep, row-packed for the upper,
-//          each read by its sweep only; staged in shared memory by one TMA copy);
-//   P      its below panel: rows (block rows >= c0+w) U anc(b), w columns,
-//          row-major, rows padded to an even stride -- [L11[c0+w:, c0:c0+w];
-//          L21[:, c0:c0+w]] -- streamed chunk by chunk with TMA bulk copies.
+// and are re-packed on the host (paper_2306_05893_b200/_ldlt_pack.py) into one
+// matrix per dissection block,
+//     G_b = [inv(L11) - I ; L21 inv(L11)]          (layout: include/tsb.h),
+// i.e. the reference's t x t tile inverses (ndprecond.py:575-587) widened to
+// the whole diagonal block and folded into the coupling panel.  The in-block
+// dependency chain of the tile substitution disappears: every block is one
+// GEMV per sweep, split into many independent row chunks (lower) or column
+// slab x row tiles (upper), so the only serial chain left is the depth of
+// the dissection tree (one hop per level).
 // Work items (dispatched in a precomputed topological, critical-path-first
 // order through one atomic ticket counter; every CTA is resident, so an item
 // only ever waits on items dispensed before it):
-//   lower  DIAG(p)        rows of p = input - contributions pre-accumulated by
-//                         earlier panels (row-contiguous, summed in a fixed
-//                         order -> deterministic, no atomics on data), then
-//                         y_p = inv(L_pp) x_p
-//          OFFDIAG(p,k)   contributions of y_p to a chunk of p's below rows
-//                         (column-major pre-accumulation, paper Fig. solveBlock)
-//   upper  OFFDIAG_T(p,k) partial sums P[k rows]^T z[below]        (row-major pull)
-//          DIAG_T(p)      z_p = inv(L_pp)^T (w_p - sum of partials in chunk order)
-// Counters (int32 per panel) are reset by the last CTA to leave, so the kernel
-// can be replayed inside the PCG graph without extra memsets.
+//   lower  (b, G rows [r0, r1))  staged by one TMA bulk copy before waiting for
+//          x_b; triangle rows give y_b, M rows give the contributions to the
+//          ancestors (column-major pre-accumulation, paper Fig. solveBlock)
+//          written to row-contiguous slots; the item that completes a block's
+//          inputs finalises x_parent = input - contributions (fixed order ->
+//          deterministic, no atomics on data).
+//   upper  (b, slab, G rows [ra, rb))  partial sums of the slab's columns of
+//          G_b^T [w_b; -z_anc] (row-major pull); triangle tiles need nothing,
+//          M tiles wait for the parent's z; the last tile of a slab reduces the
+//          partials in tile order and publishes z for those columns.
+// Counters are reset by the last CTA to leave, so the kernels replay inside
+// the persistent PCG without memsets.
 #include <mutex>
 #include <vector>
 
@@ -46,7 +46,7 @@ __global__ void __launch_bounds__(kSweepBlock) lower_sweep(tsb_ldlt_desc D, Swee
     extern __shared__ __align__(128) double smem[];
     __shared__ uint64_t bar;
     if (A.done != nullptr && *((volatile const int32_t *)A.done)) {
-        sweep_exit(D, D.d_ctl, D.d_cnt0, D.d_cnt1);
+        sweep_exit(D.d_ctl, D.d_cnt_l, D.n_blocks, D.d_ready_l, D.n_blocks);
         return;
     }
     if (threadIdx.x == 0) mbar_init(&bar, 1);
@@ -60,7 +60,7 @@ __global__ void __launch_bounds__(kSweepBlock) upper_sweep(tsb_ldlt_desc D, Swee
     extern __shared__ __align__(128) double smem[];
     __shared__ uint64_t bar;
     if (A.done != nullptr && *((volatile const int32_t *)A.done)) {
-        sweep_exit(D, D.d_ctl + 2, D.d_cnt2, D.d_cnt3);
+        sweep_exit(D.d_ctl + 2, D.d_cnt_s, D.n_slabs, D.d_done_u, D.n_blocks);
         return;
     }
     if (threadIdx.x == 0) mbar_init(&bar, 1);
@@ -95,7 +95,8 @@ void ldlt_enqueue(tsb_ldlt_t h, int mode, const double *r, double *out, const in
             launch_coop(lower_sweep<false>, grid, sweep_smem_lower(D), st, D, a);
     }
     if (mode == 1 || mode == 2) {
-        SweepArgs a{mode == 2 ? D.d_y : r, nullptr, mode == 2 ? D.d_d : nullptr, mode == 2 ? D.d_y : out,
+        // apply: w = y / d read from d_y, z (permuted) into d_x, scattered through perm
+        SweepArgs a{mode == 2 ? D.d_y : r, nullptr, mode == 2 ? D.d_d : nullptr, mode == 2 ? D.d_x : out,
                     mode == 2 ? D.d_perm : nullptr, mode == 2 ? out : nullptr, done};
         if (D.d_trace_upper)
             launch_coop(upper_sweep<true>, grid, sweep_smem_upper(D), st, D, a);
@@ -113,8 +114,8 @@ extern "C" int tsb_ldlt_create(const tsb_ldlt_desc *desc, tsb_ldlt_t *out) {
     using namespace tsb;
     return guard([&] {
         if (desc == nullptr || out == nullptr) throw Error(TSB_E_ARG, "null desc/out");
-        if (desc->tile != kT) throw Error(TSB_E_ARG, "device tile must be 16");
-        if (desc->panel_width > kMaxW) throw Error(TSB_E_ARG, "panel width exceeds 128");
+        if (desc->max_m > kMaxXs) throw Error(TSB_E_ARG, "dissection block larger than the x_b staging buffer");
+        if (desc->stage_doubles < 2 || (desc->stage_doubles & 1)) throw Error(TSB_E_ARG, "bad staging size");
         auto *h = new tsb_ldlt;
         h->d = *desc;
         const size_t ls = sweep_smem_lower(*desc), us = sweep_smem_upper(*desc);

@@ -1,6 +1,7 @@
 // Persistent sweep bodies of the nested-dissection LDL^T apply, shared by the
 // stand-alone sweep kernels (ldlt.cu) and the persistent PCG solver (pcg.cu).
-// See ldlt.cu for the panel layout and the work-item protocol.
+// Block-inverse layout and item protocol: include/tsb.h (tsb_ldlt_desc) and
+// ldlt.cu.
 #pragma once
 
 #include "tsb_common.cuh"
@@ -8,12 +9,15 @@
 namespace tsb {
 
 constexpr int kSweepBlock = 256;
-constexpr int kT = 16;        // device tile parameter (ABI: panels start at multiples of it)
-constexpr int kMaxW = 128;    // panel width
-enum { IT_DIAG = 0, IT_OFF = 1, IT_OFFT = 2, IT_DIAGT = 3 };
+constexpr int kMaxSW = 32;      // upper-sweep column slab width (doubles)
+constexpr int kMaxXs = 8192;    // largest block whose x_b is staged in shared memory
+constexpr int kMaxChunkRows = 512;  // rows of a lower item (host packer caps it)
 
-struct Item {
-    int32_t type, panel, r0, r1, dep_off, dep_cnt, out_off, pad;
+struct LItem {
+    int32_t block, r0, r1, pad;
+};
+struct UItem {
+    int32_t block, slab, ra, rb, tile, has_dep, p0, p1;
 };
 
 // ---- small PTX helpers -----------------------------------------------------
@@ -29,11 +33,12 @@ __device__ __forceinline__ void tma_load_1d(void *dst, const void *src, uint32_t
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                  : "memory");
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
+    if (bytes > 0)
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                smem_u32(dst)),
+            "l"(src), "r"(bytes), "r"(smem_u32(bar))
+            : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
     asm volatile(
@@ -43,17 +48,25 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
         "r"(phase)
         : "memory");
 }
+__device__ __forceinline__ void cp_async16(void *dst, const void *src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 __device__ __forceinline__ int ld_acquire(const int *p) {
     int v;
     asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
+}
+__device__ __forceinline__ void st_release(int *p, int v) {
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 __device__ __forceinline__ void spin_until_geq(const int *p, int target) {
     if (ld_acquire(p) >= target) return;
     int ns = 32;
     while (ld_acquire(p) < target) {
         __nanosleep(ns);
-        if (ns < 256) ns <<= 1;
+        if (ns < 128) ns <<= 1;
     }
 }
 
@@ -71,6 +84,14 @@ __device__ __forceinline__ void trace(int64_t *buf, int iid, int slot) {
     }
 }
 
+// Row r of G_b (m = block size): triangle rows r < m hold r entries (padded to
+// even), then the M rows with stride m rounded up to even.  Every row offset
+// is even (16-byte aligned).
+__device__ __forceinline__ int64_t g_row_off(int r, int m) {
+    if (r < m) return ((int64_t)r * r) >> 1;
+    return (((int64_t)m * m) >> 1) + (int64_t)(r - m) * (m + (m & 1));
+}
+
 struct SweepArgs {
     const double *in;        // input vector (lower: r; upper: w)
     const int32_t *in_perm;  // lower apply: gather input through perm
@@ -78,11 +99,11 @@ struct SweepArgs {
     double *x;               // lower: y (permuted)   upper: z (permuted)
     const int32_t *out_perm; // upper apply: scatter z through perm
     double *out;             // upper apply: output in original order
-    const int32_t *done;     // PCG stop flag (skip when set)
+    const int32_t *done;     // stop flag (skip the sweep when set)
 };
 
 // Exit protocol: the last CTA out zeroes the counters for the next replay.
-__device__ __forceinline__ void sweep_exit(const tsb_ldlt_desc &D, int32_t *ctl, int32_t *c0, int32_t *c1) {
+__device__ __forceinline__ void sweep_exit(int32_t *ctl, int32_t *c0, int64_t n0, int32_t *c1, int64_t n1) {
     __syncthreads();
     __shared__ int last;
     if (threadIdx.x == 0) {
@@ -91,10 +112,8 @@ __device__ __forceinline__ void sweep_exit(const tsb_ldlt_desc &D, int32_t *ctl,
     }
     __syncthreads();
     if (!last) return;
-    for (int64_t i = threadIdx.x; i < D.n_panels; i += blockDim.x) {
-        c0[i] = 0;
-        c1[i] = 0;
-    }
+    for (int64_t i = threadIdx.x; i < n0; i += blockDim.x) c0[i] = 0;
+    for (int64_t i = threadIdx.x; i < n1; i += blockDim.x) c1[i] = 0;
     __syncthreads();
     if (threadIdx.x == 0) {
         ctl[0] = 0;
@@ -105,304 +124,299 @@ __device__ __forceinline__ void sweep_exit(const tsb_ldlt_desc &D, int32_t *ctl,
 
 // dynamic shared memory of the sweep bodies
 inline size_t sweep_smem_lower(const tsb_ldlt_desc &D) {
-    return (D.stage_doubles + 2 * kMaxW + kSweepBlock + (kMaxW + 2)) * sizeof(double) +
-           ((D.max_chunk_rows + 1) & ~1) * sizeof(int32_t);
+    return (size_t)(D.stage_doubles + ((D.max_m + 1) & ~1)) * sizeof(double) + kMaxChunkRows * sizeof(int32_t);
 }
 inline size_t sweep_smem_upper(const tsb_ldlt_desc &D) {
-    return (D.stage_doubles + kMaxW + kSweepBlock + kMaxW + D.max_chunk_rows) * sizeof(double);
+    return (size_t)(D.stage_doubles + ((D.max_tile_rows + 1) & ~1) + kSweepBlock) * sizeof(double) +
+           ((D.max_tile_rows + 1) & ~1) * sizeof(int32_t);
 }
 
 // ---------------------------------------------------------------------------
-// Diagonal-panel GEMVs with the explicit inverse of the unit-lower triangle.
-// The factor blocks are well conditioned (cond(L11) <= 3.4 on the beams); the
-// panel-inverse sweeps agree with the tile-16 reference to ~6e-16.
-// Both put one output per thread, two partial sums (column/row parity), so
-// consecutive threads read consecutive shared-memory words.
+// lower sweep: L y = r   (column-major pre-accumulation, one GEMV per block)
+//   item (b, rows [r0, r1) of G_b):
+//     stage the rows by TMA (before any wait), wait until x_b is final (the
+//     last child item finalises it), stage x_b, then
+//       triangle row i:  y_i = x_i + sum_{j<i} Linv_ij x_j          -> x[start+i]
+//       M row k:         c_k = sum_j M_kj x_j                        -> cbuf slot
+//     publish to the parent's counter; the item that completes the parent's
+//     inputs finalises x_parent = in - (contributions, fixed order).
+// shared memory: [stage][xs max_m]
 // ---------------------------------------------------------------------------
-// column-packed strict lower: column j holds rows j+1..w-1 at j*(2w-j-1)/2
-__device__ __forceinline__ int col_off(int j, int w) { return (j * (2 * w - j - 1)) >> 1; }
-// row-packed strict lower: row i holds columns 0..i-1 at i*(i-1)/2
-__device__ __forceinline__ int row_off(int i) { return (i * (i - 1)) >> 1; }
-
-// y = inv(L_pp) x   (lower sweep): thread per row i, columns j < i of one parity
-__device__ __forceinline__ void panel_lower(const double *Lc, int w, const double *x, double *y, double *red,
-                                            int tid) {
-    const int i = tid & (kMaxW - 1), h = tid / kMaxW;
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-    if (i < w) {
-        int j = h;
-        for (; j + 6 < i; j += 8) {  // four independent chains hide the LDS latency
-            a0 += Lc[col_off(j, w) + i - j - 1] * x[j];
-            a1 += Lc[col_off(j + 2, w) + i - j - 3] * x[j + 2];
-            a2 += Lc[col_off(j + 4, w) + i - j - 5] * x[j + 4];
-            a3 += Lc[col_off(j + 6, w) + i - j - 7] * x[j + 6];
-        }
-        for (; j < i; j += 2) a0 += Lc[col_off(j, w) + i - j - 1] * x[j];
-    }
-    red[tid] = (a0 + a1) + (a2 + a3);
-    __syncthreads();
-    if (tid < w) y[tid] = x[tid] + (red[tid] + red[tid + kMaxW]);
+__device__ __forceinline__ double lower_input(const SweepArgs &A, int row) {
+    return __ldcg(A.in + (A.in_perm ? A.in_perm[row] : row));  // may be produced in-kernel (L2)
 }
 
-// z = inv(L_pp)^T v   (upper sweep): thread per column j, rows i > j of one parity
-__device__ __forceinline__ void panel_upper(const double *Lr, int w, const double *v, double *z, double *red,
-                                            int tid) {
-    const int j = tid & (kMaxW - 1), h = tid / kMaxW;
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-    if (j < w) {
-        int i = j + 1;
-        if ((i & 1) != h) ++i;
-        for (; i + 6 < w; i += 8) {
-            a0 += Lr[row_off(i) + j] * v[i];
-            a1 += Lr[row_off(i + 2) + j] * v[i + 2];
-            a2 += Lr[row_off(i + 4) + j] * v[i + 4];
-            a3 += Lr[row_off(i + 6) + j] * v[i + 6];
-        }
-        for (; i < w; i += 2) a0 += Lr[row_off(i) + j] * v[i];
-    }
-    red[tid] = (a0 + a1) + (a2 + a3);
-    __syncthreads();
-    if (tid < w) z[tid] = v[tid] + (red[tid] + red[tid + kMaxW]);
-}
-
-// ---------------------------------------------------------------------------
-// lower sweep: L y = r
-// shared memory: [stage][seg 128][yv 128][red 256][row pointers 130 x int64][dst slots]
-// ---------------------------------------------------------------------------
 template <bool TRACE>
 __device__ __forceinline__ void lower_sweep_body(const tsb_ldlt_desc &D, const SweepArgs &A, double *smem,
-                                            uint64_t &bar, uint32_t &phase) {
-    double *stage = smem;                             // TMA staging: panel inverse or factor chunk
-    double *seg = smem + D.stage_doubles;             // gathered panel rows
-    double *yv = seg + kMaxW;                         // solved panel rows
-    double *red = yv + kMaxW;                         // 256 partial sums
-    int64_t *rptr = reinterpret_cast<int64_t *>(red + kSweepBlock);  // contribution row pointers
-    int32_t *dsts = reinterpret_cast<int32_t *>(rptr + kMaxW + 2);   // chunk rows' cbuf slots
-    __shared__ int item_id;
+                                                 uint64_t &bar, uint32_t &phase) {
+    double *stage = smem;
+    double *xs = smem + D.stage_doubles;
+    int32_t *dsts = reinterpret_cast<int32_t *>(xs + ((D.max_m + 1) & ~1));  // cbuf slots of the chunk's M rows
+    __shared__ int item_id, fin_parent;
     int32_t *ctl = D.d_ctl;
-    int32_t *contrib = D.d_cnt0, *flag = D.d_cnt1;
     int64_t *const tbuf = TRACE ? D.d_trace_lower : nullptr;  // folds away when off
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const Item *items = reinterpret_cast<const Item *>(D.d_items_lower);
+    const LItem *items = reinterpret_cast<const LItem *>(D.d_items_lower);
     while (true) {
         if (tid == 0) item_id = atomicAdd(ctl, 1);
         __syncthreads();
         const int iid = item_id;
         if (iid >= D.n_items_lower) break;
         trace(tbuf, iid, 0);
-        const Item it = items[iid];
-        const int p = it.panel;
-        const int pstart = D.d_p_start[p], w = D.d_p_w[p];
-        if (it.type == IT_DIAG) {
-            // everything that does not depend on the contributions is fetched
-            // before the wait: the panel inverse (TMA), row pointers, the input
-            const int k = tid >> 1, h = tid & 1;
-            double xin = 0.0;
-            int64_t q0 = 0, q1 = 0;
-            if (tid == 0) tma_load_1d(stage, D.d_tri + D.d_p_tri[p], (uint32_t)(D.d_p_tri_len[p] * 8), &bar);
-            if (k < w) {
-                const int row = pstart + k;
-                q0 = __ldg(D.d_cin_ptr + row) + h;
-                q1 = __ldg(D.d_cin_ptr + row + 1);
-                if (h == 0) xin = __ldcg(A.in + (A.in_perm ? A.in_perm[row] : row));  // L2: may be produced in-kernel
-            }
-            if (tid == 0) spin_until_geq(contrib + p, it.dep_cnt);
-            __syncthreads();
-            trace(tbuf, iid, 1);
-            // rows: input - contributions.  Two threads per row (w <= 128), each
-            // summing every other contribution with its loads in flight, then one
-            // xor step: a fixed summation order (deterministic)
-            {
-                double acc0 = 0.0, acc1 = 0.0;
-                int64_t q = q0;
-                for (; q + 2 < q1; q += 4) {
-                    acc0 += __ldcg(D.d_cbuf + q);
-                    acc1 += __ldcg(D.d_cbuf + q + 2);
+        const LItem it = items[iid];
+        const tsb_ldlt_block B = D.d_blocks[it.block];
+        const int m = B.m, s = B.start, nr = it.r1 - it.r0;
+        const int64_t o0 = g_row_off(it.r0, m);
+        const double *gb = D.d_g + B.g_off;
+        // everything that does not depend on the sweep's progress is fetched
+        // before the wait: the factor rows (TMA), the block's input, the slots
+        if (tid == 0) tma_load_1d(stage, gb + o0, (uint32_t)((g_row_off(it.r1, m) - o0) * 8), &bar);
+        for (int j = tid; j < m; j += kSweepBlock) xs[j] = lower_input(A, s + j);
+        const int mr0 = max(it.r0, m);
+        for (int j = mr0 + tid; j < it.r1; j += kSweepBlock) dsts[j - mr0] = __ldg(D.d_cslot + B.anc_off + (j - m));
+        if (B.target_l > 0 && tid == 0) spin_until_geq(D.d_ready_l + it.block, 1);
+        __syncthreads();
+        trace(tbuf, iid, 1);
+        if (B.target_l > 0)  // x_b = input - (contributions of the descendants, summed by the finaliser)
+            for (int j = tid; j < m; j += kSweepBlock) xs[j] = xs[j] - __ldcg(D.d_x + s + j);
+        mbar_wait(&bar, phase);
+        phase ^= 1;
+        __syncthreads();
+        trace(tbuf, iid, 4);
+        // G lanes per row, 32/G rows per warp step; lanes stride the columns
+        {
+            const int G = m > 64 ? 32 : (m > 32 ? 16 : 8);
+            const int gl = lane & (G - 1), gpw = 32 / G;
+            for (int jb = warp * gpw; jb < nr; jb += (kSweepBlock / 32) * gpw) {  // warp-uniform trips
+                const int j = jb + lane / G;
+                const bool ok = j < nr;
+                const int r = it.r0 + (ok ? j : 0);
+                const int len = ok ? (r < m ? r : m) : 0;
+                const double *row = stage + (g_row_off(r, m) - o0);
+                double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+                int c = gl;
+                for (; c + 3 * G < len; c += 4 * G) {
+                    a0 += row[c] * xs[c];
+                    a1 += row[c + G] * xs[c + G];
+                    a2 += row[c + 2 * G] * xs[c + 2 * G];
+                    a3 += row[c + 3 * G] * xs[c + 3 * G];
                 }
-                if (q < q1) acc0 += __ldcg(D.d_cbuf + q);
-                double acc = acc0 + acc1;
-                acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-                if (k < w && h == 0) seg[k] = xin - acc;
-            }
-            mbar_wait(&bar, phase);
-            phase ^= 1;
-            __syncthreads();
-            trace(tbuf, iid, 4);
-            panel_lower(stage, w, seg, yv, red, tid);
-            __syncthreads();
-            for (int k = tid; k < w; k += kSweepBlock) A.x[pstart + k] = yv[k];
-            trace(tbuf, iid, 5);
-            __threadfence();
-            __syncthreads();
-            if (tid == 0) atomicExch(flag + p, 1);
-            trace(tbuf, iid, 2);
-        } else {  // IT_OFF: contributions of panel p to below rows [r0, r1)
-            // the factor chunk does not depend on the sweep: stage it with TMA while
-            // waiting for the panel's solution
-            const int ws = w + (w & 1), nr = it.r1 - it.r0;
-            if (tid == 0) {
-                tma_load_1d(stage, D.d_pan + D.d_p_pan[p] + (int64_t)it.r0 * ws, (uint32_t)(nr * ws * 8), &bar);
-                spin_until_geq(flag + p, 1);
-            }
-            const int32_t *slot = D.d_cslot + D.d_p_cb[p] + it.r0;
-            for (int j = tid; j < nr; j += kSweepBlock) dsts[j] = __ldg(slot + j);
-            __syncthreads();
-            trace(tbuf, iid, 1);
-            for (int k = tid; k < w; k += kSweepBlock) seg[k] = __ldcg(A.x + pstart + k);
-            mbar_wait(&bar, phase);
-            phase ^= 1;
-            __syncthreads();
-            trace(tbuf, iid, 4);
-            // G lanes per below row (G = 32/16/8 for wide/medium/narrow panels),
-            // two rows in flight per group, lanes over the panel columns; each
-            // result goes to the row's contiguous contribution slot
-            {
-                const int G = w > 64 ? 32 : (w > 32 ? 16 : 8);
-                const int gl = lane & (G - 1), gpw = 32 / G;
-                // warp-uniform trip count: the xor shuffles need every lane
-                for (int jb = warp * gpw * 2; jb < nr; jb += (kSweepBlock / 32) * gpw * 2) {
-                    const int j = jb + (lane / G) * 2;
-                    const bool one = j < nr, two = j + 1 < nr;
-                    const double *pa = stage + j * ws;
-                    double a0 = 0.0, a1 = 0.0;
-                    for (int c = gl; c < w; c += G) {
-                        const double s = seg[c];
-                        if (one) a0 += pa[c] * s;
-                        if (two) a1 += pa[ws + c] * s;
-                    }
-                    for (int o = G >> 1; o > 0; o >>= 1) {
-                        a0 += __shfl_xor_sync(0xffffffffu, a0, o);
-                        a1 += __shfl_xor_sync(0xffffffffu, a1, o);
-                    }
-                    if (gl == 0 && one) {
-                        D.d_cbuf[dsts[j]] = a0;
-                        if (two) D.d_cbuf[dsts[j + 1]] = a1;
-                    }
+                for (; c < len; c += G) a0 += row[c] * xs[c];
+                double a = (a0 + a1) + (a2 + a3);
+                for (int o = G >> 1; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+                if (ok && gl == 0) {
+                    if (r < m)
+                        A.x[s + r] = xs[r] + a;
+                    else
+                        D.d_cbuf[dsts[r - mr0]] = a;
                 }
             }
-            trace(tbuf, iid, 5);
-            __threadfence();
-            __syncthreads();
-            if (tid == 0) {
-                for (int q = 0; q < it.dep_cnt; ++q) atomicAdd(contrib + D.d_deps[it.dep_off + q], 1);
-            }
-            trace(tbuf, iid, 2);
         }
+        trace(tbuf, iid, 5);
+        __syncthreads();
+        if (tid == 0) {
+            fin_parent = -1;
+            if (B.parent >= 0) {
+                __threadfence();
+                const int old = atomicAdd(D.d_cnt_l + B.parent, 1);
+                if (old == D.d_blocks[B.parent].target_l - 1) {
+                    __threadfence();
+                    fin_parent = B.parent;
+                }
+            }
+        }
+        __syncthreads();
+        if (fin_parent >= 0) {
+            // Every child item is done: S_parent = sum of its rows' contributions
+            // (row-contiguous in cbuf).  Stage them piece by piece with coalesced
+            // loads (all in flight at once) together with the per-row offsets,
+            // then one thread per row sums its slots in order.
+            const tsb_ldlt_block P = D.d_blocks[fin_parent];
+            int32_t *offs = reinterpret_cast<int32_t *>(xs);  // free: this item's GEMV is done
+            const int64_t qe = __ldg(D.d_cin_ptr + P.start + P.m);
+            int i0 = 0;
+            while (i0 < P.m) {
+                const int64_t qb = __ldg(D.d_cin_ptr + P.start + i0);
+                int i1 = P.m;
+                if (qe - qb > D.stage_doubles) {  // rows [i0, i1) whose contributions fit (>= 1 row)
+                    int lo = i0 + 1, hi = P.m;
+                    while (lo < hi) {
+                        const int mid = (lo + hi + 1) >> 1;
+                        if (__ldg(D.d_cin_ptr + P.start + mid) - qb <= D.stage_doubles) lo = mid; else hi = mid - 1;
+                    }
+                    i1 = lo;
+                }
+                const int cnt = (int)(__ldg(D.d_cin_ptr + P.start + i1) - qb);
+                const bool staged = cnt <= D.stage_doubles;
+                if (staged) {
+                    constexpr int U = 8;
+                    for (int k0 = tid; k0 < cnt; k0 += U * kSweepBlock) {
+                        double t[U];
+#pragma unroll
+                        for (int u = 0; u < U; ++u) {
+                            const int k = k0 + u * kSweepBlock;
+                            t[u] = k < cnt ? __ldcg(D.d_cbuf + qb + k) : 0.0;
+                        }
+#pragma unroll
+                        for (int u = 0; u < U; ++u) {
+                            const int k = k0 + u * kSweepBlock;
+                            if (k < cnt) stage[k] = t[u];
+                        }
+                    }
+                }
+                for (int i = i0 + tid; i <= i1; i += kSweepBlock)
+                    offs[i - i0] = (int32_t)(__ldg(D.d_cin_ptr + P.start + i) - qb);
+                __syncthreads();
+                for (int i = i0 + tid; i < i1; i += kSweepBlock) {
+                    const int a0 = offs[i - i0], a1 = offs[i - i0 + 1];
+                    double c0 = 0.0, c1 = 0.0;
+                    int q = a0;
+                    if (staged) {
+                        for (; q + 1 < a1; q += 2) {
+                            c0 += stage[q];
+                            c1 += stage[q + 1];
+                        }
+                        if (q < a1) c0 += stage[q];
+                    } else {  // a single row with more contributions than the buffer
+                        for (; q + 1 < a1; q += 2) {
+                            c0 += __ldcg(D.d_cbuf + qb + q);
+                            c1 += __ldcg(D.d_cbuf + qb + q + 1);
+                        }
+                        if (q < a1) c0 += __ldcg(D.d_cbuf + qb + q);
+                    }
+                    D.d_x[P.start + i] = c0 + c1;
+                }
+                __syncthreads();
+                i0 = i1;
+            }
+            if (tid == 0) {
+                __threadfence();
+                st_release(D.d_ready_l + fin_parent, 1);
+            }
+        }
+        trace(tbuf, iid, 2);
     }
-    sweep_exit(D, ctl, contrib, flag);
+    sweep_exit(ctl, D.d_cnt_l, D.n_blocks, D.d_ready_l, D.n_blocks);
 }
 
 // ---------------------------------------------------------------------------
-// upper sweep: L^T z = w
-// shared memory: [stage][seg 128][red 256][zv 128][zb max chunk rows]
+// upper sweep: L^T z = w   (row-major pull)
+//   z_b = w_b + G_b^T v,  v = [w_b ; -z_anc]
+//   item (b, slab, G rows [ra, rb)): partial sums of the slab's columns over
+//   the tile rows (cp.async-staged before the wait; triangle-only tiles have
+//   no dependency, M tiles wait for the parent's z); the last tile of a slab
+//   adds the partials in tile order and publishes z for the slab's columns.
+// shared memory: [stage tile_rows x sw][v max_tile_rows][red 256]
 // ---------------------------------------------------------------------------
 template <bool TRACE>
 __device__ __forceinline__ void upper_sweep_body(const tsb_ldlt_desc &D, const SweepArgs &A, double *smem,
-                                            uint64_t &bar, uint32_t &phase) {
+                                                 uint64_t &bar, uint32_t &phase) {
+    (void)bar;
+    (void)phase;
     double *stage = smem;
-    double *seg = smem + D.stage_doubles;
-    double *red = seg + kMaxW;
-    double *zv = red + kSweepBlock;
-    double *zb = zv + kMaxW;
-    __shared__ int item_id;
+    double *v = smem + D.stage_doubles;
+    double *red = v + ((D.max_tile_rows + 1) & ~1);
+    int32_t *ancs = reinterpret_cast<int32_t *>(red + kSweepBlock);
+    __shared__ int item_id, last;
     int32_t *ctl = D.d_ctl + 2;
-    int32_t *ready = D.d_cnt2, *flag = D.d_cnt3;
     int64_t *const tbuf = TRACE ? D.d_trace_upper : nullptr;
     const int tid = threadIdx.x;
-    const Item *items = reinterpret_cast<const Item *>(D.d_items_upper);
+    const UItem *items = reinterpret_cast<const UItem *>(D.d_items_upper);
     while (true) {
         if (tid == 0) item_id = atomicAdd(ctl, 1);
         __syncthreads();
         const int iid = item_id;
         if (iid >= D.n_items_upper) break;
         trace(tbuf, iid, 0);
-        const Item it = items[iid];
-        const int p = it.panel;
-        const int pstart = D.d_p_start[p], w = D.d_p_w[p];
-        if (it.type == IT_OFFT) {
-            // partial[c] = sum_{j in [r0,r1)} P[j][c] * z[below[j]]; the factor chunk
-            // is staged by TMA while the owners of its rows finish
-            const int ws = w + (w & 1), nr = it.r1 - it.r0;
-            if (tid == 0) {
-                tma_load_1d(stage, D.d_pan + D.d_p_pan[p] + (int64_t)it.r0 * ws, (uint32_t)(nr * ws * 8), &bar);
-                for (int q = 0; q < it.dep_cnt; ++q) spin_until_geq(flag + D.d_deps[it.dep_off + q], 1);
+        const UItem it = items[iid];
+        const tsb_ldlt_block B = D.d_blocks[it.block];
+        const int m = B.m, s = B.start, sw = B.sw, nr = it.rb - it.ra;
+        const int c0 = (it.slab - B.slab_base) * sw;
+        const int cw = min(sw, m - c0);
+        const double *gb = D.d_g + B.g_off;
+        // stage G[ra:rb, c0:c0+sw) (16-byte pieces; missing triangle entries -> 0)
+        {
+            const int pr = sw >> 1;
+            for (int q = tid; q < nr * pr; q += kSweepBlock) {
+                const int rr = q / pr, pc = (q - rr * pr) * 2;
+                const int r = it.ra + rr, c = c0 + pc;
+                double *dst = stage + rr * sw + pc;
+                const int lim = r < m ? r : c0 + cw;  // triangle row r stores columns < r
+                if (c < lim)
+                    cp_async16(dst, gb + g_row_off(r, m) + c);
+                else
+                    dst[0] = dst[1] = 0.0;
             }
-            __syncthreads();
-            trace(tbuf, iid, 1);
-            const int32_t *below = D.d_below + D.d_p_below[p] + it.r0;
-            for (int j = tid; j < nr; j += kSweepBlock) zb[j] = __ldcg(A.x + below[j]);
-            mbar_wait(&bar, phase);
-            phase ^= 1;
-            __syncthreads();
-            trace(tbuf, iid, 4);
-            const int wp = w <= 16 ? 16 : (w <= 32 ? 32 : (w <= 64 ? 64 : 128));
-            const int c = tid % wp, rg = tid / wp, ng = kSweepBlock / wp;
+            cp_async_commit();
+        }
+        // the triangle rows' values and the M rows' ancestor indices do not
+        // depend on the sweep: fetch them before the wait
+        for (int j = tid; j < nr; j += kSweepBlock) {
+            const int r = it.ra + j;
+            if (r < m) {
+                double vj = __ldcg(A.in + s + r);  // produced earlier in the same (persistent) kernel
+                if (A.dscale) vj = vj / A.dscale[s + r];
+                v[j] = vj;
+            } else {
+                ancs[j] = __ldg(D.d_anc + B.anc_off + (r - m));
+            }
+        }
+        if (it.has_dep && tid == 0) spin_until_geq(D.d_done_u + B.parent, D.d_blocks[B.parent].nslabs);
+        __syncthreads();
+        trace(tbuf, iid, 1);
+        if (it.has_dep)
+            for (int j = tid; j < nr; j += kSweepBlock)
+                if (it.ra + j >= m) v[j] = -__ldcg(A.x + ancs[j]);
+        cp_async_wait_all();
+        __syncthreads();
+        trace(tbuf, iid, 4);
+        {
+            const int cc = tid % sw, g = tid / sw, ng = kSweepBlock / sw;
             double a0 = 0.0, a1 = 0.0;
-            if (c < w) {
-                int j = rg;
-                for (; j + ng < nr; j += 2 * ng) {
-                    a0 += stage[j * ws + c] * zb[j];
-                    a1 += stage[(j + ng) * ws + c] * zb[j + ng];
-                }
-                if (j < nr) a0 += stage[j * ws + c] * zb[j];
+            int j = g;
+            for (; j + ng < nr; j += 2 * ng) {
+                a0 += stage[j * sw + cc] * v[j];
+                a1 += stage[(j + ng) * sw + cc] * v[j + ng];
             }
+            if (j < nr) a0 += stage[j * sw + cc] * v[j];
             red[tid] = a0 + a1;
             __syncthreads();
-            if (tid < w) {
-                double s = 0.0;
-                for (int g = 0; g < ng; ++g) s += red[g * wp + tid];
-                D.d_part[it.out_off + tid] = s;
+            if (tid < cw) {
+                double p = 0.0;
+                for (int q = 0; q < ng; ++q) p += red[q * sw + tid];
+                D.d_part[D.d_slab_part[it.slab] + (int64_t)it.tile * sw + tid] = p;
             }
-            trace(tbuf, iid, 5);
-            __threadfence();
-            __syncthreads();
-            if (tid == 0) atomicAdd(ready + p, 1);
-            trace(tbuf, iid, 2);
-        } else {  // IT_DIAGT
-            const int k = tid >> 1, h = tid & 1;
-            double vin = 0.0;
-            if (tid == 0) tma_load_1d(stage, D.d_tri_u + D.d_p_tri[p], (uint32_t)(D.d_p_tri_len[p] * 8), &bar);
-            if (k < w && h == 0) {  // input (and D scaling) does not depend on the wait
-                vin = __ldcg(A.in + pstart + k);
-                if (A.dscale) vin = vin / A.dscale[pstart + k];
-            }
-            if (tid == 0) spin_until_geq(ready + p, it.dep_cnt);
-            __syncthreads();
-            trace(tbuf, iid, 1);
-            {
-                // two threads per row sum the chunk partials of one parity (fixed order)
-                double s0 = 0.0, s1 = 0.0;
-                if (k < w) {
-                    int q = h;
-                    for (; q + 2 < it.dep_cnt; q += 4) {
-                        s0 += __ldcg(D.d_part + it.out_off + q * w + k);
-                        s1 += __ldcg(D.d_part + it.out_off + (q + 2) * w + k);
-                    }
-                    if (q < it.dep_cnt) s0 += __ldcg(D.d_part + it.out_off + q * w + k);
-                }
-                double s = s0 + s1;
-                s += __shfl_xor_sync(0xffffffffu, s, 1);
-                if (k < w && h == 0) seg[k] = vin - s;
-            }
-            mbar_wait(&bar, phase);
-            phase ^= 1;
-            __syncthreads();
-            trace(tbuf, iid, 4);
-            panel_upper(stage, w, seg, zv, red, tid);
-            __syncthreads();
-            for (int k = tid; k < w; k += kSweepBlock) {
-                const double v = zv[k];
-                A.x[pstart + k] = v;
-                if (A.out_perm) A.out[A.out_perm[pstart + k]] = v;
-            }
-            trace(tbuf, iid, 5);
-            __threadfence();
-            __syncthreads();
-            if (tid == 0) atomicExch(flag + p, 1);
-            trace(tbuf, iid, 2);
         }
+        trace(tbuf, iid, 5);
+        __syncthreads();
+        if (tid == 0) {
+            __threadfence();
+            last = atomicAdd(D.d_cnt_s + it.slab, 1) == D.d_slab_ntiles[it.slab] - 1;
+            if (last) __threadfence();
+        }
+        __syncthreads();
+        if (last) {  // all tiles of the slab are in: z = w + partials (tile order)
+            if (tid < cw) {
+                const int nt = D.d_slab_ntiles[it.slab];
+                const double *pp = D.d_part + D.d_slab_part[it.slab] + tid;
+                double acc = 0.0;
+                for (int t = 0; t < nt; ++t) acc += __ldcg(pp + (int64_t)t * sw);
+                const int row = s + c0 + tid;
+                double w = __ldcg(A.in + row);
+                if (A.dscale) w = w / A.dscale[row];
+                const double z = w + acc;
+                A.x[row] = z;
+                if (A.out_perm) A.out[A.out_perm[row]] = z;
+            }
+            __syncthreads();
+            if (tid == 0) {
+                __threadfence();
+                atomicAdd(D.d_done_u + it.block, 1);
+            }
+        }
+        trace(tbuf, iid, 2);
     }
-    sweep_exit(D, ctl, ready, flag);
+    sweep_exit(ctl, D.d_cnt_s, D.n_slabs, D.d_done_u, D.n_blocks);
 }
 
 }  // namespace tsb

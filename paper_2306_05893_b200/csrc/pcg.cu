@@ -194,7 +194,7 @@ pcg_persistent(PcgWork W, PcgArgs a, tsb_ldlt_desc D) {
     }
     // preconditioner application z = M r and rz = r.z
     SweepArgs lo_args{W.r, D.d_perm, nullptr, D.d_y, nullptr, nullptr, nullptr};
-    SweepArgs up_args{D.d_y, nullptr, D.d_d, D.d_y, D.d_perm, W.z, nullptr};
+    SweepArgs up_args{D.d_y, nullptr, D.d_d, D.d_x, D.d_perm, W.z, nullptr};
     double rz = 0.0, beta = 0.0;
     if (!done) {
         double v = 0.0;

@@ -1,8 +1,10 @@
-"""CPU check of the device panel layout and the DAG item lists (csrc/ldlt.cu):
-a serial NumPy emulator executes the work items in dispatch order with the
-kernel's exact data flow; it must (a) only ever find its dependencies
-satisfied (the order is topological, hence deadlock-free on the persistent
-kernel) and (b) reproduce the oracle's level-scheduled sweeps."""
+"""CPU check of the device block-inverse layout and the DAG item lists
+(csrc/ldlt.cu, ldlt_sweep.cuh): a serial NumPy emulator executes the work
+items in dispatch order with the kernel's exact data flow (row chunks for the
+lower sweep, column-slab x row tiles with last-tile reduction for the upper);
+it must (a) only ever find its dependencies satisfied -- the order is
+topological, hence deadlock-free on the persistent kernel -- and (b)
+reproduce the oracle's level-scheduled sweeps (ndprecond.py:647-691)."""
 
 import numpy as np
 import pytest
@@ -13,85 +15,99 @@ from paper_2306_05893_b200 import _ldlt_pack as K, mesh as M, ndprecond as ND
 from paper_2306_05893_b200.assembly import CsrMatrix
 
 
-def _panel_inverse(H, p, which):
-    """Unpack the panel's explicit diagonal-triangle inverse (unit lower) from the
-    lower sweep's column-packed copy or the upper sweep's row-packed copy."""
-    w = int(H["p_w"][p])
-    blob = H[which][H["p_tri"][p]: H["p_tri"][p] + H["p_tri_len"][p]]
-    Li = np.eye(w)
-    if which == "tri":
-        cj, ri = np.triu_indices(w, 1)
-        Li[ri, cj] = blob[: len(ri)]
-    else:
-        ri, cj = np.tril_indices(w, -1)
-        Li[ri, cj] = blob[: len(ri)]
-    return Li
+def _g(H, b):
+    B = H["blocks"][b]
+    m, na = int(B["m"]), int(B["na"])
+    off = K.row_offsets(m, na)
+    return H["g"][B["g_off"]: B["g_off"] + off[-1]], off, m, na
 
 
 def emulate_lower(H, r):
-    n, P = H["n"], H["P"]
+    n, nb = H["n"], H["nb"]
+    blocks = H["blocks"]
     y = np.zeros(n)
+    xbuf = np.zeros(n)
     cbuf = np.zeros(max(H["ncbuf"], 1))
-    contrib = np.zeros(P, dtype=np.int64)
-    flag = np.zeros(P, dtype=bool)
-    for typ, p, r0, r1, doff, dcnt, _, _ in H["items_l"]:
-        s, w = int(H["p_start"][p]), int(H["p_w"][p])
-        if typ == K.IT_DIAG:
-            assert contrib[p] == dcnt, "DIAG dispatched before its contributions"
-            seg = np.empty(w)
-            for k in range(w):
-                row = s + k
-                v = r[row]
-                for q in range(H["cin_ptr"][row], H["cin_ptr"][row + 1]):
-                    v -= cbuf[q]
-                seg[k] = v
-            y[s:s + w] = _panel_inverse(H, p, "tri") @ seg
-            flag[p] = True
+    cnt = np.zeros(nb, dtype=np.int64)
+    ready = np.zeros(nb, dtype=bool)
+    for b, r0, r1, _ in H["items_l"]:
+        B = blocks[b]
+        s, m = int(B["start"]), int(B["m"])
+        g, off, _, _ = _g(H, b)
+        if B["target_l"] > 0:
+            assert ready[b], "lower item dispatched before its block input was final"
+            xs = xbuf[s:s + m].copy()
         else:
-            assert typ == K.IT_OFF and flag[p]
-            nb = H["p_below"][p + 1] - H["p_below"][p] if p + 1 < P else len(H["below"]) - H["p_below"][p]
-            ws = w + (w & 1)  # rows padded to an even stride (16-byte TMA chunks)
-            pan = H["pan"][H["p_pan"][p]: H["p_pan"][p] + nb * ws].reshape(nb, ws)[:, :w]
-            cbuf[H["cslot"][H["p_cb"][p] + r0: H["p_cb"][p] + r1]] = pan[r0:r1] @ y[s:s + w]
-            contrib[H["deps"][doff: doff + dcnt]] += 1
+            xs = r[s:s + m].copy()
+        for row in range(r0, r1):
+            if row < m:
+                y[s + row] = xs[row] + g[off[row]: off[row] + row] @ xs[:row]
+            else:
+                k = row - m
+                cbuf[H["cslot"][B["anc_off"] + k]] = g[off[row]: off[row] + m] @ xs
+        p = int(B["parent"])
+        if p >= 0:
+            cnt[p] += 1
+            if cnt[p] == blocks[p]["target_l"]:  # this item finalises the parent's input
+                P = blocks[p]
+                for i in range(int(P["m"])):
+                    row = int(P["start"]) + i
+                    xbuf[row] = r[row] - cbuf[H["cin_ptr"][row]: H["cin_ptr"][row + 1]].sum()
+                ready[p] = True
+    assert np.all(cnt == blocks["target_l"])
     return y
 
 
-def emulate_upper(H, w_in):
-    n, P = H["n"], H["P"]
+def emulate_upper(H, w):
+    n, nb = H["n"], H["nb"]
+    blocks = H["blocks"]
     z = np.zeros(n)
     part = np.zeros(max(H["npart"], 1))
-    ready = np.zeros(P, dtype=np.int64)
-    flag = np.zeros(P, dtype=bool)
-    for typ, p, r0, r1, doff, dcnt, ooff, _ in H["items_u"]:
-        s, w = int(H["p_start"][p]), int(H["p_w"][p])
-        if typ == K.IT_OFFT:
-            assert all(flag[H["deps"][doff: doff + dcnt]]), "OFFT dispatched before its owners"
-            nb = H["p_below"][p + 1] - H["p_below"][p] if p + 1 < P else len(H["below"]) - H["p_below"][p]
-            ws = w + (w & 1)  # rows padded to an even stride (16-byte TMA chunks)
-            pan = H["pan"][H["p_pan"][p]: H["p_pan"][p] + nb * ws].reshape(nb, ws)[:, :w]
-            below = H["below"][H["p_below"][p]: H["p_below"][p] + nb]
-            part[ooff: ooff + w] = pan[r0:r1].T @ z[below[r0:r1]]
-            ready[p] += 1
-        else:
-            assert typ == K.IT_DIAGT and ready[p] == dcnt
-            seg = w_in[s:s + w] - sum(part[ooff + q * w: ooff + (q + 1) * w] for q in range(dcnt))
-            z[s:s + w] = _panel_inverse(H, p, "tri_u").T @ seg
-            flag[p] = True
+    cnt_s = np.zeros(H["n_slabs"], dtype=np.int64)
+    done = np.zeros(nb, dtype=np.int64)
+    for b, slab, ra, rb, tile, has_dep, _, _ in H["items_u"]:
+        B = blocks[b]
+        s, m, sw = int(B["start"]), int(B["m"]), int(B["sw"])
+        g, off, _, _ = _g(H, b)
+        c0 = (slab - int(B["slab_base"])) * sw
+        cw = min(sw, m - c0)
+        if has_dep:
+            p = int(B["parent"])
+            assert done[p] == blocks[p]["nslabs"], "upper M tile dispatched before the parent's z"
+        acc = np.zeros(cw)
+        for row in range(ra, rb):
+            if row < m:
+                v = w[s + row]
+                hi = min(c0 + cw, row)
+                if hi > c0:
+                    acc[: hi - c0] += g[off[row] + c0: off[row] + hi] * v
+            else:
+                v = -z[H["anc"][B["anc_off"] + row - m]]
+                acc += g[off[row] + c0: off[row] + c0 + cw] * v
+        part[H["slab_part"][slab] + tile * sw: H["slab_part"][slab] + tile * sw + cw] = acc
+        cnt_s[slab] += 1
+        if cnt_s[slab] == H["slab_ntiles"][slab]:
+            nt = int(H["slab_ntiles"][slab])
+            tot = sum(part[H["slab_part"][slab] + t * sw: H["slab_part"][slab] + t * sw + cw] for t in range(nt))
+            z[s + c0: s + c0 + cw] = w[s + c0: s + c0 + cw] + tot
+            done[b] += 1
+    assert np.all(done == blocks["nslabs"])
     return z
 
 
-@pytest.mark.parametrize("dims,leaf", [((3, 3, 8), 16), ((4, 4, 12), 16), ((6, 6, 28), 64)])
-def test_panel_dag_emulation_matches_oracle(params, dims, leaf):
+def _factors(dims, leaf):
     mesh = clamped_beam(*dims)
-    from oracle import tetsim_oracle as O2  # noqa: F401
-
     rest = O.rest_data(mesh.nodes, mesh.elements, 1e5, 0.3, 1000.0)
     out = O.assemble_system(mesh.nodes, mesh.elements, mesh.fixed_nodes, rest, mesh.nodes,
                             np.zeros_like(mesh.nodes), np.zeros(mesh.ndof), 0.01, (0.0, -9.81, 0.0))
     a = CsrMatrix(mesh.ndof, mesh.ndof, out["row_ptr"], out["col_ind"], out["values"])
     plan = ND.expand_plan(ND.nested_dissection(M.vertex_adjacency(mesh), leaf))
-    f = ND.ldlt_factor(a, plan)
+    return mesh, ND.ldlt_factor(a, plan)
+
+
+@pytest.mark.parametrize("dims,leaf", [((3, 3, 8), 16), ((4, 4, 12), 16), ((6, 6, 28), 64)])
+def test_block_inverse_dag_emulation_matches_oracle(dims, leaf):
+    mesh, f = _factors(dims, leaf)
     H = K.pack(f)
     r = np.random.default_rng(7).standard_normal(mesh.ndof)
     y = emulate_lower(H, r)
@@ -100,6 +116,25 @@ def test_panel_dag_emulation_matches_oracle(params, dims, leaf):
     z = emulate_upper(H, r)
     ref = O.solve_upper(f, r)
     assert np.abs(z - ref).max() <= 1e-12 * np.abs(ref).max()
-    # item lists cover every panel exactly once per sweep
-    assert sorted(H["items_l"][H["items_l"][:, 0] == K.IT_DIAG, 1]) == list(range(H["P"]))
-    assert sorted(H["items_u"][H["items_u"][:, 0] == K.IT_DIAGT, 1]) == list(range(H["P"]))
+
+
+def test_block_layout_roundtrip_and_coverage():
+    _, f = _factors((4, 4, 12), 16)
+    H = K.pack(f)
+    for b, bf in enumerate(f.blocks):
+        g, off, m, na = _g(H, b)
+        linv, mm = K.unpack_block(g, m, na)
+        assert np.allclose(linv @ bf.l11, np.eye(m), atol=1e-12)
+        assert np.allclose(mm, bf.l21 @ linv, atol=1e-12)
+        assert np.all(off % 2 == 0)  # every row 16-byte aligned (TMA / cp.async)
+    # lower items cover each block's G rows exactly once
+    for b in range(H["nb"]):
+        B = H["blocks"][b]
+        rows = sorted((r0, r1) for bb, r0, r1, _ in H["items_l"] if bb == b)
+        assert rows[0][0] == 0 and rows[-1][1] == B["m"] + B["na"]
+        assert all(a[1] == c[0] for a, c in zip(rows, rows[1:]))
+    # every slab has at least one tile and the tile ids are 0..ntiles-1
+    for sid in range(H["n_slabs"]):
+        t = sorted(x[4] for x in H["items_u"] if x[1] == sid)
+        assert t == list(range(H["slab_ntiles"][sid]))
+    assert H["g"].size == sum(len(_g(H, b)[0]) for b in range(H["nb"]))

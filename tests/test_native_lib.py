@@ -21,10 +21,21 @@ def test_library_loads_and_exports_all_symbols():
     lib = _lib.load()
     for name in declared_symbols():
         assert hasattr(lib, name), name
-    assert lib.tsb_abi_version() == 1
+    assert lib.tsb_abi_version() == 2
 
 
 def test_error_message_roundtrip():
     lib = _lib.load()
     assert lib.tsb_ldlt_create(None, None) == _lib.TSB_E_ARG
     assert "null" in _lib.last_error()
+
+
+def test_struct_layouts_match_the_header():
+    from paper_2306_05893_b200 import _ldlt_pack
+
+    lib = _lib.load()
+    assert lib.tsb_struct_size(0) == _lib.C.sizeof(_lib.AsmPlan)
+    assert lib.tsb_struct_size(1) == _lib.C.sizeof(_lib.AsmCoeffs)
+    assert lib.tsb_struct_size(2) == _ldlt_pack.BLOCK_DTYPE.itemsize
+    assert lib.tsb_struct_size(3) == _lib.C.sizeof(_lib.LdltDesc)
+    assert lib.tsb_struct_size(4) == _lib.C.sizeof(_lib.Report)

@@ -22,32 +22,27 @@ sys.path.insert(0, str(ROOT))
 import bench  # noqa: E402
 from paper_2306_05893_b200._ldlt_pack import DevicePanels  # noqa: E402
 
-NAMES = {0: "DIAG", 1: "OFFDIAG", 2: "OFFDIAG_T", 3: "DIAG_T"}
 
-
-def summarize(tr, items):
+def summarize(tr, kinds, names):
     t0 = tr[:, 0].min()
     take, ready, end = tr[:, 0] - t0, tr[:, 1] - t0, tr[:, 2] - t0
     out = {"wall_us": float(end.max() / 1e3), "items": int(len(tr))}
     per = {}
-    for ty in np.unique(items[:, 0]):
-        m = items[:, 0] == ty
-        per[NAMES[int(ty)]] = {
+    for ty in np.unique(kinds):
+        m = kinds == ty
+        per[names[int(ty)]] = {
             "count": int(m.sum()),
             "wait_us_mean": float(((ready - take)[m]).mean() / 1e3),
             "exec_us_mean": float(((end - ready)[m]).mean() / 1e3),
-            "exec_us_sum": float(((end - ready)[m]).sum() / 1e3),
-            "wait_us_sum": float(((ready - take)[m]).sum() / 1e3),
             "stage_us_mean": float(((tr[:, 4] - tr[:, 1])[m]).mean() / 1e3),
             "compute_us_mean": float(((tr[:, 5] - tr[:, 4])[m]).mean() / 1e3),
             "publish_us_mean": float(((tr[:, 2] - tr[:, 5])[m]).mean() / 1e3),
         }
-    out["by_type"] = per
+    out["by_kind"] = per
     busy = float((end - ready).sum())
     wait = float((ready - take).sum())
     out["wait_fraction_of_item_time"] = wait / max(busy + wait, 1.0)
     out["sms_used"] = int(len(np.unique(tr[:, 3])))
-    # concurrency profile: executing items over time (10 bins)
     bins = np.linspace(0, end.max(), 11)
     conc = []
     for a, b in zip(bins[:-1], bins[1:]):
@@ -55,6 +50,30 @@ def summarize(tr, items):
         conc.append(round(float(ov), 1))
     out["mean_executing_items_per_decile"] = conc
     return out
+
+
+def lower_chain(tr, items, H):
+    """Critical chain of the lower sweep: from the last item back through the
+    child item that completed each block's input."""
+    t0 = tr[:, 0].min()
+    end = (tr[:, 2] - t0) / 1e3
+    ready = (tr[:, 1] - t0) / 1e3
+    blk = items[:, 0]
+    by_block = {}
+    for i, b in enumerate(blk):
+        by_block.setdefault(int(b), []).append(i)
+    cur = int(np.argmax(end))
+    chain = []
+    while True:
+        chain.append(cur)
+        kids = H["children"][int(blk[cur])]
+        if not kids:
+            break
+        cand = [i for c in kids for i in by_block[c]]
+        cur = max(cand, key=lambda i: end[i])
+    chain.reverse()
+    return [{"block": int(blk[i]), "m": int(H["blocks"][blk[i]]["m"]), "ready": round(float(ready[i]), 2),
+             "end": round(float(end[i]), 2)} for i in chain]
 
 
 def main():
@@ -93,16 +112,18 @@ def main():
         res_plain.append(e0.elapsed_time(e1))
     report = {
         "workload": args.workload, "apply_ms_median": float(np.median(res)),
-        "apply_ms_untraced": float(np.median(res_plain)), "panels": H["P"],
+        "apply_ms_untraced": float(np.median(res_plain)), "blocks": H["nb"],
         "n": H["n"], "grid_note": "persistent grid = SMs x resident CTAs",
-        "lower": summarize(dev.trace_l.cpu().numpy(), H["items_l"]),
-        "upper": summarize(dev.trace_u.cpu().numpy(), H["items_u"]),
+        "lower": summarize(dev.trace_l.cpu().numpy(), (H["blocks"]["target_l"][H["items_l"][:, 0]] > 0).astype(int),
+                           {0: "leaf", 1: "inner"}),
+        "upper": summarize(dev.trace_u.cpu().numpy(), H["items_u"][:, 5], {0: "tri", 1: "M"}),
+        "lower_chain": lower_chain(dev.trace_l.cpu().numpy(), H["items_l"], H),
     }
     txt = json.dumps(report, indent=1)
     print(txt)
     if args.out:
         Path(args.out).write_text(txt)
-        keep = {k: H[k] for k in ("items_l", "items_u", "p_w", "p_start", "deps", "p_below", "p_cb")}
+        keep = {k: H[k] for k in ("items_l", "items_u", "parent")}
         np.savez_compressed(Path(args.out).with_suffix(".npz"), trace_l=dev.trace_l.cpu().numpy(),
                             trace_u=dev.trace_u.cpu().numpy(), **keep)
 
