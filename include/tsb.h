@@ -171,14 +171,21 @@ int tsb_element_blocks(const tsb_asm_plan *plan, const tsb_asm_coeffs *coeffs,
  * Row r of G_b starts at g_off + off(r): off(r) = r*r/2 for triangle rows
  * (row r holds r entries, padded to even), off(r) = m*m/2 + (r-m)*ms for the
  * M rows (ms = m rounded up to even), so every row is 16-byte aligned.
- * Lower items (int4): block, r0, r1, -- one TMA-staged row chunk of G_b.
+ * Lower items (int4): block, r0, r1, -- one TMA-staged row chunk of G_b;
+ * a block's input x_b = r_b - (contributions of its descendants), summed in
+ * a fixed order either by each of its items (small blocks) or once by the
+ * child item that completes it (large blocks; tsb_ldlt_block.mode).
  * Upper items (8 x int32): block, slab, ra, rb, tile, has_dep, 0, 0 -- rows
  * [ra, rb) x columns of one slab (cp.async-staged); the last tile of a slab
  * reduces the slab's partials in tile order (deterministic). */
 typedef struct tsb_ldlt_block {
-    int32_t start, m, na, parent;   /* parent: dissection-tree parent, -1 = root */
-    int32_t target_l;               /* lower items of all children (x_b ready)     */
+    int32_t start, m, na, parent;   /* parent: block elimination-tree parent, -1 = root */
+    int32_t target_l;               /* lower items of all children (x_b complete)  */
     int32_t nslabs, slab_base, sw;  /* upper: column slabs of width sw            */
+    int32_t mode;                   /* lower input: 0 no contributions (leaf),
+                                       1 every item sums the contributions itself,
+                                       2 the last child item sums them once (FIN)  */
+    int32_t pad_;
     int64_t g_off;                  /* offset of G_b in d_g (doubles, even)       */
     int64_t anc_off;                /* offset of the block's anc rows in d_anc     */
 } tsb_ldlt_block;

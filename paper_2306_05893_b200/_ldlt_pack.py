@@ -47,9 +47,10 @@ TILE_ROWS = CHUNK // SLAB
 BLOCK_DTYPE = np.dtype([
     ("start", "<i4"), ("m", "<i4"), ("na", "<i4"), ("parent", "<i4"),
     ("target_l", "<i4"), ("nslabs", "<i4"), ("slab_base", "<i4"), ("sw", "<i4"),
-    ("g_off", "<i8"), ("anc_off", "<i8"),
+    ("mode", "<i4"), ("pad_", "<i4"), ("g_off", "<i8"), ("anc_off", "<i8"),
 ])
-assert BLOCK_DTYPE.itemsize == 48
+assert BLOCK_DTYPE.itemsize == 56
+MODE_LEAF, MODE_GATHER, MODE_FIN = 0, 1, 2
 
 
 def row_offsets(m: int, na: int) -> np.ndarray:
@@ -242,6 +243,14 @@ def pack(factors):
     blocks["nslabs"] = nslabs
     blocks["slab_base"] = slab_base[:-1]
     blocks["sw"] = sw_
+    # lower input of a block: its items sum the contributions themselves when the
+    # redundant L2 reads stay below the block's own factor bytes, else the child
+    # item that completes the block sums them once (one extra hop)
+    contrib = np.diff(cin_ptr)
+    blk_contrib = np.array([int(contrib[bf.start:bf.stop].sum()) for bf in bfs], dtype=np.int64)
+    gsize = np.array([len(g) for g in g_parts], dtype=np.int64)
+    mode = np.where(target_l == 0, MODE_LEAF, np.where(nl * blk_contrib <= gsize, MODE_GATHER, MODE_FIN))
+    blocks["mode"] = mode
     blocks["g_off"] = g_off
     blocks["anc_off"] = anc_off[:-1]
     max_lchunk = max(int(offs[i][r1] - offs[i][r0]) for i in range(nb) for r0, r1 in lchunks[i]) if nb else 2
@@ -255,7 +264,7 @@ def pack(factors):
         "npart": int(slab_part[-1]), "ncbuf": len(anc_all),
         "d": np.asarray(factors.d, dtype=np.float64), "perm": np.asarray(plan.perm, dtype=np.int64),
         "stage": int(stage), "max_m": int(ms_.max()) if nb else 1, "max_tile": int(max(max_tile, 1)),
-        "parent": parent, "children": children,
+        "parent": parent, "children": children, "mode": mode,
         "bytes_g": int(pos) * 8,
     }
 
@@ -263,9 +272,11 @@ def pack(factors):
 class DevicePanels:
     """Packed factor image in HBM + the libtsb handle (tsb_ldlt_create)."""
 
-    def __init__(self, factors, stream=None, trace=False):
+    def __init__(self, factors, stream=None, trace=False, force_mode=None):
         t = _lib.require_cuda()
         H = pack(factors)
+        if force_mode is not None:  # testing: route every inner block through one input mode
+            H["blocks"]["mode"][H["blocks"]["mode"] != MODE_LEAF] = force_mode
         n, nb = H["n"], H["nb"]
         items_l, items_u = H["items_l"], H["items_u"]
         self.host = H if trace else None

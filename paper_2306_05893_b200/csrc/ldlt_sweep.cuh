@@ -124,7 +124,8 @@ __device__ __forceinline__ void sweep_exit(int32_t *ctl, int32_t *c0, int64_t n0
 
 // dynamic shared memory of the sweep bodies
 inline size_t sweep_smem_lower(const tsb_ldlt_desc &D) {
-    return (size_t)(D.stage_doubles + ((D.max_m + 1) & ~1)) * sizeof(double) + kMaxChunkRows * sizeof(int32_t);
+    return (size_t)(D.stage_doubles + ((D.max_m + 1) & ~1)) * sizeof(double) +
+           (((D.max_m + 2) & ~1) + kMaxChunkRows) * sizeof(int32_t);
 }
 inline size_t sweep_smem_upper(const tsb_ldlt_desc &D) {
     return (size_t)(D.stage_doubles + ((D.max_tile_rows + 1) & ~1) + kSweepBlock) * sizeof(double) +
@@ -146,13 +147,87 @@ __device__ __forceinline__ double lower_input(const SweepArgs &A, int row) {
     return __ldcg(A.in + (A.in_perm ? A.in_perm[row] : row));  // may be produced in-kernel (L2)
 }
 
+// Sum of the contributions cbuf[a0, a1) in the fixed order both finalisers use
+// (even slots into c0, odd into c1, then c0 + c1); loads issued ahead.
+__device__ __forceinline__ double contrib_sum(const double *cb, int64_t a0, int64_t a1) {
+    double c0 = 0.0, c1 = 0.0;
+    int64_t q = a0;
+    for (; q + 3 < a1; q += 4) {
+        const double t0 = __ldcg(cb + q), t1 = __ldcg(cb + q + 1), t2 = __ldcg(cb + q + 2), t3 = __ldcg(cb + q + 3);
+        c0 += t0;
+        c1 += t1;
+        c0 += t2;
+        c1 += t3;
+    }
+    for (; q + 1 < a1; q += 2) {
+        c0 += __ldcg(cb + q);
+        c1 += __ldcg(cb + q + 1);
+    }
+    if (q < a1) c0 += __ldcg(cb + q);
+    return c0 + c1;
+}
+
+// One warp: dot products of 8 consecutive G rows [j0, j0+8) of the staged chunk
+// with xs (lanes stride the columns, xs read once per 8 rows), then a butterfly
+// transpose-reduction (7 + 2 shuffles for 8 rows, fixed order).  Returns the
+// row sum in lanes with (lane & 3) == 0; *krow = which of the 8 rows.
+__device__ __forceinline__ double rows8_dot(const double *stage, int64_t o0, int r0, int j0, int nr, int m,
+                                            const double *xs, int lane, int *krow) {
+    const double *rp[8];
+    int len[8];
+    int maxlen = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const int j = j0 + k;
+        const bool ok = j < nr;
+        const int r = r0 + (ok ? j : 0);
+        len[k] = ok ? (r < m ? r : m) : 0;
+        rp[k] = stage + (g_row_off(r, m) - o0);
+        maxlen = max(maxlen, len[k]);
+    }
+    double acc[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc[k] = 0.0;
+    for (int c = lane; c < maxlen; c += 32) {
+        const double xc = xs[c];
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            if (c < len[k]) acc[k] += rp[k][c] * xc;
+    }
+    const bool b16 = lane & 16, b8 = lane & 8, b4 = lane & 4;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const double send = b16 ? acc[k] : acc[k + 4];
+        const double keep = b16 ? acc[k + 4] : acc[k];
+        acc[k] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+    }
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const double send = b8 ? acc[k] : acc[k + 2];
+        const double keep = b8 ? acc[k + 2] : acc[k];
+        acc[k] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+    }
+    {
+        const double send = b4 ? acc[0] : acc[1];
+        const double keep = b4 ? acc[1] : acc[0];
+        acc[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+    }
+    double v = acc[0];
+    v += __shfl_xor_sync(0xffffffffu, v, 2);
+    v += __shfl_xor_sync(0xffffffffu, v, 1);
+    *krow = (b16 ? 4 : 0) + (b8 ? 2 : 0) + (b4 ? 1 : 0);
+    return v;
+}
+
 template <bool TRACE>
 __device__ __forceinline__ void lower_sweep_body(const tsb_ldlt_desc &D, const SweepArgs &A, double *smem,
                                                  uint64_t &bar, uint32_t &phase) {
     double *stage = smem;
     double *xs = smem + D.stage_doubles;
-    int32_t *dsts = reinterpret_cast<int32_t *>(xs + ((D.max_m + 1) & ~1));  // cbuf slots of the chunk's M rows
+    int32_t *offs = reinterpret_cast<int32_t *>(xs + ((D.max_m + 1) & ~1));  // per-row contribution offsets
+    int32_t *dsts = offs + ((D.max_m + 2) & ~1);                             // cbuf slots of the M rows
     __shared__ int item_id, fin_parent;
+    __shared__ int64_t qbase;
     int32_t *ctl = D.d_ctl;
     int64_t *const tbuf = TRACE ? D.d_trace_lower : nullptr;  // folds away when off
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -174,42 +249,38 @@ __device__ __forceinline__ void lower_sweep_body(const tsb_ldlt_desc &D, const S
         for (int j = tid; j < m; j += kSweepBlock) xs[j] = lower_input(A, s + j);
         const int mr0 = max(it.r0, m);
         for (int j = mr0 + tid; j < it.r1; j += kSweepBlock) dsts[j - mr0] = __ldg(D.d_cslot + B.anc_off + (j - m));
-        if (B.target_l > 0 && tid == 0) spin_until_geq(D.d_ready_l + it.block, 1);
+        if (B.mode == 1) {
+            const int64_t q0 = __ldg(D.d_cin_ptr + s);
+            for (int j = tid; j <= m; j += kSweepBlock) offs[j] = (int32_t)(__ldg(D.d_cin_ptr + s + j) - q0);
+            if (tid == 0) qbase = q0;
+        }
+        if (tid == 0) {
+            if (B.mode == 1) spin_until_geq(D.d_cnt_l + it.block, B.target_l);
+            else if (B.mode == 2) spin_until_geq(D.d_ready_l + it.block, 1);
+        }
         __syncthreads();
         trace(tbuf, iid, 1);
-        if (B.target_l > 0)  // x_b = input - (contributions of the descendants, summed by the finaliser)
+        // x_b = input - (contributions of the descendants)
+        if (B.mode == 1) {
+            const double *cb = D.d_cbuf + qbase;
+            for (int j = tid; j < m; j += kSweepBlock) xs[j] = xs[j] - contrib_sum(cb, offs[j], offs[j + 1]);
+        } else if (B.mode == 2) {
             for (int j = tid; j < m; j += kSweepBlock) xs[j] = xs[j] - __ldcg(D.d_x + s + j);
+        }
         mbar_wait(&bar, phase);
         phase ^= 1;
         __syncthreads();
         trace(tbuf, iid, 4);
-        // G lanes per row, 32/G rows per warp step; lanes stride the columns
-        {
-            const int G = m > 64 ? 32 : (m > 32 ? 16 : 8);
-            const int gl = lane & (G - 1), gpw = 32 / G;
-            for (int jb = warp * gpw; jb < nr; jb += (kSweepBlock / 32) * gpw) {  // warp-uniform trips
-                const int j = jb + lane / G;
-                const bool ok = j < nr;
-                const int r = it.r0 + (ok ? j : 0);
-                const int len = ok ? (r < m ? r : m) : 0;
-                const double *row = stage + (g_row_off(r, m) - o0);
-                double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-                int c = gl;
-                for (; c + 3 * G < len; c += 4 * G) {
-                    a0 += row[c] * xs[c];
-                    a1 += row[c + G] * xs[c + G];
-                    a2 += row[c + 2 * G] * xs[c + 2 * G];
-                    a3 += row[c + 3 * G] * xs[c + 3 * G];
-                }
-                for (; c < len; c += G) a0 += row[c] * xs[c];
-                double a = (a0 + a1) + (a2 + a3);
-                for (int o = G >> 1; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-                if (ok && gl == 0) {
-                    if (r < m)
-                        A.x[s + r] = xs[r] + a;
-                    else
-                        D.d_cbuf[dsts[r - mr0]] = a;
-                }
+        for (int j0 = warp * 8; j0 < nr; j0 += 8 * (kSweepBlock / 32)) {  // warp-uniform trips
+            int k;
+            const double a = rows8_dot(stage, o0, it.r0, j0, nr, m, xs, lane, &k);
+            const int j = j0 + k;
+            if ((lane & 3) == 0 && j < nr) {
+                const int r = it.r0 + j;
+                if (r < m)
+                    A.x[s + r] = xs[r] + a;
+                else
+                    D.d_cbuf[dsts[r - mr0]] = a;
             }
         }
         trace(tbuf, iid, 5);
@@ -219,7 +290,8 @@ __device__ __forceinline__ void lower_sweep_body(const tsb_ldlt_desc &D, const S
             if (B.parent >= 0) {
                 __threadfence();
                 const int old = atomicAdd(D.d_cnt_l + B.parent, 1);
-                if (old == D.d_blocks[B.parent].target_l - 1) {
+                const tsb_ldlt_block &Pb = D.d_blocks[B.parent];
+                if (Pb.mode == 2 && old == Pb.target_l - 1) {
                     __threadfence();
                     fin_parent = B.parent;
                 }
@@ -232,7 +304,7 @@ __device__ __forceinline__ void lower_sweep_body(const tsb_ldlt_desc &D, const S
             // loads (all in flight at once) together with the per-row offsets,
             // then one thread per row sums its slots in order.
             const tsb_ldlt_block P = D.d_blocks[fin_parent];
-            int32_t *offs = reinterpret_cast<int32_t *>(xs);  // free: this item's GEMV is done
+            int32_t *fo = reinterpret_cast<int32_t *>(xs);  // free: this item's GEMV is done
             const int64_t qe = __ldg(D.d_cin_ptr + P.start + P.m);
             int i0 = 0;
             while (i0 < P.m) {
@@ -265,10 +337,10 @@ __device__ __forceinline__ void lower_sweep_body(const tsb_ldlt_desc &D, const S
                     }
                 }
                 for (int i = i0 + tid; i <= i1; i += kSweepBlock)
-                    offs[i - i0] = (int32_t)(__ldg(D.d_cin_ptr + P.start + i) - qb);
+                    fo[i - i0] = (int32_t)(__ldg(D.d_cin_ptr + P.start + i) - qb);
                 __syncthreads();
                 for (int i = i0 + tid; i < i1; i += kSweepBlock) {
-                    const int a0 = offs[i - i0], a1 = offs[i - i0 + 1];
+                    const int a0 = fo[i - i0], a1 = fo[i - i0 + 1];
                     double c0 = 0.0, c1 = 0.0;
                     int q = a0;
                     if (staged) {

@@ -179,3 +179,34 @@ def test_async_preconditioner_lifecycle(params):
     res = integ.step(st, lambda a, b: krylov.pcg(a, b, pre, cfg))
     assert res.report.converged and res.report.iterations <= 5
     pre.close()
+
+
+@pytest.mark.parametrize("mode", [1, 2])
+def test_ldlt_lower_input_modes_agree(params, mode):
+    """Both ways of forming a block's input (items sum their contributions / the
+    completing child item sums them once) give the oracle's sweeps; repeated
+    applies are bitwise reproducible (fixed reduction order, counters reset)."""
+    import torch
+    from paper_2306_05893_b200._ldlt_pack import DevicePanels
+    from paper_2306_05893_b200.integrator import BackwardEulerIntegrator, IntegratorConfig, SimState
+    from paper_2306_05893_b200 import models
+
+    mesh = clamped_beam(10, 10, 60)
+    integ = BackwardEulerIntegrator(mesh, models.make_model("corotational", mesh, params),
+                                    IntegratorConfig(dt=0.01, gravity=(0.0, -9.81, 0.0)))
+    a, _, _ = integ.assemble_system(SimState.rest(mesh))
+    plan = ND.expand_plan(ND.nested_dissection(M.vertex_adjacency(mesh), 64))
+    f = ND.ldlt_factor(a, plan)
+    dev = DevicePanels(f, force_mode=mode)
+    r = np.random.default_rng(5).standard_normal(a.nrows)
+    dr = torch.from_numpy(r).cuda()
+    outs = []
+    for _ in range(3):
+        z = torch.empty_like(dr)
+        dev.run("apply", dr, z)
+        outs.append(z.cpu().numpy())
+    assert rel(outs[0], O.apply(f, r)) <= 1e-12
+    assert all(np.array_equal(outs[0], o) for o in outs[1:])
+    y = torch.empty_like(dr)
+    dev.run("lower", dr, y)
+    assert rel(y.cpu().numpy(), O.solve_lower(f, r)) <= 1e-12

@@ -34,10 +34,14 @@ def emulate_lower(H, r):
         B = blocks[b]
         s, m = int(B["start"]), int(B["m"])
         g, off, _, _ = _g(H, b)
-        if B["target_l"] > 0:
+        if B["mode"] == K.MODE_FIN:
             assert ready[b], "lower item dispatched before its block input was final"
-            xs = xbuf[s:s + m].copy()
+            xs = r[s:s + m] - xbuf[s:s + m]
+        elif B["mode"] == K.MODE_GATHER:
+            assert cnt[b] == B["target_l"], "lower item dispatched before its children finished"
+            xs = np.array([r[s + i] - cbuf[H["cin_ptr"][s + i]: H["cin_ptr"][s + i + 1]].sum() for i in range(m)])
         else:
+            assert B["target_l"] == 0
             xs = r[s:s + m].copy()
         for row in range(r0, r1):
             if row < m:
@@ -48,14 +52,26 @@ def emulate_lower(H, r):
         p = int(B["parent"])
         if p >= 0:
             cnt[p] += 1
-            if cnt[p] == blocks[p]["target_l"]:  # this item finalises the parent's input
-                P = blocks[p]
+            if cnt[p] == blocks[p]["target_l"] and blocks[p]["mode"] == K.MODE_FIN:
+                P = blocks[p]  # this item finalises the parent's contribution sums
                 for i in range(int(P["m"])):
                     row = int(P["start"]) + i
-                    xbuf[row] = r[row] - cbuf[H["cin_ptr"][row]: H["cin_ptr"][row + 1]].sum()
+                    xbuf[row] = cbuf[H["cin_ptr"][row]: H["cin_ptr"][row + 1]].sum()
                 ready[p] = True
     assert np.all(cnt == blocks["target_l"])
     return y
+
+
+def test_both_lower_input_modes_are_exercised():
+    _, f = _factors((6, 6, 28), 64)
+    H = K.pack(f)
+    modes = set(H["blocks"]["mode"].tolist())
+    assert K.MODE_LEAF in modes and K.MODE_GATHER in modes
+    # force the FIN path everywhere and re-check against the oracle
+    H["blocks"]["mode"][H["blocks"]["mode"] == K.MODE_GATHER] = K.MODE_FIN
+    r = np.random.default_rng(3).standard_normal(f.plan.n)
+    ref = O.solve_lower(f, r)
+    assert np.abs(emulate_lower(H, r) - ref).max() <= 1e-12 * np.abs(ref).max()
 
 
 def emulate_upper(H, w):
