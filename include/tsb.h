@@ -159,35 +159,40 @@ int tsb_element_blocks(const tsb_asm_plan *plan, const tsb_asm_coeffs *coeffs,
  * ---------------------------------------------------------------------- */
 /* Block-inverse layout (built by the host from LdlFactors, _ldlt_pack.py).
  * For every dissection block b (permuted rows [start, start+m), ancestors
- * anc[0..na)) the host stores ONE row-major matrix
+ * anc[0..na)) the host stores
  *     G_b = [ inv(L11) - I   (strict lower triangle, rows 1..m-1)      ]
  *           [ M = L21 inv(L11)  (na x m)                               ]
  * -- the reference's tile inverses (ndprecond.py:575-587) widened to the
- * whole diagonal block, with the coupling panel pre-multiplied by it.  Then
+ * whole diagonal block, with the coupling panel pre-multiplied by it -- once
+ * row-major for the lower sweep and once transposed for the upper sweep:
  *   lower (solve_lower, ndprecond.py:647-671):  y_b = x_b + (Linv-I) x_b,
  *          contributions to the ancestors  c_b = M x_b  (column-major
  *          pre-accumulation of the paper, one GEMV per block, no in-block chain);
- *   upper (solve_upper, ndprecond.py:674-691):  z_b = w_b + G_b^T [w_b; -z_anc].
- * Row r of G_b starts at g_off + off(r): off(r) = r*r/2 for triangle rows
- * (row r holds r entries, padded to even), off(r) = m*m/2 + (r-m)*ms for the
- * M rows (ms = m rounded up to even), so every row is 16-byte aligned.
- * Lower items (int4): block, r0, r1, -- one TMA-staged row chunk of G_b;
- * a block's input x_b = r_b - (contributions of its descendants), summed in
- * a fixed order either by each of its items (small blocks) or once by the
- * child item that completes it (large blocks; tsb_ldlt_block.mode).
- * Upper items (8 x int32): block, slab, ra, rb, tile, has_dep, 0, 0 -- rows
- * [ra, rb) x columns of one slab (cp.async-staged); the last tile of a slab
- * reduces the slab's partials in tile order (deterministic). */
+ *   upper (solve_upper, ndprecond.py:674-691):  z_b = w_b + G_b^T v,
+ *          v = [w_b; -z_anc]  (row-major pull, one GEMV per block).
+ * Row r of G_b (lower) starts at g_off + off(r): off(r) = r*r/2 for triangle
+ * rows (row r holds columns [0, r), padded to even), m*m/2 + (r-m)*ms for the
+ * M rows (columns [0, m), ms = m rounded up to even).  Row c of G_b^T (upper)
+ * holds v-entries [c+1, m+na) (length K-c, K = m+na-1, padded to even) at
+ * gt_off + sum_{j=K-c+1..K} (j + (j & 1)).  Every row is 16-byte aligned.
+ * Items (int4 {block, r0, r1, 0}): rows [r0, r1) of G_b (lower) or G_b^T
+ * (upper), each staged by one TMA bulk copy issued before the dependency wait.
+ * Lower: x_b = r_b - (contributions of its descendants), summed in a fixed
+ * order either by each of the block's items (mode 1) or once by the child item
+ * that completes the block (mode 2).  Upper: an item of b waits for every
+ * item of b's parent (z_anc final). */
 typedef struct tsb_ldlt_block {
     int32_t start, m, na, parent;   /* parent: block elimination-tree parent, -1 = root */
     int32_t target_l;               /* lower items of all children (x_b complete)  */
-    int32_t nslabs, slab_base, sw;  /* upper: column slabs of width sw            */
+    int32_t n_u;                    /* upper items of this block (z_b complete)    */
     int32_t mode;                   /* lower input: 0 no contributions (leaf),
                                        1 every item sums the contributions itself,
-                                       2 the last child item sums them once (FIN)  */
-    int32_t pad_;
-    int64_t g_off;                  /* offset of G_b in d_g (doubles, even)       */
-    int64_t anc_off;                /* offset of the block's anc rows in d_anc     */
+                                       2 the last child item sums them once       */
+    int32_t ncb;                    /* contributions into the block's rows         */
+    int64_t g_off;                  /* offset of G_b in d_g (doubles, even)        */
+    int64_t gt_off;                 /* offset of G_b^T in d_gt                     */
+    int64_t anc_off;                /* offset of the block's anc rows in d_anc      */
+    int64_t cb_off;                 /* first cbuf slot of the block's rows          */
 } tsb_ldlt_block;
 
 typedef struct tsb_ldlt_desc {
@@ -195,28 +200,27 @@ typedef struct tsb_ldlt_desc {
     int64_t n_blocks;
     int64_t n_items_lower;
     int64_t n_items_upper;
-    int64_t n_slabs;
-    int32_t stage_doubles;        /* staging buffer (doubles), >= any chunk/tile */
-    int32_t max_m;                /* largest block                                */
-    int32_t max_tile_rows;        /* rows of the largest upper tile               */
-    int32_t grid;                 /* persistent CTAs (0 = fill the GPU)           */
+    int32_t stage_doubles;        /* staging buffer (doubles), >= any item's rows   */
+    int32_t max_m;                /* largest block                                  */
+    int32_t max_v;                /* largest m + na                                 */
+    int32_t max_cb;               /* largest ncb of a mode-1 block                  */
+    int32_t grid;                 /* persistent CTAs (0 = fill the GPU)             */
+    int32_t pad_;
     const tsb_ldlt_block *d_blocks;
     const int32_t *d_items_lower; /* [n_items_lower][4], topological dispatch order */
-    const int32_t *d_items_upper; /* [n_items_upper][8]                            */
-    const double *d_g;            /* all G_b                                       */
+    const int32_t *d_items_upper; /* [n_items_upper][4]                            */
+    const double *d_g;            /* all G_b (row-major)                           */
+    const double *d_gt;           /* all G_b^T                                     */
     const int32_t *d_anc;         /* permuted ancestor rows, per block             */
     const int32_t *d_cslot;       /* cbuf slot of (block, anc k)                    */
     const int64_t *d_cin_ptr;     /* [n+1]: row r's contributions are cbuf[cin_ptr[r]..cin_ptr[r+1]) */
-    const int64_t *d_slab_part;   /* [n_slabs] offset of the slab's partials in d_part */
-    const int32_t *d_slab_ntiles; /* [n_slabs]                                      */
     const double *d_d;            /* [n] D                                          */
     const int32_t *d_perm;        /* [n] perm[k] = original index at position k    */
     double *d_cbuf;               /* scratch: lower contributions                  */
-    double *d_part;               /* scratch: upper slab partials                  */
-    double *d_x;                  /* scratch [n]: x_b of non-leaf blocks (lower)    */
+    double *d_x;                  /* scratch [n]: contribution sums (mode 2) / z    */
     double *d_y;                  /* scratch [n]: lower result inside apply         */
     int32_t *d_cnt_l, *d_ready_l; /* [n_blocks] counters (zeroed; reset on exit)    */
-    int32_t *d_cnt_s, *d_done_u;  /* [n_slabs], [n_blocks]                          */
+    int32_t *d_done_u, *d_pad;    /* [n_blocks]                                     */
     int32_t *d_ctl;               /* [4] tickets / exit counters (zeroed)          */
     int64_t *d_trace_lower;       /* optional [n_items_lower][8] item timeline     */
     int64_t *d_trace_upper;       /* optional [n_items_upper][8]                   */

@@ -22,8 +22,10 @@ tree.  The factor blocks are well conditioned (cond_1(L11) <= 12.5 on the
 cfg2 beam); the block-inverse apply matches the reference's tile-16 sweeps
 to ~4e-16 relative.
 
-Work items (csrc/ldlt.cu): lower = row chunks of G_b (~48 KB, one TMA bulk
-copy each); upper = column slab (32 columns) x row tile (<= 192 rows).  The
+G_b is stored twice: row-major for the lower sweep and transposed for the
+upper (row c of G_b^T = column c of G_b below the diagonal, i.e. the entries
+multiplying v[c+1:]), so both sweeps are row-chunked GEMVs with one TMA bulk
+copy per work item (~48 KB) and no cross-item reduction.  The
 dispatch order is a list schedule on an infinite machine keyed by each
 item's earliest start under a simple cost model, ties broken by the longest
 remaining path (critical path first).  Every dependency finishes strictly
@@ -41,15 +43,14 @@ from . import _lib
 
 CHUNK = 6144          # doubles per lower item (48 KB, one TMA bulk copy)
 CHUNK_ROWS = 512      # rows per lower item (csrc kMaxChunkRows)
-SLAB = 32             # upper slab width (columns); 16 for blocks of <= 16 columns
-TILE_ROWS = CHUNK // SLAB
+CB_MAX = 4096         # contributions a block's items may sum themselves (csrc max_cb)
 
 BLOCK_DTYPE = np.dtype([
     ("start", "<i4"), ("m", "<i4"), ("na", "<i4"), ("parent", "<i4"),
-    ("target_l", "<i4"), ("nslabs", "<i4"), ("slab_base", "<i4"), ("sw", "<i4"),
-    ("mode", "<i4"), ("pad_", "<i4"), ("g_off", "<i8"), ("anc_off", "<i8"),
+    ("target_l", "<i4"), ("n_u", "<i4"), ("mode", "<i4"), ("ncb", "<i4"),
+    ("g_off", "<i8"), ("gt_off", "<i8"), ("anc_off", "<i8"), ("cb_off", "<i8"),
 ])
-assert BLOCK_DTYPE.itemsize == 56
+assert BLOCK_DTYPE.itemsize == 64
 MODE_LEAF, MODE_GATHER, MODE_FIN = 0, 1, 2
 
 
@@ -58,6 +59,16 @@ def row_offsets(m: int, na: int) -> np.ndarray:
     r = np.arange(m + na + 1, dtype=np.int64)
     ms = m + (m & 1)
     return np.where(r < m, (r * r) // 2, (m * m) // 2 + (r - m) * ms)
+
+
+def gt_row_offsets(m: int, na: int) -> np.ndarray:
+    """Offsets (doubles) of the m + 1 row boundaries of G_b^T (csrc gt_row_off):
+    row c holds v-entries [c+1, m+na), length K - c (K = m+na-1), padded to even."""
+    K = m + na - 1
+    lens = K - np.arange(m, dtype=np.int64)
+    out = np.zeros(m + 1, dtype=np.int64)
+    np.cumsum(lens + (lens & 1), out=out[1:])
+    return out
 
 
 def block_matrix(bf):
@@ -72,8 +83,12 @@ def block_matrix(bf):
 
 def pack_block(bf) -> np.ndarray:
     """G_b in the device row layout (flat float64, even length)."""
-    m, na = bf.stop - bf.start, len(bf.anc)
     linv, mm = block_matrix(bf)
+    return _pack_rows(bf, linv, mm)
+
+
+def _pack_rows(bf, linv, mm):
+    m, na = bf.stop - bf.start, len(bf.anc)
     off = row_offsets(m, na)
     g = np.zeros(int(off[-1]))
     ir, ic = np.tril_indices(m, -1)
@@ -81,6 +96,20 @@ def pack_block(bf) -> np.ndarray:
     if na:
         ms = m + (m & 1)
         g[off[m]:].reshape(na, ms)[:, :m] = mm
+    return g
+
+
+def pack_block_t(bf, linv=None, mm=None) -> np.ndarray:
+    """G_b^T in the device row layout (flat float64, even length)."""
+    m, na = bf.stop - bf.start, len(bf.anc)
+    if linv is None:
+        linv, mm = block_matrix(bf)
+    full = np.vstack([np.tril(linv, -1), mm]) if na else np.tril(linv, -1)
+    off = gt_row_offsets(m, na)
+    g = np.zeros(int(off[-1]))
+    for c in range(m):
+        col = full[c + 1:, c]
+        g[off[c]: off[c] + len(col)] = col
     return g
 
 
@@ -145,12 +174,17 @@ def pack(factors):
     na_ = np.array([len(bf.anc) for bf in bfs], dtype=np.int64)
     # ---------------- G blobs ----------------
     g_parts, g_off = [], np.zeros(nb, dtype=np.int64)
-    pos = 0
+    gt_parts, gt_off = [], np.zeros(nb, dtype=np.int64)
+    pos = post = 0
     for i, bf in enumerate(bfs):
-        g = pack_block(bf)
-        g_off[i] = pos
+        linv, mm = block_matrix(bf)
+        g = _pack_rows(bf, linv, mm)
+        gt = pack_block_t(bf, linv, mm)
+        g_off[i], gt_off[i] = pos, post
         g_parts.append(g)
+        gt_parts.append(gt)
         pos += len(g)
+        post += len(gt)
     anc_off = np.zeros(nb + 1, dtype=np.int64)
     np.cumsum(na_, out=anc_off[1:])
     anc_all = (np.concatenate([np.asarray(bf.anc, dtype=np.int64) for bf in bfs]) if anc_off[-1]
@@ -182,51 +216,23 @@ def pack(factors):
     lower.sort()
     items_l = np.array([(x[4], x[3], x[5], 0) for x in lower], dtype=np.int32).reshape(-1, 4)
     # ---------------- upper items ----------------
-    sw_ = np.where(ms_ > 16, SLAB, 16)
-    nslabs = (ms_ + sw_ - 1) // sw_
-    slab_base = np.zeros(nb + 1, dtype=np.int64)
-    np.cumsum(nslabs, out=slab_base[1:])
-    S = int(slab_base[-1])
-    tiles = [None] * S   # per slab: list of (ra, rb, has_dep)
-    for i in range(nb):
-        m, na, sw = int(ms_[i]), int(na_[i]), int(sw_[i])
-        tr = TILE_ROWS * SLAB // sw
-        for q in range(int(nslabs[i])):
-            c0 = q * sw
-            lst = []
-            for ra in range(c0 + 1, m, tr):
-                lst.append((ra, min(ra + tr, m), 0))
-            for ra in range(m, m + na, tr):
-                lst.append((ra, min(ra + tr, m + na), 1))
-            tiles[slab_base[i] + q] = lst or [(0, 0, 0)]
-    slab_ntiles = np.array([len(t) for t in tiles], dtype=np.int64)
-    slab_part = np.zeros(S + 1, dtype=np.int64)
-    slab_sw = np.repeat(sw_, nslabs)
-    np.cumsum(slab_ntiles * slab_sw, out=slab_part[1:])
+    toffs = [gt_row_offsets(int(ms_[i]), int(na_[i])) for i in range(nb)]
+    uchunks = [_lower_chunks(toffs[i], int(ms_[i])) for i in range(nb)]
+    n_u = np.array([len(c) for c in uchunks], dtype=np.int64)
+    start_u = np.zeros(nb)
     done_u = np.zeros(nb)
-    start_of = {}
-    for i in sorted(range(nb), key=lambda i: -bfs[i].start):  # parents first
-        dep_t = done_u[parent[i]] if parent[i] >= 0 else 0.0
-        fin = 0.0
-        for q in range(int(nslabs[i])):
-            for ra, rb, dep in tiles[slab_base[i] + q]:
-                st = dep_t if dep else 0.0
-                start_of[(i, q, ra)] = st
-                fin = max(fin, st + cost((rb - ra) * int(sw_[i])))
-        done_u[i] = fin + 0.5
+    for i in reversed(order):  # parents first
+        start_u[i] = done_u[parent[i]] if parent[i] >= 0 else 0.0
+        done_u[i] = start_u[i] + max(cost(toffs[i][r1] - toffs[i][r0]) for r0, r1 in uchunks[i])
     tail_u = np.zeros(nb)
     for i in order:  # children first
-        own = done_u[i] - (done_u[parent[i]] if parent[i] >= 0 else 0.0)
-        tail_u[i] = own + max((tail_u[c] for c in children[i]), default=0.0)
+        tail_u[i] = (done_u[i] - start_u[i]) + max((tail_u[c] for c in children[i]), default=0.0)
     upper = []
     for i in range(nb):
-        for q in range(int(nslabs[i])):
-            sid = int(slab_base[i] + q)
-            for t, (ra, rb, dep) in enumerate(tiles[sid]):
-                upper.append((start_of[(i, q, ra)], -tail_u[i], -bfs[i].start, q, t, i, sid, ra, rb, dep))
+        for r0, r1 in uchunks[i]:
+            upper.append((start_u[i], -tail_u[i], -bfs[i].start, r0, i, r1))
     upper.sort()
-    items_u = np.array([(x[5], x[6], x[7], x[8], x[4], x[9], 0, 0) for x in upper],
-                       dtype=np.int32).reshape(-1, 8)
+    items_u = np.array([(x[4], x[3], x[5], 0) for x in upper], dtype=np.int32).reshape(-1, 4)
     # ---------------- contribution slots (lower) ----------------
     corder = np.argsort(anc_all, kind="stable")   # row-contiguous, block order within a row
     cin_ptr = np.zeros(n + 1, dtype=np.int64)
@@ -240,32 +246,36 @@ def pack(factors):
     blocks["na"] = na_
     blocks["parent"] = parent
     blocks["target_l"] = target_l
-    blocks["nslabs"] = nslabs
-    blocks["slab_base"] = slab_base[:-1]
-    blocks["sw"] = sw_
+    blocks["n_u"] = n_u
     # lower input of a block: its items sum the contributions themselves when the
     # redundant L2 reads stay below the block's own factor bytes, else the child
     # item that completes the block sums them once (one extra hop)
     contrib = np.diff(cin_ptr)
     blk_contrib = np.array([int(contrib[bf.start:bf.stop].sum()) for bf in bfs], dtype=np.int64)
     gsize = np.array([len(g) for g in g_parts], dtype=np.int64)
-    mode = np.where(target_l == 0, MODE_LEAF, np.where(nl * blk_contrib <= gsize, MODE_GATHER, MODE_FIN))
+    mode = np.where(target_l == 0, MODE_LEAF,
+                    np.where((nl * blk_contrib <= gsize) & (blk_contrib <= CB_MAX), MODE_GATHER, MODE_FIN))
     blocks["mode"] = mode
+    blocks["ncb"] = blk_contrib
+    blocks["cb_off"] = cin_ptr[[bf.start for bf in bfs]] if nb else []
+    blocks["gt_off"] = gt_off
     blocks["g_off"] = g_off
     blocks["anc_off"] = anc_off[:-1]
     max_lchunk = max(int(offs[i][r1] - offs[i][r0]) for i in range(nb) for r0, r1 in lchunks[i]) if nb else 2
-    max_tile = max((rb - ra for t in tiles for ra, rb, _ in t), default=1)
-    stage = max(max_lchunk, max(max_tile, 1) * SLAB, 2)
+    max_uchunk = max(int(toffs[i][r1] - toffs[i][r0]) for i in range(nb) for r0, r1 in uchunks[i]) if nb else 2
+    stage = max(max_lchunk, max_uchunk, 2)
     stage += stage & 1
+    max_cb = int(blk_contrib[mode == MODE_GATHER].max()) if np.any(mode == MODE_GATHER) else 0
     return {
         "n": n, "nb": nb, "blocks": blocks, "items_l": items_l, "items_u": items_u,
-        "g": np.concatenate(g_parts) if g_parts else np.zeros(2), "anc": anc_all, "cslot": cslot,
-        "cin_ptr": cin_ptr, "slab_part": slab_part[:-1], "slab_ntiles": slab_ntiles, "n_slabs": S,
-        "npart": int(slab_part[-1]), "ncbuf": len(anc_all),
+        "g": np.concatenate(g_parts) if g_parts else np.zeros(2),
+        "gt": np.concatenate(gt_parts) if gt_parts else np.zeros(2),
+        "anc": anc_all, "cslot": cslot, "cin_ptr": cin_ptr, "ncbuf": len(anc_all),
         "d": np.asarray(factors.d, dtype=np.float64), "perm": np.asarray(plan.perm, dtype=np.int64),
-        "stage": int(stage), "max_m": int(ms_.max()) if nb else 1, "max_tile": int(max(max_tile, 1)),
+        "stage": int(stage), "max_m": int(ms_.max()) if nb else 1,
+        "max_v": int((ms_ + na_).max()) if nb else 1, "max_cb": max_cb,
         "parent": parent, "children": children, "mode": mode,
-        "bytes_g": int(pos) * 8,
+        "bytes_g": int(pos) * 8, "bytes_gt": int(post) * 8,
     }
 
 
@@ -276,7 +286,10 @@ class DevicePanels:
         t = _lib.require_cuda()
         H = pack(factors)
         if force_mode is not None:  # testing: route every inner block through one input mode
-            H["blocks"]["mode"][H["blocks"]["mode"] != MODE_LEAF] = force_mode
+            inner = H["blocks"]["mode"] != MODE_LEAF
+            H["blocks"]["mode"][inner] = force_mode
+            if force_mode == MODE_GATHER:
+                H["max_cb"] = int(H["blocks"]["ncb"][inner].max(initial=0))
         n, nb = H["n"], H["nb"]
         items_l, items_u = H["items_l"], H["items_u"]
         self.host = H if trace else None
@@ -292,28 +305,27 @@ class DevicePanels:
             nz = lambda a: a if len(a) else np.zeros(1, dtype=a.dtype)  # noqa: E731
             self.t = {
                 "blocks": up(H["blocks"].view(np.uint8)), "items_l": up(nz(items_l.ravel())),
-                "items_u": up(nz(items_u.ravel())), "g": up(H["g"]), "anc": i32(nz(H["anc"])),
-                "cslot": i32(nz(H["cslot"])), "cin_ptr": i64(H["cin_ptr"]), "slab_part": i64(nz(H["slab_part"])),
-                "slab_ntiles": i32(nz(H["slab_ntiles"])), "d": up(H["d"]), "perm": i32(H["perm"]),
+                "items_u": up(nz(items_u.ravel())), "g": up(H["g"]), "gt": up(H["gt"]),
+                "anc": i32(nz(H["anc"])), "cslot": i32(nz(H["cslot"])), "cin_ptr": i64(H["cin_ptr"]),
+                "d": up(H["d"]), "perm": i32(H["perm"]),
             }
-            self.t.update(cbuf=z(H["ncbuf"], t.float64), part=z(H["npart"], t.float64), x=z(n, t.float64),
-                          y=z(n, t.float64), cnt=z(3 * nb + H["n_slabs"], t.int32), ctl=z(4, t.int32))
+            self.t.update(cbuf=z(H["ncbuf"], t.float64), x=z(n, t.float64), y=z(n, t.float64),
+                          cnt=z(3 * nb, t.int32), ctl=z(4, t.int32))
         self.n = n
         self.n_blocks = nb
         self.n_items = (len(items_l), len(items_u))
-        self.bytes = {"g": H["bytes_g"]}
+        self.bytes = {"g": H["bytes_g"], "gt": H["bytes_gt"]}
         tp = lambda k: _lib.ptr(self.t[k])  # noqa: E731
         cnt = self.t["cnt"]
         cp = lambda a, b: _lib.ptr(cnt[a:b]) if b > a else _lib.ptr(cnt)  # noqa: E731
         self.desc = _lib.LdltDesc(
-            n=n, n_blocks=nb, n_items_lower=len(items_l), n_items_upper=len(items_u), n_slabs=H["n_slabs"],
-            stage_doubles=H["stage"], max_m=H["max_m"], max_tile_rows=H["max_tile"], grid=0,
+            n=n, n_blocks=nb, n_items_lower=len(items_l), n_items_upper=len(items_u),
+            stage_doubles=H["stage"], max_m=H["max_m"], max_v=H["max_v"], max_cb=H["max_cb"], grid=0, pad_=0,
             d_blocks=tp("blocks"), d_items_lower=tp("items_l"), d_items_upper=tp("items_u"), d_g=tp("g"),
-            d_anc=tp("anc"), d_cslot=tp("cslot"), d_cin_ptr=tp("cin_ptr"), d_slab_part=tp("slab_part"),
-            d_slab_ntiles=tp("slab_ntiles"), d_d=tp("d"), d_perm=tp("perm"),
-            d_cbuf=tp("cbuf"), d_part=tp("part"), d_x=tp("x"), d_y=tp("y"),
-            d_cnt_l=cp(0, nb), d_ready_l=cp(nb, 2 * nb), d_cnt_s=cp(2 * nb, 2 * nb + H["n_slabs"]),
-            d_done_u=cp(2 * nb + H["n_slabs"], 3 * nb + H["n_slabs"]), d_ctl=tp("ctl"),
+            d_gt=tp("gt"), d_anc=tp("anc"), d_cslot=tp("cslot"), d_cin_ptr=tp("cin_ptr"), d_d=tp("d"),
+            d_perm=tp("perm"), d_cbuf=tp("cbuf"), d_x=tp("x"), d_y=tp("y"),
+            d_cnt_l=cp(0, nb), d_ready_l=cp(nb, 2 * nb), d_done_u=cp(2 * nb, 3 * nb), d_pad=tp("ctl"),
+            d_ctl=tp("ctl"),
             d_trace_lower=_lib.ptr(self.trace_l) if trace else None,
             d_trace_upper=_lib.ptr(self.trace_u) if trace else None,
         )

@@ -16,17 +16,15 @@
 // the dissection tree (one hop per level).
 // Work items (dispatched in a precomputed topological, critical-path-first
 // order through one atomic ticket counter; every CTA is resident, so an item
-// only ever waits on items dispensed before it):
-//   lower  (b, G rows [r0, r1))  staged by one TMA bulk copy before waiting for
-//          x_b; triangle rows give y_b, M rows give the contributions to the
+// only ever waits on items dispensed before it) are row chunks of G_b (lower)
+// or G_b^T (upper), each staged by one TMA bulk copy before its wait:
+//   lower  triangle rows give y_b, M rows give the contributions to the
 //          ancestors (column-major pre-accumulation, paper Fig. solveBlock)
-//          written to row-contiguous slots; the item that completes a block's
-//          inputs finalises x_parent = input - contributions (fixed order ->
-//          deterministic, no atomics on data).
-//   upper  (b, slab, G rows [ra, rb))  partial sums of the slab's columns of
-//          G_b^T [w_b; -z_anc] (row-major pull); triangle tiles need nothing,
-//          M tiles wait for the parent's z; the last tile of a slab reduces the
-//          partials in tile order and publishes z for those columns.
+//          written to row-contiguous slots; x_b = input - contributions is
+//          summed in a fixed order (deterministic, no atomics on data) by the
+//          block's own items or once by the child item that completes it.
+//   upper  z_b = w_b + G_b^T [w_b; -z_anc] for a range of the block's columns
+//          (row-major pull); only -z_anc waits for the parent.
 // Counters are reset by the last CTA to leave, so the kernels replay inside
 // the persistent PCG without memsets.
 #include <mutex>
@@ -60,7 +58,7 @@ __global__ void __launch_bounds__(kSweepBlock) upper_sweep(tsb_ldlt_desc D, Swee
     extern __shared__ __align__(128) double smem[];
     __shared__ uint64_t bar;
     if (A.done != nullptr && *((volatile const int32_t *)A.done)) {
-        sweep_exit(D.d_ctl + 2, D.d_cnt_s, D.n_slabs, D.d_done_u, D.n_blocks);
+        sweep_exit(D.d_ctl + 2, D.d_done_u, D.n_blocks, D.d_pad, 0);
         return;
     }
     if (threadIdx.x == 0) mbar_init(&bar, 1);
@@ -114,7 +112,8 @@ extern "C" int tsb_ldlt_create(const tsb_ldlt_desc *desc, tsb_ldlt_t *out) {
     using namespace tsb;
     return guard([&] {
         if (desc == nullptr || out == nullptr) throw Error(TSB_E_ARG, "null desc/out");
-        if (desc->max_m > kMaxXs) throw Error(TSB_E_ARG, "dissection block larger than the x_b staging buffer");
+        if (desc->max_v > kMaxV || desc->max_m > desc->max_v)
+            throw Error(TSB_E_ARG, "dissection block (m + |anc|) larger than the vector staging buffer");
         if (desc->stage_doubles < 2 || (desc->stage_doubles & 1)) throw Error(TSB_E_ARG, "bad staging size");
         auto *h = new tsb_ldlt;
         h->d = *desc;

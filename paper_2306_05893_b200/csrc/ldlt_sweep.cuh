@@ -9,15 +9,11 @@
 namespace tsb {
 
 constexpr int kSweepBlock = 256;
-constexpr int kMaxSW = 32;      // upper-sweep column slab width (doubles)
-constexpr int kMaxXs = 8192;    // largest block whose x_b is staged in shared memory
-constexpr int kMaxChunkRows = 512;  // rows of a lower item (host packer caps it)
+constexpr int kMaxV = 8192;         // largest m + na whose vector is staged in shared memory
+constexpr int kMaxChunkRows = 512;  // rows of an item (host packer caps it)
 
-struct LItem {
+struct Item {
     int32_t block, r0, r1, pad;
-};
-struct UItem {
-    int32_t block, slab, ra, rb, tile, has_dep, p0, p1;
 };
 
 // ---- small PTX helpers -----------------------------------------------------
@@ -84,12 +80,18 @@ __device__ __forceinline__ void trace(int64_t *buf, int iid, int slot) {
     }
 }
 
-// Row r of G_b (m = block size): triangle rows r < m hold r entries (padded to
-// even), then the M rows with stride m rounded up to even.  Every row offset
-// is even (16-byte aligned).
+// Row r of G_b (lower; m = block size): triangle rows r < m hold r entries
+// (padded to even), then the M rows with stride m rounded up to even.
 __device__ __forceinline__ int64_t g_row_off(int r, int m) {
     if (r < m) return ((int64_t)r * r) >> 1;
     return (((int64_t)m * m) >> 1) + (int64_t)(r - m) * (m + (m & 1));
+}
+// Row c of G_b^T (upper; K = m + na - 1): v-entries [c+1, K+1), length K - c
+// padded to even; offset = sum_{j=K-c+1..K} (j + (j & 1)).
+__device__ __forceinline__ int64_t gt_row_off(int c, int K) {
+    if (c <= 0) return 0;
+    const int64_t a = (int64_t)K - c + 1;
+    return ((K + a) * (K - a + 1)) / 2 + (((int64_t)K + 1) >> 1) - (a >> 1);
 }
 
 struct SweepArgs {
@@ -124,75 +126,66 @@ __device__ __forceinline__ void sweep_exit(int32_t *ctl, int32_t *c0, int64_t n0
 
 // dynamic shared memory of the sweep bodies
 inline size_t sweep_smem_lower(const tsb_ldlt_desc &D) {
-    return (size_t)(D.stage_doubles + ((D.max_m + 1) & ~1)) * sizeof(double) +
+    return (size_t)(D.stage_doubles + ((D.max_m + 1) & ~1) + ((D.max_cb + 1) & ~1)) * sizeof(double) +
            (((D.max_m + 2) & ~1) + kMaxChunkRows) * sizeof(int32_t);
 }
 inline size_t sweep_smem_upper(const tsb_ldlt_desc &D) {
-    return (size_t)(D.stage_doubles + ((D.max_tile_rows + 1) & ~1) + kSweepBlock) * sizeof(double) +
-           ((D.max_tile_rows + 1) & ~1) * sizeof(int32_t);
+    return (size_t)(D.stage_doubles + ((D.max_v + 1) & ~1)) * sizeof(double);
 }
 
-// ---------------------------------------------------------------------------
-// lower sweep: L y = r   (column-major pre-accumulation, one GEMV per block)
-//   item (b, rows [r0, r1) of G_b):
-//     stage the rows by TMA (before any wait), wait until x_b is final (the
-//     last child item finalises it), stage x_b, then
-//       triangle row i:  y_i = x_i + sum_{j<i} Linv_ij x_j          -> x[start+i]
-//       M row k:         c_k = sum_j M_kj x_j                        -> cbuf slot
-//     publish to the parent's counter; the item that completes the parent's
-//     inputs finalises x_parent = in - (contributions, fixed order).
-// shared memory: [stage][xs max_m]
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ double lower_input(const SweepArgs &A, int row) {
-    return __ldcg(A.in + (A.in_perm ? A.in_perm[row] : row));  // may be produced in-kernel (L2)
-}
-
-// Sum of the contributions cbuf[a0, a1) in the fixed order both finalisers use
-// (even slots into c0, odd into c1, then c0 + c1); loads issued ahead.
+// Sum of a row's contributions cb[a0, a1) in the fixed order every finaliser
+// uses (even slots into c0, odd into c1, then c0 + c1).
+template <bool GLOBAL>
 __device__ __forceinline__ double contrib_sum(const double *cb, int64_t a0, int64_t a1) {
     double c0 = 0.0, c1 = 0.0;
     int64_t q = a0;
-    for (; q + 3 < a1; q += 4) {
-        const double t0 = __ldcg(cb + q), t1 = __ldcg(cb + q + 1), t2 = __ldcg(cb + q + 2), t3 = __ldcg(cb + q + 3);
-        c0 += t0;
-        c1 += t1;
-        c0 += t2;
-        c1 += t3;
-    }
     for (; q + 1 < a1; q += 2) {
-        c0 += __ldcg(cb + q);
-        c1 += __ldcg(cb + q + 1);
+        c0 += GLOBAL ? __ldcg(cb + q) : cb[q];
+        c1 += GLOBAL ? __ldcg(cb + q + 1) : cb[q + 1];
     }
-    if (q < a1) c0 += __ldcg(cb + q);
+    if (q < a1) c0 += GLOBAL ? __ldcg(cb + q) : cb[q];
     return c0 + c1;
 }
 
-// One warp: dot products of 8 consecutive G rows [j0, j0+8) of the staged chunk
-// with xs (lanes stride the columns, xs read once per 8 rows), then a butterfly
-// transpose-reduction (7 + 2 shuffles for 8 rows, fixed order).  Returns the
-// row sum in lanes with (lane & 3) == 0; *krow = which of the 8 rows.
-__device__ __forceinline__ double rows8_dot(const double *stage, int64_t o0, int r0, int j0, int nr, int m,
-                                            const double *xs, int lane, int *krow) {
-    const double *rp[8];
-    int len[8];
-    int maxlen = 0;
+// Cooperative coalesced copy global -> shared of n doubles, all loads in flight.
+__device__ __forceinline__ void stage_copy(double *dst, const double *src, int n) {
+    constexpr int U = 8;
+    for (int k0 = threadIdx.x; k0 < n; k0 += U * kSweepBlock) {
+        double t[U];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-        const int j = j0 + k;
-        const bool ok = j < nr;
-        const int r = r0 + (ok ? j : 0);
-        len[k] = ok ? (r < m ? r : m) : 0;
-        rp[k] = stage + (g_row_off(r, m) - o0);
-        maxlen = max(maxlen, len[k]);
+        for (int u = 0; u < U; ++u) {
+            const int k = k0 + u * kSweepBlock;
+            t[u] = k < n ? __ldcg(src + k) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int k = k0 + u * kSweepBlock;
+            if (k < n) dst[k] = t[u];
+        }
+    }
+}
+
+// One warp: dot products of 8 staged rows with the shared vector v.  Row k
+// holds the entries of v[lo_k, hi_k) at p_k.  Lanes stride v (each v[t] read
+// once for the 8 rows), then a butterfly transpose-reduction (7 + 2 shuffles
+// for 8 rows, fixed order).  Returns the row sum in the lanes with
+// (lane & 3) == 0; *krow = which of the 8 rows.
+__device__ __forceinline__ double rows8_dot(const double *const p[8], const int lo[8], const int hi[8],
+                                            const double *v, int lane, int *krow) {
+    int tmin = lo[0], tmax = hi[0];
+#pragma unroll
+    for (int k = 1; k < 8; ++k) {
+        tmin = min(tmin, lo[k]);
+        tmax = max(tmax, hi[k]);
     }
     double acc[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) acc[k] = 0.0;
-    for (int c = lane; c < maxlen; c += 32) {
-        const double xc = xs[c];
+    for (int t = tmin + lane; t < tmax; t += 32) {
+        const double vt = v[t];
 #pragma unroll
         for (int k = 0; k < 8; ++k)
-            if (c < len[k]) acc[k] += rp[k][c] * xc;
+            if (t >= lo[k] && t < hi[k]) acc[k] += p[k][t - lo[k]] * vt;
     }
     const bool b16 = lane & 16, b8 = lane & 8, b4 = lane & 4;
 #pragma unroll
@@ -212,48 +205,88 @@ __device__ __forceinline__ double rows8_dot(const double *stage, int64_t o0, int
         const double keep = b4 ? acc[1] : acc[0];
         acc[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
     }
-    double v = acc[0];
-    v += __shfl_xor_sync(0xffffffffu, v, 2);
-    v += __shfl_xor_sync(0xffffffffu, v, 1);
+    double r = acc[0];
+    r += __shfl_xor_sync(0xffffffffu, r, 2);
+    r += __shfl_xor_sync(0xffffffffu, r, 1);
     *krow = (b16 ? 4 : 0) + (b8 ? 2 : 0) + (b4 ? 1 : 0);
-    return v;
+    return r;
 }
 
+__device__ __forceinline__ double lower_input(const SweepArgs &A, int row) {
+    return __ldcg(A.in + (A.in_perm ? A.in_perm[row] : row));  // may be produced in-kernel (L2)
+}
+
+// Strided per-thread loops with their global loads issued in batches of 4
+// (the loads of one batch are independent; results land in shared memory).
+// dst[j] = f(j) for j = tid, tid + 256, ... < n
+template <class F>
+__device__ __forceinline__ void batched(int n, F f) {
+    constexpr int U = 4;
+    for (int j0 = threadIdx.x; j0 < n; j0 += U * kSweepBlock) {
+        double t[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int j = j0 + u * kSweepBlock;
+            if (j < n) t[u] = f.load(j);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int j = j0 + u * kSweepBlock;
+            if (j < n) f.store(j, t[u]);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// lower sweep: L y = r   (column-major pre-accumulation, one GEMV per block)
+//   item (b, rows [r0, r1) of G_b): stage the rows by TMA and the block's
+//   input before the wait, form x_b = input - contributions, then
+//       triangle row i:  y_i = x_i + sum_{j<i} Linv_ij x_j          -> x[start+i]
+//       M row k:         c_k = sum_j M_kj x_j                        -> cbuf slot
+//   and count the item on the parent; a mode-2 parent's contribution sums
+//   are formed once by the item that completes it.
+// shared memory: [stage][xs max_m][cbs max_cb][offs int32 max_m+2][dsts int32]
+// ---------------------------------------------------------------------------
 template <bool TRACE>
 __device__ __forceinline__ void lower_sweep_body(const tsb_ldlt_desc &D, const SweepArgs &A, double *smem,
                                                  uint64_t &bar, uint32_t &phase) {
     double *stage = smem;
     double *xs = smem + D.stage_doubles;
-    int32_t *offs = reinterpret_cast<int32_t *>(xs + ((D.max_m + 1) & ~1));  // per-row contribution offsets
-    int32_t *dsts = offs + ((D.max_m + 2) & ~1);                             // cbuf slots of the M rows
+    double *cbs = xs + ((D.max_m + 1) & ~1);
+    int32_t *offs = reinterpret_cast<int32_t *>(cbs + ((D.max_cb + 1) & ~1));
+    int32_t *dsts = offs + ((D.max_m + 2) & ~1);
     __shared__ int item_id, fin_parent;
-    __shared__ int64_t qbase;
     int32_t *ctl = D.d_ctl;
     int64_t *const tbuf = TRACE ? D.d_trace_lower : nullptr;  // folds away when off
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const LItem *items = reinterpret_cast<const LItem *>(D.d_items_lower);
+    const Item *items = reinterpret_cast<const Item *>(D.d_items_lower);
     while (true) {
         if (tid == 0) item_id = atomicAdd(ctl, 1);
         __syncthreads();
         const int iid = item_id;
         if (iid >= D.n_items_lower) break;
         trace(tbuf, iid, 0);
-        const LItem it = items[iid];
+        const Item it = items[iid];
         const tsb_ldlt_block B = D.d_blocks[it.block];
         const int m = B.m, s = B.start, nr = it.r1 - it.r0;
         const int64_t o0 = g_row_off(it.r0, m);
-        const double *gb = D.d_g + B.g_off;
         // everything that does not depend on the sweep's progress is fetched
         // before the wait: the factor rows (TMA), the block's input, the slots
-        if (tid == 0) tma_load_1d(stage, gb + o0, (uint32_t)((g_row_off(it.r1, m) - o0) * 8), &bar);
-        for (int j = tid; j < m; j += kSweepBlock) xs[j] = lower_input(A, s + j);
+        if (tid == 0) tma_load_1d(stage, D.d_g + B.g_off + o0, (uint32_t)((g_row_off(it.r1, m) - o0) * 8), &bar);
+        {
+            struct In {
+                const SweepArgs &A;
+                double *xs;
+                int s;
+                __device__ double load(int j) const { return lower_input(A, s + j); }
+                __device__ void store(int j, double v) const { xs[j] = v; }
+            };
+            batched(m, In{A, xs, s});
+        }
         const int mr0 = max(it.r0, m);
         for (int j = mr0 + tid; j < it.r1; j += kSweepBlock) dsts[j - mr0] = __ldg(D.d_cslot + B.anc_off + (j - m));
-        if (B.mode == 1) {
-            const int64_t q0 = __ldg(D.d_cin_ptr + s);
-            for (int j = tid; j <= m; j += kSweepBlock) offs[j] = (int32_t)(__ldg(D.d_cin_ptr + s + j) - q0);
-            if (tid == 0) qbase = q0;
-        }
+        if (B.mode == 1)
+            for (int j = tid; j <= m; j += kSweepBlock) offs[j] = (int32_t)(__ldg(D.d_cin_ptr + s + j) - B.cb_off);
         if (tid == 0) {
             if (B.mode == 1) spin_until_geq(D.d_cnt_l + it.block, B.target_l);
             else if (B.mode == 2) spin_until_geq(D.d_ready_l + it.block, 1);
@@ -262,18 +295,35 @@ __device__ __forceinline__ void lower_sweep_body(const tsb_ldlt_desc &D, const S
         trace(tbuf, iid, 1);
         // x_b = input - (contributions of the descendants)
         if (B.mode == 1) {
-            const double *cb = D.d_cbuf + qbase;
-            for (int j = tid; j < m; j += kSweepBlock) xs[j] = xs[j] - contrib_sum(cb, offs[j], offs[j + 1]);
+            stage_copy(cbs, D.d_cbuf + B.cb_off, B.ncb);
+            __syncthreads();
+            for (int j = tid; j < m; j += kSweepBlock) xs[j] = xs[j] - contrib_sum<false>(cbs, offs[j], offs[j + 1]);
         } else if (B.mode == 2) {
-            for (int j = tid; j < m; j += kSweepBlock) xs[j] = xs[j] - __ldcg(D.d_x + s + j);
+            struct Sub {
+                const double *src;
+                double *xs;
+                __device__ double load(int j) const { return __ldcg(src + j); }
+                __device__ void store(int j, double v) const { xs[j] = xs[j] - v; }
+            };
+            batched(m, Sub{D.d_x + s, xs});
         }
         mbar_wait(&bar, phase);
         phase ^= 1;
         __syncthreads();
         trace(tbuf, iid, 4);
         for (int j0 = warp * 8; j0 < nr; j0 += 8 * (kSweepBlock / 32)) {  // warp-uniform trips
+            const double *p[8];
+            int lo[8], hi[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const bool ok = j0 + k < nr;
+                const int r = it.r0 + (ok ? j0 + k : 0);
+                lo[k] = 0;
+                hi[k] = ok ? (r < m ? r : m) : 0;
+                p[k] = stage + (g_row_off(r, m) - o0);
+            }
             int k;
-            const double a = rows8_dot(stage, o0, it.r0, j0, nr, m, xs, lane, &k);
+            const double a = rows8_dot(p, lo, hi, xs, lane, &k);
             const int j = j0 + k;
             if ((lane & 3) == 0 && j < nr) {
                 const int r = it.r0 + j;
@@ -299,13 +349,12 @@ __device__ __forceinline__ void lower_sweep_body(const tsb_ldlt_desc &D, const S
         }
         __syncthreads();
         if (fin_parent >= 0) {
-            // Every child item is done: S_parent = sum of its rows' contributions
-            // (row-contiguous in cbuf).  Stage them piece by piece with coalesced
-            // loads (all in flight at once) together with the per-row offsets,
-            // then one thread per row sums its slots in order.
+            // Every child item is done: the parent's contribution sums, formed once
+            // here (row-contiguous in cbuf; staged piece by piece with coalesced loads
+            // together with the per-row offsets, one thread per row sums in order).
             const tsb_ldlt_block P = D.d_blocks[fin_parent];
             int32_t *fo = reinterpret_cast<int32_t *>(xs);  // free: this item's GEMV is done
-            const int64_t qe = __ldg(D.d_cin_ptr + P.start + P.m);
+            const int64_t qe = P.cb_off + P.ncb;
             int i0 = 0;
             while (i0 < P.m) {
                 const int64_t qb = __ldg(D.d_cin_ptr + P.start + i0);
@@ -320,44 +369,13 @@ __device__ __forceinline__ void lower_sweep_body(const tsb_ldlt_desc &D, const S
                 }
                 const int cnt = (int)(__ldg(D.d_cin_ptr + P.start + i1) - qb);
                 const bool staged = cnt <= D.stage_doubles;
-                if (staged) {
-                    constexpr int U = 8;
-                    for (int k0 = tid; k0 < cnt; k0 += U * kSweepBlock) {
-                        double t[U];
-#pragma unroll
-                        for (int u = 0; u < U; ++u) {
-                            const int k = k0 + u * kSweepBlock;
-                            t[u] = k < cnt ? __ldcg(D.d_cbuf + qb + k) : 0.0;
-                        }
-#pragma unroll
-                        for (int u = 0; u < U; ++u) {
-                            const int k = k0 + u * kSweepBlock;
-                            if (k < cnt) stage[k] = t[u];
-                        }
-                    }
-                }
+                if (staged) stage_copy(stage, D.d_cbuf + qb, cnt);
                 for (int i = i0 + tid; i <= i1; i += kSweepBlock)
                     fo[i - i0] = (int32_t)(__ldg(D.d_cin_ptr + P.start + i) - qb);
                 __syncthreads();
-                for (int i = i0 + tid; i < i1; i += kSweepBlock) {
-                    const int a0 = fo[i - i0], a1 = fo[i - i0 + 1];
-                    double c0 = 0.0, c1 = 0.0;
-                    int q = a0;
-                    if (staged) {
-                        for (; q + 1 < a1; q += 2) {
-                            c0 += stage[q];
-                            c1 += stage[q + 1];
-                        }
-                        if (q < a1) c0 += stage[q];
-                    } else {  // a single row with more contributions than the buffer
-                        for (; q + 1 < a1; q += 2) {
-                            c0 += __ldcg(D.d_cbuf + qb + q);
-                            c1 += __ldcg(D.d_cbuf + qb + q + 1);
-                        }
-                        if (q < a1) c0 += __ldcg(D.d_cbuf + qb + q);
-                    }
-                    D.d_x[P.start + i] = c0 + c1;
-                }
+                for (int i = i0 + tid; i < i1; i += kSweepBlock)
+                    D.d_x[P.start + i] = staged ? contrib_sum<false>(stage, fo[i - i0], fo[i - i0 + 1])
+                                                : contrib_sum<true>(D.d_cbuf + qb, fo[i - i0], fo[i - i0 + 1]);
                 __syncthreads();
                 i0 = i1;
             }
@@ -372,123 +390,87 @@ __device__ __forceinline__ void lower_sweep_body(const tsb_ldlt_desc &D, const S
 }
 
 // ---------------------------------------------------------------------------
-// upper sweep: L^T z = w   (row-major pull)
+// upper sweep: L^T z = w   (row-major pull, one GEMV per block)
 //   z_b = w_b + G_b^T v,  v = [w_b ; -z_anc]
-//   item (b, slab, G rows [ra, rb)): partial sums of the slab's columns over
-//   the tile rows (cp.async-staged before the wait; triangle-only tiles have
-//   no dependency, M tiles wait for the parent's z); the last tile of a slab
-//   adds the partials in tile order and publishes z for the slab's columns.
-// shared memory: [stage tile_rows x sw][v max_tile_rows][red 256]
+//   item (b, rows [c0, c1) of G_b^T = columns of G_b): stage the rows by TMA
+//   and w_b before the wait (only -z_anc depends on the parent), then
+//   z_c = v_c + sum_{t > c} G^T[c][t] v_t for the item's columns.
+// shared memory: [stage][v max_v]
 // ---------------------------------------------------------------------------
 template <bool TRACE>
 __device__ __forceinline__ void upper_sweep_body(const tsb_ldlt_desc &D, const SweepArgs &A, double *smem,
                                                  uint64_t &bar, uint32_t &phase) {
-    (void)bar;
-    (void)phase;
     double *stage = smem;
     double *v = smem + D.stage_doubles;
-    double *red = v + ((D.max_tile_rows + 1) & ~1);
-    int32_t *ancs = reinterpret_cast<int32_t *>(red + kSweepBlock);
-    __shared__ int item_id, last;
+    __shared__ int item_id;
     int32_t *ctl = D.d_ctl + 2;
     int64_t *const tbuf = TRACE ? D.d_trace_upper : nullptr;
-    const int tid = threadIdx.x;
-    const UItem *items = reinterpret_cast<const UItem *>(D.d_items_upper);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const Item *items = reinterpret_cast<const Item *>(D.d_items_upper);
     while (true) {
         if (tid == 0) item_id = atomicAdd(ctl, 1);
         __syncthreads();
         const int iid = item_id;
         if (iid >= D.n_items_upper) break;
         trace(tbuf, iid, 0);
-        const UItem it = items[iid];
+        const Item it = items[iid];
         const tsb_ldlt_block B = D.d_blocks[it.block];
-        const int m = B.m, s = B.start, sw = B.sw, nr = it.rb - it.ra;
-        const int c0 = (it.slab - B.slab_base) * sw;
-        const int cw = min(sw, m - c0);
-        const double *gb = D.d_g + B.g_off;
-        // stage G[ra:rb, c0:c0+sw) (16-byte pieces; missing triangle entries -> 0)
-        {
-            const int pr = sw >> 1;
-            for (int q = tid; q < nr * pr; q += kSweepBlock) {
-                const int rr = q / pr, pc = (q - rr * pr) * 2;
-                const int r = it.ra + rr, c = c0 + pc;
-                double *dst = stage + rr * sw + pc;
-                const int lim = r < m ? r : c0 + cw;  // triangle row r stores columns < r
-                if (c < lim)
-                    cp_async16(dst, gb + g_row_off(r, m) + c);
-                else
-                    dst[0] = dst[1] = 0.0;
-            }
-            cp_async_commit();
+        const int m = B.m, s = B.start, na = B.na, K = m + na - 1, nr = it.r1 - it.r0;
+        const int64_t o0 = gt_row_off(it.r0, K);
+        if (tid == 0) tma_load_1d(stage, D.d_gt + B.gt_off + o0, (uint32_t)((gt_row_off(it.r1, K) - o0) * 8), &bar);
+        for (int t = it.r0 + tid; t < m; t += kSweepBlock) {  // w_b: produced before this sweep
+            double w = __ldcg(A.in + s + t);
+            if (A.dscale) w = w / A.dscale[s + t];
+            v[t] = w;
         }
-        // the triangle rows' values and the M rows' ancestor indices do not
-        // depend on the sweep: fetch them before the wait
-        for (int j = tid; j < nr; j += kSweepBlock) {
-            const int r = it.ra + j;
-            if (r < m) {
-                double vj = __ldcg(A.in + s + r);  // produced earlier in the same (persistent) kernel
-                if (A.dscale) vj = vj / A.dscale[s + r];
-                v[j] = vj;
-            } else {
-                ancs[j] = __ldg(D.d_anc + B.anc_off + (r - m));
-            }
-        }
-        if (it.has_dep && tid == 0) spin_until_geq(D.d_done_u + B.parent, D.d_blocks[B.parent].nslabs);
+        for (int k = tid; k < na; k += kSweepBlock)  // ancestor rows, parked in v until the wait is over
+            v[m + k] = __longlong_as_double((long long)__ldg(D.d_anc + B.anc_off + k));
+        if (na > 0 && tid == 0) spin_until_geq(D.d_done_u + B.parent, D.d_blocks[B.parent].n_u);
         __syncthreads();
         trace(tbuf, iid, 1);
-        if (it.has_dep)
-            for (int j = tid; j < nr; j += kSweepBlock)
-                if (it.ra + j >= m) v[j] = -__ldcg(A.x + ancs[j]);
-        cp_async_wait_all();
+        {
+            struct Anc {
+                const double *x;
+                double *va;
+                __device__ double load(int k) const { return __ldcg(x + __double_as_longlong(va[k])); }
+                __device__ void store(int k, double z) const { va[k] = -z; }
+            };
+            batched(na, Anc{A.x, v + m});
+        }
+        mbar_wait(&bar, phase);
+        phase ^= 1;
         __syncthreads();
         trace(tbuf, iid, 4);
-        {
-            const int cc = tid % sw, g = tid / sw, ng = kSweepBlock / sw;
-            double a0 = 0.0, a1 = 0.0;
-            int j = g;
-            for (; j + ng < nr; j += 2 * ng) {
-                a0 += stage[j * sw + cc] * v[j];
-                a1 += stage[(j + ng) * sw + cc] * v[j + ng];
+        for (int j0 = warp * 8; j0 < nr; j0 += 8 * (kSweepBlock / 32)) {
+            const double *p[8];
+            int lo[8], hi[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const bool ok = j0 + k < nr;
+                const int c = it.r0 + (ok ? j0 + k : 0);
+                lo[k] = c + 1;
+                hi[k] = ok ? K + 1 : c + 1;
+                p[k] = stage + (gt_row_off(c, K) - o0);
             }
-            if (j < nr) a0 += stage[j * sw + cc] * v[j];
-            red[tid] = a0 + a1;
-            __syncthreads();
-            if (tid < cw) {
-                double p = 0.0;
-                for (int q = 0; q < ng; ++q) p += red[q * sw + tid];
-                D.d_part[D.d_slab_part[it.slab] + (int64_t)it.tile * sw + tid] = p;
+            int k;
+            const double a = rows8_dot(p, lo, hi, v, lane, &k);
+            const int j = j0 + k;
+            if ((lane & 3) == 0 && j < nr) {
+                const int c = it.r0 + j;
+                const double z = v[c] + a;
+                A.x[s + c] = z;
+                if (A.out_perm) A.out[A.out_perm[s + c]] = z;
             }
         }
         trace(tbuf, iid, 5);
         __syncthreads();
         if (tid == 0) {
             __threadfence();
-            last = atomicAdd(D.d_cnt_s + it.slab, 1) == D.d_slab_ntiles[it.slab] - 1;
-            if (last) __threadfence();
-        }
-        __syncthreads();
-        if (last) {  // all tiles of the slab are in: z = w + partials (tile order)
-            if (tid < cw) {
-                const int nt = D.d_slab_ntiles[it.slab];
-                const double *pp = D.d_part + D.d_slab_part[it.slab] + tid;
-                double acc = 0.0;
-                for (int t = 0; t < nt; ++t) acc += __ldcg(pp + (int64_t)t * sw);
-                const int row = s + c0 + tid;
-                double w = __ldcg(A.in + row);
-                if (A.dscale) w = w / A.dscale[row];
-                const double z = w + acc;
-                A.x[row] = z;
-                if (A.out_perm) A.out[A.out_perm[row]] = z;
-            }
-            __syncthreads();
-            if (tid == 0) {
-                __threadfence();
-                atomicAdd(D.d_done_u + it.block, 1);
-            }
+            atomicAdd(D.d_done_u + it.block, 1);
         }
         trace(tbuf, iid, 2);
     }
-    sweep_exit(ctl, D.d_cnt_s, D.n_slabs, D.d_done_u, D.n_blocks);
+    sweep_exit(ctl, D.d_done_u, D.n_blocks, D.d_pad, 0);
 }
 
 }  // namespace tsb

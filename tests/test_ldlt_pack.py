@@ -78,36 +78,20 @@ def emulate_upper(H, w):
     n, nb = H["n"], H["nb"]
     blocks = H["blocks"]
     z = np.zeros(n)
-    part = np.zeros(max(H["npart"], 1))
-    cnt_s = np.zeros(H["n_slabs"], dtype=np.int64)
     done = np.zeros(nb, dtype=np.int64)
-    for b, slab, ra, rb, tile, has_dep, _, _ in H["items_u"]:
+    for b, c0, c1, _ in H["items_u"]:
         B = blocks[b]
-        s, m, sw = int(B["start"]), int(B["m"]), int(B["sw"])
-        g, off, _, _ = _g(H, b)
-        c0 = (slab - int(B["slab_base"])) * sw
-        cw = min(sw, m - c0)
-        if has_dep:
+        s, m, na = int(B["start"]), int(B["m"]), int(B["na"])
+        toff = K.gt_row_offsets(m, na)
+        gt = H["gt"][B["gt_off"]: B["gt_off"] + toff[-1]]
+        if na:
             p = int(B["parent"])
-            assert done[p] == blocks[p]["nslabs"], "upper M tile dispatched before the parent's z"
-        acc = np.zeros(cw)
-        for row in range(ra, rb):
-            if row < m:
-                v = w[s + row]
-                hi = min(c0 + cw, row)
-                if hi > c0:
-                    acc[: hi - c0] += g[off[row] + c0: off[row] + hi] * v
-            else:
-                v = -z[H["anc"][B["anc_off"] + row - m]]
-                acc += g[off[row] + c0: off[row] + c0 + cw] * v
-        part[H["slab_part"][slab] + tile * sw: H["slab_part"][slab] + tile * sw + cw] = acc
-        cnt_s[slab] += 1
-        if cnt_s[slab] == H["slab_ntiles"][slab]:
-            nt = int(H["slab_ntiles"][slab])
-            tot = sum(part[H["slab_part"][slab] + t * sw: H["slab_part"][slab] + t * sw + cw] for t in range(nt))
-            z[s + c0: s + c0 + cw] = w[s + c0: s + c0 + cw] + tot
-            done[b] += 1
-    assert np.all(done == blocks["nslabs"])
+            assert done[p] == blocks[p]["n_u"], "upper item dispatched before the parent's z"
+        v = np.concatenate([w[s:s + m], -z[H["anc"][B["anc_off"]: B["anc_off"] + na]]])
+        for c in range(c0, c1):
+            z[s + c] = v[c] + gt[toff[c]: toff[c] + (m + na - 1 - c)] @ v[c + 1:]
+        done[b] += 1
+    assert np.all(done == blocks["n_u"])
     return z
 
 
@@ -149,8 +133,36 @@ def test_block_layout_roundtrip_and_coverage():
         rows = sorted((r0, r1) for bb, r0, r1, _ in H["items_l"] if bb == b)
         assert rows[0][0] == 0 and rows[-1][1] == B["m"] + B["na"]
         assert all(a[1] == c[0] for a, c in zip(rows, rows[1:]))
-    # every slab has at least one tile and the tile ids are 0..ntiles-1
-    for sid in range(H["n_slabs"]):
-        t = sorted(x[4] for x in H["items_u"] if x[1] == sid)
-        assert t == list(range(H["slab_ntiles"][sid]))
+    # upper items cover each block's columns exactly once; G^T is G transposed
+    for b, bf in enumerate(f.blocks):
+        B = H["blocks"][b]
+        m, na = int(B["m"]), int(B["na"])
+        cols = sorted((c0, c1) for bb, c0, c1, _ in H["items_u"] if bb == b)
+        assert cols[0][0] == 0 and cols[-1][1] == m and all(a[1] == c[0] for a, c in zip(cols, cols[1:]))
+        toff = K.gt_row_offsets(m, na)
+        gt = H["gt"][B["gt_off"]: B["gt_off"] + toff[-1]]
+        linv, mm = K.block_matrix(bf)
+        full = np.vstack([np.tril(linv, -1), mm])
+        for c in range(m):
+            assert np.array_equal(gt[toff[c]: toff[c] + m + na - 1 - c], full[c + 1:, c])
+        assert np.all(toff % 2 == 0)
     assert H["g"].size == sum(len(_g(H, b)[0]) for b in range(H["nb"]))
+
+
+def test_device_row_offset_formulas():
+    """The closed forms in csrc (g_row_off, gt_row_off) equal the packer's offsets."""
+    def g_row_off(r, m):
+        return (r * r) >> 1 if r < m else ((m * m) >> 1) + (r - m) * (m + (m & 1))
+
+    def gt_row_off(c, K):
+        if c <= 0:
+            return 0
+        a = K - c + 1
+        return ((K + a) * (K - a + 1)) // 2 + ((K + 1) >> 1) - (a >> 1)
+
+    for m in (1, 2, 3, 7, 16, 33, 128):
+        for na in (0, 1, 5, 64):
+            off = K.row_offsets(m, na)
+            assert [g_row_off(r, m) for r in range(m + na + 1)] == off.tolist()
+            toff = K.gt_row_offsets(m, na)
+            assert [gt_row_off(c, m + na - 1) for c in range(m + 1)] == toff.tolist()

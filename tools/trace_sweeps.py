@@ -116,7 +116,8 @@ def main():
         "n": H["n"], "grid_note": "persistent grid = SMs x resident CTAs",
         "lower": summarize(dev.trace_l.cpu().numpy(), (H["blocks"]["target_l"][H["items_l"][:, 0]] > 0).astype(int),
                            {0: "leaf", 1: "inner"}),
-        "upper": summarize(dev.trace_u.cpu().numpy(), H["items_u"][:, 5], {0: "tri", 1: "M"}),
+        "upper": summarize(dev.trace_u.cpu().numpy(), (H["blocks"]["na"][H["items_u"][:, 0]] > 0).astype(int),
+                           {0: "root", 1: "inner"}),
         "lower_chain": lower_chain(dev.trace_l.cpu().numpy(), H["items_l"], H),
     }
     txt = json.dumps(report, indent=1)
