@@ -51,7 +51,8 @@ int tsb_last_error(char *buf, size_t len);
 /* Number of kernels libtsb launched in this process (for bench evidence). */
 int64_t tsb_launch_count(void);
 /* sizeof of the ABI structs (0 asm_plan, 1 asm_coeffs, 2 ldlt_block,
- * 3 ldlt_desc, 4 report) so bindings can verify their layouts; -1 = unknown. */
+ * 3 ldlt_desc, 4 report, 5 ldlt_tile) so bindings can verify their layouts;
+ * -1 = unknown. */
 int64_t tsb_struct_size(int32_t which);
 
 /* ------------------------------------------------------------------------
@@ -159,28 +160,31 @@ int tsb_element_blocks(const tsb_asm_plan *plan, const tsb_asm_coeffs *coeffs,
  * ---------------------------------------------------------------------- */
 /* Block-inverse layout (built by the host from LdlFactors, _ldlt_pack.py).
  * For every dissection block b (permuted rows [start, start+m), ancestors
- * anc[0..na)) the host stores
+ * anc[0..na)) the host forms
  *     G_b = [ inv(L11) - I   (strict lower triangle, rows 1..m-1)      ]
  *           [ M = L21 inv(L11)  (na x m)                               ]
  * -- the reference's tile inverses (ndprecond.py:575-587) widened to the
- * whole diagonal block, with the coupling panel pre-multiplied by it -- once
- * row-major for the lower sweep and once transposed for the upper sweep:
+ * whole diagonal block, with the coupling panel pre-multiplied by it:
  *   lower (solve_lower, ndprecond.py:647-671):  y_b = x_b + (Linv-I) x_b,
  *          contributions to the ancestors  c_b = M x_b  (column-major
  *          pre-accumulation of the paper, one GEMV per block, no in-block chain);
  *   upper (solve_upper, ndprecond.py:674-691):  z_b = w_b + G_b^T v,
  *          v = [w_b; -z_anc]  (row-major pull, one GEMV per block).
- * Row r of G_b (lower) starts at g_off + off(r): off(r) = r*r/2 for triangle
- * rows (row r holds columns [0, r), padded to even), m*m/2 + (r-m)*ms for the
- * M rows (columns [0, m), ms = m rounded up to even).  Row c of G_b^T (upper)
- * holds v-entries [c+1, m+na) (length K-c, K = m+na-1, padded to even) at
- * gt_off + sum_{j=K-c+1..K} (j + (j & 1)).  Every row is 16-byte aligned.
- * Items (int4 {block, r0, r1, 0}): rows [r0, r1) of G_b (lower) or G_b^T
- * (upper), each staged by one TMA bulk copy issued before the dependency wait.
+ * Each sweep's rows (lower: rows of G_b over v = x_b; upper: rows of G_b^T
+ * over v = [w_b; -z_anc]) are grouped in tiles of 32 rows, one per lane:
+ * tile i covers v-columns [tl, tl + 2 np) (tl even) and stores entry
+ * (row row0 + k, column tl + 2p + h) at off + (p*32 + k)*2 + h (zeros
+ * outside the row's range), so a warp reads 512 contiguous bytes per column
+ * pair and every lane accumulates its own row.
+ * Items (int4 {block, t0, t1, seg}): tiles [t0, t1) of one block, staged by
+ * one TMA bulk copy (<= 48 KB) issued before the dependency wait, one warp
+ * per tile; seg = s + 1: column segment s (48 KB) of one large tile, the 8
+ * warps splitting its pairs; the tile's last segment to finish adds the
+ * segments' partial sums in segment order (deterministic) and emits.
  * Lower: x_b = r_b - (contributions of its descendants), summed in a fixed
- * order either by each of the block's items (mode 1) or once by the child item
- * that completes the block (mode 2).  Upper: an item of b waits for every
- * item of b's parent (z_anc final). */
+ * order either by each of the block's items (mode 1) or once by the child
+ * item that completes the block (mode 2).  Upper: an item of b waits for
+ * every item of b's parent (z_anc final). */
 typedef struct tsb_ldlt_block {
     int32_t start, m, na, parent;   /* parent: block elimination-tree parent, -1 = root */
     int32_t target_l;               /* lower items of all children (x_b complete)  */
@@ -189,28 +193,35 @@ typedef struct tsb_ldlt_block {
                                        1 every item sums the contributions itself,
                                        2 the last child item sums them once       */
     int32_t ncb;                    /* contributions into the block's rows         */
-    int64_t g_off;                  /* offset of G_b in d_g (doubles, even)        */
-    int64_t gt_off;                 /* offset of G_b^T in d_gt                     */
     int64_t anc_off;                /* offset of the block's anc rows in d_anc      */
     int64_t cb_off;                 /* first cbuf slot of the block's rows          */
 } tsb_ldlt_block;
+
+typedef struct tsb_ldlt_tile {
+    int64_t off;                    /* offset of the tile in d_g / d_gt (doubles)  */
+    int32_t tl;                     /* first v-column (even)                        */
+    int32_t np;                     /* column pairs                                 */
+    int32_t row0, nrows;            /* block rows [row0, row0 + nrows)              */
+    int32_t nseg;                   /* 0: small tile; else 48 KB column segments   */
+    int32_t part;                   /* first partial-sum slot (x 32 doubles)        */
+} tsb_ldlt_tile;
 
 typedef struct tsb_ldlt_desc {
     int64_t n;
     int64_t n_blocks;
     int64_t n_items_lower;
     int64_t n_items_upper;
-    int32_t stage_doubles;        /* staging buffer (doubles), >= any item's rows   */
     int32_t max_m;                /* largest block                                  */
     int32_t max_v;                /* largest m + na                                 */
-    int32_t max_cb;               /* largest ncb of a mode-1 block                  */
+    int32_t max_cb;               /* contribution staging (doubles, <= 4096)        */
     int32_t grid;                 /* persistent CTAs (0 = fill the GPU)             */
-    int32_t pad_;
     const tsb_ldlt_block *d_blocks;
     const int32_t *d_items_lower; /* [n_items_lower][4], topological dispatch order */
     const int32_t *d_items_upper; /* [n_items_upper][4]                            */
-    const double *d_g;            /* all G_b (row-major)                           */
-    const double *d_gt;           /* all G_b^T                                     */
+    const tsb_ldlt_tile *d_tiles_lower;
+    const tsb_ldlt_tile *d_tiles_upper;
+    const double *d_g;            /* lower tiles                                    */
+    const double *d_gt;           /* upper tiles                                    */
     const int32_t *d_anc;         /* permuted ancestor rows, per block             */
     const int32_t *d_cslot;       /* cbuf slot of (block, anc k)                    */
     const int64_t *d_cin_ptr;     /* [n+1]: row r's contributions are cbuf[cin_ptr[r]..cin_ptr[r+1]) */
@@ -221,6 +232,11 @@ typedef struct tsb_ldlt_desc {
     double *d_y;                  /* scratch [n]: lower result inside apply         */
     int32_t *d_cnt_l, *d_ready_l; /* [n_blocks] counters (zeroed; reset on exit)    */
     int32_t *d_done_u, *d_pad;    /* [n_blocks]                                     */
+    double *d_part_lower;         /* scratch: segment partial sums (32 per slot)    */
+    double *d_part_upper;
+    int32_t *d_tcnt_lower;        /* [n_tiles_lower] segment counters (zeroed)      */
+    int32_t *d_tcnt_upper;        /* [n_tiles_upper]                                */
+    int64_t n_tiles_lower, n_tiles_upper;
     int32_t *d_ctl;               /* [4] tickets / exit counters (zeroed)          */
     int64_t *d_trace_lower;       /* optional [n_items_lower][8] item timeline     */
     int64_t *d_trace_upper;       /* optional [n_items_upper][8]                   */

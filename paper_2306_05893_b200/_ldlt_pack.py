@@ -2,7 +2,7 @@
 
 Runs once per factor refresh (on the AsyncPreconditioner worker thread for
 the async path).  For every dissection block b (rows [start, start+m),
-ancestor rows anc, na = len(anc)) it stores one row-major matrix
+ancestor rows anc, na = len(anc)) the packer forms
 
     G_b = [ inv(L11) - I        strict lower triangle, rows 1..m-1  ]
           [ M = L21 inv(L11)    na x m                              ]
@@ -16,17 +16,26 @@ block's input x_b:
     lower:  y_b = x_b + (Linv - I) x_b,   contributions  c = M x_b
     upper:  z_b = w_b + G_b^T [w_b ; -z_anc]
 
-G_b has exactly the entries of [L11 ; L21] (same bytes per sweep), serves
-both sweeps, and the only serial chain left is the depth of the dissection
-tree.  The factor blocks are well conditioned (cond_1(L11) <= 12.5 on the
-cfg2 beam); the block-inverse apply matches the reference's tile-16 sweeps
-to ~4e-16 relative.
+Both sweeps are therefore GEMVs over rows with a contiguous v-range: lower
+rows r of G_b (v = x_b, columns [0, r) or [0, m)), upper rows c of G_b^T
+(v = [w_b; -z_anc], columns [c+1, m+na)).  The factor blocks are well
+conditioned (cond_1(L11) <= 14 on the cfg2/cfg3 beams); the block-inverse
+apply matches the reference's tile-16 sweeps to ~5e-16 relative.
 
-G_b is stored twice: row-major for the lower sweep and transposed for the
-upper (row c of G_b^T = column c of G_b below the diagonal, i.e. the entries
-multiplying v[c+1:]), so both sweeps are row-chunked GEMVs with one TMA bulk
-copy per work item (~48 KB) and no cross-item reduction.  The
-dispatch order is a list schedule on an infinite machine keyed by each
+Device layout (csrc/ldlt_sweep.cuh): rows are grouped in TILES of 32 (one
+row per lane).  A tile covers the union [tl, th) of its rows' v-ranges (tl
+even) and is stored pair-major, lane-interleaved: entry (row 32i+k, column
+tl+2p+h) at ((p*32 + k)*2 + h) -- a warp reads 512 contiguous bytes per
+pair (conflict-free LDS.128), each lane accumulates its own row, no
+cross-lane reduction.  Entries outside a row's range are stored as zeros
+(the padding is reported as stored vs algorithmic bytes).
+
+Work items: up to 8 consecutive small tiles of a block (one warp each, one
+TMA bulk copy of <= 48 KB) or one 48 KB column segment of a large tile (the
+8 warps split its pairs; the segment's 32 partial sums go to a scratch
+slot and the last segment of the tile to finish adds them in segment
+order -- deterministic -- and emits the rows).
+The dispatch order is a list schedule on an infinite machine keyed by each
 item's earliest start under a simple cost model, ties broken by the longest
 remaining path (critical path first).  Every dependency finishes strictly
 before its dependant starts, so the order is topological -- all the
@@ -41,102 +50,113 @@ import numpy as np
 
 from . import _lib
 
-CHUNK = 6144          # doubles per lower item (48 KB, one TMA bulk copy)
-CHUNK_ROWS = 512      # rows per lower item (csrc kMaxChunkRows)
-CB_MAX = 4096         # contributions a block's items may sum themselves (csrc max_cb)
+TILE = 32               # rows per tile (one per lane)
+ITEM_BYTES = 48 * 1024  # small-tile item budget: one TMA bulk copy
+SEG_PAIRS = 96          # pairs per segment item of a large tile (96 * 32 * 16 B = 48 KB)
+WARPS = 8               # warps per CTA (csrc kSweepBlock / 32)
+CB_CAP = 2048           # contributions staged per piece when a block's items sum them (csrc max_cb)
 
 BLOCK_DTYPE = np.dtype([
     ("start", "<i4"), ("m", "<i4"), ("na", "<i4"), ("parent", "<i4"),
     ("target_l", "<i4"), ("n_u", "<i4"), ("mode", "<i4"), ("ncb", "<i4"),
-    ("g_off", "<i8"), ("gt_off", "<i8"), ("anc_off", "<i8"), ("cb_off", "<i8"),
+    ("anc_off", "<i8"), ("cb_off", "<i8"),
 ])
-assert BLOCK_DTYPE.itemsize == 64
+assert BLOCK_DTYPE.itemsize == 48
+TILE_DTYPE = np.dtype([("off", "<i8"), ("tl", "<i4"), ("np", "<i4"), ("row0", "<i4"), ("nrows", "<i4"),
+                       ("nseg", "<i4"), ("part", "<i4")])
+assert TILE_DTYPE.itemsize == 32
 MODE_LEAF, MODE_GATHER, MODE_FIN = 0, 1, 2
 
 
-def row_offsets(m: int, na: int) -> np.ndarray:
-    """Offsets (doubles) of the m + na + 1 row boundaries of G_b (csrc g_row_off)."""
-    r = np.arange(m + na + 1, dtype=np.int64)
-    ms = m + (m & 1)
-    return np.where(r < m, (r * r) // 2, (m * m) // 2 + (r - m) * ms)
+def block_matrix(bf):
+    """-> (Linv with unit diagonal, M = L21 Linv) of one block factor
+    (LAPACK trtri + BLAS trmm: na m^2 flops for M)."""
+    from scipy.linalg import blas, lapack
+
+    m = bf.stop - bf.start
+    linv, info = lapack.dtrtri(np.asarray(bf.l11, dtype=np.float64), lower=1, unitdiag=1)
+    if info != 0:
+        raise ValueError(f"singular diagonal block at {bf.start}")
+    linv = np.tril(linv, -1)
+    linv[np.diag_indices(m)] = 1.0
+    if len(bf.anc):
+        mm = blas.dtrmm(1.0, linv, np.asfortranarray(bf.l21, dtype=np.float64), side=1, lower=1, diag=1)
+    else:
+        mm = np.zeros((0, m))
+    return linv, mm
 
 
-def gt_row_offsets(m: int, na: int) -> np.ndarray:
-    """Offsets (doubles) of the m + 1 row boundaries of G_b^T (csrc gt_row_off):
-    row c holds v-entries [c+1, m+na), length K - c (K = m+na-1), padded to even."""
-    K = m + na - 1
-    lens = K - np.arange(m, dtype=np.int64)
-    out = np.zeros(m + 1, dtype=np.int64)
-    np.cumsum(lens + (lens & 1), out=out[1:])
+def gfull(linv, mm):
+    """G_b as a dense (m + na) x m matrix: [tril(Linv, -1); M]."""
+    return np.vstack([np.tril(linv, -1), mm])
+
+
+def row_ranges(m: int, na: int, upper: bool):
+    """v-ranges [lo, hi) of the sweep's rows: lower rows of G_b, upper rows of G_b^T."""
+    if upper:
+        c = np.arange(m, dtype=np.int64)
+        return c + 1, np.full(m, m + na, dtype=np.int64)
+    r = np.arange(m + na, dtype=np.int64)
+    return np.zeros(m + na, dtype=np.int64), np.minimum(r, m)
+
+
+def tile_block(G: np.ndarray, m: int, na: int, upper: bool):
+    """Tiles of one block for one sweep -> (list of (tl, np, row0, nrows), data parts).
+
+    G holds the sweep's rows: gfull() for the lower sweep, its transpose for the upper."""
+    lo, hi = row_ranges(m, na, upper)
+    nrows_all = len(lo)
+    tiles, parts = [], []
+    for r0 in range(0, nrows_all, TILE):
+        r1 = min(r0 + TILE, nrows_all)
+        tl = int(lo[r0:r1].min()) & ~1
+        th = int(hi[r0:r1].max())
+        npair = max((th - tl + 1) // 2, 0)
+        d = np.zeros((TILE, 2 * npair))
+        w = th - tl
+        if w > 0:
+            d[: r1 - r0, :w] = G[r0:r1, tl:th]
+        parts.append(d.reshape(TILE, npair, 2).transpose(1, 0, 2).ravel())
+        tiles.append((tl, npair, r0, r1 - r0))
+    return tiles, parts
+
+
+def untile(tiles, data, nrows, ncols):
+    """Inverse of tile_block (testing): dense nrows x ncols from a block's tile rows."""
+    out = np.zeros((nrows, ncols + 2))
+    for off, tl, npair, r0, nr in tiles:
+        d = data[off: off + npair * TILE * 2].reshape(npair, TILE, 2).transpose(1, 0, 2).reshape(TILE, 2 * npair)
+        out[r0:r0 + nr, tl:tl + 2 * npair] = d[:nr]
+    return out[:, :ncols]
+
+
+def _items(tiles_of_block, first_tile):
+    """Group a block's tiles into items -> list of (t0, t1, seg) in global tile ids
+    (seg = 0: whole small tiles; seg = s + 1: column segment s of one large tile)."""
+    out = []
+    k = 0
+    nt = len(tiles_of_block)
+    while k < nt:
+        npair = tiles_of_block[k][1]
+        if npair * TILE * 16 > ITEM_BYTES:
+            for sgi in range((npair + SEG_PAIRS - 1) // SEG_PAIRS):
+                out.append((first_tile + k, first_tile + k + 1, sgi + 1))
+            k += 1
+            continue
+        k1, tot = k, 0
+        while k1 < nt and k1 - k < WARPS:
+            b = tiles_of_block[k1][1] * TILE * 16
+            if b > ITEM_BYTES or tot + b > ITEM_BYTES:
+                break
+            tot += b
+            k1 += 1
+        out.append((first_tile + k, first_tile + k1, 0))
+        k = k1
     return out
 
 
-def block_matrix(bf):
-    """-> (Linv with unit diagonal, M = L21 Linv) of one block factor."""
-    from scipy.linalg import solve_triangular
-
-    m = bf.stop - bf.start
-    linv = solve_triangular(bf.l11, np.eye(m), lower=True, unit_diagonal=True, check_finite=False)
-    mm = bf.l21 @ linv if len(bf.anc) else np.zeros((0, m))
-    return linv, mm
-
-
-def pack_block(bf) -> np.ndarray:
-    """G_b in the device row layout (flat float64, even length)."""
-    linv, mm = block_matrix(bf)
-    return _pack_rows(bf, linv, mm)
-
-
-def _pack_rows(bf, linv, mm):
-    m, na = bf.stop - bf.start, len(bf.anc)
-    off = row_offsets(m, na)
-    g = np.zeros(int(off[-1]))
-    ir, ic = np.tril_indices(m, -1)
-    g[(ir * ir) // 2 + ic] = linv[ir, ic]
-    if na:
-        ms = m + (m & 1)
-        g[off[m]:].reshape(na, ms)[:, :m] = mm
-    return g
-
-
-def pack_block_t(bf, linv=None, mm=None) -> np.ndarray:
-    """G_b^T in the device row layout (flat float64, even length)."""
-    m, na = bf.stop - bf.start, len(bf.anc)
-    if linv is None:
-        linv, mm = block_matrix(bf)
-    full = np.vstack([np.tril(linv, -1), mm]) if na else np.tril(linv, -1)
-    off = gt_row_offsets(m, na)
-    g = np.zeros(int(off[-1]))
-    for c in range(m):
-        col = full[c + 1:, c]
-        g[off[c]: off[c] + len(col)] = col
-    return g
-
-
-def unpack_block(g, m, na):
-    """Inverse of pack_block -> (Linv with unit diagonal, M)."""
-    off = row_offsets(m, na)
-    linv = np.eye(m)
-    ir, ic = np.tril_indices(m, -1)
-    linv[ir, ic] = g[(ir * ir) // 2 + ic]
-    ms = m + (m & 1)
-    mm = g[off[m]:off[-1]].reshape(na, ms)[:, :m] if na else np.zeros((0, m))
-    return linv, mm
-
-
-def _lower_chunks(off, nrows):
-    """Row ranges of G_b with <= CHUNK doubles each (at least one row)."""
-    out, r0 = [], 0
-    while r0 < nrows:
-        r1 = int(np.searchsorted(off, off[r0] + CHUNK, side="right")) - 1
-        r1 = min(max(r1, r0 + 1), nrows, r0 + CHUNK_ROWS)
-        out.append((r0, r1))
-        r0 = r1
-    return out or [(0, 0)]
-
-
 def pack(factors):
-    """Host arrays of the block-inverse layout + item lists (pure NumPy)."""
+    """Host arrays of the tiled block-inverse layout + item lists (pure NumPy)."""
     plan = factors.plan
     n = plan.n
     bfs = list(factors.blocks)
@@ -160,85 +180,99 @@ def pack(factors):
     for i, bf in enumerate(bfs):
         p = parent[i]
         if p >= 0:
-            pb = bfs[p]
             rest = np.asarray(bf.anc)
-            rest = rest[rest >= pb.stop]
-            if len(rest) and not np.all(np.isin(rest, np.asarray(pb.anc))):
+            rest = rest[rest >= bfs[p].stop]
+            if len(rest) and not np.all(np.isin(rest, np.asarray(bfs[p].anc))):
                 raise ValueError("factor structure violates the fill property")
     children = [[] for _ in range(nb)]
     for i in range(nb):
         if parent[i] >= 0:
             children[parent[i]].append(i)
-
     ms_ = np.array([bf.stop - bf.start for bf in bfs], dtype=np.int64)
     na_ = np.array([len(bf.anc) for bf in bfs], dtype=np.int64)
-    # ---------------- G blobs ----------------
-    g_parts, g_off = [], np.zeros(nb, dtype=np.int64)
-    gt_parts, gt_off = [], np.zeros(nb, dtype=np.int64)
-    pos = post = 0
+
+    # ---------------- tiles ----------------
+    tl_rows = {False: [], True: []}       # per sweep: global tile table rows
+    data = {False: [], True: []}
+    pos = {False: 0, True: 0}
+    blk_tiles = {False: [], True: []}     # per sweep, per block: (first tile id, [tiles])
+    from threadpoolctl import threadpool_limits
+
+    big = ms_ * (ms_ + na_) > 1_000_000
+    mats = {}
+    with threadpool_limits(limits=1, user_api="blas"):  # small blocks: thread wake-ups cost more than the math
+        for i in np.flatnonzero(~big):
+            mats[i] = block_matrix(bfs[i])
+    for i in np.flatnonzero(big):
+        mats[i] = block_matrix(bfs[i])
     for i, bf in enumerate(bfs):
-        linv, mm = block_matrix(bf)
-        g = _pack_rows(bf, linv, mm)
-        gt = pack_block_t(bf, linv, mm)
-        g_off[i], gt_off[i] = pos, post
-        g_parts.append(g)
-        gt_parts.append(gt)
-        pos += len(g)
-        post += len(gt)
+        G = gfull(*mats.pop(i))
+        for up in (False, True):
+            tiles, parts = tile_block(G.T if up else G, int(ms_[i]), int(na_[i]), up)
+            blk_tiles[up].append((len(tl_rows[up]), tiles))
+            for (tl, npair, r0, nr), p in zip(tiles, parts):
+                tl_rows[up].append((pos[up], tl, npair, r0, nr))
+                data[up].append(p)
+                pos[up] += len(p)
+    tables = {}
+    npart = {}
+    for up in (False, True):
+        t = np.zeros(len(tl_rows[up]), dtype=TILE_DTYPE)
+        if tl_rows[up]:
+            arr = np.array(tl_rows[up], dtype=np.int64)
+            t["off"], t["tl"], t["np"], t["row0"], t["nrows"] = arr.T
+        big = t["np"].astype(np.int64) * TILE * 16 > ITEM_BYTES
+        t["nseg"] = np.where(big, (t["np"] + SEG_PAIRS - 1) // SEG_PAIRS, 0)
+        part = np.zeros(len(t) + 1, dtype=np.int64)
+        np.cumsum(t["nseg"], out=part[1:])
+        t["part"] = part[:-1]
+        npart[up] = int(part[-1])
+        tables[up] = t
     anc_off = np.zeros(nb + 1, dtype=np.int64)
     np.cumsum(na_, out=anc_off[1:])
     anc_all = (np.concatenate([np.asarray(bf.anc, dtype=np.int64) for bf in bfs]) if anc_off[-1]
                else np.zeros(0, dtype=np.int64))
-    # ---------------- lower items ----------------
-    offs = [row_offsets(int(ms_[i]), int(na_[i])) for i in range(nb)]
-    lchunks = [_lower_chunks(offs[i], int(ms_[i] + na_[i])) for i in range(nb)]
-    nl = np.array([len(c) for c in lchunks], dtype=np.int64)
+
+    # ---------------- items + dispatch order ----------------
+    items = {up: [_items(blk_tiles[up][i][1], blk_tiles[up][i][0]) for i in range(nb)] for up in (False, True)}
+    nl = np.array([len(x) for x in items[False]], dtype=np.int64)
+    n_u = np.array([len(x) for x in items[True]], dtype=np.int64)
     target_l = np.array([sum(int(nl[c]) for c in children[i]) for i in range(nb)], dtype=np.int64)
 
-    def cost(doubles):  # us: item overhead + streaming at ~40 GB/s per CTA
-        return 1.0 + doubles * 8 / 40e3
+    def cost(up, it):  # us: item overhead + streaming at ~40 GB/s per CTA
+        nbytes = min(int(tables[up]["np"][it[0]:it[1]].sum()) * TILE * 16, ITEM_BYTES)
+        return 1.5 + nbytes / 40e3 + (1.0 if it[2] else 0.0)
 
     order = sorted(range(nb), key=lambda i: bfs[i].start)  # children before parents
-    ready_l = np.zeros(nb)
-    done_l = np.zeros(nb)
+    ready_l, done_l = np.zeros(nb), np.zeros(nb)
     for i in order:
         if children[i]:
-            ready_l[i] = max(done_l[c] for c in children[i]) + 1.0 + 0.002 * ms_[i]
-        worst = max(cost(offs[i][r1] - offs[i][r0]) for r0, r1 in lchunks[i])
-        done_l[i] = ready_l[i] + worst
+            ready_l[i] = max(done_l[c] for c in children[i]) + 1.0
+        done_l[i] = ready_l[i] + max(cost(False, it) for it in items[False][i])
     tail_l = np.zeros(nb)
     for i in reversed(order):  # parents first
         tail_l[i] = (done_l[i] - ready_l[i]) + (tail_l[parent[i]] if parent[i] >= 0 else 0.0)
-    lower = []
-    for i in range(nb):
-        for r0, r1 in lchunks[i]:
-            lower.append((ready_l[i], -tail_l[i], bfs[i].start, r0, i, r1))
-    lower.sort()
-    items_l = np.array([(x[4], x[3], x[5], 0) for x in lower], dtype=np.int32).reshape(-1, 4)
-    # ---------------- upper items ----------------
-    toffs = [gt_row_offsets(int(ms_[i]), int(na_[i])) for i in range(nb)]
-    uchunks = [_lower_chunks(toffs[i], int(ms_[i])) for i in range(nb)]
-    n_u = np.array([len(c) for c in uchunks], dtype=np.int64)
-    start_u = np.zeros(nb)
-    done_u = np.zeros(nb)
+    lower = sorted((ready_l[i], -tail_l[i], bfs[i].start, it[0], i, it[1], it[2])
+                   for i in range(nb) for it in items[False][i])
+    items_l = np.array([(x[4], x[3], x[5], x[6]) for x in lower], dtype=np.int32).reshape(-1, 4)
+    start_u, done_u = np.zeros(nb), np.zeros(nb)
     for i in reversed(order):  # parents first
-        start_u[i] = done_u[parent[i]] if parent[i] >= 0 else 0.0
-        done_u[i] = start_u[i] + max(cost(toffs[i][r1] - toffs[i][r0]) for r0, r1 in uchunks[i])
+        start_u[i] = done_u[parent[i]] + 1.0 if parent[i] >= 0 else 0.0
+        done_u[i] = start_u[i] + max(cost(True, it) for it in items[True][i])
     tail_u = np.zeros(nb)
     for i in order:  # children first
         tail_u[i] = (done_u[i] - start_u[i]) + max((tail_u[c] for c in children[i]), default=0.0)
-    upper = []
-    for i in range(nb):
-        for r0, r1 in uchunks[i]:
-            upper.append((start_u[i], -tail_u[i], -bfs[i].start, r0, i, r1))
-    upper.sort()
-    items_u = np.array([(x[4], x[3], x[5], 0) for x in upper], dtype=np.int32).reshape(-1, 4)
+    upper = sorted((start_u[i], -tail_u[i], -bfs[i].start, it[0], i, it[1], it[2])
+                   for i in range(nb) for it in items[True][i])
+    items_u = np.array([(x[4], x[3], x[5], x[6]) for x in upper], dtype=np.int32).reshape(-1, 4)
+
     # ---------------- contribution slots (lower) ----------------
     corder = np.argsort(anc_all, kind="stable")   # row-contiguous, block order within a row
     cin_ptr = np.zeros(n + 1, dtype=np.int64)
     np.cumsum(np.bincount(anc_all, minlength=n), out=cin_ptr[1:])
     cslot = np.empty(len(anc_all), dtype=np.int64)
     cslot[corder] = np.arange(len(anc_all))
+
     # ---------------- block table ----------------
     blocks = np.zeros(nb, dtype=BLOCK_DTYPE)
     blocks["start"] = [bf.start for bf in bfs]
@@ -252,30 +286,24 @@ def pack(factors):
     # item that completes the block sums them once (one extra hop)
     contrib = np.diff(cin_ptr)
     blk_contrib = np.array([int(contrib[bf.start:bf.stop].sum()) for bf in bfs], dtype=np.int64)
-    gsize = np.array([len(g) for g in g_parts], dtype=np.int64)
-    mode = np.where(target_l == 0, MODE_LEAF,
-                    np.where((nl * blk_contrib <= gsize) & (blk_contrib <= CB_MAX), MODE_GATHER, MODE_FIN))
+    gsize = np.array([int(tables[False]["np"][f:f + len(t)].sum()) * TILE * 2 for f, t in blk_tiles[False]],
+                     dtype=np.int64)
+    mode = np.where(target_l == 0, MODE_LEAF, np.where(nl * blk_contrib <= gsize, MODE_GATHER, MODE_FIN))
     blocks["mode"] = mode
     blocks["ncb"] = blk_contrib
     blocks["cb_off"] = cin_ptr[[bf.start for bf in bfs]] if nb else []
-    blocks["gt_off"] = gt_off
-    blocks["g_off"] = g_off
     blocks["anc_off"] = anc_off[:-1]
-    max_lchunk = max(int(offs[i][r1] - offs[i][r0]) for i in range(nb) for r0, r1 in lchunks[i]) if nb else 2
-    max_uchunk = max(int(toffs[i][r1] - toffs[i][r0]) for i in range(nb) for r0, r1 in uchunks[i]) if nb else 2
-    stage = max(max_lchunk, max_uchunk, 2)
-    stage += stage & 1
-    max_cb = int(blk_contrib[mode == MODE_GATHER].max()) if np.any(mode == MODE_GATHER) else 0
+    max_cb = min(CB_CAP, int(blk_contrib[mode == MODE_GATHER].max())) if np.any(mode == MODE_GATHER) else 0
+    cat = lambda parts: np.concatenate(parts) if parts else np.zeros(2)  # noqa: E731
     return {
         "n": n, "nb": nb, "blocks": blocks, "items_l": items_l, "items_u": items_u,
-        "g": np.concatenate(g_parts) if g_parts else np.zeros(2),
-        "gt": np.concatenate(gt_parts) if gt_parts else np.zeros(2),
+        "tiles_l": tables[False], "tiles_u": tables[True], "g": cat(data[False]), "gt": cat(data[True]),
         "anc": anc_all, "cslot": cslot, "cin_ptr": cin_ptr, "ncbuf": len(anc_all),
         "d": np.asarray(factors.d, dtype=np.float64), "perm": np.asarray(plan.perm, dtype=np.int64),
-        "stage": int(stage), "max_m": int(ms_.max()) if nb else 1,
-        "max_v": int((ms_ + na_).max()) if nb else 1, "max_cb": max_cb,
+        "max_m": int(ms_.max()) if nb else 1, "max_v": int((ms_ + na_).max()) if nb else 1, "max_cb": max_cb,
         "parent": parent, "children": children, "mode": mode,
-        "bytes_g": int(pos) * 8, "bytes_gt": int(post) * 8,
+        "npart_l": npart[False], "npart_u": npart[True],
+        "bytes_g": int(pos[False]) * 8, "bytes_gt": int(pos[True]) * 8,
     }
 
 
@@ -289,7 +317,7 @@ class DevicePanels:
             inner = H["blocks"]["mode"] != MODE_LEAF
             H["blocks"]["mode"][inner] = force_mode
             if force_mode == MODE_GATHER:
-                H["max_cb"] = int(H["blocks"]["ncb"][inner].max(initial=0))
+                H["max_cb"] = min(CB_CAP, int(H["blocks"]["ncb"][inner].max(initial=0)))
         n, nb = H["n"], H["nb"]
         items_l, items_u = H["items_l"], H["items_u"]
         self.host = H if trace else None
@@ -303,14 +331,17 @@ class DevicePanels:
             i64 = lambda a: up(np.asarray(a, dtype=np.int64))  # noqa: E731
             z = lambda k, dt: t.zeros(max(k, 1), dtype=dt, device="cuda")  # noqa: E731
             nz = lambda a: a if len(a) else np.zeros(1, dtype=a.dtype)  # noqa: E731
+            raw = lambda a: up(nz(a).view(np.uint8))  # noqa: E731
             self.t = {
-                "blocks": up(H["blocks"].view(np.uint8)), "items_l": up(nz(items_l.ravel())),
-                "items_u": up(nz(items_u.ravel())), "g": up(H["g"]), "gt": up(H["gt"]),
+                "blocks": raw(H["blocks"]), "items_l": up(nz(items_l.ravel())), "items_u": up(nz(items_u.ravel())),
+                "tiles_l": raw(H["tiles_l"]), "tiles_u": raw(H["tiles_u"]), "g": up(H["g"]), "gt": up(H["gt"]),
                 "anc": i32(nz(H["anc"])), "cslot": i32(nz(H["cslot"])), "cin_ptr": i64(H["cin_ptr"]),
                 "d": up(H["d"]), "perm": i32(H["perm"]),
             }
+            ntl, ntu = len(H["tiles_l"]), len(H["tiles_u"])
             self.t.update(cbuf=z(H["ncbuf"], t.float64), x=z(n, t.float64), y=z(n, t.float64),
-                          cnt=z(3 * nb, t.int32), ctl=z(4, t.int32))
+                          part=z(TILE * (H["npart_l"] + H["npart_u"]), t.float64),
+                          cnt=z(3 * nb, t.int32), tcnt=z(ntl + ntu, t.int32), ctl=z(4, t.int32))
         self.n = n
         self.n_blocks = nb
         self.n_items = (len(items_l), len(items_u))
@@ -320,10 +351,14 @@ class DevicePanels:
         cp = lambda a, b: _lib.ptr(cnt[a:b]) if b > a else _lib.ptr(cnt)  # noqa: E731
         self.desc = _lib.LdltDesc(
             n=n, n_blocks=nb, n_items_lower=len(items_l), n_items_upper=len(items_u),
-            stage_doubles=H["stage"], max_m=H["max_m"], max_v=H["max_v"], max_cb=H["max_cb"], grid=0, pad_=0,
-            d_blocks=tp("blocks"), d_items_lower=tp("items_l"), d_items_upper=tp("items_u"), d_g=tp("g"),
-            d_gt=tp("gt"), d_anc=tp("anc"), d_cslot=tp("cslot"), d_cin_ptr=tp("cin_ptr"), d_d=tp("d"),
+            max_m=H["max_m"], max_v=H["max_v"], max_cb=H["max_cb"], grid=0,
+            d_blocks=tp("blocks"), d_items_lower=tp("items_l"), d_items_upper=tp("items_u"),
+            d_tiles_lower=tp("tiles_l"), d_tiles_upper=tp("tiles_u"), d_g=tp("g"), d_gt=tp("gt"),
+            d_anc=tp("anc"), d_cslot=tp("cslot"), d_cin_ptr=tp("cin_ptr"), d_d=tp("d"),
             d_perm=tp("perm"), d_cbuf=tp("cbuf"), d_x=tp("x"), d_y=tp("y"),
+            d_part_lower=tp("part"), d_part_upper=_lib.ptr(self.t["part"][TILE * H["npart_l"]:]),
+            d_tcnt_lower=tp("tcnt"), d_tcnt_upper=_lib.ptr(self.t["tcnt"][ntl:]),
+            n_tiles_lower=ntl, n_tiles_upper=ntu,
             d_cnt_l=cp(0, nb), d_ready_l=cp(nb, 2 * nb), d_done_u=cp(2 * nb, 3 * nb), d_pad=tp("ctl"),
             d_ctl=tp("ctl"),
             d_trace_lower=_lib.ptr(self.trace_l) if trace else None,

@@ -57,12 +57,14 @@ class AsmCoeffs(C.Structure):
 class LdltDesc(C.Structure):
     _fields_ = [
         ("n", c_i64), ("n_blocks", c_i64), ("n_items_lower", c_i64), ("n_items_upper", c_i64),
-        ("stage_doubles", c_i32), ("max_m", c_i32), ("max_v", c_i32), ("max_cb", c_i32),
-        ("grid", c_i32), ("pad_", c_i32),
-        ("d_blocks", c_vp), ("d_items_lower", c_vp), ("d_items_upper", c_vp), ("d_g", c_vp), ("d_gt", c_vp),
+        ("max_m", c_i32), ("max_v", c_i32), ("max_cb", c_i32), ("grid", c_i32),
+        ("d_blocks", c_vp), ("d_items_lower", c_vp), ("d_items_upper", c_vp),
+        ("d_tiles_lower", c_vp), ("d_tiles_upper", c_vp), ("d_g", c_vp), ("d_gt", c_vp),
         ("d_anc", c_vp), ("d_cslot", c_vp), ("d_cin_ptr", c_vp), ("d_d", c_vp), ("d_perm", c_vp),
         ("d_cbuf", c_vp), ("d_x", c_vp), ("d_y", c_vp),
-        ("d_cnt_l", c_vp), ("d_ready_l", c_vp), ("d_done_u", c_vp), ("d_pad", c_vp), ("d_ctl", c_vp),
+        ("d_cnt_l", c_vp), ("d_ready_l", c_vp), ("d_done_u", c_vp), ("d_pad", c_vp),
+        ("d_part_lower", c_vp), ("d_part_upper", c_vp), ("d_tcnt_lower", c_vp), ("d_tcnt_upper", c_vp),
+        ("n_tiles_lower", c_i64), ("n_tiles_upper", c_i64), ("d_ctl", c_vp),
         ("d_trace_lower", c_vp), ("d_trace_upper", c_vp),
     ]
 

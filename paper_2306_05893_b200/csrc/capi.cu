@@ -35,6 +35,7 @@ extern "C" int64_t tsb_struct_size(int32_t which) {
         case 2: return sizeof(tsb_ldlt_block);
         case 3: return sizeof(tsb_ldlt_desc);
         case 4: return sizeof(tsb_report);
+        case 5: return sizeof(tsb_ldlt_tile);
         default: return -1;
     }
 }

@@ -16,8 +16,9 @@
 // the dissection tree (one hop per level).
 // Work items (dispatched in a precomputed topological, critical-path-first
 // order through one atomic ticket counter; every CTA is resident, so an item
-// only ever waits on items dispensed before it) are row chunks of G_b (lower)
-// or G_b^T (upper), each staged by one TMA bulk copy before its wait:
+// only ever waits on items dispensed before it) are tiles of 32 rows of G_b
+// (lower) or G_b^T (upper), lane-interleaved so each lane owns one row, staged
+// by TMA bulk copies issued before the item's wait:
 //   lower  triangle rows give y_b, M rows give the contributions to the
 //          ancestors (column-major pre-accumulation, paper Fig. solveBlock)
 //          written to row-contiguous slots; x_b = input - contributions is
@@ -42,29 +43,35 @@ namespace tsb {
 template <bool TRACE>
 __global__ void __launch_bounds__(kSweepBlock) lower_sweep(tsb_ldlt_desc D, SweepArgs A) {
     extern __shared__ __align__(128) double smem[];
-    __shared__ uint64_t bar;
+    __shared__ uint64_t bars[2];
     if (A.done != nullptr && *((volatile const int32_t *)A.done)) {
-        sweep_exit(D.d_ctl, D.d_cnt_l, D.n_blocks, D.d_ready_l, D.n_blocks);
+        lower_exit(D);
         return;
     }
-    if (threadIdx.x == 0) mbar_init(&bar, 1);
+    if (threadIdx.x == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+    }
     __syncthreads();
     uint32_t phase = 0;
-    lower_sweep_body<TRACE>(D, A, smem, bar, phase);
+    lower_sweep_body<TRACE>(D, A, smem, bars, phase);
 }
 
 template <bool TRACE>
 __global__ void __launch_bounds__(kSweepBlock) upper_sweep(tsb_ldlt_desc D, SweepArgs A) {
     extern __shared__ __align__(128) double smem[];
-    __shared__ uint64_t bar;
+    __shared__ uint64_t bars[2];
     if (A.done != nullptr && *((volatile const int32_t *)A.done)) {
-        sweep_exit(D.d_ctl + 2, D.d_done_u, D.n_blocks, D.d_pad, 0);
+        upper_exit(D);
         return;
     }
-    if (threadIdx.x == 0) mbar_init(&bar, 1);
+    if (threadIdx.x == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+    }
     __syncthreads();
     uint32_t phase = 0;
-    upper_sweep_body<TRACE>(D, A, smem, bar, phase);
+    upper_sweep_body<TRACE>(D, A, smem, bars, phase);
 }
 
 static uint64_t g_serial = 0;
@@ -114,7 +121,7 @@ extern "C" int tsb_ldlt_create(const tsb_ldlt_desc *desc, tsb_ldlt_t *out) {
         if (desc == nullptr || out == nullptr) throw Error(TSB_E_ARG, "null desc/out");
         if (desc->max_v > kMaxV || desc->max_m > desc->max_v)
             throw Error(TSB_E_ARG, "dissection block (m + |anc|) larger than the vector staging buffer");
-        if (desc->stage_doubles < 2 || (desc->stage_doubles & 1)) throw Error(TSB_E_ARG, "bad staging size");
+        if (desc->max_cb < 0 || desc->max_cb > 4096) throw Error(TSB_E_ARG, "bad contribution staging size");
         auto *h = new tsb_ldlt;
         h->d = *desc;
         const size_t ls = sweep_smem_lower(*desc), us = sweep_smem_upper(*desc);

@@ -1,7 +1,7 @@
 // Persistent sweep bodies of the nested-dissection LDL^T apply, shared by the
 // stand-alone sweep kernels (ldlt.cu) and the persistent PCG solver (pcg.cu).
-// Block-inverse layout and item protocol: include/tsb.h (tsb_ldlt_desc) and
-// ldlt.cu.
+// Tiled block-inverse layout and item protocol: include/tsb.h (tsb_ldlt_desc),
+// ldlt.cu and paper_2306_05893_b200/_ldlt_pack.py.
 #pragma once
 
 #include "tsb_common.cuh"
@@ -9,11 +9,15 @@
 namespace tsb {
 
 constexpr int kSweepBlock = 256;
-constexpr int kMaxV = 8192;         // largest m + na whose vector is staged in shared memory
-constexpr int kMaxChunkRows = 512;  // rows of an item (host packer caps it)
+constexpr int kWarps = kSweepBlock / 32;
+constexpr int kTile = 32;               // rows per tile (one per lane)
+constexpr int kStage = 6144;            // doubles of TMA staging (48 KB): small-tile items
+constexpr int kSegPairs = 96;           // pairs per segment item of a large tile (48 KB)
+constexpr int kMaxV = 8192;             // largest m + na whose vector is staged in shared memory
+constexpr int kMaxItemRows = kWarps * kTile;
 
 struct Item {
-    int32_t block, r0, r1, pad;
+    int32_t block, t0, t1, seg;  // seg = 0: tiles [t0, t1); seg = s + 1: segment s of tile t0
 };
 
 // ---- small PTX helpers -----------------------------------------------------
@@ -80,20 +84,6 @@ __device__ __forceinline__ void trace(int64_t *buf, int iid, int slot) {
     }
 }
 
-// Row r of G_b (lower; m = block size): triangle rows r < m hold r entries
-// (padded to even), then the M rows with stride m rounded up to even.
-__device__ __forceinline__ int64_t g_row_off(int r, int m) {
-    if (r < m) return ((int64_t)r * r) >> 1;
-    return (((int64_t)m * m) >> 1) + (int64_t)(r - m) * (m + (m & 1));
-}
-// Row c of G_b^T (upper; K = m + na - 1): v-entries [c+1, K+1), length K - c
-// padded to even; offset = sum_{j=K-c+1..K} (j + (j & 1)).
-__device__ __forceinline__ int64_t gt_row_off(int c, int K) {
-    if (c <= 0) return 0;
-    const int64_t a = (int64_t)K - c + 1;
-    return ((K + a) * (K - a + 1)) / 2 + (((int64_t)K + 1) >> 1) - (a >> 1);
-}
-
 struct SweepArgs {
     const double *in;        // input vector (lower: r; upper: w)
     const int32_t *in_perm;  // lower apply: gather input through perm
@@ -105,7 +95,8 @@ struct SweepArgs {
 };
 
 // Exit protocol: the last CTA out zeroes the counters for the next replay.
-__device__ __forceinline__ void sweep_exit(int32_t *ctl, int32_t *c0, int64_t n0, int32_t *c1, int64_t n1) {
+__device__ __forceinline__ void sweep_exit(int32_t *ctl, int32_t *c0, int64_t n0, int32_t *c1, int64_t n1,
+                                           int32_t *c2, int64_t n2) {
     __syncthreads();
     __shared__ int last;
     if (threadIdx.x == 0) {
@@ -116,6 +107,7 @@ __device__ __forceinline__ void sweep_exit(int32_t *ctl, int32_t *c0, int64_t n0
     if (!last) return;
     for (int64_t i = threadIdx.x; i < n0; i += blockDim.x) c0[i] = 0;
     for (int64_t i = threadIdx.x; i < n1; i += blockDim.x) c1[i] = 0;
+    for (int64_t i = threadIdx.x; i < n2; i += blockDim.x) c2[i] = 0;
     __syncthreads();
     if (threadIdx.x == 0) {
         ctl[0] = 0;
@@ -123,14 +115,20 @@ __device__ __forceinline__ void sweep_exit(int32_t *ctl, int32_t *c0, int64_t n0
         __threadfence();
     }
 }
+__device__ __forceinline__ void lower_exit(const tsb_ldlt_desc &D) {
+    sweep_exit(D.d_ctl, D.d_cnt_l, D.n_blocks, D.d_ready_l, D.n_blocks, D.d_tcnt_lower, D.n_tiles_lower);
+}
+__device__ __forceinline__ void upper_exit(const tsb_ldlt_desc &D) {
+    sweep_exit(D.d_ctl + 2, D.d_done_u, D.n_blocks, D.d_tcnt_upper, D.n_tiles_upper, D.d_pad, 0);
+}
 
 // dynamic shared memory of the sweep bodies
 inline size_t sweep_smem_lower(const tsb_ldlt_desc &D) {
-    return (size_t)(D.stage_doubles + ((D.max_m + 1) & ~1) + ((D.max_cb + 1) & ~1)) * sizeof(double) +
-           (((D.max_m + 2) & ~1) + kMaxChunkRows) * sizeof(int32_t);
+    return (size_t)(kStage + ((D.max_m + 2) & ~1) + ((D.max_cb + 1) & ~1)) * sizeof(double) +
+           (((D.max_m + 2) & ~1) + kMaxItemRows) * sizeof(int32_t);
 }
 inline size_t sweep_smem_upper(const tsb_ldlt_desc &D) {
-    return (size_t)(D.stage_doubles + ((D.max_v + 1) & ~1)) * sizeof(double);
+    return (size_t)(kStage + ((D.max_v + 2) & ~1)) * sizeof(double);
 }
 
 // Sum of a row's contributions cb[a0, a1) in the fixed order every finaliser
@@ -165,57 +163,6 @@ __device__ __forceinline__ void stage_copy(double *dst, const double *src, int n
     }
 }
 
-// One warp: dot products of 8 staged rows with the shared vector v.  Row k
-// holds the entries of v[lo_k, hi_k) at p_k.  Lanes stride v (each v[t] read
-// once for the 8 rows), then a butterfly transpose-reduction (7 + 2 shuffles
-// for 8 rows, fixed order).  Returns the row sum in the lanes with
-// (lane & 3) == 0; *krow = which of the 8 rows.
-__device__ __forceinline__ double rows8_dot(const double *const p[8], const int lo[8], const int hi[8],
-                                            const double *v, int lane, int *krow) {
-    int tmin = lo[0], tmax = hi[0];
-#pragma unroll
-    for (int k = 1; k < 8; ++k) {
-        tmin = min(tmin, lo[k]);
-        tmax = max(tmax, hi[k]);
-    }
-    double acc[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) acc[k] = 0.0;
-    for (int t = tmin + lane; t < tmax; t += 32) {
-        const double vt = v[t];
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-            if (t >= lo[k] && t < hi[k]) acc[k] += p[k][t - lo[k]] * vt;
-    }
-    const bool b16 = lane & 16, b8 = lane & 8, b4 = lane & 4;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        const double send = b16 ? acc[k] : acc[k + 4];
-        const double keep = b16 ? acc[k + 4] : acc[k];
-        acc[k] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-    }
-#pragma unroll
-    for (int k = 0; k < 2; ++k) {
-        const double send = b8 ? acc[k] : acc[k + 2];
-        const double keep = b8 ? acc[k + 2] : acc[k];
-        acc[k] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-    }
-    {
-        const double send = b4 ? acc[0] : acc[1];
-        const double keep = b4 ? acc[1] : acc[0];
-        acc[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-    }
-    double r = acc[0];
-    r += __shfl_xor_sync(0xffffffffu, r, 2);
-    r += __shfl_xor_sync(0xffffffffu, r, 1);
-    *krow = (b16 ? 4 : 0) + (b8 ? 2 : 0) + (b4 ? 1 : 0);
-    return r;
-}
-
-__device__ __forceinline__ double lower_input(const SweepArgs &A, int row) {
-    return __ldcg(A.in + (A.in_perm ? A.in_perm[row] : row));  // may be produced in-kernel (L2)
-}
-
 // Strided per-thread loops with their global loads issued in batches of 4
 // (the loads of one batch are independent; results land in shared memory).
 // dst[j] = f(j) for j = tid, tid + 256, ... < n
@@ -237,28 +184,119 @@ __device__ __forceinline__ void batched(int n, F f) {
     }
 }
 
+// One warp, one staged tile: lane k accumulates row k of the tile over the
+// column pairs p = p0, p0 + ps, ... < p1 (pairs-major, 32 lanes x double2:
+// 512 contiguous bytes per pair, conflict-free; v read as a broadcast
+// double2).  Fixed summation order (deterministic).
+__device__ __forceinline__ double tile_dot(const double *d, const double *v, int p0, int p1, int ps, int lane) {
+    const double2 *g = reinterpret_cast<const double2 *>(d) + lane;
+    const double2 *vv = reinterpret_cast<const double2 *>(v);
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int p = p0;
+    for (; p + ps < p1; p += 2 * ps) {
+        const double2 g0 = g[p * kTile], g1 = g[(p + ps) * kTile];
+        const double2 x0 = vv[p], x1 = vv[p + ps];
+        a0 += g0.x * x0.x;
+        a1 += g0.y * x0.y;
+        a2 += g1.x * x1.x;
+        a3 += g1.y * x1.y;
+    }
+    if (p < p1) {
+        const double2 g0 = g[p * kTile], x0 = vv[p];
+        a0 += g0.x * x0.x;
+        a1 += g0.y * x0.y;
+    }
+    return (a0 + a1) + (a2 + a3);
+}
+
+// Stage an item's data (before the dependency wait) with one TMA bulk copy:
+// its small tiles, or one 48 KB column segment of a large tile.
+__device__ __forceinline__ void stage_item(const Item &it, const tsb_ldlt_tile *tiles, const double *base,
+                                           double *stage, uint64_t *bars) {
+    if (threadIdx.x != 0) return;
+    const tsb_ldlt_tile T0 = tiles[it.t0];
+    if (it.seg == 0) {
+        const tsb_ldlt_tile Tl = tiles[it.t1 - 1];
+        const int64_t end = Tl.off + (int64_t)Tl.np * (2 * kTile);
+        tma_load_1d(stage, base + T0.off, (uint32_t)((end - T0.off) * 8), &bars[0]);
+    } else {
+        const int p0 = (it.seg - 1) * kSegPairs, cnt = min(kSegPairs, T0.np - p0);
+        tma_load_1d(stage, base + T0.off + (int64_t)p0 * (2 * kTile), (uint32_t)(cnt * 2 * kTile * 8), &bars[0]);
+    }
+}
+
+// GEMV of a staged item against the shared vector v (v[t] = column t).
+// emit(row, value) once per tile row (block-relative row index).  A segment
+// item of a large tile writes its 32 partial sums to the tile's scratch; the
+// last segment to finish adds them in segment order and emits.
+template <class Emit>
+__device__ __forceinline__ void item_gemv(const Item &it, const tsb_ldlt_tile *tiles, double *stage, uint64_t *bars,
+                                          uint32_t &phase, const double *v, double *red, double *part,
+                                          int32_t *tcnt, const Emit &emit) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    mbar_wait(&bars[0], phase & 1u);
+    phase ^= 1u;
+    if (it.seg == 0) {
+        const int64_t off0 = tiles[it.t0].off;
+        for (int t = it.t0 + warp; t < it.t1; t += kWarps) {
+            const tsb_ldlt_tile T = tiles[t];
+            const double a = tile_dot(stage + (T.off - off0), v + T.tl, 0, T.np, 1, lane);
+            if (lane < T.nrows) emit(T.row0 + lane, a);
+        }
+        return;
+    }
+    __shared__ int last_seg;
+    const tsb_ldlt_tile T = tiles[it.t0];
+    const int s = it.seg - 1, p0 = s * kSegPairs, cnt = min(kSegPairs, T.np - p0);
+    red[warp * 32 + lane] = tile_dot(stage, v + T.tl + 2 * p0, warp, cnt, kWarps, lane);
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        double a = 0.0;
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) a += red[w * 32 + threadIdx.x];
+        part[((int64_t)T.part + s) * kTile + threadIdx.x] = a;
+        __threadfence();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        last_seg = atomicAdd(tcnt + it.t0, 1) == T.nseg - 1;
+        if (last_seg) __threadfence();
+    }
+    __syncthreads();
+    if (last_seg && threadIdx.x < 32) {
+        double a = 0.0;
+        for (int q = 0; q < T.nseg; ++q) a += __ldcg(part + ((int64_t)T.part + q) * kTile + threadIdx.x);
+        if ((int)threadIdx.x < T.nrows) emit(T.row0 + threadIdx.x, a);
+    }
+}
+
+__device__ __forceinline__ double lower_input(const SweepArgs &A, int row) {
+    return __ldcg(A.in + (A.in_perm ? A.in_perm[row] : row));  // may be produced in-kernel (L2)
+}
+
 // ---------------------------------------------------------------------------
 // lower sweep: L y = r   (column-major pre-accumulation, one GEMV per block)
-//   item (b, rows [r0, r1) of G_b): stage the rows by TMA and the block's
-//   input before the wait, form x_b = input - contributions, then
+//   item (b, tiles of G_b rows): stage the tiles by TMA and the block's input
+//   before the wait, form x_b = input - contributions, then
 //       triangle row i:  y_i = x_i + sum_{j<i} Linv_ij x_j          -> x[start+i]
 //       M row k:         c_k = sum_j M_kj x_j                        -> cbuf slot
 //   and count the item on the parent; a mode-2 parent's contribution sums
 //   are formed once by the item that completes it.
-// shared memory: [stage][xs max_m][cbs max_cb][offs int32 max_m+2][dsts int32]
+// shared memory: [stage][xs max_m+2][cbs max_cb][offs int32 max_m+2][dsts int32]
 // ---------------------------------------------------------------------------
 template <bool TRACE>
 __device__ __forceinline__ void lower_sweep_body(const tsb_ldlt_desc &D, const SweepArgs &A, double *smem,
-                                                 uint64_t &bar, uint32_t &phase) {
+                                                 uint64_t *bars, uint32_t &phase) {
     double *stage = smem;
-    double *xs = smem + D.stage_doubles;
-    double *cbs = xs + ((D.max_m + 1) & ~1);
+    double *xs = smem + kStage;
+    double *cbs = xs + ((D.max_m + 2) & ~1);
     int32_t *offs = reinterpret_cast<int32_t *>(cbs + ((D.max_cb + 1) & ~1));
     int32_t *dsts = offs + ((D.max_m + 2) & ~1);
     __shared__ int item_id, fin_parent;
+    __shared__ double red[kSweepBlock];
     int32_t *ctl = D.d_ctl;
     int64_t *const tbuf = TRACE ? D.d_trace_lower : nullptr;  // folds away when off
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int tid = threadIdx.x;
     const Item *items = reinterpret_cast<const Item *>(D.d_items_lower);
     while (true) {
         if (tid == 0) item_id = atomicAdd(ctl, 1);
@@ -268,11 +306,10 @@ __device__ __forceinline__ void lower_sweep_body(const tsb_ldlt_desc &D, const S
         trace(tbuf, iid, 0);
         const Item it = items[iid];
         const tsb_ldlt_block B = D.d_blocks[it.block];
-        const int m = B.m, s = B.start, nr = it.r1 - it.r0;
-        const int64_t o0 = g_row_off(it.r0, m);
+        const int m = B.m, s = B.start;
         // everything that does not depend on the sweep's progress is fetched
-        // before the wait: the factor rows (TMA), the block's input, the slots
-        if (tid == 0) tma_load_1d(stage, D.d_g + B.g_off + o0, (uint32_t)((g_row_off(it.r1, m) - o0) * 8), &bar);
+        // before the wait: the factor tiles (TMA), the block's input, the slots
+        stage_item(it, D.d_tiles_lower, D.d_g, stage, bars);
         {
             struct In {
                 const SweepArgs &A;
@@ -283,8 +320,11 @@ __device__ __forceinline__ void lower_sweep_body(const tsb_ldlt_desc &D, const S
             };
             batched(m, In{A, xs, s});
         }
-        const int mr0 = max(it.r0, m);
-        for (int j = mr0 + tid; j < it.r1; j += kSweepBlock) dsts[j - mr0] = __ldg(D.d_cslot + B.anc_off + (j - m));
+        if (tid == 0) xs[m] = 0.0;  // column pad of odd-width tiles
+        const tsb_ldlt_tile Tf = D.d_tiles_lower[it.t0], Tb = D.d_tiles_lower[it.t1 - 1];
+        const int r_lo = Tf.row0, r_hi = Tb.row0 + Tb.nrows;
+        const int mr0 = max(r_lo, m);
+        for (int j = mr0 + tid; j < r_hi; j += kSweepBlock) dsts[j - mr0] = __ldg(D.d_cslot + B.anc_off + (j - m));
         if (B.mode == 1)
             for (int j = tid; j <= m; j += kSweepBlock) offs[j] = (int32_t)(__ldg(D.d_cin_ptr + s + j) - B.cb_off);
         if (tid == 0) {
@@ -294,10 +334,28 @@ __device__ __forceinline__ void lower_sweep_body(const tsb_ldlt_desc &D, const S
         __syncthreads();
         trace(tbuf, iid, 1);
         // x_b = input - (contributions of the descendants)
-        if (B.mode == 1) {
-            stage_copy(cbs, D.d_cbuf + B.cb_off, B.ncb);
-            __syncthreads();
-            for (int j = tid; j < m; j += kSweepBlock) xs[j] = xs[j] - contrib_sum<false>(cbs, offs[j], offs[j + 1]);
+        if (B.mode == 1) {  // rows in pieces whose contributions fit the buffer
+            int i0 = 0;
+            while (i0 < m) {
+                int i1 = m;
+                if (offs[m] - offs[i0] > D.max_cb) {
+                    int lo = i0 + 1, hi = m;
+                    while (lo < hi) {
+                        const int mid = (lo + hi + 1) >> 1;
+                        if (offs[mid] - offs[i0] <= D.max_cb) lo = mid; else hi = mid - 1;
+                    }
+                    i1 = lo;
+                }
+                const int base = offs[i0], cnt = offs[i1] - base;
+                const bool fits = cnt <= D.max_cb;
+                if (fits) stage_copy(cbs, D.d_cbuf + B.cb_off + base, cnt);
+                __syncthreads();
+                for (int j = i0 + tid; j < i1; j += kSweepBlock)
+                    xs[j] = xs[j] - (fits ? contrib_sum<false>(cbs, offs[j] - base, offs[j + 1] - base)
+                                          : contrib_sum<true>(D.d_cbuf + B.cb_off, offs[j], offs[j + 1]));
+                __syncthreads();
+                i0 = i1;
+            }
         } else if (B.mode == 2) {
             struct Sub {
                 const double *src;
@@ -307,31 +365,16 @@ __device__ __forceinline__ void lower_sweep_body(const tsb_ldlt_desc &D, const S
             };
             batched(m, Sub{D.d_x + s, xs});
         }
-        mbar_wait(&bar, phase);
-        phase ^= 1;
         __syncthreads();
         trace(tbuf, iid, 4);
-        for (int j0 = warp * 8; j0 < nr; j0 += 8 * (kSweepBlock / 32)) {  // warp-uniform trips
-            const double *p[8];
-            int lo[8], hi[8];
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                const bool ok = j0 + k < nr;
-                const int r = it.r0 + (ok ? j0 + k : 0);
-                lo[k] = 0;
-                hi[k] = ok ? (r < m ? r : m) : 0;
-                p[k] = stage + (g_row_off(r, m) - o0);
-            }
-            int k;
-            const double a = rows8_dot(p, lo, hi, xs, lane, &k);
-            const int j = j0 + k;
-            if ((lane & 3) == 0 && j < nr) {
-                const int r = it.r0 + j;
+        {
+            auto emit = [&](int r, double a) {
                 if (r < m)
                     A.x[s + r] = xs[r] + a;
                 else
                     D.d_cbuf[dsts[r - mr0]] = a;
-            }
+            };
+            item_gemv(it, D.d_tiles_lower, stage, bars, phase, xs, red, D.d_part_lower, D.d_tcnt_lower, emit);
         }
         trace(tbuf, iid, 5);
         __syncthreads();
@@ -359,16 +402,16 @@ __device__ __forceinline__ void lower_sweep_body(const tsb_ldlt_desc &D, const S
             while (i0 < P.m) {
                 const int64_t qb = __ldg(D.d_cin_ptr + P.start + i0);
                 int i1 = P.m;
-                if (qe - qb > D.stage_doubles) {  // rows [i0, i1) whose contributions fit (>= 1 row)
+                if (qe - qb > kStage) {  // rows [i0, i1) whose contributions fit (>= 1 row)
                     int lo = i0 + 1, hi = P.m;
                     while (lo < hi) {
                         const int mid = (lo + hi + 1) >> 1;
-                        if (__ldg(D.d_cin_ptr + P.start + mid) - qb <= D.stage_doubles) lo = mid; else hi = mid - 1;
+                        if (__ldg(D.d_cin_ptr + P.start + mid) - qb <= kStage) lo = mid; else hi = mid - 1;
                     }
                     i1 = lo;
                 }
                 const int cnt = (int)(__ldg(D.d_cin_ptr + P.start + i1) - qb);
-                const bool staged = cnt <= D.stage_doubles;
+                const bool staged = cnt <= kStage;
                 if (staged) stage_copy(stage, D.d_cbuf + qb, cnt);
                 for (int i = i0 + tid; i <= i1; i += kSweepBlock)
                     fo[i - i0] = (int32_t)(__ldg(D.d_cin_ptr + P.start + i) - qb);
@@ -386,26 +429,27 @@ __device__ __forceinline__ void lower_sweep_body(const tsb_ldlt_desc &D, const S
         }
         trace(tbuf, iid, 2);
     }
-    sweep_exit(ctl, D.d_cnt_l, D.n_blocks, D.d_ready_l, D.n_blocks);
+    lower_exit(D);
 }
 
 // ---------------------------------------------------------------------------
 // upper sweep: L^T z = w   (row-major pull, one GEMV per block)
 //   z_b = w_b + G_b^T v,  v = [w_b ; -z_anc]
-//   item (b, rows [c0, c1) of G_b^T = columns of G_b): stage the rows by TMA
+//   item (b, tiles of G_b^T rows = columns of G_b): stage the tiles by TMA
 //   and w_b before the wait (only -z_anc depends on the parent), then
 //   z_c = v_c + sum_{t > c} G^T[c][t] v_t for the item's columns.
-// shared memory: [stage][v max_v]
+// shared memory: [stage][v max_v+2]
 // ---------------------------------------------------------------------------
 template <bool TRACE>
 __device__ __forceinline__ void upper_sweep_body(const tsb_ldlt_desc &D, const SweepArgs &A, double *smem,
-                                                 uint64_t &bar, uint32_t &phase) {
+                                                 uint64_t *bars, uint32_t &phase) {
     double *stage = smem;
-    double *v = smem + D.stage_doubles;
+    double *v = smem + kStage;
     __shared__ int item_id;
+    __shared__ double red[kSweepBlock];
     int32_t *ctl = D.d_ctl + 2;
     int64_t *const tbuf = TRACE ? D.d_trace_upper : nullptr;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int tid = threadIdx.x;
     const Item *items = reinterpret_cast<const Item *>(D.d_items_upper);
     while (true) {
         if (tid == 0) item_id = atomicAdd(ctl, 1);
@@ -415,16 +459,17 @@ __device__ __forceinline__ void upper_sweep_body(const tsb_ldlt_desc &D, const S
         trace(tbuf, iid, 0);
         const Item it = items[iid];
         const tsb_ldlt_block B = D.d_blocks[it.block];
-        const int m = B.m, s = B.start, na = B.na, K = m + na - 1, nr = it.r1 - it.r0;
-        const int64_t o0 = gt_row_off(it.r0, K);
-        if (tid == 0) tma_load_1d(stage, D.d_gt + B.gt_off + o0, (uint32_t)((gt_row_off(it.r1, K) - o0) * 8), &bar);
-        for (int t = it.r0 + tid; t < m; t += kSweepBlock) {  // w_b: produced before this sweep
+        const int m = B.m, s = B.start, na = B.na;
+        stage_item(it, D.d_tiles_upper, D.d_gt, stage, bars);
+        const int t_lo = D.d_tiles_upper[it.t0].tl;
+        for (int t = t_lo + tid; t < m; t += kSweepBlock) {  // w_b: produced before this sweep
             double w = __ldcg(A.in + s + t);
             if (A.dscale) w = w / A.dscale[s + t];
             v[t] = w;
         }
         for (int k = tid; k < na; k += kSweepBlock)  // ancestor rows, parked in v until the wait is over
             v[m + k] = __longlong_as_double((long long)__ldg(D.d_anc + B.anc_off + k));
+        if (tid == 0) v[m + na] = 0.0;  // column pad of odd-width tiles
         if (na > 0 && tid == 0) spin_until_geq(D.d_done_u + B.parent, D.d_blocks[B.parent].n_u);
         __syncthreads();
         trace(tbuf, iid, 1);
@@ -437,30 +482,15 @@ __device__ __forceinline__ void upper_sweep_body(const tsb_ldlt_desc &D, const S
             };
             batched(na, Anc{A.x, v + m});
         }
-        mbar_wait(&bar, phase);
-        phase ^= 1;
         __syncthreads();
         trace(tbuf, iid, 4);
-        for (int j0 = warp * 8; j0 < nr; j0 += 8 * (kSweepBlock / 32)) {
-            const double *p[8];
-            int lo[8], hi[8];
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                const bool ok = j0 + k < nr;
-                const int c = it.r0 + (ok ? j0 + k : 0);
-                lo[k] = c + 1;
-                hi[k] = ok ? K + 1 : c + 1;
-                p[k] = stage + (gt_row_off(c, K) - o0);
-            }
-            int k;
-            const double a = rows8_dot(p, lo, hi, v, lane, &k);
-            const int j = j0 + k;
-            if ((lane & 3) == 0 && j < nr) {
-                const int c = it.r0 + j;
+        {
+            auto emit = [&](int c, double a) {
                 const double z = v[c] + a;
                 A.x[s + c] = z;
                 if (A.out_perm) A.out[A.out_perm[s + c]] = z;
-            }
+            };
+            item_gemv(it, D.d_tiles_upper, stage, bars, phase, v, red, D.d_part_upper, D.d_tcnt_upper, emit);
         }
         trace(tbuf, iid, 5);
         __syncthreads();
@@ -470,7 +500,7 @@ __device__ __forceinline__ void upper_sweep_body(const tsb_ldlt_desc &D, const S
         }
         trace(tbuf, iid, 2);
     }
-    sweep_exit(ctl, D.d_done_u, D.n_blocks, D.d_pad, 0);
+    upper_exit(D);
 }
 
 }  // namespace tsb

@@ -108,7 +108,7 @@ pcg_persistent(PcgWork W, PcgArgs a, tsb_ldlt_desc D) {
     extern __shared__ __align__(128) double smem[];  // sweep staging (LDL^T)
     __shared__ double red[32];
     __shared__ double bc;
-    __shared__ uint64_t mbar;
+    __shared__ uint64_t mbar[2];
     const int tid = threadIdx.x;
     const int64_t n = W.n;
     const int64_t gtid = (int64_t)blockIdx.x * kPcgBlock + tid, gstride = (int64_t)gridDim.x * kPcgBlock;
@@ -117,7 +117,10 @@ pcg_persistent(PcgWork W, PcgArgs a, tsb_ldlt_desc D) {
     const int64_t grp = gtid >> 3, ngrp = gstride >> 3;
     uint32_t phase = 0;
     if (KIND == TSB_PRECOND_LDLT) {
-        if (tid == 0) mbar_init(&mbar, 1);
+        if (tid == 0) {
+            mbar_init(&mbar[0], 1);
+            mbar_init(&mbar[1], 1);
+        }
         __syncthreads();
     }
     // ---- init (krylov.py:130-141) -------------------------------------------

@@ -15,11 +15,20 @@ from paper_2306_05893_b200 import _ldlt_pack as K, mesh as M, ndprecond as ND
 from paper_2306_05893_b200.assembly import CsrMatrix
 
 
-def _g(H, b):
-    B = H["blocks"][b]
-    m, na = int(B["m"]), int(B["na"])
-    off = K.row_offsets(m, na)
-    return H["g"][B["g_off"]: B["g_off"] + off[-1]], off, m, na
+def _tile(H, up, t):
+    """(block rows, dense tile rows over v-columns [tl, tl + 2 np), tl) of tile t."""
+    T = H["tiles_u" if up else "tiles_l"][t]
+    data = H["gt" if up else "g"]
+    npair = int(T["np"])
+    d = data[T["off"]: T["off"] + npair * K.TILE * 2].reshape(npair, K.TILE, 2).transpose(1, 0, 2)
+    d = d.reshape(K.TILE, 2 * npair)[: T["nrows"]]
+    return np.arange(T["row0"], T["row0"] + T["nrows"]), d, int(T["tl"])
+
+
+def _padded(v, upto):
+    out = np.zeros(max(upto, len(v)))
+    out[: len(v)] = v
+    return out
 
 
 def emulate_lower(H, r):
@@ -30,10 +39,10 @@ def emulate_lower(H, r):
     cbuf = np.zeros(max(H["ncbuf"], 1))
     cnt = np.zeros(nb, dtype=np.int64)
     ready = np.zeros(nb, dtype=bool)
-    for b, r0, r1, _ in H["items_l"]:
+    segs = np.zeros(len(H["tiles_l"]), dtype=np.int64)
+    for b, t0, t1, sg in H["items_l"]:
         B = blocks[b]
         s, m = int(B["start"]), int(B["m"])
-        g, off, _, _ = _g(H, b)
         if B["mode"] == K.MODE_FIN:
             assert ready[b], "lower item dispatched before its block input was final"
             xs = r[s:s + m] - xbuf[s:s + m]
@@ -43,12 +52,18 @@ def emulate_lower(H, r):
         else:
             assert B["target_l"] == 0
             xs = r[s:s + m].copy()
-        for row in range(r0, r1):
-            if row < m:
-                y[s + row] = xs[row] + g[off[row]: off[row] + row] @ xs[:row]
-            else:
-                k = row - m
-                cbuf[H["cslot"][B["anc_off"] + k]] = g[off[row]: off[row] + m] @ xs
+        for t in range(t0, t1):
+            if sg:  # segment item: the tile's rows are emitted by its last segment
+                segs[t] += 1
+                if segs[t] < H["tiles_l"]["nseg"][t]:
+                    continue
+            rows, d, tl = _tile(H, False, t)
+            vals = d @ _padded(xs, tl + d.shape[1])[tl: tl + d.shape[1]]
+            for row, a in zip(rows, vals):
+                if row < m:
+                    y[s + row] = xs[row] + a
+                else:
+                    cbuf[H["cslot"][B["anc_off"] + row - m]] = a
         p = int(B["parent"])
         if p >= 0:
             cnt[p] += 1
@@ -59,6 +74,7 @@ def emulate_lower(H, r):
                     xbuf[row] = cbuf[H["cin_ptr"][row]: H["cin_ptr"][row + 1]].sum()
                 ready[p] = True
     assert np.all(cnt == blocks["target_l"])
+    assert np.array_equal(segs, H["tiles_l"]["nseg"])
     return y
 
 
@@ -79,19 +95,25 @@ def emulate_upper(H, w):
     blocks = H["blocks"]
     z = np.zeros(n)
     done = np.zeros(nb, dtype=np.int64)
-    for b, c0, c1, _ in H["items_u"]:
+    segs = np.zeros(len(H["tiles_u"]), dtype=np.int64)
+    for b, t0, t1, sg in H["items_u"]:
         B = blocks[b]
         s, m, na = int(B["start"]), int(B["m"]), int(B["na"])
-        toff = K.gt_row_offsets(m, na)
-        gt = H["gt"][B["gt_off"]: B["gt_off"] + toff[-1]]
         if na:
             p = int(B["parent"])
             assert done[p] == blocks[p]["n_u"], "upper item dispatched before the parent's z"
         v = np.concatenate([w[s:s + m], -z[H["anc"][B["anc_off"]: B["anc_off"] + na]]])
-        for c in range(c0, c1):
-            z[s + c] = v[c] + gt[toff[c]: toff[c] + (m + na - 1 - c)] @ v[c + 1:]
+        for t in range(t0, t1):
+            if sg:
+                segs[t] += 1
+                if segs[t] < H["tiles_u"]["nseg"][t]:
+                    continue
+            cols, d, tl = _tile(H, True, t)
+            vals = d @ _padded(v, tl + d.shape[1])[tl: tl + d.shape[1]]
+            z[s + cols] = v[cols] + vals
         done[b] += 1
     assert np.all(done == blocks["n_u"])
+    assert np.array_equal(segs, H["tiles_u"]["nseg"])
     return z
 
 
@@ -118,51 +140,31 @@ def test_block_inverse_dag_emulation_matches_oracle(dims, leaf):
     assert np.abs(z - ref).max() <= 1e-12 * np.abs(ref).max()
 
 
-def test_block_layout_roundtrip_and_coverage():
+def test_tile_layout_roundtrip_and_coverage():
     _, f = _factors((4, 4, 12), 16)
     H = K.pack(f)
-    for b, bf in enumerate(f.blocks):
-        g, off, m, na = _g(H, b)
-        linv, mm = K.unpack_block(g, m, na)
-        assert np.allclose(linv @ bf.l11, np.eye(m), atol=1e-12)
-        assert np.allclose(mm, bf.l21 @ linv, atol=1e-12)
-        assert np.all(off % 2 == 0)  # every row 16-byte aligned (TMA / cp.async)
-    # lower items cover each block's G rows exactly once
-    for b in range(H["nb"]):
-        B = H["blocks"][b]
-        rows = sorted((r0, r1) for bb, r0, r1, _ in H["items_l"] if bb == b)
-        assert rows[0][0] == 0 and rows[-1][1] == B["m"] + B["na"]
-        assert all(a[1] == c[0] for a, c in zip(rows, rows[1:]))
-    # upper items cover each block's columns exactly once; G^T is G transposed
-    for b, bf in enumerate(f.blocks):
-        B = H["blocks"][b]
-        m, na = int(B["m"]), int(B["na"])
-        cols = sorted((c0, c1) for bb, c0, c1, _ in H["items_u"] if bb == b)
-        assert cols[0][0] == 0 and cols[-1][1] == m and all(a[1] == c[0] for a, c in zip(cols, cols[1:]))
-        toff = K.gt_row_offsets(m, na)
-        gt = H["gt"][B["gt_off"]: B["gt_off"] + toff[-1]]
-        linv, mm = K.block_matrix(bf)
-        full = np.vstack([np.tril(linv, -1), mm])
-        for c in range(m):
-            assert np.array_equal(gt[toff[c]: toff[c] + m + na - 1 - c], full[c + 1:, c])
-        assert np.all(toff % 2 == 0)
-    assert H["g"].size == sum(len(_g(H, b)[0]) for b in range(H["nb"]))
-
-
-def test_device_row_offset_formulas():
-    """The closed forms in csrc (g_row_off, gt_row_off) equal the packer's offsets."""
-    def g_row_off(r, m):
-        return (r * r) >> 1 if r < m else ((m * m) >> 1) + (r - m) * (m + (m & 1))
-
-    def gt_row_off(c, K):
-        if c <= 0:
-            return 0
-        a = K - c + 1
-        return ((K + a) * (K - a + 1)) // 2 + ((K + 1) >> 1) - (a >> 1)
-
-    for m in (1, 2, 3, 7, 16, 33, 128):
-        for na in (0, 1, 5, 64):
-            off = K.row_offsets(m, na)
-            assert [g_row_off(r, m) for r in range(m + na + 1)] == off.tolist()
-            toff = K.gt_row_offsets(m, na)
-            assert [gt_row_off(c, m + na - 1) for c in range(m + 1)] == toff.tolist()
+    tl_ = H["tiles_l"]
+    assert np.all(tl_["off"] % 64 == 0) and np.all(tl_["tl"] % 2 == 0)  # 512-B tiles, 16-B aligned v
+    for up in (False, True):
+        items = H["items_u" if up else "items_l"]
+        for b, bf in enumerate(f.blocks):
+            m, na = bf.stop - bf.start, len(bf.anc)
+            linv, mm = K.block_matrix(bf)
+            G = K.gfull(linv, mm)
+            G = G.T if up else G
+            rows_seen = []
+            for bb, t0, t1, big in items:
+                if bb != b or big > 1:
+                    continue
+                assert big >= 0 and (not big or t1 == t0 + 1)
+                for t in range(t0, t1):
+                    rows, d, tl = _tile(H, up, t)
+                    rows_seen.extend(rows.tolist())
+                    lo, hi = K.row_ranges(m, na, up)
+                    for k, row in enumerate(rows):
+                        full = np.zeros(d.shape[1])
+                        a, e = lo[row] - tl, hi[row] - tl
+                        full[a:e] = G[row, lo[row]:hi[row]]
+                        assert np.array_equal(d[k], full)
+            assert sorted(rows_seen) == list(range(m if up else m + na))
+    assert H["g"].size == int(tl_["np"].sum()) * K.TILE * 2

@@ -39,3 +39,4 @@ def test_struct_layouts_match_the_header():
     assert lib.tsb_struct_size(2) == _ldlt_pack.BLOCK_DTYPE.itemsize
     assert lib.tsb_struct_size(3) == _lib.C.sizeof(_lib.LdltDesc)
     assert lib.tsb_struct_size(4) == _lib.C.sizeof(_lib.Report)
+    assert lib.tsb_struct_size(5) == _ldlt_pack.TILE_DTYPE.itemsize
