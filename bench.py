@@ -403,6 +403,8 @@ def main():
             "l2": "flushed (256 MB write) before every timed step", "parallelism": f"replicas x{world}",
         },
         "iterations": main_r["iterations"], "assembly_ms": main_r["assembly_ms"], "pcg_ms": main_r["solve_ms"],
+        "step_ms": {"min": min(main_r["per_step"]), "median": statistics.median(main_r["per_step"]),
+                    "max": max(main_r["per_step"])},
         other: {"ms_per_step": other_r["ms"], "iterations": other_r["iterations"],
                 "assembly_ms": other_r["assembly_ms"], "pcg_ms": other_r["solve_ms"]},
         "trisolve": {"apply_ms": apply_r["ms"], "gbs": apply_r["gbs"], "frac": apply_r["gbs"] / hbm,

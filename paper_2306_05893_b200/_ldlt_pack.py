@@ -13,12 +13,13 @@ block removes the in-block dependency chain, and pre-multiplying the
 coupling panel by it (M) makes the ancestor contributions depend only on the
 block's input x_b:
 
-    lower:  y_b = x_b + (Linv - I) x_b,   contributions  c = M x_b
-    upper:  z_b = w_b + G_b^T [w_b ; -z_anc]
+    lower:  y_b = Linv x_b,   contributions  c = M x_b
+    upper:  z_b = [Linv; M]^T [w_b ; -z_anc]
 
-Both sweeps are therefore GEMVs over rows with a contiguous v-range: lower
-rows r of G_b (v = x_b, columns [0, r) or [0, m)), upper rows c of G_b^T
-(v = [w_b; -z_anc], columns [c+1, m+na)).  The factor blocks are well
+Both sweeps are therefore GEMVs over rows with a contiguous v-range (unit
+diagonal stored): lower rows r of [Linv; M] (v = x_b, columns [0, r] or
+[0, m)), upper rows c of its transpose (v = [w_b; -z_anc], columns
+[c, m+na)).  The factor blocks are well
 conditioned (cond_1(L11) <= 14 on the cfg2/cfg3 beams); the block-inverse
 apply matches the reference's tile-16 sweeps to ~5e-16 relative.
 
@@ -87,17 +88,19 @@ def block_matrix(bf):
 
 
 def gfull(linv, mm):
-    """G_b as a dense (m + na) x m matrix: [tril(Linv, -1); M]."""
-    return np.vstack([np.tril(linv, -1), mm])
+    """Rows of the lower sweep as a dense (m + na) x m matrix: [Linv; M] (unit
+    diagonal kept, so y_r = sum_{j <= r} Linv_rj x_j needs no separate x_r)."""
+    return np.vstack([np.tril(linv), mm])
 
 
 def row_ranges(m: int, na: int, upper: bool):
-    """v-ranges [lo, hi) of the sweep's rows: lower rows of G_b, upper rows of G_b^T."""
+    """v-ranges [lo, hi) of the sweep's rows (diagonal included): lower rows r of
+    [Linv; M] over x_b, upper rows c of its transpose over [w_b; -z_anc]."""
     if upper:
         c = np.arange(m, dtype=np.int64)
-        return c + 1, np.full(m, m + na, dtype=np.int64)
+        return c, np.full(m, m + na, dtype=np.int64)
     r = np.arange(m + na, dtype=np.int64)
-    return np.zeros(m + na, dtype=np.int64), np.minimum(r, m)
+    return np.zeros(m + na, dtype=np.int64), np.minimum(r + 1, m)
 
 
 def tile_block(G: np.ndarray, m: int, na: int, upper: bool):
@@ -294,13 +297,27 @@ def pack(factors):
     blocks["cb_off"] = cin_ptr[[bf.start for bf in bfs]] if nb else []
     blocks["anc_off"] = anc_off[:-1]
     max_cb = min(CB_CAP, int(blk_contrib[mode == MODE_GATHER].max())) if np.any(mode == MODE_GATHER) else 0
+
+    def window(up, i, it):  # v-columns an item reads (csrc item_window)
+        T = tables[up]
+        lim = int(ms_[i] + (na_[i] if up else 0))
+        if it[2]:
+            p0 = (it[2] - 1) * SEG_PAIRS
+            cnt = min(SEG_PAIRS, int(T["np"][it[0]]) - p0)
+            w0 = int(T["tl"][it[0]]) + 2 * p0
+            return w0, min(w0 + 2 * cnt, lim)
+        w0 = int(T["tl"][it[0]:it[1]].min())
+        return w0, min(int((T["tl"][it[0]:it[1]] + 2 * T["np"][it[0]:it[1]]).max()), lim)
+
+    max_w = max([1] + [(lambda w: w[1] - w[0])(window(up, i, it)) for up in (False, True)
+                       for i in range(nb) for it in items[up][i]])
     cat = lambda parts: np.concatenate(parts) if parts else np.zeros(2)  # noqa: E731
     return {
         "n": n, "nb": nb, "blocks": blocks, "items_l": items_l, "items_u": items_u,
         "tiles_l": tables[False], "tiles_u": tables[True], "g": cat(data[False]), "gt": cat(data[True]),
         "anc": anc_all, "cslot": cslot, "cin_ptr": cin_ptr, "ncbuf": len(anc_all),
         "d": np.asarray(factors.d, dtype=np.float64), "perm": np.asarray(plan.perm, dtype=np.int64),
-        "max_m": int(ms_.max()) if nb else 1, "max_v": int((ms_ + na_).max()) if nb else 1, "max_cb": max_cb,
+        "max_m": int(ms_.max()) if nb else 1, "max_v": int(max_w), "max_cb": max_cb,
         "parent": parent, "children": children, "mode": mode,
         "npart_l": npart[False], "npart_u": npart[True],
         "bytes_g": int(pos[False]) * 8, "bytes_gt": int(pos[True]) * 8,

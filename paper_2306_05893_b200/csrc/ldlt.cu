@@ -119,8 +119,8 @@ extern "C" int tsb_ldlt_create(const tsb_ldlt_desc *desc, tsb_ldlt_t *out) {
     using namespace tsb;
     return guard([&] {
         if (desc == nullptr || out == nullptr) throw Error(TSB_E_ARG, "null desc/out");
-        if (desc->max_v > kMaxV || desc->max_m > desc->max_v)
-            throw Error(TSB_E_ARG, "dissection block (m + |anc|) larger than the vector staging buffer");
+        if (desc->max_v > kMaxV || desc->max_v < 1)
+            throw Error(TSB_E_ARG, "item window larger than the vector staging buffer");
         if (desc->max_cb < 0 || desc->max_cb > 4096) throw Error(TSB_E_ARG, "bad contribution staging size");
         auto *h = new tsb_ldlt;
         h->d = *desc;

@@ -122,13 +122,16 @@ __device__ __forceinline__ void upper_exit(const tsb_ldlt_desc &D) {
     sweep_exit(D.d_ctl + 2, D.d_done_u, D.n_blocks, D.d_tcnt_upper, D.n_tiles_upper, D.d_pad, 0);
 }
 
-// dynamic shared memory of the sweep bodies
+constexpr int kFinRows = 1024;          // rows per piece of a mode-2 finalisation
+
+// dynamic shared memory of the sweep bodies (max_v = widest item window)
 inline size_t sweep_smem_lower(const tsb_ldlt_desc &D) {
-    return (size_t)(kStage + ((D.max_m + 2) & ~1) + ((D.max_cb + 1) & ~1)) * sizeof(double) +
-           (((D.max_m + 2) & ~1) + kMaxItemRows) * sizeof(int32_t);
+    const int offs = (D.max_v + 2 > kFinRows + 2 ? D.max_v + 2 : kFinRows + 2);
+    return (size_t)(kStage + ((D.max_v + 3) & ~1) + ((D.max_cb + 1) & ~1)) * sizeof(double) +
+           (((offs + 1) & ~1) + kMaxItemRows) * sizeof(int32_t);
 }
 inline size_t sweep_smem_upper(const tsb_ldlt_desc &D) {
-    return (size_t)(kStage + ((D.max_v + 2) & ~1)) * sizeof(double);
+    return (size_t)(kStage + ((D.max_v + 3) & ~1)) * sizeof(double);
 }
 
 // Sum of a row's contributions cb[a0, a1) in the fixed order every finaliser
@@ -225,6 +228,21 @@ __device__ __forceinline__ void stage_item(const Item &it, const tsb_ldlt_tile *
     }
 }
 
+// v-columns [w0, w1) an item reads (lim = width of its vector: m or m + na).
+__device__ __forceinline__ void item_window(const Item &it, const tsb_ldlt_tile *tiles, int lim, int &w0, int &w1) {
+    const tsb_ldlt_tile T0 = tiles[it.t0];
+    if (it.seg) {
+        const int p0 = (it.seg - 1) * kSegPairs, cnt = min(kSegPairs, T0.np - p0);
+        w0 = T0.tl + 2 * p0;
+        w1 = min(w0 + 2 * cnt, lim);
+    } else {
+        w0 = T0.tl;  // tiles are in row order: the first has the smallest tl
+        int hi = 0;
+        for (int t = it.t0; t < it.t1; ++t) hi = max(hi, tiles[t].tl + 2 * tiles[t].np);
+        w1 = min(hi, lim);
+    }
+}
+
 // GEMV of a staged item against the shared vector v (v[t] = column t).
 // emit(row, value) once per tile row (block-relative row index).  A segment
 // item of a large tile writes its 32 partial sums to the tile's scratch; the
@@ -288,10 +306,11 @@ template <bool TRACE>
 __device__ __forceinline__ void lower_sweep_body(const tsb_ldlt_desc &D, const SweepArgs &A, double *smem,
                                                  uint64_t *bars, uint32_t &phase) {
     double *stage = smem;
-    double *xs = smem + kStage;
-    double *cbs = xs + ((D.max_m + 2) & ~1);
+    double *xs = smem + kStage;                       // x_b over the item's window [w0, w1)
+    double *cbs = xs + ((D.max_v + 3) & ~1);
     int32_t *offs = reinterpret_cast<int32_t *>(cbs + ((D.max_cb + 1) & ~1));
-    int32_t *dsts = offs + ((D.max_m + 2) & ~1);
+    const int noffs = (D.max_v + 2 > kFinRows + 2 ? D.max_v + 2 : kFinRows + 2);
+    int32_t *dsts = offs + ((noffs + 1) & ~1);
     __shared__ int item_id, fin_parent;
     __shared__ double red[kSweepBlock];
     int32_t *ctl = D.d_ctl;
@@ -307,8 +326,11 @@ __device__ __forceinline__ void lower_sweep_body(const tsb_ldlt_desc &D, const S
         const Item it = items[iid];
         const tsb_ldlt_block B = D.d_blocks[it.block];
         const int m = B.m, s = B.start;
+        int w0, w1;
+        item_window(it, D.d_tiles_lower, m, w0, w1);
+        const int nw = w1 - w0;
         // everything that does not depend on the sweep's progress is fetched
-        // before the wait: the factor tiles (TMA), the block's input, the slots
+        // before the wait: the factor tiles (TMA), the window's input, the slots
         stage_item(it, D.d_tiles_lower, D.d_g, stage, bars);
         {
             struct In {
@@ -318,28 +340,30 @@ __device__ __forceinline__ void lower_sweep_body(const tsb_ldlt_desc &D, const S
                 __device__ double load(int j) const { return lower_input(A, s + j); }
                 __device__ void store(int j, double v) const { xs[j] = v; }
             };
-            batched(m, In{A, xs, s});
+            batched(nw, In{A, xs, s + w0});
         }
-        if (tid == 0) xs[m] = 0.0;  // column pad of odd-width tiles
+        if (tid == 0) xs[nw] = 0.0;  // column pad of odd-width tiles
         const tsb_ldlt_tile Tf = D.d_tiles_lower[it.t0], Tb = D.d_tiles_lower[it.t1 - 1];
-        const int r_lo = Tf.row0, r_hi = Tb.row0 + Tb.nrows;
-        const int mr0 = max(r_lo, m);
+        const int r_hi = Tb.row0 + Tb.nrows, mr0 = max(Tf.row0, m);
         for (int j = mr0 + tid; j < r_hi; j += kSweepBlock) dsts[j - mr0] = __ldg(D.d_cslot + B.anc_off + (j - m));
-        if (B.mode == 1)
-            for (int j = tid; j <= m; j += kSweepBlock) offs[j] = (int32_t)(__ldg(D.d_cin_ptr + s + j) - B.cb_off);
+        int64_t cb0 = 0;
+        if (B.mode == 1) {
+            cb0 = __ldg(D.d_cin_ptr + s + w0);
+            for (int j = tid; j <= nw; j += kSweepBlock) offs[j] = (int32_t)(__ldg(D.d_cin_ptr + s + w0 + j) - cb0);
+        }
         if (tid == 0) {
             if (B.mode == 1) spin_until_geq(D.d_cnt_l + it.block, B.target_l);
             else if (B.mode == 2) spin_until_geq(D.d_ready_l + it.block, 1);
         }
         __syncthreads();
         trace(tbuf, iid, 1);
-        // x_b = input - (contributions of the descendants)
+        // x_b = input - (contributions of the descendants) over the window
         if (B.mode == 1) {  // rows in pieces whose contributions fit the buffer
             int i0 = 0;
-            while (i0 < m) {
-                int i1 = m;
-                if (offs[m] - offs[i0] > D.max_cb) {
-                    int lo = i0 + 1, hi = m;
+            while (i0 < nw) {
+                int i1 = nw;
+                if (offs[nw] - offs[i0] > D.max_cb) {
+                    int lo = i0 + 1, hi = nw;
                     while (lo < hi) {
                         const int mid = (lo + hi + 1) >> 1;
                         if (offs[mid] - offs[i0] <= D.max_cb) lo = mid; else hi = mid - 1;
@@ -348,11 +372,11 @@ __device__ __forceinline__ void lower_sweep_body(const tsb_ldlt_desc &D, const S
                 }
                 const int base = offs[i0], cnt = offs[i1] - base;
                 const bool fits = cnt <= D.max_cb;
-                if (fits) stage_copy(cbs, D.d_cbuf + B.cb_off + base, cnt);
+                if (fits) stage_copy(cbs, D.d_cbuf + cb0 + base, cnt);
                 __syncthreads();
                 for (int j = i0 + tid; j < i1; j += kSweepBlock)
                     xs[j] = xs[j] - (fits ? contrib_sum<false>(cbs, offs[j] - base, offs[j + 1] - base)
-                                          : contrib_sum<true>(D.d_cbuf + B.cb_off, offs[j], offs[j + 1]));
+                                          : contrib_sum<true>(D.d_cbuf + cb0, offs[j], offs[j + 1]));
                 __syncthreads();
                 i0 = i1;
             }
@@ -363,18 +387,18 @@ __device__ __forceinline__ void lower_sweep_body(const tsb_ldlt_desc &D, const S
                 __device__ double load(int j) const { return __ldcg(src + j); }
                 __device__ void store(int j, double v) const { xs[j] = xs[j] - v; }
             };
-            batched(m, Sub{D.d_x + s, xs});
+            batched(nw, Sub{D.d_x + s + w0, xs});
         }
         __syncthreads();
         trace(tbuf, iid, 4);
         {
             auto emit = [&](int r, double a) {
                 if (r < m)
-                    A.x[s + r] = xs[r] + a;
+                    A.x[s + r] = a;  // unit diagonal stored: y_r = sum_{j <= r} Linv_rj x_j
                 else
                     D.d_cbuf[dsts[r - mr0]] = a;
             };
-            item_gemv(it, D.d_tiles_lower, stage, bars, phase, xs, red, D.d_part_lower, D.d_tcnt_lower, emit);
+            item_gemv(it, D.d_tiles_lower, stage, bars, phase, xs - w0, red, D.d_part_lower, D.d_tcnt_lower, emit);
         }
         trace(tbuf, iid, 5);
         __syncthreads();
@@ -396,14 +420,14 @@ __device__ __forceinline__ void lower_sweep_body(const tsb_ldlt_desc &D, const S
             // here (row-contiguous in cbuf; staged piece by piece with coalesced loads
             // together with the per-row offsets, one thread per row sums in order).
             const tsb_ldlt_block P = D.d_blocks[fin_parent];
-            int32_t *fo = reinterpret_cast<int32_t *>(xs);  // free: this item's GEMV is done
+            int32_t *fo = offs;
             const int64_t qe = P.cb_off + P.ncb;
             int i0 = 0;
             while (i0 < P.m) {
                 const int64_t qb = __ldg(D.d_cin_ptr + P.start + i0);
-                int i1 = P.m;
-                if (qe - qb > kStage) {  // rows [i0, i1) whose contributions fit (>= 1 row)
-                    int lo = i0 + 1, hi = P.m;
+                int i1 = min(P.m, i0 + kFinRows);
+                if (__ldg(D.d_cin_ptr + P.start + i1) - qb > kStage) {  // rows whose contributions fit (>= 1 row)
+                    int lo = i0 + 1, hi = i1;
                     while (lo < hi) {
                         const int mid = (lo + hi + 1) >> 1;
                         if (__ldg(D.d_cin_ptr + P.start + mid) - qb <= kStage) lo = mid; else hi = mid - 1;
@@ -422,6 +446,7 @@ __device__ __forceinline__ void lower_sweep_body(const tsb_ldlt_desc &D, const S
                 __syncthreads();
                 i0 = i1;
             }
+            (void)qe;
             if (tid == 0) {
                 __threadfence();
                 st_release(D.d_ready_l + fin_parent, 1);
@@ -444,7 +469,7 @@ template <bool TRACE>
 __device__ __forceinline__ void upper_sweep_body(const tsb_ldlt_desc &D, const SweepArgs &A, double *smem,
                                                  uint64_t *bars, uint32_t &phase) {
     double *stage = smem;
-    double *v = smem + kStage;
+    double *v = smem + kStage;  // [w_b; -z_anc] over the item's window [w0, w1)
     __shared__ int item_id;
     __shared__ double red[kSweepBlock];
     int32_t *ctl = D.d_ctl + 2;
@@ -460,37 +485,39 @@ __device__ __forceinline__ void upper_sweep_body(const tsb_ldlt_desc &D, const S
         const Item it = items[iid];
         const tsb_ldlt_block B = D.d_blocks[it.block];
         const int m = B.m, s = B.start, na = B.na;
+        int w0, w1;
+        item_window(it, D.d_tiles_upper, m + na, w0, w1);
+        const int nw = w1 - w0;
         stage_item(it, D.d_tiles_upper, D.d_gt, stage, bars);
-        const int t_lo = D.d_tiles_upper[it.t0].tl;
-        for (int t = t_lo + tid; t < m; t += kSweepBlock) {  // w_b: produced before this sweep
+        for (int t = w0 + tid; t < min(w1, m); t += kSweepBlock) {  // w_b: produced before this sweep
             double w = __ldcg(A.in + s + t);
             if (A.dscale) w = w / A.dscale[s + t];
-            v[t] = w;
+            v[t - w0] = w;
         }
-        for (int k = tid; k < na; k += kSweepBlock)  // ancestor rows, parked in v until the wait is over
-            v[m + k] = __longlong_as_double((long long)__ldg(D.d_anc + B.anc_off + k));
-        if (tid == 0) v[m + na] = 0.0;  // column pad of odd-width tiles
-        if (na > 0 && tid == 0) spin_until_geq(D.d_done_u + B.parent, D.d_blocks[B.parent].n_u);
+        const int k0 = max(w0, m) - m, k1 = w1 - m;  // ancestor entries in the window
+        for (int k = k0 + tid; k < k1; k += kSweepBlock)  // rows parked in v until the wait is over
+            v[m + k - w0] = __longlong_as_double((long long)__ldg(D.d_anc + B.anc_off + k));
+        if (tid == 0) v[nw] = 0.0;  // column pad of odd-width tiles
+        if (k1 > k0 && tid == 0) spin_until_geq(D.d_done_u + B.parent, D.d_blocks[B.parent].n_u);
         __syncthreads();
         trace(tbuf, iid, 1);
-        {
+        if (k1 > k0) {
             struct Anc {
                 const double *x;
                 double *va;
                 __device__ double load(int k) const { return __ldcg(x + __double_as_longlong(va[k])); }
                 __device__ void store(int k, double z) const { va[k] = -z; }
             };
-            batched(na, Anc{A.x, v + m});
+            batched(k1 - k0, Anc{A.x, v + (m + k0 - w0)});
         }
         __syncthreads();
         trace(tbuf, iid, 4);
         {
-            auto emit = [&](int c, double a) {
-                const double z = v[c] + a;
+            auto emit = [&](int c, double z) {  // unit diagonal stored: z_c = sum_{t >= c} G^T[c][t] v_t
                 A.x[s + c] = z;
                 if (A.out_perm) A.out[A.out_perm[s + c]] = z;
             };
-            item_gemv(it, D.d_tiles_upper, stage, bars, phase, v, red, D.d_part_upper, D.d_tcnt_upper, emit);
+            item_gemv(it, D.d_tiles_upper, stage, bars, phase, v - w0, red, D.d_part_upper, D.d_tcnt_upper, emit);
         }
         trace(tbuf, iid, 5);
         __syncthreads();

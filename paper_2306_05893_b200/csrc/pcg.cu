@@ -103,7 +103,7 @@ __device__ __forceinline__ double all_partials(const double *part, int kind, dou
 }
 
 template <int KIND>
-__global__ void __launch_bounds__(kPcgBlock)
+__global__ void __launch_bounds__(kPcgBlock, 3)
 pcg_persistent(PcgWork W, PcgArgs a, tsb_ldlt_desc D) {
     extern __shared__ __align__(128) double smem[];  // sweep staging (LDL^T)
     __shared__ double red[32];
@@ -333,7 +333,7 @@ static int occupancy_grid(size_t smem) {
     TSB_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
     if (per_sm < 1) throw Error(TSB_E_ARG, "pcg kernel does not fit on an SM");
     // barrier cost grows with the CTA count, latency hiding with it: tunable
-    int cap = KIND == TSB_PRECOND_LDLT ? 2 : 4;
+    int cap = KIND == TSB_PRECOND_LDLT ? 3 : 4;
     if (const char *env = getenv("TSB_PCG_CTAS_PER_SM")) cap = atoi(env) > 0 ? atoi(env) : cap;
     if (per_sm > cap) per_sm = cap;
     const int g = per_sm * nsm;

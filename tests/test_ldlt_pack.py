@@ -61,7 +61,7 @@ def emulate_lower(H, r):
             vals = d @ _padded(xs, tl + d.shape[1])[tl: tl + d.shape[1]]
             for row, a in zip(rows, vals):
                 if row < m:
-                    y[s + row] = xs[row] + a
+                    y[s + row] = a  # unit diagonal stored: y_r = sum_{j <= r} Linv_rj x_j
                 else:
                     cbuf[H["cslot"][B["anc_off"] + row - m]] = a
         p = int(B["parent"])
@@ -110,7 +110,7 @@ def emulate_upper(H, w):
                     continue
             cols, d, tl = _tile(H, True, t)
             vals = d @ _padded(v, tl + d.shape[1])[tl: tl + d.shape[1]]
-            z[s + cols] = v[cols] + vals
+            z[s + cols] = vals  # unit diagonal stored
         done[b] += 1
     assert np.all(done == blocks["n_u"])
     assert np.array_equal(segs, H["tiles_u"]["nseg"])
