@@ -1,0 +1,279 @@
+"""Nested-dissection sharding of the solve across GPUs.
+
+The reference has no distributed path; its domain decomposition is a solver
+structure only (`_dissect`, ndprecond.py:180-231): subtrees of the
+dissection are independent and couple only through their ancestor
+separators (`count_coupling_violations`, ndprecond.py:295-309).  That makes
+top-level subtrees the natural unit of distribution:
+
+  * rank g owns the rows (permuted order) of its subtrees -- their diagonal
+    blocks, their rows of A and their L panels;
+  * the separators above the cut ("top" blocks) are replicated on every rank.
+
+Per PCG iteration the only exchanges are sums over the top rows:
+  1. SpMV: a top row's entries span several subtrees; every rank adds the
+     products of its own columns (rank 0 also the top columns), then one
+     all-reduce over the top rows;
+  2. forward sweep: every rank solves its subtrees and pre-accumulates their
+     contributions into the top rows (the column-major pre-accumulation of
+     the paper); one all-reduce of those sums, then every rank solves the
+     replicated top blocks redundantly; the backward sweep needs no exchange
+     (top values are replicated and identical);
+  3. dots: owned rows on every rank, top rows on rank 0 only (weights), one
+     all-reduce of the packed scalars.
+
+Everything here is host setup or a CPU emulation of the device loop for the
+world_size > 1 tests (gloo); the device loop is `DistributedPcg`.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+
+def block_etree(factors):
+    """Block elimination tree of LdlFactors: parent(b) = owner of b's first
+    ancestor row (-1 = root), plus children lists (same rule as _ldlt_pack)."""
+    bfs = list(factors.blocks)
+    n = factors.plan.n
+    owner = np.full(n, -1, dtype=np.int64)
+    for i, bf in enumerate(bfs):
+        owner[bf.start:bf.stop] = i
+    parent = np.full(len(bfs), -1, dtype=np.int64)
+    for i, bf in enumerate(bfs):
+        if len(bf.anc):
+            parent[i] = owner[int(np.min(bf.anc))]
+    children = [[] for _ in bfs]
+    for i, p in enumerate(parent):
+        if p >= 0:
+            children[p].append(i)
+    return parent, children
+
+
+def block_weights(factors):
+    """Work per block: factor entries of its diagonal triangle and coupling panel."""
+    return np.array([(bf.stop - bf.start) * ((bf.stop - bf.start) + 1) / 2 + (bf.stop - bf.start) * len(bf.anc)
+                     for bf in factors.blocks])
+
+
+@dataclass
+class ShardPlan:
+    """Block -> rank map (-1 = replicated top block) and the row sets it induces."""
+
+    nranks: int
+    owner: np.ndarray          # [n_blocks] rank or -1
+    row_owner: np.ndarray      # [n] (permuted rows) rank or -1 (top)
+    top_rows: np.ndarray       # sorted permuted rows of the top blocks
+    load: np.ndarray           # [nranks] block weight per rank
+
+    def owned_rows(self, rank: int) -> np.ndarray:
+        return np.flatnonzero(self.row_owner == rank)
+
+    def weights(self, rank: int) -> np.ndarray:
+        """Dot-product weights in permuted order: owned rows 1, top rows 1 on rank 0 only."""
+        w = (self.row_owner == rank).astype(np.float64)
+        if rank == 0:
+            w[self.row_owner < 0] = 1.0
+        return w
+
+
+def shard_blocks(factors, nranks: int) -> ShardPlan:
+    """Cut the block elimination tree into >= nranks subtrees and assign them.
+
+    Repeatedly split the heaviest subtree (its root joins the replicated top)
+    until there are at least `nranks` subtrees, then assign subtrees to ranks
+    longest-processing-time first.  A separator can have more than two
+    children (disconnected halves, ndprecond.py:187-196), so the cut balances
+    by weight instead of assuming a binary tree."""
+    if nranks < 1:
+        raise ValueError("nranks must be >= 1")
+    parent, children = block_etree(factors)
+    w = block_weights(factors)
+    nb = len(w)
+    sub = w.copy()
+    for i in sorted(range(nb), key=lambda i: factors.blocks[i].start):  # children first
+        if parent[i] >= 0:
+            sub[parent[i]] += sub[i]
+    roots = [i for i in range(nb) if parent[i] < 0]
+    top = set()
+    front = list(roots)
+    while len(front) < nranks:
+        splittable = [r for r in front if children[r]]
+        if not splittable:
+            break
+        r = max(splittable, key=lambda r: sub[r])
+        front.remove(r)
+        top.add(r)
+        front.extend(children[r])
+    load = np.zeros(nranks)
+    root_rank = {}
+    for r in sorted(front, key=lambda r: -sub[r]):
+        g = int(np.argmin(load))
+        root_rank[r] = g
+        load[g] += sub[r]
+    owner = np.full(nb, -1, dtype=np.int64)
+    for i in sorted(range(nb), key=lambda i: -factors.blocks[i].start):  # parents first
+        if i in top:
+            owner[i] = -1
+        elif i in root_rank:
+            owner[i] = root_rank[i]
+        else:
+            owner[i] = owner[parent[i]]
+    n = factors.plan.n
+    row_owner = np.full(n, -1, dtype=np.int64)
+    for i, bf in enumerate(factors.blocks):
+        row_owner[bf.start:bf.stop] = owner[i]
+    return ShardPlan(nranks, owner, row_owner, np.flatnonzero(row_owner < 0), load)
+
+
+def permuted_matrix(a, perm):
+    """(row_ptr, col_ind, values) of P A P^T in CSR (columns sorted per row)."""
+    n = a.nrows
+    iperm = np.empty(n, dtype=np.int64)
+    iperm[perm] = np.arange(n)
+    rows = np.repeat(np.arange(n), np.diff(a.row_ptr))
+    pr, pc = iperm[rows], iperm[np.asarray(a.col_ind)]
+    order = np.lexsort((pc, pr))
+    row_ptr = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(np.bincount(pr, minlength=n), out=row_ptr[1:])
+    return row_ptr, pc[order], np.asarray(a.values)[order]
+
+
+def local_matrix(row_ptr, col_ind, values, plan: ShardPlan, rank: int):
+    """Rank-local CSR (permuted, full-size index space): owned rows complete,
+    top rows restricted to the rank's columns (rank 0 also the top columns),
+    every other row empty.  Raises if an owned row couples to another rank."""
+    n = len(row_ptr) - 1
+    rows = np.repeat(np.arange(n), np.diff(row_ptr))
+    ro = plan.row_owner
+    own_row = ro[rows] == rank
+    bad = own_row & (ro[col_ind] >= 0) & (ro[col_ind] != rank)
+    if np.any(bad):
+        raise ValueError("owned rows couple to another rank's subtree: not a dissection cut")
+    top_row = ro[rows] < 0
+    col_ok = (ro[col_ind] == rank) | ((ro[col_ind] < 0) & (rank == 0))
+    keep = own_row | (top_row & col_ok)
+    rp = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(np.bincount(rows[keep], minlength=n), out=rp[1:])
+    return rp, col_ind[keep], values[keep]
+
+
+# ---------------------------------------------------------------------------
+# CPU emulation of the distributed loop (world_size > 1 tests over gloo)
+# ---------------------------------------------------------------------------
+
+def _lower_blocks(factors, idx, r, ext=None):
+    """Forward sweep over the blocks `idx` (start order): y = L^{-1} r on their
+    rows; contributions to rows outside them returned in `ext` (summed)."""
+    y = np.array(r, dtype=np.float64)
+    if ext is not None:
+        y = y - ext
+    out = np.zeros_like(y)
+    mine = np.zeros(len(y), dtype=bool)
+    for i in idx:
+        mine[factors.blocks[i].start:factors.blocks[i].stop] = True
+    for i in sorted(idx, key=lambda i: factors.blocks[i].start):
+        bf = factors.blocks[i]
+        s, e = bf.start, bf.stop
+        from scipy.linalg import solve_triangular
+
+        seg = solve_triangular(bf.l11, y[s:e], lower=True, unit_diagonal=True)
+        y[s:e] = seg
+        if len(bf.anc):
+            c = bf.l21 @ seg
+            inside = mine[bf.anc]
+            y[bf.anc[inside]] -= c[inside]
+            out[bf.anc[~inside]] += c[~inside]
+    return y, out
+
+
+def _upper_blocks(factors, idx, w, z):
+    """Backward sweep over the blocks `idx` (reverse start order) into z."""
+    from scipy.linalg import solve_triangular
+
+    for i in sorted(idx, key=lambda i: -factors.blocks[i].start):
+        bf = factors.blocks[i]
+        s, e = bf.start, bf.stop
+        seg = w[s:e].copy()
+        if len(bf.anc):
+            seg -= bf.l21.T @ z[bf.anc]
+        z[s:e] = solve_triangular(bf.l11, seg, lower=True, unit_diagonal=True, trans="T")
+    return z
+
+
+def emulate_pcg(a, b, factors, plan: ShardPlan, rank: int, allreduce, tol=1e-9, max_it=1000):
+    """One rank of the distributed PCG, NumPy kernels; `allreduce(np.ndarray)`
+    sums over ranks in place.  Works in permuted order like the device loop;
+    returns (x in original order, iterations, final residual, converged)."""
+    perm = np.asarray(factors.plan.perm)
+    n = len(perm)
+    rp, ci, va = permuted_matrix(a, perm)
+    lrp, lci, lva = local_matrix(rp, ci, va, plan, rank)
+    wgt = plan.weights(rank)
+    top = plan.top_rows
+    mine = [i for i in range(len(factors.blocks)) if plan.owner[i] == rank]
+    tops = [i for i in range(len(factors.blocks)) if plan.owner[i] < 0]
+    valid = (plan.row_owner == rank) | (plan.row_owner < 0)
+
+    def spmv(p):
+        y = np.zeros(n)
+        nz = np.flatnonzero(np.diff(lrp))
+        y[nz] = np.add.reduceat(lva * p[lci], lrp[:-1][nz]) if len(lci) else 0.0
+        seg = y[top].copy()
+        allreduce(seg)
+        y[top] = seg
+        return y
+
+    def dot(u, v):
+        s = np.array([np.sum(wgt * u * v)])
+        allreduce(s)
+        return float(s[0])
+
+    def precond(r):
+        y, ext = _lower_blocks(factors, mine, np.where(valid, r, 0.0))
+        ext_top = ext[top].copy()
+        allreduce(ext_top)
+        e = np.zeros(n)
+        e[top] = ext_top
+        y2, _ = _lower_blocks(factors, tops, np.where(plan.row_owner < 0, r, 0.0), ext=e)
+        y = np.where(plan.row_owner < 0, y2, y)
+        wv = y / factors.d
+        z = np.zeros(n)
+        _upper_blocks(factors, tops, wv, z)
+        _upper_blocks(factors, mine, wv, z)
+        return np.where(valid, z, 0.0)
+
+    bp = np.asarray(b, dtype=np.float64)[perm]
+    x = np.zeros(n)
+    bnorm = np.sqrt(dot(bp, bp))
+    if bnorm == 0.0:
+        return np.zeros(n), 0, 0.0, True
+    r = np.where(valid, bp, 0.0)
+    res = np.sqrt(dot(r, r)) / bnorm
+    if res <= tol:
+        return np.zeros(n), 0, res, True
+    z = precond(r)
+    p = z.copy()
+    rz = dot(r, z)
+    it, conv = 0, False
+    while it < max_it:
+        ap = spmv(p)
+        alpha = rz / dot(p, ap)
+        x = x + alpha * p
+        r = r - alpha * ap
+        it += 1
+        res = np.sqrt(dot(r, r)) / bnorm
+        if res <= tol:
+            conv = True
+            break
+        z = precond(r)
+        rz_new = dot(r, z)
+        p = z + (rz_new / rz) * p
+        rz = rz_new
+    xg = wgt * x  # every rank contributes its owned rows (rank 0 the top rows)
+    allreduce(xg)
+    xo = np.zeros(n)
+    xo[perm] = xg
+    return xo, it, res, conv
