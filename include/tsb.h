@@ -237,6 +237,8 @@ typedef struct tsb_ldlt_desc {
     int32_t *d_tcnt_lower;        /* [n_tiles_lower] segment counters (zeroed)      */
     int32_t *d_tcnt_upper;        /* [n_tiles_upper]                                */
     int64_t n_tiles_lower, n_tiles_upper;
+    const int32_t *d_ext_rows;    /* rows outside the handle's blocks that receive  */
+    int64_t n_ext;                /* contributions (block subsets of a shard)        */
     int32_t *d_ctl;               /* [4] tickets / exit counters (zeroed)          */
     int64_t *d_trace_lower;       /* optional [n_items_lower][8] item timeline     */
     int64_t *d_trace_upper;       /* optional [n_items_upper][8]                   */
@@ -252,6 +254,29 @@ int tsb_ldlt_lower(tsb_ldlt_t h, const double *d_r, double *d_y, void *stream);
 int tsb_ldlt_upper(tsb_ldlt_t h, const double *d_w, double *d_z, void *stream);
 /* z = P^T L^{-T} D^{-1} L^{-1} P r, original order     (apply)       */
 int tsb_ldlt_apply(tsb_ldlt_t h, const double *d_r, double *d_z, void *stream);
+/* Block subsets (one rank's shard, paper_2306_05893_b200/shard.py), permuted order:
+ * y = L^{-1} (r - ext) on the handle's blocks (d_ext may be NULL) */
+int tsb_ldlt_lower_ext(tsb_ldlt_t h, const double *d_r, const double *d_ext, double *d_y, void *stream);
+/* z = L^{-T} D^{-1} y on the handle's blocks; z of ancestor rows outside them
+ * is read from d_z (solved before) */
+int tsb_ldlt_upper_scaled(tsb_ldlt_t h, const double *d_y, double *d_z, void *stream);
+/* after a lower sweep: d_out[row] = sum of the contributions to each external
+ * row (d_ext_rows), fixed order */
+int tsb_ldlt_external_sums(tsb_ldlt_t h, double *d_out, void *stream);
+
+/* ------------------------------------------------------------------------
+ * Vector kernels of the sharded PCG (shard.py): weights w = 1 on owned rows
+ * (top rows on rank 0 only); d_part scratch of 2 * 148 doubles.
+ * ---------------------------------------------------------------------- */
+int tsb_wdot(int64_t n, const double *d_w, const double *d_a, const double *d_b, double *d_part,
+             double *d_out, void *stream);
+/* alpha = d_sc[0] / d_sc[1]; x += alpha p; r -= alpha ap; d_out[0] = sum w r^2 */
+int tsb_pcg_update(int64_t n, const double *d_w, double *d_x, const double *d_p, double *d_r,
+                   const double *d_ap, const double *d_sc, double *d_part, double *d_out, void *stream);
+/* beta = d_sc[0] / d_sc[1]; p = z + beta p; d_sc[1] = d_sc[0] */
+int tsb_pcg_direction(int64_t n, double *d_p, const double *d_z, double *d_sc, void *stream);
+int tsb_gather_rows(int64_t m, const int32_t *d_idx, const double *d_src, double *d_dst, void *stream);
+int tsb_scatter_rows(int64_t m, const int32_t *d_idx, const double *d_src, double *d_dst, void *stream);
 
 /* ------------------------------------------------------------------------
  * Device-resident preconditioned CG      replaces krylov.pcg / krylov.cg

@@ -55,6 +55,7 @@ TILE = 32               # rows per tile (one per lane)
 ITEM_BYTES = 48 * 1024  # small-tile item budget: one TMA bulk copy
 SEG_PAIRS = 96          # pairs per segment item of a large tile (96 * 32 * 16 B = 48 KB)
 WARPS = 8               # warps per CTA (csrc kSweepBlock / 32)
+MERGE_ROWS = 0          # default subtree amalgamation (rows); 0 = off
 CB_CAP = 2048           # contributions staged per piece when a block's items sum them (csrc max_cb)
 
 BLOCK_DTYPE = np.dtype([
@@ -133,6 +134,100 @@ def untile(tiles, data, nrows, ncols):
     return out[:, :ncols]
 
 
+class _Merged:
+    """Block factor of an amalgamated subtree (duck-types ndprecond._BlockFactor)."""
+
+    def __init__(self, start, stop, level, anc, l11, l21, tile=16):
+        self.start, self.stop, self.level, self.anc = start, stop, level, anc
+        self.l11, self.l21, self.tile = l11, l21, tile
+
+    @property
+    def tile_inv(self):  # only the CPU oracle reads these
+        from .ndprecond import _tile_inverses
+
+        return _tile_inverses(self.l11, self.tile)
+
+
+class _MergedFactors:
+    def __init__(self, factors, blocks):
+        self.plan, self.d, self.blocks = factors.plan, factors.d, blocks
+        nlev = 1 + max((b.level for b in blocks), default=0)
+        self.levels = [[b for b in blocks if b.level == lv] for lv in range(nlev)]
+
+
+def amalgamate(factors, max_rows: int):
+    """Merge every elimination subtree of <= max_rows rows into one block.
+
+    In dissection order a subtree owns the contiguous rows [tree_start, stop)
+    and couples outside only to its root's ancestors (fill property), so the
+    merged block is L restricted to those rows (dense unit-lower l11 holding
+    the constituents' l11 and their in-subtree l21 rows) with the root's
+    ancestors as coupling rows.  Mathematically the same L; after packing one
+    GEMV replaces a whole subtree, cutting the dependency chain (one hop per
+    merged subtree instead of one per level) at the price of the subtree's
+    dense triangle.  Returns the factors unchanged when nothing merges."""
+    bfs = list(factors.blocks)
+    nb = len(bfs)
+    if max_rows <= 0 or nb == 0:
+        return factors
+    n = factors.plan.n
+    owner = np.full(n, -1, dtype=np.int64)
+    for i, bf in enumerate(bfs):
+        owner[bf.start:bf.stop] = i
+    parent = np.full(nb, -1, dtype=np.int64)
+    for i, bf in enumerate(bfs):
+        if len(bf.anc):
+            parent[i] = owner[int(np.min(bf.anc))]
+    children = [[] for _ in range(nb)]
+    for i in range(nb):
+        if parent[i] >= 0:
+            children[parent[i]].append(i)
+    order = sorted(range(nb), key=lambda i: bfs[i].start)
+    rows = np.array([bf.stop - bf.start for bf in bfs], dtype=np.int64)
+    ts = np.array([bf.start for bf in bfs], dtype=np.int64)
+    ok = np.zeros(nb, dtype=bool)
+    for i in order:  # children first
+        for c in children[i]:
+            rows[i] += rows[c]
+            ts[i] = min(ts[i], ts[c])
+        ok[i] = rows[i] <= max_rows and all(ok[c] for c in children[i])
+        if ok[i] and rows[i] != bfs[i].stop - ts[i]:
+            ok[i] = False  # not contiguous: leave the subtree as it is
+    roots = [i for i in order if ok[i] and children[i] and (parent[i] < 0 or not ok[parent[i]])]
+    if not roots:
+        return factors
+    gone = set()
+    new_blocks = []
+    for b in roots:
+        sub, stack = [], [b]
+        while stack:
+            i = stack.pop()
+            sub.append(i)
+            stack.extend(children[i])
+        gone.update(sub)
+        s0, e0 = int(ts[b]), bfs[b].stop
+        m = e0 - s0
+        anc = np.asarray(bfs[b].anc, dtype=np.int64)
+        l11 = np.zeros((m, m))
+        l21 = np.zeros((len(anc), m))
+        for i in sub:
+            bf = bfs[i]
+            cs, ce = bf.start - s0, bf.stop - s0
+            l11[cs:ce, cs:ce] = np.tril(bf.l11)
+            if len(bf.anc):
+                a = np.asarray(bf.anc, dtype=np.int64)
+                inside = a < e0
+                l11[a[inside] - s0, cs:ce] = bf.l21[inside]
+                k = np.searchsorted(anc, a[~inside])
+                if np.any(k >= len(anc)) or np.any(anc[np.minimum(k, len(anc) - 1)] != a[~inside]):
+                    raise ValueError("subtree couples outside its root's ancestors")
+                l21[k, cs:ce] = bf.l21[~inside]
+        new_blocks.append(_Merged(s0, e0, bfs[b].level, anc, l11, l21, getattr(bfs[b], "tile", 16)))
+    blocks = [bf for i, bf in enumerate(bfs) if i not in gone] + new_blocks
+    blocks.sort(key=lambda bf: bf.start)
+    return _MergedFactors(factors, blocks)
+
+
 def _items(tiles_of_block, first_tile):
     """Group a block's tiles into items -> list of (t0, t1, seg) in global tile ids
     (seg = 0: whole small tiles; seg = s + 1: column segment s of one large tile)."""
@@ -158,11 +253,16 @@ def _items(tiles_of_block, first_tile):
     return out
 
 
-def pack(factors):
-    """Host arrays of the tiled block-inverse layout + item lists (pure NumPy)."""
+def pack(factors, subset=None):
+    """Host arrays of the tiled block-inverse layout + item lists (pure NumPy).
+
+    `subset` (block indices) packs one shard: ancestor rows outside the subset
+    are external (their contributions are summed by tsb_ldlt_external_sums,
+    their z is read from the output vector) and blocks whose parent is outside
+    become roots of the handle."""
     plan = factors.plan
     n = plan.n
-    bfs = list(factors.blocks)
+    bfs = list(factors.blocks) if subset is None else [factors.blocks[i] for i in sorted(subset)]
     nb = len(bfs)
     # block elimination tree: parent(b) = owner of b's first ancestor row.  The
     # fill property  anc(b) \ rows(parent) <= anc(parent)  makes "all children
@@ -275,6 +375,7 @@ def pack(factors):
     np.cumsum(np.bincount(anc_all, minlength=n), out=cin_ptr[1:])
     cslot = np.empty(len(anc_all), dtype=np.int64)
     cslot[corder] = np.arange(len(anc_all))
+    ext_rows = np.unique(anc_all[owner[anc_all] < 0]) if len(anc_all) else np.zeros(0, dtype=np.int64)
 
     # ---------------- block table ----------------
     blocks = np.zeros(nb, dtype=BLOCK_DTYPE)
@@ -319,7 +420,7 @@ def pack(factors):
         "d": np.asarray(factors.d, dtype=np.float64), "perm": np.asarray(plan.perm, dtype=np.int64),
         "max_m": int(ms_.max()) if nb else 1, "max_v": int(max_w), "max_cb": max_cb,
         "parent": parent, "children": children, "mode": mode,
-        "npart_l": npart[False], "npart_u": npart[True],
+        "npart_l": npart[False], "npart_u": npart[True], "ext_rows": ext_rows,
         "bytes_g": int(pos[False]) * 8, "bytes_gt": int(pos[True]) * 8,
     }
 
@@ -327,9 +428,11 @@ def pack(factors):
 class DevicePanels:
     """Packed factor image in HBM + the libtsb handle (tsb_ldlt_create)."""
 
-    def __init__(self, factors, stream=None, trace=False, force_mode=None):
+    def __init__(self, factors, stream=None, trace=False, force_mode=None, subset=None, merge=None):
         t = _lib.require_cuda()
-        H = pack(factors)
+        if merge is None:
+            merge = MERGE_ROWS if subset is None else 0
+        H = pack(amalgamate(factors, merge) if merge else factors, subset)
         if force_mode is not None:  # testing: route every inner block through one input mode
             inner = H["blocks"]["mode"] != MODE_LEAF
             H["blocks"]["mode"][inner] = force_mode
@@ -353,7 +456,7 @@ class DevicePanels:
                 "blocks": raw(H["blocks"]), "items_l": up(nz(items_l.ravel())), "items_u": up(nz(items_u.ravel())),
                 "tiles_l": raw(H["tiles_l"]), "tiles_u": raw(H["tiles_u"]), "g": up(H["g"]), "gt": up(H["gt"]),
                 "anc": i32(nz(H["anc"])), "cslot": i32(nz(H["cslot"])), "cin_ptr": i64(H["cin_ptr"]),
-                "d": up(H["d"]), "perm": i32(H["perm"]),
+                "d": up(H["d"]), "perm": i32(H["perm"]), "ext_rows": i32(nz(H["ext_rows"])),
             }
             ntl, ntu = len(H["tiles_l"]), len(H["tiles_u"])
             self.t.update(cbuf=z(H["ncbuf"], t.float64), x=z(n, t.float64), y=z(n, t.float64),
@@ -375,7 +478,7 @@ class DevicePanels:
             d_perm=tp("perm"), d_cbuf=tp("cbuf"), d_x=tp("x"), d_y=tp("y"),
             d_part_lower=tp("part"), d_part_upper=_lib.ptr(self.t["part"][TILE * H["npart_l"]:]),
             d_tcnt_lower=tp("tcnt"), d_tcnt_upper=_lib.ptr(self.t["tcnt"][ntl:]),
-            n_tiles_lower=ntl, n_tiles_upper=ntu,
+            n_tiles_lower=ntl, n_tiles_upper=ntu, d_ext_rows=tp("ext_rows"), n_ext=len(H["ext_rows"]),
             d_cnt_l=cp(0, nb), d_ready_l=cp(nb, 2 * nb), d_done_u=cp(2 * nb, 3 * nb), d_pad=tp("ctl"),
             d_ctl=tp("ctl"),
             d_trace_lower=_lib.ptr(self.trace_l) if trace else None,
@@ -397,8 +500,15 @@ class DevicePanels:
 
     def run(self, mode: str, r, out):
         fn = {"lower": self._lib.tsb_ldlt_lower, "upper": self._lib.tsb_ldlt_upper,
-              "apply": self._lib.tsb_ldlt_apply}[mode]
+              "apply": self._lib.tsb_ldlt_apply, "upper_scaled": self._lib.tsb_ldlt_upper_scaled}[mode]
         _lib.check(fn(self.h, _lib.ptr(r), _lib.ptr(out), _lib.stream_ptr()), f"ldlt_{mode}")
+
+    def lower_ext(self, r, ext, out):
+        _lib.check(self._lib.tsb_ldlt_lower_ext(self.h, _lib.ptr(r), _lib.ptr(ext), _lib.ptr(out), _lib.stream_ptr()),
+                   "ldlt_lower_ext")
+
+    def external_sums(self, out):
+        _lib.check(self._lib.tsb_ldlt_external_sums(self.h, _lib.ptr(out), _lib.stream_ptr()), "ldlt_external_sums")
 
 
 class _NullCtx:

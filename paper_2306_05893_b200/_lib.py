@@ -64,7 +64,8 @@ class LdltDesc(C.Structure):
         ("d_cbuf", c_vp), ("d_x", c_vp), ("d_y", c_vp),
         ("d_cnt_l", c_vp), ("d_ready_l", c_vp), ("d_done_u", c_vp), ("d_pad", c_vp),
         ("d_part_lower", c_vp), ("d_part_upper", c_vp), ("d_tcnt_lower", c_vp), ("d_tcnt_upper", c_vp),
-        ("n_tiles_lower", c_i64), ("n_tiles_upper", c_i64), ("d_ctl", c_vp),
+        ("n_tiles_lower", c_i64), ("n_tiles_upper", c_i64), ("d_ext_rows", c_vp), ("n_ext", c_i64),
+        ("d_ctl", c_vp),
         ("d_trace_lower", c_vp), ("d_trace_upper", c_vp),
     ]
 
@@ -94,6 +95,14 @@ _SIGNATURES = {
     "tsb_ldlt_lower": (C.c_int, [c_vp, c_vp, c_vp, c_vp]),
     "tsb_ldlt_upper": (C.c_int, [c_vp, c_vp, c_vp, c_vp]),
     "tsb_ldlt_apply": (C.c_int, [c_vp, c_vp, c_vp, c_vp]),
+    "tsb_ldlt_lower_ext": (C.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "tsb_ldlt_upper_scaled": (C.c_int, [c_vp, c_vp, c_vp, c_vp]),
+    "tsb_ldlt_external_sums": (C.c_int, [c_vp, c_vp, c_vp]),
+    "tsb_wdot": (C.c_int, [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "tsb_pcg_update": (C.c_int, [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "tsb_pcg_direction": (C.c_int, [c_i64, c_vp, c_vp, c_vp, c_vp]),
+    "tsb_gather_rows": (C.c_int, [c_i64, c_vp, c_vp, c_vp, c_vp]),
+    "tsb_scatter_rows": (C.c_int, [c_i64, c_vp, c_vp, c_vp, c_vp]),
     "tsb_pcg_create": (C.c_int, [c_i64, C.POINTER(c_vp)]),
     "tsb_pcg_destroy": (C.c_int, [c_vp]),
     "tsb_pcg_solve": (C.c_int, [c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, c_vp,

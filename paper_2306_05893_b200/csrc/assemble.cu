@@ -203,24 +203,37 @@ block_kernel(int64_t nb, const int4 *__restrict__ blk, const int32_t *__restrict
             acc[8] = add(acc[8], mv);
         }
     }
-    for (int k = info.z; k < info.w; ++k) {
-        const int c = __ldg(list + k);
-        const int64_t e = c >> 4;
-        const int a = (c >> 2) & 3, b = c & 3;
-        const double *we = work + e * kWork;
-        double ga[3], gb[3], ra[3], rb[3];
+    // contributions in ascending element order; the loads of U contributions
+    // are issued before their (ordered) accumulation
+    constexpr int U = 4;
+    for (int k0 = info.z; k0 < info.w; k0 += U) {
+        double ga[U][3], gb[U][3], G[U], V[U];
 #pragma unroll
-        for (int i = 0; i < 3; ++i) {
-            ga[i] = __ldg(we + 3 * a + i);
-            gb[i] = __ldg(we + 3 * b + i);
-            ra[i] = __ldg(grads + e * 12 + 3 * a + i);
-            rb[i] = __ldg(grads + e * 12 + 3 * b + i);
+        for (int u = 0; u < U; ++u) {
+            const int k = k0 + u < info.w ? k0 + u : info.w - 1;
+            const int c = __ldg(list + k);
+            const int64_t e = c >> 4;
+            const int a = (c >> 2) & 3, b = c & 3;
+            const double *we = work + e * kWork;
+            double ra[3], rb[3];
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+                ga[u][i] = __ldg(we + 3 * a + i);
+                gb[u][i] = __ldg(we + 3 * b + i);
+                ra[i] = __ldg(grads + e * 12 + 3 * a + i);
+                rb[i] = __ldg(grads + e * 12 + 3 * b + i);
+            }
+            G[u] = ra[0] * rb[0] + ra[1] * rb[1] + ra[2] * rb[2];
+            V[u] = __ldg(vol + e);
         }
-        const double G = ra[0] * rb[0] + ra[1] * rb[1] + ra[2] * rb[2];
-        double kb[9];
-        rot_block(ga, gb, G, __ldg(vol + e), lam, mu, kb);
 #pragma unroll
-        for (int q = 0; q < 9; ++q) acc[q] = add(acc[q], mul(ck, kb[q]));
+        for (int u = 0; u < U; ++u) {
+            if (k0 + u >= info.w) break;
+            double kb[9];
+            rot_block(ga[u], gb[u], G[u], V[u], lam, mu, kb);
+#pragma unroll
+            for (int q = 0; q < 9; ++q) acc[q] = add(acc[q], mul(ck, kb[q]));
+        }
     }
 #pragma unroll
     for (int i = 0; i < 3; ++i)
@@ -241,13 +254,30 @@ node_kernel(int64_t N, const int32_t *__restrict__ node_ptr, const int32_t *__re
     if (!finite3(x[3 * I], x[3 * I + 1], x[3 * I + 2])) atomicOr(flags, 1);
     double f[3] = {0.0, 0.0, 0.0}, k[3] = {0.0, 0.0, 0.0};
     const int lo = __ldg(node_ptr + I), hi = __ldg(node_ptr + I + 1);
-    for (int q = lo; q < hi; ++q) {
-        const int c = __ldg(node_list + q);
-        const double *we = work + (int64_t)(c >> 2) * kWork + 3 * (c & 3);
+    // incident elements in ascending order (np.bincount's order); the loads of
+    // U incidences are issued before their ordered accumulation
+    constexpr int U = 4;
+    for (int q0 = lo; q0 < hi; q0 += U) {
+        double fv[U][3], kv_[U][3];
 #pragma unroll
-        for (int i = 0; i < 3; ++i) {
-            f[i] = add(f[i], __ldg(we + 12 + i));
-            k[i] = add(k[i], __ldg(we + 24 + i));
+        for (int u = 0; u < U; ++u) {
+            const int q = q0 + u < hi ? q0 + u : hi - 1;
+            const int c = __ldg(node_list + q);
+            const double *we = work + (int64_t)(c >> 2) * kWork + 3 * (c & 3);
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+                fv[u][i] = __ldg(we + 12 + i);
+                kv_[u][i] = __ldg(we + 24 + i);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (q0 + u >= hi) break;
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+                f[i] = add(f[i], fv[u][i]);
+                k[i] = add(k[i], kv_[u][i]);
+            }
         }
     }
 #pragma unroll

@@ -110,6 +110,31 @@ void ldlt_enqueue(tsb_ldlt_t h, int mode, const double *r, double *out, const in
     }
 }
 
+__global__ void ext_sums_kernel(tsb_ldlt_desc D, double *out) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < D.n_ext; i += (int64_t)gridDim.x * blockDim.x) {
+        const int row = D.d_ext_rows[i];
+        out[row] = contrib_sum<true>(D.d_cbuf, D.d_cin_ptr[row], D.d_cin_ptr[row + 1]);
+    }
+}
+
+void ldlt_enqueue_ext(tsb_ldlt_t h, int mode, const double *r, const double *ext, double *out, cudaStream_t st) {
+    tsb_ldlt_desc &D = h->d;
+    if (D.n == 0 || D.n_blocks == 0) return;
+    if (mode == 0) {  // lower with external contributions
+        SweepArgs a{r, nullptr, nullptr, out, nullptr, nullptr, nullptr, ext};
+        launch_coop(lower_sweep<false>, D.grid, sweep_smem_lower(D), st, D, a);
+    } else if (mode == 1) {  // upper with D scaling, in place into out (permuted)
+        SweepArgs a{r, nullptr, D.d_d, out, nullptr, nullptr, nullptr, nullptr};
+        launch_coop(upper_sweep<false>, D.grid, sweep_smem_upper(D), st, D, a);
+    } else {
+        if (D.n_ext == 0) return;
+        int g = (int)((D.n_ext + 255) / 256);
+        if (g > kNumSM * 4) g = kNumSM * 4;
+        ext_sums_kernel<<<g, 256, 0, st>>>(D, out);
+        TSB_LAUNCHED();
+    }
+}
+
 const tsb_ldlt_desc &ldlt_desc(tsb_ldlt_t h) { return h->d; }
 uint64_t ldlt_serial(tsb_ldlt_t h) { return h->serial; }
 
@@ -166,4 +191,16 @@ extern "C" int tsb_ldlt_upper(tsb_ldlt_t h, const double *d_w, double *d_z, void
 
 extern "C" int tsb_ldlt_apply(tsb_ldlt_t h, const double *d_r, double *d_z, void *stream) {
     return tsb::guard([&] { tsb::ldlt_enqueue(h, 2, d_r, d_z, nullptr, tsb::as_stream(stream)); });
+}
+
+extern "C" int tsb_ldlt_lower_ext(tsb_ldlt_t h, const double *d_r, const double *d_ext, double *d_y, void *stream) {
+    return tsb::guard([&] { tsb::ldlt_enqueue_ext(h, 0, d_r, d_ext, d_y, tsb::as_stream(stream)); });
+}
+
+extern "C" int tsb_ldlt_upper_scaled(tsb_ldlt_t h, const double *d_y, double *d_z, void *stream) {
+    return tsb::guard([&] { tsb::ldlt_enqueue_ext(h, 1, d_y, nullptr, d_z, tsb::as_stream(stream)); });
+}
+
+extern "C" int tsb_ldlt_external_sums(tsb_ldlt_t h, double *d_out, void *stream) {
+    return tsb::guard([&] { tsb::ldlt_enqueue_ext(h, 2, nullptr, nullptr, d_out, tsb::as_stream(stream)); });
 }

@@ -92,6 +92,7 @@ struct SweepArgs {
     const int32_t *out_perm; // upper apply: scatter z through perm
     double *out;             // upper apply: output in original order
     const int32_t *done;     // stop flag (skip the sweep when set)
+    const double *ext;       // lower: contributions from outside the handle's blocks (subtracted), or NULL
 };
 
 // Exit protocol: the last CTA out zeroes the counters for the next replay.
@@ -289,7 +290,8 @@ __device__ __forceinline__ void item_gemv(const Item &it, const tsb_ldlt_tile *t
 }
 
 __device__ __forceinline__ double lower_input(const SweepArgs &A, int row) {
-    return __ldcg(A.in + (A.in_perm ? A.in_perm[row] : row));  // may be produced in-kernel (L2)
+    const double v = __ldcg(A.in + (A.in_perm ? A.in_perm[row] : row));  // may be produced in-kernel (L2)
+    return A.ext ? v - __ldcg(A.ext + row) : v;
 }
 
 // ---------------------------------------------------------------------------
@@ -498,7 +500,8 @@ __device__ __forceinline__ void upper_sweep_body(const tsb_ldlt_desc &D, const S
         for (int k = k0 + tid; k < k1; k += kSweepBlock)  // rows parked in v until the wait is over
             v[m + k - w0] = __longlong_as_double((long long)__ldg(D.d_anc + B.anc_off + k));
         if (tid == 0) v[nw] = 0.0;  // column pad of odd-width tiles
-        if (k1 > k0 && tid == 0) spin_until_geq(D.d_done_u + B.parent, D.d_blocks[B.parent].n_u);
+        if (k1 > k0 && B.parent >= 0 && tid == 0)  // parent outside the handle (shard): solved before
+            spin_until_geq(D.d_done_u + B.parent, D.d_blocks[B.parent].n_u);
         __syncthreads();
         trace(tbuf, iid, 1);
         if (k1 > k0) {

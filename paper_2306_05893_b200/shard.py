@@ -277,3 +277,158 @@ def emulate_pcg(a, b, factors, plan: ShardPlan, rank: int, allreduce, tol=1e-9, 
     xo = np.zeros(n)
     xo[perm] = xg
     return xo, it, res, conv
+
+
+# ---------------------------------------------------------------------------
+# device loop (one process per GPU; torch.distributed for the all-reduces)
+# ---------------------------------------------------------------------------
+
+class DistributedPcg:
+    """Sharded PCG with the nested-dissection LDL^T preconditioner.
+
+    Every rank runs the libtsb kernels on its shard (permuted order, full-length
+    vectors, only owned + top rows live): rank-local SpMV (tsb_spmv), the
+    subtree sweeps and the replicated top sweeps (tsb_ldlt_lower_ext /
+    tsb_ldlt_upper_scaled over block subsets), weighted dots and the fused
+    vector updates (tsb_pcg_update / tsb_pcg_direction, alpha and beta on the
+    device).  Exchanges: one all-reduce of the top rows after the SpMV and one
+    after the subtree forward sweep, plus the packed scalars; the host reads
+    the residual norm once per iteration for the stop test.  `allreduce`
+    defaults to torch.distributed.all_reduce (NCCL over NVLink between GPUs).
+    """
+
+    def __init__(self, a, factors, rank=None, world=None, allreduce=None):
+        from . import _lib
+        from ._ldlt_pack import DevicePanels
+
+        t = _lib.require_cuda()
+        if rank is None or world is None:
+            import torch.distributed as dist
+
+            rank = dist.get_rank() if dist.is_initialized() else 0
+            world = dist.get_world_size() if dist.is_initialized() else 1
+        if allreduce is None:
+            import torch.distributed as dist
+
+            allreduce = (lambda x: dist.all_reduce(x)) if world > 1 else (lambda x: None)
+        self.rank, self.world, self.allreduce = rank, world, allreduce
+        self.factors = factors
+        self.plan = shard_blocks(factors, world)
+        perm = np.asarray(factors.plan.perm)
+        self.n = n = len(perm)
+        rp, ci, va = permuted_matrix(a, perm)
+        lrp, lci, lva = local_matrix(rp, ci, va, self.plan, rank)
+        dev = lambda x, dt: t.from_numpy(np.ascontiguousarray(x, dtype=dt)).cuda()  # noqa: E731
+        self.rp, self.ci, self.va = dev(lrp, np.int32), dev(lci, np.int32), dev(lva, np.float64)
+        self.w = dev(self.plan.weights(rank), np.float64)
+        self.top = dev(self.plan.top_rows, np.int32)
+        self.perm = dev(perm, np.int32)
+        iperm = np.empty(n, dtype=np.int64)
+        iperm[perm] = np.arange(n)
+        self.iperm = dev(iperm, np.int32)
+        mine = [i for i in range(len(factors.blocks)) if self.plan.owner[i] == rank]
+        tops = [i for i in range(len(factors.blocks)) if self.plan.owner[i] < 0]
+        self.S = DevicePanels(factors, subset=mine) if mine else None
+        self.T = DevicePanels(factors, subset=tops) if tops else None
+        z = lambda k: t.zeros(max(k, 1), dtype=t.float64, device="cuda")  # noqa: E731
+        self.v = {k: z(n) for k in ("x", "r", "z", "p", "ap", "y", "ext", "b")}
+        self.topbuf = z(len(self.plan.top_rows))
+        self.part = z(2 * 148)
+        self.sc = z(8)  # [rz, pAp] / [rz_new, rz_old] / scratch
+        self._lib = _lib.load()
+        self._L = _lib
+
+    # -- pieces ------------------------------------------------------------
+    def _exchange_top(self, vec):
+        m = len(self.plan.top_rows)
+        if self.world == 1 or m == 0:
+            return
+        L, s = self._L, self._L.stream_ptr()
+        L.check(self._lib.tsb_gather_rows(m, L.ptr(self.top), L.ptr(vec), L.ptr(self.topbuf), s), "gather")
+        self.allreduce(self.topbuf[:m])
+        L.check(self._lib.tsb_scatter_rows(m, L.ptr(self.top), L.ptr(self.topbuf), L.ptr(vec), s), "scatter")
+
+    def _dot(self, a, b, slot):
+        L = self._L
+        L.check(self._lib.tsb_wdot(self.n, L.ptr(self.w), L.ptr(a), L.ptr(b), L.ptr(self.part),
+                                   L.ptr(self.sc[slot:slot + 1]), L.stream_ptr()), "wdot")
+        self.allreduce(self.sc[slot:slot + 1])
+
+    def _spmv(self, p, out):
+        L = self._L
+        L.check(self._lib.tsb_spmv(self.n, L.ptr(self.rp), L.ptr(self.ci), L.ptr(self.va), L.ptr(p), L.ptr(out),
+                                   L.stream_ptr()), "spmv")
+        self._exchange_top(out)
+
+    def _precond(self, r, out):
+        v = self.v
+        v["ext"].zero_()
+        if self.S is not None:
+            self.S.lower_ext(r, None, v["y"])
+            self.S.external_sums(v["ext"])
+        self._exchange_top(v["ext"])
+        if self.T is not None:
+            self.T.lower_ext(r, v["ext"], v["y"])
+            self.T.run("upper_scaled", v["y"], out)
+        if self.S is not None:
+            self.S.run("upper_scaled", v["y"], out)
+
+    # -- solve -----------------------------------------------------------------
+    def solve(self, b, tol=1e-9, max_it=1000):
+        """-> (x in original order as a CUDA tensor, iterations, residual, converged)."""
+        L, t = self._L, self._L.torch()
+        v, n = self.v, self.n
+        bd = b if L.is_tensor(b) else t.from_numpy(np.ascontiguousarray(b, dtype=np.float64)).cuda()
+        s = L.stream_ptr()
+        L.check(self._lib.tsb_gather_rows(n, L.ptr(self.perm), L.ptr(bd), L.ptr(v["b"]), s), "gather")
+        v["r"].copy_(v["b"])
+        v["x"].zero_()
+        self._dot(v["b"], v["b"], 4)
+        bnorm = float(self.sc[4].item()) ** 0.5
+        x_out = t.zeros(n, dtype=t.float64, device="cuda")
+        if bnorm == 0.0:
+            return x_out, 0, 0.0, True
+        self._dot(v["r"], v["r"], 5)
+        res = float(self.sc[5].item()) ** 0.5 / bnorm
+        it, conv = 0, res <= tol
+        if not conv:
+            self._precond(v["r"], v["z"])
+            v["p"].copy_(v["z"])
+            self._dot(v["r"], v["z"], 0)  # sc[0] = rz
+            while it < max_it:
+                self._spmv(v["p"], v["ap"])
+                self._dot(v["p"], v["ap"], 1)  # sc[1] = pAp; alpha = sc[0] / sc[1]
+                L.check(self._lib.tsb_pcg_update(n, L.ptr(self.w), L.ptr(v["x"]), L.ptr(v["p"]), L.ptr(v["r"]),
+                                                 L.ptr(v["ap"]), L.ptr(self.sc), L.ptr(self.part),
+                                                 L.ptr(self.sc[5:6]), s), "pcg_update")
+                self.allreduce(self.sc[5:6])
+                it += 1
+                res = float(self.sc[5].item()) ** 0.5 / bnorm  # the one host read per iteration
+                if res <= tol:
+                    conv = True
+                    break
+                self._precond(v["r"], v["z"])
+                self.sc[1:2].copy_(self.sc[0:1])  # rz_old
+                self._dot(v["r"], v["z"], 0)       # rz_new; beta = sc[0] / sc[1]
+                L.check(self._lib.tsb_pcg_direction(n, L.ptr(v["p"]), L.ptr(v["z"]), L.ptr(self.sc), s),
+                        "pcg_direction")
+        # x: owned rows from every rank, top rows from rank 0
+        xw = v["y"]
+        self._weighted_copy(v["x"], xw)
+        self.allreduce(xw)
+        L.check(self._lib.tsb_gather_rows(n, L.ptr(self.iperm), L.ptr(xw), L.ptr(x_out), s), "gather")
+        return x_out, it, res, conv
+
+    def _weighted_copy(self, x, out):
+        """out = x on the rows this rank contributes (owned, top on rank 0), else 0."""
+        L = self._L
+        out.zero_()
+        rows = np.flatnonzero(self.plan.weights(self.rank) > 0).astype(np.int32)
+        if not hasattr(self, "_live"):
+            t = L.torch()
+            self._live = t.from_numpy(rows).cuda()
+            self._livebuf = t.zeros(max(len(rows), 1), dtype=t.float64, device="cuda")
+        m = len(rows)
+        s = L.stream_ptr()
+        L.check(self._lib.tsb_gather_rows(m, L.ptr(self._live), L.ptr(x), L.ptr(self._livebuf), s), "gather")
+        L.check(self._lib.tsb_scatter_rows(m, L.ptr(self._live), L.ptr(self._livebuf), L.ptr(out), s), "scatter")

@@ -75,6 +75,7 @@ def emulate_lower(H, r):
                 ready[p] = True
     assert np.all(cnt == blocks["target_l"])
     assert np.array_equal(segs, H["tiles_l"]["nseg"])
+    emulate_lower.cbuf = cbuf
     return y
 
 
@@ -90,16 +91,16 @@ def test_both_lower_input_modes_are_exercised():
     assert np.abs(emulate_lower(H, r) - ref).max() <= 1e-12 * np.abs(ref).max()
 
 
-def emulate_upper(H, w):
+def emulate_upper(H, w, z=None):
     n, nb = H["n"], H["nb"]
     blocks = H["blocks"]
-    z = np.zeros(n)
+    z = np.zeros(n) if z is None else z
     done = np.zeros(nb, dtype=np.int64)
     segs = np.zeros(len(H["tiles_u"]), dtype=np.int64)
     for b, t0, t1, sg in H["items_u"]:
         B = blocks[b]
         s, m, na = int(B["start"]), int(B["m"]), int(B["na"])
-        if na:
+        if na and B["parent"] >= 0:
             p = int(B["parent"])
             assert done[p] == blocks[p]["n_u"], "upper item dispatched before the parent's z"
         v = np.concatenate([w[s:s + m], -z[H["anc"][B["anc_off"]: B["anc_off"] + na]]])
@@ -168,3 +169,59 @@ def test_tile_layout_roundtrip_and_coverage():
                         assert np.array_equal(d[k], full)
             assert sorted(rows_seen) == list(range(m if up else m + na))
     assert H["g"].size == int(tl_["np"].sum()) * K.TILE * 2
+
+
+def test_shard_subsets_compose_to_the_full_apply():
+    """Two block subsets (a shard's subtrees S and the replicated top T) packed
+    separately: lower(S) -> external sums -> lower(T, r - ext) -> upper(T) ->
+    upper(S) equals the oracle's apply (the sharded preconditioner, shard.py)."""
+    from paper_2306_05893_b200 import shard as SH
+
+    mesh, f = _factors((4, 4, 16), 16)
+    sp = SH.shard_blocks(f, 2)
+    n = f.plan.n
+    r = np.random.default_rng(11).standard_normal(n)
+    rp = r[f.plan.perm]
+    y = np.zeros(n)
+    ext = np.zeros(n)
+    for g in range(2):
+        S = [i for i in range(len(f.blocks)) if sp.owner[i] == g]
+        HS = K.pack(f, S)
+        ys = emulate_lower(HS, rp)
+        rows = sp.owned_rows(g)
+        y[rows] = ys[rows]
+        cb = emulate_lower.cbuf
+        for e in HS["ext_rows"]:
+            ext[e] += cb[HS["cin_ptr"][e]: HS["cin_ptr"][e + 1]].sum()
+    T = [i for i in range(len(f.blocks)) if sp.owner[i] < 0]
+    HT = K.pack(f, T)
+    yt = emulate_lower(HT, rp - ext)
+    y[sp.top_rows] = yt[sp.top_rows]
+    w = y / f.d
+    z = emulate_upper(HT, w)
+    for g in range(2):
+        S = [i for i in range(len(f.blocks)) if sp.owner[i] == g]
+        z = emulate_upper(K.pack(f, S), w, z)
+    out = np.empty(n)
+    out[f.plan.perm] = z
+    ref = O.apply(f, r)
+    assert np.abs(out - ref).max() <= 1e-12 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("max_rows", [150, 400, 100000])
+def test_amalgamated_factors_apply_identically(max_rows):
+    """Subtree amalgamation (one block per small elimination subtree) is the same
+    L: the oracle's level-scheduled apply on the merged factors equals the
+    original's, and the device layout of the merged factors emulates to it."""
+    mesh, f = _factors((4, 4, 16), 16)
+    g = K.amalgamate(f, max_rows)
+    assert len(g.blocks) < len(f.blocks)
+    r = np.random.default_rng(5).standard_normal(f.plan.n)
+    ref = O.apply(f, r)
+    assert np.abs(O.apply(g, r) - ref).max() <= 1e-12 * np.abs(ref).max()
+    H = K.pack(g)
+    rp = r[f.plan.perm]
+    z = emulate_upper(H, emulate_lower(H, rp) / f.d)
+    out = np.empty_like(z)
+    out[f.plan.perm] = z
+    assert np.abs(out - ref).max() <= 1e-12 * np.abs(ref).max()
