@@ -428,7 +428,7 @@ def pack(factors, subset=None):
 class DevicePanels:
     """Packed factor image in HBM + the libtsb handle (tsb_ldlt_create)."""
 
-    def __init__(self, factors, stream=None, trace=False, force_mode=None, subset=None, merge=None):
+    def __init__(self, factors, stream=None, trace=False, force_mode=None, subset=None, merge=None, grid=0):
         t = _lib.require_cuda()
         if merge is None:
             merge = MERGE_ROWS if subset is None else 0
@@ -471,7 +471,7 @@ class DevicePanels:
         cp = lambda a, b: _lib.ptr(cnt[a:b]) if b > a else _lib.ptr(cnt)  # noqa: E731
         self.desc = _lib.LdltDesc(
             n=n, n_blocks=nb, n_items_lower=len(items_l), n_items_upper=len(items_u),
-            max_m=H["max_m"], max_v=H["max_v"], max_cb=H["max_cb"], grid=0,
+            max_m=H["max_m"], max_v=H["max_v"], max_cb=H["max_cb"], grid=int(grid),
             d_blocks=tp("blocks"), d_items_lower=tp("items_l"), d_items_upper=tp("items_u"),
             d_tiles_lower=tp("tiles_l"), d_tiles_upper=tp("tiles_u"), d_g=tp("g"), d_gt=tp("gt"),
             d_anc=tp("anc"), d_cslot=tp("cslot"), d_cin_ptr=tp("cin_ptr"), d_d=tp("d"),

@@ -28,6 +28,7 @@
 //          (row-major pull); only -z_anc waits for the parent.
 // Counters are reset by the last CTA to leave, so the kernels replay inside
 // the persistent PCG without memsets.
+#include <cstdlib>
 #include <mutex>
 #include <vector>
 
@@ -81,8 +82,17 @@ static std::mutex g_serial_mu;
 // which is deadlock-free exactly when every CTA of the grid is resident.
 template <class K>
 static void launch_coop(K kernel, int grid, size_t smem, cudaStream_t st, tsb_ldlt_desc &D, SweepArgs &a) {
-    void *args[] = {&D, &a};
-    TSB_CUDA(cudaLaunchCooperativeKernel((const void *)kernel, dim3(grid), dim3(kSweepBlock), args, smem, st));
+    // TSB_SHARED_DEVICE=1: several processes share one GPU (the 2-rank shard test
+    // on a 1-GPU box), where the driver refuses cooperative launches; the grid
+    // (<= one CTA per SM there) is still co-resident, launch it plainly
+    static const bool shared = getenv("TSB_SHARED_DEVICE") != nullptr;
+    if (shared) {
+        kernel<<<grid, kSweepBlock, smem, st>>>(D, a);
+        TSB_CUDA(cudaGetLastError());
+    } else {
+        void *args[] = {&D, &a};
+        TSB_CUDA(cudaLaunchCooperativeKernel((const void *)kernel, dim3(grid), dim3(kSweepBlock), args, smem, st));
+    }
     count_launch();
 }
 
@@ -151,9 +161,9 @@ extern "C" int tsb_ldlt_create(const tsb_ldlt_desc *desc, tsb_ldlt_t *out) {
         h->d = *desc;
         const size_t ls = sweep_smem_lower(*desc), us = sweep_smem_upper(*desc);
         for (auto fn : {lower_sweep<false>, lower_sweep<true>})
-            TSB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ls));
+            allow_max_smem(fn);
         for (auto fn : {upper_sweep<false>, upper_sweep<true>})
-            TSB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)us));
+            allow_max_smem(fn);
         int per_sm_l = 0, per_sm_u = 0;
         TSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_l, lower_sweep<true>, kSweepBlock, ls));
         TSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_u, upper_sweep<true>, kSweepBlock, us));

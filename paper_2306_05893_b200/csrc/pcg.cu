@@ -326,7 +326,7 @@ namespace tsb {
 template <int KIND>
 static int occupancy_grid(size_t smem) {
     auto k = pcg_persistent<KIND>;
-    TSB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    allow_max_smem(k);
     int per_sm = 0, dev = 0, nsm = kNumSM;
     TSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kPcgBlock, smem));
     TSB_CUDA(cudaGetDevice(&dev));

@@ -52,6 +52,21 @@ int guard(F &&body) {
 
 inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// Opt a kernel into the device's full dynamic shared memory once, so handles
+// with different footprints (several factor images, block subsets) can all
+// launch it; occupancy is still computed from each launch's actual size.
+template <class K>
+inline void allow_max_smem(K kernel) {
+    int dev = 0, optin = 0;
+    check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
+    check_cuda(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev), "smem optin");
+    cudaFuncAttributes fa{};
+    check_cuda(cudaFuncGetAttributes(&fa, (const void *)kernel), "cudaFuncGetAttributes");
+    check_cuda(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    optin - (int)fa.sharedSizeBytes),
+               "cudaFuncSetAttribute(max dynamic smem)");
+}
+
 constexpr int kNumSM = 148;
 
 // ---------------------------------------------------------------------------

@@ -297,7 +297,7 @@ class DistributedPcg:
     defaults to torch.distributed.all_reduce (NCCL over NVLink between GPUs).
     """
 
-    def __init__(self, a, factors, rank=None, world=None, allreduce=None):
+    def __init__(self, a, factors, rank=None, world=None, allreduce=None, grid=0):
         from . import _lib
         from ._ldlt_pack import DevicePanels
 
@@ -328,8 +328,8 @@ class DistributedPcg:
         self.iperm = dev(iperm, np.int32)
         mine = [i for i in range(len(factors.blocks)) if self.plan.owner[i] == rank]
         tops = [i for i in range(len(factors.blocks)) if self.plan.owner[i] < 0]
-        self.S = DevicePanels(factors, subset=mine) if mine else None
-        self.T = DevicePanels(factors, subset=tops) if tops else None
+        self.S = DevicePanels(factors, subset=mine, grid=grid) if mine else None
+        self.T = DevicePanels(factors, subset=tops, grid=grid) if tops else None
         z = lambda k: t.zeros(max(k, 1), dtype=t.float64, device="cuda")  # noqa: E731
         self.v = {k: z(n) for k in ("x", "r", "z", "p", "ap", "y", "ext", "b")}
         self.topbuf = z(len(self.plan.top_rows))

@@ -40,14 +40,16 @@ def _worker(rank, world, port, q):
     import torch
     import torch.distributed as dist
 
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), TSB_SHARED_DEVICE="1")
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from paper_2306_05893_b200 import shard as S
 
         a, b, f = _system()
-        x, it, res, conv = S.DistributedPcg(a, f, rank=rank, world=world).solve(b, 1e-9, 200)
+        # both ranks share the one GPU: small persistent grids so the two processes'
+        # cooperative sweep launches fit on the device side by side
+        x, it, res, conv = S.DistributedPcg(a, f, rank=rank, world=world, grid=32).solve(b, 1e-9, 200)
         q.put((rank, x.cpu().numpy(), it, res, conv))
     except Exception as e:  # surface the failure in the parent
         q.put((rank, repr(e), -1, 0.0, False))
