@@ -58,11 +58,25 @@ __device__ __forceinline__ int ld_acquire(const int *p) {
     asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+// Release / acquire-release counter updates: issued by thread 0 after a
+// __syncthreads(), they publish every write the CTA made before the barrier
+// (bar.sync orders them before thread 0's release; release is cumulative).
+__device__ __forceinline__ int atom_add_release(int *p, int v) {
+    int old;
+    asm volatile("atom.add.release.gpu.global.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+__device__ __forceinline__ int atom_add_acq_rel(int *p, int v) {
+    int old;
+    asm volatile("atom.add.acq_rel.gpu.global.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
 __device__ __forceinline__ void st_release(int *p, int v) {
     asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 __device__ __forceinline__ void spin_until_geq(const int *p, int target) {
-    if (ld_acquire(p) >= target) return;
+    for (int k = 0; k < 16; ++k)
+        if (ld_acquire(p) >= target) return;
     int ns = 32;
     while (ld_acquire(p) < target) {
         __nanosleep(ns);
@@ -274,13 +288,9 @@ __device__ __forceinline__ void item_gemv(const Item &it, const tsb_ldlt_tile *t
 #pragma unroll
         for (int w = 0; w < kWarps; ++w) a += red[w * 32 + threadIdx.x];
         part[((int64_t)T.part + s) * kTile + threadIdx.x] = a;
-        __threadfence();
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        last_seg = atomicAdd(tcnt + it.t0, 1) == T.nseg - 1;
-        if (last_seg) __threadfence();
-    }
+    if (threadIdx.x == 0) last_seg = atom_add_acq_rel(tcnt + it.t0, 1) == T.nseg - 1;
     __syncthreads();
     if (last_seg && threadIdx.x < 32) {
         double a = 0.0;
@@ -407,13 +417,9 @@ __device__ __forceinline__ void lower_sweep_body(const tsb_ldlt_desc &D, const S
         if (tid == 0) {
             fin_parent = -1;
             if (B.parent >= 0) {
-                __threadfence();
-                const int old = atomicAdd(D.d_cnt_l + B.parent, 1);
+                const int old = atom_add_acq_rel(D.d_cnt_l + B.parent, 1);
                 const tsb_ldlt_block &Pb = D.d_blocks[B.parent];
-                if (Pb.mode == 2 && old == Pb.target_l - 1) {
-                    __threadfence();
-                    fin_parent = B.parent;
-                }
+                if (Pb.mode == 2 && old == Pb.target_l - 1) fin_parent = B.parent;
             }
         }
         __syncthreads();
@@ -449,10 +455,7 @@ __device__ __forceinline__ void lower_sweep_body(const tsb_ldlt_desc &D, const S
                 i0 = i1;
             }
             (void)qe;
-            if (tid == 0) {
-                __threadfence();
-                st_release(D.d_ready_l + fin_parent, 1);
-            }
+            if (tid == 0) st_release(D.d_ready_l + fin_parent, 1);
         }
         trace(tbuf, iid, 2);
     }
@@ -524,10 +527,7 @@ __device__ __forceinline__ void upper_sweep_body(const tsb_ldlt_desc &D, const S
         }
         trace(tbuf, iid, 5);
         __syncthreads();
-        if (tid == 0) {
-            __threadfence();
-            atomicAdd(D.d_done_u + it.block, 1);
-        }
+        if (tid == 0) atom_add_release(D.d_done_u + it.block, 1);
         trace(tbuf, iid, 2);
     }
     upper_exit(D);
