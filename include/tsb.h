@@ -182,8 +182,9 @@ int tsb_element_blocks(const tsb_asm_plan *plan, const tsb_asm_coeffs *coeffs,
  * warps splitting its pairs; the tile's last segment to finish adds the
  * segments' partial sums in segment order (deterministic) and emits.
  * Lower: x_b = r_b - (contributions of its descendants), summed in a fixed
- * order either by each of the block's items (mode 1) or once by the child
- * item that completes the block (mode 2).  Upper: an item of b waits for
+ * order either by each of the block's items (mode 1) or once by nfin
+ * finaliser items {block, row0, row1, -1} dispatched before the block's
+ * items (mode 2).  Upper: an item of b waits for
  * every item of b's parent (z_anc final). */
 typedef struct tsb_ldlt_block {
     int32_t start, m, na, parent;   /* parent: block elimination-tree parent, -1 = root */
@@ -191,8 +192,9 @@ typedef struct tsb_ldlt_block {
     int32_t n_u;                    /* upper items of this block (z_b complete)    */
     int32_t mode;                   /* lower input: 0 no contributions (leaf),
                                        1 every item sums the contributions itself,
-                                       2 the last child item sums them once       */
+                                       2 nfin finaliser items form x_b once        */
     int32_t ncb;                    /* contributions into the block's rows         */
+    int32_t nfin, pad_;             /* finaliser items (mode 2)                     */
     int64_t anc_off;                /* offset of the block's anc rows in d_anc      */
     int64_t cb_off;                 /* first cbuf slot of the block's rows          */
 } tsb_ldlt_block;

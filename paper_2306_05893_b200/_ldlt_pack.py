@@ -61,9 +61,10 @@ CB_CAP = 2048           # contributions staged per piece when a block's items su
 BLOCK_DTYPE = np.dtype([
     ("start", "<i4"), ("m", "<i4"), ("na", "<i4"), ("parent", "<i4"),
     ("target_l", "<i4"), ("n_u", "<i4"), ("mode", "<i4"), ("ncb", "<i4"),
-    ("anc_off", "<i8"), ("cb_off", "<i8"),
+    ("nfin", "<i4"), ("pad_", "<i4"), ("anc_off", "<i8"), ("cb_off", "<i8"),
 ])
-assert BLOCK_DTYPE.itemsize == 48
+assert BLOCK_DTYPE.itemsize == 56
+FIN_CONTRIB = 4096      # contributions per finaliser item of a mode-2 block
 TILE_DTYPE = np.dtype([("off", "<i8"), ("tl", "<i4"), ("np", "<i4"), ("row0", "<i4"), ("nrows", "<i4"),
                        ("nseg", "<i4"), ("part", "<i4")])
 assert TILE_DTYPE.itemsize == 32
@@ -336,11 +337,37 @@ def pack(factors, subset=None):
     anc_all = (np.concatenate([np.asarray(bf.anc, dtype=np.int64) for bf in bfs]) if anc_off[-1]
                else np.zeros(0, dtype=np.int64))
 
-    # ---------------- items + dispatch order ----------------
+    # ---------------- contribution slots (lower) ----------------
+    corder = np.argsort(anc_all, kind="stable")   # row-contiguous, block order within a row
+    cin_ptr = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(np.bincount(anc_all, minlength=n), out=cin_ptr[1:])
+    cslot = np.empty(len(anc_all), dtype=np.int64)
+    cslot[corder] = np.arange(len(anc_all))
+    ext_rows = np.unique(anc_all[owner[anc_all] < 0]) if len(anc_all) else np.zeros(0, dtype=np.int64)
+
+    # ---------------- items + lower input modes ----------------
     items = {up: [_items(blk_tiles[up][i][1], blk_tiles[up][i][0]) for i in range(nb)] for up in (False, True)}
     nl = np.array([len(x) for x in items[False]], dtype=np.int64)
     n_u = np.array([len(x) for x in items[True]], dtype=np.int64)
     target_l = np.array([sum(int(nl[c]) for c in children[i]) for i in range(nb)], dtype=np.int64)
+    # lower input of a block: its items sum the contributions themselves when the
+    # redundant L2 reads stay below the block's own factor bytes (mode 1), else
+    # nfin finaliser items (dispatched first) form x_b = input - contributions
+    # once, each for a slice of rows, and the block's items read it (mode 2)
+    contrib = np.diff(cin_ptr)
+    blk_contrib = np.array([int(contrib[bf.start:bf.stop].sum()) for bf in bfs], dtype=np.int64)
+    gsize = np.array([int(tables[False]["np"][f:f + len(t)].sum()) * TILE * 2 for f, t in blk_tiles[False]],
+                     dtype=np.int64)
+    mode = np.where(target_l == 0, MODE_LEAF, np.where(nl * blk_contrib <= gsize, MODE_GATHER, MODE_FIN))
+    nfin = np.where(mode == MODE_FIN,
+                    np.minimum(np.minimum(32, (ms_ + 31) // 32), np.maximum(1, (blk_contrib + FIN_CONTRIB - 1) // FIN_CONTRIB)),
+                    0)
+    fin_items = [[] for _ in range(nb)]
+    for i in np.flatnonzero(nfin):
+        k = int(nfin[i])
+        edges = np.linspace(0, int(ms_[i]), k + 1).astype(np.int64)
+        fin_items[i] = [(int(edges[j]), int(edges[j + 1]), -1) for j in range(k) if edges[j + 1] > edges[j]]
+        nfin[i] = len(fin_items[i])
 
     def cost(up, it):  # us: item overhead + streaming at ~40 GB/s per CTA
         nbytes = min(int(tables[up]["np"][it[0]:it[1]].sum()) * TILE * 16, ITEM_BYTES)
@@ -351,13 +378,15 @@ def pack(factors, subset=None):
     for i in order:
         if children[i]:
             ready_l[i] = max(done_l[c] for c in children[i]) + 1.0
-        done_l[i] = ready_l[i] + max(cost(False, it) for it in items[False][i])
+        done_l[i] = ready_l[i] + max(cost(False, it) for it in items[False][i]) + (2.0 if nfin[i] else 0.0)
     tail_l = np.zeros(nb)
     for i in reversed(order):  # parents first
         tail_l[i] = (done_l[i] - ready_l[i]) + (tail_l[parent[i]] if parent[i] >= 0 else 0.0)
-    lower = sorted((ready_l[i], -tail_l[i], bfs[i].start, it[0], i, it[1], it[2])
-                   for i in range(nb) for it in items[False][i])
-    items_l = np.array([(x[4], x[3], x[5], x[6]) for x in lower], dtype=np.int32).reshape(-1, 4)
+    lower = sorted([(ready_l[i], -tail_l[i], bfs[i].start, 0, it[0], i, it[1], it[2])
+                    for i in range(nb) for it in fin_items[i]] +
+                   [(ready_l[i], -tail_l[i], bfs[i].start, 1, it[0], i, it[1], it[2])
+                    for i in range(nb) for it in items[False][i]])
+    items_l = np.array([(x[5], x[4], x[6], x[7]) for x in lower], dtype=np.int32).reshape(-1, 4)
     start_u, done_u = np.zeros(nb), np.zeros(nb)
     for i in reversed(order):  # parents first
         start_u[i] = done_u[parent[i]] + 1.0 if parent[i] >= 0 else 0.0
@@ -369,13 +398,6 @@ def pack(factors, subset=None):
                    for i in range(nb) for it in items[True][i])
     items_u = np.array([(x[4], x[3], x[5], x[6]) for x in upper], dtype=np.int32).reshape(-1, 4)
 
-    # ---------------- contribution slots (lower) ----------------
-    corder = np.argsort(anc_all, kind="stable")   # row-contiguous, block order within a row
-    cin_ptr = np.zeros(n + 1, dtype=np.int64)
-    np.cumsum(np.bincount(anc_all, minlength=n), out=cin_ptr[1:])
-    cslot = np.empty(len(anc_all), dtype=np.int64)
-    cslot[corder] = np.arange(len(anc_all))
-    ext_rows = np.unique(anc_all[owner[anc_all] < 0]) if len(anc_all) else np.zeros(0, dtype=np.int64)
 
     # ---------------- block table ----------------
     blocks = np.zeros(nb, dtype=BLOCK_DTYPE)
@@ -385,15 +407,8 @@ def pack(factors, subset=None):
     blocks["parent"] = parent
     blocks["target_l"] = target_l
     blocks["n_u"] = n_u
-    # lower input of a block: its items sum the contributions themselves when the
-    # redundant L2 reads stay below the block's own factor bytes, else the child
-    # item that completes the block sums them once (one extra hop)
-    contrib = np.diff(cin_ptr)
-    blk_contrib = np.array([int(contrib[bf.start:bf.stop].sum()) for bf in bfs], dtype=np.int64)
-    gsize = np.array([int(tables[False]["np"][f:f + len(t)].sum()) * TILE * 2 for f, t in blk_tiles[False]],
-                     dtype=np.int64)
-    mode = np.where(target_l == 0, MODE_LEAF, np.where(nl * blk_contrib <= gsize, MODE_GATHER, MODE_FIN))
     blocks["mode"] = mode
+    blocks["nfin"] = nfin
     blocks["ncb"] = blk_contrib
     blocks["cb_off"] = cin_ptr[[bf.start for bf in bfs]] if nb else []
     blocks["anc_off"] = anc_off[:-1]
@@ -434,10 +449,13 @@ class DevicePanels:
             merge = MERGE_ROWS if subset is None else 0
         H = pack(amalgamate(factors, merge) if merge else factors, subset)
         if force_mode is not None:  # testing: route every inner block through one input mode
+            if force_mode != MODE_GATHER:
+                raise ValueError("only the item-gather mode can be forced (finaliser items are planned)")
             inner = H["blocks"]["mode"] != MODE_LEAF
             H["blocks"]["mode"][inner] = force_mode
-            if force_mode == MODE_GATHER:
-                H["max_cb"] = min(CB_CAP, int(H["blocks"]["ncb"][inner].max(initial=0)))
+            H["blocks"]["nfin"][inner] = 0
+            H["items_l"] = H["items_l"][H["items_l"][:, 3] >= 0]
+            H["max_cb"] = min(CB_CAP, int(H["blocks"]["ncb"][inner].max(initial=0)))
         n, nb = H["n"], H["nb"]
         items_l, items_u = H["items_l"], H["items_u"]
         self.host = H if trace else None

@@ -323,7 +323,7 @@ __device__ __forceinline__ void lower_sweep_body(const tsb_ldlt_desc &D, const S
     int32_t *offs = reinterpret_cast<int32_t *>(cbs + ((D.max_cb + 1) & ~1));
     const int noffs = (D.max_v + 2 > kFinRows + 2 ? D.max_v + 2 : kFinRows + 2);
     int32_t *dsts = offs + ((noffs + 1) & ~1);
-    __shared__ int item_id, fin_parent;
+    __shared__ int item_id;
     __shared__ double red[kSweepBlock];
     int32_t *ctl = D.d_ctl;
     int64_t *const tbuf = TRACE ? D.d_trace_lower : nullptr;  // folds away when off
@@ -338,6 +338,41 @@ __device__ __forceinline__ void lower_sweep_body(const tsb_ldlt_desc &D, const S
         const Item it = items[iid];
         const tsb_ldlt_block B = D.d_blocks[it.block];
         const int m = B.m, s = B.start;
+        if (it.seg < 0) {
+            // finaliser item (mode 2): x_b = input - contributions for rows
+            // [t0, t1), once the children are done; contributions staged piece
+            // by piece with coalesced loads, one thread per row sums in order
+            if (tid == 0) spin_until_geq(D.d_cnt_l + it.block, B.target_l);
+            __syncthreads();
+            trace(tbuf, iid, 1);
+            int i0 = it.t0;
+            while (i0 < it.t1) {
+                const int64_t qb = __ldg(D.d_cin_ptr + s + i0);
+                int i1 = min(it.t1, i0 + kFinRows);
+                if (__ldg(D.d_cin_ptr + s + i1) - qb > kStage) {  // rows whose contributions fit (>= 1 row)
+                    int lo = i0 + 1, hi = i1;
+                    while (lo < hi) {
+                        const int mid = (lo + hi + 1) >> 1;
+                        if (__ldg(D.d_cin_ptr + s + mid) - qb <= kStage) lo = mid; else hi = mid - 1;
+                    }
+                    i1 = lo;
+                }
+                const int cnt = (int)(__ldg(D.d_cin_ptr + s + i1) - qb);
+                const bool staged = cnt <= kStage;
+                if (staged) stage_copy(stage, D.d_cbuf + qb, cnt);
+                for (int i = i0 + tid; i <= i1; i += kSweepBlock) offs[i - i0] = (int32_t)(__ldg(D.d_cin_ptr + s + i) - qb);
+                __syncthreads();
+                for (int i = i0 + tid; i < i1; i += kSweepBlock)
+                    D.d_x[s + i] = lower_input(A, s + i) -
+                                   (staged ? contrib_sum<false>(stage, offs[i - i0], offs[i - i0 + 1])
+                                           : contrib_sum<true>(D.d_cbuf + qb, offs[i - i0], offs[i - i0 + 1]));
+                __syncthreads();
+                i0 = i1;
+            }
+            if (tid == 0) atom_add_release(D.d_ready_l + it.block, 1);
+            trace(tbuf, iid, 2);
+            continue;
+        }
         int w0, w1;
         item_window(it, D.d_tiles_lower, m, w0, w1);
         const int nw = w1 - w0;
@@ -352,7 +387,7 @@ __device__ __forceinline__ void lower_sweep_body(const tsb_ldlt_desc &D, const S
                 __device__ double load(int j) const { return lower_input(A, s + j); }
                 __device__ void store(int j, double v) const { xs[j] = v; }
             };
-            batched(nw, In{A, xs, s + w0});
+            if (B.mode != 2) batched(nw, In{A, xs, s + w0});  // mode 2: x_b comes from the finalisers
         }
         if (tid == 0) xs[nw] = 0.0;  // column pad of odd-width tiles
         const tsb_ldlt_tile Tf = D.d_tiles_lower[it.t0], Tb = D.d_tiles_lower[it.t1 - 1];
@@ -365,7 +400,7 @@ __device__ __forceinline__ void lower_sweep_body(const tsb_ldlt_desc &D, const S
         }
         if (tid == 0) {
             if (B.mode == 1) spin_until_geq(D.d_cnt_l + it.block, B.target_l);
-            else if (B.mode == 2) spin_until_geq(D.d_ready_l + it.block, 1);
+            else if (B.mode == 2) spin_until_geq(D.d_ready_l + it.block, B.nfin);
         }
         __syncthreads();
         trace(tbuf, iid, 1);
@@ -392,14 +427,14 @@ __device__ __forceinline__ void lower_sweep_body(const tsb_ldlt_desc &D, const S
                 __syncthreads();
                 i0 = i1;
             }
-        } else if (B.mode == 2) {
-            struct Sub {
+        } else if (B.mode == 2) {  // formed by the block's finaliser items
+            struct Ld {
                 const double *src;
                 double *xs;
                 __device__ double load(int j) const { return __ldcg(src + j); }
-                __device__ void store(int j, double v) const { xs[j] = xs[j] - v; }
+                __device__ void store(int j, double v) const { xs[j] = v; }
             };
-            batched(nw, Sub{D.d_x + s + w0, xs});
+            batched(nw, Ld{D.d_x + s + w0, xs});
         }
         __syncthreads();
         trace(tbuf, iid, 4);
@@ -414,49 +449,7 @@ __device__ __forceinline__ void lower_sweep_body(const tsb_ldlt_desc &D, const S
         }
         trace(tbuf, iid, 5);
         __syncthreads();
-        if (tid == 0) {
-            fin_parent = -1;
-            if (B.parent >= 0) {
-                const int old = atom_add_acq_rel(D.d_cnt_l + B.parent, 1);
-                const tsb_ldlt_block &Pb = D.d_blocks[B.parent];
-                if (Pb.mode == 2 && old == Pb.target_l - 1) fin_parent = B.parent;
-            }
-        }
-        __syncthreads();
-        if (fin_parent >= 0) {
-            // Every child item is done: the parent's contribution sums, formed once
-            // here (row-contiguous in cbuf; staged piece by piece with coalesced loads
-            // together with the per-row offsets, one thread per row sums in order).
-            const tsb_ldlt_block P = D.d_blocks[fin_parent];
-            int32_t *fo = offs;
-            const int64_t qe = P.cb_off + P.ncb;
-            int i0 = 0;
-            while (i0 < P.m) {
-                const int64_t qb = __ldg(D.d_cin_ptr + P.start + i0);
-                int i1 = min(P.m, i0 + kFinRows);
-                if (__ldg(D.d_cin_ptr + P.start + i1) - qb > kStage) {  // rows whose contributions fit (>= 1 row)
-                    int lo = i0 + 1, hi = i1;
-                    while (lo < hi) {
-                        const int mid = (lo + hi + 1) >> 1;
-                        if (__ldg(D.d_cin_ptr + P.start + mid) - qb <= kStage) lo = mid; else hi = mid - 1;
-                    }
-                    i1 = lo;
-                }
-                const int cnt = (int)(__ldg(D.d_cin_ptr + P.start + i1) - qb);
-                const bool staged = cnt <= kStage;
-                if (staged) stage_copy(stage, D.d_cbuf + qb, cnt);
-                for (int i = i0 + tid; i <= i1; i += kSweepBlock)
-                    fo[i - i0] = (int32_t)(__ldg(D.d_cin_ptr + P.start + i) - qb);
-                __syncthreads();
-                for (int i = i0 + tid; i < i1; i += kSweepBlock)
-                    D.d_x[P.start + i] = staged ? contrib_sum<false>(stage, fo[i - i0], fo[i - i0 + 1])
-                                                : contrib_sum<true>(D.d_cbuf + qb, fo[i - i0], fo[i - i0 + 1]);
-                __syncthreads();
-                i0 = i1;
-            }
-            (void)qe;
-            if (tid == 0) st_release(D.d_ready_l + fin_parent, 1);
-        }
+        if (tid == 0 && B.parent >= 0) atom_add_release(D.d_cnt_l + B.parent, 1);
         trace(tbuf, iid, 2);
     }
     lower_exit(D);

@@ -38,17 +38,24 @@ def emulate_lower(H, r):
     xbuf = np.zeros(n)
     cbuf = np.zeros(max(H["ncbuf"], 1))
     cnt = np.zeros(nb, dtype=np.int64)
-    ready = np.zeros(nb, dtype=bool)
+    ready = np.zeros(nb, dtype=np.int64)
     segs = np.zeros(len(H["tiles_l"]), dtype=np.int64)
+    csum = lambda row: cbuf[H["cin_ptr"][row]: H["cin_ptr"][row + 1]].sum()  # noqa: E731
     for b, t0, t1, sg in H["items_l"]:
         B = blocks[b]
         s, m = int(B["start"]), int(B["m"])
+        if sg < 0:  # finaliser item: x_b over rows [t0, t1) once the children are done
+            assert B["mode"] == K.MODE_FIN and cnt[b] == B["target_l"], "finaliser before the children"
+            for i in range(t0, t1):
+                xbuf[s + i] = r[s + i] - csum(s + i)
+            ready[b] += 1
+            continue
         if B["mode"] == K.MODE_FIN:
-            assert ready[b], "lower item dispatched before its block input was final"
-            xs = r[s:s + m] - xbuf[s:s + m]
+            assert ready[b] == B["nfin"], "lower item dispatched before its block input was final"
+            xs = xbuf[s:s + m].copy()
         elif B["mode"] == K.MODE_GATHER:
             assert cnt[b] == B["target_l"], "lower item dispatched before its children finished"
-            xs = np.array([r[s + i] - cbuf[H["cin_ptr"][s + i]: H["cin_ptr"][s + i + 1]].sum() for i in range(m)])
+            xs = np.array([r[s + i] - csum(s + i) for i in range(m)])
         else:
             assert B["target_l"] == 0
             xs = r[s:s + m].copy()
@@ -67,25 +74,18 @@ def emulate_lower(H, r):
         p = int(B["parent"])
         if p >= 0:
             cnt[p] += 1
-            if cnt[p] == blocks[p]["target_l"] and blocks[p]["mode"] == K.MODE_FIN:
-                P = blocks[p]  # this item finalises the parent's contribution sums
-                for i in range(int(P["m"])):
-                    row = int(P["start"]) + i
-                    xbuf[row] = cbuf[H["cin_ptr"][row]: H["cin_ptr"][row + 1]].sum()
-                ready[p] = True
     assert np.all(cnt == blocks["target_l"])
     assert np.array_equal(segs, H["tiles_l"]["nseg"])
     emulate_lower.cbuf = cbuf
     return y
 
 
-def test_both_lower_input_modes_are_exercised():
-    _, f = _factors((6, 6, 28), 64)
+def test_all_lower_input_modes_are_exercised():
+    _, f = _factors((10, 10, 60), 64)
     H = K.pack(f)
     modes = set(H["blocks"]["mode"].tolist())
-    assert K.MODE_LEAF in modes and K.MODE_GATHER in modes
-    # force the FIN path everywhere and re-check against the oracle
-    H["blocks"]["mode"][H["blocks"]["mode"] == K.MODE_GATHER] = K.MODE_FIN
+    assert modes == {K.MODE_LEAF, K.MODE_GATHER, K.MODE_FIN}
+    assert (H["items_l"][:, 3] < 0).sum() == H["blocks"]["nfin"].sum() > 0
     r = np.random.default_rng(3).standard_normal(f.plan.n)
     ref = O.solve_lower(f, r)
     assert np.abs(emulate_lower(H, r) - ref).max() <= 1e-12 * np.abs(ref).max()
