@@ -99,6 +99,8 @@ class L2Flush:
 
 
 def time_steps(W, mode, steps, warmup, flush):
+    import gc
+
     import torch
     from paper_2306_05893_b200 import _lib
 
@@ -109,6 +111,8 @@ def time_steps(W, mode, steps, warmup, flush):
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
     iters, asm, slv = [], [], []
     launches = 0
+    gc.collect()
+    gc.disable()  # no collector pauses between the host calls of a timed step
     for k in range(steps):
         flush()
         l0 = _lib.launch_count()
@@ -120,6 +124,7 @@ def time_steps(W, mode, steps, warmup, flush):
         asm.append(res.assembly_time * 1e3)
         slv.append(res.solve_time * 1e3)
     torch.cuda.synchronize()
+    gc.enable()
     per = [a.elapsed_time(b) for a, b in ev]
     return dict(total_ms=sum(per), ms=statistics.median(per), iterations=statistics.median(iters),
                 assembly_ms=statistics.median(asm), solve_ms=statistics.median(slv), launches=launches,

@@ -60,9 +60,12 @@ struct PcgArgs {
     double *x;
     double tol;
     long long max_it;
+    int fuse_p;  // 1: p = z + beta p computed inside the SpMV gathers (small systems:
+                 // one grid barrier less); 0: a separate pass (large systems: one gather)
 };
 
 constexpr int kPcgBlock = 256;
+constexpr int64_t kFuseRows = 150000;
 constexpr int kMaxGrid = kNumSM * 8;
 
 // Sense-counting grid barrier (all CTAs co-resident: cooperative launch).
@@ -228,21 +231,43 @@ pcg_persistent(PcgWork W, PcgArgs a, tsb_ldlt_desc D) {
         ph[k] += t - tl;
         tl = t;
     };
+    // p = z + beta p (krylov.py:156): either fused into the SpMV gathers (every
+    // reader rounds identically; the row owner stores it) or materialised once
+    // per iteration by a separate pass (P3) so the SpMV gathers one vector
+    double *pcur = W.p0, *pnxt = W.p1;
+    if (!done && !a.fuse_p) {  // p = z for the first iteration (beta = 0, p0 = 0)
+        for (int64_t i = gtid; i < n; i += gstride) pnxt[i] = add(__ldcg(W.z + i), mul(beta, __ldcg(pcur + i)));
+        double *t = pcur;
+        pcur = pnxt;
+        pnxt = t;
+        grid_sync(W.bar);
+    }
     while (!done) {
-        double *pold = (it & 1) ? W.p1 : W.p0;
-        double *pnew = (it & 1) ? W.p0 : W.p1;
-        // P1: ap = A (z + beta p_old); p_new stored by the row owner
+        // P1: ap = A p (bit-exact row sums), p.ap block partials
         double v = 0.0;
-        {
-            XDirection xa{W.z, pold, beta};
+        if (a.fuse_p) {
+            XDirection xa{W.z, pcur, beta};
             for (int64_t row = grp; row < n; row += ngrp) {
                 const int lo = a.rp[row], hi = a.rp[row + 1];
                 const double s = row_sum_exact(lo, hi - lo, a.ci, a.val, xa, lane8, gmask);
                 if (lane8 == 0) {
                     const double pr = xa((int)row);
-                    pnew[row] = pr;
+                    pnxt[row] = pr;
                     W.ap[row] = s;
                     v += pr * s;
+                }
+            }
+            double *t = pcur;  // the new direction is in pnxt
+            pcur = pnxt;
+            pnxt = t;
+        } else {
+            XPlainCG xa{pcur};
+            for (int64_t row = grp; row < n; row += ngrp) {
+                const int lo = a.rp[row], hi = a.rp[row + 1];
+                const double s = row_sum_exact(lo, hi - lo, a.ci, a.val, xa, lane8, gmask);
+                if (lane8 == 0) {
+                    W.ap[row] = s;
+                    v += __ldcg(pcur + row) * s;
                 }
             }
         }
@@ -254,7 +279,7 @@ pcg_persistent(PcgWork W, PcgArgs a, tsb_ldlt_desc D) {
         // P2: x, r updates, ||r||^2 (+ z, r.z for diagonal preconditioners)
         double vr = 0.0, vz = 0.0;
         for (int64_t i = gtid; i < n; i += gstride) {
-            a.x[i] = add(__ldcg(a.x + i), mul(alpha, __ldcg(pnew + i)));
+            a.x[i] = add(__ldcg(a.x + i), mul(alpha, __ldcg(pcur + i)));
             const double ri = sub(__ldcg(W.r + i), mul(alpha, __ldcg(W.ap + i)));
             W.r[i] = ri;
             vr += ri * ri;
@@ -298,6 +323,13 @@ pcg_persistent(PcgWork W, PcgArgs a, tsb_ldlt_desc D) {
         beta = rzn / rz;
         rz = rzn;
         lap(4);
+        if (!a.fuse_p) {  // P3: p = z + beta p, NumPy rounding
+            for (int64_t i = gtid; i < n; i += gstride) pnxt[i] = add(__ldcg(W.z + i), mul(beta, __ldcg(pcur + i)));
+            double *t = pcur;
+            pcur = pnxt;
+            pnxt = t;
+            grid_sync(W.bar);
+        }
     }
     ph[5] = gtimer() - t_loop;
     if (blockIdx.x == 0 && tid == 0) {
@@ -434,7 +466,9 @@ extern "C" int tsb_pcg_solve(tsb_pcg_t h, int64_t nrows, const int32_t *d_row_pt
         // status word = 0, first zero row = all ones (atomicMin target) for this solve
         TSB_CUDA(cudaMemsetAsync(W.status, 0, 8, s));
         TSB_CUDA(cudaMemsetAsync(W.status + 2, 0xff, 8, s));
-        PcgArgs a{d_row_ptr, d_col_ind, d_values, d_b, d_x0, d_inv_diag, d_x, tol, (long long)max_iterations};
+        // small systems are barrier-latency bound, large ones gather bound
+        PcgArgs a{d_row_ptr, d_col_ind, d_values, d_b, d_x0, d_inv_diag, d_x, tol, (long long)max_iterations,
+                  nrows < kFuseRows ? 1 : 0};
         tsb_ldlt_desc D{};
         if (kind == TSB_PRECOND_LDLT) {
             D = ldlt_desc(ldlt);

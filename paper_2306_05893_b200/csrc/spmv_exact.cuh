@@ -23,6 +23,12 @@ struct XPlain {
     __device__ __forceinline__ double operator()(int j) const { return __ldg(x + j); }
 };
 
+// x[j] produced earlier in the same (persistent) kernel: read through L2.
+struct XPlainCG {
+    const double *x;
+    __device__ __forceinline__ double operator()(int j) const { return __ldcg(x + j); }
+};
+
 // p_j = z_j + beta * p_old_j computed on the fly (PCG direction update
 // fused into the SpMV, krylov.py:156); every reader rounds identically.
 struct XDirection {
