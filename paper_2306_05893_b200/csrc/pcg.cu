@@ -105,8 +105,10 @@ __device__ __forceinline__ double all_partials(const double *part, int kind, dou
     return out;
 }
 
+// LDL^T: 3 CTAs/SM (sweep staging in shared memory); Jacobi / identity: the
+// SpMV is gather-latency bound, more resident warps per SM
 template <int KIND>
-__global__ void __launch_bounds__(kPcgBlock, 3)
+__global__ void __launch_bounds__(kPcgBlock, KIND == TSB_PRECOND_LDLT ? 3 : 6)
 pcg_persistent(PcgWork W, PcgArgs a, tsb_ldlt_desc D) {
     extern __shared__ __align__(128) double smem[];  // sweep staging (LDL^T)
     __shared__ double red[32];
@@ -356,7 +358,7 @@ struct tsb_pcg {
 namespace tsb {
 
 template <int KIND>
-static int occupancy_grid(size_t smem) {
+static int occupancy_grid(size_t smem, int64_t n) {
     auto k = pcg_persistent<KIND>;
     allow_max_smem(k);
     int per_sm = 0, dev = 0, nsm = kNumSM;
@@ -365,7 +367,9 @@ static int occupancy_grid(size_t smem) {
     TSB_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
     if (per_sm < 1) throw Error(TSB_E_ARG, "pcg kernel does not fit on an SM");
     // barrier cost grows with the CTA count, latency hiding with it: tunable
-    int cap = KIND == TSB_PRECOND_LDLT ? 3 : 4;
+    // small systems: grid-barrier latency dominates (fewer CTAs); large ones
+    // are gather bound (more resident warps)
+    int cap = KIND == TSB_PRECOND_LDLT ? 3 : (n < kFuseRows ? 3 : 6);
     if (const char *env = getenv("TSB_PCG_CTAS_PER_SM")) cap = atoi(env) > 0 ? atoi(env) : cap;
     if (per_sm > cap) per_sm = cap;
     const int g = per_sm * nsm;
@@ -414,8 +418,8 @@ extern "C" int tsb_pcg_create(int64_t n, tsb_pcg_t *out) {
         W.status = reinterpret_cast<int32_t *>(take(256));
         TSB_CUDA(cudaMemset(W.bar, 0, 256));
         TSB_CUDA(cudaMallocHost(&h->h_state, sizeof(PcgState)));
-        h->grid[TSB_PRECOND_IDENTITY] = occupancy_grid<TSB_PRECOND_IDENTITY>(0);
-        h->grid[TSB_PRECOND_JACOBI] = occupancy_grid<TSB_PRECOND_JACOBI>(0);
+        h->grid[TSB_PRECOND_IDENTITY] = occupancy_grid<TSB_PRECOND_IDENTITY>(0, n);
+        h->grid[TSB_PRECOND_JACOBI] = occupancy_grid<TSB_PRECOND_JACOBI>(0, n);
         *out = h;
     });
 }
@@ -474,7 +478,7 @@ extern "C" int tsb_pcg_solve(tsb_pcg_t h, int64_t nrows, const int32_t *d_row_pt
             D = ldlt_desc(ldlt);
             const size_t sm = sweep_smem_lower(D) > sweep_smem_upper(D) ? sweep_smem_lower(D) : sweep_smem_upper(D);
             if (sm != h->smem_ldlt || h->grid[TSB_PRECOND_LDLT] == 0) {
-                h->grid[TSB_PRECOND_LDLT] = occupancy_grid<TSB_PRECOND_LDLT>(sm);
+                h->grid[TSB_PRECOND_LDLT] = occupancy_grid<TSB_PRECOND_LDLT>(sm, W.n);
                 h->smem_ldlt = sm;
             }
             launch<TSB_PRECOND_LDLT>(h, a, D, h->grid[TSB_PRECOND_LDLT], sm, s);

@@ -6,7 +6,7 @@ namespace tsb {
 
 constexpr int kSpmvBlock = 256;  // 32 rows per CTA (8 lanes per row)
 
-__global__ void __launch_bounds__(kSpmvBlock)
+__global__ void __launch_bounds__(kSpmvBlock, 8)
 spmv_kernel(int64_t nrows, const int32_t *__restrict__ rp, const int32_t *__restrict__ ci,
             const double *__restrict__ val, const double *__restrict__ x, double *__restrict__ y) {
     const int lane = threadIdx.x & 31;
