@@ -105,10 +105,11 @@ __device__ __forceinline__ double all_partials(const double *part, int kind, dou
     return out;
 }
 
-// LDL^T: 3 CTAs/SM (sweep staging in shared memory); Jacobi / identity: the
-// SpMV is gather-latency bound, more resident warps per SM
-template <int KIND>
-__global__ void __launch_bounds__(kPcgBlock, KIND == TSB_PRECOND_LDLT ? 3 : 6)
+// MINB = resident CTAs per SM the register budget is sized for: LDL^T 3
+// (sweep staging in shared memory); Jacobi / identity 3 for small systems
+// (grid-barrier bound), 6 for large ones (the SpMV is gather-latency bound)
+template <int KIND, int MINB>
+__global__ void __launch_bounds__(kPcgBlock, MINB)
 pcg_persistent(PcgWork W, PcgArgs a, tsb_ldlt_desc D) {
     extern __shared__ __align__(128) double smem[];  // sweep staging (LDL^T)
     __shared__ double red[32];
@@ -352,14 +353,15 @@ struct tsb_pcg {
     void *mem = nullptr;
     tsb::PcgState *h_state = nullptr;  // pinned
     int grid[3] = {0, 0, 0};
+    bool big = false;
     size_t smem_ldlt = 0;
 };
 
 namespace tsb {
 
-template <int KIND>
-static int occupancy_grid(size_t smem, int64_t n) {
-    auto k = pcg_persistent<KIND>;
+template <int KIND, int MINB>
+static int occupancy_grid(size_t smem) {
+    auto k = pcg_persistent<KIND, MINB>;
     allow_max_smem(k);
     int per_sm = 0, dev = 0, nsm = kNumSM;
     TSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kPcgBlock, smem));
@@ -367,19 +369,17 @@ static int occupancy_grid(size_t smem, int64_t n) {
     TSB_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
     if (per_sm < 1) throw Error(TSB_E_ARG, "pcg kernel does not fit on an SM");
     // barrier cost grows with the CTA count, latency hiding with it: tunable
-    // small systems: grid-barrier latency dominates (fewer CTAs); large ones
-    // are gather bound (more resident warps)
-    int cap = KIND == TSB_PRECOND_LDLT ? 3 : (n < kFuseRows ? 3 : 6);
+    int cap = MINB;
     if (const char *env = getenv("TSB_PCG_CTAS_PER_SM")) cap = atoi(env) > 0 ? atoi(env) : cap;
     if (per_sm > cap) per_sm = cap;
     const int g = per_sm * nsm;
     return g < kMaxGrid ? g : kMaxGrid;
 }
 
-template <int KIND>
+template <int KIND, int MINB>
 static void launch(tsb_pcg *h, PcgArgs &a, tsb_ldlt_desc &D, int grid, size_t smem, cudaStream_t s) {
     void *args[] = {&h->W, &a, &D};
-    TSB_CUDA(cudaLaunchCooperativeKernel((const void *)pcg_persistent<KIND>, dim3(grid), dim3(kPcgBlock),
+    TSB_CUDA(cudaLaunchCooperativeKernel((const void *)pcg_persistent<KIND, MINB>, dim3(grid), dim3(kPcgBlock),
                                          args, smem, s));
     count_launch();
 }
@@ -418,8 +418,11 @@ extern "C" int tsb_pcg_create(int64_t n, tsb_pcg_t *out) {
         W.status = reinterpret_cast<int32_t *>(take(256));
         TSB_CUDA(cudaMemset(W.bar, 0, 256));
         TSB_CUDA(cudaMallocHost(&h->h_state, sizeof(PcgState)));
-        h->grid[TSB_PRECOND_IDENTITY] = occupancy_grid<TSB_PRECOND_IDENTITY>(0, n);
-        h->grid[TSB_PRECOND_JACOBI] = occupancy_grid<TSB_PRECOND_JACOBI>(0, n);
+        h->big = n >= kFuseRows;
+        h->grid[TSB_PRECOND_IDENTITY] = h->big ? occupancy_grid<TSB_PRECOND_IDENTITY, 6>(0)
+                                               : occupancy_grid<TSB_PRECOND_IDENTITY, 3>(0);
+        h->grid[TSB_PRECOND_JACOBI] = h->big ? occupancy_grid<TSB_PRECOND_JACOBI, 6>(0)
+                                             : occupancy_grid<TSB_PRECOND_JACOBI, 3>(0);
         *out = h;
     });
 }
@@ -478,14 +481,20 @@ extern "C" int tsb_pcg_solve(tsb_pcg_t h, int64_t nrows, const int32_t *d_row_pt
             D = ldlt_desc(ldlt);
             const size_t sm = sweep_smem_lower(D) > sweep_smem_upper(D) ? sweep_smem_lower(D) : sweep_smem_upper(D);
             if (sm != h->smem_ldlt || h->grid[TSB_PRECOND_LDLT] == 0) {
-                h->grid[TSB_PRECOND_LDLT] = occupancy_grid<TSB_PRECOND_LDLT>(sm, W.n);
+                h->grid[TSB_PRECOND_LDLT] = occupancy_grid<TSB_PRECOND_LDLT, 3>(sm);
                 h->smem_ldlt = sm;
             }
-            launch<TSB_PRECOND_LDLT>(h, a, D, h->grid[TSB_PRECOND_LDLT], sm, s);
+            launch<TSB_PRECOND_LDLT, 3>(h, a, D, h->grid[TSB_PRECOND_LDLT], sm, s);
         } else if (kind == TSB_PRECOND_JACOBI) {
-            launch<TSB_PRECOND_JACOBI>(h, a, D, h->grid[TSB_PRECOND_JACOBI], 0, s);
+            if (h->big)
+                launch<TSB_PRECOND_JACOBI, 6>(h, a, D, h->grid[TSB_PRECOND_JACOBI], 0, s);
+            else
+                launch<TSB_PRECOND_JACOBI, 3>(h, a, D, h->grid[TSB_PRECOND_JACOBI], 0, s);
         } else {
-            launch<TSB_PRECOND_IDENTITY>(h, a, D, h->grid[TSB_PRECOND_IDENTITY], 0, s);
+            if (h->big)
+                launch<TSB_PRECOND_IDENTITY, 6>(h, a, D, h->grid[TSB_PRECOND_IDENTITY], 0, s);
+            else
+                launch<TSB_PRECOND_IDENTITY, 3>(h, a, D, h->grid[TSB_PRECOND_IDENTITY], 0, s);
         }
         if (report != nullptr) {
             TSB_CUDA(cudaMemcpyAsync(h->h_state, W.st, sizeof(PcgState), cudaMemcpyDeviceToHost, s));

@@ -2,9 +2,9 @@
 
 `spmv` is bit-identical to the reference (same per-row summation order).
 `pcg`/`cg` run entirely on the device for the identity, Jacobi and
-nested-dissection LDL^T preconditioners: one CUDA graph with a conditional
-WHILE node per solve, alpha/beta/convergence on the device, one report read
-back per solve.  Vectors may be NumPy arrays (copied in/out, reference
+nested-dissection LDL^T preconditioners: one persistent cooperative kernel
+per solve (csrc/pcg.cu), alpha/beta/convergence on the device, one report
+read back per solve.  Vectors may be NumPy arrays (copied in/out, reference
 semantics) or CUDA tensors (stay resident; the solution is returned as a
 CUDA tensor).
 """
@@ -137,7 +137,9 @@ def jacobi_precond(a: CsrMatrix) -> JacobiPreconditioner:
 # ---------------------------------------------------------------------------
 
 class _PcgHandle:
-    """One libtsb PCG workspace (graphs cached per preconditioner)."""
+    """One libtsb PCG workspace (device vectors + report struct)."""
+
+    pending = None
 
     def __init__(self, n: int):
         import ctypes as C
@@ -186,8 +188,39 @@ def _precond_kind(precond, a):
     return None
 
 
+class _DeviceReport:
+    """SolveReport of a device solve whose report struct is read back lazily:
+    a caller that only enqueues more device work (the integrator's kinematic
+    update) does not stall the stream; the first attribute read synchronises."""
+
+    def __init__(self, handle, t0):
+        self._h, self._t0, self._r = handle, t0, None
+        handle.pending = self  # the next solve on this workspace reads it first
+
+    def _get(self):
+        if self._r is None:
+            import ctypes as C
+
+            rep = _lib.Report()
+            _lib.check(_lib.load().tsb_pcg_report(self._h.h, C.byref(rep), _lib.stream_ptr()), "pcg_report")
+            if rep.status == _lib.TSB_E_SOLVER:
+                raise SolverError(f"zero diagonal entry at row {int(rep.zero_diag_row)}")
+            self._r = SolveReport(int(rep.iterations), float(rep.final_residual), bool(rep.converged),
+                                  time.perf_counter() - self._t0)
+        return self._r
+
+    iterations = property(lambda self: self._get().iterations)
+    final_residual = property(lambda self: self._get().final_residual)
+    converged = property(lambda self: self._get().converged)
+    wall_time = property(lambda self: self._get().wall_time)
+
+    def __repr__(self):
+        return repr(self._get())
+
+
 def pcg(a: CsrMatrix, b, precond, config: SolverConfig, x0=None, workers: int = 1):
-    """Preconditioned CG (krylov.py:120-158); returns (x, SolveReport)."""
+    """Preconditioned CG (krylov.py:120-158); returns (x, SolveReport).  With a
+    device right-hand side the report is read back lazily (see _DeviceReport)."""
     t0 = time.perf_counter()
     n = a.ncols
     kind = _precond_kind(precond, a)
@@ -198,10 +231,14 @@ def pcg(a: CsrMatrix, b, precond, config: SolverConfig, x0=None, workers: int = 
     db, host = _vec_in(b, n, "rhs")
     dx0 = _vec_in(x0, n, "x0")[0] if x0 is not None else None
     x = t.empty(n, dtype=t.float64, device="cuda")
+    if not host:
+        solve_device(a, db, x, kind, ldlt, config.tolerance, config.max_iterations, x0=dx0, inv_diag=inv,
+                     sync=False)
+        return x, _DeviceReport(_handle(a.nrows), t0)
     rep = solve_device(a, db, x, kind, ldlt, config.tolerance, config.max_iterations, x0=dx0, inv_diag=inv)
     report = SolveReport(int(rep.iterations), float(rep.final_residual), bool(rep.converged),
                          time.perf_counter() - t0)
-    return (x.cpu().numpy() if host else x), report
+    return x.cpu().numpy(), report
 
 
 def solve_device(a: CsrMatrix, d_b, d_x, kind, ldlt, tol, max_it, x0=None, inv_diag=None, sync=True):
@@ -212,6 +249,9 @@ def solve_device(a: CsrMatrix, d_b, d_x, kind, ldlt, tol, max_it, x0=None, inv_d
     if a.nrows != a.ncols:
         raise SolverError(f"pcg needs a square matrix, got {a.nrows}x{a.ncols}")
     h = _handle(a.nrows)
+    if h.pending is not None:  # a lazily read report of this workspace: fetch it before it is overwritten
+        h.pending._get()
+        h.pending = None
     d_rp, d_ci = a.device_pattern()
     dv = a.device_values()
     rep = _lib.Report()
