@@ -19,7 +19,6 @@ import os
 import statistics
 import subprocess
 import sys
-import threading
 import time
 from pathlib import Path
 
@@ -245,6 +244,9 @@ def cpu_baseline(W, mode, budget_s=20.0, max_steps=10, threads=1):
 # ---------------------------------------------------------------------------
 
 class ClockSampler:
+    """nvidia-smi samples clocks into a file while the timed region runs (no
+    Python reader thread competing for the GIL with the launch path)."""
+
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,utilization.gpu")
 
@@ -254,19 +256,17 @@ class ClockSampler:
         self.lines = []
 
     def __enter__(self):
+        import tempfile
+
+        self.path = tempfile.NamedTemporaryFile(prefix="clocks_", suffix=".csv", delete=False).name
         try:
+            self.fh = open(self.path, "w")
             self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                                          "-lms", "50", "-i", str(self.gpu)], stdout=subprocess.PIPE,
+                                          "-lms", "50", "-i", str(self.gpu)], stdout=self.fh,
                                          stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
-            self.thread.start()
         except Exception:
             self.proc = None
         return self
-
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
 
     def __exit__(self, *a):
         if self.proc is not None:
@@ -275,6 +275,12 @@ class ClockSampler:
                 self.proc.wait(timeout=5)
             except Exception:
                 self.proc.kill()
+            self.fh.close()
+            try:
+                self.lines = [ln.strip() for ln in open(self.path) if ln.strip()]
+                os.unlink(self.path)
+            except Exception:
+                self.lines = []
         return False
 
     def summary(self):
