@@ -415,7 +415,8 @@ def main():
         },
         "iterations": main_r["iterations"], "assembly_ms": main_r["assembly_ms"], "pcg_ms": main_r["solve_ms"],
         "step_ms": {"min": min(main_r["per_step"]), "median": statistics.median(main_r["per_step"]),
-                    "max": max(main_r["per_step"])},
+                    "max": max(main_r["per_step"]),
+                    "argmax": int(max(range(len(main_r["per_step"])), key=lambda k: main_r["per_step"][k]))},
         other: {"ms_per_step": other_r["ms"], "iterations": other_r["iterations"],
                 "assembly_ms": other_r["assembly_ms"], "pcg_ms": other_r["solve_ms"]},
         "trisolve": {"apply_ms": apply_r["ms"], "gbs": apply_r["gbs"], "frac": apply_r["gbs"] / hbm,

@@ -254,6 +254,104 @@ def _items(tiles_of_block, first_tile):
     return out
 
 
+HOP = 1.5               # us: dependency release -> consumer sees it
+SCHED_WORKERS = 444     # resident CTAs the list schedule assumes (148 SMs x 3)
+
+
+def _window(T, lim, it):
+    """v-columns [w0, w1) an item reads (csrc item_window); T = the sweep's tile table."""
+    if it[2] > 0:
+        p0 = (it[2] - 1) * SEG_PAIRS
+        cnt = min(SEG_PAIRS, int(T["np"][it[0]]) - p0)
+        w0 = int(T["tl"][it[0]]) + 2 * p0
+        return w0, min(w0 + 2 * cnt, lim)
+    w0 = int(T["tl"][it[0]:it[1]].min())
+    return w0, min(int((T["tl"][it[0]:it[1]] + 2 * T["np"][it[0]:it[1]]).max()), lim)
+
+
+def _list_schedule(entries, cost, children, sweep):
+    """Ticket order = start order of a list schedule of the items on
+    SCHED_WORKERS workers: whenever a worker frees, it starts the ready item
+    with the longest remaining path (critical path first).  An item starts
+    only after its dependencies finished, so the order is topological (what
+    the persistent kernel needs to be deadlock-free).  entries: (block, item,
+    dep, tail); dep: None, ("children", b) = every GEMV item of b's children,
+    ("fin", b) = b's finalisers, ("parent", p) = every item of block p."""
+    import heapq
+
+    n = len(entries)
+    by_block = {}
+    fin_of = {}
+    for k, (b, it, dep, tail) in enumerate(entries):
+        if it[2] < 0:
+            fin_of.setdefault(b, []).append(k)
+        else:
+            by_block.setdefault(b, []).append(k)
+    # dependency counts and successor lists per "dependency group"
+    group_members = {}
+    for k, (b, it, dep, tail) in enumerate(entries):
+        if dep is None:
+            continue
+        kind, blk = dep
+        if kind == "children":
+            members = [j for c in children[blk] for j in by_block.get(c, [])]
+        elif kind == "fin":
+            members = fin_of.get(blk, [])
+        else:
+            members = by_block.get(blk, [])
+        group_members.setdefault(dep, members)
+    waiting = {}
+    succ = [[] for _ in range(n)]
+    remaining = {}
+    for dep, members in group_members.items():
+        remaining[dep] = len(members)
+        for j in members:
+            succ[j].append(dep)
+    dependants = {}
+    for k, (b, it, dep, tail) in enumerate(entries):
+        if dep is not None:
+            dependants.setdefault(dep, []).append(k)
+    ready = []     # released items, by priority (longest remaining path first)
+    pending = []   # items whose dependencies finished, by release time
+    for k, (b, it, dep, tail) in enumerate(entries):
+        if dep is None or remaining.get(dep, 0) == 0:
+            heapq.heappush(ready, (-tail, k))
+    running = []   # (finish time, k)
+    free = SCHED_WORKERS
+    t = 0.0
+    start_order = []
+    while ready or pending or running:
+        while pending and pending[0][0] <= t:
+            _, k = heapq.heappop(pending)
+            heapq.heappush(ready, (-entries[k][3], k))
+        while free and ready:
+            _, k = heapq.heappop(ready)
+            start_order.append(k)
+            heapq.heappush(running, (t + cost(entries[k]), k))
+            free -= 1
+        # next event: a worker finishes or a pending item is released
+        nxt_run = running[0][0] if running else float("inf")
+        nxt_rel = pending[0][0] if pending else float("inf")
+        if nxt_rel < nxt_run and free:
+            t = nxt_rel
+            continue
+        if not running:
+            t = nxt_rel
+            continue
+        t, k = heapq.heappop(running)
+        free += 1
+        for dep in succ[k]:
+            remaining[dep] -= 1
+            if remaining[dep] == 0:
+                for j in dependants.get(dep, []):
+                    heapq.heappush(pending, (t + HOP, j))
+    if len(start_order) != n:
+        raise RuntimeError(f"{sweep} item list has a dependency cycle")
+    out = np.array([(entries[k][0], entries[k][1][0], entries[k][1][1], entries[k][1][2]) for k in start_order],
+                   dtype=np.int32)
+    return out.reshape(-1, 4)
+
+
 def pack(factors, subset=None):
     """Host arrays of the tiled block-inverse layout + item lists (pure NumPy).
 
@@ -369,35 +467,44 @@ def pack(factors, subset=None):
         fin_items[i] = [(int(edges[j]), int(edges[j + 1]), -1) for j in range(k) if edges[j + 1] > edges[j]]
         nfin[i] = len(fin_items[i])
 
-    def cost(up, it):  # us: item overhead + streaming at ~40 GB/s per CTA
+    def cost(up, it):  # us: item latency + streaming at ~25 GB/s per CTA (calibrated on B200 traces)
+        if it[2] < 0:
+            return 2.5
         nbytes = min(int(tables[up]["np"][it[0]:it[1]].sum()) * TILE * 16, ITEM_BYTES)
-        return 1.5 + nbytes / 40e3 + (1.0 if it[2] else 0.0)
+        return 2.5 + nbytes / 25e3 + (0.5 if it[2] else 0.0)
+
+    def touches_anc(i, it):  # upper item whose column window reaches -z_anc (waits for the parent)
+        if not na_[i]:
+            return False
+        w0, w1 = _window(tables[True], int(ms_[i]) + int(na_[i]), it)
+        return w1 > ms_[i]
 
     order = sorted(range(nb), key=lambda i: bfs[i].start)  # children before parents
-    ready_l, done_l = np.zeros(nb), np.zeros(nb)
-    for i in order:
-        if children[i]:
-            ready_l[i] = max(done_l[c] for c in children[i]) + 1.0
-        done_l[i] = ready_l[i] + max(cost(False, it) for it in items[False][i]) + (2.0 if nfin[i] else 0.0)
+    # lower: blocks wait for their children's items (or their finalisers)
+    own_l = np.array([max(cost(False, it) for it in items[False][i]) + (cost(False, (0, 0, -1)) + HOP if nfin[i] else 0.0)
+                      for i in range(nb)])
     tail_l = np.zeros(nb)
     for i in reversed(order):  # parents first
-        tail_l[i] = (done_l[i] - ready_l[i]) + (tail_l[parent[i]] if parent[i] >= 0 else 0.0)
-    lower = sorted([(ready_l[i], -tail_l[i], bfs[i].start, 0, it[0], i, it[1], it[2])
-                    for i in range(nb) for it in fin_items[i]] +
-                   [(ready_l[i], -tail_l[i], bfs[i].start, 1, it[0], i, it[1], it[2])
-                    for i in range(nb) for it in items[False][i]])
-    items_l = np.array([(x[5], x[4], x[6], x[7]) for x in lower], dtype=np.int32).reshape(-1, 4)
-    start_u, done_u = np.zeros(nb), np.zeros(nb)
-    for i in reversed(order):  # parents first
-        start_u[i] = done_u[parent[i]] + 1.0 if parent[i] >= 0 else 0.0
-        done_u[i] = start_u[i] + max(cost(True, it) for it in items[True][i])
+        tail_l[i] = own_l[i] + (HOP + tail_l[parent[i]] if parent[i] >= 0 else 0.0)
+    lower = []  # (item, block, kind, deps-key): kind 0 finaliser, 1 GEMV
+    for i in range(nb):
+        for it in fin_items[i]:
+            lower.append((i, it, ("children", i), tail_l[i] + 1.0))
+        for it in items[False][i]:
+            dep = ("fin", i) if nfin[i] else (("children", i) if target_l[i] else None)
+            lower.append((i, it, dep, tail_l[i]))
+    items_l = _list_schedule(lower, lambda x: cost(False, x[1]), children, "lower")
+    # upper: items reading -z_anc wait for their parent's items
+    own_u = np.array([max(cost(True, it) for it in items[True][i]) for i in range(nb)])
     tail_u = np.zeros(nb)
     for i in order:  # children first
-        tail_u[i] = (done_u[i] - start_u[i]) + max((tail_u[c] for c in children[i]), default=0.0)
-    upper = sorted((start_u[i], -tail_u[i], -bfs[i].start, it[0], i, it[1], it[2])
-                   for i in range(nb) for it in items[True][i])
-    items_u = np.array([(x[4], x[3], x[5], x[6]) for x in upper], dtype=np.int32).reshape(-1, 4)
-
+        tail_u[i] = own_u[i] + max((HOP + tail_u[c] for c in children[i]), default=0.0)
+    upper = []
+    for i in range(nb):
+        for it in items[True][i]:
+            dep = ("parent", int(parent[i])) if (parent[i] >= 0 and touches_anc(i, it)) else None
+            upper.append((i, it, dep, tail_u[i]))
+    items_u = _list_schedule(upper, lambda x: cost(True, x[1]), children, "upper")
 
     # ---------------- block table ----------------
     blocks = np.zeros(nb, dtype=BLOCK_DTYPE)
@@ -414,16 +521,8 @@ def pack(factors, subset=None):
     blocks["anc_off"] = anc_off[:-1]
     max_cb = min(CB_CAP, int(blk_contrib[mode == MODE_GATHER].max())) if np.any(mode == MODE_GATHER) else 0
 
-    def window(up, i, it):  # v-columns an item reads (csrc item_window)
-        T = tables[up]
-        lim = int(ms_[i] + (na_[i] if up else 0))
-        if it[2]:
-            p0 = (it[2] - 1) * SEG_PAIRS
-            cnt = min(SEG_PAIRS, int(T["np"][it[0]]) - p0)
-            w0 = int(T["tl"][it[0]]) + 2 * p0
-            return w0, min(w0 + 2 * cnt, lim)
-        w0 = int(T["tl"][it[0]:it[1]].min())
-        return w0, min(int((T["tl"][it[0]:it[1]] + 2 * T["np"][it[0]:it[1]]).max()), lim)
+    def window(up, i, it):
+        return _window(tables[up], int(ms_[i] + (na_[i] if up else 0)), it)
 
     max_w = max([1] + [(lambda w: w[1] - w[0])(window(up, i, it)) for up in (False, True)
                        for i in range(nb) for it in items[up][i]])

@@ -100,7 +100,8 @@ def emulate_upper(H, w, z=None):
     for b, t0, t1, sg in H["items_u"]:
         B = blocks[b]
         s, m, na = int(B["start"]), int(B["m"]), int(B["na"])
-        if na and B["parent"] >= 0:
+        w0, w1 = K._window(H["tiles_u"], m + na, (t0, t1, sg))
+        if na and B["parent"] >= 0 and w1 > m:  # the item reads -z_anc (as the kernel: window-based)
             p = int(B["parent"])
             assert done[p] == blocks[p]["n_u"], "upper item dispatched before the parent's z"
         v = np.concatenate([w[s:s + m], -z[H["anc"][B["anc_off"]: B["anc_off"] + na]]])
