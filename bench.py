@@ -104,15 +104,19 @@ def time_steps(W, mode, steps, warmup, flush):
     from paper_2306_05893_b200 import _lib
 
     integ, st, solve = W["integ"], W["state"], W["solvers"][mode]
+    gc.disable()  # collector runs between steps (outside the events), never inside one
     for _ in range(warmup):
+        flush()
         integ.compute_step(st, solve)
+        gc.collect(0)
     torch.cuda.synchronize()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
     iters, asm, slv = [], [], []
     launches = 0
-    gc.collect()
-    gc.disable()  # no collector pauses between the host calls of a timed step
+    res = None
     for k in range(steps):
+        res = None
+        gc.collect(0)  # frees the previous step's device buffers held in reference cycles
         flush()
         l0 = _lib.launch_count()
         ev[k][0].record()
@@ -264,6 +268,12 @@ class ClockSampler:
             self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
                                           "-lms", "50", "-i", str(self.gpu)], stdout=self.fh,
                                          stderr=subprocess.DEVNULL, text=True)
+            # nvidia-smi's start-up (NVML init, first query) stalls the device for
+            # tens of ms: let it settle before the timed region starts
+            t0 = time.time()
+            while time.time() - t0 < 5.0 and os.path.getsize(self.path) < 2:
+                time.sleep(0.05)
+            time.sleep(0.2)
         except Exception:
             self.proc = None
         return self
