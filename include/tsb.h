@@ -101,7 +101,7 @@ typedef struct tsb_asm_plan {
     int64_t nnz;                /* CSR nnz                                   */
     int64_t n_fixed_slots;      /* pinned diagonal slots                     */
     const int32_t *d_conn;      /* [4][m] element node ids                   */
-    const double *d_grads;      /* [12][m] rest shape gradients (a*3+i)      */
+    const double *d_grads;      /* [m][12] rest shape gradients (a*3+i)      */
     const double *d_vol;        /* [m] rest volumes                          */
     const double *d_mass_share; /* [m] rho*V/4 (integrator._mass_vals)       */
     const double *d_rest;       /* [3N] rest positions                       */
@@ -113,9 +113,11 @@ typedef struct tsb_asm_plan {
     const int32_t *d_node_ptr;  /* [N+1] incidence offsets                   */
     const int32_t *d_node_list; /* e*4 + a, ascending e per node             */
     const int32_t *d_fixed_slots; /* [n_fixed_slots]                         */
-    double *d_work;             /* [36][m] scratch: rotated grads, f_e, K v_e */
+    double *d_work;             /* [48][m] scratch: [m][36] grads', f_e, K v_e; [m][12] F F^T, S (StVK) */
     int32_t *d_flags;           /* [4] device status words                   */
 } tsb_asm_plan;
+
+enum { TSB_LAW_COROTATIONAL = 0, TSB_LAW_LINEAR = 1, TSB_LAW_STVK = 2 };
 
 typedef struct tsb_asm_coeffs {
     double lam, mu;             /* Lame constants (models.py:57-64)          */
@@ -123,7 +125,7 @@ typedef struct tsb_asm_coeffs {
     double rayleigh_stiffness;  /* beta                                      */
     double rayleigh_mass;       /* alpha                                     */
     double cm, ck;              /* per-triplet coefficients (integrator.py:135-143) */
-    int32_t linear;             /* 1: R := I (linear elastic)                */
+    int32_t law;                /* TSB_LAW_*: 0 corotational, 1 linear (R := I), 2 StVK */
     int32_t want_matrix;        /* 0: forces only (model.internal_forces)    */
 } tsb_asm_coeffs;
 

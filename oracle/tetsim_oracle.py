@@ -160,8 +160,38 @@ def corotational(nodes, elements, rest, positions, velocities, linear=False):
     return f, kv, krot
 
 
+def stvk(nodes, elements, rest, positions, velocities):
+    """(f, kv, kblocks) of the St-Venant-Kirchhoff law (models.py:241-287):
+    F = sum_a x_a g_a^T, G = (F^T F - I)/2, S = lam tr(G) I + 2 mu G,
+    f_a = V F S g_a, K_ab = V(lam h_a h_b^T + mu h_b h_a^T + mu (g_a.g_b) F F^T
+    + (g_a^T S g_b) I) with h_a = F g_a (material + geometric tangent)."""
+    el = np.asarray(elements)
+    m = len(el)
+    ndof = 3 * len(positions)
+    g, vol, lam, mu = rest["grads"], rest["vol"], rest["lam"], rest["mu"]
+    xe = np.asarray(positions)[el]
+    f = np.einsum("eai,eaj->eij", xe, g)
+    green = 0.5 * (np.einsum("eki,ekj->eij", f, f) - np.eye(3))
+    s = lam * np.trace(green, axis1=1, axis2=2)[:, None, None] * np.eye(3) + 2.0 * mu * green
+    fe = vol[:, None, None] * np.einsum("eij,eaj->eai", f @ s, g)
+    force = np.bincount(rest["gdof"].ravel(), weights=fe.reshape(m, 12).ravel(), minlength=ndof)
+    fg = np.einsum("eij,eaj->eai", f, g)
+    fft = f @ np.transpose(f, (0, 2, 1))
+    gg = np.einsum("eai,ebi->eab", g, g)
+    gsg = np.einsum("eai,eij,ebj->eab", g, s, g)
+    k = lam * np.einsum("eai,ebk->eaibk", fg, fg)
+    k += mu * np.einsum("eak,ebi->eaibk", fg, fg)
+    k += mu * np.einsum("eab,eik->eaibk", gg, fft)
+    k += np.einsum("eab,ik->eaibk", gsg, np.eye(3))
+    k *= vol[:, None, None, None, None]
+    kblocks = k.reshape(m, 12, 12)
+    ve = np.asarray(velocities).reshape(-1, 3)[el].reshape(m, 12)
+    kv = np.bincount(rest["gdof"].ravel(), weights=np.einsum("epq,eq->ep", kblocks, ve).ravel(), minlength=ndof)
+    return force, kv, kblocks
+
+
 def assemble_system(nodes, elements, fixed_nodes, rest, positions, velocities, f_ext_state,
-                    dt, gravity, rayleigh_mass=0.0, rayleigh_stiffness=0.0, linear=False):
+                    dt, gravity, rayleigh_mass=0.0, rayleigh_stiffness=0.0, linear=False, law=None):
     """A values (CSR order), b, f_int, f_ext, row_ptr, col_ind of one fused pass
     (integrator.py:145-169): mass triplets first, then 144 stiffness triplets
     per element, per-triplet coefficients, bincount merge, pinned rows identity."""
@@ -171,7 +201,10 @@ def assemble_system(nodes, elements, fixed_nodes, rest, positions, velocities, f
     gdof = rest["gdof"]
     mass_rows = gdof.reshape(-1)
     mass_vals = np.repeat(rest["share"], 12)
-    f_int, kv, krot = corotational(nodes, elements, rest, positions, velocities, linear)
+    if law == "stvk":
+        f_int, kv, krot = stvk(nodes, elements, rest, positions, velocities)
+    else:
+        f_int, kv, krot = corotational(nodes, elements, rest, positions, velocities, linear or law == "linear")
     rows = np.concatenate([mass_rows, np.repeat(gdof, 12, axis=1).ravel()])
     cols = np.concatenate([mass_rows, np.tile(gdof, (1, 12)).ravel()])
     vals = np.concatenate([mass_vals, krot.reshape(-1)])

@@ -50,7 +50,7 @@ class AsmCoeffs(C.Structure):
     _fields_ = [
         ("lam", C.c_double), ("mu", C.c_double), ("h", C.c_double),
         ("rayleigh_stiffness", C.c_double), ("rayleigh_mass", C.c_double),
-        ("cm", C.c_double), ("ck", C.c_double), ("linear", c_i32), ("want_matrix", c_i32),
+        ("cm", C.c_double), ("ck", C.c_double), ("law", c_i32), ("want_matrix", c_i32),
     ]
 
 

@@ -95,6 +95,16 @@ def _i32(a):
     return np.ascontiguousarray(a, dtype=np.int32)
 
 
+LAWS = {"corotational": 0, "linear": 1, "stvk": 2}  # tsb.h TSB_LAW_*
+
+
+def law_code(law) -> int:
+    try:
+        return LAWS[law]
+    except KeyError:
+        raise ValueError(f"no device kernel for material law {law!r}") from None
+
+
 class AssemblyPlan:
     """Device buffers + the C struct handed to tsb_assemble_corot."""
 
@@ -121,7 +131,7 @@ class AssemblyPlan:
         if fixed_dof is not None:
             fd[fixed_dof] = 1
         self.fixed_dof = up(fd, np.uint8)
-        self.work = t.empty(max(m, 1) * 36, dtype=t.float64, device=dev)
+        self.work = t.empty(max(m, 1) * 48, dtype=t.float64, device=dev)
         self.flags = t.zeros(4, dtype=t.int32, device=dev)
         self.pattern = pattern
         if pattern is not None:
@@ -154,10 +164,10 @@ class AssemblyPlan:
     def for_model(cls, precomp):
         return cls(precomp)
 
-    def coeffs(self, h=0.0, beta=0.0, alpha=0.0, cm=1.0, ck=1.0, linear=False, want_matrix=True):
+    def coeffs(self, h=0.0, beta=0.0, alpha=0.0, cm=1.0, ck=1.0, law="corotational", want_matrix=True):
         lam, mu = self.lame
         return _lib.AsmCoeffs(lam=lam, mu=mu, h=h, rayleigh_stiffness=beta, rayleigh_mass=alpha,
-                              cm=cm, ck=ck, linear=int(linear), want_matrix=int(want_matrix))
+                              cm=cm, ck=ck, law=law_code(law), want_matrix=int(want_matrix))
 
     def run(self, coeffs, x, v, f_ext_state, values, b, f_int, kv, f_ext):
         import ctypes as C
@@ -167,7 +177,7 @@ class AssemblyPlan:
             C.byref(self.c), C.byref(coeffs), P(x), P(v), P(f_ext_state), P(values), P(b),
             P(f_int), P(kv), P(f_ext), _lib.stream_ptr()), "assemble")
 
-    def element_pass(self, positions, velocities, want_blocks=False, linear=False):
+    def element_pass(self, positions, velocities, want_blocks=False, law="corotational"):
         """Model-level pass (no matrix): (f, kv, kblocks|None) in the caller's array kind."""
         import ctypes as C
 
@@ -182,7 +192,7 @@ class AssemblyPlan:
         n = 3 * self.N
         f = t.empty(n, dtype=t.float64, device="cuda")
         kv = t.empty(n, dtype=t.float64, device="cuda")
-        co = self.coeffs(linear=linear, want_matrix=False)
+        co = self.coeffs(law=law, want_matrix=False)
         self.flags.zero_()
         vz = v if v is not None else t.zeros(n, dtype=t.float64, device="cuda")
         self.run(co, x, vz, None, None, None, f, kv, None)

@@ -25,11 +25,23 @@
 //                    b = f_ext - f_int - (h+beta) K v - alpha M v, b[pinned]=0
 //                    (integrator.py:158-162), every operation rounded as NumPy
 //                    rounds it.
+//
+// Material laws (tsb_asm_coeffs.law): corotational (above), linear (R := I)
+// and St-Venant-Kirchhoff (stvk_forces_and_stiffness, models.py:241-287).
+// For StVK the element pass stores h_a = F g_a in place of the rotated
+// gradients plus F F^T and S (second Piola-Kirchhoff stress) in an auxiliary
+// [m][12] region after the [m][36] scratch; f_e = V F S g_a and, in stress
+// form, (K v)_a = V(lam (sum_b h_b.v_b) h_a + mu W h_a + mu F F^T Hv g_a
+// + Hv S g_a) with W = sum_b h_b v_b^T, Hv = sum_b v_b g_b^T -- the 12x12
+// element tangent is never formed.  The block pass evaluates
+// K_ab = V(lam h_a h_b^T + mu h_b h_a^T + mu (g_a.g_b) F F^T + (g_a^T S g_b) I)
+// in the reference's term order.
 #include "tsb_common.cuh"
 
 namespace tsb {
 
 constexpr int kWork = 36;  // per-element scratch: g^[12], f_e[12], (Kv)_e[12]
+constexpr int kAux = 12;   // StVK: F F^T (xx xy xz yy yz zz), S (same order), after m * kWork
 
 __device__ __forceinline__ bool finite3(double a, double b, double c) {
     return isfinite(a) && isfinite(b) && isfinite(c);
@@ -86,11 +98,86 @@ __device__ __forceinline__ void ke_apply(const double u[12], const double g[12],
             out[3 * a + i] = V * (S[3 * i] * g[3 * a] + S[3 * i + 1] * g[3 * a + 1] + S[3 * i + 2] * g[3 * a + 2]);
 }
 
+// St-Venant-Kirchhoff element pass (models.py:258-285), see the header.
+__device__ __forceinline__ void stvk_element(int64_t e, int64_t m, const double g[12], const double xe[12],
+                                             const double ve[12], double V, double lam, double mu,
+                                             double *__restrict__ work) {
+    double F[9];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+            F[3 * i + j] = xe[i] * g[j] + xe[3 + i] * g[3 + j] + xe[6 + i] * g[6 + j] + xe[9 + i] * g[9 + j];
+    double S[9], FFt[9];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            S[3 * i + j] = 0.5 * ((F[i] * F[j] + F[3 + i] * F[3 + j] + F[6 + i] * F[6 + j]) - (i == j ? 1.0 : 0.0));
+            FFt[3 * i + j] = F[3 * i] * F[3 * j] + F[3 * i + 1] * F[3 * j + 1] + F[3 * i + 2] * F[3 * j + 2];
+        }
+    const double trg = S[0] + S[4] + S[8];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) S[k] = 2.0 * mu * S[k] + (k % 4 == 0 ? lam * trg : 0.0);
+    double FS[9];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) FS[3 * i + j] = F[3 * i] * S[j] + F[3 * i + 1] * S[3 + j] + F[3 * i + 2] * S[6 + j];
+    double h[12], t[12];
+    double s1 = 0.0, W[9], Hv[9];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            h[3 * a + i] = F[3 * i] * g[3 * a] + F[3 * i + 1] * g[3 * a + 1] + F[3 * i + 2] * g[3 * a + 2];
+            t[3 * a + i] = V * (FS[3 * i] * g[3 * a] + FS[3 * i + 1] * g[3 * a + 1] + FS[3 * i + 2] * g[3 * a + 2]);
+        }
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            W[3 * i + k] = h[i] * ve[k] + h[3 + i] * ve[3 + k] + h[6 + i] * ve[6 + k] + h[9 + i] * ve[9 + k];
+            Hv[3 * i + k] = ve[i] * g[k] + ve[3 + i] * g[3 + k] + ve[6 + i] * g[6 + k] + ve[9 + i] * g[9 + k];
+        }
+#pragma unroll
+    for (int a = 0; a < 12; ++a) s1 += h[a] * ve[a];
+    double2 *out = reinterpret_cast<double2 *>(work + e * kWork);
+#pragma unroll
+    for (int k = 0; k < 6; ++k) out[k] = make_double2(h[2 * k], h[2 * k + 1]);
+#pragma unroll
+    for (int k = 0; k < 6; ++k) out[6 + k] = make_double2(t[2 * k], t[2 * k + 1]);
+    // M1 = mu FF^T Hv + Hv S, so the last two terms are M1 g_a
+    double M1[9];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+            M1[3 * i + j] = mu * (FFt[3 * i] * Hv[j] + FFt[3 * i + 1] * Hv[3 + j] + FFt[3 * i + 2] * Hv[6 + j]) +
+                            (Hv[3 * i] * S[j] + Hv[3 * i + 1] * S[3 + j] + Hv[3 * i + 2] * S[6 + j]);
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+            t[3 * a + i] = V * (lam * s1 * h[3 * a + i] +
+                                mu * (W[3 * i] * h[3 * a] + W[3 * i + 1] * h[3 * a + 1] + W[3 * i + 2] * h[3 * a + 2]) +
+                                (M1[3 * i] * g[3 * a] + M1[3 * i + 1] * g[3 * a + 1] + M1[3 * i + 2] * g[3 * a + 2]));
+#pragma unroll
+    for (int k = 0; k < 6; ++k) out[12 + k] = make_double2(t[2 * k], t[2 * k + 1]);
+    double2 *aux = reinterpret_cast<double2 *>(work + m * kWork + e * kAux);
+    aux[0] = make_double2(FFt[0], FFt[1]);
+    aux[1] = make_double2(FFt[2], FFt[4]);
+    aux[2] = make_double2(FFt[5], FFt[8]);
+    aux[3] = make_double2(S[0], S[1]);
+    aux[4] = make_double2(S[2], S[4]);
+    aux[5] = make_double2(S[5], S[8]);
+}
+
 __global__ void __launch_bounds__(128)
 elem_kernel(int64_t m, const int32_t *__restrict__ conn, const double *__restrict__ grads,
             const double *__restrict__ vol, const double *__restrict__ rest,
             const double *__restrict__ x, const double *__restrict__ v, double lam, double mu,
-            int linear, double *__restrict__ work, int32_t *__restrict__ flags) {
+            int law, double *__restrict__ work, int32_t *__restrict__ flags) {
     const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (e >= m) return;
     int nd[4];
@@ -117,9 +204,13 @@ elem_kernel(int64_t m, const int32_t *__restrict__ conn, const double *__restric
     }
     if (!ok) atomicOr(flags, 1);
     const double V = __ldg(vol + e);
+    if (law == TSB_LAW_STVK) {
+        stvk_element(e, m, g, xe, ve, V, lam, mu, work);
+        return;
+    }
 
     double R[9];
-    if (linear) {
+    if (law == TSB_LAW_LINEAR) {
 #pragma unroll
         for (int k = 0; k < 9; ++k) R[k] = (k % 4 == 0) ? 1.0 : 0.0;
     } else {
@@ -181,8 +272,41 @@ __device__ __forceinline__ void rot_block(const double *ga, const double *gb, do
             k[3 * i + j] = V * (lam * ga[i] * gb[j] + mu * ga[j] * gb[i] + (i == j ? mu * G : 0.0));
 }
 
+// StVK element block entry (models.py:272-279, same term order):
+// V (((lam h_a,i h_b,k + mu h_a,k h_b,i) + mu (G fft_ik)) + gsg d_ik).
+__device__ __forceinline__ void stvk_block(const double *ha, const double *hb, const double *ra,
+                                           const double *rb, const double aux[12], double V, double lam,
+                                           double mu, double k[9]) {
+    const double G = ra[0] * rb[0] + ra[1] * rb[1] + ra[2] * rb[2];
+    const double S[9] = {aux[6], aux[7], aux[8], aux[7], aux[9], aux[10], aux[8], aux[10], aux[11]};
+    const double P[9] = {aux[0], aux[1], aux[2], aux[1], aux[3], aux[4], aux[2], aux[4], aux[5]};
+    double sb[3];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) sb[j] = S[3 * j] * rb[0] + S[3 * j + 1] * rb[1] + S[3 * j + 2] * rb[2];
+    const double gsg = ra[0] * sb[0] + ra[1] * sb[1] + ra[2] * sb[2];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            double v = add(add(mul(lam, mul(ha[i], hb[j])), mul(mu, mul(ha[j], hb[i]))), mul(mu, mul(G, P[3 * i + j])));
+            if (i == j) v = add(v, gsg);
+            k[3 * i + j] = mul(v, V);
+        }
+}
+
+__device__ __forceinline__ void load_aux(const double *__restrict__ work, int64_t m, int64_t e, double aux[12]) {
+    const double2 *p = reinterpret_cast<const double2 *>(work + m * kWork + e * kAux);
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+        const double2 t = __ldg(p + k);
+        aux[2 * k] = t.x;
+        aux[2 * k + 1] = t.y;
+    }
+}
+
+template <bool STVK>
 __global__ void __launch_bounds__(256)
-block_kernel(int64_t nb, const int4 *__restrict__ blk, const int32_t *__restrict__ list,
+block_kernel(int64_t nb, int64_t m, const int4 *__restrict__ blk, const int32_t *__restrict__ list,
              const double *__restrict__ work, const double *__restrict__ grads,
              const double *__restrict__ vol, const double *__restrict__ share, double lam,
              double mu, double cm, double ck, double *__restrict__ values) {
@@ -208,6 +332,7 @@ block_kernel(int64_t nb, const int4 *__restrict__ blk, const int32_t *__restrict
     constexpr int U = 4;
     for (int k0 = info.z; k0 < info.w; k0 += U) {
         double ga[U][3], gb[U][3], G[U], V[U];
+        double ra[U][3], rb[U][3], aux[STVK ? U : 1][12];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int k = k0 + u < info.w ? k0 + u : info.w - 1;
@@ -215,22 +340,25 @@ block_kernel(int64_t nb, const int4 *__restrict__ blk, const int32_t *__restrict
             const int64_t e = c >> 4;
             const int a = (c >> 2) & 3, b = c & 3;
             const double *we = work + e * kWork;
-            double ra[3], rb[3];
 #pragma unroll
             for (int i = 0; i < 3; ++i) {
                 ga[u][i] = __ldg(we + 3 * a + i);
                 gb[u][i] = __ldg(we + 3 * b + i);
-                ra[i] = __ldg(grads + e * 12 + 3 * a + i);
-                rb[i] = __ldg(grads + e * 12 + 3 * b + i);
+                ra[u][i] = __ldg(grads + e * 12 + 3 * a + i);
+                rb[u][i] = __ldg(grads + e * 12 + 3 * b + i);
             }
-            G[u] = ra[0] * rb[0] + ra[1] * rb[1] + ra[2] * rb[2];
+            if constexpr (STVK) load_aux(work, m, e, aux[u]);
+            G[u] = ra[u][0] * rb[u][0] + ra[u][1] * rb[u][1] + ra[u][2] * rb[u][2];
             V[u] = __ldg(vol + e);
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             if (k0 + u >= info.w) break;
             double kb[9];
-            rot_block(ga[u], gb[u], G[u], V[u], lam, mu, kb);
+            if constexpr (STVK)
+                stvk_block(ga[u], gb[u], ra[u], rb[u], aux[u], V[u], lam, mu, kb);
+            else
+                rot_block(ga[u], gb[u], G[u], V[u], lam, mu, kb);
 #pragma unroll
             for (int q = 0; q < 9; ++q) acc[q] = add(acc[q], mul(ck, kb[q]));
         }
@@ -298,16 +426,21 @@ node_kernel(int64_t N, const int32_t *__restrict__ node_ptr, const int32_t *__re
 
 __global__ void __launch_bounds__(128)
 kblock_kernel(int64_t m, const double *__restrict__ work, const double *__restrict__ grads,
-              const double *__restrict__ vol, double lam, double mu, double *__restrict__ out) {
+              const double *__restrict__ vol, double lam, double mu, int law, double *__restrict__ out) {
     const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (e >= m) return;
     const double *we = work + e * kWork;
     const double V = vol[e];
+    double aux[12];
+    if (law == TSB_LAW_STVK) load_aux(work, m, e, aux);
     for (int a = 0; a < 4; ++a)
         for (int b = 0; b < 4; ++b) {
             const double *ra = grads + e * 12 + 3 * a, *rb = grads + e * 12 + 3 * b;
             double kb[9];
-            rot_block(we + 3 * a, we + 3 * b, ra[0] * rb[0] + ra[1] * rb[1] + ra[2] * rb[2], V, lam, mu, kb);
+            if (law == TSB_LAW_STVK)
+                stvk_block(we + 3 * a, we + 3 * b, ra, rb, aux, V, lam, mu, kb);
+            else
+                rot_block(we + 3 * a, we + 3 * b, ra[0] * rb[0] + ra[1] * rb[1] + ra[2] * rb[2], V, lam, mu, kb);
             for (int i = 0; i < 3; ++i)
                 for (int j = 0; j < 3; ++j) out[e * 144 + (3 * a + i) * 12 + 3 * b + j] = kb[3 * i + j];
         }
@@ -353,7 +486,7 @@ void launch_elem(const tsb_asm_plan *p, const tsb_asm_coeffs *c, const double *x
                  cudaStream_t s) {
     if (p->n_elems <= 0) return;
     elem_kernel<<<grid_for(p->n_elems, 128), 128, 0, s>>>(p->n_elems, p->d_conn, p->d_grads, p->d_vol,
-                                                          p->d_rest, x, v, c->lam, c->mu, c->linear,
+                                                          p->d_rest, x, v, c->lam, c->mu, c->law,
                                                           p->d_work, p->d_flags);
     TSB_LAUNCHED();
 }
@@ -367,12 +500,14 @@ extern "C" int tsb_assemble_corot(const tsb_asm_plan *p, const tsb_asm_coeffs *c
     using namespace tsb;
     return guard([&] {
         if (p == nullptr || c == nullptr) throw Error(TSB_E_ARG, "null plan/coeffs");
+        if (c->law < TSB_LAW_COROTATIONAL || c->law > TSB_LAW_STVK) throw Error(TSB_E_ARG, "unknown material law");
         cudaStream_t s = as_stream(stream);
         launch_elem(p, c, d_x, d_v, s);
         if (c->want_matrix && d_values != nullptr) {
             if (p->n_blocks > 0) {
-                block_kernel<<<grid_for(p->n_blocks, 256), 256, 0, s>>>(
-                    p->n_blocks, reinterpret_cast<const int4 *>(p->d_blk), p->d_blk_list, p->d_work,
+                auto kern = c->law == TSB_LAW_STVK ? block_kernel<true> : block_kernel<false>;
+                kern<<<grid_for(p->n_blocks, 256), 256, 0, s>>>(
+                    p->n_blocks, p->n_elems, reinterpret_cast<const int4 *>(p->d_blk), p->d_blk_list, p->d_work,
                     p->d_grads, p->d_vol, p->d_mass_share, c->lam, c->mu, c->cm, c->ck, d_values);
                 TSB_LAUNCHED();
             }
@@ -400,7 +535,7 @@ extern "C" int tsb_element_blocks(const tsb_asm_plan *p, const tsb_asm_coeffs *c
         launch_elem(p, c, d_x, nullptr, s);
         if (p->n_elems > 0) {
             kblock_kernel<<<grid_for(p->n_elems, 128), 128, 0, s>>>(p->n_elems, p->d_work, p->d_grads,
-                                                                    p->d_vol, c->lam, c->mu, d_kblocks);
+                                                                    p->d_vol, c->lam, c->mu, c->law, d_kblocks);
             TSB_LAUNCHED();
         }
     });

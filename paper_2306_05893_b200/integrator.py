@@ -176,7 +176,7 @@ class BackwardEulerIntegrator:
         self._mass_share = share
         self._gravity_force = (self.mass_diag.reshape(-1, 3) * np.asarray(config.gravity)).ravel()
         self._plan: AssemblyPlan | None = None
-        self._linear = bool(getattr(model, "linear", False))
+        self._law = getattr(model, "law", "corotational")
 
     @property
     def _mass_vals(self) -> np.ndarray:
@@ -207,7 +207,7 @@ class BackwardEulerIntegrator:
         cfg = self.config
         cm, ck = self._coefficients()
         co = plan.coeffs(h=cfg.dt, beta=cfg.rayleigh_stiffness, alpha=cfg.rayleigh_mass, cm=cm, ck=ck,
-                         linear=self._linear, want_matrix=True)
+                         law=self._law, want_matrix=True)
         values = t.empty(len(pat["col_ind"]), dtype=t.float64, device="cuda")
         b = t.empty(n, dtype=t.float64, device="cuda")
         f_int = t.empty(n, dtype=t.float64, device="cuda")

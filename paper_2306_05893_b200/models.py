@@ -1,6 +1,6 @@
 """Element physics for linear tetrahedra (drop-in for tetsim.models, models.py:1-346).
 
-The corotational law runs on the B200 (libtsb elem/block/node kernels, see
+The corotational, linear and St-Venant-Kirchhoff laws run on the B200 (libtsb elem/block/node kernels, see
 csrc/assemble.cu): `accumulate` returns the internal forces and K v computed
 on the device and, when a TripletStream is given, the rotated element blocks
 in the reference's emission order (element-major, row-major 12x12,
@@ -29,6 +29,8 @@ __all__ = [
     "lumped_mass",
     "CorotationalModel",
     "LinearElasticModel",
+    "StVenantKirchhoffModel",
+    "stvk_forces_and_stiffness",
     "make_model",
 ]
 
@@ -155,12 +157,12 @@ def _device_plan(precomp: ElementPrecomp, mesh: Mesh | None = None):
     return precomp._device
 
 
-def _element_pass(precomp, positions, velocities, stream, linear):
+def _element_pass(precomp, positions, velocities, stream, law):
     if not (_lib.is_tensor(positions) or np.all(np.isfinite(positions))):
         raise ModelError("non-finite positions")
     plan = _device_plan(precomp)
     f, kv, kblocks = plan.element_pass(positions, velocities, want_blocks=stream is not None,
-                                       linear=linear)
+                                       law=law)
     if stream is not None:
         stream.add_block(precomp.block_rows, precomp.block_cols, kblocks.reshape(-1))
     return f, kv
@@ -172,7 +174,18 @@ def corotational_forces_and_stiffness(precomp: ElementPrecomp, positions, stream
     Returns (f, kv) as NumPy arrays for NumPy input, CUDA tensors for tensor
     input; kv is None when velocities is None.
     """
-    return _element_pass(precomp, positions, velocities, stream, linear=False)
+    return _element_pass(precomp, positions, velocities, stream, "corotational")
+
+
+def stvk_forces_and_stiffness(precomp: ElementPrecomp, positions, stream=None, velocities=None):
+    """St-Venant-Kirchhoff forces V F S g_a and K v on the device (models.py:241-287).
+
+    Same elem/block/node kernels as the corotational law with the law switch
+    set (csrc/assemble.cu): the element pass stores h_a = F g_a, F F^T and S,
+    the block pass forms V(lam h_a h_b^T + mu h_b h_a^T + mu (g_a.g_b) F F^T
+    + (g_a^T S g_b) I) per contribution.
+    """
+    return _element_pass(precomp, positions, velocities, stream, "stvk")
 
 
 def lumped_mass(mesh: Mesh, params: MaterialParams, stream=None) -> np.ndarray:
@@ -187,7 +200,6 @@ def lumped_mass(mesh: Mesh, params: MaterialParams, stream=None) -> np.ndarray:
 
 class CorotationalModel:
     law = "corotational"
-    linear = False
 
     def __init__(self, mesh: Mesh, params: MaterialParams):
         self.mesh = mesh
@@ -195,7 +207,7 @@ class CorotationalModel:
         self.precomp = precompute(mesh, params)
 
     def accumulate(self, positions, stream=None, velocities=None):
-        return _element_pass(self.precomp, positions, velocities, stream, linear=self.linear)
+        return _element_pass(self.precomp, positions, velocities, stream, self.law)
 
     def internal_forces(self, positions):
         return self.accumulate(positions)[0]
@@ -206,12 +218,19 @@ class LinearElasticModel(CorotationalModel):
     (BASELINE config 1, 'linear elastic'); f = Ke (x - x0), K = Ke."""
 
     law = "linear"
-    linear = True
+
+
+class StVenantKirchhoffModel(CorotationalModel):
+    """St-Venant-Kirchhoff hyperelasticity (models.py:320-331): exact tangent
+    with material and geometric parts, assembled by the same device kernels."""
+
+    law = "stvk"
 
 
 _MODEL_CLASSES = {
     CorotationalModel.law: CorotationalModel,
     LinearElasticModel.law: LinearElasticModel,
+    StVenantKirchhoffModel.law: StVenantKirchhoffModel,
 }
 
 

@@ -32,11 +32,11 @@ def clamped(nx, ny, nz, spacing=0.1):
     return mesh.with_fixed_nodes(np.flatnonzero(mesh.nodes[:, 2] == 0.0))
 
 
-def scenario_system(dims, steps, tol=1e-9, with_triplets=False):
+def scenario_system(dims, steps, tol=1e-9, with_triplets=False, law="corotational"):
     """Run `steps` Jacobi-PCG steps from rest (gravity along -y), then record
     the next step's assembled system and its solves."""
     mesh = clamped(*dims)
-    model = tetsim.make_model("corotational", mesh, PARAMS)
+    model = tetsim.make_model(law, mesh, PARAMS)
     integ = BackwardEulerIntegrator(mesh, model, IntegratorConfig(dt=0.01, gravity=(0.0, -9.81, 0.0)))
     cfg = krylov.SolverConfig(tol, 8000)
     solve = lambda a, b: krylov.pcg(a, b, krylov.jacobi_precond(a), cfg)  # noqa: E731
@@ -156,6 +156,10 @@ def nd_cases():
 
 def main():
     meta = dict(numpy_version=np.array(np.__version__), reference=np.array("tetsim " + tetsim.__version__))
+    stvk = dict(law=np.array("stvk"))
+    np.savez_compressed(OUT / "beam_stvk.npz", **scenario_system((3, 3, 8), 6, law="stvk"), **stvk, **meta)
+    if "--only-stvk" in sys.argv:
+        return
     np.savez_compressed(OUT / "beam_small.npz", **scenario_system((3, 3, 8), 6, with_triplets=True), **meta)
     np.savez_compressed(OUT / "beam_cfg1.npz", **scenario_system((6, 6, 28), 6), **meta)
     np.savez_compressed(OUT / "ldlt_small.npz", **ldlt_case((4, 4, 12), 16, stale_from=4, at=7), **meta)

@@ -158,3 +158,48 @@ def test_device_resident_state_matches_host_state(golden, params):
         rd = integ.step(st_d, solve)
         assert rh.report.iterations == rd.report.iterations
     assert np.array_equal(st_h.positions, st_d.positions.cpu().numpy())
+
+
+def _stvk_setup(golden, params):
+    g = golden("beam_stvk")
+    mesh = clamped_beam(*map(int, g["dims"]))
+    model = models.make_model("stvk", mesh, params)
+    assert isinstance(model, models.StVenantKirchhoffModel)
+    integ = BackwardEulerIntegrator(mesh, model, IntegratorConfig(dt=0.01, gravity=(0.0, -9.81, 0.0)))
+    st = SimState(g["positions"].copy(), g["velocities"].copy(), np.zeros_like(g["positions"]),
+                  np.zeros(len(g["b"])), g["f_ext_state"])
+    return g, mesh, model, integ, st
+
+
+def test_stvk_assemble_system_vs_reference(golden, params):
+    """St-Venant-Kirchhoff law (models.py:241-287) through the fused device assembly."""
+    g, mesh, model, integ, st = _stvk_setup(golden, params)
+    a, b, info = integ.assemble_system(st)
+    assert np.array_equal(a.row_ptr, g["row_ptr"]) and np.array_equal(a.col_ind, g["col_ind"])
+    assert rel(a.values, g["values"]) <= 1e-12
+    assert rel(b, g["b"]) <= 1e-12
+    assert rel(info["f_int"], g["f_int"]) <= 1e-12
+    assert np.array_equal(info["f_ext"], g["f_ext"])
+
+
+def test_stvk_accumulate_and_blocks(golden, params):
+    g, mesh, model, integ, st = _stvk_setup(golden, params)
+    s = TripletStream()
+    s.begin_pass()
+    f, kv = model.accumulate(g["positions"], stream=s, velocities=g["velocities"].ravel())
+    s.end_pass()
+    assert rel(f, g["f_int"]) <= 1e-12 and rel(kv, g["kv"]) <= 1e-12
+    rest = O.rest_data(mesh.nodes, mesh.elements, 1e5, 0.3, 1000.0)
+    _, _, kb = O.stvk(mesh.nodes, mesh.elements, rest, g["positions"], g["velocities"])
+    assert rel(s.vals(), kb.reshape(-1)) <= 1e-12
+    assert rel(models.stvk_forces_and_stiffness(model.precomp, g["positions"])[0], g["f_int"]) <= 1e-12
+
+
+def test_stvk_integrator_step_vs_reference(golden, params):
+    g, mesh, model, integ, st = _stvk_setup(golden, params)
+    cfg = krylov.SolverConfig(1e-9, 8000)
+    res = integ.step(st, lambda a, b: krylov.pcg(a, b, krylov.jacobi_precond(a), cfg))
+    assert res.report.converged and res.report.iterations == int(g["next_iterations"])
+    assert rel(res.accelerations, g["next_accel"]) <= 1e-10
+    assert rel(res.velocities, g["next_velocities"]) <= 1e-10
+    assert rel(res.positions - g["positions"], g["next_positions"] - g["positions"]) <= 1e-10

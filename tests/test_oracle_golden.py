@@ -113,3 +113,18 @@ def test_corotational_kv_matches_reference(golden):
     f, kv, _ = O.corotational(g["nodes"], g["elements"], rest, g["positions"], g["velocities"])
     assert np.array_equal(kv, g["kv"])
     assert np.array_equal(f, g["f_int"])
+
+
+def test_stvk_assembly_matches_reference(golden):
+    """St-Venant-Kirchhoff law (models.py:241-287) through the fused assembly."""
+    g = golden("beam_stvk")
+    rest = O.rest_data(g["nodes"], g["elements"], 1e5, 0.3, 1000.0)
+    out = O.assemble_system(g["nodes"], g["elements"], g["fixed_nodes"], rest, g["positions"], g["velocities"],
+                            g["f_ext_state"], 0.01, (0.0, -G, 0.0), law="stvk")
+    assert np.array_equal(out["row_ptr"], g["row_ptr"]) and np.array_equal(out["col_ind"], g["col_ind"])
+    scale = np.abs(g["values"]).max()
+    assert np.abs(out["values"] - g["values"]).max() <= 1e-12 * scale
+    assert np.abs(out["b"] - g["b"]).max() <= 1e-12 * np.abs(g["b"]).max()
+    assert np.abs(out["f_int"] - g["f_int"]).max() <= 1e-12 * np.abs(g["f_int"]).max()
+    _, kv, _ = O.stvk(g["nodes"], g["elements"], rest, g["positions"], g["velocities"])
+    assert np.abs(kv - g["kv"]).max() <= 1e-12 * np.abs(g["kv"]).max()
