@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define TSB_ABI_VERSION 2
+#define TSB_ABI_VERSION 3
 
 enum tsb_status {
     TSB_OK = 0,
@@ -267,6 +267,76 @@ int tsb_ldlt_upper_scaled(tsb_ldlt_t h, const double *d_y, double *d_z, void *st
 /* after a lower sweep: d_out[row] = sum of the contributions to each external
  * row (d_ext_rows), fixed order */
 int tsb_ldlt_external_sums(tsb_ldlt_t h, double *d_out, void *stream);
+
+/* ------------------------------------------------------------------------
+ * Device LDL^T refactorisation        replaces ldlt_factor (numeric phase)
+ *                                     ndprecond.py:501-572 (+ the host pack
+ *                                     of the factor into the sweep layout)
+ * Multifrontal over the dissection tree: per front F = [A_bb A_b,anc; A_anc,b 0]
+ * + extend-added children updates, a tiled (64 x 64) partial Cholesky of its
+ * m pivots gives C, LS = F21 C^-T and U = F22 - LS LS^T (sent to the parent);
+ * a right triangular solve gives [C^-1; LS C^-1] and the pack writes
+ * Linv = diag(C) C^-1 and M = LS C^-1 into the tiles of an existing
+ * tsb_ldlt handle layout (d_g, d_gt) and d = diag(C)^2 into d_d.  The host
+ * "program" (8 int64 per op, built once per pattern by
+ * paper_2306_05893_b200/refactor.py) lists the launches in order.
+ * ---------------------------------------------------------------------- */
+typedef struct tsb_front {
+    int64_t off;                  /* front F (nf x nf, column-major) in d_ws    */
+    int64_t woff;                 /* C^-1 (m x m, column-major) in d_wb         */
+    int64_t ioff;                 /* pivot-tile inverses (P x 2 x 64 x 64) in d_inv */
+    int32_t m, na, nf, P, NT;     /* pivots, coupling rows, m + na, pivot tiles, tiles */
+    int32_t start;                /* first permuted row                          */
+} tsb_front;
+
+typedef struct tsb_front_pair {   /* extend-add child -> parent                  */
+    int32_t child, parent;
+    int64_t tp_off;               /* child's na positions in the parent front    */
+} tsb_front_pair;
+
+enum {
+    TSB_RF_SCATTER = 1,           /* a: entries                                  */
+    TSB_RF_EXTEND = 2,            /* a, b: pair range; c: max child na           */
+    TSB_RF_DIAG = 3,              /* a: k; b: list offset; c: fronts             */
+    TSB_RF_PANEL = 4,             /* a: k; b: list offset; c: fronts; d: tasks   */
+    TSB_RF_UPDATE = 5,            /* same                                        */
+    TSB_RF_TSCALE = 6,            /* same (right solve, column tile k)           */
+    TSB_RF_TUPDATE = 7,           /* same                                        */
+    TSB_RF_PACK = 8,              /* pack tiles + d                              */
+    TSB_RF_IDENT = 9              /* C^-1 buffers := I                           */
+};
+
+typedef struct tsb_refactor_desc {
+    int64_t n_fronts;
+    int64_t n_prog;               /* ops                                          */
+    const int64_t *h_prog;        /* HOST [n_prog][8]: op, a, b, c, d, 0, 0, 0    */
+    const tsb_front *d_fronts;
+    const int32_t *d_lists;       /* [.][4]: front, panel/scale prefix, update prefix, 0 */
+    const int32_t *d_sc_src;      /* A entry (original CSR order) ...           */
+    const int64_t *d_sc_dst;      /* ... -> d_ws offset (lower triangle only)   */
+    const tsb_front_pair *d_pairs;
+    const int32_t *d_tp;
+    const tsb_ldlt_tile *d_tiles_lower;
+    const tsb_ldlt_tile *d_tiles_upper;
+    const int32_t *d_tile_blk_lower;  /* tile -> front (= handle block) */
+    const int32_t *d_tile_blk_upper;
+    int64_t n_tiles_lower, n_tiles_upper;
+    double *d_ws;                 /* fronts                                       */
+    double *d_wb;                 /* C^-1 blocks                                  */
+    double *d_inv;                /* pivot-tile inverses                          */
+    int64_t ws_size, wb_size;     /* doubles                                      */
+    int32_t *d_ctl;               /* [1] first failing front + 1 (0 = ok)         */
+} tsb_refactor_desc;
+
+typedef struct tsb_refactor *tsb_refactor_t;
+
+int tsb_refactor_create(const tsb_refactor_desc *desc, tsb_refactor_t *out);
+int tsb_refactor_destroy(tsb_refactor_t h);
+/* Factor the values of A (original CSR order) into d_g / d_gt / d_d of the
+ * handle layout the program was planned for.  A non-positive pivot is
+ * reported in d_ctl[0] (IndefiniteMatrixError), read by the caller. */
+int tsb_refactor_run(tsb_refactor_t h, const double *d_values, double *d_g, double *d_gt, double *d_d,
+                     void *stream);
 
 /* ------------------------------------------------------------------------
  * Vector kernels of the sharded PCG (shard.py): weights w = 1 on owned rows

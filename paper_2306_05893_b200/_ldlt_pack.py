@@ -105,10 +105,12 @@ def row_ranges(m: int, na: int, upper: bool):
     return np.zeros(m + na, dtype=np.int64), np.minimum(r + 1, m)
 
 
-def tile_block(G: np.ndarray, m: int, na: int, upper: bool):
+def tile_block(G, m: int, na: int, upper: bool):
     """Tiles of one block for one sweep -> (list of (tl, np, row0, nrows), data parts).
 
-    G holds the sweep's rows: gfull() for the lower sweep, its transpose for the upper."""
+    G holds the sweep's rows: gfull() for the lower sweep, its transpose for
+    the upper; None gives zero tiles (structure only, filled on the device by
+    tsb_refactor_run)."""
     lo, hi = row_ranges(m, na, upper)
     nrows_all = len(lo)
     tiles, parts = [], []
@@ -119,7 +121,7 @@ def tile_block(G: np.ndarray, m: int, na: int, upper: bool):
         npair = max((th - tl + 1) // 2, 0)
         d = np.zeros((TILE, 2 * npair))
         w = th - tl
-        if w > 0:
+        if w > 0 and G is not None:
             d[: r1 - r0, :w] = G[r0:r1, tl:th]
         parts.append(d.reshape(TILE, npair, 2).transpose(1, 0, 2).ravel())
         tiles.append((tl, npair, r0, r1 - r0))
@@ -398,20 +400,24 @@ def pack(factors, subset=None):
     data = {False: [], True: []}
     pos = {False: 0, True: 0}
     blk_tiles = {False: [], True: []}     # per sweep, per block: (first tile id, [tiles])
+    tile_blk = {False: [], True: []}      # per sweep: tile -> block
     from threadpoolctl import threadpool_limits
 
+    values = all(getattr(bf, "l11", None) is not None for bf in bfs)  # else structure only (zero tiles)
     big = ms_ * (ms_ + na_) > 1_000_000
     mats = {}
-    with threadpool_limits(limits=1, user_api="blas"):  # small blocks: thread wake-ups cost more than the math
-        for i in np.flatnonzero(~big):
+    if values:
+        with threadpool_limits(limits=1, user_api="blas"):  # small blocks: thread wake-ups cost more than the math
+            for i in np.flatnonzero(~big):
+                mats[i] = block_matrix(bfs[i])
+        for i in np.flatnonzero(big):
             mats[i] = block_matrix(bfs[i])
-    for i in np.flatnonzero(big):
-        mats[i] = block_matrix(bfs[i])
     for i, bf in enumerate(bfs):
-        G = gfull(*mats.pop(i))
+        G = gfull(*mats.pop(i)) if values else None
         for up in (False, True):
-            tiles, parts = tile_block(G.T if up else G, int(ms_[i]), int(na_[i]), up)
+            tiles, parts = tile_block(G.T if (up and G is not None) else G, int(ms_[i]), int(na_[i]), up)
             blk_tiles[up].append((len(tl_rows[up]), tiles))
+            tile_blk[up].extend([i] * len(tiles))
             for (tl, npair, r0, nr), p in zip(tiles, parts):
                 tl_rows[up].append((pos[up], tl, npair, r0, nr))
                 data[up].append(p)
@@ -531,11 +537,12 @@ def pack(factors, subset=None):
         "n": n, "nb": nb, "blocks": blocks, "items_l": items_l, "items_u": items_u,
         "tiles_l": tables[False], "tiles_u": tables[True], "g": cat(data[False]), "gt": cat(data[True]),
         "anc": anc_all, "cslot": cslot, "cin_ptr": cin_ptr, "ncbuf": len(anc_all),
-        "d": np.asarray(factors.d, dtype=np.float64), "perm": np.asarray(plan.perm, dtype=np.int64),
+        "d": np.asarray(factors.d if factors.d is not None else np.zeros(n), dtype=np.float64), "perm": np.asarray(plan.perm, dtype=np.int64),
         "max_m": int(ms_.max()) if nb else 1, "max_v": int(max_w), "max_cb": max_cb,
         "parent": parent, "children": children, "mode": mode,
         "npart_l": npart[False], "npart_u": npart[True], "ext_rows": ext_rows,
         "bytes_g": int(pos[False]) * 8, "bytes_gt": int(pos[True]) * 8,
+        "tile_blk_l": np.asarray(tile_blk[False], dtype=np.int32), "tile_blk_u": np.asarray(tile_blk[True], dtype=np.int32),
     }
 
 
@@ -558,6 +565,7 @@ class DevicePanels:
         n, nb = H["n"], H["nb"]
         items_l, items_u = H["items_l"], H["items_u"]
         self.host = H if trace else None
+        self.tile_blk = (H["tile_blk_l"], H["tile_blk_u"])  # tile -> block (device refactorisation)
         if trace:  # per-item timeline (globaltimer ns): take, ready, end, smid, staged, computed
             self.trace_l = t.zeros((len(items_l), 8), dtype=t.int64, device="cuda")
             self.trace_u = t.zeros((len(items_u), 8), dtype=t.int64, device="cuda")

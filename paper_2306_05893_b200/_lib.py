@@ -70,6 +70,16 @@ class LdltDesc(C.Structure):
     ]
 
 
+class RefactorDesc(C.Structure):
+    _fields_ = [
+        ("n_fronts", c_i64), ("n_prog", c_i64), ("h_prog", c_vp), ("d_fronts", c_vp), ("d_lists", c_vp),
+        ("d_sc_src", c_vp), ("d_sc_dst", c_vp), ("d_pairs", c_vp), ("d_tp", c_vp),
+        ("d_tiles_lower", c_vp), ("d_tiles_upper", c_vp), ("d_tile_blk_lower", c_vp), ("d_tile_blk_upper", c_vp),
+        ("n_tiles_lower", c_i64), ("n_tiles_upper", c_i64),
+        ("d_ws", c_vp), ("d_wb", c_vp), ("d_inv", c_vp), ("ws_size", c_i64), ("wb_size", c_i64), ("d_ctl", c_vp),
+    ]
+
+
 class Report(C.Structure):
     _fields_ = [
         ("iterations", c_i64), ("final_residual", C.c_double), ("converged", c_i32),
@@ -109,10 +119,14 @@ _SIGNATURES = {
                                 c_vp, C.c_double, c_i64, C.POINTER(Report), c_vp]),
     "tsb_pcg_report": (C.c_int, [c_vp, C.POINTER(Report), c_vp]),
     "tsb_pcg_phase_times": (C.c_int, [c_vp, c_vp, c_vp]),
+    "tsb_refactor_create": (C.c_int, [C.POINTER(RefactorDesc), C.POINTER(c_vp)]),
+    "tsb_refactor_destroy": (C.c_int, [c_vp]),
+    "tsb_refactor_run": (C.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "tsb_nested_dissection": (C.c_int, [c_i64, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp,
                                         c_vp, c_vp, c_vp]),
 }
 
+ABI_VERSION = 3
 _lib = None
 _lock = threading.Lock()
 
@@ -139,9 +153,9 @@ def load() -> C.CDLL:
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
-        if lib.tsb_abi_version() != 2:
+        if lib.tsb_abi_version() != ABI_VERSION:
             raise NativeLibraryError("libtsb ABI version mismatch")
-        for k, st in enumerate((AsmPlan, AsmCoeffs, None, LdltDesc, Report)):
+        for k, st in enumerate((AsmPlan, AsmCoeffs, None, LdltDesc, Report, None, None, None, RefactorDesc)):
             if st is not None and lib.tsb_struct_size(k) != C.sizeof(st):
                 raise NativeLibraryError(f"libtsb struct layout mismatch: {st.__name__}")
         _lib = lib

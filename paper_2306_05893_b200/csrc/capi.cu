@@ -36,6 +36,9 @@ extern "C" int64_t tsb_struct_size(int32_t which) {
         case 3: return sizeof(tsb_ldlt_desc);
         case 4: return sizeof(tsb_report);
         case 5: return sizeof(tsb_ldlt_tile);
+        case 6: return sizeof(tsb_front);
+        case 7: return sizeof(tsb_front_pair);
+        case 8: return sizeof(tsb_refactor_desc);
         default: return -1;
     }
 }

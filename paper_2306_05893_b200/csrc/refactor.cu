@@ -1,0 +1,473 @@
+// Device LDL^T refactorisation (numeric phase of ldlt_factor, ndprecond.py:501-572,
+// plus the pack of the factor into the sweep layout of ldlt_sweep.cuh).
+//
+// Multifrontal over the dissection tree, one height of the tree at a time.
+// Front of block b (m pivots, na coupling rows, nf = m + na), column-major:
+//
+//     F = [ A_bb       .   ]   + extend-add of every child's update matrix U_c
+//         [ A_anc,b    0   ]     (children in start order: fixed summation order)
+//
+// A tiled right-looking partial Cholesky of the m pivots (64 x 64 tiles; the
+// pivot tiles end at m so the coupling part starts on a tile boundary) leaves
+//     C  (m x m lower),   LS = F21 C^-T,   U = F22 - LS LS^T  (to the parent).
+// Then a right triangular solve  [W; M] C = [I; LS]  gives W = C^-1 and
+// M = LS C^-1 = L21 L11^-1, and the pack writes the sweep operator
+// G = [Linv; M] with Linv = diag(C) C^-1 (unit diagonal stored as 1.0) into
+// the tiles of the handle (d_g lower rows, d_gt upper rows) and d = diag(C)^2.
+//
+// Every op is a batch of 64 x 64 x 64 fp64 tile products (one CTA each,
+// 256 threads x 4 x 4 register tile) over all fronts of a height: the work is
+// dense FP64 (DFMA-bound; B200 FP64 DMMA is no faster than DFMA, measured),
+// the launch sequence is a host "program" planned once per pattern
+// (paper_2306_05893_b200/refactor.py).  All sums run in a fixed order: the
+// result is bit-reproducible run to run.
+#include <vector>
+
+#include "tsb_common.cuh"
+
+namespace tsb {
+namespace rf {
+
+constexpr int NB = 64;
+constexpr int LDS = 66;  // smem row stride (doubles): 16 B aligned rows
+constexpr int kThreads = 256;
+constexpr int kGemmSmem = 2 * NB * LDS * (int)sizeof(double);
+constexpr int kDiagLd = 65;
+constexpr int kDiagSmem = (2 * NB * kDiagLd + NB) * (int)sizeof(double);
+
+__device__ __forceinline__ int tile_start(const tsb_front &f, int t) {
+    return t < f.P ? t * NB : f.m + (t - f.P) * NB;
+}
+__device__ __forceinline__ int tile_width(const tsb_front &f, int t) {
+    return t < f.P ? min(NB, f.m - t * NB) : min(NB, f.nf - (f.m + (t - f.P) * NB));
+}
+
+// task -> list entry: last entry whose exclusive prefix (field 1 or 2) <= task
+__device__ __forceinline__ int find_entry(const int4 *L, int n, bool second, int task, int *local) {
+    int lo = 0, hi = n - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        const int v = second ? __ldg(&L[mid].z) : __ldg(&L[mid].y);
+        if (v <= task) lo = mid; else hi = mid - 1;
+    }
+    *local = task - (second ? __ldg(&L[lo].z) : __ldg(&L[lo].y));
+    return lo;
+}
+
+// dst[q][r] = src[q * ld + r]  (element (r, q) of a column-major matrix), zero-padded
+__device__ __forceinline__ void load_n(double *dst, const double *src, int64_t ld, int rows, int cols) {
+    for (int i = threadIdx.x; i < NB * NB; i += kThreads) {
+        const int r = i & (NB - 1), q = i >> 6;
+        dst[q * LDS + r] = (r < rows && q < cols) ? src[(int64_t)q * ld + r] : 0.0;
+    }
+}
+// dst[q][c] = src[c * ld + q]  (element (q, c) of a column-major matrix), zero-padded
+__device__ __forceinline__ void load_t(double *dst, const double *src, int64_t ld, int qs, int cs) {
+    for (int i = threadIdx.x; i < NB * NB; i += kThreads) {
+        const int q = i & (NB - 1), c = i >> 6;
+        dst[q * LDS + c] = (q < qs && c < cs) ? src[(int64_t)c * ld + q] : 0.0;
+    }
+}
+
+// acc[a][b] = sum_q As[q][tx + 16 a] * Bs[q][4 ty + b]
+__device__ __forceinline__ void tile_mma(const double *As, const double *Bs, int K, double acc[4][4]) {
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+#pragma unroll 4
+    for (int q = 0; q < K; ++q) {
+        const double *ar = As + q * LDS + tx;
+        const double2 b0 = *reinterpret_cast<const double2 *>(Bs + q * LDS + 4 * ty);
+        const double2 b1 = *reinterpret_cast<const double2 *>(Bs + q * LDS + 4 * ty + 2);
+        const double bv[4] = {b0.x, b0.y, b1.x, b1.y};
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+            const double av = ar[16 * a];
+#pragma unroll
+            for (int b = 0; b < 4; ++b) acc[a][b] = fma(av, bv[b], acc[a][b]);
+        }
+    }
+}
+
+// MODE 0: dst = acc; 1: dst -= acc; 2: dst -= acc on the lower triangle (r >= c)
+template <int MODE>
+__device__ __forceinline__ void store_tile(double *dst, int64_t ld, int rows, int cols, const double acc[4][4]) {
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+        const int c = 4 * ty + b;
+        if (c >= cols) continue;
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+            const int r = tx + 16 * a;
+            if (r >= rows || (MODE == 2 && r < c)) continue;
+            double *p = dst + (int64_t)c * ld + r;
+            if (MODE == 0) *p = acc[a][b];
+            else *p -= acc[a][b];
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) scatter_kernel(int64_t n, const int32_t *__restrict__ src,
+                                                      const int64_t *__restrict__ dst,
+                                                      const double *__restrict__ vals, double *__restrict__ ws) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        ws[__ldg(dst + i)] = __ldg(vals + __ldg(src + i));
+}
+
+// U_child (lower) += into the parent front at tp positions; one warp per child column.
+__global__ void __launch_bounds__(256) extend_kernel(const tsb_front_pair *__restrict__ pairs,
+                                                     const tsb_front *__restrict__ F,
+                                                     const int32_t *__restrict__ tp_all, double *__restrict__ ws) {
+    const tsb_front_pair pr = pairs[blockIdx.y];
+    const tsb_front c = F[pr.child], p = F[pr.parent];
+    const int32_t *tp = tp_all + pr.tp_off;
+    const double *u = ws + c.off + (int64_t)c.m * c.nf + c.m;
+    double *fp = ws + p.off;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int j = blockIdx.x * 8 + warp; j < c.na; j += gridDim.x * 8) {
+        const int64_t pcol = (int64_t)__ldg(tp + j) * p.nf;
+        const double *uc = u + (int64_t)j * c.nf;
+        for (int i = j + lane; i < c.na; i += 32) fp[pcol + __ldg(tp + i)] += uc[i];
+    }
+}
+
+// Cholesky of pivot tile k (in smem) + its inverse W_kk (to the inverse scratch).
+__global__ void __launch_bounds__(256) diag_kernel(const tsb_front *__restrict__ F, const int4 *__restrict__ list,
+                                                   int k, double *__restrict__ ws, double *__restrict__ inv,
+                                                   int32_t *__restrict__ ctl) {
+    extern __shared__ __align__(16) double sm[];
+    double *S = sm, *W = sm + NB * kDiagLd, *dsq = sm + 2 * NB * kDiagLd;
+    const int fi = __ldg(&list[blockIdx.x].x);
+    const tsb_front f = F[fi];
+    const int c0 = k * NB, w = min(NB, f.m - c0);
+    double *base = ws + f.off + (int64_t)c0 * f.nf + c0;
+    const int tid = threadIdx.x;
+    for (int i = tid; i < NB * NB; i += kThreads) {
+        const int r = i & (NB - 1), c = i >> 6;
+        S[r * kDiagLd + c] = (r < w && c < w && r >= c) ? base[(int64_t)c * f.nf + r] : 0.0;
+    }
+    __syncthreads();
+    for (int j = 0; j < w; ++j) {
+        double djj = S[j * kDiagLd + j];
+        if (!(djj > 0.0)) {
+            if (tid == 0) atomicCAS(ctl, 0, fi + 1);
+        }
+        const double sj = sqrt(djj), rs = 1.0 / sj;
+        if (tid == 0) dsq[j] = sj;
+        if (tid > j && tid < w) S[tid * kDiagLd + j] *= rs;
+        __syncthreads();
+        for (int i = tid; i < NB * NB; i += kThreads) {
+            const int r = i & (NB - 1), c = i >> 6;
+            if (c > j && r >= c && r < w) S[r * kDiagLd + c] -= S[r * kDiagLd + j] * S[c * kDiagLd + j];
+        }
+        __syncthreads();
+    }
+    if (tid < w) S[tid * kDiagLd + tid] = dsq[tid];
+    __syncthreads();
+    // W = C^-1 (lower): column c by a group of 4 lanes, forward substitution
+    {
+        const int c = tid >> 2, l4 = tid & 3;
+        for (int i = 0; i < w; ++i) {
+            const bool act = c < w && i >= c;
+            double part = 0.0;
+            if (act)
+                for (int q = c + l4; q < i; q += 4) part += S[i * kDiagLd + q] * W[q * kDiagLd + c];
+            part += __shfl_xor_sync(0xffffffffu, part, 1);
+            part += __shfl_xor_sync(0xffffffffu, part, 2);
+            if (act && l4 == 0) W[i * kDiagLd + c] = ((i == c ? 1.0 : 0.0) - part) / S[i * kDiagLd + i];
+            __syncwarp();
+        }
+    }
+    __syncthreads();
+    double *wo = inv + f.ioff + (int64_t)k * NB * NB;
+    for (int i = tid; i < NB * NB; i += kThreads) {
+        const int r = i & (NB - 1), c = i >> 6;
+        const bool in = r < w && c < w && r >= c;
+        if (in) base[(int64_t)c * f.nf + r] = S[r * kDiagLd + c];
+        wo[c * NB + r] = in ? W[r * kDiagLd + c] : 0.0;  // W(r, c), column-major
+    }
+}
+
+// L_ik = F_ik W_kk^T for the row tiles below pivot tile k.
+__global__ void __launch_bounds__(256) panel_kernel(const tsb_front *__restrict__ F, const int4 *__restrict__ list,
+                                                    int nlist, int k, double *__restrict__ ws,
+                                                    const double *__restrict__ inv) {
+    extern __shared__ __align__(16) double sm[];
+    double *As = sm, *Bs = sm + NB * LDS;
+    int local;
+    const int e = find_entry(list, nlist, false, blockIdx.x, &local);
+    const tsb_front f = F[__ldg(&list[e].x)];
+    const int i = k + 1 + local;
+    const int r0 = tile_start(f, i), h = tile_width(f, i);
+    const int c0 = k * NB, w = min(NB, f.m - c0);
+    double *src = ws + f.off + (int64_t)c0 * f.nf + r0;
+    load_n(As, src, f.nf, h, w);
+    load_n(Bs, inv + f.ioff + (int64_t)k * NB * NB, NB, w, w);  // Bs[q][c] = W(c, q)
+    __syncthreads();
+    double acc[4][4];
+    tile_mma(As, Bs, w, acc);
+    store_tile<0>(src, f.nf, h, w, acc);
+}
+
+// F_ij -= L_ik L_jk^T for k < j <= i (lower tiles of the trailing matrix, U included).
+__global__ void __launch_bounds__(256) update_kernel(const tsb_front *__restrict__ F, const int4 *__restrict__ list,
+                                                     int nlist, int k, double *__restrict__ ws) {
+    extern __shared__ __align__(16) double sm[];
+    double *As = sm, *Bs = sm + NB * LDS;
+    int local;
+    const int e = find_entry(list, nlist, true, blockIdx.x, &local);
+    const tsb_front f = F[__ldg(&list[e].x)];
+    int rr = (int)((sqrt(8.0 * local + 1.0) - 1.0) * 0.5);
+    while ((rr + 1) * (rr + 2) / 2 <= local) ++rr;
+    while (rr * (rr + 1) / 2 > local) --rr;
+    const int ss = local - rr * (rr + 1) / 2;
+    const int i = k + 1 + rr, j = k + 1 + ss;
+    const int ri = tile_start(f, i), hi = tile_width(f, i);
+    const int rj = tile_start(f, j), hj = tile_width(f, j);
+    const int c0 = k * NB, w = min(NB, f.m - c0);
+    const double *col = ws + f.off + (int64_t)c0 * f.nf;
+    load_n(As, col + ri, f.nf, hi, w);
+    load_n(Bs, col + rj, f.nf, hj, w);
+    __syncthreads();
+    double acc[4][4];
+    tile_mma(As, Bs, w, acc);
+    double *dst = ws + f.off + (int64_t)rj * f.nf + ri;
+    if (i == j) store_tile<2>(dst, f.nf, hi, hj, acc);
+    else store_tile<1>(dst, f.nf, hi, hj, acc);
+}
+
+// Row tile idx of the right solve's B = [W-buffer (m rows); LS (na rows)].
+__device__ __forceinline__ double *rhs_tile(const tsb_front &f, double *ws, double *wb, int k, int idx, int64_t *ld,
+                                            int *rows) {
+    if (idx < f.P - k) {
+        const int i = k + idx;
+        *ld = f.m;
+        *rows = min(NB, f.m - i * NB);
+        return wb + f.woff + i * NB;
+    }
+    const int b = idx - (f.P - k);
+    *ld = f.nf;
+    *rows = min(NB, f.na - b * NB);
+    return ws + f.off + f.m + b * NB;
+}
+
+// X_:,k = B_:,k W_kk (right solve, column tile k, descending k)
+__global__ void __launch_bounds__(256) tscale_kernel(const tsb_front *__restrict__ F, const int4 *__restrict__ list,
+                                                     int nlist, int k, double *__restrict__ ws, double *__restrict__ wb,
+                                                     const double *__restrict__ inv) {
+    extern __shared__ __align__(16) double sm[];
+    double *As = sm, *Bs = sm + NB * LDS;
+    int local;
+    const int e = find_entry(list, nlist, false, blockIdx.x, &local);
+    const tsb_front f = F[__ldg(&list[e].x)];
+    int64_t ld;
+    int rows;
+    double *b = rhs_tile(f, ws, wb, k, local, &ld, &rows);
+    const int w = min(NB, f.m - k * NB);
+    double *src = b + (int64_t)k * NB * ld;
+    load_n(As, src, ld, rows, w);
+    load_t(Bs, inv + f.ioff + (int64_t)k * NB * NB, NB, w, w);  // Bs[q][c] = W(q, c)
+    __syncthreads();
+    double acc[4][4];
+    tile_mma(As, Bs, w, acc);
+    store_tile<0>(src, ld, rows, w, acc);
+}
+
+// B_:,j -= X_:,k C_kj for j < k
+__global__ void __launch_bounds__(256) tupdate_kernel(const tsb_front *__restrict__ F, const int4 *__restrict__ list,
+                                                      int nlist, int k, double *__restrict__ ws, double *__restrict__ wb) {
+    extern __shared__ __align__(16) double sm[];
+    double *As = sm, *Bs = sm + NB * LDS;
+    int local;
+    const int e = find_entry(list, nlist, true, blockIdx.x, &local);
+    const tsb_front f = F[__ldg(&list[e].x)];
+    const int idx = local / k, j = local % k;
+    int64_t ld;
+    int rows;
+    double *b = rhs_tile(f, ws, wb, k, idx, &ld, &rows);
+    const int w = min(NB, f.m - k * NB);
+    load_n(As, b + (int64_t)k * NB * ld, ld, rows, w);
+    load_t(Bs, ws + f.off + (int64_t)j * NB * f.nf + k * NB, f.nf, w, NB);  // Bs[q][c] = C(kNB + q, jNB + c)
+    __syncthreads();
+    double acc[4][4];
+    tile_mma(As, Bs, w, acc);
+    store_tile<1>(b + (int64_t)j * NB * ld, ld, rows, NB, acc);
+}
+
+__global__ void ident_kernel(const tsb_front *__restrict__ F, double *__restrict__ wb) {
+    const tsb_front f = F[blockIdx.x];
+    for (int r = threadIdx.x; r < f.m; r += blockDim.x) wb[f.woff + (int64_t)r * f.m + r] = 1.0;
+}
+
+// G(r, c), c < m: r < m -> Linv(r, c) = C_rr W(r, c) (1 on the diagonal); r >= m -> M(r - m, c)
+__device__ __forceinline__ double gval(const tsb_front &f, const double *ws, const double *wb, int r, int c) {
+    if (r < f.m) {
+        if (r == c) return 1.0;
+        if (r < c) return 0.0;
+        return ws[f.off + (int64_t)r * f.nf + r] * wb[f.woff + (int64_t)c * f.m + r];
+    }
+    return ws[f.off + (int64_t)c * f.nf + r];
+}
+
+// Tile image of the sweep operator (layout of _ldlt_pack.tile_block).
+template <bool UPPER>
+__global__ void __launch_bounds__(256) pack_kernel(const tsb_ldlt_tile *__restrict__ T, const int32_t *__restrict__ tblk,
+                                                   const tsb_front *__restrict__ F, const double *__restrict__ ws,
+                                                   const double *__restrict__ wb, double *__restrict__ out) {
+    const tsb_ldlt_tile t = T[blockIdx.x];
+    const tsb_front f = F[__ldg(tblk + blockIdx.x)];
+    const int64_t n = (int64_t)t.np * 64;
+    for (int64_t idx = threadIdx.x; idx < n; idx += blockDim.x) {
+        const int p = (int)(idx >> 6), rem = (int)(idx & 63), kk = rem >> 1, h = rem & 1;
+        const int row = t.row0 + kk, col = t.tl + 2 * p + h;
+        double v = 0.0;
+        if (kk < t.nrows) {
+            if (!UPPER) {
+                if (col < min(row + 1, f.m)) v = gval(f, ws, wb, row, col);
+            } else if (col >= row && col < f.nf) {
+                v = gval(f, ws, wb, col, row);
+            }
+        }
+        out[t.off + idx] = v;
+    }
+}
+
+__global__ void d_kernel(const tsb_front *__restrict__ F, const double *__restrict__ ws, double *__restrict__ d) {
+    const tsb_front f = F[blockIdx.x];
+    for (int r = threadIdx.x; r < f.m; r += blockDim.x) {
+        const double c = ws[f.off + (int64_t)r * f.nf + r];
+        d[f.start + r] = c * c;
+    }
+}
+
+}  // namespace rf
+}  // namespace tsb
+
+struct tsb_refactor {
+    tsb_refactor_desc d;
+    std::vector<int64_t> prog;
+};
+
+extern "C" int tsb_refactor_create(const tsb_refactor_desc *desc, tsb_refactor_t *out) {
+    using namespace tsb;
+    return guard([&] {
+        if (desc == nullptr || out == nullptr) throw Error(TSB_E_ARG, "null refactor desc");
+        if (desc->n_prog < 0 || (desc->n_prog > 0 && desc->h_prog == nullptr)) throw Error(TSB_E_ARG, "bad program");
+        static bool once = [] {
+            allow_max_smem(rf::diag_kernel);
+            allow_max_smem(rf::panel_kernel);
+            allow_max_smem(rf::update_kernel);
+            allow_max_smem(rf::tscale_kernel);
+            allow_max_smem(rf::tupdate_kernel);
+            return true;
+        }();
+        (void)once;
+        auto *h = new tsb_refactor;
+        h->d = *desc;
+        h->prog.assign(desc->h_prog, desc->h_prog + 8 * desc->n_prog);
+        h->d.h_prog = nullptr;
+        *out = h;
+    });
+}
+
+extern "C" int tsb_refactor_destroy(tsb_refactor_t h) {
+    delete h;
+    return TSB_OK;
+}
+
+extern "C" int tsb_refactor_run(tsb_refactor_t h, const double *d_values, double *d_g, double *d_gt, double *d_d,
+                                void *stream) {
+    using namespace tsb;
+    using namespace tsb::rf;
+    return guard([&] {
+        if (h == nullptr) throw Error(TSB_E_ARG, "null refactor handle");
+        cudaStream_t s = as_stream(stream);
+        const tsb_refactor_desc &D = h->d;
+        const int4 *lists = reinterpret_cast<const int4 *>(D.d_lists);
+        TSB_CUDA(cudaMemsetAsync(D.d_ctl, 0, sizeof(int32_t), s));
+        for (int64_t o = 0; o < (int64_t)h->prog.size() / 8; ++o) {
+            const int64_t *op = h->prog.data() + 8 * o;
+            const int64_t a = op[1], b = op[2], c = op[3], dd = op[4];
+            switch (op[0]) {
+                case TSB_RF_SCATTER: {
+                    TSB_CUDA(cudaMemsetAsync(D.d_ws, 0, sizeof(double) * D.ws_size, s));
+                    if (a > 0) {
+                        const int g = (int)std::min<int64_t>((a + 255) / 256, kNumSM * 16);
+                        scatter_kernel<<<g, 256, 0, s>>>(a, D.d_sc_src, D.d_sc_dst, d_values, D.d_ws);
+                        TSB_LAUNCHED();
+                    }
+                    break;
+                }
+                case TSB_RF_IDENT:
+                    TSB_CUDA(cudaMemsetAsync(D.d_wb, 0, sizeof(double) * D.wb_size, s));
+                    if (D.n_fronts > 0) {
+                        ident_kernel<<<(unsigned)D.n_fronts, 256, 0, s>>>(D.d_fronts, D.d_wb);
+                        TSB_LAUNCHED();
+                    }
+                    break;
+                case TSB_RF_EXTEND: {
+                    if (b > a && c > 0) {
+                        dim3 g((unsigned)std::min<int64_t>((c + 7) / 8, 1024), (unsigned)(b - a));
+                        extend_kernel<<<g, 256, 0, s>>>(D.d_pairs + a, D.d_fronts, D.d_tp, D.d_ws);
+                        TSB_LAUNCHED();
+                    }
+                    break;
+                }
+                case TSB_RF_DIAG:
+                    diag_kernel<<<(unsigned)c, 256, kDiagSmem, s>>>(D.d_fronts, lists + b, (int)a, D.d_ws, D.d_inv,
+                                                                    D.d_ctl);
+                    TSB_LAUNCHED();
+                    break;
+                case TSB_RF_PANEL:
+                    if (dd > 0) {
+                        panel_kernel<<<(unsigned)dd, 256, kGemmSmem, s>>>(D.d_fronts, lists + b, (int)c, (int)a,
+                                                                          D.d_ws, D.d_inv);
+                        TSB_LAUNCHED();
+                    }
+                    break;
+                case TSB_RF_UPDATE:
+                    if (dd > 0) {
+                        update_kernel<<<(unsigned)dd, 256, kGemmSmem, s>>>(D.d_fronts, lists + b, (int)c, (int)a,
+                                                                           D.d_ws);
+                        TSB_LAUNCHED();
+                    }
+                    break;
+                case TSB_RF_TSCALE:
+                    if (dd > 0) {
+                        tscale_kernel<<<(unsigned)dd, 256, kGemmSmem, s>>>(D.d_fronts, lists + b, (int)c, (int)a,
+                                                                           D.d_ws, D.d_wb, D.d_inv);
+                        TSB_LAUNCHED();
+                    }
+                    break;
+                case TSB_RF_TUPDATE:
+                    if (dd > 0) {
+                        tupdate_kernel<<<(unsigned)dd, 256, kGemmSmem, s>>>(D.d_fronts, lists + b, (int)c, (int)a,
+                                                                            D.d_ws, D.d_wb);
+                        TSB_LAUNCHED();
+                    }
+                    break;
+                case TSB_RF_PACK:
+                    if (D.n_tiles_lower > 0) {
+                        pack_kernel<false><<<(unsigned)D.n_tiles_lower, 256, 0, s>>>(
+                            D.d_tiles_lower, D.d_tile_blk_lower, D.d_fronts, D.d_ws, D.d_wb, d_g);
+                        TSB_LAUNCHED();
+                    }
+                    if (D.n_tiles_upper > 0) {
+                        pack_kernel<true><<<(unsigned)D.n_tiles_upper, 256, 0, s>>>(
+                            D.d_tiles_upper, D.d_tile_blk_upper, D.d_fronts, D.d_ws, D.d_wb, d_gt);
+                        TSB_LAUNCHED();
+                    }
+                    if (D.n_fronts > 0) {
+                        d_kernel<<<(unsigned)D.n_fronts, 256, 0, s>>>(D.d_fronts, D.d_ws, d_d);
+                        TSB_LAUNCHED();
+                    }
+                    break;
+                default:
+                    throw Error(TSB_E_ARG, "unknown refactor op");
+            }
+        }
+    });
+}

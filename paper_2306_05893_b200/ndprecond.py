@@ -39,6 +39,8 @@ __all__ = [
     "graph_from_pattern",
     "count_coupling_violations",
     "ldlt_factor",
+    "ldlt_factor_device",
+    "DeviceLdlFactors",
     "solve_lower",
     "solve_upper",
     "apply",
@@ -302,6 +304,52 @@ class LdlFactors:
         return apply(self, r, workers=workers)
 
 
+@dataclass
+class DeviceLdlFactors(LdlFactors):
+    """LdlFactors computed on the device (refactor.DeviceRefactor): the values
+    exist only in the sweep image (`device()`); `to_host()` downloads them as
+    a plain LdlFactors (L11 = inv(Linv), L21 = M L11) for host-side use."""
+
+    _host: LdlFactors | None = field(repr=False, default=None)
+
+    def to_host(self) -> LdlFactors:
+        if self._host is None:
+            from scipy.linalg import lapack
+
+            from ._ldlt_pack import TILE_DTYPE, untile
+
+            img = self._device
+            tiles = img.t["tiles_l"].cpu().numpy().view(TILE_DTYPE)
+            g = img.t["g"].cpu().numpy()
+            tblk = img.tile_blk[0]
+            blocks = []
+            for i, bf in enumerate(self.blocks):
+                m, na = bf.stop - bf.start, len(bf.anc)
+                sel = np.flatnonzero(tblk == i)
+                tl = [(int(x["off"]), int(x["tl"]), int(x["np"]), int(x["row0"]), int(x["nrows"])) for x in tiles[sel]]
+                G = untile(tl, g, m + na, m)
+                l11, info = lapack.dtrtri(np.ascontiguousarray(G[:m]), lower=1, unitdiag=1)
+                if info != 0:
+                    raise PrecondError(f"singular device factor block at {bf.start}")
+                l11 = np.tril(l11, -1) + np.eye(m)
+                l21 = G[m:] @ l11 if na else np.empty((0, m))
+                blocks.append(_BlockFactor(bf.start, bf.stop, bf.level, bf.anc, l11, l21, bf.tile,
+                                           _tile_inverses(l11, bf.tile)))
+            d = img.t["d"].cpu().numpy().copy()
+            nlev = len(self.levels)
+            levels = [[b for b in blocks if b.level == lv] for lv in range(nlev)]
+            self._host = LdlFactors(d, self.plan, self.source_step, blocks, levels, self.symbolic)
+        return self._host
+
+    @property
+    def l_matrix(self) -> CsrMatrix:
+        return self.to_host().l_matrix
+
+    @property
+    def fill_in(self) -> int:
+        return self.to_host().fill_in
+
+
 def ldlt_factor(a: CsrMatrix, plan: DissectionPlan, tile: int = 16, symbolic: LdlSymbolic | None = None,
                 source_step: int = 0) -> LdlFactors:
     """Sparse LDL^T of an SPD matrix, front by front in start order (host BLAS).
@@ -447,6 +495,14 @@ def solve_upper(factors: LdlFactors, w, workers: int = 1):
 def apply(factors: LdlFactors, r, workers: int = 1):
     """z = (L D L^T)^-1 r in original order (ndprecond.py:694-700)."""
     return _run(factors, "apply", r)
+
+
+def ldlt_factor_device(a: CsrMatrix, plan: DissectionPlan, tile: int = 16, symbolic: LdlSymbolic | None = None,
+                       source_step: int = 0) -> DeviceLdlFactors:
+    """ldlt_factor computed on the B200 (refactor.py / csrc/refactor.cu)."""
+    from .refactor import ldlt_factor_device as _f
+
+    return _f(a, plan, tile, symbolic, source_step)
 
 
 # ---------------------------------------------------------------------------

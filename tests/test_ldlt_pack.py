@@ -126,7 +126,9 @@ def _factors(dims, leaf):
                             np.zeros_like(mesh.nodes), np.zeros(mesh.ndof), 0.01, (0.0, -9.81, 0.0))
     a = CsrMatrix(mesh.ndof, mesh.ndof, out["row_ptr"], out["col_ind"], out["values"])
     plan = ND.expand_plan(ND.nested_dissection(M.vertex_adjacency(mesh), leaf))
-    return mesh, ND.ldlt_factor(a, plan)
+    f = ND.ldlt_factor(a, plan)
+    f._a = a
+    return mesh, f
 
 
 @pytest.mark.parametrize("dims,leaf", [((3, 3, 8), 16), ((4, 4, 12), 16), ((6, 6, 28), 64)])

@@ -21,7 +21,7 @@ def test_library_loads_and_exports_all_symbols():
     lib = _lib.load()
     for name in declared_symbols():
         assert hasattr(lib, name), name
-    assert lib.tsb_abi_version() == 2
+    assert lib.tsb_abi_version() == 3
 
 
 def test_error_message_roundtrip():
