@@ -184,6 +184,72 @@ def time_spmv(W, reps, flush):
     return dict(ms=ms, bytes=byts, gbs=byts / (ms * 1e-3) / 1e9, nnz=a.nnz)
 
 
+FP64_PEAK_TFLOPS = 36.0  # DFMA, measured on this B200 (tools/ubench_fp64.cu); not in MEASURED_PEAKS.json
+
+
+def time_refactor(W, reps=3):
+    """Device LDL^T refactorisation (csrc/refactor.cu) of the current step's matrix."""
+    import torch
+    from paper_2306_05893_b200 import refactor as R
+
+    a, _, _ = W["integ"].assemble_system(W["state"])
+    t0 = time.perf_counter()
+    rf = R.DeviceRefactor(a, W["plan"], TILE)
+    t_plan = time.perf_counter() - t0
+    img = rf.images[0]
+    ts = []
+    for i in range(1 + reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        rf.enqueue(a, img)
+        e1.record()
+        e1.synchronize()
+        if i:
+            ts.append(e0.elapsed_time(e1))
+    if rf.failed_block() >= 0:
+        raise RuntimeError("device refactorisation hit a non-positive pivot")
+    ms = statistics.median(ts)
+    tf = rf.rplan.flops / (ms * 1e-3) / 1e12
+    out = dict(ms=ms, gflop=rf.rplan.flops / 1e9, tflops=tf, peak_tflops=FP64_PEAK_TFLOPS,
+               frac=tf / FP64_PEAK_TFLOPS, bound="fp64", plan_s=t_plan, workspace_gb=rf.workspace_bytes / 1e9)
+    W["refactor"] = rf
+    return out
+
+
+def time_async_device(W, steps, flush):
+    """Steady state of AsyncPreconditioner(device=True) on a running simulation
+    (a copy of the scenario state, committed every step): each step polls,
+    solves with the newest published factor (Jacobi until the first lands) and
+    submits the step's matrix for refactorisation on a side stream."""
+    import torch
+    from paper_2306_05893_b200 import krylov, ndprecond as ND
+
+    pre = ND.AsyncPreconditioner(W["plan"], tile=TILE, device=True)
+    cfg = W["cfg"]
+    integ = W["integ"]
+    st = W["state"].copy()  # the run advances its own copy of the scenario state
+    stale, iters, per = [], [], []
+    k0 = 1000
+    for k in range(steps + 5):
+        pre.poll()
+        ready = pre.status is ND.PrecondStatus.READY
+        solve = (lambda a, b: krylov.pcg(a, b, pre, cfg)) if ready else W["solvers"]["jacobi"]
+        flush()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        res = integ.step(st, solve)
+        pre.update(res.matrix, k0 + k)
+        e1.record()
+        e1.synchronize()
+        if k >= 5:
+            per.append(e0.elapsed_time(e1))
+            iters.append(res.report.iterations)
+            stale.append(pre.staleness(k0 + k) if ready else -1)
+    pre.close()
+    return dict(ms_per_step=statistics.median(per), iterations=statistics.median(iters),
+                staleness_median=statistics.median(stale), steps=len(per))
+
+
 def time_e2e(W, mode, steps):
     """Same step through the reference-facing API with HOST (NumPy) state:
     H2D of x, v, f_ext and D2H of the step's results inside the timed region."""
@@ -401,6 +467,8 @@ def main():
     apply_r = time_apply(W, 20, flush)
     spmv_r = time_spmv(W, 20, flush)
     e2e_r = time_e2e(W, args.precond, max(5, min(args.steps, 30)))
+    refac_r = time_refactor(W)
+    async_r = time_async_device(W, max(10, min(args.steps, 30)), flush)
     ms = total_ms / args.steps
     if rank != 0:
         if dist:
@@ -440,6 +508,9 @@ def main():
         "gpu_launches": main_r["launches"],
         "clocks": clk.summary(),
         "setup_s": {"nested_dissection": W["t_nd"], "host_factor": W["t_factor"]},
+        "refactor": dict(refac_r, host_factor_s=W["t_factor"],
+                         kernel="device LDL^T refactorisation (multifrontal 64x64 tiles, csrc/refactor.cu)"),
+        "ldlt_async_device": async_r,
     }
     if cpu is not None:
         line["cpu_baseline"] = {"value": cpu["ms"], "unit": "ms", "cores": 1, "kind": "port",

@@ -541,13 +541,18 @@ class AsyncPreconditioner:
     """
 
     def __init__(self, plan: DissectionPlan, policy: str = "on-completion",
-                 refactor_every: int = 4, tile: int = 16):
+                 refactor_every: int = 4, tile: int = 16, device: bool = False):
         if policy not in ("on-completion", "every-k"):
             raise PrecondError(f"unknown refactor policy {policy!r}")
         self.plan = plan
         self.policy = policy
         self.refactor_every = refactor_every
         self.tile = tile
+        # device=True: the refactorisation runs on the GPU (refactor.py) on a
+        # side stream into a second sweep image; no host thread, no download
+        self.device = device
+        self._rf = None
+        self._dev_job = None
         self.factors: LdlFactors | None = None
         self.disabled = False
         self._pool: ThreadPoolExecutor | None = None
@@ -560,11 +565,11 @@ class AsyncPreconditioner:
     def status(self) -> PrecondStatus:
         if self.factors is not None:
             return PrecondStatus.READY
-        return PrecondStatus.FACTORIZING if self._future is not None else PrecondStatus.EMPTY
+        return PrecondStatus.FACTORIZING if self.refresh_in_flight else PrecondStatus.EMPTY
 
     @property
     def refresh_in_flight(self) -> bool:
-        return self._future is not None
+        return self._future is not None or self._dev_job is not None
 
     def staleness(self, step: int) -> int:
         return -1 if self.factors is None else step - self.factors.source_step
@@ -574,7 +579,49 @@ class AsyncPreconditioner:
             return True
         return step - self._last_submitted >= self.refactor_every
 
+    def _publish_device(self, wait: bool = False):
+        job = self._dev_job
+        if job is None:
+            return
+        factors, event, flag, _ = job
+        if not wait and not event.query():
+            return
+        event.synchronize()
+        self._dev_job = None
+        if int(flag[0]) != 0:
+            bf = self._rf.rplan.blocks[int(flag[0]) - 1]
+            logger.warning("device factorization failed (non-positive pivot in block [%d, %d)); "
+                           "preconditioner disabled", bf.start, bf.stop)
+            self.disabled = True
+            return
+        _lib.torch().cuda.current_stream().wait_event(event)
+        self.factors = factors
+
+    def _submit_device(self, a: CsrMatrix, step: int):
+        """Refactor `a` on a side stream into the sweep image not in use."""
+        from .refactor import DeviceRefactor, make_factors
+
+        t = _lib.torch()
+        if self._rf is None or self._rf.symbolic.pattern_key != _pattern_key(a):
+            self._rf = DeviceRefactor(a, self.plan, self.tile, buffers=2)
+            self._side = t.cuda.Stream()
+            self._flag = t.zeros(4, dtype=t.int32).pin_memory()
+        rf = self._rf
+        img = rf.images[rf._next]
+        rf._next = (rf._next + 1) % len(rf.images)
+        snapshot = a.copy_values()          # the caller may overwrite a's values next step
+        self._side.wait_stream(t.cuda.current_stream())
+        with t.cuda.stream(self._side):
+            rf.enqueue(snapshot, img)
+            self._flag.copy_(rf.d["ctl"], non_blocking=True)
+            event = t.cuda.Event()
+            event.record(self._side)
+        self._dev_job = (make_factors(rf, img, step), event, self._flag, snapshot)  # snapshot lives until publish
+
     def _publish_if_done(self):
+        if self.device:
+            self._publish_device()
+            return
         if self._future is not None and self._future.done():
             try:
                 factors, event = self._future.result()
@@ -592,7 +639,7 @@ class AsyncPreconditioner:
 
     def update(self, a: CsrMatrix, step: int):
         self._publish_if_done()
-        if self.disabled or self._future is not None:
+        if self.disabled or self.refresh_in_flight:
             return
         key = _pattern_key(a)
         if self._pattern_key is not None and key != self._pattern_key:
@@ -600,6 +647,10 @@ class AsyncPreconditioner:
             self.factors = None
         self._pattern_key = key
         if not self._policy_fires(step):
+            return
+        if self.device:
+            self._last_submitted = step
+            self._submit_device(a, step)
             return
         snapshot = a.copy_values()
         ready = None
@@ -614,8 +665,13 @@ class AsyncPreconditioner:
                                          step, upload, ready)
 
     def wait_ready(self, timeout: float = 60.0):
-        if self._future is None and self.factors is None:
+        if not self.refresh_in_flight and self.factors is None:
             raise LifecycleError("no factorization in flight")
+        if self.device:
+            self._publish_device(wait=True)
+            if self.disabled:
+                raise LifecycleError("factorization failed; preconditioner disabled")
+            return
         if self._future is not None:
             self._future.exception(timeout=timeout)
             self._publish_if_done()

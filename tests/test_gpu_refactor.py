@@ -112,3 +112,34 @@ def test_device_factor_indefinite_raises(params):
     bad = CsrMatrix(a.nrows, a.ncols, a.row_ptr, a.col_ind, vals)
     with pytest.raises(ND.IndefiniteMatrixError):
         ND.ldlt_factor_device(bad, plan)
+
+
+def test_async_preconditioner_device_refactor(params):
+    """AsyncPreconditioner(device=True): refactorisation on a side stream into
+    the idle sweep image, published at step boundaries (ndprecond.py:714-831)."""
+    mesh = clamped_beam(6, 6, 28)
+    integ = BackwardEulerIntegrator(mesh, models.make_model("corotational", mesh, params),
+                                    IntegratorConfig(dt=0.01, gravity=(0.0, -9.81, 0.0)))
+    plan = ND.expand_plan(ND.nested_dissection(M.vertex_adjacency(mesh), 64))
+    pre = ND.AsyncPreconditioner(plan, device=True)
+    assert pre.status is ND.PrecondStatus.EMPTY
+    cfg = krylov.SolverConfig(1e-9, 8000)
+    st = SimState.rest(mesh, device=True)
+    seen = set()
+    for k in range(1, 9):
+        pre.poll()
+        solve = (lambda a, b: krylov.pcg(a, b, pre, cfg)) if pre.status is ND.PrecondStatus.READY else \
+            (lambda a, b: krylov.pcg(a, b, krylov.jacobi_precond(a), cfg))
+        res = integ.step(st, solve)
+        assert res.report.converged
+        if pre.status is ND.PrecondStatus.READY:
+            assert res.report.iterations <= 8      # stale factors (reference acceptance: <= 15)
+            seen.add(id(pre.factors.device()))
+        pre.update(res.matrix, k)
+        if k == 1:
+            assert pre.status is ND.PrecondStatus.FACTORIZING
+            pre.wait_ready()
+            assert pre.staleness(2) == 1
+    assert len(seen) == 2                      # both sweep images were used
+    assert not pre.disabled
+    pre.close()
