@@ -32,8 +32,6 @@ constexpr int NB = 64;
 constexpr int LDS = 66;  // smem row stride (doubles): 16 B aligned rows
 constexpr int kThreads = 256;
 constexpr int kGemmSmem = 2 * NB * LDS * (int)sizeof(double);
-constexpr int kDiagLd = 65;
-constexpr int kDiagSmem = (2 * NB * kDiagLd + NB) * (int)sizeof(double);
 
 __device__ __forceinline__ int tile_start(const tsb_front &f, int t) {
     return t < f.P ? t * NB : f.m + (t - f.P) * NB;
@@ -54,18 +52,32 @@ __device__ __forceinline__ int find_entry(const int4 *L, int n, bool second, int
     return lo;
 }
 
-// dst[q][r] = src[q * ld + r]  (element (r, q) of a column-major matrix), zero-padded
+__device__ __forceinline__ void cp_async8(double *dst, const double *src, bool valid) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(sa), "l"(src), "r"(valid ? 8 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// dst[q][r] = src[q * ld + r]  (element (r, q) of a column-major matrix), zero-padded;
+// asynchronous (cp.async, zero-fill outside): every thread's 16 copies are in
+// flight together.  Complete with cp_async_wait() + __syncthreads().
 __device__ __forceinline__ void load_n(double *dst, const double *src, int64_t ld, int rows, int cols) {
-    for (int i = threadIdx.x; i < NB * NB; i += kThreads) {
+#pragma unroll
+    for (int u = 0; u < NB * NB / kThreads; ++u) {
+        const int i = threadIdx.x + u * kThreads;
         const int r = i & (NB - 1), q = i >> 6;
-        dst[q * LDS + r] = (r < rows && q < cols) ? src[(int64_t)q * ld + r] : 0.0;
+        const bool ok = r < rows && q < cols;
+        cp_async8(dst + q * LDS + r, ok ? src + (int64_t)q * ld + r : src, ok);
     }
 }
 // dst[q][c] = src[c * ld + q]  (element (q, c) of a column-major matrix), zero-padded
 __device__ __forceinline__ void load_t(double *dst, const double *src, int64_t ld, int qs, int cs) {
-    for (int i = threadIdx.x; i < NB * NB; i += kThreads) {
+#pragma unroll
+    for (int u = 0; u < NB * NB / kThreads; ++u) {
+        const int i = threadIdx.x + u * kThreads;
         const int q = i & (NB - 1), c = i >> 6;
-        dst[q * LDS + c] = (q < qs && c < cs) ? src[(int64_t)c * ld + q] : 0.0;
+        const bool ok = q < qs && c < cs;
+        cp_async8(dst + q * LDS + c, ok ? src + (int64_t)c * ld + q : src, ok);
     }
 }
 
@@ -91,23 +103,28 @@ __device__ __forceinline__ void tile_mma(const double *As, const double *Bs, int
     }
 }
 
-// MODE 0: dst = acc; 1: dst -= acc; 2: dst -= acc on the lower triangle (r >= c)
+// MODE 0: dst = acc; 1: dst -= acc; 2: dst -= acc on the lower triangle (r >= c).
+// The read-modify-write issues all 16 loads before the first store.
 template <int MODE>
 __device__ __forceinline__ void store_tile(double *dst, int64_t ld, int rows, int cols, const double acc[4][4]) {
     const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    double old[4][4];
 #pragma unroll
-    for (int b = 0; b < 4; ++b) {
-        const int c = 4 * ty + b;
-        if (c >= cols) continue;
+    for (int b = 0; b < 4; ++b)
 #pragma unroll
         for (int a = 0; a < 4; ++a) {
-            const int r = tx + 16 * a;
-            if (r >= rows || (MODE == 2 && r < c)) continue;
-            double *p = dst + (int64_t)c * ld + r;
-            if (MODE == 0) *p = acc[a][b];
-            else *p -= acc[a][b];
+            const int r = tx + 16 * a, c = 4 * ty + b;
+            const bool ok = r < rows && c < cols && (MODE != 2 || r >= c);
+            old[a][b] = (MODE != 0 && ok) ? __ldcg(dst + (int64_t)c * ld + r) : 0.0;
         }
-    }
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+            const int r = tx + 16 * a, c = 4 * ty + b;
+            if (r >= rows || c >= cols || (MODE == 2 && r < c)) continue;
+            dst[(int64_t)c * ld + r] = MODE == 0 ? acc[a][b] : old[a][b] - acc[a][b];
+        }
 }
 
 __global__ void __launch_bounds__(256) scatter_kernel(int64_t n, const int32_t *__restrict__ src,
@@ -130,64 +147,101 @@ __global__ void __launch_bounds__(256) extend_kernel(const tsb_front_pair *__res
     for (int j = blockIdx.x * 8 + warp; j < c.na; j += gridDim.x * 8) {
         const int64_t pcol = (int64_t)__ldg(tp + j) * p.nf;
         const double *uc = u + (int64_t)j * c.nf;
-        for (int i = j + lane; i < c.na; i += 32) fp[pcol + __ldg(tp + i)] += uc[i];
+        constexpr int U = 4;  // loads of U rows in flight before their read-modify-writes
+        for (int i0 = j + lane; i0 < c.na; i0 += 32 * U) {
+            int64_t dst[U];
+            double val[U], cur[U];
+#pragma unroll
+            for (int q = 0; q < U; ++q) {
+                const int i = i0 + 32 * q;
+                dst[q] = i < c.na ? pcol + __ldg(tp + i) : -1;
+                val[q] = i < c.na ? __ldcg(uc + i) : 0.0;
+            }
+#pragma unroll
+            for (int q = 0; q < U; ++q) cur[q] = dst[q] >= 0 ? __ldcg(fp + dst[q]) : 0.0;
+#pragma unroll
+            for (int q = 0; q < U; ++q)
+                if (dst[q] >= 0) fp[dst[q]] = cur[q] + val[q];
+        }
     }
 }
 
-// Cholesky of pivot tile k (in smem) + its inverse W_kk (to the inverse scratch).
+// Pivot tile k: W_kk = C_kk^-1 and diag(C_kk) by in-place Gauss-Jordan style
+// elimination in shared memory (one CTA of 256 threads per front).  X starts
+// as the full symmetric tile; step j eliminates column j from rows i > j with
+// the unscaled row j (m_i = X_ij / p_j): the trailing A part and the inverse
+// part (columns < j) update uniformly as X_it -= m_i X_jt, and the inverse
+// entry born at (i, j) is -m_i, stored where the eliminated A entry was.  Row
+// j of the inverse is scaled by p_j^-1/2 one step later, so X's lower
+// triangle ends as D^-1/2 L^-1 = C^-1.  Only diag(C) and C^-1 of the pivot
+// tile are consumed downstream (panel, right solve, pack).
+constexpr int kDiagLd = 65;
+constexpr int kDiagSmem = (NB * kDiagLd + 3 * NB) * (int)sizeof(double);
+
 __global__ void __launch_bounds__(256) diag_kernel(const tsb_front *__restrict__ F, const int4 *__restrict__ list,
                                                    int k, double *__restrict__ ws, double *__restrict__ inv,
                                                    int32_t *__restrict__ ctl) {
     extern __shared__ __align__(16) double sm[];
-    double *S = sm, *W = sm + NB * kDiagLd, *dsq = sm + 2 * NB * kDiagLd;
+    double *X = sm, *mv = sm + NB * kDiagLd, *dsq = mv + NB, *rsq = dsq + NB;
     const int fi = __ldg(&list[blockIdx.x].x);
     const tsb_front f = F[fi];
     const int c0 = k * NB, w = min(NB, f.m - c0);
     double *base = ws + f.off + (int64_t)c0 * f.nf + c0;
-    const int tid = threadIdx.x;
-    for (int i = tid; i < NB * NB; i += kThreads) {
-        const int r = i & (NB - 1), c = i >> 6;
-        S[r * kDiagLd + c] = (r < w && c < w && r >= c) ? base[(int64_t)c * f.nf + r] : 0.0;
+    const int tid = threadIdx.x, t = tid & (NB - 1), rg = tid >> 6;
+    {
+        double v[NB * NB / kThreads];  // all 16 loads in flight together
+#pragma unroll
+        for (int u = 0; u < NB * NB / kThreads; ++u) {
+            const int i = tid + u * kThreads, r = i & (NB - 1), c = i >> 6;
+            v[u] = (r < w && c < w) ? base[r >= c ? (int64_t)c * f.nf + r : (int64_t)r * f.nf + c] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < NB * NB / kThreads; ++u) {
+            const int i = tid + u * kThreads, r = i & (NB - 1), c = i >> 6;
+            X[r * kDiagLd + c] = v[u];
+        }
     }
     __syncthreads();
     for (int j = 0; j < w; ++j) {
-        double djj = S[j * kDiagLd + j];
-        if (!(djj > 0.0)) {
-            if (tid == 0) atomicCAS(ctl, 0, fi + 1);
+        // phase 1: multipliers of column j, pivot, scaling of row j-1 of the inverse
+        const double p = X[j * kDiagLd + j];
+        if (tid < NB) {
+            const int i = j + 1 + tid;
+            if (i < w) mv[i] = X[i * kDiagLd + j] * __drcp_rn(p);
+        } else if (tid < 2 * NB) {
+            const int c = tid - NB;
+            if (j > 0 && c < j) X[(j - 1) * kDiagLd + c] *= (c == j - 1) ? 1.0 : rsq[j - 1];
+        } else if (tid == 2 * NB) {
+            if (!(p > 0.0)) atomicCAS(ctl, 0, fi + 1);
+            dsq[j] = sqrt(p);
+            rsq[j] = 1.0 / dsq[j];
         }
-        const double sj = sqrt(djj), rs = 1.0 / sj;
-        if (tid == 0) dsq[j] = sj;
-        if (tid > j && tid < w) S[tid * kDiagLd + j] *= rs;
         __syncthreads();
-        for (int i = tid; i < NB * NB; i += kThreads) {
-            const int r = i & (NB - 1), c = i >> 6;
-            if (c > j && r >= c && r < w) S[r * kDiagLd + c] -= S[r * kDiagLd + j] * S[c * kDiagLd + j];
+        if (tid == 2 * NB) X[j * kDiagLd + j] = rsq[j];  // W_jj = p_j^-1/2 (unscaled 1)
+        // phase 2: rows i = j + 1 + rg + 4u, column t; loads before stores
+        const double xj = X[j * kDiagLd + t];
+        double m[16], xv[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+            const int i = j + 1 + rg + 4 * u;
+            const bool ok = i < w;
+            m[u] = ok ? mv[i] : 0.0;
+            xv[u] = ok ? X[i * kDiagLd + t] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+            const int i = j + 1 + rg + 4 * u;
+            if (i < w) X[i * kDiagLd + t] = (t == j) ? -m[u] : fma(-m[u], xj, xv[u]);
         }
         __syncthreads();
     }
-    if (tid < w) S[tid * kDiagLd + tid] = dsq[tid];
-    __syncthreads();
-    // W = C^-1 (lower): column c by a group of 4 lanes, forward substitution
-    {
-        const int c = tid >> 2, l4 = tid & 3;
-        for (int i = 0; i < w; ++i) {
-            const bool act = c < w && i >= c;
-            double part = 0.0;
-            if (act)
-                for (int q = c + l4; q < i; q += 4) part += S[i * kDiagLd + q] * W[q * kDiagLd + c];
-            part += __shfl_xor_sync(0xffffffffu, part, 1);
-            part += __shfl_xor_sync(0xffffffffu, part, 2);
-            if (act && l4 == 0) W[i * kDiagLd + c] = ((i == c ? 1.0 : 0.0) - part) / S[i * kDiagLd + i];
-            __syncwarp();
-        }
-    }
+    if (tid < w - 1) X[(w - 1) * kDiagLd + tid] *= rsq[w - 1];
+    if (tid < w) base[(int64_t)tid * f.nf + tid] = dsq[tid];  // diag(C); the pack and d read it
     __syncthreads();
     double *wo = inv + f.ioff + (int64_t)k * NB * NB;
     for (int i = tid; i < NB * NB; i += kThreads) {
         const int r = i & (NB - 1), c = i >> 6;
-        const bool in = r < w && c < w && r >= c;
-        if (in) base[(int64_t)c * f.nf + r] = S[r * kDiagLd + c];
-        wo[c * NB + r] = in ? W[r * kDiagLd + c] : 0.0;  // W(r, c), column-major
+        wo[c * NB + r] = (r < w && c <= r) ? X[r * kDiagLd + c] : 0.0;  // W(r, c), column-major
     }
 }
 
@@ -206,6 +260,7 @@ __global__ void __launch_bounds__(256) panel_kernel(const tsb_front *__restrict_
     double *src = ws + f.off + (int64_t)c0 * f.nf + r0;
     load_n(As, src, f.nf, h, w);
     load_n(Bs, inv + f.ioff + (int64_t)k * NB * NB, NB, w, w);  // Bs[q][c] = W(c, q)
+    cp_async_wait();
     __syncthreads();
     double acc[4][4];
     tile_mma(As, Bs, w, acc);
@@ -231,6 +286,7 @@ __global__ void __launch_bounds__(256) update_kernel(const tsb_front *__restrict
     const double *col = ws + f.off + (int64_t)c0 * f.nf;
     load_n(As, col + ri, f.nf, hi, w);
     load_n(Bs, col + rj, f.nf, hj, w);
+    cp_async_wait();
     __syncthreads();
     double acc[4][4];
     tile_mma(As, Bs, w, acc);
@@ -270,6 +326,7 @@ __global__ void __launch_bounds__(256) tscale_kernel(const tsb_front *__restrict
     double *src = b + (int64_t)k * NB * ld;
     load_n(As, src, ld, rows, w);
     load_t(Bs, inv + f.ioff + (int64_t)k * NB * NB, NB, w, w);  // Bs[q][c] = W(q, c)
+    cp_async_wait();
     __syncthreads();
     double acc[4][4];
     tile_mma(As, Bs, w, acc);
@@ -291,6 +348,7 @@ __global__ void __launch_bounds__(256) tupdate_kernel(const tsb_front *__restric
     const int w = min(NB, f.m - k * NB);
     load_n(As, b + (int64_t)k * NB * ld, ld, rows, w);
     load_t(Bs, ws + f.off + (int64_t)j * NB * f.nf + k * NB, f.nf, w, NB);  // Bs[q][c] = C(kNB + q, jNB + c)
+    cp_async_wait();
     __syncthreads();
     double acc[4][4];
     tile_mma(As, Bs, w, acc);

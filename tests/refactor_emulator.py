@@ -86,7 +86,7 @@ def run(rp: R.RefactorPlan, values, tiles_l, tiles_u, tblk_l, tblk_u, n):
                     bad = fi if bad < 0 else bad
                     Cc = np.eye(w)
                 W = np.linalg.inv(Cc)
-                _put(ws, base, nf, Cc, lower=True)
+                ws[base + np.arange(w) * (nf + 1)] = np.diagonal(Cc)  # the kernel stores diag(C_kk) only
                 Wf = np.zeros((NB, NB))
                 Wf[:w, :w] = np.tril(W)
                 inv[int(f["ioff"]) + k * NB * NB + np.arange(NB * NB)] = Wf.T.ravel()  # column-major
