@@ -269,6 +269,37 @@ int tsb_ldlt_upper_scaled(tsb_ldlt_t h, const double *d_y, double *d_z, void *st
 int tsb_ldlt_external_sums(tsb_ldlt_t h, double *d_out, void *stream);
 
 /* ------------------------------------------------------------------------
+ * Device pattern build                 replaces build_pattern (assembly.py:
+ *                                      235-312) for whole pinned nodes: the
+ * same CSR (row_ptr, col_ind) and gather lists as _plan.topology_pattern.
+ * Two calls: count (synchronises once, fills n_blocks / nnz), then fill
+ * into caller-allocated outputs (synchronises once, fills n_contrib).
+ * ---------------------------------------------------------------------- */
+typedef struct tsb_pattern {
+    int64_t n_nodes, n_elems;
+    const int32_t *d_conn;        /* [4][m] element node ids                      */
+    const uint8_t *d_pinned;      /* [N] 1 = pinned node                          */
+    int64_t *d_tmp;               /* scratch [N]                                  */
+    int64_t *d_sums;              /* scratch [max(N, n_blocks) / 1024 + 1]        */
+    int64_t *d_node_ptr;          /* out [N + 1]                                  */
+    int32_t *d_node_list;         /* out [4 m]: e*4 + a, ascending per node       */
+    int32_t *d_cand;              /* scratch [16 m]: sorted neighbours per node   */
+    int64_t *d_nbr;               /* out [N]: node blocks per node row            */
+    int64_t *d_blk_ptr;           /* out [N + 1]                                  */
+    int64_t *d_row_base;          /* out [N + 1]: first slot of row 3I            */
+    int64_t n_blocks, nnz, n_contrib;  /* filled by the calls                    */
+    int64_t *d_ccount;            /* scratch [n_blocks]                           */
+    int64_t *d_cptr;              /* out [n_blocks + 1]                           */
+    int32_t *d_row_ptr;           /* out [3N + 1]                                 */
+    int32_t *d_col_ind;           /* out [nnz]                                    */
+    int32_t *d_blk;               /* out [n_blocks][4]                            */
+    int32_t *d_blk_list;          /* out [<= 16 m]                                */
+} tsb_pattern;
+
+int tsb_pattern_count(tsb_pattern *p, void *stream);
+int tsb_pattern_fill(tsb_pattern *p, void *stream);
+
+/* ------------------------------------------------------------------------
  * Device LDL^T refactorisation        replaces ldlt_factor (numeric phase)
  *                                     ndprecond.py:501-572 (+ the host pack
  *                                     of the factor into the sweep layout)

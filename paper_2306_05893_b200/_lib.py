@@ -80,6 +80,16 @@ class RefactorDesc(C.Structure):
     ]
 
 
+class PatternDesc(C.Structure):
+    _fields_ = [
+        ("n_nodes", c_i64), ("n_elems", c_i64), ("d_conn", c_vp), ("d_pinned", c_vp), ("d_tmp", c_vp),
+        ("d_sums", c_vp), ("d_node_ptr", c_vp), ("d_node_list", c_vp), ("d_cand", c_vp), ("d_nbr", c_vp),
+        ("d_blk_ptr", c_vp), ("d_row_base", c_vp), ("n_blocks", c_i64), ("nnz", c_i64), ("n_contrib", c_i64),
+        ("d_ccount", c_vp), ("d_cptr", c_vp), ("d_row_ptr", c_vp), ("d_col_ind", c_vp), ("d_blk", c_vp),
+        ("d_blk_list", c_vp),
+    ]
+
+
 class Report(C.Structure):
     _fields_ = [
         ("iterations", c_i64), ("final_residual", C.c_double), ("converged", c_i32),
@@ -119,6 +129,8 @@ _SIGNATURES = {
                                 c_vp, C.c_double, c_i64, C.POINTER(Report), c_vp]),
     "tsb_pcg_report": (C.c_int, [c_vp, C.POINTER(Report), c_vp]),
     "tsb_pcg_phase_times": (C.c_int, [c_vp, c_vp, c_vp]),
+    "tsb_pattern_count": (C.c_int, [C.POINTER(PatternDesc), c_vp]),
+    "tsb_pattern_fill": (C.c_int, [C.POINTER(PatternDesc), c_vp]),
     "tsb_refactor_create": (C.c_int, [C.POINTER(RefactorDesc), C.POINTER(c_vp)]),
     "tsb_refactor_destroy": (C.c_int, [c_vp]),
     "tsb_refactor_run": (C.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
@@ -155,7 +167,7 @@ def load() -> C.CDLL:
             fn.argtypes = args
         if lib.tsb_abi_version() != ABI_VERSION:
             raise NativeLibraryError("libtsb ABI version mismatch")
-        for k, st in enumerate((AsmPlan, AsmCoeffs, None, LdltDesc, Report, None, None, None, RefactorDesc)):
+        for k, st in enumerate((AsmPlan, AsmCoeffs, None, LdltDesc, Report, None, None, None, RefactorDesc, PatternDesc)):
             if st is not None and lib.tsb_struct_size(k) != C.sizeof(st):
                 raise NativeLibraryError(f"libtsb struct layout mismatch: {st.__name__}")
         _lib = lib

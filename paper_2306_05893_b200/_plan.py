@@ -88,6 +88,58 @@ def topology_pattern(mesh):
     }
 
 
+def device_topology_pattern(mesh, keep_device=False):
+    """topology_pattern built on the device (csrc/pattern.cu, tsb_pattern_count/fill):
+    the same arrays, downloaded for the host-side CsrMatrix; with keep_device
+    the int32 device copies the assembly plan uses are returned under "dev"."""
+    import ctypes as C
+
+    t = _lib.require_cuda()
+    N, el = mesh.node_count, mesh.elements
+    m = len(el)
+    dev = "cuda"
+    conn = t.from_numpy(_i32(el.T)).to(dev)
+    pinned = np.zeros(N, dtype=np.uint8)
+    pinned[mesh.fixed_nodes] = 1
+    pin = t.from_numpy(pinned).to(dev)
+    i64 = lambda k: t.empty(max(k, 1), dtype=t.int64, device=dev)  # noqa: E731
+    i32 = lambda k: t.empty(max(k, 1), dtype=t.int32, device=dev)  # noqa: E731
+    buf = {"tmp": i64(N), "sums": i64(N // 1024 + 2), "node_ptr": i64(N + 1), "node_list": i32(4 * m),
+           "cand": i32(16 * m), "nbr": i64(N), "blk_ptr": i64(N + 1), "row_base": i64(N + 1)}
+    P = _lib.ptr
+    d = _lib.PatternDesc(n_nodes=N, n_elems=m, d_conn=P(conn), d_pinned=P(pin), d_tmp=P(buf["tmp"]),
+                         d_sums=P(buf["sums"]), d_node_ptr=P(buf["node_ptr"]), d_node_list=P(buf["node_list"]),
+                         d_cand=P(buf["cand"]), d_nbr=P(buf["nbr"]), d_blk_ptr=P(buf["blk_ptr"]),
+                         d_row_base=P(buf["row_base"]), n_blocks=-1, nnz=-1, n_contrib=-1)
+    lib = _lib.load()
+    _lib.check(lib.tsb_pattern_count(C.byref(d), _lib.stream_ptr()), "pattern_count")
+    nb, nnz = int(d.n_blocks), int(d.nnz)
+    if nnz >= 2**31:
+        raise OverflowError("pattern exceeds int32 range of the device layout")
+    buf.update(sums2=i64(nb // 1024 + 2), ccount=i64(nb), cptr=i64(nb + 1), row_ptr=i32(3 * N + 1),
+               col_ind=i32(nnz), blk=i32(4 * nb), blk_list=i32(16 * m))
+    d.d_sums = P(buf["sums2"])
+    d.d_ccount, d.d_cptr, d.d_row_ptr = P(buf["ccount"]), P(buf["cptr"]), P(buf["row_ptr"])
+    d.d_col_ind, d.d_blk, d.d_blk_list = P(buf["col_ind"]), P(buf["blk"]), P(buf["blk_list"])
+    _lib.check(lib.tsb_pattern_fill(C.byref(d), _lib.stream_ptr()), "pattern_fill")
+    nc = int(d.n_contrib)
+    row_ptr = buf["row_ptr"][:3 * N + 1].cpu().numpy().astype(np.int64)
+    col_ind = buf["col_ind"][:nnz].cpu().numpy().astype(np.int64)
+    fixed_dofs = mesh.fixed_dofs()
+    out = {
+        "row_ptr": row_ptr, "col_ind": col_ind, "fixed_diag_slots": row_ptr[fixed_dofs],
+        "blk": buf["blk"][:4 * nb].cpu().numpy().astype(np.int64).reshape(nb, 4),
+        "blk_list": buf["blk_list"][:nc].cpu().numpy().astype(np.int64),
+        "node_ptr": buf["node_ptr"][:N + 1].cpu().numpy(),
+        "node_list": buf["node_list"][:4 * m].cpu().numpy().astype(np.int64),
+    }
+    for a in (out["row_ptr"], out["col_ind"], out["fixed_diag_slots"]):
+        a.setflags(write=False)
+    if keep_device:
+        out["dev"] = {k: buf[k] for k in ("row_ptr", "col_ind", "blk", "blk_list", "node_list")}
+    return out
+
+
 def _i32(a):
     a = np.asarray(a)
     if a.size and (a.max() >= 2**31 or a.min() < -(2**31)):

@@ -39,6 +39,7 @@ extern "C" int64_t tsb_struct_size(int32_t which) {
         case 6: return sizeof(tsb_front);
         case 7: return sizeof(tsb_front_pair);
         case 8: return sizeof(tsb_refactor_desc);
+        case 9: return sizeof(tsb_pattern);
         default: return -1;
     }
 }

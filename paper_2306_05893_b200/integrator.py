@@ -19,7 +19,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib
-from ._plan import AssemblyPlan, topology_pattern
+from ._plan import AssemblyPlan, device_topology_pattern, topology_pattern
 from .assembly import CsrMatrix, build_pattern, TripletStream
 from .krylov import SolveReport
 from .mesh import Mesh
@@ -139,7 +139,7 @@ class _DeviceAssembler:
 
     def ensure(self) -> bool:
         if self.pattern is None or self.force_rebuild:
-            self.pattern = topology_pattern(self.mesh)
+            self.pattern = device_topology_pattern(self.mesh)  # csrc/pattern.cu
             self.pattern_rebuilds += 1
             self._mapping = None
             return True
