@@ -381,3 +381,68 @@ def backward_substitution(row_ptr, col_ind, values, w):
         if hi > lo:
             z[col_ind[lo:hi]] -= values[lo:hi] * z[j]
     return z
+
+
+# ---------------------------------------------------------------------------
+# Plane contact stage -- contact.py:89-257
+# ---------------------------------------------------------------------------
+
+
+def detect_plane_contacts(positions, plane_z):
+    """Unilateral rows for nodes below z = plane_z (contact.py:89-106):
+    -> (nodes, dof columns 3i+2, coefficients -1, violation plane_z - z)."""
+    pen = plane_z - np.asarray(positions)[:, 2]
+    nodes = np.flatnonzero(pen > 0.0)
+    return nodes, 3 * nodes + 2, np.full(len(nodes), -1.0), pen[nodes]
+
+
+def build_compliance(cols, coefs, ndof, solve_fn):
+    """W = J A^-1 J^T column by column for one-entry rows (contact.py:109-125),
+    symmetrised by averaging; -> (W, S)."""
+    m = len(cols)
+    s = np.empty((ndof, m))
+    for i in range(m):
+        e = np.zeros(ndof)
+        e[cols[i]] = coefs[i]
+        s[:, i] = solve_fn(e)
+    w = np.empty((m, m))
+    for i in range(m):
+        w[i] = coefs * s[cols, i]
+    return 0.5 * (w + w.T), s
+
+
+def projected_gauss_seidel(w, rhs, unilateral, tol=1e-12, max_sweeps=500):
+    """Projected Gauss-Seidel in constraint order (contact.py:128-166)."""
+    m = len(rhs)
+    lam = np.zeros(m)
+    if m == 0:
+        return lam
+    diag = np.diagonal(w).copy()
+    usable = diag != 0.0
+    for _ in range(max_sweeps):
+        dmax = 0.0
+        for i in range(m):
+            if not usable[i]:
+                lam[i] = 0.0
+                continue
+            new = lam[i] + (rhs[i] - w[i] @ lam) / diag[i]
+            if unilateral[i] and new < 0.0:
+                new = 0.0
+            dmax = max(dmax, abs(new - lam[i]))
+            lam[i] = new
+        scale = np.abs(lam).max()
+        if dmax <= tol * scale or scale == 0.0:
+            break
+    return lam
+
+
+def advance(acc, x, v, dt, fixed_nodes):
+    """Kinematic update of an implicit step (integrator.py:192-208 /
+    contact.py:169-195): a[pinned] = 0, v' = v + h a, x' = x + h v', pinned keep."""
+    acc = np.asarray(acc, dtype=np.float64).reshape(-1, 3).copy()
+    acc[fixed_nodes] = 0.0
+    vel = v + dt * acc
+    pos = x + dt * vel
+    vel[fixed_nodes] = v[fixed_nodes]
+    pos[fixed_nodes] = x[fixed_nodes]
+    return pos, vel, acc

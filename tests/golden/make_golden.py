@@ -157,8 +157,12 @@ def nd_cases():
 def main():
     meta = dict(numpy_version=np.array(np.__version__), reference=np.array("tetsim " + tetsim.__version__))
     stvk = dict(law=np.array("stvk"))
-    np.savez_compressed(OUT / "beam_stvk.npz", **scenario_system((3, 3, 8), 6, law="stvk"), **stvk, **meta)
+    if "--only-contact" not in sys.argv:
+        np.savez_compressed(OUT / "beam_stvk.npz", **scenario_system((3, 3, 8), 6, law="stvk"), **stvk, **meta)
     if "--only-stvk" in sys.argv:
+        return
+    np.savez_compressed(OUT / "contact_drop.npz", **contact_case(), **meta)
+    if "--only-contact" in sys.argv:
         return
     np.savez_compressed(OUT / "beam_small.npz", **scenario_system((3, 3, 8), 6, with_triplets=True), **meta)
     np.savez_compressed(OUT / "beam_cfg1.npz", **scenario_system((6, 6, 28), 6), **meta)
@@ -166,6 +170,51 @@ def main():
     np.savez_compressed(OUT / "nd_plans.npz", **nd_cases(), **meta)
     for p in sorted(OUT.glob("*.npz")):
         print(p.name, p.stat().st_size)
+
+
+
+def contact_case(steps=14, plane_z=-0.03, dims=(3, 3, 4)):
+    """Drop onto a plane through the reference's PlaneContactPipeline
+    (contact.py:196-257): free beam, default gravity, LDL^T factors of the
+    previous step's matrix as apply_inverse (deterministic staleness 1; CG
+    compliance solves on the first step), Jacobi-PCG free motion."""
+    from tetsim.contact import PlaneContactPipeline, build_compliance, detect_plane_contacts, projected_gauss_seidel
+
+    mesh = tetsim.generate_beam(*dims, 0.1)
+    model = tetsim.make_model("corotational", mesh, PARAMS)
+    integ = BackwardEulerIntegrator(mesh, model, IntegratorConfig(dt=0.01))
+    pipe = PlaneContactPipeline(integ, plane_z)
+    cfg = krylov.SolverConfig(1e-10, 8000)
+    solve = lambda a, b: krylov.pcg(a, b, krylov.jacobi_precond(a), cfg)  # noqa: E731
+    plan = ndprecond.expand_plan(ndprecond.nested_dissection(tetsim.vertex_adjacency(mesh), 16))
+    st = SimState.rest(mesh)
+    out = dict(c_dims=np.array(dims), c_plane=np.array(plane_z), c_steps=np.array(steps))
+    factors = None
+    hist = {k: [] for k in ("ncontacts", "residual", "maxpen", "iterations")}
+    first = None
+    for k in range(steps):
+        apply_inverse = (lambda rhs, f=factors: f.apply(rhs)) if factors is not None else None
+        if first is None and factors is not None:
+            free = integ.compute_step(st, solve)
+            cs = detect_plane_contacts(free.positions, plane_z)
+            if cs.nconstraints:
+                w, s_cols = build_compliance(cs, apply_inverse)
+                h = integ.config.dt
+                lam = projected_gauss_seidel(h * h * w, cs.violation, cs.types)
+                first = dict(c_step=np.array(k), c_x=st.positions.copy(), c_v=st.velocities.copy(),
+                             c_nodes=(cs.col_ind - 2) // 3, c_violation=cs.violation, c_w=w, c_lam=lam,
+                             c_free_pos=free.positions)
+        info = pipe.step(st, solve, apply_inverse)
+        hist["ncontacts"].append(info.ncontacts)
+        hist["residual"].append(info.complementarity_residual)
+        hist["maxpen"].append(info.max_penetration)
+        hist["iterations"].append(info.result.report.iterations)
+        factors = ndprecond.ldlt_factor(info.result.matrix, plan)
+        out[f"c_pos_{k}"] = st.positions.copy()
+        out[f"c_vel_{k}"] = st.velocities.copy()
+    out.update({f"c_{k}": np.array(v) for k, v in hist.items()})
+    out.update(first or {})
+    return out
 
 
 if __name__ == "__main__":

@@ -128,3 +128,46 @@ def test_stvk_assembly_matches_reference(golden):
     assert np.abs(out["f_int"] - g["f_int"]).max() <= 1e-12 * np.abs(g["f_int"]).max()
     _, kv, _ = O.stvk(g["nodes"], g["elements"], rest, g["positions"], g["velocities"])
     assert np.abs(kv - g["kv"]).max() <= 1e-12 * np.abs(g["kv"]).max()
+
+
+def test_contact_stage_matches_reference(golden):
+    """First contact step of the reference's drop scenario (contact_drop.npz):
+    free motion, detection, compliance with LDL^T factors of the previous
+    step's matrix, PGS multipliers, corrected state (contact.py:89-257)."""
+    from paper_2306_05893_b200 import mesh as M, ndprecond as ND
+    from paper_2306_05893_b200.assembly import CsrMatrix
+
+    g = golden("contact_drop")
+    k = int(g["c_step"])
+    dims = tuple(int(v) for v in g["c_dims"])
+    plane = float(g["c_plane"])
+    import paper_2306_05893_b200 as P
+
+    mesh = P.generate_beam(*dims, 0.1)
+    rest = O.rest_data(mesh.nodes, mesh.elements, 1e5, 0.3, 1000.0)
+    nofix = np.zeros(0, dtype=np.int64)
+    grav = (0.0, 0.0, -G)
+
+    def system(x, v):
+        return O.assemble_system(mesh.nodes, mesh.elements, nofix, rest, x, v, np.zeros(mesh.ndof), 0.01, grav)
+
+    prev = system(g[f"c_pos_{k - 2}"], g[f"c_vel_{k - 2}"])
+    plan = ND.expand_plan(ND.nested_dissection(M.vertex_adjacency(mesh), 16))
+    f = ND.ldlt_factor(CsrMatrix(mesh.ndof, mesh.ndof, prev["row_ptr"], prev["col_ind"], prev["values"]), plan)
+    x0, v0 = g["c_x"], g["c_v"]
+    assert np.array_equal(x0, g[f"c_pos_{k - 1}"])
+    cur = system(x0, v0)
+    inv = O.jacobi_inv_diag(cur["row_ptr"], cur["col_ind"], cur["values"], mesh.ndof)
+    acc, it, _, _ = O.pcg(cur["row_ptr"], cur["col_ind"], cur["values"], cur["b"], lambda r: r * inv, 1e-10, 8000)
+    assert it == int(g["c_iterations"][k])
+    pos, vel, acc = O.advance(acc, x0, v0, 0.01, nofix)
+    assert np.abs(pos - g["c_free_pos"]).max() <= 1e-12
+    nodes, cols, coefs, viol = O.detect_plane_contacts(pos, plane)
+    assert np.array_equal(nodes, g["c_nodes"]) and np.abs(viol - g["c_violation"]).max() <= 1e-15
+    w, s = O.build_compliance(cols, coefs, mesh.ndof, lambda e: O.apply(f, e))
+    assert np.abs(w - g["c_w"]).max() <= 1e-12 * np.abs(g["c_w"]).max()
+    lam = O.projected_gauss_seidel(0.01 ** 2 * w, viol, np.ones(len(viol), dtype=bool))
+    assert np.abs(lam - g["c_lam"]).max() <= 1e-10 * np.abs(g["c_lam"]).max()
+    pos2, vel2, _ = O.advance(acc.reshape(-1, 3) - (s @ lam).reshape(-1, 3), x0, v0, 0.01, nofix)
+    assert np.abs(pos2 - g[f"c_pos_{k}"]).max() <= 1e-12
+    assert np.abs(vel2 - g[f"c_vel_{k}"]).max() <= 1e-10 * np.abs(g[f"c_vel_{k}"]).max()
