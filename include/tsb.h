@@ -300,6 +300,39 @@ int tsb_pattern_count(tsb_pattern *p, void *stream);
 int tsb_pattern_fill(tsb_pattern *p, void *stream);
 
 /* ------------------------------------------------------------------------
+ * Plane contact stage                   replaces detect_plane_contacts,
+ *                                       build_compliance,
+ * projected_gauss_seidel, correct_motion (contact.py:89-195).  J is CSR over
+ * the constraint rows (int64 indptr, int32 columns).  With LDL^T factors
+ * W = Y^T D^-1 Y with Y = L^-1 P J^T (tsb_ldlt_lower per column) and
+ * S lambda = P^T L^-T D^-1 (Y lambda) (one tsb_ldlt_upper_scaled).
+ * ---------------------------------------------------------------------- */
+/* nodes with z < plane_z in ascending order, their penetration, the count and
+ * max(plane_z - z, 0); d_nodes / d_pen may be NULL (count + max only) */
+int tsb_plane_contacts(int64_t n_nodes, const double *d_pos, double plane_z, int32_t *d_nodes, double *d_pen,
+                       int64_t *d_count, double *d_maxpen, void *stream);
+/* R[:, i] = J^T e_i (scattered through iperm when non-NULL), R n x m column-major */
+int tsb_contact_rhs(int64_t m, const int64_t *d_indptr, const int32_t *d_cols, const double *d_coefs,
+                    const int32_t *d_iperm, int64_t n, double *d_R, void *stream);
+/* W = scale * Y^T diag(1/d) Y (d may be NULL: identity); d_part scratch of
+ * tsb_gram_scratch(n, m) doubles */
+int64_t tsb_gram_scratch(int64_t n, int64_t m);
+int tsb_gram(int64_t n, int64_t m, const double *d_Y, const double *d_d, double scale, double *d_part, double *d_W,
+             void *stream);
+/* W = scale * (J S + (J S)^T) / 2 for solution columns S (n x m) */
+int tsb_compliance_from_columns(int64_t m, int64_t n, const int64_t *d_indptr, const int32_t *d_cols,
+                                const double *d_coefs, const double *d_S, double scale, double *d_W, void *stream);
+/* lambda of W lambda = rhs, lambda >= 0 on unilateral rows; info: sweeps,
+ * complementarity residual sum |lambda (W lambda - rhs)|, dropped rows */
+int tsb_pgs(int64_t m, const double *d_W, const double *d_rhs, const uint8_t *d_unilateral, double tol,
+            int32_t max_sweeps, double *d_lam, double *d_info, void *stream);
+/* out = Y lambda (n x m column-major) */
+int tsb_gemv_cols(int64_t n, int64_t m, const double *d_Y, const double *d_lam, double *d_out, void *stream);
+/* acc = acc_free - delta (delta in permuted order when iperm is non-NULL) */
+int tsb_contact_correct(int64_t n, const double *d_acc_free, const double *d_delta, const int32_t *d_iperm,
+                        double *d_acc, void *stream);
+
+/* ------------------------------------------------------------------------
  * Device LDL^T refactorisation        replaces ldlt_factor (numeric phase)
  *                                     ndprecond.py:501-572 (+ the host pack
  *                                     of the factor into the sweep layout)

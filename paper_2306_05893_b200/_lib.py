@@ -129,6 +129,14 @@ _SIGNATURES = {
                                 c_vp, C.c_double, c_i64, C.POINTER(Report), c_vp]),
     "tsb_pcg_report": (C.c_int, [c_vp, C.POINTER(Report), c_vp]),
     "tsb_pcg_phase_times": (C.c_int, [c_vp, c_vp, c_vp]),
+    "tsb_plane_contacts": (C.c_int, [c_i64, c_vp, C.c_double, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "tsb_contact_rhs": (C.c_int, [c_i64, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp]),
+    "tsb_gram_scratch": (c_i64, [c_i64, c_i64]),
+    "tsb_gram": (C.c_int, [c_i64, c_i64, c_vp, c_vp, C.c_double, c_vp, c_vp, c_vp]),
+    "tsb_compliance_from_columns": (C.c_int, [c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, C.c_double, c_vp, c_vp]),
+    "tsb_pgs": (C.c_int, [c_i64, c_vp, c_vp, c_vp, C.c_double, c_i32, c_vp, c_vp, c_vp]),
+    "tsb_gemv_cols": (C.c_int, [c_i64, c_i64, c_vp, c_vp, c_vp, c_vp]),
+    "tsb_contact_correct": (C.c_int, [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "tsb_pattern_count": (C.c_int, [C.POINTER(PatternDesc), c_vp]),
     "tsb_pattern_fill": (C.c_int, [C.POINTER(PatternDesc), c_vp]),
     "tsb_refactor_create": (C.c_int, [C.POINTER(RefactorDesc), C.POINTER(c_vp)]),
