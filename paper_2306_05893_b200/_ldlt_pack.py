@@ -588,6 +588,8 @@ class DevicePanels:
                           part=z(TILE * (H["npart_l"] + H["npart_u"]), t.float64),
                           cnt=z(3 * nb, t.int32), tcnt=z(ntl + ntu, t.int32), ctl=z(4, t.int32))
         self.n = n
+        self.ncbuf, self.npart_l = int(H["ncbuf"]), int(H["npart_l"])
+        self._multi = {}
         self.n_blocks = nb
         self.n_items = (len(items_l), len(items_u))
         self.bytes = {"g": H["bytes_g"], "gt": H["bytes_gt"]}
@@ -627,6 +629,30 @@ class DevicePanels:
         fn = {"lower": self._lib.tsb_ldlt_lower, "upper": self._lib.tsb_ldlt_upper,
               "apply": self._lib.tsb_ldlt_apply, "upper_scaled": self._lib.tsb_ldlt_upper_scaled}[mode]
         _lib.check(fn(self.h, _lib.ptr(r), _lib.ptr(out), _lib.stream_ptr()), f"ldlt_{mode}")
+
+    MULTI_RHS = 8  # right-hand sides per multi-RHS lower sweep
+
+    def lower_multi(self, R, Y):
+        """Y[j] = L^-1 R[j] (permuted order) for the rows of R ([k][n] CUDA
+        tensors), MULTI_RHS right-hand sides per sweep (tsb_ldlt_lower_multi)."""
+        t = _lib.torch()
+        k = R.shape[0]
+        for j0 in range(0, k, self.MULTI_RHS):
+            nr = min(self.MULTI_RHS, k - j0)
+            if nr == 1:
+                self.run("lower", R[j0], Y[j0])
+                continue
+            sc = self._multi.get(nr)
+            if sc is None:
+                ld_part = max(TILE * self.npart_l, 1)
+                sc = (t.zeros(nr * max(self.ncbuf, 1), dtype=t.float64, device="cuda"),
+                      t.zeros(nr * self.n, dtype=t.float64, device="cuda"),
+                      t.zeros(nr * ld_part, dtype=t.float64, device="cuda"), ld_part)
+                self._multi[nr] = sc
+            cb, xs, part, ld_part = sc
+            _lib.check(self._lib.tsb_ldlt_lower_multi(self.h, nr, _lib.ptr(R[j0]), _lib.ptr(Y[j0]), _lib.ptr(cb),
+                                                      max(self.ncbuf, 1), _lib.ptr(xs), _lib.ptr(part), ld_part,
+                                                      _lib.stream_ptr()), "ldlt_lower_multi")
 
     def lower_ext(self, r, ext, out):
         _lib.check(self._lib.tsb_ldlt_lower_ext(self.h, _lib.ptr(r), _lib.ptr(ext), _lib.ptr(out), _lib.stream_ptr()),

@@ -115,6 +115,7 @@ _SIGNATURES = {
     "tsb_ldlt_lower": (C.c_int, [c_vp, c_vp, c_vp, c_vp]),
     "tsb_ldlt_upper": (C.c_int, [c_vp, c_vp, c_vp, c_vp]),
     "tsb_ldlt_apply": (C.c_int, [c_vp, c_vp, c_vp, c_vp]),
+    "tsb_ldlt_lower_multi": (C.c_int, [c_vp, c_i32, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_vp]),
     "tsb_ldlt_lower_ext": (C.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp]),
     "tsb_ldlt_upper_scaled": (C.c_int, [c_vp, c_vp, c_vp, c_vp]),
     "tsb_ldlt_external_sums": (C.c_int, [c_vp, c_vp, c_vp]),

@@ -331,8 +331,7 @@ class PlaneContactPipeline:
         _check(lib.tsb_contact_rhs(m, _lib.ptr(ip), _lib.ptr(ci), _lib.ptr(co), _lib.ptr(iperm), n, _lib.ptr(R), sp),
                "contact_rhs")
         Y = t.empty((m, n), dtype=t.float64, device="cuda")
-        for i in range(m):  # lower sweeps (permuted order)
-            dev.run("lower", R[i], Y[i])
+        dev.lower_multi(R, Y)  # multi-RHS lower sweeps (permuted order)
         W = t.empty((m, m), dtype=t.float64, device="cuda")
         part = t.empty(max(int(lib.tsb_gram_scratch(n, m)), 1), dtype=t.float64, device="cuda")
         _check(lib.tsb_gram(n, m, _lib.ptr(Y), _lib.ptr(dev.t["d"]), float(h * h), _lib.ptr(part), _lib.ptr(W), sp),

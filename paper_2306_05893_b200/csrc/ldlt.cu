@@ -203,6 +203,41 @@ extern "C" int tsb_ldlt_apply(tsb_ldlt_t h, const double *d_r, double *d_z, void
     return tsb::guard([&] { tsb::ldlt_enqueue(h, 2, d_r, d_z, nullptr, tsb::as_stream(stream)); });
 }
 
+// y_j = L^-1 r_j for nr right-hand sides in one sweep (every factor tile read
+// once for all of them); r, y: [nr][n] permuted; scratch: cbuf [nr][ld_cb]
+// (ld_cb >= contribution slots), x [nr][n], part [nr][ld_part] (>= the lower
+// segment partials).
+extern "C" int tsb_ldlt_lower_multi(tsb_ldlt_t h, int32_t nr, const double *d_r, double *d_y, double *d_cbuf,
+                                    int64_t ld_cb, double *d_x, double *d_part, int64_t ld_part, void *stream) {
+    using namespace tsb;
+    return guard([&] {
+        if (h == nullptr || nr < 1) throw Error(TSB_E_ARG, "bad multi-RHS lower sweep");
+        tsb_ldlt_desc D = h->d;
+        if (D.n == 0) return;
+        const size_t smem = sweep_smem_lower(D, nr);
+        int dev = 0, optin = 0;
+        TSB_CUDA(cudaGetDevice(&dev));
+        TSB_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+        if (smem + 8192 > (size_t)optin) throw Error(TSB_E_ARG, "too many right-hand sides for the staging buffer");
+        D.d_cbuf = d_cbuf;
+        D.d_x = d_x;
+        D.d_part_lower = d_part;
+        SweepArgs a{d_r, nullptr, nullptr, d_y, nullptr, nullptr, nullptr, nullptr};
+        a.nr = nr;
+        a.ld = D.n;
+        a.ld_cb = ld_cb;
+        a.ld_part = ld_part;
+        // the grid of the handle was sized for the 1-RHS footprint: keep it co-resident
+        int per_sm = 0;
+        TSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lower_sweep<false>, kSweepBlock, smem));
+        int nsm = kNumSM;
+        TSB_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+        const int grid = D.grid < nsm * per_sm ? D.grid : nsm * per_sm;
+        if (grid < 1) throw Error(TSB_E_ARG, "multi-RHS lower sweep does not fit on an SM");
+        launch_coop(lower_sweep<false>, grid, smem, as_stream(stream), D, a);
+    });
+}
+
 extern "C" int tsb_ldlt_lower_ext(tsb_ldlt_t h, const double *d_r, const double *d_ext, double *d_y, void *stream) {
     return tsb::guard([&] { tsb::ldlt_enqueue_ext(h, 0, d_r, d_ext, d_y, tsb::as_stream(stream)); });
 }

@@ -107,6 +107,11 @@ struct SweepArgs {
     double *out;             // upper apply: output in original order
     const int32_t *done;     // stop flag (skip the sweep when set)
     const double *ext;       // lower: contributions from outside the handle's blocks (subtracted), or NULL
+    // multi-RHS lower sweep (tsb_ldlt_lower_multi): nr right-hand sides, vector j
+    // of in / x / d_x at j * ld, of the contributions at j * ld_cb, of the
+    // segment partial sums at j * ld_part
+    int nr = 1;
+    int64_t ld = 0, ld_cb = 0, ld_part = 0;
 };
 
 // Exit protocol: the last CTA out zeroes the counters for the next replay.
@@ -139,10 +144,11 @@ __device__ __forceinline__ void upper_exit(const tsb_ldlt_desc &D) {
 
 constexpr int kFinRows = 1024;          // rows per piece of a mode-2 finalisation
 
-// dynamic shared memory of the sweep bodies (max_v = widest item window)
-inline size_t sweep_smem_lower(const tsb_ldlt_desc &D) {
+// dynamic shared memory of the sweep bodies (max_v = widest item window;
+// nr right-hand sides stage nr windows)
+inline size_t sweep_smem_lower(const tsb_ldlt_desc &D, int nr = 1) {
     const int offs = (D.max_v + 2 > kFinRows + 2 ? D.max_v + 2 : kFinRows + 2);
-    return (size_t)(kStage + ((D.max_v + 3) & ~1) + ((D.max_cb + 1) & ~1)) * sizeof(double) +
+    return (size_t)(kStage + nr * ((D.max_v + 3) & ~1) + ((D.max_cb + 1) & ~1)) * sizeof(double) +
            (((offs + 1) & ~1) + kMaxItemRows) * sizeof(int32_t);
 }
 inline size_t sweep_smem_upper(const tsb_ldlt_desc &D) {
@@ -299,9 +305,55 @@ __device__ __forceinline__ void item_gemv(const Item &it, const tsb_ldlt_tile *t
     }
 }
 
-__device__ __forceinline__ double lower_input(const SweepArgs &A, int row) {
-    const double v = __ldcg(A.in + (A.in_perm ? A.in_perm[row] : row));  // may be produced in-kernel (L2)
+__device__ __forceinline__ double lower_input(const SweepArgs &A, int row, int j = 0) {
+    const double v = __ldcg(A.in + j * A.ld + (A.in_perm ? A.in_perm[row] : row));  // may be produced in-kernel (L2)
     return A.ext ? v - __ldcg(A.ext + row) : v;
+}
+
+// item_gemv for nr right-hand sides (v_j = v + j * vstride): every tile read
+// once from the staged data per right-hand side; emit(row, j, value).
+template <class Emit>
+__device__ __forceinline__ void item_gemv_multi(const Item &it, const tsb_ldlt_tile *tiles, double *stage,
+                                                uint64_t *bars, uint32_t &phase, const double *v, int vstride, int nr,
+                                                double *red, double *part, int64_t ld_part, int32_t *tcnt,
+                                                const Emit &emit) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    mbar_wait(&bars[0], phase & 1u);
+    phase ^= 1u;
+    if (it.seg == 0) {
+        const int64_t off0 = tiles[it.t0].off;
+        for (int t = it.t0 + warp; t < it.t1; t += kWarps) {
+            const tsb_ldlt_tile T = tiles[t];
+            for (int j = 0; j < nr; ++j) {
+                const double a = tile_dot(stage + (T.off - off0), v + j * vstride + T.tl, 0, T.np, 1, lane);
+                if (lane < T.nrows) emit(T.row0 + lane, j, a);
+            }
+        }
+        return;
+    }
+    __shared__ int last_seg_m;
+    const tsb_ldlt_tile T = tiles[it.t0];
+    const int s = it.seg - 1, p0 = s * kSegPairs, cnt = min(kSegPairs, T.np - p0);
+    for (int j = 0; j < nr; ++j) {
+        red[warp * 32 + lane] = tile_dot(stage, v + j * vstride + T.tl + 2 * p0, warp, cnt, kWarps, lane);
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            double a = 0.0;
+#pragma unroll
+            for (int w = 0; w < kWarps; ++w) a += red[w * 32 + threadIdx.x];
+            part[j * ld_part + ((int64_t)T.part + s) * kTile + threadIdx.x] = a;
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) last_seg_m = atom_add_acq_rel(tcnt + it.t0, 1) == T.nseg - 1;
+    __syncthreads();
+    if (last_seg_m && threadIdx.x < 32) {
+        for (int j = 0; j < nr; ++j) {
+            double a = 0.0;
+            for (int q = 0; q < T.nseg; ++q) a += __ldcg(part + j * ld_part + ((int64_t)T.part + q) * kTile + threadIdx.x);
+            if ((int)threadIdx.x < T.nrows) emit(T.row0 + threadIdx.x, j, a);
+        }
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -318,8 +370,9 @@ template <bool TRACE>
 __device__ __forceinline__ void lower_sweep_body(const tsb_ldlt_desc &D, const SweepArgs &A, double *smem,
                                                  uint64_t *bars, uint32_t &phase) {
     double *stage = smem;
-    double *xs = smem + kStage;                       // x_b over the item's window [w0, w1)
-    double *cbs = xs + ((D.max_v + 3) & ~1);
+    double *xs = smem + kStage;                       // x_b over the item's window [w0, w1) (nr windows)
+    const int nr = A.nr, xstride = (D.max_v + 3) & ~1;
+    double *cbs = xs + nr * xstride;
     int32_t *offs = reinterpret_cast<int32_t *>(cbs + ((D.max_cb + 1) & ~1));
     const int noffs = (D.max_v + 2 > kFinRows + 2 ? D.max_v + 2 : kFinRows + 2);
     int32_t *dsts = offs + ((noffs + 1) & ~1);
@@ -358,14 +411,16 @@ __device__ __forceinline__ void lower_sweep_body(const tsb_ldlt_desc &D, const S
                     i1 = lo;
                 }
                 const int cnt = (int)(__ldg(D.d_cin_ptr + s + i1) - qb);
-                const bool staged = cnt <= kStage;
+                const bool staged = cnt <= kStage && nr == 1;
                 if (staged) stage_copy(stage, D.d_cbuf + qb, cnt);
                 for (int i = i0 + tid; i <= i1; i += kSweepBlock) offs[i - i0] = (int32_t)(__ldg(D.d_cin_ptr + s + i) - qb);
                 __syncthreads();
                 for (int i = i0 + tid; i < i1; i += kSweepBlock)
-                    D.d_x[s + i] = lower_input(A, s + i) -
-                                   (staged ? contrib_sum<false>(stage, offs[i - i0], offs[i - i0 + 1])
-                                           : contrib_sum<true>(D.d_cbuf + qb, offs[i - i0], offs[i - i0 + 1]));
+                    for (int j = 0; j < nr; ++j)
+                        D.d_x[j * A.ld + s + i] =
+                            lower_input(A, s + i, j) -
+                            (staged ? contrib_sum<false>(stage, offs[i - i0], offs[i - i0 + 1])
+                                    : contrib_sum<true>(D.d_cbuf + j * A.ld_cb + qb, offs[i - i0], offs[i - i0 + 1]));
                 __syncthreads();
                 i0 = i1;
             }
@@ -383,13 +438,14 @@ __device__ __forceinline__ void lower_sweep_body(const tsb_ldlt_desc &D, const S
             struct In {
                 const SweepArgs &A;
                 double *xs;
-                int s;
-                __device__ double load(int j) const { return lower_input(A, s + j); }
+                int s, r;
+                __device__ double load(int j) const { return lower_input(A, s + j, r); }
                 __device__ void store(int j, double v) const { xs[j] = v; }
             };
-            if (B.mode != 2) batched(nw, In{A, xs, s + w0});  // mode 2: x_b comes from the finalisers
+            if (B.mode != 2)  // mode 2: x_b comes from the finalisers
+                for (int j = 0; j < nr; ++j) batched(nw, In{A, xs + j * xstride, s + w0, j});
         }
-        if (tid == 0) xs[nw] = 0.0;  // column pad of odd-width tiles
+        if (tid < nr) xs[tid * xstride + nw] = 0.0;  // column pad of odd-width tiles
         const tsb_ldlt_tile Tf = D.d_tiles_lower[it.t0], Tb = D.d_tiles_lower[it.t1 - 1];
         const int r_hi = Tb.row0 + Tb.nrows, mr0 = max(Tf.row0, m);
         for (int j = mr0 + tid; j < r_hi; j += kSweepBlock) dsts[j - mr0] = __ldg(D.d_cslot + B.anc_off + (j - m));
@@ -405,7 +461,11 @@ __device__ __forceinline__ void lower_sweep_body(const tsb_ldlt_desc &D, const S
         __syncthreads();
         trace(tbuf, iid, 1);
         // x_b = input - (contributions of the descendants) over the window
-        if (B.mode == 1) {  // rows in pieces whose contributions fit the buffer
+        if (B.mode == 1 && nr > 1) {  // several right-hand sides: sum straight from L2
+            for (int j = 0; j < nr; ++j)
+                for (int jj = tid; jj < nw; jj += kSweepBlock)
+                    xs[j * xstride + jj] -= contrib_sum<true>(D.d_cbuf + j * A.ld_cb + cb0, offs[jj], offs[jj + 1]);
+        } else if (B.mode == 1) {  // rows in pieces whose contributions fit the buffer
             int i0 = 0;
             while (i0 < nw) {
                 int i1 = nw;
@@ -434,11 +494,11 @@ __device__ __forceinline__ void lower_sweep_body(const tsb_ldlt_desc &D, const S
                 __device__ double load(int j) const { return __ldcg(src + j); }
                 __device__ void store(int j, double v) const { xs[j] = v; }
             };
-            batched(nw, Ld{D.d_x + s + w0, xs});
+            for (int j = 0; j < nr; ++j) batched(nw, Ld{D.d_x + j * A.ld + s + w0, xs + j * xstride});
         }
         __syncthreads();
         trace(tbuf, iid, 4);
-        {
+        if (nr == 1) {
             auto emit = [&](int r, double a) {
                 if (r < m)
                     A.x[s + r] = a;  // unit diagonal stored: y_r = sum_{j <= r} Linv_rj x_j
@@ -446,6 +506,15 @@ __device__ __forceinline__ void lower_sweep_body(const tsb_ldlt_desc &D, const S
                     D.d_cbuf[dsts[r - mr0]] = a;
             };
             item_gemv(it, D.d_tiles_lower, stage, bars, phase, xs - w0, red, D.d_part_lower, D.d_tcnt_lower, emit);
+        } else {
+            auto emit = [&](int r, int j, double a) {
+                if (r < m)
+                    A.x[j * A.ld + s + r] = a;
+                else
+                    D.d_cbuf[j * A.ld_cb + dsts[r - mr0]] = a;
+            };
+            item_gemv_multi(it, D.d_tiles_lower, stage, bars, phase, xs - w0, xstride, nr, red, D.d_part_lower,
+                            A.ld_part, D.d_tcnt_lower, emit);
         }
         trace(tbuf, iid, 5);
         __syncthreads();
