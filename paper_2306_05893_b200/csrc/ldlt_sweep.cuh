@@ -411,17 +411,19 @@ __device__ __forceinline__ void lower_sweep_body(const tsb_ldlt_desc &D, const S
                     i1 = lo;
                 }
                 const int cnt = (int)(__ldg(D.d_cin_ptr + s + i1) - qb);
-                const bool staged = cnt <= kStage && nr == 1;
-                if (staged) stage_copy(stage, D.d_cbuf + qb, cnt);
+                const bool staged = cnt <= kStage;
                 for (int i = i0 + tid; i <= i1; i += kSweepBlock) offs[i - i0] = (int32_t)(__ldg(D.d_cin_ptr + s + i) - qb);
-                __syncthreads();
-                for (int i = i0 + tid; i < i1; i += kSweepBlock)
-                    for (int j = 0; j < nr; ++j)
+                for (int j = 0; j < nr; ++j) {  // right-hand side j (nr > 1: multi-RHS sweep)
+                    const double *cbj = D.d_cbuf + j * A.ld_cb + qb;
+                    if (staged) stage_copy(stage, cbj, cnt);
+                    __syncthreads();
+                    for (int i = i0 + tid; i < i1; i += kSweepBlock)
                         D.d_x[j * A.ld + s + i] =
                             lower_input(A, s + i, j) -
                             (staged ? contrib_sum<false>(stage, offs[i - i0], offs[i - i0 + 1])
-                                    : contrib_sum<true>(D.d_cbuf + j * A.ld_cb + qb, offs[i - i0], offs[i - i0 + 1]));
-                __syncthreads();
+                                    : contrib_sum<true>(cbj, offs[i - i0], offs[i - i0 + 1]));
+                    __syncthreads();
+                }
                 i0 = i1;
             }
             if (tid == 0) atom_add_release(D.d_ready_l + it.block, 1);
@@ -461,31 +463,31 @@ __device__ __forceinline__ void lower_sweep_body(const tsb_ldlt_desc &D, const S
         __syncthreads();
         trace(tbuf, iid, 1);
         // x_b = input - (contributions of the descendants) over the window
-        if (B.mode == 1 && nr > 1) {  // several right-hand sides: sum straight from L2
-            for (int j = 0; j < nr; ++j)
-                for (int jj = tid; jj < nw; jj += kSweepBlock)
-                    xs[j * xstride + jj] -= contrib_sum<true>(D.d_cbuf + j * A.ld_cb + cb0, offs[jj], offs[jj + 1]);
-        } else if (B.mode == 1) {  // rows in pieces whose contributions fit the buffer
-            int i0 = 0;
-            while (i0 < nw) {
-                int i1 = nw;
-                if (offs[nw] - offs[i0] > D.max_cb) {
-                    int lo = i0 + 1, hi = nw;
-                    while (lo < hi) {
-                        const int mid = (lo + hi + 1) >> 1;
-                        if (offs[mid] - offs[i0] <= D.max_cb) lo = mid; else hi = mid - 1;
+        if (B.mode == 1) {  // rows in pieces whose contributions fit the buffer, per right-hand side
+            for (int j = 0; j < nr; ++j) {
+                double *xj = xs + j * xstride;
+                const double *cbj = D.d_cbuf + j * A.ld_cb + cb0;
+                int i0 = 0;
+                while (i0 < nw) {
+                    int i1 = nw;
+                    if (offs[nw] - offs[i0] > D.max_cb) {
+                        int lo = i0 + 1, hi = nw;
+                        while (lo < hi) {
+                            const int mid = (lo + hi + 1) >> 1;
+                            if (offs[mid] - offs[i0] <= D.max_cb) lo = mid; else hi = mid - 1;
+                        }
+                        i1 = lo;
                     }
-                    i1 = lo;
+                    const int base = offs[i0], cnt = offs[i1] - base;
+                    const bool fits = cnt <= D.max_cb;
+                    if (fits) stage_copy(cbs, cbj + base, cnt);
+                    __syncthreads();
+                    for (int jj = i0 + tid; jj < i1; jj += kSweepBlock)
+                        xj[jj] = xj[jj] - (fits ? contrib_sum<false>(cbs, offs[jj] - base, offs[jj + 1] - base)
+                                                : contrib_sum<true>(cbj, offs[jj], offs[jj + 1]));
+                    __syncthreads();
+                    i0 = i1;
                 }
-                const int base = offs[i0], cnt = offs[i1] - base;
-                const bool fits = cnt <= D.max_cb;
-                if (fits) stage_copy(cbs, D.d_cbuf + cb0 + base, cnt);
-                __syncthreads();
-                for (int j = i0 + tid; j < i1; j += kSweepBlock)
-                    xs[j] = xs[j] - (fits ? contrib_sum<false>(cbs, offs[j] - base, offs[j + 1] - base)
-                                          : contrib_sum<true>(D.d_cbuf + cb0, offs[j], offs[j + 1]));
-                __syncthreads();
-                i0 = i1;
             }
         } else if (B.mode == 2) {  // formed by the block's finaliser items
             struct Ld {
