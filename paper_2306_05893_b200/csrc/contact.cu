@@ -135,12 +135,18 @@ __global__ void jsym_kernel(int64_t m, int64_t n, const int64_t *__restrict__ in
 // Projected Gauss-Seidel (contact.py:128-166), one warp: row dot products
 // lane-strided with a fixed shuffle tree; lambda in shared memory.
 // info: [0] sweeps, [1] complementarity residual sum |lam (W lam - rhs)|, [2] dropped rows
-__global__ void __launch_bounds__(32) pgs_kernel(int64_t m, const double *__restrict__ W, const double *__restrict__ rhs,
+__global__ void __launch_bounds__(32) pgs_kernel(int64_t m, const double *W, const double *__restrict__ rhs,
                                                  const uint8_t *__restrict__ unilateral, double tol, int max_sweeps,
-                                                 double *__restrict__ lam_out, double *__restrict__ info) {
-    extern __shared__ double lam[];
+                                                 double *__restrict__ lam_out, double *__restrict__ info,
+                                                 bool W_in_smem) {
+    extern __shared__ double lam[];  // [m] multipliers, then W itself when it fits (row dots from smem)
     const int lane = threadIdx.x;
     for (int64_t i = lane; i < m; i += 32) lam[i] = 0.0;
+    double *Ws = lam + ((m + 1) & ~1);
+    if (W_in_smem) {
+        for (int64_t i = lane; i < m * m; i += 32) Ws[i] = W[i];
+        W = Ws;
+    }
     __syncwarp();
     int dropped = 0;
     for (int64_t i = 0; i < m; ++i) dropped += W[i * m + i] == 0.0;
@@ -270,14 +276,17 @@ extern "C" int tsb_pgs(int64_t m, const double *d_W, const double *d_rhs, const 
     using namespace tsb;
     return guard([&] {
         if (m <= 0) return;
-        const size_t smem = sizeof(double) * (size_t)m;
+        size_t smem = sizeof(double) * (size_t)((m + 1) & ~1);
         if (smem > 200 * 1024) throw Error(TSB_E_ARG, "too many constraints for the shared-memory PGS");
+        const bool w_smem = smem + sizeof(double) * (size_t)(m * m) <= 200 * 1024;
+        if (w_smem) smem += sizeof(double) * (size_t)(m * m);
         static bool once = [] {
             allow_max_smem(ct::pgs_kernel);
             return true;
         }();
         (void)once;
-        ct::pgs_kernel<<<1, 32, smem, as_stream(stream)>>>(m, d_W, d_rhs, d_unilateral, tol, max_sweeps, d_lam, d_info);
+        ct::pgs_kernel<<<1, 32, smem, as_stream(stream)>>>(m, d_W, d_rhs, d_unilateral, tol, max_sweeps, d_lam, d_info,
+                                                          w_smem);
         TSB_LAUNCHED();
     });
 }
