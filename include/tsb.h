@@ -372,8 +372,12 @@ enum {
     TSB_RF_TSCALE = 6,            /* same (right solve, column tile k)           */
     TSB_RF_TUPDATE = 7,           /* same                                        */
     TSB_RF_PACK = 8,              /* pack tiles + d                              */
-    TSB_RF_IDENT = 9              /* C^-1 buffers := I                           */
+    TSB_RF_IDENT = 9,             /* C^-1 buffers := I                           */
+    TSB_RF_RECORD = 10,           /* a: event id, recorded on the op's stream    */
+    TSB_RF_WAIT = 11              /* a: event id, waited for by the op's stream  */
 };
+/* op[5] selects the stream: 0 the caller's, 1 a side stream of the handle
+ * (the right solve of a finished tree height overlaps the next heights). */
 
 typedef struct tsb_refactor_desc {
     int64_t n_fronts;

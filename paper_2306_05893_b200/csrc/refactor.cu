@@ -21,6 +21,7 @@
 // the launch sequence is a host "program" planned once per pattern
 // (paper_2306_05893_b200/refactor.py).  All sums run in a fixed order: the
 // result is bit-reproducible run to run.
+#include <algorithm>
 #include <vector>
 
 #include "tsb_common.cuh"
@@ -407,6 +408,8 @@ __global__ void d_kernel(const tsb_front *__restrict__ F, const double *__restri
 struct tsb_refactor {
     tsb_refactor_desc d;
     std::vector<int64_t> prog;
+    cudaStream_t side = nullptr;
+    std::vector<cudaEvent_t> ev;  // [0] start, [1] side done, [2 + i] program events
 };
 
 extern "C" int tsb_refactor_create(const tsb_refactor_desc *desc, tsb_refactor_t *out) {
@@ -427,11 +430,22 @@ extern "C" int tsb_refactor_create(const tsb_refactor_desc *desc, tsb_refactor_t
         h->d = *desc;
         h->prog.assign(desc->h_prog, desc->h_prog + 8 * desc->n_prog);
         h->d.h_prog = nullptr;
+        int64_t nev = 0;
+        for (int64_t o = 0; o < desc->n_prog; ++o)
+            if (h->prog[8 * o] == TSB_RF_RECORD || h->prog[8 * o] == TSB_RF_WAIT)
+                nev = std::max<int64_t>(nev, h->prog[8 * o + 1] + 1);
+        TSB_CUDA(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
+        h->ev.resize(2 + nev);
+        for (auto &e : h->ev) TSB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         *out = h;
     });
 }
 
 extern "C" int tsb_refactor_destroy(tsb_refactor_t h) {
+    if (h != nullptr) {
+        for (auto e : h->ev) cudaEventDestroy(e);
+        if (h->side) cudaStreamDestroy(h->side);
+    }
     delete h;
     return TSB_OK;
 }
@@ -442,14 +456,23 @@ extern "C" int tsb_refactor_run(tsb_refactor_t h, const double *d_values, double
     using namespace tsb::rf;
     return guard([&] {
         if (h == nullptr) throw Error(TSB_E_ARG, "null refactor handle");
-        cudaStream_t s = as_stream(stream);
+        cudaStream_t s0 = as_stream(stream);
         const tsb_refactor_desc &D = h->d;
         const int4 *lists = reinterpret_cast<const int4 *>(D.d_lists);
-        TSB_CUDA(cudaMemsetAsync(D.d_ctl, 0, sizeof(int32_t), s));
+        TSB_CUDA(cudaMemsetAsync(D.d_ctl, 0, sizeof(int32_t), s0));
+        TSB_CUDA(cudaEventRecord(h->ev[0], s0));  // the side stream starts after the caller's prior work
+        TSB_CUDA(cudaStreamWaitEvent(h->side, h->ev[0], 0));
         for (int64_t o = 0; o < (int64_t)h->prog.size() / 8; ++o) {
             const int64_t *op = h->prog.data() + 8 * o;
             const int64_t a = op[1], b = op[2], c = op[3], dd = op[4];
+            cudaStream_t s = op[5] ? h->side : s0;
             switch (op[0]) {
+                case TSB_RF_RECORD:
+                    TSB_CUDA(cudaEventRecord(h->ev[2 + a], s));
+                    break;
+                case TSB_RF_WAIT:
+                    TSB_CUDA(cudaStreamWaitEvent(s, h->ev[2 + a], 0));
+                    break;
                 case TSB_RF_SCATTER: {
                     TSB_CUDA(cudaMemsetAsync(D.d_ws, 0, sizeof(double) * D.ws_size, s));
                     if (a > 0) {
@@ -527,5 +550,7 @@ extern "C" int tsb_refactor_run(tsb_refactor_t h, const double *d_values, double
                     throw Error(TSB_E_ARG, "unknown refactor op");
             }
         }
+        TSB_CUDA(cudaEventRecord(h->ev[1], h->side));  // everything on the side stream before the caller goes on
+        TSB_CUDA(cudaStreamWaitEvent(s0, h->ev[1], 0));
     });
 }

@@ -35,7 +35,9 @@ FRONT_DTYPE = np.dtype([("off", "<i8"), ("woff", "<i8"), ("ioff", "<i8"), ("m", 
 assert FRONT_DTYPE.itemsize == 48
 PAIR_DTYPE = np.dtype([("child", "<i4"), ("parent", "<i4"), ("tp_off", "<i8")])
 assert PAIR_DTYPE.itemsize == 16
-OP_SCATTER, OP_EXTEND, OP_DIAG, OP_PANEL, OP_UPDATE, OP_TSCALE, OP_TUPDATE, OP_PACK, OP_IDENT = range(1, 10)
+OP_SCATTER, OP_EXTEND, OP_DIAG, OP_PANEL, OP_UPDATE, OP_TSCALE, OP_TUPDATE, OP_PACK, OP_IDENT, OP_RECORD, OP_WAIT = \
+    range(1, 12)
+SIDE = 1  # op[5]: the handle's side stream
 
 
 class _StructBlock:
@@ -122,8 +124,10 @@ def plan_refactor(symbolic, plan) -> RefactorPlan:
     prog, lists, pairs, tps = [], [], [], []
     tp_pos = 0
 
-    def op(*a):
-        prog.append(list(a) + [0] * (8 - len(a)))
+    def op(*a, stream=0):
+        row = list(a) + [0] * (8 - len(a))
+        row[5] = stream
+        prog.append(row)
 
     def add_list(entries):
         o = len(lists)
@@ -163,21 +167,27 @@ def plan_refactor(symbolic, plan) -> RefactorPlan:
             op(OP_DIAG, k, lo, len(act))
             op(OP_PANEL, k, lo, len(act), pp)
             op(OP_UPDATE, k, lo, len(act), uu)
+        # right solve of this height on the side stream (it only touches the
+        # fronts' L21 / C^-1 parts, never the update matrices the parents read)
+        if len(at):
+            op(OP_RECORD, h)
+            op(OP_WAIT, h, stream=SIDE)
+            for k in range(kmax - 1, -1, -1):
+                act = [int(i) for i in at if P[i] > k]
+                ent, ss, uu = [], 0, 0
+                for i in act:
+                    rows = int(P[i]) - k + (int(na[i]) + NB - 1) // NB
+                    ent.append((i, ss, uu, 0))
+                    ss += rows
+                    uu += rows * k
+                lo = add_list(ent)
+                op(OP_TSCALE, k, lo, len(act), ss, stream=SIDE)
+                op(OP_TUPDATE, k, lo, len(act), uu, stream=SIDE)
     for i in range(nb):  # partial Cholesky + U + right solve (FMA = 2 flops)
         mi, ai = float(m[i]), float(na[i])
         flops += mi ** 3 / 3 + mi * mi * ai + mi * ai * ai + mi ** 3 / 3 + ai * mi * mi
-    kmax = int(P.max()) if nb else 0
-    for k in range(kmax - 1, -1, -1):
-        act = [int(i) for i in range(nb) if P[i] > k]
-        ent, ss, uu = [], 0, 0
-        for i in act:
-            rows = int(P[i]) - k + (int(na[i]) + NB - 1) // NB
-            ent.append((i, ss, uu, 0))
-            ss += rows
-            uu += rows * k
-        lo = add_list(ent)
-        op(OP_TSCALE, k, lo, len(act), ss)
-        op(OP_TUPDATE, k, lo, len(act), uu)
+    op(OP_RECORD, H, stream=SIDE)
+    op(OP_WAIT, H)
     op(OP_PACK)
 
     pair_arr = np.zeros(len(pairs), dtype=PAIR_DTYPE)

@@ -56,6 +56,8 @@ def run(rp: R.RefactorPlan, values, tiles_l, tiles_u, tblk_l, tblk_u, n):
     bad = -1
     for op in rp.prog:
         kind, a, b, c, dd = (int(x) for x in op[:5])
+        if kind in (R.OP_RECORD, R.OP_WAIT):  # stream ordering: the emulator runs ops in program order
+            continue
         if kind == R.OP_SCATTER:
             ws[:] = 0.0
             ws[rp.sc_dst] = values[rp.sc_src]
