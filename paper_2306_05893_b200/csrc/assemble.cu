@@ -6,20 +6,21 @@
 //   polar_rotations                             models.py:174-189
 //   MatrixAssembler.finish -> compress          assembly.py:407-419, 332-343
 //
-// Three kernels, no atomics, fixed summation order:
+// Two launches, no atomics, fixed summation order (the block and node gathers
+// share one launch, gather_kernel):
 //   1. elem_kernel   one thread per tetrahedron: F = sum_a x_a g_a^T, Newton
 //                    polar R <- (R + R^-T)/2, rotated gradients g^_a = R g_a,
 //                    f_e = R Ke (R^T x - x0) and (K v)_e = R Ke R^T v in
 //                    stress form (no 12x12 Ke is ever read: 104 B of rest data
 //                    per tet instead of 1,152 B).
-//   2. block_kernel  one thread per 3x3 node block of the CSR pattern: sums
+//   2. gather_kernel (block part) one thread per 3x3 node block of the CSR pattern: sums
 //                    cm*mass (diagonal blocks) then ck*(R Ke R^T)_ab over the
 //                    contributing elements in ascending element order -- the
 //                    ascending-triplet order np.bincount uses
 //                    (assembly.py:341), so slot sums follow the reference's
 //                    association exactly.  Block entry (i,j) of element e:
 //                    V (lam g^_a,i g^_b,j + mu g^_a,j g^_b,i + mu (g_a.g_b) d_ij)
-//   3. node_kernel   one thread per node: f_int and K v gathered over incident
+//   3. gather_kernel (node part) one thread per node: f_int and K v gathered over incident
 //                    elements in ascending order (np.bincount order,
 //                    models.py:192-193), then
 //                    b = f_ext - f_int - (h+beta) K v - alpha M v, b[pinned]=0
@@ -305,12 +306,11 @@ __device__ __forceinline__ void load_aux(const double *__restrict__ work, int64_
 }
 
 template <bool STVK>
-__global__ void __launch_bounds__(256)
-block_kernel(int64_t nb, int64_t m, const int4 *__restrict__ blk, const int32_t *__restrict__ list,
-             const double *__restrict__ work, const double *__restrict__ grads,
-             const double *__restrict__ vol, const double *__restrict__ share, double lam,
-             double mu, double cm, double ck, double *__restrict__ values) {
-    const int64_t bi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+__device__ __forceinline__ void block_body(int64_t bi, int64_t nb, int64_t m, const int4 *__restrict__ blk,
+                                           const int32_t *__restrict__ list, const double *__restrict__ work,
+                                           const double *__restrict__ grads, const double *__restrict__ vol,
+                                           const double *__restrict__ share, double lam, double mu, double cm,
+                                           double ck, double *__restrict__ values) {
     if (bi >= nb) return;
     const int4 info = __ldg(blk + bi);  // slot0, rowlen, begin, end
     double acc[9];
@@ -369,15 +369,14 @@ block_kernel(int64_t nb, int64_t m, const int4 *__restrict__ blk, const int32_t 
         for (int j = 0; j < 3; ++j) values[info.x + i * info.y + j] = acc[3 * i + j];
 }
 
-__global__ void __launch_bounds__(256)
-node_kernel(int64_t N, const int32_t *__restrict__ node_ptr, const int32_t *__restrict__ node_list,
-            const double *__restrict__ work, const double *__restrict__ x,
-            const double *__restrict__ v, const double *__restrict__ fext_state,
-            const double *__restrict__ gravity, const double *__restrict__ mass_diag,
-            const uint8_t *__restrict__ fixed, double hb, double alpha,
-            double *__restrict__ f_int, double *__restrict__ kv, double *__restrict__ b,
-            double *__restrict__ f_ext, int32_t *__restrict__ flags) {
-    const int64_t I = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+__device__ __forceinline__ void node_body(int64_t I, int64_t N, const int32_t *__restrict__ node_ptr,
+                                          const int32_t *__restrict__ node_list, const double *__restrict__ work,
+                                          const double *__restrict__ x, const double *__restrict__ v,
+                                          const double *__restrict__ fext_state, const double *__restrict__ gravity,
+                                          const double *__restrict__ mass_diag, const uint8_t *__restrict__ fixed,
+                                          double hb, double alpha, double *__restrict__ f_int,
+                                          double *__restrict__ kv, double *__restrict__ b,
+                                          double *__restrict__ f_ext, int32_t *__restrict__ flags) {
     if (I >= N) return;
     if (!finite3(x[3 * I], x[3 * I + 1], x[3 * I + 2])) atomicOr(flags, 1);
     double f[3] = {0.0, 0.0, 0.0}, k[3] = {0.0, 0.0, 0.0};
@@ -422,6 +421,30 @@ node_kernel(int64_t N, const int32_t *__restrict__ node_ptr, const int32_t *__re
             if (f_ext != nullptr) f_ext[d] = fe;
         }
     }
+}
+
+// One launch for both gathers: the first CTAs gather the nodes' f_int / K v /
+// rhs (thread per node), the rest sum the 3x3 blocks (thread per block); the
+// two are independent, so the small node gather overlaps the block gather
+// instead of running after it.
+template <bool STVK>
+__global__ void __launch_bounds__(256)
+gather_kernel(int64_t nbc, int64_t nb, int64_t m, const int4 *__restrict__ blk, const int32_t *__restrict__ list,
+              const double *__restrict__ work, const double *__restrict__ grads, const double *__restrict__ vol,
+              const double *__restrict__ share, double lam, double mu, double cm, double ck,
+              double *__restrict__ values, int64_t N, const int32_t *__restrict__ node_ptr,
+              const int32_t *__restrict__ node_list, const double *__restrict__ x, const double *__restrict__ v,
+              const double *__restrict__ fext_state, const double *__restrict__ gravity,
+              const double *__restrict__ mass_diag, const uint8_t *__restrict__ fixed, double hb, double alpha,
+              double *__restrict__ f_int, double *__restrict__ kv, double *__restrict__ b,
+              double *__restrict__ f_ext, int32_t *__restrict__ flags) {
+    const int64_t nnc = (N + blockDim.x - 1) / blockDim.x;  // node CTAs first: their chains are the longest
+    if ((int64_t)blockIdx.x < nnc)
+        node_body(blockIdx.x * (int64_t)blockDim.x + threadIdx.x, N, node_ptr, node_list, work, x, v, fext_state,
+                  gravity, mass_diag, fixed, hb, alpha, f_int, kv, b, f_ext, flags);
+    else
+        block_body<STVK>((blockIdx.x - nnc) * (int64_t)blockDim.x + threadIdx.x, nb, m, blk, list, work, grads, vol,
+                         share, lam, mu, cm, ck, values);
 }
 
 __global__ void __launch_bounds__(128)
@@ -503,25 +526,22 @@ extern "C" int tsb_assemble_corot(const tsb_asm_plan *p, const tsb_asm_coeffs *c
         if (c->law < TSB_LAW_COROTATIONAL || c->law > TSB_LAW_STVK) throw Error(TSB_E_ARG, "unknown material law");
         cudaStream_t s = as_stream(stream);
         launch_elem(p, c, d_x, d_v, s);
-        if (c->want_matrix && d_values != nullptr) {
-            if (p->n_blocks > 0) {
-                auto kern = c->law == TSB_LAW_STVK ? block_kernel<true> : block_kernel<false>;
-                kern<<<grid_for(p->n_blocks, 256), 256, 0, s>>>(
-                    p->n_blocks, p->n_elems, reinterpret_cast<const int4 *>(p->d_blk), p->d_blk_list, p->d_work,
-                    p->d_grads, p->d_vol, p->d_mass_share, c->lam, c->mu, c->cm, c->ck, d_values);
-                TSB_LAUNCHED();
-            }
-            if (p->n_fixed_slots > 0) {
-                set_ones_kernel<<<grid_for(p->n_fixed_slots, 256), 256, 0, s>>>(p->n_fixed_slots,
-                                                                                p->d_fixed_slots, d_values);
-                TSB_LAUNCHED();
-            }
+        const bool mat = c->want_matrix && d_values != nullptr;
+        const int64_t nbc = mat && p->n_blocks > 0 ? grid_for(p->n_blocks, 256) : 0;
+        const int64_t nnc = p->n_nodes > 0 ? grid_for(p->n_nodes, 256) : 0;
+        if (nbc + nnc > 0) {
+            auto kern = c->law == TSB_LAW_STVK ? gather_kernel<true> : gather_kernel<false>;
+            kern<<<(unsigned)(nbc + nnc), 256, 0, s>>>(
+                nbc, p->n_blocks, p->n_elems, reinterpret_cast<const int4 *>(p->d_blk), p->d_blk_list, p->d_work,
+                p->d_grads, p->d_vol, p->d_mass_share, c->lam, c->mu, c->cm, c->ck, d_values, p->n_nodes,
+                p->d_node_ptr, p->d_node_list, d_x, d_v, d_f_ext_state, p->d_gravity, p->d_mass_diag,
+                p->d_fixed_dof, c->h + c->rayleigh_stiffness, c->rayleigh_mass, d_f_int, d_kv, d_b, d_f_ext,
+                p->d_flags);
+            TSB_LAUNCHED();
         }
-        if (p->n_nodes > 0) {
-            node_kernel<<<grid_for(p->n_nodes, 256), 256, 0, s>>>(
-                p->n_nodes, p->d_node_ptr, p->d_node_list, p->d_work, d_x, d_v, d_f_ext_state,
-                p->d_gravity, p->d_mass_diag, p->d_fixed_dof, c->h + c->rayleigh_stiffness,
-                c->rayleigh_mass, d_f_int, d_kv, d_b, d_f_ext, p->d_flags);
+        if (mat && p->n_fixed_slots > 0) {
+            set_ones_kernel<<<grid_for(p->n_fixed_slots, 256), 256, 0, s>>>(p->n_fixed_slots, p->d_fixed_slots,
+                                                                            d_values);
             TSB_LAUNCHED();
         }
     });

@@ -7,7 +7,7 @@ set -u
 TAG=${1:-r1}
 WL=${2:-cfg2}
 shift 2 || true
-KERNELS=${*:-"pcg_persistent<(int)2>:8 pcg_persistent<(int)1>:8 lower_sweep:3 upper_sweep:3 elem_kernel:10 block_kernel:10 node_kernel:10 spmv_kernel:3"}
+KERNELS=${*:-"pcg_persistent<(int)2>:8 pcg_persistent<(int)1>:8 lower_sweep:3 upper_sweep:3 elem_kernel:10 gather_kernel:10 spmv_kernel:3"}
 OUT=gpurun_out/ncu_${TAG}_${WL}
 mkdir -p "$OUT"
 CMD="python bench.py --workload $WL --steps 3 --warmup 3 --no-cpu-baseline"
