@@ -245,7 +245,6 @@ class AssemblyPlan:
         f = t.empty(n, dtype=t.float64, device="cuda")
         kv = t.empty(n, dtype=t.float64, device="cuda")
         co = self.coeffs(law=law, want_matrix=False)
-        self.flags.zero_()
         vz = v if v is not None else t.zeros(n, dtype=t.float64, device="cuda")
         self.run(co, x, vz, None, None, None, f, kv, None)
         kb = None

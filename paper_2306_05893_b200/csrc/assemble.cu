@@ -525,6 +525,7 @@ extern "C" int tsb_assemble_corot(const tsb_asm_plan *p, const tsb_asm_coeffs *c
         if (p == nullptr || c == nullptr) throw Error(TSB_E_ARG, "null plan/coeffs");
         if (c->law < TSB_LAW_COROTATIONAL || c->law > TSB_LAW_STVK) throw Error(TSB_E_ARG, "unknown material law");
         cudaStream_t s = as_stream(stream);
+        TSB_CUDA(cudaMemsetAsync(p->d_flags, 0, 4 * sizeof(int32_t), s));  // status words of this pass
         launch_elem(p, c, d_x, d_v, s);
         const bool mat = c->want_matrix && d_values != nullptr;
         const int64_t nbc = mat && p->n_blocks > 0 ? grid_for(p->n_blocks, 256) : 0;

@@ -197,24 +197,30 @@ class BackwardEulerIntegrator:
         return rebuilt
 
     # -- device core ------------------------------------------------------
-    def _assemble_device(self, x, v, f_ext_state):
-        """Enqueue the fused assembly; returns (A, b, f_int, f_ext, rebuilt) as device objects."""
+    def _assemble_device(self, x, v, f_ext_state, outs=None):
+        """Enqueue the fused assembly; returns (A, b, f_int, f_ext, rebuilt) as device objects
+        (`outs` = preallocated (b, f_int, f_ext) device views, else fresh tensors)."""
         t = _lib.torch()
         rebuilt = self._ensure_plan()
         plan = self._plan
         pat = self.assembler.pattern
         n = self.mesh.ndof
         cfg = self.config
-        cm, ck = self._coefficients()
-        co = plan.coeffs(h=cfg.dt, beta=cfg.rayleigh_stiffness, alpha=cfg.rayleigh_mass, cm=cm, ck=ck,
-                         law=self._law, want_matrix=True)
-        values = t.empty(len(pat["col_ind"]), dtype=t.float64, device="cuda")
-        b = t.empty(n, dtype=t.float64, device="cuda")
-        f_int = t.empty(n, dtype=t.float64, device="cuda")
-        kv = t.empty(n, dtype=t.float64, device="cuda")
-        f_ext = t.empty(n, dtype=t.float64, device="cuda")
-        plan.flags.zero_()
-        plan.run(co, x, v, f_ext_state, values, b, f_int, kv, f_ext)
+        key = (cfg.dt, cfg.rayleigh_stiffness, cfg.rayleigh_mass, self._law)
+        co = self._co.get(key) if hasattr(self, "_co") else None
+        if co is None:  # per-step coefficients (integrator.py:135-143), built once per config
+            cm, ck = self._coefficients()
+            co = plan.coeffs(h=cfg.dt, beta=cfg.rayleigh_stiffness, alpha=cfg.rayleigh_mass, cm=cm, ck=ck,
+                             law=self._law, want_matrix=True)
+            self._co = {key: co}
+        nnz = len(pat["col_ind"])
+        buf = t.empty(nnz + (n if outs is not None else 4 * n), dtype=t.float64, device="cuda")  # one allocation
+        values, kv = buf[:nnz], buf[nnz:nnz + n]
+        if outs is not None:
+            b, f_int, f_ext = outs
+        else:
+            b, f_int, f_ext = buf[nnz + n:nnz + 2 * n], buf[nnz + 2 * n:nnz + 3 * n], buf[nnz + 3 * n:]
+        plan.run(co, x, v, f_ext_state, values, b, f_int, kv, f_ext)  # zeroes the status words first
         a = CsrMatrix(n, n, pat["row_ptr"], pat["col_ind"], values)
         return a, b, f_int, f_ext, rebuilt
 
@@ -258,28 +264,49 @@ class BackwardEulerIntegrator:
         cfg = self.config
         h = cfg.dt
         host = not state.on_device
-        x0 = self._flat_dev(state.positions)
-        v0 = self._flat_dev(state.velocities)
-        fe_state = self._flat_dev(state.f_ext)
         n = self.mesh.ndof
+        stage = None
+        if host:  # one pinned H2D of (x, v, f_ext), one D2H of the six results
+            stage = self._host_stage(n)
+            hin = stage["h_in"].numpy()
+            np.copyto(hin[:n], np.asarray(state.positions, dtype=np.float64).reshape(-1))
+            np.copyto(hin[n:2 * n], np.asarray(state.velocities, dtype=np.float64).reshape(-1))
+            np.copyto(hin[2 * n:], np.asarray(state.f_ext, dtype=np.float64).reshape(-1))
+            d_in = stage["d_in"]
+            d_in.copy_(stage["h_in"], non_blocking=True)
+            x0, v0, fe_state = d_in[:n], d_in[n:2 * n], d_in[2 * n:]
+        else:
+            x0 = self._flat_dev(state.positions)
+            v0 = self._flat_dev(state.velocities)
+            fe_state = self._flat_dev(state.f_ext)
         dev_solve = bool(getattr(solve, "accepts_device", False))
-        ev = [t.cuda.Event(enable_timing=True) for _ in range(3)]
+        ev = getattr(self, "_ev", None)
+        if ev is None:
+            ev = self._ev = [t.cuda.Event(enable_timing=True) for _ in range(3)]
         assembly_time = solve_time = 0.0
         rebuilt_any = False
         x_tr, v_tr = x0, v0
         fixed = self._plan.fixed_dof if self._plan is not None else None
         for _ in range(cfg.newton_iterations):
             ev[0].record()
-            a, b, f_int, f_ext, rebuilt = self._assemble_device(x_tr, v_tr, fe_state)
+            d_out = stage["d_out"] if host else None
+            a, b, f_int, f_ext, rebuilt = self._assemble_device(
+                x_tr, v_tr, fe_state, None if d_out is None else (d_out[3 * n:4 * n], d_out[4 * n:5 * n],
+                                                                  d_out[5 * n:]))
             fixed = self._plan.fixed_dof
             ev[1].record()
             rebuilt_any = rebuilt_any or rebuilt
             accel, report = solve(a, b if dev_solve else b.cpu().numpy())
             ev[2].record()
             d_acc = self._flat_dev(accel)
-            acc = t.empty(n, dtype=t.float64, device="cuda")
-            v1 = t.empty(n, dtype=t.float64, device="cuda")
-            x1 = t.empty(n, dtype=t.float64, device="cuda")
+            if host:  # results land in the staging buffer: [x1 | v1 | acc | b | f_int | f_ext]
+                x1, v1, acc = (d_out[k * n:(k + 1) * n] for k in range(3))
+                if d_acc.data_ptr() == acc.data_ptr():
+                    d_acc = d_acc.clone()
+            else:
+                acc = t.empty(n, dtype=t.float64, device="cuda")
+                v1 = t.empty(n, dtype=t.float64, device="cuda")
+                x1 = t.empty(n, dtype=t.float64, device="cuda")
             P = _lib.ptr
             _lib.check(_lib.load().tsb_advance(n, P(d_acc), P(v0), P(x0), P(fixed), h, P(acc), P(v1),
                                                P(x1), P(self._plan.flags), _lib.stream_ptr()), "advance")
@@ -296,15 +323,31 @@ class BackwardEulerIntegrator:
                 raise StepError("solver produced non-finite accelerations", report)
             x_tr, v_tr = x1, v1
         if host:
-            out = lambda a_: a_.cpu().numpy()  # noqa: E731
-            pos, vel, acc_o = out(x_tr).reshape(-1, 3), out(v_tr).reshape(-1, 3), out(acc).reshape(-1, 3)
-            f_int_o, f_ext_o = out(f_int), out(f_ext)
-            rhs = out(b)
+            h_out = stage["h_out"]
+            h_out.copy_(stage["d_out"], non_blocking=True)
+            t.cuda.current_stream().synchronize()
+            o = h_out.numpy()
+            part = lambda k: o[k * n:(k + 1) * n].copy()  # noqa: E731  (caller-owned arrays)
+            pos, vel, acc_o = part(0).reshape(-1, 3), part(1).reshape(-1, 3), part(2).reshape(-1, 3)
+            rhs, f_int_o, f_ext_o = part(3), part(4), part(5)
         else:
             pos, vel, acc_o = x_tr.view(-1, 3), v_tr.view(-1, 3), acc.view(-1, 3)
             f_int_o, f_ext_o, rhs = f_int, f_ext, b
         return StepResult(pos, vel, acc_o, f_int_o, f_ext_o, a, rhs, report, rebuilt_any,
                           assembly_time, solve_time)
+
+    def _host_stage(self, n):
+        """Pinned host / device staging of a host-state step (allocated once)."""
+        st = getattr(self, "_stage", None)
+        if st is None or st["n"] != n:
+            t = _lib.torch()
+            st = {"n": n,
+                  "h_in": t.empty(3 * n, dtype=t.float64).pin_memory(),
+                  "d_in": t.empty(3 * n, dtype=t.float64, device="cuda"),
+                  "h_out": t.empty(6 * n, dtype=t.float64).pin_memory(),
+                  "d_out": t.empty(6 * n, dtype=t.float64, device="cuda")}
+            self._stage = st
+        return st
 
     def commit(self, state: SimState, result: StepResult):
         state.positions = result.positions
