@@ -258,7 +258,8 @@ int tsb_ldlt_lower(tsb_ldlt_t h, const double *d_r, double *d_y, void *stream);
 int tsb_ldlt_upper(tsb_ldlt_t h, const double *d_w, double *d_z, void *stream);
 /* z = P^T L^{-T} D^{-1} L^{-1} P r, original order     (apply)       */
 int tsb_ldlt_apply(tsb_ldlt_t h, const double *d_r, double *d_z, void *stream);
-/* Multi-RHS lower sweep (contact compliance columns): y_j = L^{-1} r_j for nr
+/* Multi-RHS lower sweep (the compliance columns of build_compliance,
+ * contact.py:109-125): y_j = L^{-1} r_j for nr
  * right-hand sides [nr][n] (permuted order) in one pass over the factor;
  * scratch cbuf [nr][ld_cb], x [nr][n], part [nr][ld_part]. */
 int tsb_ldlt_lower_multi(tsb_ldlt_t h, int32_t nr, const double *d_r, double *d_y, double *d_cbuf, int64_t ld_cb,

@@ -40,3 +40,9 @@ def test_struct_layouts_match_the_header():
     assert lib.tsb_struct_size(3) == _lib.C.sizeof(_lib.LdltDesc)
     assert lib.tsb_struct_size(4) == _lib.C.sizeof(_lib.Report)
     assert lib.tsb_struct_size(5) == _ldlt_pack.TILE_DTYPE.itemsize
+    from paper_2306_05893_b200 import refactor
+
+    assert lib.tsb_struct_size(6) == refactor.FRONT_DTYPE.itemsize
+    assert lib.tsb_struct_size(7) == refactor.PAIR_DTYPE.itemsize
+    assert lib.tsb_struct_size(8) == _lib.C.sizeof(_lib.RefactorDesc)
+    assert lib.tsb_struct_size(9) == _lib.C.sizeof(_lib.PatternDesc)
