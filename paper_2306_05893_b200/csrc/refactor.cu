@@ -15,9 +15,9 @@
 // G = [Linv; M] with Linv = diag(C) C^-1 (unit diagonal stored as 1.0) into
 // the tiles of the handle (d_g lower rows, d_gt upper rows) and d = diag(C)^2.
 //
-// Every op is a batch of 64 x 64 x 64 fp64 tile products (one CTA each,
-// 256 threads x 4 x 4 register tile) over all fronts of a height: the work is
-// dense FP64 (DFMA-bound; B200 FP64 DMMA is no faster than DFMA, measured),
+// Every op is a batch of 64 x 64 x 64 fp64 tile products (one CTA each, 8
+// warps x 32 x 16 on the FP64 tensor path, mma.sync m8n8k4) over all fronts
+// of a height: the work is dense FP64,
 // the launch sequence is a host "program" planned once per pattern
 // (paper_2306_05893_b200/refactor.py).  All sums run in a fixed order: the
 // result is bit-reproducible run to run.
@@ -82,25 +82,44 @@ __device__ __forceinline__ void load_t(double *dst, const double *src, int64_t l
     }
 }
 
-// acc[a][b] = sum_q As[q][tx + 16 a] * Bs[q][4 ty + b]
+// 64 x 64 tile product on the FP64 tensor path (mma.sync m8n8k4 f64, DMMA):
+// warp w owns rows (w & 1) * 32 + [0, 32) and columns (w >> 1) * 16 + [0, 16)
+// as 4 x 2 tiles of 8 x 8; per k-step of 4 a lane loads one A element per
+// row tile and one B element per column tile (fragment layout of m8n8k4:
+// A (groupID, threadID_in_group), B (threadID_in_group, groupID), C
+// (groupID, 2 threadID_in_group + i)).  acc[a][2 nt + i] is element
+// acc_rc(a, 2 nt + i).
+__device__ __forceinline__ void acc_rc(int a, int b, int &r, int &c) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    r = (w & 1) * 32 + a * 8 + (lane >> 2);
+    c = (w >> 1) * 16 + (b >> 1) * 8 + (lane & 3) * 2 + (b & 1);
+}
+
+// acc(r, c) = sum_q As[q][r] * Bs[q][c]
 __device__ __forceinline__ void tile_mma(const double *As, const double *Bs, int K, double acc[4][4]) {
-    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int gid = lane >> 2, tig = lane & 3;
+    const int r0 = (w & 1) * 32 + gid, c0 = (w >> 1) * 16 + gid;
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
         for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+    const int ks_end = (K + 3) >> 2;
 #pragma unroll 4
-    for (int q = 0; q < K; ++q) {
-        const double *ar = As + q * LDS + tx;
-        const double2 b0 = *reinterpret_cast<const double2 *>(Bs + q * LDS + 4 * ty);
-        const double2 b1 = *reinterpret_cast<const double2 *>(Bs + q * LDS + 4 * ty + 2);
-        const double bv[4] = {b0.x, b0.y, b1.x, b1.y};
+    for (int ks = 0; ks < ks_end; ++ks) {
+        const int q = ks * 4 + tig;
+        double av[4], bv[2];
 #pragma unroll
-        for (int a = 0; a < 4; ++a) {
-            const double av = ar[16 * a];
+        for (int a = 0; a < 4; ++a) av[a] = As[q * LDS + r0 + a * 8];
 #pragma unroll
-            for (int b = 0; b < 4; ++b) acc[a][b] = fma(av, bv[b], acc[a][b]);
-        }
+        for (int nt = 0; nt < 2; ++nt) bv[nt] = Bs[q * LDS + c0 + nt * 8];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt)
+                asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                             : "+d"(acc[a][2 * nt]), "+d"(acc[a][2 * nt + 1])
+                             : "d"(av[a]), "d"(bv[nt]));
     }
 }
 
@@ -108,21 +127,22 @@ __device__ __forceinline__ void tile_mma(const double *As, const double *Bs, int
 // The read-modify-write issues all 16 loads before the first store.
 template <int MODE>
 __device__ __forceinline__ void store_tile(double *dst, int64_t ld, int rows, int cols, const double acc[4][4]) {
-    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
     double old[4][4];
 #pragma unroll
-    for (int b = 0; b < 4; ++b)
+    for (int a = 0; a < 4; ++a)
 #pragma unroll
-        for (int a = 0; a < 4; ++a) {
-            const int r = tx + 16 * a, c = 4 * ty + b;
+        for (int b = 0; b < 4; ++b) {
+            int r, c;
+            acc_rc(a, b, r, c);
             const bool ok = r < rows && c < cols && (MODE != 2 || r >= c);
             old[a][b] = (MODE != 0 && ok) ? __ldcg(dst + (int64_t)c * ld + r) : 0.0;
         }
 #pragma unroll
-    for (int b = 0; b < 4; ++b)
+    for (int a = 0; a < 4; ++a)
 #pragma unroll
-        for (int a = 0; a < 4; ++a) {
-            const int r = tx + 16 * a, c = 4 * ty + b;
+        for (int b = 0; b < 4; ++b) {
+            int r, c;
+            acc_rc(a, b, r, c);
             if (r >= rows || c >= cols || (MODE == 2 && r < c)) continue;
             dst[(int64_t)c * ld + r] = MODE == 0 ? acc[a][b] : old[a][b] - acc[a][b];
         }
