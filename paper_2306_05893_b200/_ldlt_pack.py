@@ -46,6 +46,7 @@ persistent kernel needs to be deadlock-free.
 from __future__ import annotations
 
 import ctypes as C
+import os
 
 import numpy as np
 
@@ -630,7 +631,7 @@ class DevicePanels:
               "apply": self._lib.tsb_ldlt_apply, "upper_scaled": self._lib.tsb_ldlt_upper_scaled}[mode]
         _lib.check(fn(self.h, _lib.ptr(r), _lib.ptr(out), _lib.stream_ptr()), f"ldlt_{mode}")
 
-    MULTI_RHS = 8  # right-hand sides per multi-RHS lower sweep
+    MULTI_RHS = int(os.environ.get("TSB_MULTI_RHS", "8"))  # right-hand sides per multi-RHS lower sweep
 
     def lower_multi(self, R, Y):
         """Y[j] = L^-1 R[j] (permuted order) for the rows of R ([k][n] CUDA

@@ -165,3 +165,35 @@ def test_multi_rhs_lower_sweep_equals_single(params, k):
         dev.run("lower", R[j], Y1[j])
     assert bool((Y == Y1).all())
     assert rel(Y[k - 1].cpu().numpy(), O.solve_lower(f, R[k - 1].cpu().numpy())) <= 1e-12
+
+
+@pytest.mark.parametrize("k,leaf", [(30, 8), (45, 40)])
+def test_device_factor_on_grid_laplacian(k, leaf):
+    """Non-mesh pattern (2D 5-point Laplacian + random SPD perturbation,
+    plan from graph_from_pattern as in the reference's random-SPD tests):
+    ragged blocks, several pivot tiles per front, multi-child separators."""
+    rng = np.random.default_rng(k)
+    n = k * k
+    rows, cols, vals = [], [], []
+    for i in range(k):
+        for j in range(k):
+            p = i * k + j
+            rows.append(p); cols.append(p); vals.append(4.5 + rng.random())
+            for di, dj in ((0, 1), (1, 0)):
+                if i + di < k and j + dj < k:
+                    q = (i + di) * k + (j + dj)
+                    w = -1.0 + 0.1 * rng.standard_normal()
+                    rows += [p, q]; cols += [q, p]; vals += [w, w]
+    rows, cols, vals = map(np.asarray, (rows, cols, vals))
+    o = np.lexsort((cols, rows))
+    rows, cols, vals = rows[o], cols[o], vals[o]
+    row_ptr = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(np.bincount(rows, minlength=n), out=row_ptr[1:])
+    a = CsrMatrix(n, n, row_ptr, cols.astype(np.int64), vals)
+    plan = ND.nested_dissection(ND.graph_from_pattern(a), leaf)
+    hf = ND.ldlt_factor(a, plan)
+    df = ND.ldlt_factor_device(a, plan)
+    r = rng.standard_normal(n)
+    assert rel(ND.apply(df, r), O.apply(hf, r)) <= 1e-12
+    assert rel(ND.apply(df, r), np.linalg.solve(a.to_dense(), r)) <= 1e-10
+    assert rel(df.to_host().d, hf.d) <= 1e-12
