@@ -19,7 +19,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib
-from ._plan import AssemblyPlan, device_topology_pattern, topology_pattern
+from ._plan import AssemblyPlan, device_topology_pattern
 from .assembly import CsrMatrix, build_pattern, TripletStream
 from .krylov import SolveReport
 from .mesh import Mesh
