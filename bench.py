@@ -97,17 +97,26 @@ class L2Flush:
         self.buf.zero_()
 
 
-def time_steps(W, mode, steps, warmup, flush):
+def time_steps(W, mode, steps, warmup, flush, graph=False):
+    """Device step time.  graph=True replays the step captured as one CUDA
+    graph (integrator.CapturedStep: the same kernels, no host work between
+    them); otherwise compute_step runs eagerly."""
     import gc
 
     import torch
     from paper_2306_05893_b200 import _lib
 
     integ, st, solve = W["integ"], W["state"], W["solvers"][mode]
+    step = integ.compute_step
+    per_replay = None
+    if graph:
+        cap = integ.capture(st, solve)
+        step = lambda s_, _solve: cap.replay(s_)  # noqa: E731
+        per_replay = cap.kernels
     gc.disable()  # collector runs between steps (outside the events), never inside one
     for _ in range(warmup):
         flush()
-        integ.compute_step(st, solve)
+        step(st, solve)
         gc.collect(0)
     torch.cuda.synchronize()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
@@ -120,9 +129,10 @@ def time_steps(W, mode, steps, warmup, flush):
         flush()
         l0 = _lib.launch_count()
         ev[k][0].record()
-        res = integ.compute_step(st, solve)
+        res = step(st, solve)
         ev[k][1].record()
-        launches += _lib.launch_count() - l0  # every libtsb kernel launch (the PCG solve is one)
+        # every libtsb kernel launch (the PCG solve is one); a graph replay runs the captured ones
+        launches += per_replay if per_replay is not None else _lib.launch_count() - l0
         iters.append(res.report.iterations)
         asm.append(res.assembly_time * 1e3)
         slv.append(res.solve_time * 1e3)
@@ -439,6 +449,7 @@ def main():
     ap.add_argument("--precond", default="ldlt", choices=["ldlt", "jacobi"])
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--eager", action="store_true", help="time compute_step eagerly instead of the captured graph")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -464,9 +475,10 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
-        main_r = time_steps(W, args.precond, args.steps, args.warmup, flush)
+        main_r = time_steps(W, args.precond, args.steps, args.warmup, flush, graph=not args.eager)
+    eager_r = time_steps(W, args.precond, max(10, args.steps // 4), 3, flush)
     other = "jacobi" if args.precond == "ldlt" else "ldlt"
-    other_r = time_steps(W, other, max(10, args.steps // 4), 3, flush)
+    other_r = time_steps(W, other, max(10, args.steps // 4), 3, flush, graph=not args.eager)
     torch.cuda.synchronize()
     t_local = torch.tensor([main_r["total_ms"]], dtype=torch.float64, device="cuda")
     if dist:
@@ -500,12 +512,13 @@ def main():
             "scenario_step": AT_STEP, "tol": TOL, "leaf": LEAF, "tile": TILE,
             "l2": "flushed (256 MB write) before every timed step", "parallelism": f"replicas x{world}",
         },
-        "iterations": main_r["iterations"], "assembly_ms": main_r["assembly_ms"], "pcg_ms": main_r["solve_ms"],
+        "iterations": main_r["iterations"], "assembly_ms": eager_r["assembly_ms"], "pcg_ms": eager_r["solve_ms"],
+        "step_mode": "eager compute_step" if args.eager else "CUDA graph replay of compute_step (CapturedStep)",
+        "eager_ms_per_step": eager_r["ms"],
         "step_ms": {"min": min(main_r["per_step"]), "median": statistics.median(main_r["per_step"]),
                     "max": max(main_r["per_step"]),
                     "argmax": int(max(range(len(main_r["per_step"])), key=lambda k: main_r["per_step"][k]))},
-        other: {"ms_per_step": other_r["ms"], "iterations": other_r["iterations"],
-                "assembly_ms": other_r["assembly_ms"], "pcg_ms": other_r["solve_ms"]},
+        other: {"ms_per_step": other_r["ms"], "iterations": other_r["iterations"]},
         "trisolve": {"apply_ms": apply_r["ms"], "gbs": apply_r["gbs"], "frac": apply_r["gbs"] / hbm,
                      "algorithmic_bytes": apply_r["bytes"], "stored_bytes": apply_r["stored_bytes"]},
         "spmv": {"ms": spmv_r["ms"], "gbs": spmv_r["gbs"], "frac": spmv_r["gbs"] / hbm},

@@ -336,6 +336,11 @@ class BackwardEulerIntegrator:
         return StepResult(pos, vel, acc_o, f_int_o, f_ext_o, a, rhs, report, rebuilt_any,
                           assembly_time, solve_time)
 
+    def capture(self, state: SimState, solve) -> "CapturedStep":
+        """The device step (assembly + device PCG + kinematic update) of
+        `state`'s shape captured once as a CUDA graph; see CapturedStep."""
+        return CapturedStep(self, state, solve)
+
     def _host_stage(self, n):
         """Pinned host / device staging of a host-state step (allocated once)."""
         st = getattr(self, "_stage", None)
@@ -360,3 +365,84 @@ class BackwardEulerIntegrator:
         result = self.compute_step(state, solve)
         self.commit(state, result)
         return result
+
+
+class CapturedStep:
+    """compute_step as ONE CUDA graph: the fused assembly, the persistent PCG
+    kernel (cooperative launch captured as a kernel node) and the kinematic
+    update replay without any host work between them.
+
+    `replay(state)` copies the state into the graph's static inputs, replays,
+    reads the status words once and returns a StepResult whose tensors are the
+    graph's static outputs -- valid until the next replay (clone to keep).
+    The solver must be a device solver (`accepts_device`) whose preconditioner
+    does not change between replays (same factor image / Jacobi of the step's
+    own matrix).  Same kernels, same arithmetic as compute_step: results are
+    bit-identical to it."""
+
+    def __init__(self, integ: BackwardEulerIntegrator, state: SimState, solve):
+        t = _lib.require_cuda()
+        if not state.on_device:
+            raise IntegratorError("CapturedStep needs a device-resident SimState")
+        if not getattr(solve, "accepts_device", False):
+            raise IntegratorError("CapturedStep needs a device solver (accepts_device)")
+        self.integ, self.solve = integ, solve
+        n = integ.mesh.ndof
+        self.n = n
+        self.x0, self.v0, self.fe = (t.empty(n, dtype=t.float64, device="cuda") for _ in range(3))
+        self._load(state)
+        integ.compute_step(state, solve)   # warm: plan, pattern, handles, launch grids
+        from .krylov import _handle
+
+        self._pcg = _handle(n)
+        if self._pcg.pending is not None:
+            self._pcg.pending._get()
+            self._pcg.pending = None
+        side = t.cuda.Stream()
+        side.wait_stream(t.cuda.current_stream())
+        with t.cuda.stream(side):  # one eager pass on the capture stream (allocator warm-up)
+            self._body()
+            self._pcg.pending = None
+        t.cuda.current_stream().wait_stream(side)
+        t.cuda.synchronize()
+        self.graph = t.cuda.CUDAGraph()
+        l0 = _lib.launch_count()
+        with t.cuda.graph(self.graph):
+            self.outs = self._body()
+        self.kernels = _lib.launch_count() - l0  # libtsb kernels in one replay
+        self._pcg.pending = None
+
+    def _load(self, state):
+        self.x0.copy_(state.positions.reshape(-1))
+        self.v0.copy_(state.velocities.reshape(-1))
+        self.fe.copy_(state.f_ext.reshape(-1))
+
+    def _body(self):
+        integ, n = self.integ, self.n
+        t = _lib.torch()
+        a, b, f_int, f_ext, _ = integ._assemble_device(self.x0, self.v0, self.fe)
+        accel, _ = self.solve(a, b)
+        acc, v1, x1 = (t.empty(n, dtype=t.float64, device="cuda") for _ in range(3))
+        P = _lib.ptr
+        _lib.check(_lib.load().tsb_advance(n, P(accel), P(self.v0), P(self.x0), P(integ._plan.fixed_dof),
+                                           integ.config.dt, P(acc), P(v1), P(x1), P(integ._plan.flags),
+                                           _lib.stream_ptr()), "advance")
+        return a, b, f_int, f_ext, acc, v1, x1
+
+    def replay(self, state: SimState) -> StepResult:
+        from .krylov import _DeviceReport
+
+        t0 = time.perf_counter()
+        self._load(state)
+        self.graph.replay()
+        a, b, f_int, f_ext, acc, v1, x1 = self.outs
+        report = _DeviceReport(self._pcg, t0)
+        flags = self.integ._plan.flags.cpu()
+        self.integ._raise_model_flags(flags)
+        if not report.converged:
+            raise StepError(f"linear solve did not converge: residual {report.final_residual:g} "
+                            f"after {report.iterations} iterations", report)
+        if int(flags[1]):
+            raise StepError("solver produced non-finite accelerations", report)
+        return StepResult(x1.view(-1, 3), v1.view(-1, 3), acc.view(-1, 3), f_int, f_ext, a, b, report, False,
+                          0.0, time.perf_counter() - t0)

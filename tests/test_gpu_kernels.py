@@ -203,3 +203,41 @@ def test_stvk_integrator_step_vs_reference(golden, params):
     assert rel(res.accelerations, g["next_accel"]) <= 1e-10
     assert rel(res.velocities, g["next_velocities"]) <= 1e-10
     assert rel(res.positions - g["positions"], g["next_positions"] - g["positions"]) <= 1e-10
+
+
+@pytest.mark.parametrize("precond", ["jacobi", "ldlt"])
+def test_captured_step_equals_compute_step(params, precond):
+    """CapturedStep (assembly + persistent PCG + kinematics as one CUDA graph)
+    gives bit-identical results to the eager compute_step, replay after replay."""
+    from paper_2306_05893_b200 import mesh as M, ndprecond as ND
+
+    mesh = clamped_beam(6, 6, 28)
+    integ = BackwardEulerIntegrator(mesh, models.make_model("corotational", mesh, params),
+                                    IntegratorConfig(dt=0.01, gravity=(0.0, -9.81, 0.0)))
+    cfg = krylov.SolverConfig(1e-9, 8000)
+    st = SimState.rest(mesh, device=True)
+
+    def jac(a, b):
+        return krylov.pcg(a, b, krylov.jacobi_precond(a), cfg)
+
+    jac.accepts_device = True
+    for _ in range(3):
+        integ.step(st, jac)
+    solve = jac
+    if precond == "ldlt":
+        plan = ND.expand_plan(ND.nested_dissection(M.vertex_adjacency(mesh), 64))
+        f = ND.ldlt_factor(integ.assemble_system(st)[0], plan)
+
+        def solve(a, b):
+            return krylov.pcg(a, b, f, cfg)
+
+        solve.accepts_device = True
+    cap = integ.capture(st, solve)
+    assert cap.kernels >= 3
+    for _ in range(3):
+        ref = integ.compute_step(st, solve)
+        got = cap.replay(st)
+        assert got.report.iterations == ref.report.iterations
+        for name in ("positions", "velocities", "accelerations", "f_int", "rhs"):
+            assert bool((getattr(got, name) == getattr(ref, name)).all()), name
+        integ.commit(st, ref)
