@@ -14,6 +14,7 @@ System: A = (1 + h alpha) M + h (h + beta) K,
 from __future__ import annotations
 
 import time
+import weakref
 from dataclasses import dataclass
 
 import numpy as np
@@ -266,14 +267,13 @@ class BackwardEulerIntegrator:
         host = not state.on_device
         n = self.mesh.ndof
         stage = None
-        if host:  # one pinned H2D of (x, v, f_ext), one D2H of the six results
+        if host:  # H2D of (x, v, f_ext) into one device buffer, one D2H of the six results
             stage = self._host_stage(n)
-            hin = stage["h_in"].numpy()
-            np.copyto(hin[:n], np.asarray(state.positions, dtype=np.float64).reshape(-1))
-            np.copyto(hin[n:2 * n], np.asarray(state.velocities, dtype=np.float64).reshape(-1))
-            np.copyto(hin[2 * n:], np.asarray(state.f_ext, dtype=np.float64).reshape(-1))
             d_in = stage["d_in"]
-            d_in.copy_(stage["h_in"], non_blocking=True)
+            for k, arr in enumerate((state.positions, state.velocities, state.f_ext)):
+                # results of an earlier step are views of pinned memory: straight DMA; user arrays stage
+                src = t.from_numpy(np.ascontiguousarray(np.asarray(arr, dtype=np.float64)).reshape(-1))
+                d_in[k * n:(k + 1) * n].copy_(src, non_blocking=True)
             x0, v0, fe_state = d_in[:n], d_in[n:2 * n], d_in[2 * n:]
         else:
             x0 = self._flat_dev(state.positions)
@@ -323,11 +323,12 @@ class BackwardEulerIntegrator:
                 raise StepError("solver produced non-finite accelerations", report)
             x_tr, v_tr = x1, v1
         if host:
-            h_out = stage["h_out"]
-            h_out.copy_(stage["d_out"], non_blocking=True)
+            ent = self._out_buffer(n)
+            ent[0].copy_(stage["d_out"], non_blocking=True)
             t.cuda.current_stream().synchronize()
-            o = h_out.numpy()
-            part = lambda k: o[k * n:(k + 1) * n].copy()  # noqa: E731  (caller-owned arrays)
+            o = ent[0].numpy()  # the six results are views of this pinned buffer, which is
+            weakref.finalize(o, _release_buffer, ent)  # reused only once every view is gone
+            part = lambda k: o[k * n:(k + 1) * n]  # noqa: E731
             pos, vel, acc_o = part(0).reshape(-1, 3), part(1).reshape(-1, 3), part(2).reshape(-1, 3)
             rhs, f_int_o, f_ext_o = part(3), part(4), part(5)
         else:
@@ -342,17 +343,27 @@ class BackwardEulerIntegrator:
         return CapturedStep(self, state, solve)
 
     def _host_stage(self, n):
-        """Pinned host / device staging of a host-state step (allocated once)."""
+        """Device staging of a host-state step (allocated once)."""
         st = getattr(self, "_stage", None)
         if st is None or st["n"] != n:
             t = _lib.torch()
             st = {"n": n,
-                  "h_in": t.empty(3 * n, dtype=t.float64).pin_memory(),
                   "d_in": t.empty(3 * n, dtype=t.float64, device="cuda"),
-                  "h_out": t.empty(6 * n, dtype=t.float64).pin_memory(),
                   "d_out": t.empty(6 * n, dtype=t.float64, device="cuda")}
             self._stage = st
+            self._out_pool = []
         return st
+
+    def _out_buffer(self, n):
+        """A pinned [6n] result buffer none of whose earlier results is still referenced."""
+        for ent in self._out_pool:
+            if ent[1]:
+                ent[1] = False
+                return ent
+        t = _lib.torch()
+        ent = [t.empty(6 * n, dtype=t.float64).pin_memory(), False]
+        self._out_pool.append(ent)
+        return ent
 
     def commit(self, state: SimState, result: StepResult):
         state.positions = result.positions
@@ -365,6 +376,10 @@ class BackwardEulerIntegrator:
         result = self.compute_step(state, solve)
         self.commit(state, result)
         return result
+
+
+def _release_buffer(ent):
+    ent[1] = True
 
 
 class CapturedStep:
