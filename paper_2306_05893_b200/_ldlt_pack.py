@@ -631,7 +631,7 @@ class DevicePanels:
               "apply": self._lib.tsb_ldlt_apply, "upper_scaled": self._lib.tsb_ldlt_upper_scaled}[mode]
         _lib.check(fn(self.h, _lib.ptr(r), _lib.ptr(out), _lib.stream_ptr()), f"ldlt_{mode}")
 
-    MULTI_RHS = int(os.environ.get("TSB_MULTI_RHS", "8"))  # right-hand sides per multi-RHS lower sweep
+    MULTI_RHS = min(8, int(os.environ.get("TSB_MULTI_RHS", "8")))  # right-hand sides per multi-RHS lower sweep (<= 8)
 
     def lower_multi(self, R, Y):
         """Y[j] = L^-1 R[j] (permuted order) for the rows of R ([k][n] CUDA

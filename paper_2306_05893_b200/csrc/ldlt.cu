@@ -41,7 +41,7 @@ struct tsb_ldlt {
 
 namespace tsb {
 
-template <bool TRACE>
+template <bool TRACE, bool MULTI = false>
 __global__ void __launch_bounds__(kSweepBlock) lower_sweep(tsb_ldlt_desc D, SweepArgs A) {
     extern __shared__ __align__(128) double smem[];
     __shared__ uint64_t bars[2];
@@ -55,7 +55,7 @@ __global__ void __launch_bounds__(kSweepBlock) lower_sweep(tsb_ldlt_desc D, Swee
     }
     __syncthreads();
     uint32_t phase = 0;
-    lower_sweep_body<TRACE>(D, A, smem, bars, phase);
+    lower_sweep_body<TRACE, MULTI>(D, A, smem, bars, phase);
 }
 
 template <bool TRACE>
@@ -229,12 +229,18 @@ extern "C" int tsb_ldlt_lower_multi(tsb_ldlt_t h, int32_t nr, const double *d_r,
         a.ld_part = ld_part;
         // the grid of the handle was sized for the 1-RHS footprint: keep it co-resident
         int per_sm = 0;
-        TSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lower_sweep<false>, kSweepBlock, smem));
+        static bool once = [] {
+            allow_max_smem(lower_sweep<false, true>);
+            return true;
+        }();
+        (void)once;
+        if (nr > 8) throw Error(TSB_E_ARG, "at most 8 right-hand sides per multi-RHS sweep");
+        TSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lower_sweep<false, true>, kSweepBlock, smem));
         int nsm = kNumSM;
         TSB_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
         const int grid = D.grid < nsm * per_sm ? D.grid : nsm * per_sm;
         if (grid < 1) throw Error(TSB_E_ARG, "multi-RHS lower sweep does not fit on an SM");
-        launch_coop(lower_sweep<false>, grid, smem, as_stream(stream), D, a);
+        launch_coop(lower_sweep<false, true>, grid, smem, as_stream(stream), D, a);
     });
 }
 

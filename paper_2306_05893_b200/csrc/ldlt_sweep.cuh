@@ -149,7 +149,8 @@ constexpr int kFinRows = 1024;          // rows per piece of a mode-2 finalisati
 inline size_t sweep_smem_lower(const tsb_ldlt_desc &D, int nr = 1) {
     const int offs = (D.max_v + 2 > kFinRows + 2 ? D.max_v + 2 : kFinRows + 2);
     return (size_t)(kStage + nr * ((D.max_v + 3) & ~1) + ((D.max_cb + 1) & ~1)) * sizeof(double) +
-           (((offs + 1) & ~1) + kMaxItemRows) * sizeof(int32_t);
+           (((offs + 1) & ~1) + kMaxItemRows) * sizeof(int32_t) +
+           (nr > 1 ? (size_t)nr * kSweepBlock * sizeof(double) : 0);  // multi-RHS segment partials
 }
 inline size_t sweep_smem_upper(const tsb_ldlt_desc &D) {
     return (size_t)(kStage + ((D.max_v + 3) & ~1)) * sizeof(double);
@@ -310,41 +311,94 @@ __device__ __forceinline__ double lower_input(const SweepArgs &A, int row, int j
     return A.ext ? v - __ldcg(A.ext + row) : v;
 }
 
-// item_gemv for nr right-hand sides (v_j = v + j * vstride): every tile read
-// once from the staged data per right-hand side; emit(row, j, value).
+// tile_dot for NR right-hand sides at once: every tile pair is read from
+// shared memory once and applied to the NR vectors (v_j = v + j * vstride);
+// per right-hand side the same four accumulators and summation order as
+// tile_dot, so each result is bit-identical to a single-vector sweep.
+template <int NR>
+__device__ __forceinline__ void tile_dot_multi(const double *d, const double *v, int vstride, int p0, int p1, int ps,
+                                               int lane, double *out) {
+    const double2 *g = reinterpret_cast<const double2 *>(d) + lane;
+    double a0[NR], a1[NR], a2[NR], a3[NR];
+#pragma unroll
+    for (int j = 0; j < NR; ++j) a0[j] = a1[j] = a2[j] = a3[j] = 0.0;
+    int p = p0;
+    for (; p + ps < p1; p += 2 * ps) {
+        const double2 g0 = g[p * kTile], g1 = g[(p + ps) * kTile];
+#pragma unroll
+        for (int j = 0; j < NR; ++j) {
+            const double2 *vv = reinterpret_cast<const double2 *>(v + j * vstride);
+            const double2 x0 = vv[p], x1 = vv[p + ps];
+            a0[j] += g0.x * x0.x;
+            a1[j] += g0.y * x0.y;
+            a2[j] += g1.x * x1.x;
+            a3[j] += g1.y * x1.y;
+        }
+    }
+    if (p < p1) {
+        const double2 g0 = g[p * kTile];
+#pragma unroll
+        for (int j = 0; j < NR; ++j) {
+            const double2 x0 = reinterpret_cast<const double2 *>(v + j * vstride)[p];
+            a0[j] += g0.x * x0.x;
+            a1[j] += g0.y * x0.y;
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < NR; ++j) out[j] = (a0[j] + a1[j]) + (a2[j] + a3[j]);
+}
+
+// out[0..nr) for a runtime nr <= 8 (compile-time unrolled per width)
+__device__ __forceinline__ void tile_dot_nr(int nr, const double *d, const double *v, int vstride, int p0, int p1,
+                                            int ps, int lane, double *out) {
+    switch (nr) {
+        case 1: tile_dot_multi<1>(d, v, vstride, p0, p1, ps, lane, out); break;
+        case 2: tile_dot_multi<2>(d, v, vstride, p0, p1, ps, lane, out); break;
+        case 3: tile_dot_multi<3>(d, v, vstride, p0, p1, ps, lane, out); break;
+        case 4: tile_dot_multi<4>(d, v, vstride, p0, p1, ps, lane, out); break;
+        case 5: tile_dot_multi<5>(d, v, vstride, p0, p1, ps, lane, out); break;
+        case 6: tile_dot_multi<6>(d, v, vstride, p0, p1, ps, lane, out); break;
+        case 7: tile_dot_multi<7>(d, v, vstride, p0, p1, ps, lane, out); break;
+        default: tile_dot_multi<8>(d, v, vstride, p0, p1, ps, lane, out); break;
+    }
+}
+
+// item_gemv for nr <= 8 right-hand sides: each staged tile pair read once for
+// all of them; segment partials of all right-hand sides reduced after one
+// barrier (red: [nr][8 warps][32]); emit(row, j, value).
 template <class Emit>
 __device__ __forceinline__ void item_gemv_multi(const Item &it, const tsb_ldlt_tile *tiles, double *stage,
                                                 uint64_t *bars, uint32_t &phase, const double *v, int vstride, int nr,
                                                 double *red, double *part, int64_t ld_part, int32_t *tcnt,
                                                 const Emit &emit) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double out[8];
     mbar_wait(&bars[0], phase & 1u);
     phase ^= 1u;
     if (it.seg == 0) {
         const int64_t off0 = tiles[it.t0].off;
         for (int t = it.t0 + warp; t < it.t1; t += kWarps) {
             const tsb_ldlt_tile T = tiles[t];
-            for (int j = 0; j < nr; ++j) {
-                const double a = tile_dot(stage + (T.off - off0), v + j * vstride + T.tl, 0, T.np, 1, lane);
-                if (lane < T.nrows) emit(T.row0 + lane, j, a);
-            }
+            tile_dot_nr(nr, stage + (T.off - off0), v + T.tl, vstride, 0, T.np, 1, lane, out);
+            if (lane < T.nrows)
+                for (int j = 0; j < nr; ++j) emit(T.row0 + lane, j, out[j]);
         }
         return;
     }
     __shared__ int last_seg_m;
     const tsb_ldlt_tile T = tiles[it.t0];
     const int s = it.seg - 1, p0 = s * kSegPairs, cnt = min(kSegPairs, T.np - p0);
-    for (int j = 0; j < nr; ++j) {
-        red[warp * 32 + lane] = tile_dot(stage, v + j * vstride + T.tl + 2 * p0, warp, cnt, kWarps, lane);
-        __syncthreads();
-        if (threadIdx.x < 32) {
-            double a = 0.0;
+    tile_dot_nr(nr, stage, v + T.tl + 2 * p0, vstride, warp, cnt, kWarps, lane, out);
+    for (int j = 0; j < nr; ++j) red[(j * kWarps + warp) * 32 + lane] = out[j];
+    __syncthreads();
+    if ((int)threadIdx.x < 32 * nr) {
+        const int j = threadIdx.x >> 5, l = threadIdx.x & 31;
+        double a = 0.0;
 #pragma unroll
-            for (int w = 0; w < kWarps; ++w) a += red[w * 32 + threadIdx.x];
-            part[j * ld_part + ((int64_t)T.part + s) * kTile + threadIdx.x] = a;
-        }
-        __syncthreads();
+        for (int w = 0; w < kWarps; ++w) a += red[(j * kWarps + w) * 32 + l];
+        part[j * ld_part + ((int64_t)T.part + s) * kTile + l] = a;
     }
+    __syncthreads();
     if (threadIdx.x == 0) last_seg_m = atom_add_acq_rel(tcnt + it.t0, 1) == T.nseg - 1;
     __syncthreads();
     if (last_seg_m && threadIdx.x < 32) {
@@ -366,16 +420,17 @@ __device__ __forceinline__ void item_gemv_multi(const Item &it, const tsb_ldlt_t
 //   are formed once by the item that completes it.
 // shared memory: [stage][xs max_m+2][cbs max_cb][offs int32 max_m+2][dsts int32]
 // ---------------------------------------------------------------------------
-template <bool TRACE>
+template <bool TRACE, bool MULTI = false>
 __device__ __forceinline__ void lower_sweep_body(const tsb_ldlt_desc &D, const SweepArgs &A, double *smem,
                                                  uint64_t *bars, uint32_t &phase) {
     double *stage = smem;
     double *xs = smem + kStage;                       // x_b over the item's window [w0, w1) (nr windows)
-    const int nr = A.nr, xstride = (D.max_v + 3) & ~1;
+    const int nr = MULTI ? A.nr : 1, xstride = (D.max_v + 3) & ~1;
     double *cbs = xs + nr * xstride;
     int32_t *offs = reinterpret_cast<int32_t *>(cbs + ((D.max_cb + 1) & ~1));
     const int noffs = (D.max_v + 2 > kFinRows + 2 ? D.max_v + 2 : kFinRows + 2);
     int32_t *dsts = offs + ((noffs + 1) & ~1);
+    double *redm = reinterpret_cast<double *>(dsts + kMaxItemRows);  // MULTI: [nr][8 warps][32] segment partials
     __shared__ int item_id;
     __shared__ double red[kSweepBlock];
     int32_t *ctl = D.d_ctl;
@@ -500,7 +555,7 @@ __device__ __forceinline__ void lower_sweep_body(const tsb_ldlt_desc &D, const S
         }
         __syncthreads();
         trace(tbuf, iid, 4);
-        if (nr == 1) {
+        if (!MULTI) {
             auto emit = [&](int r, double a) {
                 if (r < m)
                     A.x[s + r] = a;  // unit diagonal stored: y_r = sum_{j <= r} Linv_rj x_j
@@ -515,7 +570,7 @@ __device__ __forceinline__ void lower_sweep_body(const tsb_ldlt_desc &D, const S
                 else
                     D.d_cbuf[j * A.ld_cb + dsts[r - mr0]] = a;
             };
-            item_gemv_multi(it, D.d_tiles_lower, stage, bars, phase, xs - w0, xstride, nr, red, D.d_part_lower,
+            item_gemv_multi(it, D.d_tiles_lower, stage, bars, phase, xs - w0, xstride, nr, redm, D.d_part_lower,
                             A.ld_part, D.d_tcnt_lower, emit);
         }
         trace(tbuf, iid, 5);
