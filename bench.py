@@ -1,6 +1,6 @@
 """Benchmark of the B200 implicit-FEM solve path (BASELINE.json metric).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg2|cfg1|cfg3]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg2|cfg1|cfg3|cfg5]
                     [--precond ldlt|jacobi] [--impl reference]
 
 A step = one implicit time step of the scenario (assemble A, b on the device
@@ -9,6 +9,8 @@ beam under transverse gravity, LDL^T factors replayed at a fixed staleness of
 3 steps (SURVEY.md 8d / BASELINE.md section 2).  Every timed step repeats the
 same step from the same state (nothing committed), L2 flushed between steps.
 N > 1: one independent simulation per GPU (replicas, weak scaling).
+cfg5: 64 independent ~50k-node simulations (own gravity direction each)
+split over the GPUs; a step advances all of them (strong scaling).
 """
 
 from __future__ import annotations
@@ -32,6 +34,8 @@ WORKLOADS = {
     "cfg1": dict(dims=(6, 6, 28), law="linear", desc="config 1: ~1k-node beam, linear elastic"),
     "cfg2": dict(dims=(10, 10, 100), law="corotational", desc="config 2: ~10k-node corotational beam"),
     "cfg3": dict(dims=(20, 20, 250), law="corotational", desc="config 3: ~100k-node corotational beam"),
+    "cfg5": dict(dims=(20, 20, 125), law="corotational", batch=64,
+                 desc="config 5: 64 independent ~50k-node corotational beams (batched, Jacobi-PCG)"),
 }
 STALE_FROM, AT_STEP = 4, 7
 TOL, MAX_IT, LEAF, TILE = 1e-9, 8000, 64, 16
@@ -405,11 +409,172 @@ def traffic_from_profiles(workload):
 
 
 # ---------------------------------------------------------------------------
+# config 5: a batch of independent simulations per GPU
+# ---------------------------------------------------------------------------
+
+def batch_gravity(i):
+    """Gravity of simulation i: a random unit direction (default_rng(i)) x 9.81."""
+    g = np.random.default_rng(i).standard_normal(3)
+    return tuple(float(v) for v in 9.81 * g / np.linalg.norm(g))
+
+
+def build_batch(world, rank):
+    import paper_2306_05893_b200 as P
+    from paper_2306_05893_b200 import krylov
+    from paper_2306_05893_b200.integrator import BackwardEulerIntegrator, IntegratorConfig, SimState
+
+    w = WORKLOADS["cfg5"]
+    mesh = P.generate_beam(*w["dims"], 0.1)
+    mesh = mesh.with_fixed_nodes(np.flatnonzero(mesh.nodes[:, 2] == 0.0))
+    params = P.MaterialParams(1e5, 0.3, 1000.0)
+    cfg = krylov.SolverConfig(TOL, MAX_IT)
+
+    def jacobi(a, b):
+        return krylov.pcg(a, b, krylov.jacobi_precond(a), cfg)
+
+    jacobi.accepts_device = True
+    sims = []
+    for i in range(w["batch"]):
+        if i % world != rank:
+            continue
+        integ = BackwardEulerIntegrator(mesh, P.make_model(w["law"], mesh, params),
+                                        IntegratorConfig(dt=0.01, gravity=batch_gravity(i)))
+        st = SimState.rest(mesh, device=True)
+        for _ in range(3):  # a few scenario steps: non-trivial velocities and rotations
+            integ.step(st, jacobi)
+        sims.append({"id": i, "integ": integ, "state": st})
+    return mesh, sims, jacobi
+
+
+def run_batched(args, world, rank, local, dist):
+    """Config 5: every rank steps its share of the 64 simulations (sequentially,
+    each as a captured CUDA graph); value = ms per batch step (all 64
+    simulations), max over ranks; strong scaling (the batch is fixed)."""
+    import gc
+
+    import torch
+    from paper_2306_05893_b200 import _lib, krylov
+    from paper_2306_05893_b200.integrator import SimState
+
+    mesh, sims, solve = build_batch(world, rank)
+    for sm in sims:
+        sm["cap"] = sm["integ"].capture(sm["state"], solve)
+    flush = L2Flush()
+    pk, pk_kind = peaks()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    gc.disable()
+
+    def batch_step():
+        its = []
+        for sm in sims:
+            its.append(sm["cap"].replay(sm["state"]).report.iterations)
+        return its
+
+    for _ in range(args.warmup):
+        flush()
+        batch_step()
+    torch.cuda.synchronize()
+    per, iters = [], []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            iters += batch_step()
+            e1.record()
+            e1.synchronize()
+            per.append(e0.elapsed_time(e1))
+    gc.enable()
+    t_local = torch.tensor([sum(per)], dtype=torch.float64, device="cuda")
+    if dist:
+        dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
+        dist.barrier()
+    ms = float(t_local.item()) / args.steps
+    # isolated SpMV of simulation 0's matrix (the Jacobi-PCG iteration is SpMV-bound)
+    W0 = {"integ": sims[0]["integ"], "state": sims[0]["state"]}
+    spmv_r = time_spmv(W0, 20, flush)
+    # e2e: one batch step through the public API with host (NumPy) state
+    hosts = [SimState(*(a.detach().cpu().numpy() for a in (sm["state"].positions, sm["state"].velocities,
+                                                          sm["state"].accelerations, sm["state"].f_int,
+                                                          sm["state"].f_ext)), sm["state"].time) for sm in sims]
+
+    def host_solve(a, b):
+        return krylov.pcg(a, b, krylov.jacobi_precond(a), krylov.SolverConfig(TOL, MAX_IT))
+
+    host_solve.accepts_device = True
+    e2e = []
+    for _ in range(2):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for sm, hs in zip(sims, hosts):
+            res = sm["integ"].compute_step(hs, host_solve)
+            _ = res.positions.sum()
+        e2e.append((time.perf_counter() - t0) * 1e3)
+    t_e2e = torch.tensor([min(e2e)], dtype=torch.float64, device="cuda")
+    if dist:
+        dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
+    n = mesh.ndof
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return 0
+    hbm = pk.get("hbm_gbs", 6650.0)
+    batch = WORKLOADS["cfg5"]["batch"]
+    line = {
+        "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": WORKLOADS["cfg5"]["desc"], "mesh": "x".join(map(str, WORKLOADS["cfg5"]["dims"])),
+                   "simulations": batch, "per_rank": len(sims), "nodes": mesh.node_count, "dofs": n,
+                   "precond": "jacobi", "tol": TOL, "parallelism": f"batch split over {world} GPU(s), no collective",
+                   "l2": "flushed (256 MB write) before every batch step",
+                   "step": "one implicit step of every simulation (CUDA-graph replays, one after another)"},
+        "sim_steps_per_s": batch / (ms * 1e-3),
+        "iterations_median": statistics.median(iters),
+        "spmv": {"ms": spmv_r["ms"], "gbs": spmv_r["gbs"], "frac": spmv_r["gbs"] / hbm},
+        "roofline": {"bound": "hbm", "kernel": "CSR SpMV (bit-exact), the Jacobi-PCG iteration's dominant part",
+                     "achieved": spmv_r["gbs"], "peak": hbm, "peak_kind": pk_kind, "unit": "GB/s",
+                     "frac": spmv_r["gbs"] / hbm, "traffic": None},
+        "e2e": {"value": float(t_e2e.item()), "unit": "ms", "h2d_bytes_per_step": 3 * 8 * n * len(sims),
+                "d2h_bytes_per_step": 6 * 8 * n * len(sims)},
+        "gpu_launches": sum(sm["cap"].kernels for sm in sims) * args.steps,
+        "clocks": clk.summary(),
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        cb = batch_cpu_baseline(sims[0])
+        line["cpu_baseline"] = {"value": cb * batch, "unit": "ms", "cores": 1, "kind": "port",
+                                "sample": f"one oracle step (assembly + Jacobi-PCG) of simulation 0 ({cb:.0f} ms), "
+                                          f"x {batch} simulations, 1 BLAS thread"}
+    print(json.dumps(line))
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+def batch_cpu_baseline(sim, threads=1):
+    from oracle import tetsim_oracle as O
+    from threadpoolctl import threadpool_limits
+
+    integ, st = sim["integ"], sim["state"].to_host()
+    mesh = integ.mesh
+    with threadpool_limits(limits=threads):
+        rest = O.rest_data(mesh.nodes, mesh.elements, 1e5, 0.3, 1000.0)
+        t0 = time.perf_counter()
+        out = O.assemble_system(mesh.nodes, mesh.elements, mesh.fixed_nodes, rest, st.positions, st.velocities,
+                                st.f_ext, 0.01, integ.config.gravity)
+        inv = O.jacobi_inv_diag(out["row_ptr"], out["col_ind"], out["values"], len(out["b"]))
+        O.pcg(out["row_ptr"], out["col_ind"], out["values"], out["b"], lambda r: r * inv, TOL, MAX_IT)
+        return (time.perf_counter() - t0) * 1e3
+
 
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
+    if args.workload == "cfg5":
+        return run_reference_batched(args)
     W = build_workload(args.workload)
     ncores = os.cpu_count()
     from oracle import tetsim_oracle as O
@@ -437,6 +602,29 @@ def run_reference(args):
         "e2e": {"value": ms, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
+    return 0
+
+
+def run_reference_batched(args):
+    """Reference arm of config 5: the oracle port steps simulation 0 (all host
+    BLAS threads) and the batch time is that times 64."""
+    import torch  # noqa: F401  (the oracle sample runs on the host; the state comes from a device scenario)
+
+    _, sims, _ = build_batch(1, 0)
+    ts = []
+    for _ in range(max(1, args.steps)):
+        ts.append(batch_cpu_baseline(sims[0], threads=os.cpu_count()))
+    batch = WORKLOADS["cfg5"]["batch"]
+    ms = statistics.mean(ts) * batch
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOADS["cfg5"]["desc"], "precond": "jacobi"},
+        "cpu_baseline": {"value": ms, "unit": "ms", "cores": os.cpu_count(), "kind": "port",
+                         "sample": f"{len(ts)} oracle steps of simulation 0 x {batch} simulations, all host BLAS threads"},
+        "e2e": {"value": ms, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
     return 0
 
 
@@ -468,6 +656,8 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2306_05893_b200 import _lib
 
+    if args.workload == "cfg5":
+        return run_batched(args, world, rank, local, dist)
     W = build_workload(args.workload)
     flush = L2Flush()
     pk, pk_kind = peaks()
