@@ -141,3 +141,35 @@ def test_device_state_drop_with_async_device_factors(params):
         pre.update(info.result.matrix, k)
     assert landed
     pre.close()
+
+
+def test_factor_path_equals_column_path_for_general_rows(params, rng):
+    """Multi-entry (bilateral) constraint rows: the lower-sweep compliance
+    Y^T D^-1 Y and the one-upper-sweep correction equal the reference's
+    column-by-column form with the same factors."""
+    mesh = P.generate_beam(3, 3, 6, 0.1)
+    integ = BackwardEulerIntegrator(mesh, P.make_model("corotational", mesh, params), IntegratorConfig(dt=0.01))
+    cfg = krylov.SolverConfig(1e-10, 8000)
+    st = SimState.rest(mesh)
+    solve = lambda a, b: krylov.pcg(a, b, krylov.jacobi_precond(a), cfg)  # noqa: E731
+    free = integ.compute_step(st, solve)
+    plan = ND.expand_plan(ND.nested_dissection(M.vertex_adjacency(mesh), 16))
+    f = ND.ldlt_factor(free.matrix, plan)
+    m = 7
+    indptr = np.concatenate([[0], np.cumsum(rng.integers(1, 4, m))])
+    cols = np.concatenate([rng.choice(mesh.ndof, indptr[i + 1] - indptr[i], replace=False) for i in range(m)])
+    cs = CT.ConstraintSet(ndof=mesh.ndof, indptr=indptr, col_ind=cols, coeffs=rng.standard_normal(len(cols)),
+                          violation=1e-4 * rng.standard_normal(m), types=[CT.BILATERAL] * m)
+    pipe = CT.PlaneContactPipeline(integ, -100.0)
+    lam_f, info_f, acc_f = pipe._resolve_with_factors(free, cs, f, 0.01)
+    w_f = pipe.last_w.cpu().numpy()
+    lam_c, info_c, acc_c = pipe._resolve_with_columns(free, cs, lambda r: f.apply(r), 0.01)
+    J = np.stack([cs.row_dense(i) for i in range(m)])
+    S = np.stack([O.apply(f, J[i]) for i in range(m)], axis=1)
+    W = J @ S
+    W = 0.5 * (W + W.T) * 0.01 ** 2
+    assert rel(w_f, W) <= 1e-12
+    lam = O.projected_gauss_seidel(W, cs.violation, np.zeros(m, dtype=bool))
+    assert rel(lam_f.cpu().numpy(), lam) <= 1e-9 and rel(lam_c.cpu().numpy(), lam) <= 1e-9
+    acc = free.accelerations.reshape(-1) - S @ lam
+    assert rel(acc_f.cpu().numpy(), acc) <= 1e-9 and rel(acc_c.cpu().numpy(), acc) <= 1e-9
