@@ -424,6 +424,13 @@ int tsb_pcg_update(int64_t n, const double *d_w, double *d_x, const double *d_p,
 /* beta = d_sc[0] / d_sc[1]; p = z + beta p; d_sc[1] = d_sc[0] */
 int tsb_pcg_direction(int64_t n, double *d_p, const double *d_z, double *d_sc, void *stream);
 int tsb_gather_rows(int64_t m, const int32_t *d_idx, const double *d_src, double *d_dst, void *stream);
+/* All-reduce over peer memory (shard.PeerAllreduce, replaces the NCCL
+ * all-reduce of the exchanges): x (rows d_idx[0..m), or the first m entries
+ * when d_idx is NULL) := sum over ranks in rank order.  d_bufs[r], d_flags[r]:
+ * rank r's exchange buffer (2 x half doubles) and epoch word as mapped in this
+ * process (CUDA IPC); epoch strictly increasing per call. */
+int tsb_peer_allreduce(int64_t m, int32_t world, int32_t rank, double *const *d_bufs, int64_t *const *d_flags,
+                       const int32_t *d_idx, double *d_x, int64_t epoch, int64_t half, void *stream);
 int tsb_scatter_rows(int64_t m, const int32_t *d_idx, const double *d_src, double *d_dst, void *stream);
 
 /* ------------------------------------------------------------------------

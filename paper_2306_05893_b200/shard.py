@@ -283,6 +283,60 @@ def emulate_pcg(a, b, factors, plan: ShardPlan, rank: int, allreduce, tol=1e-9, 
 # device loop (one process per GPU; torch.distributed for the all-reduces)
 # ---------------------------------------------------------------------------
 
+class PeerAllreduce:
+    """All-reduce of small device vectors over peer memory (csrc/peer.cu).
+
+    Every rank allocates a double-buffered exchange buffer and an epoch word;
+    they are shared with the other ranks once through CUDA IPC (the handles
+    travel over the process group with all_gather_object), after which an
+    exchange is ONE kernel: gather the rows into the rank's buffer, publish
+    the epoch (release, system scope), wait for every peer's epoch (acquire),
+    sum the ranks' rows in rank order and scatter them back -- no NCCL call,
+    no host synchronisation.  Between GPUs the peers' buffers are read over
+    NVLink / NVSwitch."""
+
+    def __init__(self, world: int, rank: int, capacity: int, group=None):
+        import torch.distributed as dist
+        from torch.multiprocessing.reductions import reduce_tensor
+
+        from . import _lib
+
+        t = _lib.require_cuda()
+        self.world, self.rank, self.half = world, rank, int(max(capacity, 1))
+        self.buf = t.zeros(2 * self.half, dtype=t.float64, device="cuda")
+        self.flag = t.zeros(1, dtype=t.int64, device="cuda")
+        t.cuda.synchronize()
+        mine = (reduce_tensor(self.buf), reduce_tensor(self.flag))
+        allh = [None] * world
+        dist.all_gather_object(allh, mine, group=group)
+        self._peers = []  # keep the mapped peer tensors alive
+        bufs, flags = [], []
+        for r, (hb, hf) in enumerate(allh):
+            if r == rank:
+                b, f = self.buf, self.flag
+            else:
+                b, f = hb[0](*hb[1]), hf[0](*hf[1])
+                self._peers.append((b, f))
+            bufs.append(b.data_ptr())
+            flags.append(f.data_ptr())
+        self.d_bufs = t.tensor(bufs, dtype=t.int64, device="cuda")
+        self.d_flags = t.tensor(flags, dtype=t.int64, device="cuda")
+        self.epoch = 0
+        self._lib, self._L = _lib.load(), _lib
+        dist.barrier(group=group)
+
+    def __call__(self, x, idx=None, m=None):
+        """x[idx] (or x[:m]) := the sum over ranks, in place, on the current stream."""
+        L = self._L
+        m = int(idx.numel() if idx is not None else (x.numel() if m is None else m))
+        if m > self.half:
+            raise ValueError(f"exchange of {m} rows exceeds the buffer ({self.half})")
+        self.epoch += 1
+        L.check(self._lib.tsb_peer_allreduce(m, self.world, self.rank, L.ptr(self.d_bufs), L.ptr(self.d_flags),
+                                             L.ptr(idx), L.ptr(x), self.epoch, self.half, L.stream_ptr()),
+                "peer_allreduce")
+
+
 class DistributedPcg:
     """Sharded PCG with the nested-dissection LDL^T preconditioner.
 
@@ -297,7 +351,7 @@ class DistributedPcg:
     defaults to torch.distributed.all_reduce (NCCL over NVLink between GPUs).
     """
 
-    def __init__(self, a, factors, rank=None, world=None, allreduce=None, grid=0):
+    def __init__(self, a, factors, rank=None, world=None, allreduce=None, grid=0, exchange="nccl"):
         from . import _lib
         from ._ldlt_pack import DevicePanels
 
@@ -337,11 +391,21 @@ class DistributedPcg:
         self.sc = z(8)  # [rz, pAp] / [rz_new, rz_old] / scratch
         self._lib = _lib.load()
         self._L = _lib
+        # exchange="peer": the top-row exchanges and the scalars go through
+        # PeerAllreduce (one kernel each over IPC-mapped peer memory) instead
+        # of the process group's all-reduce
+        self.peer = None
+        if exchange == "peer" and world > 1:
+            self.peer = PeerAllreduce(world, rank, max(len(self.plan.top_rows), n))
+            self.allreduce = lambda x: self.peer(x)
 
     # -- pieces ------------------------------------------------------------
     def _exchange_top(self, vec):
         m = len(self.plan.top_rows)
         if self.world == 1 or m == 0:
+            return
+        if self.peer is not None:  # gather + exchange + scatter in one kernel
+            self.peer(vec, idx=self.top)
             return
         L, s = self._L, self._L.stream_ptr()
         L.check(self._lib.tsb_gather_rows(m, L.ptr(self.top), L.ptr(vec), L.ptr(self.topbuf), s), "gather")

@@ -36,7 +36,7 @@ def test_single_rank_equals_device_pcg():
     assert rep.iterations == it
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, exchange="nccl"):
     import torch
     import torch.distributed as dist
 
@@ -49,7 +49,8 @@ def _worker(rank, world, port, q):
         a, b, f = _system()
         # both ranks share the one GPU: small persistent grids so the two processes'
         # cooperative sweep launches fit on the device side by side
-        x, it, res, conv = S.DistributedPcg(a, f, rank=rank, world=world, grid=32).solve(b, 1e-9, 200)
+        x, it, res, conv = S.DistributedPcg(a, f, rank=rank, world=world, grid=32,
+                                            exchange=exchange).solve(b, 1e-9, 200)
         q.put((rank, x.cpu().numpy(), it, res, conv))
     except Exception as e:  # surface the failure in the parent
         q.put((rank, repr(e), -1, 0.0, False))
@@ -57,7 +58,10 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-def test_two_ranks_match_the_oracle():
+@pytest.mark.parametrize("exchange", ["nccl", "peer"])
+def test_two_ranks_match_the_oracle(exchange):
+    """exchange="nccl": the process group's all-reduce (gloo here); "peer": the
+    IPC-mapped peer-memory all-reduce kernel (csrc/peer.cu)."""
     import torch.multiprocessing as mp
     from oracle import tetsim_oracle as O
 
@@ -66,7 +70,7 @@ def test_two_ranks_match_the_oracle():
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, exchange)) for r in range(2)]
     for p in procs:
         p.start()
     outs = [q.get(timeout=300) for _ in procs]
