@@ -431,6 +431,17 @@ int tsb_gather_rows(int64_t m, const int32_t *d_idx, const double *d_src, double
  * process (CUDA IPC); epoch strictly increasing per call. */
 int tsb_peer_allreduce(int64_t m, int32_t world, int32_t rank, double *const *d_bufs, int64_t *const *d_flags,
                        const int32_t *d_idx, double *d_x, int64_t epoch, int64_t half, void *stream);
+/* tsb_ldlt_external_sums + peer all-reduce of d_out's rows d_idx[0..m) in one
+ * kernel (the shard's forward-sweep exchange); d_ticket: one int32, zero. */
+int tsb_ldlt_external_sums_peer(tsb_ldlt_t h, double *d_out, int64_t m, int32_t world, int32_t rank,
+                                double *const *d_bufs, int64_t *const *d_flags, const int32_t *d_idx, int64_t epoch,
+                                int64_t half, int32_t *d_ticket, void *stream);
+/* Fused SpMV + peer all-reduce of the shared rows (one kernel: the last CTA
+ * of the product runs the exchange).  d_ticket: one int32, initially zero. */
+int tsb_spmv_peer(int64_t nrows, const int32_t *d_row_ptr, const int32_t *d_col_ind, const double *d_values,
+                  const double *d_x, double *d_y, int64_t m, int32_t world, int32_t rank, double *const *d_bufs,
+                  int64_t *const *d_flags, const int32_t *d_idx, int64_t epoch, int64_t half, int32_t *d_ticket,
+                  void *stream);
 int tsb_scatter_rows(int64_t m, const int32_t *d_idx, const double *d_src, double *d_dst, void *stream);
 
 /* ------------------------------------------------------------------------

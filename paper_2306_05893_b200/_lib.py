@@ -123,6 +123,10 @@ _SIGNATURES = {
     "tsb_pcg_update": (C.c_int, [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "tsb_pcg_direction": (C.c_int, [c_i64, c_vp, c_vp, c_vp, c_vp]),
     "tsb_peer_allreduce": (C.c_int, [c_i64, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp]),
+    "tsb_spmv_peer": (C.c_int, [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i32, c_i32, c_vp, c_vp, c_vp,
+                                c_i64, c_i64, c_vp, c_vp]),
+    "tsb_ldlt_external_sums_peer": (C.c_int, [c_vp, c_vp, c_i64, c_i32, c_i32, c_vp, c_vp, c_vp, c_i64, c_i64,
+                                              c_vp, c_vp]),
     "tsb_gather_rows": (C.c_int, [c_i64, c_vp, c_vp, c_vp, c_vp]),
     "tsb_scatter_rows": (C.c_int, [c_i64, c_vp, c_vp, c_vp, c_vp]),
     "tsb_pcg_create": (C.c_int, [c_i64, C.POINTER(c_vp)]),

@@ -33,6 +33,7 @@
 #include <vector>
 
 #include "ldlt_sweep.cuh"
+#include "peer_exchange.cuh"
 
 struct tsb_ldlt {
     tsb_ldlt_desc d;
@@ -125,6 +126,26 @@ __global__ void ext_sums_kernel(tsb_ldlt_desc D, double *out) {
         const int row = D.d_ext_rows[i];
         out[row] = contrib_sum<true>(D.d_cbuf, D.d_cin_ptr[row], D.d_cin_ptr[row + 1]);
     }
+}
+
+// external sums + the peer all-reduce of the shared rows in one kernel (the
+// last CTA exchanges, as spmv_exchange_kernel)
+__global__ void ext_sums_peer_kernel(tsb_ldlt_desc D, double *out, PeerArgs P, int32_t *ticket) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < D.n_ext; i += (int64_t)gridDim.x * blockDim.x) {
+        const int row = D.d_ext_rows[i];
+        out[row] = contrib_sum<true>(D.d_cbuf, D.d_cin_ptr[row], D.d_cin_ptr[row + 1]);
+    }
+    __shared__ int last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(ticket, 1) == (int)gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    exchange_block(P, out);
+    if (threadIdx.x == 0) *ticket = 0;
 }
 
 void ldlt_enqueue_ext(tsb_ldlt_t h, int mode, const double *r, const double *ext, double *out, cudaStream_t st) {
@@ -254,4 +275,24 @@ extern "C" int tsb_ldlt_upper_scaled(tsb_ldlt_t h, const double *d_y, double *d_
 
 extern "C" int tsb_ldlt_external_sums(tsb_ldlt_t h, double *d_out, void *stream) {
     return tsb::guard([&] { tsb::ldlt_enqueue_ext(h, 2, nullptr, nullptr, d_out, tsb::as_stream(stream)); });
+}
+
+// tsb_ldlt_external_sums followed by the peer all-reduce of d_out's rows
+// d_idx[0..m) (see tsb_peer_allreduce), in one kernel; d_ticket: one int32,
+// initially zero.
+extern "C" int tsb_ldlt_external_sums_peer(tsb_ldlt_t h, double *d_out, int64_t m, int32_t world, int32_t rank,
+                                           double *const *d_bufs, int64_t *const *d_flags, const int32_t *d_idx,
+                                           int64_t epoch, int64_t half, int32_t *d_ticket, void *stream) {
+    using namespace tsb;
+    return guard([&] {
+        if (h == nullptr) throw Error(TSB_E_ARG, "null ldlt handle");
+        if (m < 0 || m > half || world < 1 || rank < 0 || rank >= world) throw Error(TSB_E_ARG, "bad peer arguments");
+        const tsb_ldlt_desc &D = ldlt_desc(h);
+        int g = (int)((D.n_ext + 255) / 256);
+        if (g > kNumSM * 4) g = kNumSM * 4;
+        if (g < 1) g = 1;
+        PeerArgs P{m, world, rank, d_bufs, d_flags, d_idx, epoch, half};
+        ext_sums_peer_kernel<<<g, 256, 0, as_stream(stream)>>>(D, d_out, P, d_ticket);
+        TSB_LAUNCHED();
+    });
 }

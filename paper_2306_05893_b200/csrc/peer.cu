@@ -15,47 +15,14 @@
 // Reuse of a buffer half two epochs later is safe: a rank only reaches epoch
 // e + 2 after every peer published e + 1, which each peer does after its
 // epoch-e kernel (the last reader of the half) completed on its stream.
-#include "tsb_common.cuh"
+#include "peer_exchange.cuh"
 
 namespace tsb {
 namespace peer {
 
 constexpr int kThreads = 1024;
 
-__device__ __forceinline__ void st_release_sys(int64_t *p, int64_t v) {
-    asm volatile("st.release.sys.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ int64_t ld_acquire_sys(const int64_t *p) {
-    int64_t v;
-    asm volatile("ld.acquire.sys.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-
-__global__ void __launch_bounds__(kThreads) allreduce_kernel(int64_t m, int world, int rank,
-                                                             double *const *__restrict__ bufs,
-                                                             int64_t *const *__restrict__ flags,
-                                                             const int32_t *__restrict__ idx, double *x,
-                                                             int64_t epoch, int64_t half) {
-    const int tid = threadIdx.x;
-    const int64_t off = (epoch & 1) * half;
-    double *mine = bufs[rank] + off;
-    for (int64_t i = tid; i < m; i += kThreads) mine[i] = x[idx ? idx[i] : i];
-    __syncthreads();
-    if (tid == 0) {
-        __threadfence_system();
-        st_release_sys(flags[rank], epoch);
-    }
-    if (tid < world && tid != rank) {
-        const int64_t *f = flags[tid];
-        while (ld_acquire_sys(f) < epoch) __nanosleep(64);
-    }
-    __syncthreads();
-    for (int64_t i = tid; i < m; i += kThreads) {
-        double a = 0.0;
-        for (int r = 0; r < world; ++r) a += __ldcv(bufs[r] + off + i);
-        x[idx ? idx[i] : i] = a;
-    }
-}
+__global__ void __launch_bounds__(kThreads) allreduce_kernel(PeerArgs P, double *x) { exchange_block(P, x); }
 
 }  // namespace peer
 }  // namespace tsb
@@ -71,8 +38,8 @@ extern "C" int tsb_peer_allreduce(int64_t m, int32_t world, int32_t rank, double
         if (m < 0 || m > half || world < 1 || world > 1024 || rank < 0 || rank >= world)
             throw Error(TSB_E_ARG, "bad peer all-reduce arguments");
         if (m == 0) return;
-        peer::allreduce_kernel<<<1, peer::kThreads, 0, as_stream(stream)>>>(m, world, rank, d_bufs, d_flags, d_idx,
-                                                                            d_x, epoch, half);
+        PeerArgs P{m, world, rank, d_bufs, d_flags, d_idx, epoch, half};
+        peer::allreduce_kernel<<<1, peer::kThreads, 0, as_stream(stream)>>>(P, d_x);
         TSB_LAUNCHED();
     });
 }

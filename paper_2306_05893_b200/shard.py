@@ -325,6 +325,28 @@ class PeerAllreduce:
         self._lib, self._L = _lib.load(), _lib
         dist.barrier(group=group)
 
+    def spmv(self, nrows, rp, ci, va, x, y, idx):
+        """y = A x on this rank's rows, then y[idx] all-reduced -- one fused kernel (tsb_spmv_peer)."""
+        L = self._L
+        if not hasattr(self, "_ticket"):
+            self._ticket = L.torch().zeros(1, dtype=L.torch().int32, device="cuda")
+        m = int(idx.numel())
+        self.epoch += 1
+        L.check(self._lib.tsb_spmv_peer(nrows, L.ptr(rp), L.ptr(ci), L.ptr(va), L.ptr(x), L.ptr(y), m, self.world,
+                                        self.rank, L.ptr(self.d_bufs), L.ptr(self.d_flags), L.ptr(idx), self.epoch,
+                                        self.half, L.ptr(self._ticket), L.stream_ptr()), "spmv_peer")
+
+    def external_sums(self, panels, out, idx):
+        """panels' external contribution sums into out, then out[idx] all-reduced (one kernel)."""
+        L = self._L
+        if not hasattr(self, "_ticket2"):
+            self._ticket2 = L.torch().zeros(1, dtype=L.torch().int32, device="cuda")
+        self.epoch += 1
+        L.check(self._lib.tsb_ldlt_external_sums_peer(panels.h, L.ptr(out), int(idx.numel()), self.world, self.rank,
+                                                      L.ptr(self.d_bufs), L.ptr(self.d_flags), L.ptr(idx), self.epoch,
+                                                      self.half, L.ptr(self._ticket2), L.stream_ptr()),
+                "external_sums_peer")
+
     def __call__(self, x, idx=None, m=None):
         """x[idx] (or x[:m]) := the sum over ranks, in place, on the current stream."""
         L = self._L
@@ -420,6 +442,9 @@ class DistributedPcg:
 
     def _spmv(self, p, out):
         L = self._L
+        if self.peer is not None and len(self.plan.top_rows):  # product + exchange in one kernel
+            self.peer.spmv(self.n, self.rp, self.ci, self.va, p, out, self.top)
+            return
         L.check(self._lib.tsb_spmv(self.n, L.ptr(self.rp), L.ptr(self.ci), L.ptr(self.va), L.ptr(p), L.ptr(out),
                                    L.stream_ptr()), "spmv")
         self._exchange_top(out)
@@ -429,8 +454,13 @@ class DistributedPcg:
         v["ext"].zero_()
         if self.S is not None:
             self.S.lower_ext(r, None, v["y"])
-            self.S.external_sums(v["ext"])
-        self._exchange_top(v["ext"])
+            if self.peer is not None and len(self.plan.top_rows):  # sums + exchange in one kernel
+                self.peer.external_sums(self.S, v["ext"], self.top)
+            else:
+                self.S.external_sums(v["ext"])
+                self._exchange_top(v["ext"])
+        else:
+            self._exchange_top(v["ext"])
         if self.T is not None:
             self.T.lower_ext(r, v["ext"], v["y"])
             self.T.run("upper_scaled", v["y"], out)
