@@ -94,14 +94,14 @@ class ConstraintSet:
     def device(self):
         """(indptr int64, col_ind int32, coeffs f64, violation f64, unilateral u8) on the device."""
         t = _lib.torch()
-        up = lambda a, dt: t.from_numpy(np.ascontiguousarray(a, dtype=dt)).cuda()  # noqa: E731
-        m = self.nconstraints
-        nz = lambda a: a if len(a) else np.zeros(1, dtype=a.dtype)  # noqa: E731
-        return (up(self.indptr, np.int64), up(nz(np.asarray(self.col_ind, dtype=np.int32)), np.int32),
-                up(nz(np.asarray(self.coeffs, dtype=np.float64)), np.float64),
-                up(nz(np.asarray(self.violation, dtype=np.float64)), np.float64),
-                up(nz(np.array([t_ == UNILATERAL for t_ in self.types] or [False], dtype=np.uint8))[:max(m, 1)],
-                   np.uint8))
+
+        def up(a, dt):  # at least one element, so every pointer is valid
+            a = np.asarray(a, dtype=dt)
+            return t.from_numpy(np.ascontiguousarray(a if len(a) else np.zeros(1, dtype=dt))).cuda()
+
+        unilateral = np.array([kind == UNILATERAL for kind in self.types], dtype=np.uint8)
+        return (up(self.indptr, np.int64), up(self.col_ind, np.int32), up(self.coeffs, np.float64),
+                up(self.violation, np.float64), up(unilateral, np.uint8))
 
 
 def _host(a):
@@ -192,7 +192,7 @@ def projected_gauss_seidel(w, rhs, types, tol: float = 1e-12, max_sweeps: int = 
     return lam.cpu().numpy()
 
 
-def _advance(acc, state, dt, fixed_nodes, integ=None):
+def _advance(acc, state, dt, fixed_nodes):
     """a[pinned] = 0, v' = v + h a, x' = x + h v', pinned keep (tsb_advance)."""
     t = _lib.torch()
     n = acc.numel()
@@ -227,12 +227,13 @@ def correct_motion(free: StepResult, state: SimState, constraints: ConstraintSet
     """a_corr = a_free - S lambda and the kinematic update (contact.py:169-195)."""
     t = _lib.require_cuda()
     n = constraints.ndof
-    S = _dev(s_cols).reshape(n, -1).t().contiguous()  # column-major n x m
     lam_d = _dev(lam).reshape(-1)
-    delta = t.empty(n, dtype=t.float64, device="cuda")
+    m = lam_d.numel()
+    delta = t.zeros(n, dtype=t.float64, device="cuda")
     lib = _lib.load()
-    _check(lib.tsb_gemv_cols(n, lam_d.numel(), _lib.ptr(S), _lib.ptr(lam_d), _lib.ptr(delta), _lib.stream_ptr()),
-           "gemv")
+    if m:
+        S = _dev(s_cols).reshape(n, m).t().contiguous()  # column-major n x m
+        _check(lib.tsb_gemv_cols(n, m, _lib.ptr(S), _lib.ptr(lam_d), _lib.ptr(delta), _lib.stream_ptr()), "gemv")
     acc = t.empty(n, dtype=t.float64, device="cuda")
     _check(lib.tsb_contact_correct(n, _lib.ptr(_dev(free.accelerations).reshape(-1)), _lib.ptr(delta), None,
                                    _lib.ptr(acc), _lib.stream_ptr()), "correct")

@@ -173,3 +173,19 @@ def test_factor_path_equals_column_path_for_general_rows(params, rng):
     assert rel(lam_f.cpu().numpy(), lam) <= 1e-9 and rel(lam_c.cpu().numpy(), lam) <= 1e-9
     acc = free.accelerations.reshape(-1) - S @ lam
     assert rel(acc_f.cpu().numpy(), acc) <= 1e-9 and rel(acc_c.cpu().numpy(), acc) <= 1e-9
+
+
+def test_zero_multiplier_correction_is_identity(params):
+    """reference test_contact.py:183-196: lambda = 0 leaves the free motion unchanged (and m = 0 works)."""
+    mesh = P.generate_beam(2, 2, 3, 0.1)
+    integ = BackwardEulerIntegrator(mesh, P.make_model("corotational", mesh, params), IntegratorConfig(dt=0.01))
+    st = SimState.rest(mesh)
+    cfg = krylov.SolverConfig(1e-10, 5000)
+    free = integ.compute_step(st, lambda a, b: krylov.cg(a, b, cfg))
+    for plane in (-2.0, 100.0):
+        cs = CT.detect_plane_contacts(free.positions - np.array([0, 0, 1.0]), plane_z=plane)
+        lam = np.zeros(cs.nconstraints)
+        s_cols = np.zeros((mesh.ndof, cs.nconstraints))
+        corrected = CT.correct_motion(free, st, cs, lam, s_cols, 0.01, mesh.fixed_nodes)
+        assert np.array_equal(corrected.positions, free.positions)
+        assert np.array_equal(corrected.velocities, free.velocities)
