@@ -189,3 +189,21 @@ def test_zero_multiplier_correction_is_identity(params):
         corrected = CT.correct_motion(free, st, cs, lam, s_cols, 0.01, mesh.fixed_nodes)
         assert np.array_equal(corrected.positions, free.positions)
         assert np.array_equal(corrected.velocities, free.velocities)
+
+
+def test_committed_penetration_bounded_and_pattern_constant(params):
+    """reference test_contact.py:198-212: 40 steps of a drop onto z = -0.03 with CG
+    compliance columns -- committed penetration <= 1e-5, complementarity residual
+    <= 1e-8, and the CSR pattern is built once."""
+    mesh, integ, pipe, st = drop(params, (3, 3, 4), -0.03)
+    cfg = krylov.SolverConfig(1e-10, 5000)
+    solve = lambda a, b: krylov.cg(a, b, cfg)  # noqa: E731
+    contacts = 0
+    for _ in range(40):
+        info = pipe.step(st, solve)
+        assert info.max_penetration <= 1e-5
+        if info.ncontacts:
+            contacts += 1
+            assert info.complementarity_residual <= 1e-8
+    assert contacts > 0
+    assert integ.assembler.pattern_rebuilds == 1
