@@ -265,6 +265,8 @@ def to_device(a, dtype=None, device="cuda"):
     arr = np.ascontiguousarray(a)
     if dtype is not None:
         arr = arr.astype(np.dtype(str(dtype).replace("torch.", "")), copy=False)
+    if not arr.flags.writeable:  # read-only inputs (e.g. Mesh.nodes): torch wants a writable buffer
+        arr = arr.copy()
     return t.from_numpy(arr).to(device=device, non_blocking=False)
 
 
