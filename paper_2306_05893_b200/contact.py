@@ -113,7 +113,7 @@ def _dev(a, dtype=None):
     dtype = dtype or t.float64
     if _lib.is_tensor(a):
         return a.to(device="cuda", dtype=dtype).contiguous()
-    return t.from_numpy(np.ascontiguousarray(np.asarray(a))).to(device="cuda", dtype=dtype)
+    return _lib.to_device(np.asarray(a)).to(dtype=dtype)
 
 
 def _check(st, what):

@@ -272,7 +272,8 @@ class BackwardEulerIntegrator:
             d_in = stage["d_in"]
             for k, arr in enumerate((state.positions, state.velocities, state.f_ext)):
                 # results of an earlier step are views of pinned memory: straight DMA; user arrays stage
-                src = t.from_numpy(np.ascontiguousarray(np.asarray(arr, dtype=np.float64)).reshape(-1))
+                a_ = np.ascontiguousarray(np.asarray(arr, dtype=np.float64)).reshape(-1)
+                src = t.from_numpy(a_ if a_.flags.writeable else a_.copy())
                 d_in[k * n:(k + 1) * n].copy_(src, non_blocking=True)
             x0, v0, fe_state = d_in[:n], d_in[n:2 * n], d_in[2 * n:]
         else:
