@@ -423,10 +423,10 @@ __device__ __forceinline__ void node_body(int64_t I, int64_t N, const int32_t *_
     }
 }
 
-// One launch for both gathers: the first CTAs gather the nodes' f_int / K v /
-// rhs (thread per node), the rest sum the 3x3 blocks (thread per block); the
-// two are independent, so the small node gather overlaps the block gather
-// instead of running after it.
+// One launch for both gathers: node CTAs gather the nodes' f_int / K v / rhs
+// (thread per node), block CTAs sum the 3x3 blocks (thread per block); the two
+// are independent, so the small node gather overlaps the block gather instead
+// of running after it.
 template <bool STVK>
 __global__ void __launch_bounds__(256)
 gather_kernel(int64_t nbc, int64_t nb, int64_t m, const int4 *__restrict__ blk, const int32_t *__restrict__ list,
@@ -438,13 +438,27 @@ gather_kernel(int64_t nbc, int64_t nb, int64_t m, const int4 *__restrict__ blk, 
               const double *__restrict__ mass_diag, const uint8_t *__restrict__ fixed, double hb, double alpha,
               double *__restrict__ f_int, double *__restrict__ kv, double *__restrict__ b,
               double *__restrict__ f_ext, int32_t *__restrict__ flags) {
-    const int64_t nnc = (N + blockDim.x - 1) / blockDim.x;  // node CTAs first: their chains are the longest
-    if ((int64_t)blockIdx.x < nnc)
-        node_body(blockIdx.x * (int64_t)blockDim.x + threadIdx.x, N, node_ptr, node_list, work, x, v, fext_state,
+    // CTA order: each node CTA is followed by the r block CTAs covering about
+    // the same node rows (blocks are in node-row order, ~r blocks per node), so
+    // an element's scratch row is read by its nodes and its blocks while it is
+    // still in L2; leftover block CTAs come last
+    const int64_t nnc = (N + blockDim.x - 1) / blockDim.x;
+    const int64_t r = nnc > 0 ? nbc / nnc : 0;
+    const int64_t bx = blockIdx.x;
+    int64_t node_cta = -1, blk_cta;
+    if (bx < nnc * (r + 1)) {
+        const int64_t g = bx / (r + 1), o = bx % (r + 1);
+        if (o == 0) node_cta = g;
+        blk_cta = g * r + (o - 1);
+    } else {
+        blk_cta = nnc * r + (bx - nnc * (r + 1));
+    }
+    if (node_cta >= 0)
+        node_body(node_cta * (int64_t)blockDim.x + threadIdx.x, N, node_ptr, node_list, work, x, v, fext_state,
                   gravity, mass_diag, fixed, hb, alpha, f_int, kv, b, f_ext, flags);
     else
-        block_body<STVK>((blockIdx.x - nnc) * (int64_t)blockDim.x + threadIdx.x, nb, m, blk, list, work, grads, vol,
-                         share, lam, mu, cm, ck, values);
+        block_body<STVK>(blk_cta * (int64_t)blockDim.x + threadIdx.x, nb, m, blk, list, work, grads, vol, share, lam,
+                         mu, cm, ck, values);
 }
 
 __global__ void __launch_bounds__(128)
