@@ -115,6 +115,7 @@ typedef struct tsb_asm_plan {
     const int32_t *d_fixed_slots; /* [n_fixed_slots]                         */
     double *d_work;             /* [48][m] scratch: [m][36] grads', f_e, K v_e; [m][12] F F^T, S (StVK) */
     int32_t *d_flags;           /* [4] device status words                   */
+    const double *d_gab;        /* [m][10] rest-gradient products g_a.g_b (tsb_assembly_setup) */
 } tsb_asm_plan;
 
 enum { TSB_LAW_COROTATIONAL = 0, TSB_LAW_LINEAR = 1, TSB_LAW_STVK = 2 };
@@ -134,6 +135,9 @@ typedef struct tsb_asm_coeffs {
  * d_values when want_matrix == 0, and for d_b/d_f_ext).  d_flags[0] is set
  * to 1 when a position or deformation gradient is non-finite (ModelError);
  * the caller reads it back when it reads the solve report. */
+/* Plan setup (once per plan): fills d_gab from d_grads. */
+int tsb_assembly_setup(const tsb_asm_plan *plan, void *stream);
+
 int tsb_assemble_corot(const tsb_asm_plan *plan, const tsb_asm_coeffs *coeffs,
                        const double *d_x, const double *d_v, const double *d_f_ext_state,
                        double *d_values, double *d_b, double *d_f_int, double *d_kv,

@@ -42,7 +42,7 @@ class AsmPlan(C.Structure):
         ("d_conn", c_vp), ("d_grads", c_vp), ("d_vol", c_vp), ("d_mass_share", c_vp),
         ("d_rest", c_vp), ("d_mass_diag", c_vp), ("d_gravity", c_vp), ("d_fixed_dof", c_vp),
         ("d_blk", c_vp), ("d_blk_list", c_vp), ("d_node_ptr", c_vp), ("d_node_list", c_vp),
-        ("d_fixed_slots", c_vp), ("d_work", c_vp), ("d_flags", c_vp),
+        ("d_fixed_slots", c_vp), ("d_work", c_vp), ("d_flags", c_vp), ("d_gab", c_vp),
     ]
 
 
@@ -106,6 +106,7 @@ _SIGNATURES = {
     "tsb_spmv": (C.c_int, [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "tsb_csr_diagonal": (C.c_int, [c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "tsb_compress": (C.c_int, [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp]),
+    "tsb_assembly_setup": (C.c_int, [C.POINTER(AsmPlan), c_vp]),
     "tsb_assemble_corot": (C.c_int, [C.POINTER(AsmPlan), C.POINTER(AsmCoeffs), c_vp, c_vp, c_vp,
                                      c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "tsb_element_blocks": (C.c_int, [C.POINTER(AsmPlan), C.POINTER(AsmCoeffs), c_vp, c_vp, c_vp]),

@@ -184,6 +184,7 @@ class AssemblyPlan:
             fd[fixed_dof] = 1
         self.fixed_dof = up(fd, np.uint8)
         self.work = t.empty(max(m, 1) * 48, dtype=t.float64, device=dev)
+        self.gab = t.empty(max(m, 1) * 10, dtype=t.float64, device=dev)  # g_a . g_b per tet (tsb_assembly_setup)
         self.flags = t.zeros(4, dtype=t.int32, device=dev)
         self.pattern = pattern
         if pattern is not None:
@@ -209,7 +210,11 @@ class AssemblyPlan:
             d_fixed_dof=P(self.fixed_dof), d_blk=P(self.blk), d_blk_list=P(self.blk_list),
             d_node_ptr=P(self.node_ptr), d_node_list=P(self.node_list),
             d_fixed_slots=P(self.fixed_slots), d_work=P(self.work), d_flags=P(self.flags),
+            d_gab=P(self.gab),
         )
+        import ctypes as C
+
+        _lib.check(_lib.load().tsb_assembly_setup(C.byref(self.c), _lib.stream_ptr()), "assembly_setup")
         self.lame = precomp.lame
 
     @classmethod

@@ -305,10 +305,32 @@ __device__ __forceinline__ void load_aux(const double *__restrict__ work, int64_
     }
 }
 
+// slot of the symmetric pair (a, b) in a tet's 10 rest-gradient products
+__device__ __forceinline__ int gab_slot(int a, int b) {
+    const int lo = a < b ? a : b, hi = a < b ? b : a;
+    return lo * 4 - lo * (lo - 1) / 2 + (hi - lo);  // (0,0..3) 0..3, (1,1..3) 4..6, (2,2..3) 7..8, (3,3) 9
+}
+
+// gab[e][slot(a, b)] = g_a . g_b (plan setup; the same expression the block
+// gather evaluated per contribution)
+__global__ void gab_kernel(int64_t m, const double *__restrict__ grads, double *__restrict__ gab) {
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e >= m) return;
+    double g[12];
+#pragma unroll
+    for (int t = 0; t < 12; ++t) g[t] = grads[e * 12 + t];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = a; b < 4; ++b)
+            gab[e * 10 + gab_slot(a, b)] = g[3 * a] * g[3 * b] + g[3 * a + 1] * g[3 * b + 1] + g[3 * a + 2] * g[3 * b + 2];
+}
+
 template <bool STVK>
 __device__ __forceinline__ void block_body(int64_t bi, int64_t nb, int64_t m, const int4 *__restrict__ blk,
                                            const int32_t *__restrict__ list, const double *__restrict__ work,
-                                           const double *__restrict__ grads, const double *__restrict__ vol,
+                                           const double *__restrict__ grads, const double *__restrict__ gab,
+                                           const double *__restrict__ vol,
                                            const double *__restrict__ share, double lam, double mu, double cm,
                                            double ck, double *__restrict__ values) {
     if (bi >= nb) return;
@@ -344,11 +366,18 @@ __device__ __forceinline__ void block_body(int64_t bi, int64_t nb, int64_t m, co
             for (int i = 0; i < 3; ++i) {
                 ga[u][i] = __ldg(we + 3 * a + i);
                 gb[u][i] = __ldg(we + 3 * b + i);
-                ra[u][i] = __ldg(grads + e * 12 + 3 * a + i);
-                rb[u][i] = __ldg(grads + e * 12 + 3 * b + i);
             }
-            if constexpr (STVK) load_aux(work, m, e, aux[u]);
-            G[u] = ra[u][0] * rb[u][0] + ra[u][1] * rb[u][1] + ra[u][2] * rb[u][2];
+            if constexpr (STVK) {
+#pragma unroll
+                for (int i = 0; i < 3; ++i) {
+                    ra[u][i] = __ldg(grads + e * 12 + 3 * a + i);
+                    rb[u][i] = __ldg(grads + e * 12 + 3 * b + i);
+                }
+                load_aux(work, m, e, aux[u]);
+                G[u] = 0.0;
+            } else {  // g_a . g_b of the rest gradients, tabulated once per plan
+                G[u] = __ldg(gab + e * 10 + gab_slot(a, b));
+            }
             V[u] = __ldg(vol + e);
         }
 #pragma unroll
@@ -430,7 +459,8 @@ __device__ __forceinline__ void node_body(int64_t I, int64_t N, const int32_t *_
 template <bool STVK>
 __global__ void __launch_bounds__(256)
 gather_kernel(int64_t nbc, int64_t nb, int64_t m, const int4 *__restrict__ blk, const int32_t *__restrict__ list,
-              const double *__restrict__ work, const double *__restrict__ grads, const double *__restrict__ vol,
+              const double *__restrict__ work, const double *__restrict__ grads, const double *__restrict__ gab,
+              const double *__restrict__ vol,
               const double *__restrict__ share, double lam, double mu, double cm, double ck,
               double *__restrict__ values, int64_t N, const int32_t *__restrict__ node_ptr,
               const int32_t *__restrict__ node_list, const double *__restrict__ x, const double *__restrict__ v,
@@ -457,8 +487,8 @@ gather_kernel(int64_t nbc, int64_t nb, int64_t m, const int4 *__restrict__ blk, 
         node_body(node_cta * (int64_t)blockDim.x + threadIdx.x, N, node_ptr, node_list, work, x, v, fext_state,
                   gravity, mass_diag, fixed, hb, alpha, f_int, kv, b, f_ext, flags);
     else
-        block_body<STVK>(blk_cta * (int64_t)blockDim.x + threadIdx.x, nb, m, blk, list, work, grads, vol, share, lam,
-                         mu, cm, ck, values);
+        block_body<STVK>(blk_cta * (int64_t)blockDim.x + threadIdx.x, nb, m, blk, list, work, grads, gab, vol, share,
+                         lam, mu, cm, ck, values);
 }
 
 __global__ void __launch_bounds__(128)
@@ -548,7 +578,7 @@ extern "C" int tsb_assemble_corot(const tsb_asm_plan *p, const tsb_asm_coeffs *c
             auto kern = c->law == TSB_LAW_STVK ? gather_kernel<true> : gather_kernel<false>;
             kern<<<(unsigned)(nbc + nnc), 256, 0, s>>>(
                 nbc, p->n_blocks, p->n_elems, reinterpret_cast<const int4 *>(p->d_blk), p->d_blk_list, p->d_work,
-                p->d_grads, p->d_vol, p->d_mass_share, c->lam, c->mu, c->cm, c->ck, d_values, p->n_nodes,
+                p->d_grads, p->d_gab, p->d_vol, p->d_mass_share, c->lam, c->mu, c->cm, c->ck, d_values, p->n_nodes,
                 p->d_node_ptr, p->d_node_list, d_x, d_v, d_f_ext_state, p->d_gravity, p->d_mass_diag,
                 p->d_fixed_dof, c->h + c->rayleigh_stiffness, c->rayleigh_mass, d_f_int, d_kv, d_b, d_f_ext,
                 p->d_flags);
@@ -586,6 +616,19 @@ extern "C" int tsb_advance(int64_t n_dof, const double *d_accel, const double *d
         if (g > kNumSM * 8) g = kNumSM * 8;
         advance_kernel<<<g, 256, 0, as_stream(stream)>>>(n_dof, d_accel, d_v, d_x, d_fixed_dof, h,
                                                          d_acc_out, d_v_out, d_x_out, d_flags);
+        TSB_LAUNCHED();
+    });
+}
+
+// Plan setup: the rest-gradient products g_a . g_b per tet into d_gab
+// ([m][10]), read by the block gather instead of the two gradient rows.
+extern "C" int tsb_assembly_setup(const tsb_asm_plan *p, void *stream) {
+    using namespace tsb;
+    return guard([&] {
+        if (p == nullptr || p->d_gab == nullptr) throw Error(TSB_E_ARG, "plan without a g_a.g_b table");
+        if (p->n_elems <= 0) return;
+        gab_kernel<<<grid_for(p->n_elems, 128), 128, 0, as_stream(stream)>>>(p->n_elems, p->d_grads,
+                                                                             const_cast<double *>(p->d_gab));
         TSB_LAUNCHED();
     });
 }
