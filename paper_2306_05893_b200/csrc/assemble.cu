@@ -174,7 +174,7 @@ __device__ __forceinline__ void stvk_element(int64_t e, int64_t m, const double 
     aux[5] = make_double2(S[5], S[8]);
 }
 
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(128, 4)
 elem_kernel(int64_t m, const int32_t *__restrict__ conn, const double *__restrict__ grads,
             const double *__restrict__ vol, const double *__restrict__ rest,
             const double *__restrict__ x, const double *__restrict__ v, double lam, double mu,
