@@ -58,6 +58,14 @@ SEG_PAIRS = 96          # pairs per segment item of a large tile (96 * 32 * 16 B
 WARPS = 8               # warps per CTA (csrc kSweepBlock / 32)
 MERGE_ROWS = 0          # default subtree amalgamation (rows); 0 = off
 CB_CAP = 2048           # contributions staged per piece when a block's items sum them (csrc max_cb)
+# lower input mode: a block's items sum their contributions themselves while the
+# redundant reads (items x contributions) stay below ratio x its factor entries,
+# else finaliser items form x_b once.  Latency-bound (small) factors favour the
+# item gathers (one hop less), bandwidth-bound (large) ones the finalisers (no
+# redundant reads): measured apply cfg2 0.142 ms (ratio 1) vs 0.161 (0), cfg3
+# 1.82 ms (1) vs 1.70 (0).  TSB_GATHER_RATIO overrides.
+GATHER_RATIO = float(os.environ["TSB_GATHER_RATIO"]) if "TSB_GATHER_RATIO" in os.environ else None
+GATHER_BIG_BYTES = 512 << 20  # stored lower tiles above this: bandwidth-bound regime
 
 BLOCK_DTYPE = np.dtype([
     ("start", "<i4"), ("m", "<i4"), ("na", "<i4"), ("parent", "<i4"),
@@ -463,7 +471,9 @@ def pack(factors, subset=None):
     blk_contrib = np.array([int(contrib[bf.start:bf.stop].sum()) for bf in bfs], dtype=np.int64)
     gsize = np.array([int(tables[False]["np"][f:f + len(t)].sum()) * TILE * 2 for f, t in blk_tiles[False]],
                      dtype=np.int64)
-    mode = np.where(target_l == 0, MODE_LEAF, np.where(nl * blk_contrib <= gsize, MODE_GATHER, MODE_FIN))
+    ratio = GATHER_RATIO if GATHER_RATIO is not None else (0.0 if pos[False] * 8 > GATHER_BIG_BYTES else 1.0)
+    mode = np.where(target_l == 0, MODE_LEAF,
+                    np.where(nl * blk_contrib <= ratio * gsize, MODE_GATHER, MODE_FIN))
     nfin = np.where(mode == MODE_FIN,
                     np.minimum(np.minimum(32, (ms_ + 31) // 32), np.maximum(1, (blk_contrib + FIN_CONTRIB - 1) // FIN_CONTRIB)),
                     0)
