@@ -207,6 +207,30 @@ def time_spmv(W, reps, flush):
     return dict(ms=ms, bytes=byts, gbs=byts / (ms * 1e-3) / 1e9, nnz=a.nnz)
 
 
+def time_assembly(W, reps, flush):
+    """Fused device assembly of the step (elem + gather launches), CUDA events, L2 flushed."""
+    import torch
+
+    integ, st = W["integ"], W["state"]
+    x, v, fe = (integ._flat_dev(a) for a in (st.positions, st.velocities, st.f_ext))
+    for _ in range(3):
+        integ._assemble_device(x, v, fe)
+    ts = []
+    for _ in range(reps):
+        flush()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        integ._assemble_device(x, v, fe)
+        e1.record()
+        e1.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    ms = statistics.median(ts)
+    mesh = W["mesh"]
+    nnz = len(integ.assembler.pattern["col_ind"])
+    byts = 8 * nnz + mesh.element_count * (16 + 104 + 64) + mesh.node_count * 144  # SURVEY.md 8(d)
+    return dict(ms=ms, bytes=byts, gbs=byts / (ms * 1e-3) / 1e9)
+
+
 FP64_PEAK_TFLOPS = 37.0  # DMMA (the refactorisation's tile path), measured on this B200 (tools/ubench_fp64.cu); not in MEASURED_PEAKS.json
 
 
@@ -677,6 +701,7 @@ def main():
     total_ms = float(t_local.item())
     apply_r = time_apply(W, 20, flush)
     spmv_r = time_spmv(W, 20, flush)
+    asm_r = time_assembly(W, 20, flush)
     e2e_r = time_e2e(W, args.precond, max(5, min(args.steps, 30)))
     refac_r = time_refactor(W)
     async_r = time_async_device(W, max(10, min(args.steps, 30)), flush)
@@ -712,6 +737,8 @@ def main():
         "trisolve": {"apply_ms": apply_r["ms"], "gbs": apply_r["gbs"], "frac": apply_r["gbs"] / hbm,
                      "algorithmic_bytes": apply_r["bytes"], "stored_bytes": apply_r["stored_bytes"]},
         "spmv": {"ms": spmv_r["ms"], "gbs": spmv_r["gbs"], "frac": spmv_r["gbs"] / hbm},
+        "assembly": {"ms": asm_r["ms"], "gbs": asm_r["gbs"], "frac": asm_r["gbs"] / hbm,
+                     "algorithmic_bytes": asm_r["bytes"]},
         "roofline": {"bound": "hbm", "kernel": "ldlt apply (level-scheduled L and L^T sweeps)",
                      "achieved": apply_r["gbs"], "peak": hbm, "peak_kind": pk_kind, "unit": "GB/s",
                      "frac": apply_r["gbs"] / hbm, "traffic": traffic},
