@@ -188,27 +188,33 @@ __global__ void __launch_bounds__(256) extend_kernel(const tsb_front_pair *__res
 }
 
 // Pivot tile k: W_kk = C_kk^-1 and diag(C_kk) by in-place Gauss-Jordan style
-// elimination in shared memory (one CTA of 256 threads per front).  X starts
-// as the full symmetric tile; step j eliminates column j from rows i > j with
-// the unscaled row j (m_i = X_ij / p_j): the trailing A part and the inverse
-// part (columns < j) update uniformly as X_it -= m_i X_jt, and the inverse
-// entry born at (i, j) is -m_i, stored where the eliminated A entry was.  Row
-// j of the inverse is scaled by p_j^-1/2 one step later, so X's lower
-// triangle ends as D^-1/2 L^-1 = C^-1.  Only diag(C) and C^-1 of the pivot
-// tile are consumed downstream (panel, right solve, pack).
+// elimination (one CTA of 256 threads per front).  X starts as the full
+// symmetric tile; step j eliminates column j from rows i > j with the unscaled
+// row j (m_i = X_ij / p_j): the trailing A part and the inverse part (columns
+// < j) update uniformly as X_it -= m_i X_jt, and the inverse entry born at
+// (i, j) is -m_i, stored where the eliminated A entry was.  Row j is never
+// read after step j, so every row of the inverse is scaled by p^-1/2 at the
+// end, and X's lower triangle ends as D^-1/2 L^-1 = C^-1.  Only diag(C) and C^-1 of the pivot tile are
+// consumed downstream (panel, right solve, pack).
+//
+// The tile lives in registers: thread (a = tid & 63, g = tid >> 6) owns row a,
+// columns g + 4u (u < 16).  A step is one barrier: the owners of column j and
+// row j publish them into a double-buffered pair of shared vectors, then every
+// thread updates its 16 entries.  The 64 steps are unrolled so the register
+// index of column / row j is static.
 constexpr int kDiagLd = 65;
-constexpr int kDiagSmem = (NB * kDiagLd + 3 * NB) * (int)sizeof(double);
+constexpr int kDiagSmem = (NB * kDiagLd + 4 * NB) * (int)sizeof(double);
 
-__global__ void __launch_bounds__(256) diag_kernel(const tsb_front *__restrict__ F, const int4 *__restrict__ list,
+__global__ void __launch_bounds__(256, 1) diag_kernel(const tsb_front *__restrict__ F, const int4 *__restrict__ list,
                                                    int k, double *__restrict__ ws, double *__restrict__ inv,
                                                    int32_t *__restrict__ ctl) {
     extern __shared__ __align__(16) double sm[];
-    double *X = sm, *mv = sm + NB * kDiagLd, *dsq = mv + NB, *rsq = dsq + NB;
+    double *X = sm, *colb = sm + NB * kDiagLd, *rowb = colb + 2 * NB;
     const int fi = __ldg(&list[blockIdx.x].x);
     const tsb_front f = F[fi];
     const int c0 = k * NB, w = min(NB, f.m - c0);
     double *base = ws + f.off + (int64_t)c0 * f.nf + c0;
-    const int tid = threadIdx.x, t = tid & (NB - 1), rg = tid >> 6;
+    const int tid = threadIdx.x, a = tid & (NB - 1), g = tid >> 6;
     {
         double v[NB * NB / kThreads];  // all 16 loads in flight together
 #pragma unroll
@@ -223,46 +229,62 @@ __global__ void __launch_bounds__(256) diag_kernel(const tsb_front *__restrict__
         }
     }
     __syncthreads();
-    for (int j = 0; j < w; ++j) {
-        // phase 1: multipliers of column j, pivot, scaling of row j-1 of the inverse
-        const double p = X[j * kDiagLd + j];
-        if (tid < NB) {
-            const int i = j + 1 + tid;
-            if (i < w) mv[i] = X[i * kDiagLd + j] * __drcp_rn(p);
-        } else if (tid < 2 * NB) {
-            const int c = tid - NB;
-            if (j > 0 && c < j) X[(j - 1) * kDiagLd + c] *= (c == j - 1) ? 1.0 : rsq[j - 1];
-        } else if (tid == 2 * NB) {
-            if (!(p > 0.0)) atomicCAS(ctl, 0, fi + 1);
-            dsq[j] = sqrt(p);
-            rsq[j] = 1.0 / dsq[j];
-        }
-        __syncthreads();
-        if (tid == 2 * NB) X[j * kDiagLd + j] = rsq[j];  // W_jj = p_j^-1/2 (unscaled 1)
-        // phase 2: rows i = j + 1 + rg + 4u, column t; loads before stores
-        const double xj = X[j * kDiagLd + t];
-        double m[16], xv[16];
+    double x[16], piv = 1.0;
 #pragma unroll
-        for (int u = 0; u < 16; ++u) {
-            const int i = j + 1 + rg + 4 * u;
-            const bool ok = i < w;
-            m[u] = ok ? mv[i] : 0.0;
-            xv[u] = ok ? X[i * kDiagLd + t] : 0.0;
-        }
+    for (int u = 0; u < 16; ++u) x[u] = X[a * kDiagLd + g + 4 * u];
 #pragma unroll
-        for (int u = 0; u < 16; ++u) {
-            const int i = j + 1 + rg + 4 * u;
-            if (i < w) X[i * kDiagLd + t] = (t == j) ? -m[u] : fma(-m[u], xj, xv[u]);
+    for (int uj = 0; uj < 16; ++uj) {
+#pragma unroll
+        for (int ph = 0; ph < 4; ++ph) {
+            const int j = 4 * uj + ph;
+            if (j >= w) break;
+            double *cb = colb + (j & 1) * NB, *rb = rowb + (j & 1) * NB;
+            if (g == ph) cb[a] = x[uj];  // column j
+            if (a == j) {
+#pragma unroll
+                for (int u = 0; u < 16; u += 2)  // row j, column g + 4u at rb[16 g + u]
+                    *reinterpret_cast<double2 *>(rb + 16 * g + u) = make_double2(x[u], x[u + 1]);
+            }
+            __syncthreads();
+            const double p = rb[16 * ph + uj];
+            if (a > j) {
+                double r[16];
+#pragma unroll
+                for (int u = 0; u < 16; u += 2) {
+                    const double2 t = *reinterpret_cast<const double2 *>(rb + 16 * g + u);
+                    r[u] = t.x;
+                    r[u + 1] = t.y;
+                }
+                const double m = cb[a] * __drcp_rn(p);
+#pragma unroll
+                for (int u = 0; u < 16; ++u) {
+                    if (u == uj && g == ph) x[u] = -m;  // inverse entry born at (a, j)
+                    else x[u] = fma(-m, r[u], x[u]);
+                }
+            } else if (a == j) {
+                piv = p;
+            }
         }
-        __syncthreads();
     }
-    if (tid < w - 1) X[(w - 1) * kDiagLd + tid] *= rsq[w - 1];
-    if (tid < w) base[(int64_t)tid * f.nf + tid] = dsq[tid];  // diag(C); the pack and d read it
-    __syncthreads();
+    // row a of the inverse: scale by p_a^-1/2 (row a is final once step a used it)
+    if (a < w) {
+        const double dsq = sqrt(piv), rsq = 1.0 / dsq;
+        if (g == (a & 3)) {
+            if (!(piv > 0.0)) atomicCAS(ctl, 0, fi + 1);
+            base[(int64_t)a * f.nf + a] = dsq;  // diag(C); the pack and d read it
+        }
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+            const int c = g + 4 * u;
+            if (c < a) x[u] *= rsq;
+            else if (c == a) x[u] = rsq;  // W_aa = p_a^-1/2
+        }
+    }
     double *wo = inv + f.ioff + (int64_t)k * NB * NB;
-    for (int i = tid; i < NB * NB; i += kThreads) {
-        const int r = i & (NB - 1), c = i >> 6;
-        wo[c * NB + r] = (r < w && c <= r) ? X[r * kDiagLd + c] : 0.0;  // W(r, c), column-major
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+        const int c = g + 4 * u;
+        wo[c * NB + a] = (a < w && c <= a) ? x[u] : 0.0;  // W(a, c), column-major
     }
 }
 
