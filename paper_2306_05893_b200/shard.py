@@ -161,8 +161,92 @@ def local_matrix(row_ptr, col_ind, values, plan: ShardPlan, rank: int):
 
 
 # ---------------------------------------------------------------------------
+# sharded assembly (SURVEY.md 8e "Assembly"): each rank assembles only its
+# elements; owned rows come out complete, top-separator rows as partial sums
+# that the SpMV's top-row all-reduce adds up.
+# ---------------------------------------------------------------------------
+
+def node_ranks(plan: ShardPlan, perm) -> np.ndarray:
+    """Rank owning each mesh node (-1: a replicated top-separator node); the
+    dissection orders whole nodes (expand_plan), so a node's dofs agree."""
+    perm = np.asarray(perm)
+    ro = np.empty(len(perm), dtype=np.int64)
+    ro[perm] = plan.row_owner  # original dof -> owner
+    ro = ro.reshape(-1, 3)
+    if np.any(ro != ro[:, :1]):
+        raise ValueError("a node's dofs are split across ranks")
+    return ro[:, 0].copy()
+
+
+def element_ranks(elements, node_rank: np.ndarray) -> np.ndarray:
+    """Rank assembling each element: the rank of its non-separator nodes (all
+    the same: a tet spanning two subtrees would be an uncut edge), rank 0 for
+    elements entirely inside the top separators."""
+    nr = node_rank[np.asarray(elements)]
+    hi, lo = nr.max(axis=1), np.where(nr >= 0, nr, np.iinfo(np.int64).max).min(axis=1)
+    if np.any((hi >= 0) & (lo != hi)):
+        raise ValueError("an element spans two ranks' subtrees: not a dissection cut")
+    return np.where(hi >= 0, hi, 0)
+
+
+def rank_mesh(mesh, plan: ShardPlan, perm, rank: int):
+    """(mesh of rank `rank`'s elements over all nodes, node ranks): what the
+    rank's integrator assembles; its owned rows are the full assembly's."""
+    from .mesh import Mesh
+
+    nr = node_ranks(plan, perm)
+    er = element_ranks(mesh.elements, nr)
+    return Mesh(mesh.nodes, np.asarray(mesh.elements)[er == rank], mesh.element_kind, mesh.fixed_nodes), nr
+
+
+def rank_f_ext(f_ext, node_rank: np.ndarray, rank: int) -> np.ndarray:
+    """The state's external forces as rank `rank` passes them to its partial
+    assembly: its owned nodes, plus the top nodes on rank 0 (counted once)."""
+    keep = (node_rank == rank) | ((node_rank < 0) & (rank == 0))
+    return np.where(np.repeat(keep, 3), np.asarray(f_ext, dtype=np.float64).reshape(-1), 0.0)
+
+
+def local_system(row_ptr, col_ind, values, b, plan: ShardPlan, perm, rank: int, fixed_dofs):
+    """Rank-local permuted CSR and rhs from the rank's partial assembly (its
+    elements only, original dof order): owned rows kept as assembled
+    (complete), top rows kept as partial sums, pinned top rows (identity) kept
+    on rank 0 only, every other row dropped.  The sum over ranks of the local
+    matrices is P A P^T; owned rows are bit-identical to the full assembly's."""
+    from .assembly import CsrMatrix
+
+    perm = np.asarray(perm)
+    n = len(perm)
+    rp, ci, va = permuted_matrix(CsrMatrix(n, n, row_ptr, col_ind, values), perm)
+    iperm = np.empty(n, dtype=np.int64)
+    iperm[perm] = np.arange(n)
+    pinned = np.zeros(n, dtype=bool)
+    pinned[iperm[np.asarray(fixed_dofs, dtype=np.int64)]] = True
+    ro = plan.row_owner
+    rows = np.repeat(np.arange(n), np.diff(rp))
+    keep = (ro[rows] == rank) | ((ro[rows] < 0) & (~pinned[rows] | (rank == 0)))
+    lrp = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(np.bincount(rows[keep], minlength=n), out=lrp[1:])
+    bp = np.asarray(b, dtype=np.float64)[perm]
+    lb = np.where((ro == rank) | (ro < 0), bp, 0.0)
+    return lrp, ci[keep], va[keep], lb
+
+
+# ---------------------------------------------------------------------------
 # CPU emulation of the distributed loop (world_size > 1 tests over gloo)
 # ---------------------------------------------------------------------------
+
+def _sharded_rhs(lb, plan: ShardPlan, perm, allreduce):
+    """Original-order rhs as a rank's solve consumes it: owned rows as
+    assembled, top rows summed over ranks (other rows are never read)."""
+    top = plan.top_rows
+    seg = np.array(lb[top], dtype=np.float64)
+    allreduce(seg)
+    bp = np.array(lb, dtype=np.float64)
+    bp[top] = seg
+    out = np.empty_like(bp)
+    out[np.asarray(perm)] = bp
+    return out
+
 
 def _lower_blocks(factors, idx, r, ext=None):
     """Forward sweep over the blocks `idx` (start order): y = L^{-1} r on their
@@ -203,14 +287,20 @@ def _upper_blocks(factors, idx, w, z):
     return z
 
 
-def emulate_pcg(a, b, factors, plan: ShardPlan, rank: int, allreduce, tol=1e-9, max_it=1000):
+def emulate_pcg(a, b, factors, plan: ShardPlan, rank: int, allreduce, tol=1e-9, max_it=1000, local=None):
     """One rank of the distributed PCG, NumPy kernels; `allreduce(np.ndarray)`
     sums over ranks in place.  Works in permuted order like the device loop;
-    returns (x in original order, iterations, final residual, converged)."""
+    returns (x in original order, iterations, final residual, converged).
+    local=(row_ptr, col_ind, values, b) from local_system (sharded assembly)
+    replaces a and b: the top rows of b are all-reduced first."""
     perm = np.asarray(factors.plan.perm)
     n = len(perm)
-    rp, ci, va = permuted_matrix(a, perm)
-    lrp, lci, lva = local_matrix(rp, ci, va, plan, rank)
+    if local is not None:
+        lrp, lci, lva, lb = local
+        b = _sharded_rhs(lb, plan, perm, allreduce)
+    else:
+        rp, ci, va = permuted_matrix(a, perm)
+        lrp, lci, lva = local_matrix(rp, ci, va, plan, rank)
     wgt = plan.weights(rank)
     top = plan.top_rows
     mine = [i for i in range(len(factors.blocks)) if plan.owner[i] == rank]
@@ -373,7 +463,7 @@ class DistributedPcg:
     defaults to torch.distributed.all_reduce (NCCL over NVLink between GPUs).
     """
 
-    def __init__(self, a, factors, rank=None, world=None, allreduce=None, grid=0, exchange="nccl"):
+    def __init__(self, a, factors, rank=None, world=None, allreduce=None, grid=0, exchange="nccl", local=None):
         from . import _lib
         from ._ldlt_pack import DevicePanels
 
@@ -392,8 +482,14 @@ class DistributedPcg:
         self.plan = shard_blocks(factors, world)
         perm = np.asarray(factors.plan.perm)
         self.n = n = len(perm)
-        rp, ci, va = permuted_matrix(a, perm)
-        lrp, lci, lva = local_matrix(rp, ci, va, self.plan, rank)
+        # local=(row_ptr, col_ind, values, b) from local_system: this rank's share of a
+        # sharded assembly (owned rows complete, top rows partial); a is not needed
+        self._lb = None
+        if local is not None:
+            lrp, lci, lva, self._lb = local
+        else:
+            rp, ci, va = permuted_matrix(a, perm)
+            lrp, lci, lva = local_matrix(rp, ci, va, self.plan, rank)
         dev = lambda x, dt: t.from_numpy(np.ascontiguousarray(x, dtype=dt)).cuda()  # noqa: E731
         self.rp, self.ci, self.va = dev(lrp, np.int32), dev(lci, np.int32), dev(lva, np.float64)
         self.w = dev(self.plan.weights(rank), np.float64)
@@ -468,13 +564,20 @@ class DistributedPcg:
             self.S.run("upper_scaled", v["y"], out)
 
     # -- solve -----------------------------------------------------------------
-    def solve(self, b, tol=1e-9, max_it=1000):
-        """-> (x in original order as a CUDA tensor, iterations, residual, converged)."""
+    def solve(self, b=None, tol=1e-9, max_it=1000):
+        """-> (x in original order as a CUDA tensor, iterations, residual, converged).
+        b=None with a sharded assembly: the rank's partial rhs, top rows all-reduced."""
         L, t = self._L, self._L.torch()
         v, n = self.v, self.n
-        bd = b if L.is_tensor(b) else t.from_numpy(np.ascontiguousarray(b, dtype=np.float64)).cuda()
         s = L.stream_ptr()
-        L.check(self._lib.tsb_gather_rows(n, L.ptr(self.perm), L.ptr(bd), L.ptr(v["b"]), s), "gather")
+        if b is None:
+            if self._lb is None:
+                raise ValueError("solve() needs b unless built from a sharded assembly (local=)")
+            v["b"].copy_(t.from_numpy(np.ascontiguousarray(self._lb, dtype=np.float64)))
+            self._exchange_top(v["b"])
+        else:
+            bd = b if L.is_tensor(b) else t.from_numpy(np.ascontiguousarray(b, dtype=np.float64)).cuda()
+            L.check(self._lib.tsb_gather_rows(n, L.ptr(self.perm), L.ptr(bd), L.ptr(v["b"]), s), "gather")
         v["r"].copy_(v["b"])
         v["x"].zero_()
         self._dot(v["b"], v["b"], 4)

@@ -79,3 +79,66 @@ def test_two_ranks_match_the_oracle(exchange):
     for rank, x, it, res, conv in outs:
         assert conv and it == oit, (rank, x if isinstance(x, str) else it, oit)
         assert np.abs(x - ox).max() <= 1e-10 * np.abs(ox).max()
+
+
+def _worker_sharded(rank, world, port, q, exchange):
+    import torch
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), TSB_SHARED_DEVICE="1")
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2306_05893_b200 as P
+        from paper_2306_05893_b200 import shard as S
+        from paper_2306_05893_b200.integrator import BackwardEulerIntegrator, IntegratorConfig, SimState
+        from test_shard_assembly import DT, G, _case
+
+        mesh, f, x, v, fe = _case()
+        sp = S.shard_blocks(f, world)
+        perm = f.plan.perm
+        sub, nr = S.rank_mesh(mesh, sp, perm, rank)
+        integ = BackwardEulerIntegrator(sub, P.make_model("corotational", sub, P.MaterialParams(1e5, 0.3, 1000.0)),
+                                        IntegratorConfig(dt=DT, gravity=G))
+        n = mesh.ndof
+        st = SimState(x.copy(), v.copy(), np.zeros_like(x), np.zeros(n), S.rank_f_ext(fe, nr, rank))
+        a, b, _ = integ.assemble_system(st)
+        host = lambda z: z.cpu().numpy() if hasattr(z, "cpu") else np.asarray(z)  # noqa: E731
+        fixed = (3 * np.asarray(mesh.fixed_nodes)[:, None] + np.arange(3)).ravel()
+        local = S.local_system(host(a.row_ptr), host(a.col_ind), host(a.values), host(b), sp, perm, rank, fixed)
+        xs, it, res, conv = S.DistributedPcg(None, f, rank=rank, world=world, grid=32, exchange=exchange,
+                                             local=local).solve(None, 1e-9, 200)
+        q.put((rank, xs.cpu().numpy(), it, res, conv))
+    except Exception as e:  # surface the failure in the parent
+        import traceback
+
+        q.put((rank, repr(e) + traceback.format_exc(), -1, 0.0, False))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("exchange", ["nccl", "peer"])
+def test_two_ranks_sharded_device_assembly(exchange):
+    """Each rank assembles only its subtree's elements on the device
+    (shard.rank_mesh / local_system); the distributed PCG over the partial
+    systems matches the oracle PCG on the full assembly."""
+    import torch.multiprocessing as mp
+    from oracle import tetsim_oracle as O
+    from test_shard_assembly import _case, _full
+
+    mesh, f, x, v, fe = _case()
+    full = _full(mesh, x, v, fe)
+    ox, oit, _, _ = O.pcg(full["row_ptr"], full["col_ind"], full["values"], full["b"],
+                          lambda r: O.apply(f, r), 1e-9, 200)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_sharded, args=(r, 2, port, q, exchange)) for r in range(2)]
+    for p in procs:
+        p.start()
+    outs = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, xs, it, res, conv in outs:
+        assert conv and it == oit, (rank, xs if isinstance(xs, str) else it, oit)
+        assert np.abs(xs - ox).max() <= 1e-10 * np.abs(ox).max()
