@@ -22,6 +22,7 @@
 // (paper_2306_05893_b200/refactor.py).  All sums run in a fixed order: the
 // result is bit-reproducible run to run.
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "tsb_common.cuh"
@@ -452,6 +453,15 @@ struct tsb_refactor {
     std::vector<int64_t> prog;
     cudaStream_t side = nullptr;
     std::vector<cudaEvent_t> ev;  // [0] start, [1] side done, [2 + i] program events
+    // the program captured once per (values, g, gt, d) as a CUDA graph and replayed
+    // on an internal stream (capture works whatever stream the caller uses)
+    struct Graph {
+        const void *key[4];
+        cudaGraphExec_t exec;
+    };
+    std::vector<Graph> graphs;
+    cudaStream_t cap = nullptr;
+    cudaEvent_t gev[2] = {nullptr, nullptr};  // caller -> graph, graph -> caller
 };
 
 extern "C" int tsb_refactor_create(const tsb_refactor_desc *desc, tsb_refactor_t *out) {
@@ -486,19 +496,22 @@ extern "C" int tsb_refactor_create(const tsb_refactor_desc *desc, tsb_refactor_t
 extern "C" int tsb_refactor_destroy(tsb_refactor_t h) {
     if (h != nullptr) {
         for (auto e : h->ev) cudaEventDestroy(e);
+        for (auto &g : h->graphs) cudaGraphExecDestroy(g.exec);
+        for (auto e : h->gev)
+            if (e) cudaEventDestroy(e);
+        if (h->cap) cudaStreamDestroy(h->cap);
         if (h->side) cudaStreamDestroy(h->side);
     }
     delete h;
     return TSB_OK;
 }
 
-extern "C" int tsb_refactor_run(tsb_refactor_t h, const double *d_values, double *d_g, double *d_gt, double *d_d,
-                                void *stream) {
-    using namespace tsb;
-    using namespace tsb::rf;
-    return guard([&] {
-        if (h == nullptr) throw Error(TSB_E_ARG, "null refactor handle");
-        cudaStream_t s0 = as_stream(stream);
+namespace tsb {
+namespace rf {
+
+// Enqueue the whole program on s0 (+ the handle's side stream, joined back).
+static void enqueue_program(tsb_refactor *h, const double *d_values, double *d_g, double *d_gt, double *d_d,
+                            cudaStream_t s0) {
         const tsb_refactor_desc &D = h->d;
         const int4 *lists = reinterpret_cast<const int4 *>(D.d_lists);
         TSB_CUDA(cudaMemsetAsync(D.d_ctl, 0, sizeof(int32_t), s0));
@@ -594,5 +607,66 @@ extern "C" int tsb_refactor_run(tsb_refactor_t h, const double *d_values, double
         }
         TSB_CUDA(cudaEventRecord(h->ev[1], h->side));  // everything on the side stream before the caller goes on
         TSB_CUDA(cudaStreamWaitEvent(s0, h->ev[1], 0));
+}
+
+static bool use_graph() {
+    static const bool v = [] {
+        const char *e = getenv("TSB_RF_GRAPH");
+        return e == nullptr || atoi(e) != 0;
+    }();
+    return v;
+}
+
+}  // namespace rf
+}  // namespace tsb
+
+extern "C" int tsb_refactor_run(tsb_refactor_t h, const double *d_values, double *d_g, double *d_gt, double *d_d,
+                                void *stream) {
+    using namespace tsb;
+    using namespace tsb::rf;
+    return guard([&] {
+        if (h == nullptr) throw Error(TSB_E_ARG, "null refactor handle");
+        cudaStream_t s0 = as_stream(stream);
+        if (!use_graph()) {
+            enqueue_program(h, d_values, d_g, d_gt, d_d, s0);
+            return;
+        }
+        const void *key[4] = {d_values, d_g, d_gt, d_d};
+        cudaGraphExec_t exec = nullptr;
+        for (auto &g : h->graphs)
+            if (std::equal(key, key + 4, g.key)) exec = g.exec;
+        if (exec == nullptr) {
+            if (h->cap == nullptr) {
+                TSB_CUDA(cudaStreamCreateWithFlags(&h->cap, cudaStreamNonBlocking));
+                for (auto &e : h->gev) TSB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            }
+            TSB_CUDA(cudaStreamBeginCapture(h->cap, cudaStreamCaptureModeThreadLocal));
+            cudaGraph_t graph = nullptr;
+            try {
+                enqueue_program(h, d_values, d_g, d_gt, d_d, h->cap);
+            } catch (...) {
+                cudaStreamEndCapture(h->cap, &graph);
+                if (graph) cudaGraphDestroy(graph);
+                throw;
+            }
+            TSB_CUDA(cudaStreamEndCapture(h->cap, &graph));
+            const cudaError_t e = cudaGraphInstantiate(&exec, graph, 0);
+            cudaGraphDestroy(graph);
+            TSB_CUDA(e);
+            if (h->graphs.size() >= 4) {  // a few image/value buffers in rotation at most
+                cudaGraphExecDestroy(h->graphs.front().exec);
+                h->graphs.erase(h->graphs.begin());
+            }
+            tsb_refactor::Graph g;
+            std::copy(key, key + 4, g.key);
+            g.exec = exec;
+            h->graphs.push_back(g);
+        }
+        TSB_CUDA(cudaEventRecord(h->gev[0], s0));
+        TSB_CUDA(cudaStreamWaitEvent(h->cap, h->gev[0], 0));
+        TSB_CUDA(cudaGraphLaunch(exec, h->cap));
+        TSB_LAUNCHED();
+        TSB_CUDA(cudaEventRecord(h->gev[1], h->cap));
+        TSB_CUDA(cudaStreamWaitEvent(s0, h->gev[1], 0));
     });
 }
