@@ -149,3 +149,21 @@ def test_distributed_pcg_over_sharded_assembly(world):
     for rank, xs, it, res, conv in outs:
         assert conv and it == oit, (rank, it, oit)
         assert np.abs(xs - ox).max() <= 1e-10 * np.abs(ox).max()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_rank_meshes_partition_the_elements(world):
+    mesh, f, _, _, fe = _case()
+    sp = S.shard_blocks(f, world)
+    parts = [S.rank_mesh(mesh, sp, f.plan.perm, g) for g in range(world)]
+    rows = np.concatenate([p.elements for p, _ in parts])
+    assert len(rows) == len(mesh.elements)
+    assert len(np.unique(rows, axis=0)) == len(np.unique(np.asarray(mesh.elements), axis=0))
+    # every rank keeps the full node set and the pinned nodes
+    for p, _ in parts:
+        assert p.node_count == mesh.node_count
+        assert np.array_equal(p.fixed_nodes, mesh.fixed_nodes)
+    # the external forces are handed out exactly once
+    nr = parts[0][1]
+    tot = sum(S.rank_f_ext(fe, nr, g) for g in range(world))
+    assert np.array_equal(tot, fe)
