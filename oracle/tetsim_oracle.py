@@ -190,11 +190,31 @@ def stvk(nodes, elements, rest, positions, velocities):
     return force, kv, kblocks
 
 
+def assembly_pattern(nodes, elements, fixed_nodes, rest):
+    """Triplet -> CSR slot mapping of the fused pass (the reference's full
+    assembly, assembly.py:235-312; reused while the fill order and the pinned
+    DOFs do not change, assembly.py:399-405): mass triplets first, then 144
+    stiffness triplets per element."""
+    ndof = 3 * len(nodes)
+    gdof = rest["gdof"]
+    mass_rows = gdof.reshape(-1)
+    rows = np.concatenate([mass_rows, np.repeat(gdof, 12, axis=1).ravel()])
+    cols = np.concatenate([mass_rows, np.tile(gdof, (1, 12)).ravel()])
+    fixed = (3 * np.asarray(fixed_nodes, dtype=np.int64)[:, None] + np.arange(3)).ravel()
+    row_ptr, col_ind, slot, fixed_slots = _fast_pattern(rows, cols, ndof, fixed)
+    kept = np.flatnonzero(slot >= 0)
+    return {"row_ptr": row_ptr, "col_ind": col_ind, "kept": kept, "kept_slots": slot[kept],
+            "fixed_slots": fixed_slots, "fixed": fixed}
+
+
 def assemble_system(nodes, elements, fixed_nodes, rest, positions, velocities, f_ext_state,
-                    dt, gravity, rayleigh_mass=0.0, rayleigh_stiffness=0.0, linear=False, law=None):
+                    dt, gravity, rayleigh_mass=0.0, rayleigh_stiffness=0.0, linear=False, law=None,
+                    pattern=None):
     """A values (CSR order), b, f_int, f_ext, row_ptr, col_ind of one fused pass
     (integrator.py:145-169): mass triplets first, then 144 stiffness triplets
-    per element, per-triplet coefficients, bincount merge, pinned rows identity."""
+    per element, per-triplet coefficients, bincount merge, pinned rows identity.
+    `pattern` (assembly_pattern) is the cached mapping of the reference's fast
+    path; without it the mapping is rebuilt (full assembly)."""
     el = np.asarray(elements)
     m = len(el)
     ndof = 3 * len(nodes)
@@ -205,17 +225,16 @@ def assemble_system(nodes, elements, fixed_nodes, rest, positions, velocities, f
         f_int, kv, krot = stvk(nodes, elements, rest, positions, velocities)
     else:
         f_int, kv, krot = corotational(nodes, elements, rest, positions, velocities, linear or law == "linear")
-    rows = np.concatenate([mass_rows, np.repeat(gdof, 12, axis=1).ravel()])
-    cols = np.concatenate([mass_rows, np.tile(gdof, (1, 12)).ravel()])
     vals = np.concatenate([mass_vals, krot.reshape(-1)])
     h = dt
     coeffs = np.empty(len(vals))
     coeffs[: 12 * m] = 1.0 + h * rayleigh_mass
     coeffs[12 * m:] = h * (h + rayleigh_stiffness)
-    fixed = (3 * np.asarray(fixed_nodes, dtype=np.int64)[:, None] + np.arange(3)).ravel()
-    row_ptr, col_ind, slot, fixed_slots = _fast_pattern(rows, cols, ndof, fixed)
-    kept = np.flatnonzero(slot >= 0)
-    values = compress(vals, kept, slot[kept], len(col_ind), fixed_slots, coeffs)
+    if pattern is None:
+        pattern = assembly_pattern(nodes, elements, fixed_nodes, rest)
+    row_ptr, col_ind, fixed = pattern["row_ptr"], pattern["col_ind"], pattern["fixed"]
+    fixed_slots = pattern["fixed_slots"]
+    values = compress(vals, pattern["kept"], pattern["kept_slots"], len(col_ind), fixed_slots, coeffs)
     mass_diag = np.bincount(mass_rows, weights=mass_vals, minlength=ndof)
     f_ext = np.asarray(f_ext_state) + (mass_diag.reshape(-1, 3) * np.asarray(gravity)).ravel()
     b = f_ext - f_int - (h + rayleigh_stiffness) * kv

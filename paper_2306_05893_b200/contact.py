@@ -279,6 +279,11 @@ class PlaneContactPipeline:
         if factors is not None:
             lam, info, acc = self._resolve_with_factors(free, constraints, factors, h)
         else:
+            from .ndprecond import AsyncPreconditioner
+
+            if isinstance(apply_inverse, AsyncPreconditioner):
+                # not ready yet: the reference falls back to solving each column (contact.py:109-125)
+                apply_inverse = None
             if apply_inverse is None:
                 def apply_inverse(rhs):
                     x, report = solve(free.matrix, rhs)

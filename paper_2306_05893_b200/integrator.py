@@ -460,5 +460,8 @@ class CapturedStep:
                             f"after {report.iterations} iterations", report)
         if int(flags[1]):
             raise StepError("solver produced non-finite accelerations", report)
+        # a fresh CsrMatrix per replay: a host snapshot cached by an earlier result's
+        # `.values` must not be served for this replay's device values
+        a = CsrMatrix(a.nrows, a.ncols, a.row_ptr, a.col_ind, a.device_values())
         return StepResult(x1.view(-1, 3), v1.view(-1, 3), acc.view(-1, 3), f_int, f_ext, a, b, report, False,
                           0.0, time.perf_counter() - t0)

@@ -113,6 +113,26 @@ class JacobiPreconditioner:
             self._inv = 1.0 / self._diag
         return self._inv
 
+    def device_inv_diag(self):
+        """1/diag of the matrix this preconditioner was built from, as a CUDA
+        tensor (computed once; on the device for a device matrix)."""
+        if getattr(self, "_dinv", None) is None:
+            t = _lib.require_cuda()
+            m = self._matrix
+            if self._inv is None and m is not None and m.on_device:
+                d = t.empty(min(m.nrows, m.ncols), dtype=t.float64, device="cuda")
+                d_rp, d_ci = m.device_pattern()
+                _lib.check(_lib.load().tsb_csr_diagonal(m.nrows, m.ncols, _lib.ptr(d_rp), _lib.ptr(d_ci),
+                                                        _lib.ptr(m.device_values()), _lib.ptr(d),
+                                                        _lib.stream_ptr()), "csr_diagonal")
+                zero = t.nonzero(d == 0.0)
+                if zero.numel():
+                    raise SolverError(f"zero diagonal entry at row {int(zero[0, 0])}")
+                self._dinv = 1.0 / d
+            else:
+                self._dinv = t.from_numpy(np.ascontiguousarray(self.inv_diag)).cuda()
+        return self._dinv
+
     def apply(self, r):
         if _lib.is_tensor(r):
             t = _lib.torch()
@@ -177,11 +197,11 @@ def _precond_kind(precond, a):
     if precond is None or isinstance(precond, IdentityPreconditioner):
         return _lib.PRECOND_IDENTITY, None, None
     if isinstance(precond, JacobiPreconditioner):
-        if precond._matrix is a or (precond._matrix is not None and precond._inv is None
-                                    and precond._matrix.row_ptr is a.row_ptr):
+        if precond._matrix is a:
+            # the diagonal of the matrix being solved: extracted and inverted inside the kernel
             return _lib.PRECOND_JACOBI, None, None
-        t = _lib.torch()
-        return _lib.PRECOND_JACOBI, None, t.from_numpy(np.ascontiguousarray(precond.inv_diag)).cuda()
+        # built from another matrix: keep ITS diagonal, as the reference does (krylov.py:104-117)
+        return _lib.PRECOND_JACOBI, None, precond.device_inv_diag()
     factors = ndprecond.as_factors(precond)
     if factors is not None:
         return _lib.PRECOND_LDLT, factors.device(), None

@@ -370,43 +370,45 @@ def ldlt_factor(a: CsrMatrix, plan: DissectionPlan, tile: int = 16, symbolic: Ld
 
     vals = np.asarray(a.values, dtype=np.float64)
     limiter = threadpool_limits(limits=1, user_api="blas")  # small fronts: threads only thrash
-    n = a.nrows
-    d_out = np.empty(n)
-    pending: dict[int, list] = {}
-    factors = {}
-    for b in symbolic.order:
-        blk = plan.blocks[b]
-        s, e, m = blk.start, blk.stop, blk.size
-        cb = symbolic.couple[b]
-        na = len(cb)
-        F = np.zeros((m + na, m + na))
-        F.reshape(-1)[_front_index(symbolic.ds_dst[b], m, m + na)] = vals[symbolic.ds_src[b]]
-        if na:
-            r_, c_ = np.divmod(symbolic.pn_dst[b], m)
-            F[m + r_, c_] = vals[symbolic.pn_src[b]]
-        for pos, U in pending.pop(b, []):
-            F[np.ix_(pos, pos)] += U
-        big = m + na >= _BIG_FRONT
-        if big:
-            limiter.restore_original_limits()
-        try:
-            c = np.linalg.cholesky(F[:m, :m])
-        except np.linalg.LinAlgError as exc:
-            raise IndefiniteMatrixError(f"non-positive pivot while factoring block [{s}, {e}): {exc}") from None
-        dv = np.diagonal(c).copy()
-        d_out[s:e] = dv * dv
-        l11 = c / dv[None, :]
-        if na:
-            ls = solve_triangular(c, F[m:, :m].T, lower=True, check_finite=False).T
-            l21 = ls / dv[None, :]
-            U = F[m:, m:] - ls @ ls.T
-            pending.setdefault(symbolic.parent[b], []).append((symbolic.to_parent[b], U))
-        else:
-            l21 = np.empty((0, m))
-        if big:
-            limiter = threadpool_limits(limits=1, user_api="blas")
-        factors[b] = _BlockFactor(s, e, blk.level, cb, l11, l21, tile, _tile_inverses(l11, tile))
-    limiter.restore_original_limits()
+    try:
+        n = a.nrows
+        d_out = np.empty(n)
+        pending: dict[int, list] = {}
+        factors = {}
+        for b in symbolic.order:
+            blk = plan.blocks[b]
+            s, e, m = blk.start, blk.stop, blk.size
+            cb = symbolic.couple[b]
+            na = len(cb)
+            F = np.zeros((m + na, m + na))
+            F.reshape(-1)[_front_index(symbolic.ds_dst[b], m, m + na)] = vals[symbolic.ds_src[b]]
+            if na:
+                r_, c_ = np.divmod(symbolic.pn_dst[b], m)
+                F[m + r_, c_] = vals[symbolic.pn_src[b]]
+            for pos, U in pending.pop(b, []):
+                F[np.ix_(pos, pos)] += U
+            big = m + na >= _BIG_FRONT
+            if big:
+                limiter.restore_original_limits()
+            try:
+                c = np.linalg.cholesky(F[:m, :m])
+            except np.linalg.LinAlgError as exc:
+                raise IndefiniteMatrixError(f"non-positive pivot while factoring block [{s}, {e}): {exc}") from None
+            dv = np.diagonal(c).copy()
+            d_out[s:e] = dv * dv
+            l11 = c / dv[None, :]
+            if na:
+                ls = solve_triangular(c, F[m:, :m].T, lower=True, check_finite=False).T
+                l21 = ls / dv[None, :]
+                U = F[m:, m:] - ls @ ls.T
+                pending.setdefault(symbolic.parent[b], []).append((symbolic.to_parent[b], U))
+            else:
+                l21 = np.empty((0, m))
+            if big:
+                limiter = threadpool_limits(limits=1, user_api="blas")
+            factors[b] = _BlockFactor(s, e, blk.level, cb, l11, l21, tile, _tile_inverses(l11, tile))
+    finally:
+        limiter.restore_original_limits()  # also on IndefiniteMatrixError
     blocks = [factors[b] for b in symbolic.order]
     nlev = 1 + max((bf.level for bf in blocks), default=0)
     levels = [[] for _ in range(nlev)]

@@ -171,3 +171,115 @@ def test_contact_stage_matches_reference(golden):
     pos2, vel2, _ = O.advance(acc.reshape(-1, 3) - (s @ lam).reshape(-1, 3), x0, v0, 0.01, nofix)
     assert np.abs(pos2 - g[f"c_pos_{k}"]).max() <= 1e-12
     assert np.abs(vel2 - g[f"c_vel_{k}"]).max() <= 1e-10 * np.abs(g[f"c_vel_{k}"]).max()
+
+
+# ---------------------------------------------------------------------------
+# oracle/tetsim_nd.py: mesh, dissection and factorisation restated for the
+# reference arm of bench.py (which must not import the product package)
+# ---------------------------------------------------------------------------
+
+from oracle import tetsim_nd as OND  # noqa: E402
+
+
+def _golden_plan(g, prefix):
+    blocks, nch, ch = g[f"{prefix}_blocks"], g[f"{prefix}_nchildren"], g[f"{prefix}_children"]
+    out, k = [], 0
+    for row, c in zip(blocks, nch):
+        out.append((int(row[0]), int(row[1]), int(row[2]), "separator" if row[3] else "leaf",
+                    tuple(int(v) for v in ch[k:k + c]), int(row[4])))
+        k += c
+    return g[f"{prefix}_perm"], out
+
+
+def _grid_graph(k):
+    src, dst = [], []
+    for i in range(k):
+        for j in range(k):
+            v = i * k + j
+            for w in ([v - k] if i else []) + ([v - 1] if j else []) + ([v + 1] if j + 1 < k else []) \
+                    + ([v + k] if i + 1 < k else []):
+                src.append(v)
+                dst.append(w)
+    indptr = np.zeros(k * k + 1, dtype=np.int64)
+    np.cumsum(np.bincount(src, minlength=k * k), out=indptr[1:])
+    return indptr, np.array(dst, dtype=np.int64)
+
+
+def _beam_graph(dims):
+    nodes, el = OND.generate_beam(*dims, 0.1)
+    return OND.vertex_adjacency(len(nodes), el)
+
+
+@pytest.mark.parametrize("prefix,graph,leaf", [
+    ("path3_leaf1", lambda: (np.array([0, 1, 3, 4]), np.array([1, 0, 2, 1])), 1),
+    ("grid8_leaf4", lambda: _grid_graph(8), 4),
+    ("pairs_leaf1", lambda: (np.arange(7), np.array([1, 0, 3, 2, 5, 4])), 1),
+    ("beam_3x3x8_leaf16", lambda: _beam_graph((3, 3, 8)), 16),
+    ("beam_6x6x28_leaf64", lambda: _beam_graph((6, 6, 28)), 64),
+    ("beam_10x10x100_leaf64", lambda: _beam_graph((10, 10, 100)), 64),
+])
+def test_oracle_nested_dissection_identical_to_reference(golden, prefix, graph, leaf):
+    perm, blocks = _golden_plan(golden("nd_plans"), prefix)
+    plan = OND.nested_dissection(*graph(), leaf)
+    assert np.array_equal(plan.perm, perm)
+    assert [(b.start, b.stop, b.tree_start, b.kind, b.children, b.level) for b in plan.blocks] == blocks
+
+
+@pytest.mark.parametrize("name", ["beam_small", "beam_cfg1"])
+def test_oracle_beam_matches_reference(golden, name):
+    g = golden(name)
+    nodes, el = OND.generate_beam(*map(int, g["dims"]), 0.1)
+    assert np.array_equal(nodes, g["nodes"]) and np.array_equal(el, g["elements"])
+    assert np.array_equal(OND.clamped_nodes(nodes), g["fixed_nodes"])
+
+
+def test_oracle_ldlt_factor_matches_reference(golden):
+    """Factors of the golden system vs the reference's fresh d, and the stale
+    factors' apply of the golden (reference) run: same blocks, same apply."""
+    g = golden("ldlt_small")
+    ref = GoldenFactors(g)
+    nodes, el = OND.generate_beam(*map(int, g["dims"]), 0.1)
+    plan = OND.expand_plan(OND.nested_dissection(*OND.vertex_adjacency(len(nodes), el), int(g["leaf"])))
+    assert np.array_equal(plan.perm, g["f_perm"])
+    f = OND.ldlt_factor(g["row_ptr"], g["col_ind"], g["values"], plan, tile=16)
+    assert np.abs(f.d - g["fresh_d"]).max() <= 1e-13 * np.abs(g["fresh_d"]).max()
+    assert [(b.start, b.stop, b.level) for b in f.blocks] == [(b.start, b.stop, b.level) for b in ref.blocks]
+    assert all(np.array_equal(x.anc, y.anc) for x, y in zip(f.blocks, ref.blocks))
+    z = O.apply(f, g["r"])
+    x = np.linalg.solve(_dense(g), g["r"])
+    assert np.abs(z - x).max() <= 1e-10 * np.abs(x).max()
+
+
+def test_oracle_ldlt_factor_reproduces_reference_stale_factors(golden):
+    """Re-run the reference's stale-factor case end to end with the oracle:
+    scenario steps 1..at-1, factor at step stale_from, PCG at step at."""
+    g = golden("ldlt_small")
+    dims = tuple(map(int, g["dims"]))
+    nodes, el = OND.generate_beam(*dims, 0.1)
+    fixed = OND.clamped_nodes(nodes)
+    plan = OND.expand_plan(OND.nested_dissection(*OND.vertex_adjacency(len(nodes), el), int(g["leaf"])))
+    rest = O.rest_data(nodes, el, 1e5, 0.3, 1000.0)
+    x, v, fe = nodes.copy(), np.zeros_like(nodes), np.zeros(3 * len(nodes))
+    f = None
+    for k in range(1, int(g["at"])):
+        out = O.assemble_system(nodes, el, fixed, rest, x, v, fe, 0.01, (0.0, -G, 0.0))
+        inv = O.jacobi_inv_diag(out["row_ptr"], out["col_ind"], out["values"], len(out["b"]))
+        acc, _, _, conv = O.pcg(out["row_ptr"], out["col_ind"], out["values"], out["b"], lambda r: r * inv)
+        assert conv
+        if k == int(g["stale_from"]):
+            f = OND.ldlt_factor(out["row_ptr"], out["col_ind"], out["values"], plan, tile=16)
+        x, v, _ = O.advance(acc, x, v, 0.01, fixed)
+    assert np.abs(x - g["positions"]).max() <= 1e-10 * np.abs(g["positions"]).max()
+    for bf, rb in zip(f.blocks, GoldenFactors(g).blocks):
+        assert np.abs(bf.l11 - rb.l11).max() <= 1e-11 and (not len(rb.anc) or np.abs(bf.l21 - rb.l21).max() <= 1e-11)
+    out = O.assemble_system(nodes, el, fixed, rest, x, v, fe, 0.01, (0.0, -G, 0.0))
+    sol, it, _, conv = O.pcg(out["row_ptr"], out["col_ind"], out["values"], out["b"], lambda r: O.apply(f, r))
+    assert conv and it == int(g["it_ldlt"])
+    assert np.abs(sol - g["x_ldlt"]).max() <= 1e-10 * np.abs(g["x_ldlt"]).max()
+
+
+def _dense(g):
+    n = len(g["b"])
+    d = np.zeros((n, n))
+    d[np.repeat(np.arange(n), np.diff(g["row_ptr"])), g["col_ind"]] = g["values"]
+    return d
