@@ -1,14 +1,21 @@
 """Benchmark of the B200 implicit-FEM solve path (BASELINE.json metric).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg2|cfg1|cfg3|cfg5]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg3|cfg1|cfg2|cfg5]
                     [--precond ldlt|jacobi] [--impl reference]
 
+Default workload: config 3 of BASELINE.json (20x20x250 = 100k-node corotational
+beam, nested-dissection LDL^T-PCG), the largest configuration that fits one GPU.
 A step = one implicit time step of the scenario (assemble A, b on the device
-+ device PCG + kinematic update) at scenario step 7 of a clamped corotational
-beam under transverse gravity, LDL^T factors replayed at a fixed staleness of
-3 steps (SURVEY.md 8d / BASELINE.md section 2).  Every timed step repeats the
-same step from the same state (nothing committed), L2 flushed between steps.
++ device PCG + kinematic update) at scenario step 4 of a clamped corotational
+beam under transverse gravity, LDL^T factors of step 1 replayed (fixed
+staleness 3, SURVEY.md 8d / BASELINE.md section 2).  Every timed step repeats
+the same step from the same state (nothing committed), L2 flushed between
+steps.  The CPU oracle solves the same system with the same factors and the
+run fails unless the iteration counts agree and x matches within 1e-10.
 N > 1: one independent simulation per GPU (replicas, weak scaling).
+--impl reference: the CPU reference path (the NumPy oracle port, oracle/),
+workload built from scratch by the oracle -- the product package is never
+imported on that arm.
 cfg5: 64 independent ~50k-node simulations (own gravity direction each)
 split over the GPUs; a step advances all of them (strong scaling).
 """
@@ -37,8 +44,22 @@ WORKLOADS = {
     "cfg5": dict(dims=(20, 20, 125), law="corotational", batch=64,
                  desc="config 5: 64 independent ~50k-node corotational beams (batched, Jacobi-PCG)"),
 }
-STALE_FROM, AT_STEP = 4, 7
+STALE_FROM, AT_STEP = 1, 4
 TOL, MAX_IT, LEAF, TILE = 1e-9, 8000, 64, 16
+
+
+def workload_config(name, precond, world):
+    """The `config` object of both arms' JSON lines (static: derived from the
+    workload definition alone, so the reference arm reports the same dict)."""
+    w = WORKLOADS[name]
+    nx, ny, nz = w["dims"]
+    return {
+        "workload": w["desc"], "mesh": "x".join(map(str, w["dims"])), "law": w["law"],
+        "nodes": nx * ny * nz, "tets": 6 * (nx - 1) * (ny - 1) * (nz - 1), "dofs": 3 * nx * ny * nz,
+        "precond": precond, "staleness": AT_STEP - STALE_FROM, "scenario_step": AT_STEP, "tol": TOL,
+        "leaf": LEAF, "tile": TILE, "l2": "flushed (256 MB write) before every timed step",
+        "parallelism": f"replicas x{world}",
+    }
 
 
 def peaks():
@@ -323,13 +344,16 @@ def time_e2e(W, mode, steps):
 # CPU baseline: the oracle port of the reference on the host cores
 # ---------------------------------------------------------------------------
 
-def oracle_step(W, mode, rest, host_state):
+def oracle_step(W, mode, rest, pattern, host_state):
+    """One reference step on the host: the oracle's fused assembly through the
+    cached mapping (the reference's fast path) + PCG with the same
+    preconditioner as the GPU arm (the very same host LdlFactors object)."""
     from oracle import tetsim_oracle as O
 
     mesh = W["mesh"]
     x, v, fe = host_state
     out = O.assemble_system(mesh.nodes, mesh.elements, mesh.fixed_nodes, rest, x, v, fe, 0.01,
-                            (0.0, -9.81, 0.0), linear=WORKLOADS[W["name"]]["law"] == "linear")
+                            (0.0, -9.81, 0.0), linear=WORKLOADS[W["name"]]["law"] == "linear", pattern=pattern)
     if mode == "ldlt":
         f = W["factors"]
         pre = lambda r: O.apply(f, r)  # noqa: E731
@@ -340,20 +364,40 @@ def oracle_step(W, mode, rest, host_state):
 
 
 def cpu_baseline(W, mode, budget_s=20.0, max_steps=10, threads=1):
+    """The oracle port of the reference step on one host core (median of full
+    steps within the budget) -- and the parity check of the GPU step: same
+    state, same preconditioner, the oracle's iterations and x."""
     from oracle import tetsim_oracle as O
     from threadpoolctl import threadpool_limits
 
     st = W["state"].to_host()
     host_state = (st.positions, st.velocities, st.f_ext)
+    mesh = W["mesh"]
     with threadpool_limits(limits=threads):
-        rest = O.rest_data(W["mesh"].nodes, W["mesh"].elements, 1e5, 0.3, 1000.0)
+        rest = O.rest_data(mesh.nodes, mesh.elements, 1e5, 0.3, 1000.0)
+        pattern = O.assembly_pattern(mesh.nodes, mesh.elements, mesh.fixed_nodes, rest)
         ts = []
         t_start = time.perf_counter()
         while len(ts) < max_steps and (time.perf_counter() - t_start) < budget_s:
             t0 = time.perf_counter()
-            _, it, _, _ = oracle_step(W, mode, rest, host_state)
+            x, it, res, conv = oracle_step(W, mode, rest, pattern, host_state)
             ts.append((time.perf_counter() - t0) * 1e3)
-    return dict(ms=statistics.median(ts), steps=len(ts), iterations=it)
+    return dict(ms=statistics.median(ts), steps=len(ts), iterations=it, x=x, residual=res, converged=conv)
+
+
+def check_parity(W, mode, cpu):
+    """The GPU step must reproduce the oracle: same PCG iteration count, x
+    within 1e-10 relative (north_star tolerance); raises otherwise."""
+    res = W["integ"].compute_step(W["state"], W["solvers"][mode])
+    x = res.accelerations.reshape(-1).cpu().numpy()
+    it = int(res.report.iterations)
+    ref = cpu["x"]
+    err = float(np.abs(x - ref).max() / max(np.abs(ref).max(), 1e-300))
+    out = {"iterations_gpu": it, "iterations_oracle": int(cpu["iterations"]), "x_rel_err": err,
+           "tolerance": 1e-10, "ok": it == int(cpu["iterations"]) and err <= 1e-10}
+    if not out["ok"]:
+        raise SystemExit(f"parity check failed: {out}")
+    return out
 
 
 # ---------------------------------------------------------------------------
@@ -435,6 +479,16 @@ def traffic_from_profiles(workload):
 # ---------------------------------------------------------------------------
 # config 5: a batch of independent simulations per GPU
 # ---------------------------------------------------------------------------
+
+def batch_config(world):
+    w = WORKLOADS["cfg5"]
+    nx, ny, nz = w["dims"]
+    return {"workload": w["desc"], "mesh": "x".join(map(str, w["dims"])), "simulations": w["batch"],
+            "nodes": nx * ny * nz, "dofs": 3 * nx * ny * nz, "precond": "jacobi", "scenario_step": 4, "tol": TOL,
+            "parallelism": f"batch split over {world} GPU(s), no collective",
+            "l2": "flushed (256 MB write) before every batch step",
+            "step": "one implicit step of every simulation (CUDA-graph replays, one after another)"}
+
 
 def batch_gravity(i):
     """Gravity of simulation i: a random unit direction (default_rng(i)) x 9.81."""
@@ -550,11 +604,7 @@ def run_batched(args, world, rank, local, dist):
         "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms, "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": WORKLOADS["cfg5"]["desc"], "mesh": "x".join(map(str, WORKLOADS["cfg5"]["dims"])),
-                   "simulations": batch, "per_rank": len(sims), "nodes": mesh.node_count, "dofs": n,
-                   "precond": "jacobi", "tol": TOL, "parallelism": f"batch split over {world} GPU(s), no collective",
-                   "l2": "flushed (256 MB write) before every batch step",
-                   "step": "one implicit step of every simulation (CUDA-graph replays, one after another)"},
+        "config": batch_config(world), "per_rank": len(sims),
         "sim_steps_per_s": batch / (ms * 1e-3),
         "iterations_median": statistics.median(iters),
         "spmv": {"ms": spmv_r["ms"], "gbs": spmv_r["gbs"], "frac": spmv_r["gbs"] / hbm},
@@ -593,36 +643,127 @@ def batch_cpu_baseline(sim, threads=1):
         return (time.perf_counter() - t0) * 1e3
 
 
+def reference_workload(name, gravity=(0.0, -9.81, 0.0), at_step=AT_STEP, with_factors=True):
+    """The whole workload built by the oracle alone (no product import):
+    beam, rest data, cached assembly mapping, dissection, the scenario run
+    from rest to step AT_STEP with Jacobi-PCG steps, the factors of step
+    STALE_FROM's matrix."""
+    from oracle import tetsim_nd as OND, tetsim_oracle as O
+
+    w = WORKLOADS[name]
+    linear = w["law"] == "linear"
+    nodes, el = OND.generate_beam(*w["dims"], 0.1)
+    fixed = OND.clamped_nodes(nodes)
+    t0 = time.perf_counter()
+    rest = O.rest_data(nodes, el, 1e5, 0.3, 1000.0)
+    pattern = O.assembly_pattern(nodes, el, fixed, rest)
+    plan = (OND.expand_plan(OND.nested_dissection(*OND.vertex_adjacency(len(nodes), el), LEAF))
+            if with_factors else None)
+    x, v, fe = nodes.copy(), np.zeros_like(nodes), np.zeros(3 * len(nodes))
+    factors = None
+    for k in range(1, at_step):
+        out = O.assemble_system(nodes, el, fixed, rest, x, v, fe, 0.01, gravity, linear=linear, pattern=pattern)
+        inv = O.jacobi_inv_diag(out["row_ptr"], out["col_ind"], out["values"], len(out["b"]))
+        acc, _, _, _ = O.pcg(out["row_ptr"], out["col_ind"], out["values"], out["b"], lambda r: r * inv, TOL, MAX_IT)
+        if with_factors and k == STALE_FROM:
+            factors = OND.ldlt_factor(out["row_ptr"], out["col_ind"], out["values"], plan, TILE)
+        x, v, _ = O.advance(acc, x, v, 0.01, fixed)
+    return dict(nodes=nodes, el=el, fixed=fixed, rest=rest, pattern=pattern, plan=plan, factors=factors,
+                state=(x, v, fe), linear=linear, gravity=gravity, setup_s=time.perf_counter() - t0)
+
+
+def reference_sample(R, precond, part, nparts):
+    """One bounded sample of the reference step (ms of the full step it stands
+    for): the oracle's element pass + merge over element chunk `part` of
+    `nparts` (x nparts) and the rest of the fused pass (mass share, rhs), then
+    ONE PCG iteration (SpMV, preconditioner, dots, updates) x the iteration
+    count of the full solve at this state."""
+    from oracle import tetsim_oracle as O
+
+    nodes, el, rest, pat = R["nodes"], R["el"], R["rest"], R["pattern"]
+    x, v, fe = R["state"]
+    m = len(el)
+    c0, c1 = part * m // nparts, (part + 1) * m // nparts
+    sub = {k: (val[c0:c1] if isinstance(val, np.ndarray) and len(val) == m else val) for k, val in rest.items()}
+    t0 = time.perf_counter()
+    _, _, krot = O.corotational(nodes, el[c0:c1], sub, x, v, R["linear"])
+    lo, hi = 12 * m + 144 * c0, 12 * m + 144 * c1
+    sel = (pat["kept"] >= lo) & (pat["kept"] < hi)
+    np.bincount(pat["kept_slots"][sel], weights=(0.01 * 0.01) * krot.reshape(-1)[pat["kept"][sel] - lo],
+                minlength=len(pat["col_ind"]))
+    t_chunk = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    np.bincount(rest["gdof"].reshape(-1), weights=np.repeat(rest["share"], 12), minlength=3 * len(nodes))
+    t_rest = time.perf_counter() - t0
+    sysm = R["system"]
+    rp, ci, vals, b = sysm["row_ptr"], sysm["col_ind"], sysm["values"], sysm["b"]
+    pre = R["pre"]
+    p = pre(b)
+    t0 = time.perf_counter()
+    ap = O.spmv(rp, ci, vals, p)
+    alpha = float(b @ p) / float(p @ ap)
+    xx = alpha * p
+    r = b - alpha * ap
+    float(np.linalg.norm(r))
+    z = pre(r)
+    beta = float(r @ z) / float(b @ p)
+    p = z + beta * p
+    t_iter = time.perf_counter() - t0
+    del xx
+    return (nparts * t_chunk + t_rest + R["iterations"] * t_iter) * 1e3
+
+
+def reference_system(R, precond):
+    """Assemble the timed step's system with the oracle and solve it once in
+    full (iteration count of the step; the samples time one iteration)."""
+    from oracle import tetsim_oracle as O
+
+    x, v, fe = R["state"]
+    out = O.assemble_system(R["nodes"], R["el"], R["fixed"], R["rest"], x, v, fe, 0.01, R["gravity"],
+                            linear=R["linear"], pattern=R["pattern"])
+    if precond == "ldlt":
+        f = R["factors"]
+        pre = lambda r: O.apply(f, r)  # noqa: E731
+    else:
+        inv = O.jacobi_inv_diag(out["row_ptr"], out["col_ind"], out["values"], len(out["b"]))
+        pre = lambda r: r * inv  # noqa: E731
+    t0 = time.perf_counter()
+    _, it, _, conv = O.pcg(out["row_ptr"], out["col_ind"], out["values"], out["b"], pre, TOL, MAX_IT)
+    R.update(system=out, pre=pre, iterations=it)
+    return it, conv, time.perf_counter() - t0
+
+
 def run_reference(args):
+    """Reference arm: the reference's CPU path (the NumPy oracle port of tetsim,
+    oracle/) on the host cores, all BLAS threads; the product package is never
+    imported.  Rank 0 only."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     if args.workload == "cfg5":
         return run_reference_batched(args)
-    W = build_workload(args.workload)
-    ncores = os.cpu_count()
     from oracle import tetsim_oracle as O
 
-    st = W["state"].to_host()
-    rest = O.rest_data(W["mesh"].nodes, W["mesh"].elements, 1e5, 0.3, 1000.0)
-    hs = (st.positions, st.velocities, st.f_ext)
-    for _ in range(args.warmup):
-        oracle_step(W, args.precond, rest, hs)
-    ts = []
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        _, it, _, _ = oracle_step(W, args.precond, rest, hs)
-        ts.append((time.perf_counter() - t0) * 1e3)
-    ms = statistics.mean(ts)
+    R = reference_workload(args.workload)
+    it, conv, t_full_solve = reference_system(R, args.precond)
+    nparts = 8 if args.workload in ("cfg3",) else 1
+    for k in range(args.warmup):
+        reference_sample(R, args.precond, k % nparts, nparts)
+    ts = [reference_sample(R, args.precond, k % nparts, nparts) for k in range(args.steps)]
+    ms = statistics.median(ts)
+    ncores = os.cpu_count()
+    sample = (f"per step: the oracle's element pass + merge over 1/{nparts} of the elements (x{nparts}), the rest "
+              f"of the fused pass, and one PCG iteration x {it} iterations (the full {args.precond}-PCG solve of "
+              f"this system took {it} iterations, {t_full_solve * 1e3:.0f} ms); median of {args.steps} steps; "
+              "workload built by the oracle (beam, dissection, scenario steps, stale factors)")
+    assert not any(k.startswith("paper_2306_05893_b200") for k in sys.modules), "reference arm imported the product"
     line = {
         "impl": "reference", "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOADS[args.workload]["desc"], "precond": args.precond,
-                   "staleness": AT_STEP - STALE_FROM, "iterations": it},
-        "cpu_baseline": {"value": ms, "unit": "ms", "cores": ncores, "kind": "port",
-                         "sample": f"{args.steps} full steps (assembly + PCG) of {args.workload} with the "
-                                   "NumPy oracle port of the reference, all host BLAS threads"},
+        "config": workload_config(args.workload, args.precond, args.gpus),
+        "iterations": it, "converged": bool(conv), "setup_s": R["setup_s"],
+        "cpu_baseline": {"value": ms, "unit": "ms", "cores": ncores, "kind": "port", "sample": sample},
         "e2e": {"value": ms, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -630,23 +771,27 @@ def run_reference(args):
 
 
 def run_reference_batched(args):
-    """Reference arm of config 5: the oracle port steps simulation 0 (all host
-    BLAS threads) and the batch time is that times 64."""
-    import torch  # noqa: F401  (the oracle sample runs on the host; the state comes from a device scenario)
-
-    _, sims, _ = build_batch(1, 0)
-    ts = []
-    for _ in range(max(1, args.steps)):
-        ts.append(batch_cpu_baseline(sims[0], threads=os.cpu_count()))
+    """Reference arm of config 5: simulation 0 (own gravity direction) built by
+    the oracle from rest (3 Jacobi steps, as the GPU arm), then bounded samples
+    of its step (1/4 of the elements + one Jacobi-PCG iteration x the
+    iteration count); the batch step is 64 x that.  No product import."""
+    R = reference_workload("cfg5", gravity=batch_gravity(0), at_step=4, with_factors=False)
+    it, conv, t_full = reference_system(R, "jacobi")
+    nparts = 4
+    for k in range(args.warmup):
+        reference_sample(R, "jacobi", k % nparts, nparts)
+    ts = [reference_sample(R, "jacobi", k % nparts, nparts) for k in range(args.steps)]
     batch = WORKLOADS["cfg5"]["batch"]
-    ms = statistics.mean(ts) * batch
+    ms = statistics.median(ts) * batch
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOADS["cfg5"]["desc"], "precond": "jacobi"},
+        "config": batch_config(args.gpus), "iterations": it, "converged": bool(conv),
         "cpu_baseline": {"value": ms, "unit": "ms", "cores": os.cpu_count(), "kind": "port",
-                         "sample": f"{len(ts)} oracle steps of simulation 0 x {batch} simulations, all host BLAS threads"},
+                         "sample": f"simulation 0: element pass + merge over 1/{nparts} of the elements (x{nparts}) "
+                                   f"+ one Jacobi-PCG iteration x {it} iterations, median of {args.steps}, "
+                                   f"x {batch} simulations; all host BLAS threads"},
         "e2e": {"value": ms, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
     return 0
@@ -657,7 +802,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default="cfg3", choices=sorted(WORKLOADS))
     ap.add_argument("--precond", default="ldlt", choices=["ldlt", "jacobi"])
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -710,9 +855,10 @@ def main():
         if dist:
             dist.destroy_process_group()
         return 0
-    cpu = None
+    cpu = parity = None
     if world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(W, args.precond)
+        parity = check_parity(W, args.precond, cpu)
     hbm = pk.get("hbm_gbs", 6650.0)
     traffic = traffic_from_profiles(args.workload)
     mesh, f = W["mesh"], W["factors"]
@@ -720,13 +866,8 @@ def main():
         "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {
-            "workload": WORKLOADS[args.workload]["desc"], "mesh": "x".join(map(str, WORKLOADS[args.workload]["dims"])),
-            "nodes": mesh.node_count, "tets": mesh.element_count, "dofs": mesh.ndof, "nnz": spmv_r["nnz"],
-            "nnz_L": apply_r["nnzL"], "precond": args.precond, "staleness": AT_STEP - STALE_FROM,
-            "scenario_step": AT_STEP, "tol": TOL, "leaf": LEAF, "tile": TILE,
-            "l2": "flushed (256 MB write) before every timed step", "parallelism": f"replicas x{world}",
-        },
+        "config": workload_config(args.workload, args.precond, world),
+        "sizes": {"nnz": spmv_r["nnz"], "nnz_L": apply_r["nnzL"]},
         "iterations": main_r["iterations"], "assembly_ms": eager_r["assembly_ms"], "pcg_ms": eager_r["solve_ms"],
         "step_mode": "eager compute_step" if args.eager else "CUDA graph replay of compute_step (CapturedStep)",
         "eager_ms_per_step": eager_r["ms"],
@@ -753,8 +894,10 @@ def main():
     }
     if cpu is not None:
         line["cpu_baseline"] = {"value": cpu["ms"], "unit": "ms", "cores": 1, "kind": "port",
-                                "sample": f"median of {cpu['steps']} oracle steps (assembly + {args.precond}-PCG, "
-                                          f"{cpu['iterations']} it) of the same {args.workload} state, 1 BLAS thread"}
+                                "sample": f"median of {cpu['steps']} oracle steps (fused assembly through the cached "
+                                          f"mapping + {args.precond}-PCG, {cpu['iterations']} it, same host factors) "
+                                          f"of the same {args.workload} state, 1 BLAS thread"}
+        line["parity"] = parity
     print(json.dumps(line))
     if dist:
         dist.destroy_process_group()

@@ -125,8 +125,10 @@ def rest_data(nodes, elements, young, poisson, density):
     return {"grads": g, "vol": vol, "ke": ke, "share": share, "gdof": gdof, "lam": lam, "mu": mu}
 
 
-def polar(F, tol=1e-12, max_iter=50):
-    """Newton R <- (R + R^-T)/2, global stop on max |dR| (models.py:174-189)."""
+def polar(F, tol=1e-12, max_iter=50, extra=0):
+    """Newton R <- (R + R^-T)/2, global stop on max |dR| (models.py:174-189).
+    `extra` > 0 runs that many more iterations after the stop (test knob: the
+    rounding-level sensitivity of the forces to where the iteration stops)."""
     r = F.copy()
     for _ in range(max_iter):
         nxt = 0.5 * (r + np.transpose(np.linalg.inv(r), (0, 2, 1)))
@@ -134,10 +136,12 @@ def polar(F, tol=1e-12, max_iter=50):
         r = nxt
         if d < tol:
             break
+    for _ in range(extra):
+        r = 0.5 * (r + np.transpose(np.linalg.inv(r), (0, 2, 1)))
     return r
 
 
-def corotational(nodes, elements, rest, positions, velocities, linear=False):
+def corotational(nodes, elements, rest, positions, velocities, linear=False, extra_newton=0):
     """(f, kv, krot) of the corotational law (models.py:200-238); linear=True
     uses R = I (BASELINE config 1)."""
     el = np.asarray(elements)
@@ -145,7 +149,7 @@ def corotational(nodes, elements, rest, positions, velocities, linear=False):
     ndof = 3 * len(positions)
     xe = np.asarray(positions)[el]
     F = np.einsum("eai,eaj->eij", xe, rest["grads"])
-    R = np.broadcast_to(np.eye(3), (m, 3, 3)).copy() if linear else polar(F)
+    R = np.broadcast_to(np.eye(3), (m, 3, 3)).copy() if linear else polar(F, extra=extra_newton)
     rb = np.zeros((m, 12, 12))
     for a in range(4):
         rb[:, 3 * a:3 * a + 3, 3 * a:3 * a + 3] = R
@@ -209,7 +213,7 @@ def assembly_pattern(nodes, elements, fixed_nodes, rest):
 
 def assemble_system(nodes, elements, fixed_nodes, rest, positions, velocities, f_ext_state,
                     dt, gravity, rayleigh_mass=0.0, rayleigh_stiffness=0.0, linear=False, law=None,
-                    pattern=None):
+                    pattern=None, extra_newton=0):
     """A values (CSR order), b, f_int, f_ext, row_ptr, col_ind of one fused pass
     (integrator.py:145-169): mass triplets first, then 144 stiffness triplets
     per element, per-triplet coefficients, bincount merge, pinned rows identity.
@@ -224,7 +228,8 @@ def assemble_system(nodes, elements, fixed_nodes, rest, positions, velocities, f
     if law == "stvk":
         f_int, kv, krot = stvk(nodes, elements, rest, positions, velocities)
     else:
-        f_int, kv, krot = corotational(nodes, elements, rest, positions, velocities, linear or law == "linear")
+        f_int, kv, krot = corotational(nodes, elements, rest, positions, velocities, linear or law == "linear",
+                                       extra_newton)
     vals = np.concatenate([mass_vals, krot.reshape(-1)])
     h = dt
     coeffs = np.empty(len(vals))
