@@ -127,8 +127,9 @@ def rest_data(nodes, elements, young, poisson, density):
 
 def polar(F, tol=1e-12, max_iter=50, extra=0):
     """Newton R <- (R + R^-T)/2, global stop on max |dR| (models.py:174-189).
-    `extra` > 0 runs that many more iterations after the stop (test knob: the
-    rounding-level sensitivity of the forces to where the iteration stops)."""
+    `extra` > 0 runs that many more iterations after the stop; a Generator
+    perturbs every entry of the result by a random relative 2^-52 (test
+    knobs: the rounding-level sensitivity of the forces to R)."""
     r = F.copy()
     for _ in range(max_iter):
         nxt = 0.5 * (r + np.transpose(np.linalg.inv(r), (0, 2, 1)))
@@ -136,6 +137,8 @@ def polar(F, tol=1e-12, max_iter=50, extra=0):
         r = nxt
         if d < tol:
             break
+    if isinstance(extra, np.random.Generator):
+        return r * (1.0 + 2.0 ** -52 * extra.uniform(-1.0, 1.0, r.shape))
     for _ in range(extra):
         r = 0.5 * (r + np.transpose(np.linalg.inv(r), (0, 2, 1)))
     return r
