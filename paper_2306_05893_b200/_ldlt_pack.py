@@ -32,9 +32,10 @@ cross-lane reduction.  Entries outside a row's range are stored as zeros
 (the padding is reported as stored vs algorithmic bytes).
 
 Work items: up to 8 consecutive small tiles of a block (one warp each, one
-TMA bulk copy of <= 48 KB) or one 48 KB column segment of a large tile (the
-8 warps split its pairs; the segment's 32 partial sums go to a scratch
-slot and the last segment of the tile to finish adds them in segment
+TMA bulk copy of <= 40 KB) or one chunk of SEGS_PER_ITEM 40 KB column
+segments of a large tile, streamed through two shared-memory stages (the 8
+warps split each segment's pairs; the chunk's 32 partial sums go to a
+scratch slot and the last chunk of the tile to finish adds them in chunk
 order -- deterministic -- and emits the rows).
 The dispatch order is a list schedule on an infinite machine keyed by each
 item's earliest start under a simple cost model, ties broken by the longest
@@ -53,11 +54,13 @@ import numpy as np
 from . import _lib
 
 TILE = 32               # rows per tile (one per lane)
-ITEM_BYTES = 48 * 1024  # small-tile item budget: one TMA bulk copy
-SEG_PAIRS = 96          # pairs per segment item of a large tile (96 * 32 * 16 B = 48 KB)
-WARPS = 8               # warps per CTA (csrc kSweepBlock / 32)
+ITEM_BYTES = 40 * 1024  # small-tile item budget: one TMA bulk copy (csrc kStage)
+SEG_PAIRS = 80          # pairs per column segment of a large tile (80 * 32 * 16 B = 40 KB, csrc kSegPairs)
+SEGS_PER_ITEM = int(os.environ.get("TSB_SEGS_PER_ITEM", "4"))  # segments streamed by one chunk item
+GROUPS_PER_ITEM = int(os.environ.get("TSB_GROUPS_PER_ITEM", "4"))  # small-tile TMA groups per item (<= csrc kGroupsPerItem)
+WARPS = 7               # consumer warps per CTA (csrc kWarps): one small tile each
 MERGE_ROWS = 0          # default subtree amalgamation (rows); 0 = off
-CB_CAP = 2048           # contributions staged per piece when a block's items sum them (csrc max_cb)
+CB_CAP = 1024           # contributions staged per piece when a block's items sum them (csrc max_cb)
 # lower input mode: a block's items sum their contributions themselves while the
 # redundant reads (items x contributions) stay below ratio x its factor entries,
 # else finaliser items form x_b once.  Latency-bound (small) factors favour the
@@ -242,40 +245,57 @@ def amalgamate(factors, max_rows: int):
 
 def _items(tiles_of_block, first_tile):
     """Group a block's tiles into items -> list of (t0, t1, seg) in global tile ids
-    (seg = 0: whole small tiles; seg = s + 1: column segment s of one large tile)."""
+    (seg = 0: small tiles [t0, t1); seg = c + 1: chunk c of large tile t0, i.e.
+    its column segments [c t1, c t1 + t1), t1 = SEGS_PER_ITEM)."""
     out = []
     k = 0
     nt = len(tiles_of_block)
     while k < nt:
         npair = tiles_of_block[k][1]
         if npair * TILE * 16 > ITEM_BYTES:
-            for sgi in range((npair + SEG_PAIRS - 1) // SEG_PAIRS):
-                out.append((first_tile + k, first_tile + k + 1, sgi + 1))
+            for c in range(_nchunks(npair)):
+                out.append((first_tile + k, SEGS_PER_ITEM, c + 1))
             k += 1
             continue
-        k1, tot = k, 0
-        while k1 < nt and k1 - k < WARPS:
-            b = tiles_of_block[k1][1] * TILE * 16
-            if b > ITEM_BYTES or tot + b > ITEM_BYTES:
-                break
-            tot += b
-            k1 += 1
+        k1, groups = k, 0  # up to GROUPS_PER_ITEM TMA groups of small tiles (csrc group_end)
+        while groups < GROUPS_PER_ITEM and k1 < nt and tiles_of_block[k1][1] * TILE * 16 <= ITEM_BYTES:
+            g1, tot = k1, 0
+            while g1 < nt and g1 - k1 < WARPS:
+                b = tiles_of_block[g1][1] * TILE * 16
+                if b > ITEM_BYTES or tot + b > ITEM_BYTES:
+                    break
+                tot += b
+                g1 += 1
+            k1 = g1
+            groups += 1
         out.append((first_tile + k, first_tile + k1, 0))
         k = k1
     return out
 
 
+def _nchunks(npair):
+    nsegs = (int(npair) + SEG_PAIRS - 1) // SEG_PAIRS
+    return (nsegs + SEGS_PER_ITEM - 1) // SEGS_PER_ITEM
+
+
+def _chunk_pairs(npair, it):
+    """pairs [p0, p1) of chunk item it of a tile with npair pairs (csrc chunk_range)."""
+    nsegs = (int(npair) + SEG_PAIRS - 1) // SEG_PAIRS
+    s0 = (it[2] - 1) * it[1]
+    s1 = min(s0 + it[1], nsegs)
+    return s0 * SEG_PAIRS, min(s1 * SEG_PAIRS, int(npair))
+
+
 HOP = 1.5               # us: dependency release -> consumer sees it
-SCHED_WORKERS = 444     # resident CTAs the list schedule assumes (148 SMs x 3)
+SCHED_WORKERS = 296     # resident CTAs the list schedule assumes (148 SMs x 2)
 
 
 def _window(T, lim, it):
     """v-columns [w0, w1) an item reads (csrc item_window); T = the sweep's tile table."""
     if it[2] > 0:
-        p0 = (it[2] - 1) * SEG_PAIRS
-        cnt = min(SEG_PAIRS, int(T["np"][it[0]]) - p0)
+        p0, p1 = _chunk_pairs(T["np"][it[0]], it)
         w0 = int(T["tl"][it[0]]) + 2 * p0
-        return w0, min(w0 + 2 * cnt, lim)
+        return w0, min(int(T["tl"][it[0]]) + 2 * p1, lim)
     w0 = int(T["tl"][it[0]:it[1]].min())
     return w0, min(int((T["tl"][it[0]:it[1]] + 2 * T["np"][it[0]:it[1]]).max()), lim)
 
@@ -439,7 +459,7 @@ def pack(factors, subset=None):
             arr = np.array(tl_rows[up], dtype=np.int64)
             t["off"], t["tl"], t["np"], t["row0"], t["nrows"] = arr.T
         big = t["np"].astype(np.int64) * TILE * 16 > ITEM_BYTES
-        t["nseg"] = np.where(big, (t["np"] + SEG_PAIRS - 1) // SEG_PAIRS, 0)
+        t["nseg"] = np.where(big, [_nchunks(v) for v in t["np"]], 0)  # chunk items (partial slots) per tile
         part = np.zeros(len(t) + 1, dtype=np.int64)
         np.cumsum(t["nseg"], out=part[1:])
         t["part"] = part[:-1]
@@ -484,11 +504,13 @@ def pack(factors, subset=None):
         fin_items[i] = [(int(edges[j]), int(edges[j + 1]), -1) for j in range(k) if edges[j + 1] > edges[j]]
         nfin[i] = len(fin_items[i])
 
-    def cost(up, it):  # us: item latency + streaming at ~25 GB/s per CTA (calibrated on B200 traces)
+    def cost(up, it):  # us: item latency + streaming at ~24 GB/s per CTA (HBM shared by 296 CTAs)
         if it[2] < 0:
             return 2.5
-        nbytes = min(int(tables[up]["np"][it[0]:it[1]].sum()) * TILE * 16, ITEM_BYTES)
-        return 2.5 + nbytes / 25e3 + (0.5 if it[2] else 0.0)
+        if it[2] > 0:
+            p0, p1 = _chunk_pairs(tables[up]["np"][it[0]], it)
+            return 3.0 + (p1 - p0) * TILE * 16 / 24e3
+        return 3.0 + int(tables[up]["np"][it[0]:it[1]].sum()) * TILE * 16 / 24e3
 
     def touches_anc(i, it):  # upper item whose column window reaches -z_anc (waits for the parent)
         if not na_[i]:

@@ -45,35 +45,25 @@ namespace tsb {
 template <bool TRACE, bool MULTI = false>
 __global__ void __launch_bounds__(kSweepBlock) lower_sweep(tsb_ldlt_desc D, SweepArgs A) {
     extern __shared__ __align__(128) double smem[];
-    __shared__ uint64_t bars[2];
+    __shared__ SweepRing R;
     if (A.done != nullptr && *((volatile const int32_t *)A.done)) {
         lower_exit(D);
         return;
     }
-    if (threadIdx.x == 0) {
-        mbar_init(&bars[0], 1);
-        mbar_init(&bars[1], 1);
-    }
-    __syncthreads();
-    uint32_t phase = 0;
-    lower_sweep_body<TRACE, MULTI>(D, A, smem, bars, phase);
+    ring_init(R);
+    lower_sweep_body<TRACE, MULTI>(D, A, smem, R);
 }
 
 template <bool TRACE>
 __global__ void __launch_bounds__(kSweepBlock) upper_sweep(tsb_ldlt_desc D, SweepArgs A) {
     extern __shared__ __align__(128) double smem[];
-    __shared__ uint64_t bars[2];
+    __shared__ SweepRing R;
     if (A.done != nullptr && *((volatile const int32_t *)A.done)) {
         upper_exit(D);
         return;
     }
-    if (threadIdx.x == 0) {
-        mbar_init(&bars[0], 1);
-        mbar_init(&bars[1], 1);
-    }
-    __syncthreads();
-    uint32_t phase = 0;
-    upper_sweep_body<TRACE>(D, A, smem, bars, phase);
+    ring_init(R);
+    upper_sweep_body<TRACE>(D, A, smem, R);
 }
 
 static uint64_t g_serial = 0;

@@ -2,6 +2,21 @@
 // stand-alone sweep kernels (ldlt.cu) and the persistent PCG solver (pcg.cu).
 // Tiled block-inverse layout and item protocol: include/tsb.h (tsb_ldlt_desc),
 // ldlt.cu and paper_2306_05893_b200/_ldlt_pack.py.
+//
+// Warp roles inside a sweep (256-thread CTA):
+//   warp 7 (producer, lane 0) takes the item tickets, posts each item id in a
+//          two-entry mailbox and streams the item's factor data -- one TMA
+//          bulk copy per small-tile group or per 40 KB column segment --
+//          through a two-stage shared-memory ring, running up to two items /
+//          two copies ahead of the consumers;
+//   warps 0-6 (consumers, 224 threads, named barrier 1) stage each item's
+//          vector window, wait for its dependency, form the block input,
+//          run the GEMV out of the ring and publish.
+// So the ticket atomic, the descriptor loads and the factor copies of the next
+// item overlap the current item's dependency wait, input staging and math: the
+// per-item latency chain no longer gates the HBM stream.  Consumers process
+// their CTA's tickets in ticket order and every dependency points to an
+// earlier ticket, so the persistent grid stays deadlock-free.
 #pragma once
 
 #include "tsb_common.cuh"
@@ -9,15 +24,24 @@
 namespace tsb {
 
 constexpr int kSweepBlock = 256;
-constexpr int kWarps = kSweepBlock / 32;
+constexpr int kWarps = 7;               // consumer warps
+constexpr int kCThreads = kWarps * 32;  // consumer threads
+constexpr int kProducerWarp = 7;
 constexpr int kTile = 32;               // rows per tile (one per lane)
-constexpr int kStage = 6144;            // doubles of TMA staging (48 KB): small-tile items
-constexpr int kSegPairs = 96;           // pairs per segment item of a large tile (48 KB)
-constexpr int kMaxV = 8192;             // largest m + na whose vector is staged in shared memory
-constexpr int kMaxItemRows = kWarps * kTile;
+constexpr int kStage = 5120;            // doubles per ring stage (40 KB; 2 stages + vectors fit 2 CTAs/SM)
+constexpr int kStages = 2;
+constexpr int kSegPairs = 80;           // pairs per column segment of a large tile (40 KB)
+constexpr int kMaxV = 8192;             // largest item window staged in shared memory
+constexpr int kGroupsPerItem = 4;       // TMA groups (<= kWarps small tiles, <= 40 KB each) per small-tile item
+constexpr int kMailTiles = kGroupsPerItem * kWarps;
+constexpr int kMaxItemRows = kMailTiles * kTile;
 
+// seg = 0: small tiles [t0, t1), streamed as up to kGroupsPerItem TMA groups
+// (greedy: <= kWarps tiles and <= 40 KB per group); seg = c + 1 (chunk item of a large
+// tile): column segments [c*t1, min(c*t1 + t1, nsegs)) of tile t0, one TMA
+// each (t1 = segments per chunk); seg < 0: finaliser of rows [t0, t1).
 struct Item {
-    int32_t block, t0, t1, seg;  // seg = 0: tiles [t0, t1); seg = s + 1: segment s of tile t0
+    int32_t block, t0, t1, seg;
 };
 
 // ---- small PTX helpers -----------------------------------------------------
@@ -28,7 +52,11 @@ __device__ __forceinline__ void mbar_init(uint64_t *bar, int count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 // one-thread TMA bulk copy global -> shared, completion on the mbarrier
+// (bytes == 0: the arrive alone completes the phase)
 __device__ __forceinline__ void tma_load_1d(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
@@ -48,23 +76,18 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
         "r"(phase)
         : "memory");
 }
-__device__ __forceinline__ void cp_async16(void *dst, const void *src) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+// barrier of the consumer warps only (the producer warp runs its own loop)
+__device__ __forceinline__ void csync() { asm volatile("bar.sync 1, %0;" ::"n"(kCThreads) : "memory"); }
 __device__ __forceinline__ int ld_acquire(const int *p) {
     int v;
     asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
-// Release / acquire-release counter updates: issued by thread 0 after a
-// __syncthreads(), they publish every write the CTA made before the barrier
+// Release / acquire-release counter updates: issued by consumer thread 0 after
+// a csync(), they publish every write the consumers made before the barrier
 // (bar.sync orders them before thread 0's release; release is cumulative).
-__device__ __forceinline__ int atom_add_release(int *p, int v) {
-    int old;
-    asm volatile("atom.add.release.gpu.global.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
-    return old;
+__device__ __forceinline__ void red_add_release(int *p, int v) {
+    asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 __device__ __forceinline__ int atom_add_acq_rel(int *p, int v) {
     int old;
@@ -109,10 +132,46 @@ struct SweepArgs {
     const double *ext;       // lower: contributions from outside the handle's blocks (subtracted), or NULL
     // multi-RHS lower sweep (tsb_ldlt_lower_multi): nr right-hand sides, vector j
     // of in / x / d_x at j * ld, of the contributions at j * ld_cb, of the
-    // segment partial sums at j * ld_part
+    // chunk partial sums at j * ld_part
     int nr = 1;
     int64_t ld = 0, ld_cb = 0, ld_part = 0;
 };
+
+// Producer/consumer ring of one CTA (static shared memory of the kernel; its
+// sequence counters persist across the sweeps of one launch, e.g. inside the
+// persistent PCG).  TMA copy q uses stage q % 2 (barrier parity (q / 2) & 1);
+// item k uses mailbox entry k % 2.
+// A mailbox entry carries everything the consumers need about an item, loaded
+// by the producer while the consumers work on the previous one: the item, its
+// block, its tiles (small groups: up to kWarps; chunks: the tile) and its
+// vector window.
+struct MailEntry {
+    int32_t iid, w0, w1, pad_;
+    Item it;
+    tsb_ldlt_block B;
+    tsb_ldlt_tile T[kMailTiles];
+};
+struct SweepRing {
+    uint64_t full[kStages], empty[kStages];  // stage landed / stage read by the consumers
+    uint64_t posted[2], taken[2];            // mailbox entry written / consumed
+    MailEntry mail[2];
+    uint32_t q_prod, k_prod, q_cons, k_cons;
+};
+
+__device__ __forceinline__ void ring_init(SweepRing &R) {
+    if (threadIdx.x == 0) {
+        for (int k = 0; k < kStages; ++k) {
+            mbar_init(&R.full[k], 1);
+            mbar_init(&R.empty[k], 1);
+        }
+        for (int k = 0; k < 2; ++k) {
+            mbar_init(&R.posted[k], 1);
+            mbar_init(&R.taken[k], 1);
+        }
+        R.q_prod = R.k_prod = R.q_cons = R.k_cons = 0;
+    }
+    __syncthreads();
+}
 
 // Exit protocol: the last CTA out zeroes the counters for the next replay.
 __device__ __forceinline__ void sweep_exit(int32_t *ctl, int32_t *c0, int64_t n0, int32_t *c1, int64_t n1,
@@ -148,12 +207,12 @@ constexpr int kFinRows = 1024;          // rows per piece of a mode-2 finalisati
 // nr right-hand sides stage nr windows)
 inline size_t sweep_smem_lower(const tsb_ldlt_desc &D, int nr = 1) {
     const int offs = (D.max_v + 2 > kFinRows + 2 ? D.max_v + 2 : kFinRows + 2);
-    return (size_t)(kStage + nr * ((D.max_v + 3) & ~1) + ((D.max_cb + 1) & ~1)) * sizeof(double) +
+    return (size_t)(kStages * kStage + nr * ((D.max_v + 3) & ~1) + ((D.max_cb + 1) & ~1)) * sizeof(double) +
            (((offs + 1) & ~1) + kMaxItemRows) * sizeof(int32_t) +
-           (nr > 1 ? (size_t)nr * kSweepBlock * sizeof(double) : 0);  // multi-RHS segment partials
+           (nr > 1 ? (size_t)nr * kSweepBlock * sizeof(double) : 0);  // multi-RHS chunk partials
 }
 inline size_t sweep_smem_upper(const tsb_ldlt_desc &D) {
-    return (size_t)(kStage + ((D.max_v + 3) & ~1)) * sizeof(double);
+    return (size_t)(kStages * kStage + ((D.max_v + 3) & ~1)) * sizeof(double);
 }
 
 // Sum of a row's contributions cb[a0, a1) in the fixed order every finaliser
@@ -170,40 +229,40 @@ __device__ __forceinline__ double contrib_sum(const double *cb, int64_t a0, int6
     return c0 + c1;
 }
 
-// Cooperative coalesced copy global -> shared of n doubles, all loads in flight.
+// Consumer-cooperative coalesced copy global -> shared of n doubles, all loads in flight.
 __device__ __forceinline__ void stage_copy(double *dst, const double *src, int n) {
     constexpr int U = 8;
-    for (int k0 = threadIdx.x; k0 < n; k0 += U * kSweepBlock) {
+    for (int k0 = threadIdx.x; k0 < n; k0 += U * kCThreads) {
         double t[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const int k = k0 + u * kSweepBlock;
+            const int k = k0 + u * kCThreads;
             t[u] = k < n ? __ldcg(src + k) : 0.0;
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const int k = k0 + u * kSweepBlock;
+            const int k = k0 + u * kCThreads;
             if (k < n) dst[k] = t[u];
         }
     }
 }
 
-// Strided per-thread loops with their global loads issued in batches of 4
-// (the loads of one batch are independent; results land in shared memory).
-// dst[j] = f(j) for j = tid, tid + 256, ... < n
+// Strided per-consumer-thread loops with their global loads issued in batches
+// of 4 (the loads of one batch are independent; results land in shared memory).
+// dst[j] = f(j) for j = tid, tid + 224, ... < n
 template <class F>
 __device__ __forceinline__ void batched(int n, F f) {
     constexpr int U = 4;
-    for (int j0 = threadIdx.x; j0 < n; j0 += U * kSweepBlock) {
+    for (int j0 = threadIdx.x; j0 < n; j0 += U * kCThreads) {
         double t[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const int j = j0 + u * kSweepBlock;
+            const int j = j0 + u * kCThreads;
             if (j < n) t[u] = f.load(j);
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const int j = j0 + u * kSweepBlock;
+            const int j = j0 + u * kCThreads;
             if (j < n) f.store(j, t[u]);
         }
     }
@@ -234,74 +293,181 @@ __device__ __forceinline__ double tile_dot(const double *d, const double *v, int
     return (a0 + a1) + (a2 + a3);
 }
 
-// Stage an item's data (before the dependency wait) with one TMA bulk copy:
-// its small tiles, or one 48 KB column segment of a large tile.
-__device__ __forceinline__ void stage_item(const Item &it, const tsb_ldlt_tile *tiles, const double *base,
-                                           double *stage, uint64_t *bars) {
-    if (threadIdx.x != 0) return;
-    const tsb_ldlt_tile T0 = tiles[it.t0];
-    if (it.seg == 0) {
-        const tsb_ldlt_tile Tl = tiles[it.t1 - 1];
-        const int64_t end = Tl.off + (int64_t)Tl.np * (2 * kTile);
-        tma_load_1d(stage, base + T0.off, (uint32_t)((end - T0.off) * 8), &bars[0]);
-    } else {
-        const int p0 = (it.seg - 1) * kSegPairs, cnt = min(kSegPairs, T0.np - p0);
-        tma_load_1d(stage, base + T0.off + (int64_t)p0 * (2 * kTile), (uint32_t)(cnt * 2 * kTile * 8), &bars[0]);
-    }
+// segments [s0, s1) of a chunk item's tile (see Item)
+__device__ __forceinline__ void chunk_range(const Item &it, const tsb_ldlt_tile &T, int &s0, int &s1) {
+    const int nsegs = (T.np + kSegPairs - 1) / kSegPairs;
+    s0 = (it.seg - 1) * it.t1;
+    s1 = min(s0 + it.t1, nsegs);
 }
 
-// v-columns [w0, w1) an item reads (lim = width of its vector: m or m + na).
-__device__ __forceinline__ void item_window(const Item &it, const tsb_ldlt_tile *tiles, int lim, int &w0, int &w1) {
-    const tsb_ldlt_tile T0 = tiles[it.t0];
+// end of the TMA group of a small-tile item that starts at tile g0 (of nt):
+// the longest run of <= kWarps tiles whose data fit one stage
+__device__ __forceinline__ int group_end(const tsb_ldlt_tile *T, int nt, int g0) {
+    int g1 = g0, tot = 0;
+    while (g1 < nt && g1 - g0 < kWarps) {
+        const int b = T[g1].np * 2 * kTile;
+        if (tot + b > kStage) break;
+        tot += b;
+        ++g1;
+    }
+    return g1 > g0 ? g1 : g0 + 1;
+}
+
+// v-columns [w0, w1) an item reads (lim = width of its vector: m or m + na);
+// T = the item's tiles.
+__device__ __forceinline__ void item_window(const Item &it, const tsb_ldlt_tile *T, int lim, int &w0, int &w1) {
     if (it.seg) {
-        const int p0 = (it.seg - 1) * kSegPairs, cnt = min(kSegPairs, T0.np - p0);
-        w0 = T0.tl + 2 * p0;
-        w1 = min(w0 + 2 * cnt, lim);
+        int s0, s1;
+        chunk_range(it, T[0], s0, s1);
+        w0 = T[0].tl + 2 * s0 * kSegPairs;
+        w1 = min(T[0].tl + 2 * min(s1 * kSegPairs, T[0].np), lim);
     } else {
-        w0 = T0.tl;  // tiles are in row order: the first has the smallest tl
+        w0 = T[0].tl;  // tiles are in row order: the first has the smallest tl
         int hi = 0;
-        for (int t = it.t0; t < it.t1; ++t) hi = max(hi, tiles[t].tl + 2 * tiles[t].np);
+        for (int t = 0; t < it.t1 - it.t0; ++t) hi = max(hi, T[t].tl + 2 * T[t].np);
         w1 = min(hi, lim);
     }
 }
 
-// GEMV of a staged item against the shared vector v (v[t] = column t).
-// emit(row, value) once per tile row (block-relative row index).  A segment
-// item of a large tile writes its 32 partial sums to the tile's scratch; the
-// last segment to finish adds them in segment order and emits.
+// ---- producer warp ---------------------------------------------------------
+// Lane 0 of the producer warp: ticket -> mailbox -> the item's ring copies
+// (one per small-tile group or chunk segment; a finaliser reserves one stage
+// as scratch), until the ticket runs past the item list (that sentinel is
+// posted too, so the consumers stop).
+__device__ __forceinline__ void sweep_producer(SweepRing &R, int32_t *ticket, int64_t n_items, const Item *items,
+                                               const tsb_ldlt_block *blocks, const tsb_ldlt_tile *tiles,
+                                               const double *base, double *stage, bool upper) {
+    if ((threadIdx.x & 31) != 0) return;
+    uint32_t q = R.q_prod, k = R.k_prod;
+    while (true) {
+        const int iid = atomicAdd(ticket, 1);
+        const int e = k & 1;
+        MailEntry &M = R.mail[e];
+        Item it{0, 0, 0, 0};
+        tsb_ldlt_tile T0{};
+        if (iid < n_items) {  // descriptors: loaded while the entry may still be in use
+            it = items[iid];
+            const tsb_ldlt_block B = blocks[it.block];
+            if (it.seg >= 0) T0 = tiles[it.t0];
+            if (k >= 2) mbar_wait(&R.taken[e], ((k >> 1) - 1) & 1u);
+            M.it = it;
+            M.B = B;
+            if (it.seg > 0) {
+                M.T[0] = T0;
+            } else if (it.seg == 0) {
+                for (int t = it.t0; t < it.t1; ++t) M.T[t - it.t0] = t == it.t0 ? T0 : tiles[t];
+            }
+            if (it.seg >= 0) item_window(it, M.T, B.m + (upper ? B.na : 0), M.w0, M.w1);
+        } else if (k >= 2) {
+            mbar_wait(&R.taken[e], ((k >> 1) - 1) & 1u);
+        }
+        M.iid = iid;
+        mbar_arrive(&R.posted[e]);
+        ++k;
+        if (iid >= n_items) break;
+        int s0 = 0, s1 = 1, g0 = 0;
+        const int nt = it.t1 - it.t0;
+        if (it.seg > 0) chunk_range(it, T0, s0, s1);
+        for (int sg = s0; it.seg == 0 ? g0 < nt : sg < s1; ++sg, ++q) {
+            const int st = q % kStages;
+            if (q >= (uint32_t)kStages) mbar_wait(&R.empty[st], ((q / kStages) - 1) & 1u);
+            double *dst = stage + st * kStage;
+            if (it.seg < 0) {
+                tma_load_1d(dst, base, 0u, &R.full[st]);  // finaliser: the stage is its scratch
+            } else if (it.seg == 0) {  // one group of small tiles
+                const int g1 = group_end(M.T, nt, g0);
+                const tsb_ldlt_tile &Tl = M.T[g1 - 1];
+                const int64_t end = Tl.off + (int64_t)Tl.np * (2 * kTile);
+                tma_load_1d(dst, base + M.T[g0].off, (uint32_t)((end - M.T[g0].off) * 8), &R.full[st]);
+                g0 = g1;
+            } else {
+                const int p0 = sg * kSegPairs, cnt = min(kSegPairs, T0.np - p0);
+                tma_load_1d(dst, base + T0.off + (int64_t)p0 * (2 * kTile), (uint32_t)(cnt * 2 * kTile * 8),
+                            &R.full[st]);
+            }
+        }
+    }
+    R.q_prod = q;
+    R.k_prod = k;
+}
+
+// ---- consumer side ---------------------------------------------------------
+// Next mailbox entry (all consumer threads); hand it back with mail_done()
+// once the item is finished.
+__device__ __forceinline__ const MailEntry &next_item(SweepRing &R, uint32_t k) {
+    const int e = k & 1;
+    mbar_wait(&R.posted[e], (k >> 1) & 1u);
+    return R.mail[e];
+}
+__device__ __forceinline__ void mail_done(SweepRing &R, uint32_t &k) {  // after a csync()
+    if (threadIdx.x == 0) mbar_arrive(&R.taken[k & 1]);
+    ++k;
+}
+// Wait for ring copy q; returns its stage.
+__device__ __forceinline__ double *ring_wait(SweepRing &R, uint32_t q, double *stage) {
+    const int st = q % kStages;
+    mbar_wait(&R.full[st], (q / kStages) & 1u);
+    return stage + st * kStage;
+}
+// Hand ring copy q's stage back to the producer (after a csync()).
+__device__ __forceinline__ void ring_release(SweepRing &R, uint32_t q) {
+    if (threadIdx.x == 0) mbar_arrive(&R.empty[q % kStages]);
+}
+
+// GEMV of an item against the shared vector v (v[t] = column t).
+// emit(row, value) once per tile row (block-relative row index).  A chunk
+// item of a large tile consumes its segments from the ring in order, each
+// consumer warp accumulating its share of every segment's pairs; the chunk's
+// 32 partial sums go to the tile's scratch and the last chunk to finish adds
+// them in chunk order and emits.  q = the item's first ring copy (advanced).
 template <class Emit>
-__device__ __forceinline__ void item_gemv(const Item &it, const tsb_ldlt_tile *tiles, double *stage, uint64_t *bars,
-                                          uint32_t &phase, const double *v, double *red, double *part,
-                                          int32_t *tcnt, const Emit &emit) {
+__device__ __forceinline__ void item_gemv(SweepRing &R, uint32_t &q, const Item &it, const tsb_ldlt_tile *tiles,
+                                          double *stage, const double *v, double *red, double *part, int32_t *tcnt,
+                                          const Emit &emit) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    mbar_wait(&bars[0], phase & 1u);
-    phase ^= 1u;
-    if (it.seg == 0) {
-        const int64_t off0 = tiles[it.t0].off;
-        for (int t = it.t0 + warp; t < it.t1; t += kWarps) {
-            const tsb_ldlt_tile T = tiles[t];
-            const double a = tile_dot(stage + (T.off - off0), v + T.tl, 0, T.np, 1, lane);
-            if (lane < T.nrows) emit(T.row0 + lane, a);
+    if (it.seg == 0) {  // tiles = the item's tiles (mailbox), one ring copy per group, one warp per tile
+        const int nt = it.t1 - it.t0;
+        for (int g0 = 0; g0 < nt; ++q) {
+            const int g1 = group_end(tiles, nt, g0);
+            const double *sd = ring_wait(R, q, stage);
+            const int64_t off0 = tiles[g0].off;
+            if (g0 + warp < g1) {
+                const tsb_ldlt_tile T = tiles[g0 + warp];
+                const double a = tile_dot(sd + (T.off - off0), v + T.tl, 0, T.np, 1, lane);
+                if (lane < T.nrows) emit(T.row0 + lane, a);
+            }
+            csync();
+            ring_release(R, q);
+            g0 = g1;
         }
         return;
     }
     __shared__ int last_seg;
-    const tsb_ldlt_tile T = tiles[it.t0];
-    const int s = it.seg - 1, p0 = s * kSegPairs, cnt = min(kSegPairs, T.np - p0);
-    red[warp * 32 + lane] = tile_dot(stage, v + T.tl + 2 * p0, warp, cnt, kWarps, lane);
-    __syncthreads();
+    const tsb_ldlt_tile T = tiles[0];
+    int s0, s1;
+    chunk_range(it, T, s0, s1);
+    double acc = 0.0;
+    for (int sg = s0; sg < s1; ++sg, ++q) {
+        const double *sd = ring_wait(R, q, stage);
+        const int p0 = sg * kSegPairs, cnt = min(kSegPairs, T.np - p0);
+        acc += tile_dot(sd, v + T.tl + 2 * p0, warp, cnt, kWarps, lane);
+        csync();  // every consumer warp is done with the stage
+        ring_release(R, q);
+    }
+    red[warp * 32 + lane] = acc;
+    csync();
     if (threadIdx.x < 32) {
         double a = 0.0;
 #pragma unroll
         for (int w = 0; w < kWarps; ++w) a += red[w * 32 + threadIdx.x];
-        part[((int64_t)T.part + s) * kTile + threadIdx.x] = a;
+        part[((int64_t)T.part + it.seg - 1) * kTile + threadIdx.x] = a;
     }
-    __syncthreads();
+    csync();
     if (threadIdx.x == 0) last_seg = atom_add_acq_rel(tcnt + it.t0, 1) == T.nseg - 1;
-    __syncthreads();
+    csync();
     if (last_seg && threadIdx.x < 32) {
         double a = 0.0;
-        for (int q = 0; q < T.nseg; ++q) a += __ldcg(part + ((int64_t)T.part + q) * kTile + threadIdx.x);
+        for (int c = 0; c < T.nseg; ++c) a += __ldcg(part + ((int64_t)T.part + c) * kTile + threadIdx.x);
         if ((int)threadIdx.x < T.nrows) emit(T.row0 + threadIdx.x, a);
     }
 }
@@ -364,47 +530,64 @@ __device__ __forceinline__ void tile_dot_nr(int nr, const double *d, const doubl
 }
 
 // item_gemv for nr <= 8 right-hand sides: each staged tile pair read once for
-// all of them; segment partials of all right-hand sides reduced after one
-// barrier (red: [nr][8 warps][32]); emit(row, j, value).
+// all of them; chunk partials of all right-hand sides reduced after one
+// barrier (red: [nr][7 warps][32]); emit(row, j, value).
 template <class Emit>
-__device__ __forceinline__ void item_gemv_multi(const Item &it, const tsb_ldlt_tile *tiles, double *stage,
-                                                uint64_t *bars, uint32_t &phase, const double *v, int vstride, int nr,
-                                                double *red, double *part, int64_t ld_part, int32_t *tcnt,
-                                                const Emit &emit) {
+__device__ __forceinline__ void item_gemv_multi(SweepRing &R, uint32_t &q, const Item &it, const tsb_ldlt_tile *tiles,
+                                                double *stage, const double *v, int vstride, int nr, double *red,
+                                                double *part, int64_t ld_part, int32_t *tcnt, const Emit &emit) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     double out[8];
-    mbar_wait(&bars[0], phase & 1u);
-    phase ^= 1u;
     if (it.seg == 0) {
-        const int64_t off0 = tiles[it.t0].off;
-        for (int t = it.t0 + warp; t < it.t1; t += kWarps) {
-            const tsb_ldlt_tile T = tiles[t];
-            tile_dot_nr(nr, stage + (T.off - off0), v + T.tl, vstride, 0, T.np, 1, lane, out);
-            if (lane < T.nrows)
-                for (int j = 0; j < nr; ++j) emit(T.row0 + lane, j, out[j]);
+        const int nt = it.t1 - it.t0;
+        for (int g0 = 0; g0 < nt; ++q) {
+            const int g1 = group_end(tiles, nt, g0);
+            const double *sd = ring_wait(R, q, stage);
+            const int64_t off0 = tiles[g0].off;
+            if (g0 + warp < g1) {
+                const tsb_ldlt_tile T = tiles[g0 + warp];
+                tile_dot_nr(nr, sd + (T.off - off0), v + T.tl, vstride, 0, T.np, 1, lane, out);
+                if (lane < T.nrows)
+                    for (int j = 0; j < nr; ++j) emit(T.row0 + lane, j, out[j]);
+            }
+            csync();
+            ring_release(R, q);
+            g0 = g1;
         }
         return;
     }
     __shared__ int last_seg_m;
-    const tsb_ldlt_tile T = tiles[it.t0];
-    const int s = it.seg - 1, p0 = s * kSegPairs, cnt = min(kSegPairs, T.np - p0);
-    tile_dot_nr(nr, stage, v + T.tl + 2 * p0, vstride, warp, cnt, kWarps, lane, out);
-    for (int j = 0; j < nr; ++j) red[(j * kWarps + warp) * 32 + lane] = out[j];
-    __syncthreads();
-    if ((int)threadIdx.x < 32 * nr) {
-        const int j = threadIdx.x >> 5, l = threadIdx.x & 31;
+    const tsb_ldlt_tile T = tiles[0];
+    int s0, s1;
+    chunk_range(it, T, s0, s1);
+    double acc[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] = 0.0;
+    for (int sg = s0; sg < s1; ++sg, ++q) {
+        const double *sd = ring_wait(R, q, stage);
+        const int p0 = sg * kSegPairs, cnt = min(kSegPairs, T.np - p0);
+        tile_dot_nr(nr, sd, v + T.tl + 2 * p0, vstride, warp, cnt, kWarps, lane, out);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] += out[j];
+        csync();
+        ring_release(R, q);
+    }
+    for (int j = 0; j < nr; ++j) red[(j * kWarps + warp) * 32 + lane] = acc[j];
+    csync();
+    for (int idx = threadIdx.x; idx < 32 * nr; idx += kCThreads) {
+        const int j = idx >> 5, l = idx & 31;
         double a = 0.0;
 #pragma unroll
         for (int w = 0; w < kWarps; ++w) a += red[(j * kWarps + w) * 32 + l];
-        part[j * ld_part + ((int64_t)T.part + s) * kTile + l] = a;
+        part[j * ld_part + ((int64_t)T.part + it.seg - 1) * kTile + l] = a;
     }
-    __syncthreads();
+    csync();
     if (threadIdx.x == 0) last_seg_m = atom_add_acq_rel(tcnt + it.t0, 1) == T.nseg - 1;
-    __syncthreads();
+    csync();
     if (last_seg_m && threadIdx.x < 32) {
         for (int j = 0; j < nr; ++j) {
             double a = 0.0;
-            for (int q = 0; q < T.nseg; ++q) a += __ldcg(part + j * ld_part + ((int64_t)T.part + q) * kTile + threadIdx.x);
+            for (int c = 0; c < T.nseg; ++c) a += __ldcg(part + j * ld_part + ((int64_t)T.part + c) * kTile + threadIdx.x);
             if ((int)threadIdx.x < T.nrows) emit(T.row0 + threadIdx.x, j, a);
         }
     }
@@ -412,46 +595,54 @@ __device__ __forceinline__ void item_gemv_multi(const Item &it, const tsb_ldlt_t
 
 // ---------------------------------------------------------------------------
 // lower sweep: L y = r   (column-major pre-accumulation, one GEMV per block)
-//   item (b, tiles of G_b rows): stage the tiles by TMA and the block's input
-//   before the wait, form x_b = input - contributions, then
+//   item (b, tiles of G_b rows): stage the block's input window while the
+//   item's tiles stream in, form x_b = input - contributions, then
 //       triangle row i:  y_i = x_i + sum_{j<i} Linv_ij x_j          -> x[start+i]
 //       M row k:         c_k = sum_j M_kj x_j                        -> cbuf slot
 //   and count the item on the parent; a mode-2 parent's contribution sums
-//   are formed once by the item that completes it.
-// shared memory: [stage][xs max_m+2][cbs max_cb][offs int32 max_m+2][dsts int32]
+//   are formed once by its finaliser items.
+// shared memory: [ring stages][xs max_v+2][cbs max_cb][offs int32][dsts int32]
 // ---------------------------------------------------------------------------
 template <bool TRACE, bool MULTI = false>
 __device__ __forceinline__ void lower_sweep_body(const tsb_ldlt_desc &D, const SweepArgs &A, double *smem,
-                                                 uint64_t *bars, uint32_t &phase) {
+                                                 SweepRing &R) {
     double *stage = smem;
-    double *xs = smem + kStage;                       // x_b over the item's window [w0, w1) (nr windows)
+    const Item *items = reinterpret_cast<const Item *>(D.d_items_lower);
+    if ((threadIdx.x >> 5) == kProducerWarp) {
+        sweep_producer(R, D.d_ctl, D.n_items_lower, items, D.d_blocks, D.d_tiles_lower, D.d_g, stage, false);
+        lower_exit(D);
+        return;
+    }
+    double *xs = smem + kStages * kStage;             // x_b over the item's window [w0, w1) (nr windows)
     const int nr = MULTI ? A.nr : 1, xstride = (D.max_v + 3) & ~1;
     double *cbs = xs + nr * xstride;
     int32_t *offs = reinterpret_cast<int32_t *>(cbs + ((D.max_cb + 1) & ~1));
     const int noffs = (D.max_v + 2 > kFinRows + 2 ? D.max_v + 2 : kFinRows + 2);
     int32_t *dsts = offs + ((noffs + 1) & ~1);
-    double *redm = reinterpret_cast<double *>(dsts + kMaxItemRows);  // MULTI: [nr][8 warps][32] segment partials
-    __shared__ int item_id;
+    double *redm = reinterpret_cast<double *>(dsts + kMaxItemRows);  // MULTI: [nr][7 warps][32] chunk partials
     __shared__ double red[kSweepBlock];
-    int32_t *ctl = D.d_ctl;
     int64_t *const tbuf = TRACE ? D.d_trace_lower : nullptr;  // folds away when off
     const int tid = threadIdx.x;
-    const Item *items = reinterpret_cast<const Item *>(D.d_items_lower);
+    uint32_t q = R.q_cons, k = R.k_cons;
     while (true) {
-        if (tid == 0) item_id = atomicAdd(ctl, 1);
-        __syncthreads();
-        const int iid = item_id;
-        if (iid >= D.n_items_lower) break;
+        const MailEntry &M = next_item(R, k);
+        const int iid = M.iid;
+        if (iid >= D.n_items_lower) {
+            csync();
+            mail_done(R, k);
+            break;
+        }
         trace(tbuf, iid, 0);
-        const Item it = items[iid];
-        const tsb_ldlt_block B = D.d_blocks[it.block];
+        const Item it = M.it;
+        const tsb_ldlt_block B = M.B;
         const int m = B.m, s = B.start;
         if (it.seg < 0) {
             // finaliser item (mode 2): x_b = input - contributions for rows
             // [t0, t1), once the children are done; contributions staged piece
-            // by piece with coalesced loads, one thread per row sums in order
+            // by piece in the item's ring stage, one thread per row sums in order
+            double *scratch = ring_wait(R, q, stage);
             if (tid == 0) spin_until_geq(D.d_cnt_l + it.block, B.target_l);
-            __syncthreads();
+            csync();
             trace(tbuf, iid, 1);
             int i0 = it.t0;
             while (i0 < it.t1) {
@@ -467,30 +658,32 @@ __device__ __forceinline__ void lower_sweep_body(const tsb_ldlt_desc &D, const S
                 }
                 const int cnt = (int)(__ldg(D.d_cin_ptr + s + i1) - qb);
                 const bool staged = cnt <= kStage;
-                for (int i = i0 + tid; i <= i1; i += kSweepBlock) offs[i - i0] = (int32_t)(__ldg(D.d_cin_ptr + s + i) - qb);
+                for (int i = i0 + tid; i <= i1; i += kCThreads) offs[i - i0] = (int32_t)(__ldg(D.d_cin_ptr + s + i) - qb);
                 for (int j = 0; j < nr; ++j) {  // right-hand side j (nr > 1: multi-RHS sweep)
                     const double *cbj = D.d_cbuf + j * A.ld_cb + qb;
-                    if (staged) stage_copy(stage, cbj, cnt);
-                    __syncthreads();
-                    for (int i = i0 + tid; i < i1; i += kSweepBlock)
+                    if (staged) stage_copy(scratch, cbj, cnt);
+                    csync();
+                    for (int i = i0 + tid; i < i1; i += kCThreads)
                         D.d_x[j * A.ld + s + i] =
                             lower_input(A, s + i, j) -
-                            (staged ? contrib_sum<false>(stage, offs[i - i0], offs[i - i0 + 1])
+                            (staged ? contrib_sum<false>(scratch, offs[i - i0], offs[i - i0 + 1])
                                     : contrib_sum<true>(cbj, offs[i - i0], offs[i - i0 + 1]));
-                    __syncthreads();
+                    csync();
                 }
                 i0 = i1;
             }
-            if (tid == 0) atom_add_release(D.d_ready_l + it.block, 1);
+            ring_release(R, q);
+            ++q;
+            mail_done(R, k);
+            if (tid == 0) red_add_release(D.d_ready_l + it.block, 1);
             trace(tbuf, iid, 2);
             continue;
         }
-        int w0, w1;
-        item_window(it, D.d_tiles_lower, m, w0, w1);
+        const int w0 = M.w0, w1 = M.w1;
         const int nw = w1 - w0;
         // everything that does not depend on the sweep's progress is fetched
-        // before the wait: the factor tiles (TMA), the window's input, the slots
-        stage_item(it, D.d_tiles_lower, D.d_g, stage, bars);
+        // before the wait: the window's input, the contribution slots (the
+        // factor tiles are already streaming in through the ring)
         {
             struct In {
                 const SweepArgs &A;
@@ -503,19 +696,19 @@ __device__ __forceinline__ void lower_sweep_body(const tsb_ldlt_desc &D, const S
                 for (int j = 0; j < nr; ++j) batched(nw, In{A, xs + j * xstride, s + w0, j});
         }
         if (tid < nr) xs[tid * xstride + nw] = 0.0;  // column pad of odd-width tiles
-        const tsb_ldlt_tile Tf = D.d_tiles_lower[it.t0], Tb = D.d_tiles_lower[it.t1 - 1];
+        const tsb_ldlt_tile &Tf = M.T[0], &Tb = M.T[it.seg ? 0 : it.t1 - 1 - it.t0];
         const int r_hi = Tb.row0 + Tb.nrows, mr0 = max(Tf.row0, m);
-        for (int j = mr0 + tid; j < r_hi; j += kSweepBlock) dsts[j - mr0] = __ldg(D.d_cslot + B.anc_off + (j - m));
+        for (int j = mr0 + tid; j < r_hi; j += kCThreads) dsts[j - mr0] = __ldg(D.d_cslot + B.anc_off + (j - m));
         int64_t cb0 = 0;
         if (B.mode == 1) {
             cb0 = __ldg(D.d_cin_ptr + s + w0);
-            for (int j = tid; j <= nw; j += kSweepBlock) offs[j] = (int32_t)(__ldg(D.d_cin_ptr + s + w0 + j) - cb0);
+            for (int j = tid; j <= nw; j += kCThreads) offs[j] = (int32_t)(__ldg(D.d_cin_ptr + s + w0 + j) - cb0);
         }
         if (tid == 0) {
             if (B.mode == 1) spin_until_geq(D.d_cnt_l + it.block, B.target_l);
             else if (B.mode == 2) spin_until_geq(D.d_ready_l + it.block, B.nfin);
         }
-        __syncthreads();
+        csync();
         trace(tbuf, iid, 1);
         // x_b = input - (contributions of the descendants) over the window
         if (B.mode == 1) {  // rows in pieces whose contributions fit the buffer, per right-hand side
@@ -536,11 +729,11 @@ __device__ __forceinline__ void lower_sweep_body(const tsb_ldlt_desc &D, const S
                     const int base = offs[i0], cnt = offs[i1] - base;
                     const bool fits = cnt <= D.max_cb;
                     if (fits) stage_copy(cbs, cbj + base, cnt);
-                    __syncthreads();
-                    for (int jj = i0 + tid; jj < i1; jj += kSweepBlock)
+                    csync();
+                    for (int jj = i0 + tid; jj < i1; jj += kCThreads)
                         xj[jj] = xj[jj] - (fits ? contrib_sum<false>(cbs, offs[jj] - base, offs[jj + 1] - base)
                                                 : contrib_sum<true>(cbj, offs[jj], offs[jj + 1]));
-                    __syncthreads();
+                    csync();
                     i0 = i1;
                 }
             }
@@ -553,7 +746,7 @@ __device__ __forceinline__ void lower_sweep_body(const tsb_ldlt_desc &D, const S
             };
             for (int j = 0; j < nr; ++j) batched(nw, Ld{D.d_x + j * A.ld + s + w0, xs + j * xstride});
         }
-        __syncthreads();
+        csync();
         trace(tbuf, iid, 4);
         if (!MULTI) {
             auto emit = [&](int r, double a) {
@@ -562,7 +755,7 @@ __device__ __forceinline__ void lower_sweep_body(const tsb_ldlt_desc &D, const S
                 else
                     D.d_cbuf[dsts[r - mr0]] = a;
             };
-            item_gemv(it, D.d_tiles_lower, stage, bars, phase, xs - w0, red, D.d_part_lower, D.d_tcnt_lower, emit);
+            item_gemv(R, q, it, M.T, stage, xs - w0, red, D.d_part_lower, D.d_tcnt_lower, emit);
         } else {
             auto emit = [&](int r, int j, double a) {
                 if (r < m)
@@ -570,13 +763,18 @@ __device__ __forceinline__ void lower_sweep_body(const tsb_ldlt_desc &D, const S
                 else
                     D.d_cbuf[j * A.ld_cb + dsts[r - mr0]] = a;
             };
-            item_gemv_multi(it, D.d_tiles_lower, stage, bars, phase, xs - w0, xstride, nr, redm, D.d_part_lower,
-                            A.ld_part, D.d_tcnt_lower, emit);
+            item_gemv_multi(R, q, it, M.T, stage, xs - w0, xstride, nr, redm, D.d_part_lower, A.ld_part,
+                            D.d_tcnt_lower, emit);
         }
         trace(tbuf, iid, 5);
-        __syncthreads();
-        if (tid == 0 && B.parent >= 0) atom_add_release(D.d_cnt_l + B.parent, 1);
+        csync();
+        mail_done(R, k);
+        if (tid == 0 && B.parent >= 0) red_add_release(D.d_cnt_l + B.parent, 1);
         trace(tbuf, iid, 2);
+    }
+    if (tid == 0) {
+        R.q_cons = q;
+        R.k_cons = k;
     }
     lower_exit(D);
 }
@@ -584,70 +782,80 @@ __device__ __forceinline__ void lower_sweep_body(const tsb_ldlt_desc &D, const S
 // ---------------------------------------------------------------------------
 // upper sweep: L^T z = w   (row-major pull, one GEMV per block)
 //   z_b = w_b + G_b^T v,  v = [w_b ; -z_anc]
-//   item (b, tiles of G_b^T rows = columns of G_b): stage the tiles by TMA
-//   and w_b before the wait (only -z_anc depends on the parent), then
-//   z_c = v_c + sum_{t > c} G^T[c][t] v_t for the item's columns.
-// shared memory: [stage][v max_v+2]
+//   item (b, tiles of G_b^T rows = columns of G_b): w_b is staged before the
+//   wait (only -z_anc depends on the parent), the tiles stream through the
+//   ring, then z_c = v_c + sum_{t > c} G^T[c][t] v_t for the item's columns.
+// shared memory: [ring stages][v max_v+2]
 // ---------------------------------------------------------------------------
 template <bool TRACE>
 __device__ __forceinline__ void upper_sweep_body(const tsb_ldlt_desc &D, const SweepArgs &A, double *smem,
-                                                 uint64_t *bars, uint32_t &phase) {
+                                                 SweepRing &R) {
     double *stage = smem;
-    double *v = smem + kStage;  // [w_b; -z_anc] over the item's window [w0, w1)
-    __shared__ int item_id;
+    const Item *items = reinterpret_cast<const Item *>(D.d_items_upper);
+    if ((threadIdx.x >> 5) == kProducerWarp) {
+        sweep_producer(R, D.d_ctl + 2, D.n_items_upper, items, D.d_blocks, D.d_tiles_upper, D.d_gt, stage, true);
+        upper_exit(D);
+        return;
+    }
+    double *v = smem + kStages * kStage;  // [w_b; -z_anc] over the item's window [w0, w1)
     __shared__ double red[kSweepBlock];
-    int32_t *ctl = D.d_ctl + 2;
     int64_t *const tbuf = TRACE ? D.d_trace_upper : nullptr;
     const int tid = threadIdx.x;
-    const Item *items = reinterpret_cast<const Item *>(D.d_items_upper);
+    uint32_t q = R.q_cons, k = R.k_cons;
     while (true) {
-        if (tid == 0) item_id = atomicAdd(ctl, 1);
-        __syncthreads();
-        const int iid = item_id;
-        if (iid >= D.n_items_upper) break;
+        const MailEntry &M = next_item(R, k);
+        const int iid = M.iid;
+        if (iid >= D.n_items_upper) {
+            csync();
+            mail_done(R, k);
+            break;
+        }
         trace(tbuf, iid, 0);
-        const Item it = items[iid];
-        const tsb_ldlt_block B = D.d_blocks[it.block];
+        const Item it = M.it;
+        const tsb_ldlt_block B = M.B;
         const int m = B.m, s = B.start, na = B.na;
-        int w0, w1;
-        item_window(it, D.d_tiles_upper, m + na, w0, w1);
+        const int w0 = M.w0, w1 = M.w1;
         const int nw = w1 - w0;
-        stage_item(it, D.d_tiles_upper, D.d_gt, stage, bars);
-        for (int t = w0 + tid; t < min(w1, m); t += kSweepBlock) {  // w_b: produced before this sweep
+        for (int t = w0 + tid; t < min(w1, m); t += kCThreads) {  // w_b: produced before this sweep
             double w = __ldcg(A.in + s + t);
             if (A.dscale) w = w / A.dscale[s + t];
             v[t - w0] = w;
         }
         const int k0 = max(w0, m) - m, k1 = w1 - m;  // ancestor entries in the window
-        for (int k = k0 + tid; k < k1; k += kSweepBlock)  // rows parked in v until the wait is over
-            v[m + k - w0] = __longlong_as_double((long long)__ldg(D.d_anc + B.anc_off + k));
+        for (int kk = k0 + tid; kk < k1; kk += kCThreads)  // rows parked in v until the wait is over
+            v[m + kk - w0] = __longlong_as_double((long long)__ldg(D.d_anc + B.anc_off + kk));
         if (tid == 0) v[nw] = 0.0;  // column pad of odd-width tiles
         if (k1 > k0 && B.parent >= 0 && tid == 0)  // parent outside the handle (shard): solved before
             spin_until_geq(D.d_done_u + B.parent, D.d_blocks[B.parent].n_u);
-        __syncthreads();
+        csync();
         trace(tbuf, iid, 1);
         if (k1 > k0) {
             struct Anc {
                 const double *x;
                 double *va;
-                __device__ double load(int k) const { return __ldcg(x + __double_as_longlong(va[k])); }
-                __device__ void store(int k, double z) const { va[k] = -z; }
+                __device__ double load(int j) const { return __ldcg(x + __double_as_longlong(va[j])); }
+                __device__ void store(int j, double z) const { va[j] = -z; }
             };
             batched(k1 - k0, Anc{A.x, v + (m + k0 - w0)});
         }
-        __syncthreads();
+        csync();
         trace(tbuf, iid, 4);
         {
             auto emit = [&](int c, double z) {  // unit diagonal stored: z_c = sum_{t >= c} G^T[c][t] v_t
                 A.x[s + c] = z;
                 if (A.out_perm) A.out[A.out_perm[s + c]] = z;
             };
-            item_gemv(it, D.d_tiles_upper, stage, bars, phase, v - w0, red, D.d_part_upper, D.d_tcnt_upper, emit);
+            item_gemv(R, q, it, M.T, stage, v - w0, red, D.d_part_upper, D.d_tcnt_upper, emit);
         }
         trace(tbuf, iid, 5);
-        __syncthreads();
-        if (tid == 0) atom_add_release(D.d_done_u + it.block, 1);
+        csync();
+        mail_done(R, k);
+        if (tid == 0) red_add_release(D.d_done_u + it.block, 1);
         trace(tbuf, iid, 2);
+    }
+    if (tid == 0) {
+        R.q_cons = q;
+        R.k_cons = k;
     }
     upper_exit(D);
 }

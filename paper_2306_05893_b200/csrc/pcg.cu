@@ -105,8 +105,8 @@ __device__ __forceinline__ double all_partials(const double *part, int kind, dou
     return out;
 }
 
-// MINB = resident CTAs per SM the register budget is sized for: LDL^T 3
-// (sweep staging in shared memory); Jacobi / identity 3 for small systems
+// MINB = resident CTAs per SM the register budget is sized for: LDL^T 2
+// (two 40 KB sweep stages per CTA in shared memory); Jacobi / identity 3 for small systems
 // (grid-barrier bound), 6 for large ones (the SpMV is gather-latency bound)
 template <int KIND, int MINB>
 __global__ void __launch_bounds__(kPcgBlock, MINB)
@@ -114,21 +114,14 @@ pcg_persistent(PcgWork W, PcgArgs a, tsb_ldlt_desc D) {
     extern __shared__ __align__(128) double smem[];  // sweep staging (LDL^T)
     __shared__ double red[32];
     __shared__ double bc;
-    __shared__ uint64_t mbar[2];
+    __shared__ SweepRing ring;
     const int tid = threadIdx.x;
     const int64_t n = W.n;
     const int64_t gtid = (int64_t)blockIdx.x * kPcgBlock + tid, gstride = (int64_t)gridDim.x * kPcgBlock;
     const int lane8 = tid & 7;
     const unsigned gmask = 0xffu << ((tid & 31) & 24);
     const int64_t grp = gtid >> 3, ngrp = gstride >> 3;
-    uint32_t phase = 0;
-    if (KIND == TSB_PRECOND_LDLT) {
-        if (tid == 0) {
-            mbar_init(&mbar[0], 1);
-            mbar_init(&mbar[1], 1);
-        }
-        __syncthreads();
-    }
+    if (KIND == TSB_PRECOND_LDLT) ring_init(ring);
     // ---- init (krylov.py:130-141) -------------------------------------------
     double bb = 0.0, rr = 0.0;
     for (int64_t i = gtid; i < n; i += gstride) {
@@ -208,9 +201,9 @@ pcg_persistent(PcgWork W, PcgArgs a, tsb_ldlt_desc D) {
     if (!done) {
         double v = 0.0;
         if (KIND == TSB_PRECOND_LDLT) {
-            lower_sweep_body<false>(D, lo_args, smem, mbar, phase);
+            lower_sweep_body<false>(D, lo_args, smem, ring);
             grid_sync(W.bar);
-            upper_sweep_body<false>(D, up_args, smem, mbar, phase);
+            upper_sweep_body<false>(D, up_args, smem, ring);
             grid_sync(W.bar);
             for (int64_t i = gtid; i < n; i += gstride) v += __ldcg(W.r + i) * __ldcg(W.z + i);
         } else {
@@ -313,9 +306,9 @@ pcg_persistent(PcgWork W, PcgArgs a, tsb_ldlt_desc D) {
         } else if (KIND == TSB_PRECOND_JACOBI) {
             rzn = all_partials(W.part, 1, red, &bc);
         } else {
-            lower_sweep_body<false>(D, lo_args, smem, mbar, phase);
+            lower_sweep_body<false>(D, lo_args, smem, ring);
             grid_sync(W.bar);
-            upper_sweep_body<false>(D, up_args, smem, mbar, phase);
+            upper_sweep_body<false>(D, up_args, smem, ring);
             grid_sync(W.bar);
             double w2 = 0.0;
             for (int64_t i = gtid; i < n; i += gstride) w2 += __ldcg(W.r + i) * __ldcg(W.z + i);
@@ -481,10 +474,10 @@ extern "C" int tsb_pcg_solve(tsb_pcg_t h, int64_t nrows, const int32_t *d_row_pt
             D = ldlt_desc(ldlt);
             const size_t sm = sweep_smem_lower(D) > sweep_smem_upper(D) ? sweep_smem_lower(D) : sweep_smem_upper(D);
             if (sm != h->smem_ldlt || h->grid[TSB_PRECOND_LDLT] == 0) {
-                h->grid[TSB_PRECOND_LDLT] = occupancy_grid<TSB_PRECOND_LDLT, 3>(sm);
+                h->grid[TSB_PRECOND_LDLT] = occupancy_grid<TSB_PRECOND_LDLT, 2>(sm);
                 h->smem_ldlt = sm;
             }
-            launch<TSB_PRECOND_LDLT, 3>(h, a, D, h->grid[TSB_PRECOND_LDLT], sm, s);
+            launch<TSB_PRECOND_LDLT, 2>(h, a, D, h->grid[TSB_PRECOND_LDLT], sm, s);
         } else if (kind == TSB_PRECOND_JACOBI) {
             if (h->big)
                 launch<TSB_PRECOND_JACOBI, 6>(h, a, D, h->grid[TSB_PRECOND_JACOBI], 0, s);

@@ -59,7 +59,7 @@ def emulate_lower(H, r):
         else:
             assert B["target_l"] == 0
             xs = r[s:s + m].copy()
-        for t in range(t0, t1):
+        for t in ([t0] if sg > 0 else range(t0, t1)):
             if sg:  # segment item: the tile's rows are emitted by its last segment
                 segs[t] += 1
                 if segs[t] < H["tiles_l"]["nseg"][t]:
@@ -80,9 +80,13 @@ def emulate_lower(H, r):
     return y
 
 
-def test_all_lower_input_modes_are_exercised():
+def test_all_lower_input_modes_are_exercised(monkeypatch):
     _, f = _factors((10, 10, 60), 64)
-    H = K.pack(f)
+    for ratio in (1.0, 0.5, 0.25, 0.1):  # a gather/finaliser threshold that splits the inner blocks
+        monkeypatch.setattr(K, "GATHER_RATIO", ratio)
+        H = K.pack(f)
+        if len(set(H["blocks"]["mode"].tolist())) == 3:
+            break
     modes = set(H["blocks"]["mode"].tolist())
     assert modes == {K.MODE_LEAF, K.MODE_GATHER, K.MODE_FIN}
     assert (H["items_l"][:, 3] < 0).sum() == H["blocks"]["nfin"].sum() > 0
@@ -105,7 +109,7 @@ def emulate_upper(H, w, z=None):
             p = int(B["parent"])
             assert done[p] == blocks[p]["n_u"], "upper item dispatched before the parent's z"
         v = np.concatenate([w[s:s + m], -z[H["anc"][B["anc_off"]: B["anc_off"] + na]]])
-        for t in range(t0, t1):
+        for t in ([t0] if sg > 0 else range(t0, t1)):
             if sg:
                 segs[t] += 1
                 if segs[t] < H["tiles_u"]["nseg"][t]:

@@ -125,6 +125,8 @@ def main():
     if args.out:
         Path(args.out).write_text(txt)
         keep = {k: H[k] for k in ("items_l", "items_u", "parent")}
+        keep.update(np_l=H["tiles_l"]["np"], np_u=H["tiles_u"]["np"], m=H["blocks"]["m"], na=H["blocks"]["na"],
+                    mode=H["blocks"]["mode"])
         np.savez_compressed(Path(args.out).with_suffix(".npz"), trace_l=dev.trace_l.cpu().numpy(),
                             trace_u=dev.trace_u.cpu().numpy(), **keep)
 
