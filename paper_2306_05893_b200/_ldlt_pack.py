@@ -56,8 +56,13 @@ from . import _lib
 TILE = 32               # rows per tile (one per lane)
 ITEM_BYTES = 40 * 1024  # small-tile item budget: one TMA bulk copy (csrc kStage)
 SEG_PAIRS = 80          # pairs per column segment of a large tile (80 * 32 * 16 B = 40 KB, csrc kSegPairs)
-SEGS_PER_ITEM = int(os.environ.get("TSB_SEGS_PER_ITEM", "4"))  # segments streamed by one chunk item
-GROUPS_PER_ITEM = int(os.environ.get("TSB_GROUPS_PER_ITEM", "4"))  # small-tile TMA groups per item (<= csrc kGroupsPerItem)
+# item granularity by regime (tools/item_tune.py, B200): latency-bound factors
+# (stored lower tiles <= GATHER_BIG_BYTES) keep items short -- cfg2 apply
+# 0.168 ms at 2/2 vs 0.198 at 4/4 -- bandwidth-bound ones amortise the per-item
+# chain over more bytes -- cfg3 1.13 ms at 8/4 and 6/4 vs 1.16 at 4/4, 1.86 at 16/4
+SEGS_PER_ITEM = int(os.environ["TSB_SEGS_PER_ITEM"]) if "TSB_SEGS_PER_ITEM" in os.environ else None
+GROUPS_PER_ITEM = min(4, int(os.environ["TSB_GROUPS_PER_ITEM"])) if "TSB_GROUPS_PER_ITEM" in os.environ else None
+SEGS_SMALL, GROUPS_SMALL, SEGS_BIG, GROUPS_BIG = 2, 2, 8, 4
 WARPS = 7               # consumer warps per CTA (csrc kWarps): one small tile each
 MERGE_ROWS = 0          # default subtree amalgamation (rows); 0 = off
 CB_CAP = 1024           # contributions staged per piece when a block's items sum them (csrc max_cb)
@@ -243,22 +248,22 @@ def amalgamate(factors, max_rows: int):
     return _MergedFactors(factors, blocks)
 
 
-def _items(tiles_of_block, first_tile):
+def _items(tiles_of_block, first_tile, segs, groups_per_item):
     """Group a block's tiles into items -> list of (t0, t1, seg) in global tile ids
     (seg = 0: small tiles [t0, t1); seg = c + 1: chunk c of large tile t0, i.e.
-    its column segments [c t1, c t1 + t1), t1 = SEGS_PER_ITEM)."""
+    its column segments [c t1, c t1 + t1), t1 = segs)."""
     out = []
     k = 0
     nt = len(tiles_of_block)
     while k < nt:
         npair = tiles_of_block[k][1]
         if npair * TILE * 16 > ITEM_BYTES:
-            for c in range(_nchunks(npair)):
-                out.append((first_tile + k, SEGS_PER_ITEM, c + 1))
+            for c in range(_nchunks(npair, segs)):
+                out.append((first_tile + k, segs, c + 1))
             k += 1
             continue
-        k1, groups = k, 0  # up to GROUPS_PER_ITEM TMA groups of small tiles (csrc group_end)
-        while groups < GROUPS_PER_ITEM and k1 < nt and tiles_of_block[k1][1] * TILE * 16 <= ITEM_BYTES:
+        k1, groups = k, 0  # up to groups_per_item TMA groups of small tiles (csrc group_end)
+        while groups < groups_per_item and k1 < nt and tiles_of_block[k1][1] * TILE * 16 <= ITEM_BYTES:
             g1, tot = k1, 0
             while g1 < nt and g1 - k1 < WARPS:
                 b = tiles_of_block[g1][1] * TILE * 16
@@ -273,9 +278,17 @@ def _items(tiles_of_block, first_tile):
     return out
 
 
-def _nchunks(npair):
+def _nchunks(npair, segs):
     nsegs = (int(npair) + SEG_PAIRS - 1) // SEG_PAIRS
-    return (nsegs + SEGS_PER_ITEM - 1) // SEGS_PER_ITEM
+    return (nsegs + segs - 1) // segs
+
+
+def item_granularity(stored_lower_bytes):
+    """(segments per chunk item, TMA groups per small-tile item) for a factor."""
+    big = stored_lower_bytes > GATHER_BIG_BYTES
+    segs = SEGS_PER_ITEM if SEGS_PER_ITEM is not None else (SEGS_BIG if big else SEGS_SMALL)
+    groups = GROUPS_PER_ITEM if GROUPS_PER_ITEM is not None else (GROUPS_BIG if big else GROUPS_SMALL)
+    return segs, groups
 
 
 def _chunk_pairs(npair, it):
@@ -451,6 +464,7 @@ def pack(factors, subset=None):
                 tl_rows[up].append((pos[up], tl, npair, r0, nr))
                 data[up].append(p)
                 pos[up] += len(p)
+    segs, groups_per_item = item_granularity(pos[False] * 8)
     tables = {}
     npart = {}
     for up in (False, True):
@@ -459,7 +473,7 @@ def pack(factors, subset=None):
             arr = np.array(tl_rows[up], dtype=np.int64)
             t["off"], t["tl"], t["np"], t["row0"], t["nrows"] = arr.T
         big = t["np"].astype(np.int64) * TILE * 16 > ITEM_BYTES
-        t["nseg"] = np.where(big, [_nchunks(v) for v in t["np"]], 0)  # chunk items (partial slots) per tile
+        t["nseg"] = np.where(big, [_nchunks(v, segs) for v in t["np"]], 0)  # chunk items (partial slots) per tile
         part = np.zeros(len(t) + 1, dtype=np.int64)
         np.cumsum(t["nseg"], out=part[1:])
         t["part"] = part[:-1]
@@ -479,7 +493,8 @@ def pack(factors, subset=None):
     ext_rows = np.unique(anc_all[owner[anc_all] < 0]) if len(anc_all) else np.zeros(0, dtype=np.int64)
 
     # ---------------- items + lower input modes ----------------
-    items = {up: [_items(blk_tiles[up][i][1], blk_tiles[up][i][0]) for i in range(nb)] for up in (False, True)}
+    items = {up: [_items(blk_tiles[up][i][1], blk_tiles[up][i][0], segs, groups_per_item) for i in range(nb)]
+             for up in (False, True)}
     nl = np.array([len(x) for x in items[False]], dtype=np.int64)
     n_u = np.array([len(x) for x in items[True]], dtype=np.int64)
     target_l = np.array([sum(int(nl[c]) for c in children[i]) for i in range(nb)], dtype=np.int64)

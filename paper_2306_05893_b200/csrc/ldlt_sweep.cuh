@@ -76,6 +76,15 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
         "r"(phase)
         : "memory");
 }
+__device__ __forceinline__ bool mbar_test(uint64_t *bar, uint32_t phase) {
+    uint32_t ok;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+    return ok != 0;
+}
 // barrier of the consumer warps only (the producer warp runs its own loop)
 __device__ __forceinline__ void csync() { asm volatile("bar.sync 1, %0;" ::"n"(kCThreads) : "memory"); }
 __device__ __forceinline__ int ld_acquire(const int *p) {
@@ -151,11 +160,18 @@ struct MailEntry {
     tsb_ldlt_block B;
     tsb_ldlt_tile T[kMailTiles];
 };
+// Publication queue: the consumers hand each finished item's counter update
+// (a gpu-scope release of the item's outputs) to the producer lane, which
+// issues it between its copies -- the release fence's round trip then costs
+// the consumers nothing.  Entry j % 2 holds publication j (nullptr = the
+// consumers left the sweep).
 struct SweepRing {
     uint64_t full[kStages], empty[kStages];  // stage landed / stage read by the consumers
     uint64_t posted[2], taken[2];            // mailbox entry written / consumed
+    uint64_t pub_full[2], pub_done[2];       // publication posted / issued
     MailEntry mail[2];
-    uint32_t q_prod, k_prod, q_cons, k_cons;
+    int32_t *pub[2];
+    uint32_t q_prod, k_prod, q_cons, k_cons, p_prod, p_cons;
 };
 
 __device__ __forceinline__ void ring_init(SweepRing &R) {
@@ -167,8 +183,10 @@ __device__ __forceinline__ void ring_init(SweepRing &R) {
         for (int k = 0; k < 2; ++k) {
             mbar_init(&R.posted[k], 1);
             mbar_init(&R.taken[k], 1);
+            mbar_init(&R.pub_full[k], 1);
+            mbar_init(&R.pub_done[k], 1);
         }
-        R.q_prod = R.k_prod = R.q_cons = R.k_cons = 0;
+        R.q_prod = R.k_prod = R.q_cons = R.k_cons = R.p_prod = R.p_cons = 0;
     }
     __syncthreads();
 }
@@ -334,11 +352,31 @@ __device__ __forceinline__ void item_window(const Item &it, const tsb_ldlt_tile 
 // (one per small-tile group or chunk segment; a finaliser reserves one stage
 // as scratch), until the ticket runs past the item list (that sentinel is
 // posted too, so the consumers stop).
+// Issue every publication the consumers have posted (in order); returns false
+// once the consumers' end-of-sweep marker has been seen.
+__device__ __forceinline__ bool serve_pubs(SweepRing &R, uint32_t &p) {
+    while (true) {
+        const int e = p & 1;
+        if (!mbar_test(&R.pub_full[e], (p >> 1) & 1u)) return true;
+        int32_t *addr = R.pub[e];
+        if (addr != nullptr) red_add_release(addr, 1);
+        mbar_arrive(&R.pub_done[e]);
+        ++p;
+        if (addr == nullptr) return false;
+    }
+}
+// mbar_wait that keeps issuing publications meanwhile
+__device__ __forceinline__ void wait_serving(SweepRing &R, uint64_t *bar, uint32_t phase, uint32_t &p, bool &live) {
+    while (!mbar_test(bar, phase))
+        if (live) live = serve_pubs(R, p);
+}
+
 __device__ __forceinline__ void sweep_producer(SweepRing &R, int32_t *ticket, int64_t n_items, const Item *items,
                                                const tsb_ldlt_block *blocks, const tsb_ldlt_tile *tiles,
                                                const double *base, double *stage, bool upper) {
     if ((threadIdx.x & 31) != 0) return;
-    uint32_t q = R.q_prod, k = R.k_prod;
+    uint32_t q = R.q_prod, k = R.k_prod, p = R.p_prod;
+    bool live = true;
     while (true) {
         const int iid = atomicAdd(ticket, 1);
         const int e = k & 1;
@@ -349,7 +387,7 @@ __device__ __forceinline__ void sweep_producer(SweepRing &R, int32_t *ticket, in
             it = items[iid];
             const tsb_ldlt_block B = blocks[it.block];
             if (it.seg >= 0) T0 = tiles[it.t0];
-            if (k >= 2) mbar_wait(&R.taken[e], ((k >> 1) - 1) & 1u);
+            if (k >= 2) wait_serving(R, &R.taken[e], ((k >> 1) - 1) & 1u, p, live);
             M.it = it;
             M.B = B;
             if (it.seg > 0) {
@@ -359,7 +397,7 @@ __device__ __forceinline__ void sweep_producer(SweepRing &R, int32_t *ticket, in
             }
             if (it.seg >= 0) item_window(it, M.T, B.m + (upper ? B.na : 0), M.w0, M.w1);
         } else if (k >= 2) {
-            mbar_wait(&R.taken[e], ((k >> 1) - 1) & 1u);
+            wait_serving(R, &R.taken[e], ((k >> 1) - 1) & 1u, p, live);
         }
         M.iid = iid;
         mbar_arrive(&R.posted[e]);
@@ -370,7 +408,7 @@ __device__ __forceinline__ void sweep_producer(SweepRing &R, int32_t *ticket, in
         if (it.seg > 0) chunk_range(it, T0, s0, s1);
         for (int sg = s0; it.seg == 0 ? g0 < nt : sg < s1; ++sg, ++q) {
             const int st = q % kStages;
-            if (q >= (uint32_t)kStages) mbar_wait(&R.empty[st], ((q / kStages) - 1) & 1u);
+            if (q >= (uint32_t)kStages) wait_serving(R, &R.empty[st], ((q / kStages) - 1) & 1u, p, live);
             double *dst = stage + st * kStage;
             if (it.seg < 0) {
                 tma_load_1d(dst, base, 0u, &R.full[st]);  // finaliser: the stage is its scratch
@@ -387,8 +425,10 @@ __device__ __forceinline__ void sweep_producer(SweepRing &R, int32_t *ticket, in
             }
         }
     }
+    while (live) live = serve_pubs(R, p);  // until the consumers leave the sweep
     R.q_prod = q;
     R.k_prod = k;
+    R.p_prod = p;
 }
 
 // ---- consumer side ---------------------------------------------------------
@@ -402,6 +442,17 @@ __device__ __forceinline__ const MailEntry &next_item(SweepRing &R, uint32_t k) 
 __device__ __forceinline__ void mail_done(SweepRing &R, uint32_t &k) {  // after a csync()
     if (threadIdx.x == 0) mbar_arrive(&R.taken[k & 1]);
     ++k;
+}
+// Post a publication (consumer thread 0, after a csync()): the producer lane
+// issues red.release.gpu(addr, 1); addr == nullptr ends the sweep's queue.
+__device__ __forceinline__ void publish(SweepRing &R, uint32_t &p, int32_t *addr) {
+    if (threadIdx.x == 0) {
+        const int e = p & 1;
+        if (p >= 2) mbar_wait(&R.pub_done[e], ((p >> 1) - 1) & 1u);
+        R.pub[e] = addr;
+        mbar_arrive(&R.pub_full[e]);
+    }
+    ++p;
 }
 // Wait for ring copy q; returns its stage.
 __device__ __forceinline__ double *ring_wait(SweepRing &R, uint32_t q, double *stage) {
@@ -623,13 +674,14 @@ __device__ __forceinline__ void lower_sweep_body(const tsb_ldlt_desc &D, const S
     __shared__ double red[kSweepBlock];
     int64_t *const tbuf = TRACE ? D.d_trace_lower : nullptr;  // folds away when off
     const int tid = threadIdx.x;
-    uint32_t q = R.q_cons, k = R.k_cons;
+    uint32_t q = R.q_cons, k = R.k_cons, pc = R.p_cons;
     while (true) {
         const MailEntry &M = next_item(R, k);
         const int iid = M.iid;
         if (iid >= D.n_items_lower) {
             csync();
             mail_done(R, k);
+            publish(R, pc, nullptr);  // end of this CTA's publications
             break;
         }
         trace(tbuf, iid, 0);
@@ -675,7 +727,7 @@ __device__ __forceinline__ void lower_sweep_body(const tsb_ldlt_desc &D, const S
             ring_release(R, q);
             ++q;
             mail_done(R, k);
-            if (tid == 0) red_add_release(D.d_ready_l + it.block, 1);
+            publish(R, pc, D.d_ready_l + it.block);
             trace(tbuf, iid, 2);
             continue;
         }
@@ -769,12 +821,13 @@ __device__ __forceinline__ void lower_sweep_body(const tsb_ldlt_desc &D, const S
         trace(tbuf, iid, 5);
         csync();
         mail_done(R, k);
-        if (tid == 0 && B.parent >= 0) red_add_release(D.d_cnt_l + B.parent, 1);
+        if (B.parent >= 0) publish(R, pc, D.d_cnt_l + B.parent);
         trace(tbuf, iid, 2);
     }
     if (tid == 0) {
         R.q_cons = q;
         R.k_cons = k;
+        R.p_cons = pc;
     }
     lower_exit(D);
 }
@@ -801,13 +854,14 @@ __device__ __forceinline__ void upper_sweep_body(const tsb_ldlt_desc &D, const S
     __shared__ double red[kSweepBlock];
     int64_t *const tbuf = TRACE ? D.d_trace_upper : nullptr;
     const int tid = threadIdx.x;
-    uint32_t q = R.q_cons, k = R.k_cons;
+    uint32_t q = R.q_cons, k = R.k_cons, pc = R.p_cons;
     while (true) {
         const MailEntry &M = next_item(R, k);
         const int iid = M.iid;
         if (iid >= D.n_items_upper) {
             csync();
             mail_done(R, k);
+            publish(R, pc, nullptr);  // end of this CTA's publications
             break;
         }
         trace(tbuf, iid, 0);
@@ -850,12 +904,13 @@ __device__ __forceinline__ void upper_sweep_body(const tsb_ldlt_desc &D, const S
         trace(tbuf, iid, 5);
         csync();
         mail_done(R, k);
-        if (tid == 0) red_add_release(D.d_done_u + it.block, 1);
+        publish(R, pc, D.d_done_u + it.block);
         trace(tbuf, iid, 2);
     }
     if (tid == 0) {
         R.q_cons = q;
         R.k_cons = k;
+        R.p_cons = pc;
     }
     upper_exit(D);
 }

@@ -1,0 +1,58 @@
+"""Apply time of the LDL^T sweeps vs the item granularity (segments per chunk
+item, TMA groups per small-tile item): packs the bench workload's factors
+once per setting and times dev.run("apply") with CUDA events, L2 flushed.
+
+    python tools/item_tune.py [--workload cfg3] [--segs 1,2,4,8] [--groups 1,2,4]
+"""
+import argparse
+import json
+import statistics
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+
+import bench  # noqa: E402
+from paper_2306_05893_b200 import _ldlt_pack as K  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--workload", default="cfg3")
+    ap.add_argument("--segs", default="1,2,4,8")
+    ap.add_argument("--groups", default="1,2,4")
+    ap.add_argument("--reps", type=int, default=20)
+    args = ap.parse_args()
+    import torch
+
+    W = bench.build_workload(args.workload)
+    f = W["factors"]
+    flush = bench.L2Flush()
+    r = torch.randn(f.plan.n, dtype=torch.float64, device="cuda")
+    z = torch.empty_like(r)
+    out = []
+    for sg in map(int, args.segs.split(",")):
+        for gr in map(int, args.groups.split(",")):
+            K.SEGS_PER_ITEM, K.GROUPS_PER_ITEM = sg, min(gr, 4)  # overrides of item_granularity (csrc kGroupsPerItem)
+            dev = K.DevicePanels(f)
+            for _ in range(3):
+                dev.run("apply", r, z)
+            ts = []
+            for _ in range(args.reps):
+                flush()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                dev.run("apply", r, z)
+                e1.record()
+                e1.synchronize()
+                ts.append(e0.elapsed_time(e1))
+            row = {"segs": sg, "groups": gr, "apply_ms": statistics.median(ts), "items": dev.n_items}
+            print(json.dumps(row), flush=True)
+            out.append(row)
+            del dev
+    print(json.dumps({"workload": args.workload, "best": min(out, key=lambda x: x["apply_ms"])}))
+
+
+if __name__ == "__main__":
+    main()
