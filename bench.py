@@ -12,7 +12,8 @@ staleness 3, SURVEY.md 8d / BASELINE.md section 2).  Every timed step repeats
 the same step from the same state (nothing committed), L2 flushed between
 steps.  The CPU oracle solves the same system with the same factors and the
 run fails unless the iteration counts agree and x matches within 1e-10.
-N > 1: one independent simulation per GPU (replicas, weak scaling).
+N > 1 (torchrun): the nested-dissection sharded solve of the same mesh
+(strong scaling; --replicas: one independent simulation per GPU instead).
 --impl reference: the CPU reference path (the NumPy oracle port, oracle/),
 workload built from scratch by the oracle -- the product package is never
 imported on that arm.
@@ -41,6 +42,8 @@ WORKLOADS = {
     "cfg1": dict(dims=(6, 6, 28), law="linear", desc="config 1: ~1k-node beam, linear elastic"),
     "cfg2": dict(dims=(10, 10, 100), law="corotational", desc="config 2: ~10k-node corotational beam"),
     "cfg3": dict(dims=(20, 20, 250), law="corotational", desc="config 3: ~100k-node corotational beam"),
+    "cfg4": dict(dims=(20, 20, 2500), law="corotational",
+                 desc="config 4: ~1M-node corotational beam (nested-dissection sharded across the GPUs)"),
     "cfg5": dict(dims=(20, 20, 125), law="corotational", batch=64,
                  desc="config 5: 64 independent ~50k-node corotational beams (batched, Jacobi-PCG)"),
 }
@@ -643,6 +646,110 @@ def batch_cpu_baseline(sim, threads=1):
         return (time.perf_counter() - t0) * 1e3
 
 
+# ---------------------------------------------------------------------------
+# nested-dissection sharded step: one process per GPU
+# ---------------------------------------------------------------------------
+
+def run_sharded(args, world, rank, local, dist):
+    """Every rank assembles only its subtrees' elements (shard.rank_mesh), the
+    rank's local system is gathered on the device (shard.LocalSystem) and the
+    LDL^T-PCG runs sharded (shard.DistributedPcg: owned subtrees + replicated
+    top separators, top-row exchanges by NCCL or by our peer-memory kernels,
+    device stop flag, iterations replayed as CUDA graphs).  A step = sharded
+    assembly + local extraction + sharded solve of the scenario step's system;
+    ms per step = max over ranks; strong scaling (the mesh is fixed).  Rank 0
+    checks the result against the single-GPU PCG on the same factors."""
+    import gc
+
+    import torch
+    import paper_2306_05893_b200 as P
+    from paper_2306_05893_b200 import krylov, shard as S
+    from paper_2306_05893_b200.integrator import BackwardEulerIntegrator, IntegratorConfig, SimState
+
+    W = build_workload(args.workload)
+    mesh, f = W["mesh"], W["factors"]
+    sp = S.shard_blocks(f, world)
+    perm = np.asarray(f.plan.perm)
+    sub, nr = S.rank_mesh(mesh, sp, perm, rank)
+    integ = BackwardEulerIntegrator(sub, P.make_model(WORKLOADS[args.workload]["law"], sub,
+                                                      P.MaterialParams(1e5, 0.3, 1000.0)),
+                                    IntegratorConfig(dt=0.01, gravity=(0.0, -9.81, 0.0)))
+    full = W["state"]
+    n = mesh.ndof
+    fe = torch.from_numpy(S.rank_f_ext(full.f_ext.cpu().numpy(), nr, rank)).cuda()
+    st = SimState(full.positions.clone(), full.velocities.clone(), torch.zeros_like(full.positions),
+                  torch.zeros(n, dtype=torch.float64, device="cuda"), fe)
+    a, b, _ = integ.assemble_system(st)
+    fixed = mesh.fixed_dofs()
+    t0 = time.perf_counter()
+    ls = S.LocalSystem(np.asarray(a.row_ptr), np.asarray(a.col_ind), sp, perm, rank, fixed)
+    t_plan = time.perf_counter() - t0
+    grid = 32 if args.share_gpu else 0
+    dp = S.DistributedPcg(None, f, rank=rank, world=world, grid=grid, exchange=args.exchange,
+                          local=ls.system(a.device_values(), b))
+
+    def step():
+        a_, b_, _ = integ.assemble_system(st)
+        dp.set_values(ls.values(a_.device_values()), ls.rhs(b_))
+        return dp.solve(None, TOL, MAX_IT)
+
+    flush = L2Flush()
+    x, it, res, conv = step()
+    # parity: the sharded solve vs the single-GPU device PCG of the same system and factors
+    parity = None
+    if rank == 0:
+        af, bf_, _ = W["integ"].assemble_system(full)
+        xr, rep = krylov.pcg(af, bf_, f, W["cfg"])
+        xr = xr.cpu().numpy()
+        err = float(np.abs(x.cpu().numpy() - xr).max() / max(np.abs(xr).max(), 1e-300))
+        parity = {"iterations_sharded": it, "iterations_single_gpu": int(rep.iterations), "x_rel_err": err,
+                  "tolerance": 1e-10, "ok": it == int(rep.iterations) and err <= 1e-10 and conv}
+        if not parity["ok"]:
+            raise SystemExit(f"sharded parity check failed: {parity}")
+    for _ in range(args.warmup):
+        flush()
+        step()
+    dist.barrier() if dist else None
+    torch.cuda.synchronize()
+    gc.disable()
+    per = []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            step()
+            e1.record()
+            e1.synchronize()
+            per.append(e0.elapsed_time(e1))
+    gc.enable()
+    t_local = torch.tensor([sum(per)], dtype=torch.float64, device="cuda")
+    if dist:
+        dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
+        dist.barrier()
+    ms = float(t_local.item()) / args.steps
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return 0
+    cfgd = workload_config(args.workload, "ldlt", world)
+    cfgd["parallelism"] = (f"nested-dissection shards x{world} ({args.exchange} exchange)"
+                           + (", all ranks on one GPU" if args.share_gpu else ""))
+    cfgd["step"] = "sharded assembly + device local-system gather + sharded LDL^T-PCG (graph-replayed, device stop flag)"
+    line = {
+        "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": cfgd, "iterations": it, "parity": parity,
+        "shards": {"top_rows": int(len(sp.top_rows)), "load": [float(v) for v in sp.load],
+                   "local_plan_s": t_plan},
+        "gpu_launches": None, "clocks": clk.summary(),
+    }
+    print(json.dumps(line))
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
 def reference_workload(name, gravity=(0.0, -9.81, 0.0), at_step=AT_STEP, with_factors=True):
     """The whole workload built by the oracle alone (no product import):
     beam, rest data, cached assembly mapping, dissection, the scenario run
@@ -807,6 +914,12 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--eager", action="store_true", help="time compute_step eagerly instead of the captured graph")
+    ap.add_argument("--shard", action="store_true",
+                    help="nested-dissection sharded solve (the default for N > 1; N = 1 runs it on one rank)")
+    ap.add_argument("--replicas", action="store_true", help="N > 1: independent replicas instead of shards")
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "peer"])
+    ap.add_argument("--share-gpu", action="store_true",
+                    help="all ranks on cuda:0 (gloo group + peer exchange): exercises the N > 1 path on one GPU")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -817,16 +930,25 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.share_gpu:
+        local = 0
+        args.exchange = "peer"
+        os.environ["TSB_SHARED_DEVICE"] = "1"
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.share_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2306_05893_b200 import _lib
 
     if args.workload == "cfg5":
         return run_batched(args, world, rank, local, dist)
+    if args.shard or (world > 1 and not args.replicas):
+        return run_sharded(args, world, rank, local, dist)
     W = build_workload(args.workload)
     flush = L2Flush()
     pk, pk_kind = peaks()

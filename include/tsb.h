@@ -422,17 +422,27 @@ int tsb_refactor_run(tsb_refactor_t h, const double *d_values, double *d_g, doub
  * ---------------------------------------------------------------------- */
 int tsb_wdot(int64_t n, const double *d_w, const double *d_a, const double *d_b, double *d_part,
              double *d_out, void *stream);
-/* alpha = d_sc[0] / d_sc[1]; x += alpha p; r -= alpha ap; d_out[0] = sum w r^2 */
+/* alpha = d_sc[0] / d_sc[1]; x += alpha p; r -= alpha ap; d_out[0] = sum w r^2.
+ * d_done (may be NULL): device stop flag -- when set, nothing is updated. */
 int tsb_pcg_update(int64_t n, const double *d_w, double *d_x, const double *d_p, double *d_r,
-                   const double *d_ap, const double *d_sc, double *d_part, double *d_out, void *stream);
-/* beta = d_sc[0] / d_sc[1]; p = z + beta p; d_sc[1] = d_sc[0] */
-int tsb_pcg_direction(int64_t n, double *d_p, const double *d_z, double *d_sc, void *stream);
+                   const double *d_ap, const double *d_sc, double *d_part, double *d_out,
+                   const int32_t *d_done, void *stream);
+/* beta = d_sc[0] / d_sc[1]; p = z + beta p; d_sc[1] = d_sc[0] (skipped when *d_done) */
+int tsb_pcg_direction(int64_t n, double *d_p, const double *d_z, double *d_sc, const int32_t *d_done,
+                      void *stream);
+/* Device-side stop test of the sharded loop (krylov.py:150-153): unless
+ * *d_done, count the iteration (*d_it += 1), res = sqrt(*d_rr) / bnorm into
+ * *d_res, and set *d_done when res <= tol or *d_it == max_it.  With it the
+ * iterations can be replayed from a CUDA graph with no host read. */
+int tsb_pcg_check(const double *d_rr, double bnorm, double tol, int64_t max_it, int32_t *d_done,
+                  int64_t *d_it, double *d_res, void *stream);
 int tsb_gather_rows(int64_t m, const int32_t *d_idx, const double *d_src, double *d_dst, void *stream);
 /* All-reduce over peer memory (shard.PeerAllreduce, replaces the NCCL
  * all-reduce of the exchanges): x (rows d_idx[0..m), or the first m entries
  * when d_idx is NULL) := sum over ranks in rank order.  d_bufs[r], d_flags[r]:
  * rank r's exchange buffer (2 x half doubles) and epoch word as mapped in this
- * process (CUDA IPC); epoch strictly increasing per call. */
+ * process (CUDA IPC).  `epoch` is ignored: each exchange takes one more than
+ * the rank's own epoch word (device-side numbering, CUDA-graph replayable). */
 int tsb_peer_allreduce(int64_t m, int32_t world, int32_t rank, double *const *d_bufs, int64_t *const *d_flags,
                        const int32_t *d_idx, double *d_x, int64_t epoch, int64_t half, void *stream);
 /* tsb_ldlt_external_sums + peer all-reduce of d_out's rows d_idx[0..m) in one

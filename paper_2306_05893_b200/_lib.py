@@ -121,8 +121,9 @@ _SIGNATURES = {
     "tsb_ldlt_upper_scaled": (C.c_int, [c_vp, c_vp, c_vp, c_vp]),
     "tsb_ldlt_external_sums": (C.c_int, [c_vp, c_vp, c_vp]),
     "tsb_wdot": (C.c_int, [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
-    "tsb_pcg_update": (C.c_int, [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
-    "tsb_pcg_direction": (C.c_int, [c_i64, c_vp, c_vp, c_vp, c_vp]),
+    "tsb_pcg_update": (C.c_int, [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "tsb_pcg_direction": (C.c_int, [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "tsb_pcg_check": (C.c_int, [c_vp, C.c_double, C.c_double, c_i64, c_vp, c_vp, c_vp, c_vp]),
     "tsb_peer_allreduce": (C.c_int, [c_i64, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp]),
     "tsb_spmv_peer": (C.c_int, [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i32, c_i32, c_vp, c_vp, c_vp,
                                 c_i64, c_i64, c_vp, c_vp]),

@@ -37,6 +37,8 @@
 // element tangent is never formed.  The block pass evaluates
 // K_ab = V(lam h_a h_b^T + mu h_b h_a^T + mu (g_a.g_b) F F^T + (g_a^T S g_b) I)
 // in the reference's term order.
+#include <cstdlib>
+
 #include "tsb_common.cuh"
 
 namespace tsb {
@@ -326,7 +328,7 @@ __global__ void gab_kernel(int64_t m, const double *__restrict__ grads, double *
             gab[e * 10 + gab_slot(a, b)] = g[3 * a] * g[3 * b] + g[3 * a + 1] * g[3 * b + 1] + g[3 * a + 2] * g[3 * b + 2];
 }
 
-template <bool STVK>
+template <bool STVK, int U>
 __device__ __forceinline__ void block_body(int64_t bi, int64_t nb, int64_t m, const int4 *__restrict__ blk,
                                            const int32_t *__restrict__ list, const double *__restrict__ work,
                                            const double *__restrict__ grads, const double *__restrict__ gab,
@@ -351,7 +353,7 @@ __device__ __forceinline__ void block_body(int64_t bi, int64_t nb, int64_t m, co
     }
     // contributions in ascending element order; the loads of U contributions
     // are issued before their (ordered) accumulation
-    constexpr int U = 4;
+    // U contributions' loads in flight per thread (template)
     for (int k0 = info.z; k0 < info.w; k0 += U) {
         double ga[U][3], gb[U][3], G[U], V[U];
         double ra[U][3], rb[U][3], aux[STVK ? U : 1][12];
@@ -456,8 +458,8 @@ __device__ __forceinline__ void node_body(int64_t I, int64_t N, const int32_t *_
 // (thread per node), block CTAs sum the 3x3 blocks (thread per block); the two
 // are independent, so the small node gather overlaps the block gather instead
 // of running after it.
-template <bool STVK>
-__global__ void __launch_bounds__(256)
+template <bool STVK, int U, int MINB>
+__global__ void __launch_bounds__(256, MINB)
 gather_kernel(int64_t nbc, int64_t nb, int64_t m, const int4 *__restrict__ blk, const int32_t *__restrict__ list,
               const double *__restrict__ work, const double *__restrict__ grads, const double *__restrict__ gab,
               const double *__restrict__ vol,
@@ -487,8 +489,8 @@ gather_kernel(int64_t nbc, int64_t nb, int64_t m, const int4 *__restrict__ blk, 
         node_body(node_cta * (int64_t)blockDim.x + threadIdx.x, N, node_ptr, node_list, work, x, v, fext_state,
                   gravity, mass_diag, fixed, hb, alpha, f_int, kv, b, f_ext, flags);
     else
-        block_body<STVK>(blk_cta * (int64_t)blockDim.x + threadIdx.x, nb, m, blk, list, work, grads, gab, vol, share,
-                         lam, mu, cm, ck, values);
+        block_body<STVK, U>(blk_cta * (int64_t)blockDim.x + threadIdx.x, nb, m, blk, list, work, grads, gab, vol,
+                            share, lam, mu, cm, ck, values);
 }
 
 __global__ void __launch_bounds__(128)
@@ -575,7 +577,15 @@ extern "C" int tsb_assemble_corot(const tsb_asm_plan *p, const tsb_asm_coeffs *c
         const int64_t nbc = mat && p->n_blocks > 0 ? grid_for(p->n_blocks, 256) : 0;
         const int64_t nnc = p->n_nodes > 0 ? grid_for(p->n_nodes, 256) : 0;
         if (nbc + nnc > 0) {
-            auto kern = c->law == TSB_LAW_STVK ? gather_kernel<true> : gather_kernel<false>;
+            // occupancy vs loads in flight per thread (TSB_GATHER_VARIANT, measured in tools/asm_bench.py)
+            static const int variant = getenv("TSB_GATHER_VARIANT") ? atoi(getenv("TSB_GATHER_VARIANT")) : 0;
+            auto kern = c->law == TSB_LAW_STVK ? gather_kernel<true, 4, 1> : gather_kernel<false, 4, 1>;
+            if (c->law != TSB_LAW_STVK) {
+                if (variant == 1) kern = gather_kernel<false, 2, 6>;
+                else if (variant == 2) kern = gather_kernel<false, 4, 4>;
+                else if (variant == 3) kern = gather_kernel<false, 2, 4>;
+                else if (variant == 4) kern = gather_kernel<false, 1, 8>;
+            }
             kern<<<(unsigned)(nbc + nnc), 256, 0, s>>>(
                 nbc, p->n_blocks, p->n_elems, reinterpret_cast<const int4 *>(p->d_blk), p->d_blk_list, p->d_work,
                 p->d_grads, p->d_gab, p->d_vol, p->d_mass_share, c->lam, c->mu, c->cm, c->ck, d_values, p->n_nodes,

@@ -20,8 +20,9 @@ constexpr int kVecGrid = kNumSM * 2;
 template <int OP>
 __global__ void __launch_bounds__(kVecBlock)
 vec_kernel(int64_t n, const double *__restrict__ w, double *a, double *b, double *c, double *d,
-           const double *__restrict__ sc, double *__restrict__ part) {
+           const double *__restrict__ sc, double *__restrict__ part, const int32_t *done) {
     __shared__ double red[32];
+    if (done != nullptr && *((volatile const int32_t *)done)) return;  // uniform per launch
     double acc = 0.0;
     double coef = 0.0;
     if (OP == 1 || OP == 2) coef = sc[0] / sc[1];
@@ -43,15 +44,29 @@ vec_kernel(int64_t n, const double *__restrict__ w, double *a, double *b, double
     }
 }
 
-__global__ void finish_kernel(int nparts, const double *__restrict__ part, double *__restrict__ out) {
+__global__ void finish_kernel(int nparts, const double *__restrict__ part, double *__restrict__ out,
+                              const int32_t *done) {
     __shared__ double red[32];
+    if (done != nullptr && *((volatile const int32_t *)done)) return;
     double acc = 0.0;
     for (int i = threadIdx.x; i < nparts; i += kVecBlock) acc += part[i];
     const double s = block_sum<kVecBlock>(acc, red);
     if (threadIdx.x == 0) out[0] = s;
 }
 
-__global__ void roll_kernel(double *sc) { sc[1] = sc[0]; }
+__global__ void roll_kernel(double *sc, const int32_t *done) {
+    if (done == nullptr || !*done) sc[1] = sc[0];
+}
+
+__global__ void check_kernel(const double *rr, double bnorm, double tol, int64_t max_it, int32_t *done,
+                             int64_t *it, double *res) {
+    if (*done) return;
+    const int64_t k = *it + 1;
+    *it = k;
+    const double r = sqrt(*rr) / bnorm;
+    *res = r;
+    if (r <= tol || k >= max_it) *done = 1;
+}
 
 __global__ void gather_kernel(int64_t m, const int32_t *__restrict__ idx, const double *__restrict__ src,
                               double *__restrict__ dst) {
@@ -81,8 +96,8 @@ extern "C" int tsb_wdot(int64_t n, const double *d_w, const double *d_a, const d
         cudaStream_t s = as_stream(stream);
         const int g = grid_for(n);
         vec_kernel<0><<<g, kVecBlock, 0, s>>>(n, d_w, const_cast<double *>(d_a), const_cast<double *>(d_b),
-                                              nullptr, nullptr, nullptr, d_part);
-        finish_kernel<<<1, kVecBlock, 0, s>>>(g, d_part, d_out);
+                                              nullptr, nullptr, nullptr, d_part, nullptr);
+        finish_kernel<<<1, kVecBlock, 0, s>>>(g, d_part, d_out, nullptr);
         count_launch(2);
         TSB_CUDA(cudaGetLastError());
     });
@@ -91,28 +106,39 @@ extern "C" int tsb_wdot(int64_t n, const double *d_w, const double *d_a, const d
 // alpha = d_sc[0] / d_sc[1]; x += alpha p; r -= alpha ap; d_out[0] = sum w r^2
 extern "C" int tsb_pcg_update(int64_t n, const double *d_w, double *d_x, const double *d_p, double *d_r,
                               const double *d_ap, const double *d_sc, double *d_part, double *d_out,
-                              void *stream) {
+                              const int32_t *d_done, void *stream) {
     using namespace tsb;
     return guard([&] {
         cudaStream_t s = as_stream(stream);
         const int g = grid_for(n);
         vec_kernel<1><<<g, kVecBlock, 0, s>>>(n, d_w, d_x, const_cast<double *>(d_p), d_r,
-                                              const_cast<double *>(d_ap), d_sc, d_part);
-        finish_kernel<<<1, kVecBlock, 0, s>>>(g, d_part, d_out);
+                                              const_cast<double *>(d_ap), d_sc, d_part, d_done);
+        finish_kernel<<<1, kVecBlock, 0, s>>>(g, d_part, d_out, d_done);
         count_launch(2);
         TSB_CUDA(cudaGetLastError());
     });
 }
 
 // beta = d_sc[0] / d_sc[1]; p = z + beta p; then d_sc[1] = d_sc[0]
-extern "C" int tsb_pcg_direction(int64_t n, double *d_p, const double *d_z, double *d_sc, void *stream) {
+extern "C" int tsb_pcg_direction(int64_t n, double *d_p, const double *d_z, double *d_sc, const int32_t *d_done,
+                                 void *stream) {
     using namespace tsb;
     return guard([&] {
         cudaStream_t s = as_stream(stream);
         vec_kernel<2><<<grid_for(n), kVecBlock, 0, s>>>(n, nullptr, d_p, const_cast<double *>(d_z), nullptr,
-                                                        nullptr, d_sc, nullptr);
-        roll_kernel<<<1, 1, 0, s>>>(d_sc);
+                                                        nullptr, d_sc, nullptr, d_done);
+        roll_kernel<<<1, 1, 0, s>>>(d_sc, d_done);
         count_launch(2);
+        TSB_CUDA(cudaGetLastError());
+    });
+}
+
+extern "C" int tsb_pcg_check(const double *d_rr, double bnorm, double tol, int64_t max_it, int32_t *d_done,
+                             int64_t *d_it, double *d_res, void *stream) {
+    using namespace tsb;
+    return guard([&] {
+        check_kernel<<<1, 1, 0, as_stream(stream)>>>(d_rr, bnorm, tol, max_it, d_done, d_it, d_res);
+        count_launch();
         TSB_CUDA(cudaGetLastError());
     });
 }

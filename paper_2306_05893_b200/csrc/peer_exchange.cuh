@@ -13,7 +13,8 @@ struct PeerArgs {
     double *const *bufs;       // [world] exchange buffers (2 x half doubles), as mapped here
     int64_t *const *flags;     // [world] epoch words, as mapped here
     const int32_t *idx;        // rows of x (NULL: the first m)
-    int64_t epoch, half;
+    int64_t epoch;             // unused: derived on the device (exchange_block)
+    int64_t half;
 };
 
 __device__ __forceinline__ void st_release_sys(int64_t *p, int64_t v) {
@@ -29,19 +30,24 @@ __device__ __forceinline__ int64_t ld_acquire_sys(const int64_t *p) {
 // the epoch (release, system scope), wait for every peer's, then x's rows :=
 // the sum over ranks in rank order.  x may have been written by other CTAs of
 // the same kernel (read through L2).
+// The epoch is derived on the device -- one more than this rank's own epoch
+// word, which only this rank's exchanges write, in stream order -- so every
+// rank numbers the same sequence of exchanges identically and the kernels
+// replay inside CUDA graphs (P.epoch is not used).
 __device__ __forceinline__ void exchange_block(const PeerArgs &P, double *x) {
     const int tid = threadIdx.x, nt = blockDim.x;
-    const int64_t off = (P.epoch & 1) * P.half;
+    const int64_t epoch = *((volatile const int64_t *)P.flags[P.rank]) + 1;
+    const int64_t off = (epoch & 1) * P.half;
     double *mine = P.bufs[P.rank] + off;
     for (int64_t i = tid; i < P.m; i += nt) mine[i] = __ldcg(x + (P.idx ? P.idx[i] : i));
     __syncthreads();
     if (tid == 0) {
         __threadfence_system();
-        st_release_sys(P.flags[P.rank], P.epoch);
+        st_release_sys(P.flags[P.rank], epoch);
     }
     if (tid < P.world && tid != P.rank) {
         const int64_t *f = P.flags[tid];
-        while (ld_acquire_sys(f) < P.epoch) __nanosleep(64);
+        while (ld_acquire_sys(f) < epoch) __nanosleep(64);
     }
     __syncthreads();
     for (int64_t i = tid; i < P.m; i += nt) {

@@ -231,6 +231,41 @@ def local_system(row_ptr, col_ind, values, b, plan: ShardPlan, perm, rank: int, 
     return lrp, ci[keep], va[keep], lb
 
 
+class LocalSystem:
+    """Per-step extraction of a rank's local system ON THE DEVICE.
+
+    local_system() is planned once per (pattern, shard plan, rank) on index
+    arrays -- the entry values are their own positions -- which yields the
+    source slot of every local entry; each step is then one gather of the
+    rank's assembled values (still in HBM) and one masked gather of its rhs,
+    instead of a host NumPy lexsort of every new matrix."""
+
+    def __init__(self, row_ptr, col_ind, plan: ShardPlan, perm, rank: int, fixed_dofs):
+        from . import _lib
+
+        t = _lib.require_cuda()
+        nnz, n = len(col_ind), len(perm)
+        idx = np.arange(nnz, dtype=np.float64)  # exact below 2^53
+        lrp, lci, src, _ = local_system(row_ptr, col_ind, idx, np.zeros(n), plan, perm, rank, fixed_dofs)
+        self.row_ptr, self.col_ind = lrp, lci
+        self.src = t.from_numpy(src.astype(np.int64)).cuda()
+        ro = plan.row_owner
+        self.mask = t.from_numpy(((ro == rank) | (ro < 0)).astype(np.float64)).cuda()
+        self.perm = t.from_numpy(np.asarray(perm, dtype=np.int64)).cuda()
+
+    def values(self, values):
+        """Local entry values from the rank's assembled values (device tensor)."""
+        return values.index_select(0, self.src)
+
+    def rhs(self, b):
+        """Permuted local rhs: owned and top rows of the rank's partial b."""
+        return b.index_select(0, self.perm) * self.mask
+
+    def system(self, values, b):
+        """(row_ptr, col_ind, values, b) -- the DistributedPcg `local=` tuple."""
+        return self.row_ptr, self.col_ind, self.values(values), self.rhs(b)
+
+
 # ---------------------------------------------------------------------------
 # CPU emulation of the distributed loop (world_size > 1 tests over gloo)
 # ---------------------------------------------------------------------------
@@ -491,7 +526,8 @@ class DistributedPcg:
             rp, ci, va = permuted_matrix(a, perm)
             lrp, lci, lva = local_matrix(rp, ci, va, self.plan, rank)
         dev = lambda x, dt: t.from_numpy(np.ascontiguousarray(x, dtype=dt)).cuda()  # noqa: E731
-        self.rp, self.ci, self.va = dev(lrp, np.int32), dev(lci, np.int32), dev(lva, np.float64)
+        self.rp, self.ci = dev(lrp, np.int32), dev(lci, np.int32)
+        self.va = lva.to(dtype=t.float64).clone() if _lib.is_tensor(lva) else dev(lva, np.float64)
         self.w = dev(self.plan.weights(rank), np.float64)
         self.top = dev(self.plan.top_rows, np.int32)
         self.perm = dev(perm, np.int32)
@@ -507,6 +543,10 @@ class DistributedPcg:
         self.topbuf = z(len(self.plan.top_rows))
         self.part = z(2 * 148)
         self.sc = z(8)  # [rz, pAp] / [rz_new, rz_old] / scratch
+        self.done = t.zeros(1, dtype=t.int32, device="cuda")   # device stop flag
+        self.it = t.zeros(1, dtype=t.int64, device="cuda")     # iteration count
+        self.res = z(1)                                          # final relative residual
+        self.done_host = t.zeros(1, dtype=t.int32).pin_memory()
         self._lib = _lib.load()
         self._L = _lib
         # exchange="peer": the top-row exchanges and the scalars go through
@@ -516,6 +556,14 @@ class DistributedPcg:
         if exchange == "peer" and world > 1:
             self.peer = PeerAllreduce(world, rank, max(len(self.plan.top_rows), n))
             self.allreduce = lambda x: self.peer(x)
+
+    def set_values(self, values, b=None):
+        """New values (same local pattern) and, for a sharded assembly, the
+        rank's new local rhs -- e.g. LocalSystem.values / .rhs of the next step;
+        the factor panels (the preconditioner) are kept."""
+        self.va.copy_(values)
+        if b is not None:
+            self._lb = b
 
     # -- pieces ------------------------------------------------------------
     def _exchange_top(self, vec):
@@ -564,16 +612,56 @@ class DistributedPcg:
             self.S.run("upper_scaled", v["y"], out)
 
     # -- solve -----------------------------------------------------------------
-    def solve(self, b=None, tol=1e-9, max_it=1000):
+    def _iteration(self, bnorm, tol, max_it):
+        """One PCG iteration, entirely on the device: alpha, beta, the stop test
+        and the iteration count never leave it (tsb_pcg_check sets the stop
+        flag; the updates are no-ops once it is set)."""
+        L, v, n = self._L, self.v, self.n
+        s = L.stream_ptr()
+        self._spmv(v["p"], v["ap"])
+        self._dot(v["p"], v["ap"], 1)  # sc[1] = pAp; alpha = sc[0] / sc[1]
+        L.check(self._lib.tsb_pcg_update(n, L.ptr(self.w), L.ptr(v["x"]), L.ptr(v["p"]), L.ptr(v["r"]),
+                                         L.ptr(v["ap"]), L.ptr(self.sc), L.ptr(self.part), L.ptr(self.sc[5:6]),
+                                         L.ptr(self.done), s), "pcg_update")
+        self.allreduce(self.sc[5:6])
+        L.check(self._lib.tsb_pcg_check(L.ptr(self.sc[5:6]), bnorm, tol, max_it, L.ptr(self.done),
+                                        L.ptr(self.it), L.ptr(self.res), s), "pcg_check")
+        self._precond(v["r"], v["z"])
+        self.sc[1:2].copy_(self.sc[0:1])  # rz_old
+        self._dot(v["r"], v["z"], 0)       # rz_new; beta = sc[0] / sc[1]
+        L.check(self._lib.tsb_pcg_direction(n, L.ptr(v["p"]), L.ptr(v["z"]), L.ptr(self.sc), L.ptr(self.done), s),
+                "pcg_direction")
+
+    def _graph_ok(self):
+        """CUDA-graph replay needs capturable exchanges: our peer kernels, NCCL,
+        or none (one rank); a gloo process group runs the iterations eagerly."""
+        if self.world == 1 or self.peer is not None:
+            return True
+        import torch.distributed as dist
+
+        return dist.is_initialized() and dist.get_backend() == "nccl"
+
+    GRAPH_ITERS = 4  # iterations per graph replay: one host read of the stop flag per replay
+
+    def solve(self, b=None, tol=1e-9, max_it=1000, graph=None):
         """-> (x in original order as a CUDA tensor, iterations, residual, converged).
-        b=None with a sharded assembly: the rank's partial rhs, top rows all-reduced."""
+        b=None with a sharded assembly: the rank's partial rhs, top rows all-reduced.
+
+        The iterations run device-resident: alpha, beta, the residual test and
+        the count stay on the device, and (graph=True, the default where the
+        exchanges allow it) GRAPH_ITERS iterations are replayed as one CUDA
+        graph, the stop flag read once per replay -- no host round trip per
+        iteration."""
         L, t = self._L, self._L.torch()
         v, n = self.v, self.n
         s = L.stream_ptr()
         if b is None:
             if self._lb is None:
                 raise ValueError("solve() needs b unless built from a sharded assembly (local=)")
-            v["b"].copy_(t.from_numpy(np.ascontiguousarray(self._lb, dtype=np.float64)))
+            if L.is_tensor(self._lb):
+                v["b"].copy_(self._lb)
+            else:
+                v["b"].copy_(t.from_numpy(np.ascontiguousarray(self._lb, dtype=np.float64)))
             self._exchange_top(v["b"])
         else:
             bd = b if L.is_tensor(b) else t.from_numpy(np.ascontiguousarray(b, dtype=np.float64)).cuda()
@@ -581,40 +669,64 @@ class DistributedPcg:
         v["r"].copy_(v["b"])
         v["x"].zero_()
         self._dot(v["b"], v["b"], 4)
-        bnorm = float(self.sc[4].item()) ** 0.5
+        bnorm = float(self.sc[4].item()) ** 0.5  # one read per solve (the reference's ||b||)
         x_out = t.zeros(n, dtype=t.float64, device="cuda")
         if bnorm == 0.0:
             return x_out, 0, 0.0, True
-        self._dot(v["r"], v["r"], 5)
-        res = float(self.sc[5].item()) ** 0.5 / bnorm
-        it, conv = 0, res <= tol
-        if not conv:
+        # x0 = 0: r = b, the initial relative residual is 1 > tol
+        self.done.zero_()
+        self.it.zero_()
+        self.res.fill_(1.0)
+        if max_it > 0 and tol < 1.0:
             self._precond(v["r"], v["z"])
             v["p"].copy_(v["z"])
             self._dot(v["r"], v["z"], 0)  # sc[0] = rz
-            while it < max_it:
-                self._spmv(v["p"], v["ap"])
-                self._dot(v["p"], v["ap"], 1)  # sc[1] = pAp; alpha = sc[0] / sc[1]
-                L.check(self._lib.tsb_pcg_update(n, L.ptr(self.w), L.ptr(v["x"]), L.ptr(v["p"]), L.ptr(v["r"]),
-                                                 L.ptr(v["ap"]), L.ptr(self.sc), L.ptr(self.part),
-                                                 L.ptr(self.sc[5:6]), s), "pcg_update")
-                self.allreduce(self.sc[5:6])
-                it += 1
-                res = float(self.sc[5].item()) ** 0.5 / bnorm  # the one host read per iteration
-                if res <= tol:
-                    conv = True
-                    break
-                self._precond(v["r"], v["z"])
-                self.sc[1:2].copy_(self.sc[0:1])  # rz_old
-                self._dot(v["r"], v["z"], 0)       # rz_new; beta = sc[0] / sc[1]
-                L.check(self._lib.tsb_pcg_direction(n, L.ptr(v["p"]), L.ptr(v["z"]), L.ptr(self.sc), s),
-                        "pcg_direction")
+            use_graph = self._graph_ok() if graph is None else graph
+            if use_graph:
+                key = (bnorm, tol, max_it)
+                if getattr(self, "_graph_key", None) != key:
+                    self._capture(bnorm, tol, max_it)
+                    self._graph_key = key
+                while True:
+                    self._graph.replay()
+                    self.done_host.copy_(self.done, non_blocking=True)
+                    t.cuda.current_stream().synchronize()
+                    if int(self.done_host[0]):
+                        break
+            else:
+                while True:
+                    self._iteration(bnorm, tol, max_it)
+                    if int(self.done.item()):
+                        break
+        it = int(self.it.item())
+        res = float(self.res.item())
+        conv = res <= tol
         # x: owned rows from every rank, top rows from rank 0
         xw = v["y"]
         self._weighted_copy(v["x"], xw)
         self.allreduce(xw)
         L.check(self._lib.tsb_gather_rows(n, L.ptr(self.iperm), L.ptr(xw), L.ptr(x_out), s), "gather")
         return x_out, it, res, conv
+
+    def _capture(self, bnorm, tol, max_it):
+        t = self._L.torch()
+        side = t.cuda.Stream()
+        side.wait_stream(t.cuda.current_stream())
+        saved = (self.done.clone(), self.it.clone(), self.res.clone(), self.sc.clone(),
+                 *(self.v[k].clone() for k in ("x", "r", "z", "p")))
+        with t.cuda.stream(side):  # one eager pass on the capture stream warms every handle
+            self._iteration(bnorm, tol, max_it)
+        t.cuda.current_stream().wait_stream(side)
+        t.cuda.synchronize()
+        self._graph = t.cuda.CUDAGraph()
+        with t.cuda.graph(self._graph):
+            for _ in range(self.GRAPH_ITERS):
+                self._iteration(bnorm, tol, max_it)
+        t.cuda.synchronize()
+        # capture does not execute: restore the state the warm-up pass advanced
+        for dst, src in zip((self.done, self.it, self.res, self.sc,
+                             *(self.v[k] for k in ("x", "r", "z", "p"))), saved):
+            dst.copy_(src)
 
     def _weighted_copy(self, x, out):
         """out = x on the rows this rank contributes (owned, top on rank 0), else 0."""

@@ -23,12 +23,18 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def test_single_rank_equals_device_pcg():
+@pytest.mark.parametrize("graph", [True, False])
+def test_single_rank_equals_device_pcg(graph):
+    """One rank, device-resident loop replayed as CUDA graphs (device stop
+    flag, no host read per iteration) or eagerly: same as the single-GPU PCG."""
     from oracle import tetsim_oracle as O
     from paper_2306_05893_b200 import krylov, shard as S
 
     a, b, f = _system()
-    x, it, res, conv = S.DistributedPcg(a, f, rank=0, world=1).solve(b, 1e-9, 200)
+    dp = S.DistributedPcg(a, f, rank=0, world=1)
+    x, it, res, conv = dp.solve(b, 1e-9, 200, graph=graph)
+    x2, it2, res2, _ = dp.solve(b, 1e-9, 200, graph=graph)  # replays the captured graph
+    assert it2 == it and np.array_equal(x.cpu().numpy(), x2.cpu().numpy())
     ox, oit, ores, oconv = O.pcg(a.row_ptr, a.col_ind, a.values, b, lambda r: O.apply(f, r), 1e-9, 200)
     assert conv and it == oit
     assert np.abs(x.cpu().numpy() - ox).max() <= 1e-10 * np.abs(ox).max()
@@ -105,7 +111,12 @@ def _worker_sharded(rank, world, port, q, exchange):
         a, b, _ = integ.assemble_system(st)
         host = lambda z: z.cpu().numpy() if hasattr(z, "cpu") else np.asarray(z)  # noqa: E731
         fixed = (3 * np.asarray(mesh.fixed_nodes)[:, None] + np.arange(3)).ravel()
-        local = S.local_system(host(a.row_ptr), host(a.col_ind), host(a.values), host(b), sp, perm, rank, fixed)
+        if exchange == "peer":  # device-side extraction (planned once, two gathers per step)
+            ls = S.LocalSystem(host(a.row_ptr), host(a.col_ind), sp, perm, rank, fixed)
+            bd = b if hasattr(b, "cuda") else torch.from_numpy(np.asarray(b)).cuda()
+            local = ls.system(a.device_values(), bd)
+        else:
+            local = S.local_system(host(a.row_ptr), host(a.col_ind), host(a.values), host(b), sp, perm, rank, fixed)
         xs, it, res, conv = S.DistributedPcg(None, f, rank=rank, world=world, grid=32, exchange=exchange,
                                              local=local).solve(None, 1e-9, 200)
         q.put((rank, xs.cpu().numpy(), it, res, conv))
@@ -120,8 +131,10 @@ def _worker_sharded(rank, world, port, q, exchange):
 @pytest.mark.parametrize("exchange", ["nccl", "peer"])
 def test_two_ranks_sharded_device_assembly(exchange):
     """Each rank assembles only its subtree's elements on the device
-    (shard.rank_mesh / local_system); the distributed PCG over the partial
-    systems matches the oracle PCG on the full assembly."""
+    (shard.rank_mesh / local_system; with the peer exchange the local system
+    is extracted on the device by LocalSystem and the iterations replay as
+    CUDA graphs with the device stop flag); the distributed PCG over the
+    partial systems matches the oracle PCG on the full assembly."""
     import torch.multiprocessing as mp
     from oracle import tetsim_oracle as O
     from test_shard_assembly import _case, _full

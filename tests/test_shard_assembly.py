@@ -167,3 +167,21 @@ def test_rank_meshes_partition_the_elements(world):
     nr = parts[0][1]
     tot = sum(S.rank_f_ext(fe, nr, g) for g in range(world))
     assert np.array_equal(tot, fe)
+
+
+def test_local_system_index_map_equals_value_extraction():
+    """shard.LocalSystem plans local_system once on index arrays and gathers
+    values per step: the gathered values equal local_system on the values."""
+    mesh, f, x, v, fe = _case()
+    full = _full(mesh, x, v, fe)
+    sp = S.shard_blocks(f, 2)
+    perm = f.plan.perm
+    fixed = (3 * np.asarray(mesh.fixed_nodes)[:, None] + np.arange(3)).ravel()
+    rp, ci, va, b = full["row_ptr"], full["col_ind"], full["values"], full["b"]
+    for rank in range(2):
+        lrp, lci, lva, lb = S.local_system(rp, ci, va, b, sp, perm, rank, fixed)
+        irp, ici, src, _ = S.local_system(rp, ci, np.arange(len(ci), dtype=np.float64), b, sp, perm, rank, fixed)
+        assert np.array_equal(lrp, irp) and np.array_equal(lci, ici)
+        assert np.array_equal(va[src.astype(np.int64)], lva)
+        ro = sp.row_owner
+        assert np.array_equal(np.where((ro == rank) | (ro < 0), np.asarray(b)[perm], 0.0), lb)
