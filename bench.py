@@ -76,7 +76,7 @@ def peaks():
 # workload
 # ---------------------------------------------------------------------------
 
-def build_workload(name, device=True):
+def build_workload(name, device=True, with_factors=True):
     import paper_2306_05893_b200 as P
     from paper_2306_05893_b200 import krylov, ndprecond as ND
     from paper_2306_05893_b200.integrator import BackwardEulerIntegrator, IntegratorConfig, SimState
@@ -94,18 +94,19 @@ def build_workload(name, device=True):
 
     jacobi.accepts_device = True
     t0 = time.perf_counter()
-    plan = ND.expand_plan(ND.nested_dissection(P.vertex_adjacency(mesh), LEAF))
+    plan = ND.expand_plan(ND.nested_dissection(P.vertex_adjacency(mesh), LEAF)) if with_factors else None
     t_nd = time.perf_counter() - t0
     st = SimState.rest(mesh, device=True)
     factors = None
     t_factor = 0.0
     for k in range(1, AT_STEP):
         res = integ.step(st, jacobi)
-        if k == STALE_FROM:
+        if with_factors and k == STALE_FROM:
             t0 = time.perf_counter()
             factors = ND.ldlt_factor(res.matrix, plan, tile=TILE, source_step=k)
             t_factor = time.perf_counter() - t0
-    factors.device()
+    if factors is not None:
+        factors.device()
 
     def ldlt(a, b):
         return krylov.pcg(a, b, factors, cfg)
@@ -299,6 +300,9 @@ def time_async_device(W, steps, flush):
     cfg = W["cfg"]
     integ = W["integ"]
     st = W["state"].copy()  # the run advances its own copy of the scenario state
+    t0 = time.perf_counter()
+    pre.prepare(integ.assemble_system(st)[0])  # setup: refactorisation planning off the stepping path
+    t_prep = time.perf_counter() - t0
     stale, iters, per = [], [], []
     k0 = 1000
     for k in range(steps + 5):
@@ -318,7 +322,8 @@ def time_async_device(W, steps, flush):
             stale.append(pre.staleness(k0 + k) if ready else -1)
     pre.close()
     return dict(ms_per_step=statistics.median(per), iterations=statistics.median(iters),
-                staleness_median=statistics.median(stale), steps=len(per))
+                staleness_median=statistics.median(stale), steps=len(per), prepare_s=t_prep,
+                first_ready_step=next((k for k, sv in enumerate(stale) if sv >= 0), -1))
 
 
 def time_e2e(W, mode, steps):
@@ -949,7 +954,8 @@ def main():
         return run_batched(args, world, rank, local, dist)
     if args.shard or (world > 1 and not args.replicas):
         return run_sharded(args, world, rank, local, dist)
-    W = build_workload(args.workload)
+    ldlt_extras = args.precond == "ldlt" or args.workload != "cfg4"  # cfg4 Jacobi: no 25 GB host factor
+    W = build_workload(args.workload, with_factors=ldlt_extras)
     flush = L2Flush()
     pk, pk_kind = peaks()
     if dist:
@@ -959,26 +965,27 @@ def main():
         main_r = time_steps(W, args.precond, args.steps, args.warmup, flush, graph=not args.eager)
     eager_r = time_steps(W, args.precond, max(10, args.steps // 4), 3, flush)
     other = "jacobi" if args.precond == "ldlt" else "ldlt"
-    other_r = time_steps(W, other, max(10, args.steps // 4), 3, flush, graph=not args.eager)
+    other_r = (time_steps(W, other, max(10, args.steps // 4), 3, flush, graph=not args.eager) if ldlt_extras
+               else None)
     torch.cuda.synchronize()
     t_local = torch.tensor([main_r["total_ms"]], dtype=torch.float64, device="cuda")
     if dist:
         dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
         dist.barrier()
     total_ms = float(t_local.item())
-    apply_r = time_apply(W, 20, flush)
+    apply_r = time_apply(W, 20, flush) if ldlt_extras else None
     spmv_r = time_spmv(W, 20, flush)
     asm_r = time_assembly(W, 20, flush)
     e2e_r = time_e2e(W, args.precond, max(5, min(args.steps, 30)))
-    refac_r = time_refactor(W)
-    async_r = time_async_device(W, max(10, min(args.steps, 30)), flush)
+    refac_r = time_refactor(W) if ldlt_extras else None
+    async_r = time_async_device(W, max(10, min(args.steps, 30)), flush) if ldlt_extras else None
     ms = total_ms / args.steps
     if rank != 0:
         if dist:
             dist.destroy_process_group()
         return 0
     cpu = parity = None
-    if world == 1 and not args.no_cpu_baseline:
+    if world == 1 and not args.no_cpu_baseline and args.workload != "cfg4":  # the oracle needs ~10 min at 1M nodes
         cpu = cpu_baseline(W, args.precond)
         parity = check_parity(W, args.precond, cpu)
     hbm = pk.get("hbm_gbs", 6650.0)
@@ -989,29 +996,33 @@ def main():
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": workload_config(args.workload, args.precond, world),
-        "sizes": {"nnz": spmv_r["nnz"], "nnz_L": apply_r["nnzL"]},
+        "sizes": {"nnz": spmv_r["nnz"], "nnz_L": apply_r["nnzL"] if apply_r else None},
         "iterations": main_r["iterations"], "assembly_ms": eager_r["assembly_ms"], "pcg_ms": eager_r["solve_ms"],
         "step_mode": "eager compute_step" if args.eager else "CUDA graph replay of compute_step (CapturedStep)",
         "eager_ms_per_step": eager_r["ms"],
         "step_ms": {"min": min(main_r["per_step"]), "median": statistics.median(main_r["per_step"]),
                     "max": max(main_r["per_step"]),
                     "argmax": int(max(range(len(main_r["per_step"])), key=lambda k: main_r["per_step"][k]))},
-        other: {"ms_per_step": other_r["ms"], "iterations": other_r["iterations"]},
+        other: {"ms_per_step": other_r["ms"], "iterations": other_r["iterations"]} if other_r else None,
         "trisolve": {"apply_ms": apply_r["ms"], "gbs": apply_r["gbs"], "frac": apply_r["gbs"] / hbm,
-                     "algorithmic_bytes": apply_r["bytes"], "stored_bytes": apply_r["stored_bytes"]},
+                     "algorithmic_bytes": apply_r["bytes"], "stored_bytes": apply_r["stored_bytes"]} if apply_r else None,
         "spmv": {"ms": spmv_r["ms"], "gbs": spmv_r["gbs"], "frac": spmv_r["gbs"] / hbm},
         "assembly": {"ms": asm_r["ms"], "gbs": asm_r["gbs"], "frac": asm_r["gbs"] / hbm,
                      "algorithmic_bytes": asm_r["bytes"]},
-        "roofline": {"bound": "hbm", "kernel": "ldlt apply (level-scheduled L and L^T sweeps)",
-                     "achieved": apply_r["gbs"], "peak": hbm, "peak_kind": pk_kind, "unit": "GB/s",
-                     "frac": apply_r["gbs"] / hbm, "traffic": traffic},
+        "roofline": ({"bound": "hbm", "kernel": "ldlt apply (level-scheduled L and L^T sweeps)",
+                      "achieved": apply_r["gbs"], "peak": hbm, "peak_kind": pk_kind, "unit": "GB/s",
+                      "frac": apply_r["gbs"] / hbm, "traffic": traffic} if args.precond == "ldlt" else
+                     {"bound": "hbm", "kernel": "CSR SpMV (bit-exact), the Jacobi-PCG iteration's dominant part",
+                      "achieved": spmv_r["gbs"], "peak": hbm, "peak_kind": pk_kind, "unit": "GB/s",
+                      "frac": spmv_r["gbs"] / hbm, "traffic": None}),
         "e2e": {"value": e2e_r["ms"], "unit": "ms", "h2d_bytes_per_step": e2e_r["h2d"],
                 "d2h_bytes_per_step": e2e_r["d2h"]},
         "gpu_launches": main_r["launches"],
         "clocks": clk.summary(),
         "setup_s": {"nested_dissection": W["t_nd"], "host_factor": W["t_factor"]},
         "refactor": dict(refac_r, host_factor_s=W["t_factor"],
-                         kernel="device LDL^T refactorisation (multifrontal 64x64 tiles, csrc/refactor.cu)"),
+                         kernel="device LDL^T refactorisation (multifrontal 64x64 tiles, csrc/refactor.cu)")
+        if refac_r else None,
         "ldlt_async_device": async_r,
     }
     if cpu is not None:

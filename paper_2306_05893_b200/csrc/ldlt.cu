@@ -73,6 +73,7 @@ static std::mutex g_serial_mu;
 // which is deadlock-free exactly when every CTA of the grid is resident.
 template <class K>
 static void launch_coop(K kernel, int grid, size_t smem, cudaStream_t st, tsb_ldlt_desc &D, SweepArgs &a) {
+    sync_pub_direct();
     // TSB_SHARED_DEVICE=1: several processes share one GPU (the 2-rank shard test
     // on a 1-GPU box), where the driver refuses cooperative launches; the grid
     // (<= one CTA per SM there) is still co-resident, launch it plainly

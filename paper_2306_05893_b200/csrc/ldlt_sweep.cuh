@@ -19,6 +19,8 @@
 // earlier ticket, so the persistent grid stays deadlock-free.
 #pragma once
 
+#include <cstdlib>
+
 #include "tsb_common.cuh"
 
 namespace tsb {
@@ -445,7 +447,24 @@ __device__ __forceinline__ void mail_done(SweepRing &R, uint32_t &k) {  // after
 }
 // Post a publication (consumer thread 0, after a csync()): the producer lane
 // issues red.release.gpu(addr, 1); addr == nullptr ends the sweep's queue.
+// tuning switch (TSB_PUB_DIRECT=1): the consumers issue their releases
+// themselves instead of handing them to the producer lane; one copy per
+// translation unit, set by sync_pub_direct() before its first sweep launch
+static __device__ int g_pub_direct;
+static inline void sync_pub_direct() {
+    static bool done = false;
+    if (done) return;
+    const char *e = getenv("TSB_PUB_DIRECT");
+    const int v = (e != nullptr && atoi(e) != 0) ? 1 : 0;
+    cudaMemcpyToSymbol(g_pub_direct, &v, sizeof(int));
+    done = true;
+}
+
 __device__ __forceinline__ void publish(SweepRing &R, uint32_t &p, int32_t *addr) {
+    if (addr != nullptr && g_pub_direct) {
+        if (threadIdx.x == 0) red_add_release(addr, 1);
+        return;
+    }
     if (threadIdx.x == 0) {
         const int e = p & 1;
         if (p >= 2) mbar_wait(&R.pub_done[e], ((p >> 1) - 1) & 1u);

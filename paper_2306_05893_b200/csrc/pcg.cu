@@ -371,6 +371,7 @@ static int occupancy_grid(size_t smem) {
 
 template <int KIND, int MINB>
 static void launch(tsb_pcg *h, PcgArgs &a, tsb_ldlt_desc &D, int grid, size_t smem, cudaStream_t s) {
+    if (KIND == TSB_PRECOND_LDLT) sync_pub_direct();
     void *args[] = {&h->W, &a, &D};
     TSB_CUDA(cudaLaunchCooperativeKernel((const void *)pcg_persistent<KIND, MINB>, dim3(grid), dim3(kPcgBlock),
                                          args, smem, s));

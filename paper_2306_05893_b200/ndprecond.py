@@ -599,15 +599,27 @@ class AsyncPreconditioner:
         _lib.torch().cuda.current_stream().wait_event(event)
         self.factors = factors
 
-    def _submit_device(self, a: CsrMatrix, step: int):
-        """Refactor `a` on a side stream into the sweep image not in use."""
-        from .refactor import DeviceRefactor, make_factors
+    def prepare(self, a: CsrMatrix):
+        """device=True: plan the device refactorisation of `a`'s pattern now
+        (host setup: symbolic structure, front maps, launch program, the two
+        sweep images -- seconds at 100k nodes) instead of inside the first
+        update(), which then only enqueues device work."""
+        if not self.device:
+            return
+        from .refactor import DeviceRefactor
 
-        t = _lib.torch()
         if self._rf is None or self._rf.symbolic.pattern_key != _pattern_key(a):
+            t = _lib.torch()
             self._rf = DeviceRefactor(a, self.plan, self.tile, buffers=2)
             self._side = t.cuda.Stream()
             self._flag = t.zeros(4, dtype=t.int32).pin_memory()
+
+    def _submit_device(self, a: CsrMatrix, step: int):
+        """Refactor `a` on a side stream into the sweep image not in use."""
+        from .refactor import make_factors
+
+        t = _lib.torch()
+        self.prepare(a)
         rf = self._rf
         img = rf.images[rf._next]
         rf._next = (rf._next + 1) % len(rf.images)
