@@ -256,6 +256,15 @@ pcg_persistent(PcgWork W, PcgArgs a, tsb_ldlt_desc D) {
             double *t = pcur;  // the new direction is in pnxt
             pcur = pnxt;
             pnxt = t;
+        } else if (KIND == TSB_PRECOND_LDLT) {
+            // two CTAs per SM (the sweep staging): a third of the Jacobi kernel's
+            // warps, so each 8-lane group keeps two rows' loads in flight
+            XPlainCG xa{pcur};
+            auto out = [&](int64_t row, double s) {
+                W.ap[row] = s;
+                v += __ldcg(pcur + row) * s;
+            };
+            rows_exact<2>(grp, ngrp, n, a.rp, a.ci, a.val, xa, lane8, gmask, out);
         } else {
             XPlainCG xa{pcur};
             for (int64_t row = grp; row < n; row += ngrp) {

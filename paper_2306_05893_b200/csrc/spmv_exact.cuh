@@ -111,4 +111,93 @@ __device__ __forceinline__ double row_sum_exact(int lo, int len, const int32_t *
     return add(p0, res);
 }
 
+// Two-phase form of row_sum_exact for rows of <= 65 entries (the FEM case):
+// row_terms issues every load of a row (its first product and each lane's <= 8
+// terms) without waiting for them, row_reduce combines them in exactly
+// row_sum_exact's order -- a kernel with registers to spare but few resident
+// warps (the LDL^T PCG: two CTAs per SM) keeps several rows' loads in flight.
+struct RowTerms {
+    double p0, t[8];
+    int n;
+};
+template <class XAcc>
+__device__ __forceinline__ void row_terms(int lo, int len, const int32_t *__restrict__ col,
+                                          const double *__restrict__ val, const XAcc &xa, int lane8, RowTerms &R) {
+    R.n = len - 1;
+    R.p0 = 0.0;
+    if (len > 0 && lane8 == 0) R.p0 = mul(__ldg(val + lo), xa(__ldg(col + lo)));
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+        const int idx = 8 * u + lane8;
+        R.t[u] = idx < R.n ? mul(__ldg(val + lo + 1 + idx), xa(__ldg(col + lo + 1 + idx))) : 0.0;
+    }
+}
+__device__ __forceinline__ double row_reduce(const RowTerms &R, unsigned gmask) {
+    const int n = R.n;
+    if (n < 0) return 0.0;
+    double res;
+    if (n >= 8) {
+        const int nfull = (n - (n % 8)) / 8;
+        double r = R.t[0];
+#pragma unroll
+        for (int u = 1; u < 8; ++u)
+            if (u < nfull) r = add(r, R.t[u]);
+        r = add(r, __shfl_xor_sync(gmask, r, 1, 8));
+        r = add(r, __shfl_xor_sync(gmask, r, 2, 8));
+        r = add(r, __shfl_xor_sync(gmask, r, 4, 8));
+        const int tail = n % 8;
+        double tv = 0.0;
+#pragma unroll
+        for (int u = 1; u < 8; ++u)
+            if (u == nfull) tv = R.t[u];
+        for (int k = 0; k < tail; ++k) r = add(r, __shfl_sync(gmask, tv, k, 8));
+        res = r;
+    } else {
+        double r = -0.0;
+        for (int k = 0; k < n; ++k) r = add(r, __shfl_sync(gmask, R.t[0], k, 8));
+        res = r;
+    }
+    return add(__shfl_sync(gmask, R.p0, 0, 8), res);
+}
+
+// Rows row0, row0 + stride, ... < n by one 8-lane group, RPG rows' loads in
+// flight at a time; out(row, sum) in the lane-0 thread of the group.
+// Bit-identical to row_sum_exact per row.
+template <int RPG, class XAcc, class Out>
+__device__ __forceinline__ void rows_exact(int64_t row0, int64_t stride, int64_t n, const int32_t *__restrict__ rp,
+                                           const int32_t *__restrict__ col, const double *__restrict__ val,
+                                           const XAcc &xa, int lane8, unsigned gmask, const Out &out) {
+    for (int64_t r0 = row0; r0 < n; r0 += RPG * stride) {
+        int lo[RPG], len[RPG];
+        bool fast = true;
+#pragma unroll
+        for (int g = 0; g < RPG; ++g) {
+            const int64_t r = r0 + g * stride;
+            lo[g] = r < n ? rp[r] : 0;
+            len[g] = r < n ? rp[r + 1] - lo[g] : 0;
+            fast = fast && len[g] <= 65;
+        }
+        if (!fast) {  // long rows: the general path, one at a time
+#pragma unroll
+            for (int g = 0; g < RPG; ++g) {
+                const int64_t r = r0 + g * stride;
+                if (r < n) {
+                    const double v = row_sum_exact(lo[g], len[g], col, val, xa, lane8, gmask);
+                    if (lane8 == 0) out(r, v);
+                }
+            }
+            continue;
+        }
+        RowTerms T[RPG];
+#pragma unroll
+        for (int g = 0; g < RPG; ++g) row_terms(lo[g], len[g], col, val, xa, lane8, T[g]);
+#pragma unroll
+        for (int g = 0; g < RPG; ++g) {
+            const int64_t r = r0 + g * stride;
+            const double v = row_reduce(T[g], gmask);
+            if (lane8 == 0 && r < n) out(r, v);
+        }
+    }
+}
+
 }  // namespace tsb
