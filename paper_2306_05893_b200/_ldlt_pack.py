@@ -47,11 +47,22 @@ persistent kernel needs to be deadlock-free.
 from __future__ import annotations
 
 import ctypes as C
+import logging
 import os
 
 import numpy as np
 
 from . import _lib
+
+logger = logging.getLogger(__name__)
+
+# The block-inverse layout applies explicit inverses Linv = inv(L11): their
+# rounding error grows like cond_1(L11) * eps (the reference's tile-16
+# substitution like cond of the 16 x 16 tiles).  pack() measures
+# cond_1(L11) = ||L11||_1 ||Linv||_1 for every block (1.0e1 - 1.4e1 on the
+# beams) and warns above COND_WARN, where the apply can drift from the
+# reference's by more than ~1e-8 relative.
+COND_WARN = 1e8
 
 TILE = 32               # rows per tile (one per lane)
 ITEM_BYTES = 40 * 1024  # small-tile item budget: one TMA bulk copy (csrc kStage)
@@ -454,7 +465,13 @@ def pack(factors, subset=None):
                 mats[i] = block_matrix(bfs[i])
         for i in np.flatnonzero(big):
             mats[i] = block_matrix(bfs[i])
+    cond_l11 = 1.0
     for i, bf in enumerate(bfs):
+        if values:
+            linv_i = mats[i][0]
+            l11 = np.tril(np.asarray(bf.l11, dtype=np.float64), -1) + np.eye(len(linv_i))
+            c1 = float(np.abs(l11).sum(axis=0).max() * np.abs(linv_i).sum(axis=0).max()) if len(linv_i) else 1.0
+            cond_l11 = max(cond_l11, c1)
         G = gfull(*mats.pop(i)) if values else None
         for up in (False, True):
             tiles, parts = tile_block(G.T if (up and G is not None) else G, int(ms_[i]), int(na_[i]), up)
@@ -586,7 +603,7 @@ def pack(factors, subset=None):
         "tiles_l": tables[False], "tiles_u": tables[True], "g": cat(data[False]), "gt": cat(data[True]),
         "anc": anc_all, "cslot": cslot, "cin_ptr": cin_ptr, "ncbuf": len(anc_all),
         "d": np.asarray(factors.d if factors.d is not None else np.zeros(n), dtype=np.float64), "perm": np.asarray(plan.perm, dtype=np.int64),
-        "max_m": int(ms_.max()) if nb else 1, "max_v": int(max_w), "max_cb": max_cb,
+        "max_m": int(ms_.max()) if nb else 1, "max_v": int(max_w), "max_cb": max_cb, "cond_l11": cond_l11,
         "parent": parent, "children": children, "mode": mode,
         "npart_l": npart[False], "npart_u": npart[True], "ext_rows": ext_rows,
         "bytes_g": int(pos[False]) * 8, "bytes_gt": int(pos[True]) * 8,
@@ -612,6 +629,10 @@ class DevicePanels:
             H["max_cb"] = min(CB_CAP, int(H["blocks"]["ncb"][inner].max(initial=0)))
         n, nb = H["n"], H["nb"]
         items_l, items_u = H["items_l"], H["items_u"]
+        self.cond_l11 = H["cond_l11"]  # max cond_1(L11) over the blocks (explicit-inverse accuracy guard)
+        if self.cond_l11 > COND_WARN:
+            logger.warning("LDL^T block-inverse apply: cond_1(L11) up to %.3g; the explicit inverses lose about "
+                           "cond * eps relative accuracy against the reference's tile substitution", self.cond_l11)
         self.host = H if trace else None
         self.tile_blk = (H["tile_blk_l"], H["tile_blk_u"])  # tile -> block (device refactorisation)
         if trace:  # per-item timeline (globaltimer ns): take, ready, end, smid, staged, computed

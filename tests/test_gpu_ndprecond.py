@@ -8,6 +8,7 @@ import pytest
 
 pytestmark = pytest.mark.gpu
 
+from oracle import tetsim_oracle as O  # noqa: E402
 from paper_2306_05893_b200 import krylov, ndprecond as ND  # noqa: E402
 from paper_2306_05893_b200.assembly import CsrMatrix  # noqa: E402
 from paper_2306_05893_b200.mesh import Graph  # noqa: E402
@@ -49,10 +50,18 @@ def test_random_patterns_thresholds_tiles(rng):
         a = csr_from_dense(dense)
         plan = ND.nested_dissection(ND.graph_from_pattern(a), int(rng.integers(1, 8)))
         assert ND.count_coupling_violations(a, plan) == 0
-        f = ND.ldlt_factor_device(a, plan, tile=int(rng.integers(1, 20)))
+        tile = int(rng.integers(1, 20))
+        f = ND.ldlt_factor_device(a, plan, tile=tile)
         r = rng.standard_normal(n)
         z = ND.apply(f, r)
         assert np.abs(krylov.spmv(a, z) - r).max() / np.abs(r).max() < 1e-9
+        # the block-inverse device apply of the HOST factors vs the reference's
+        # tile substitution (oracle) on the same factors, within the guard's bound
+        fh = ND.ldlt_factor(a, plan, tile=tile)
+        zo = O.apply(fh, r)
+        cond = fh.device().cond_l11
+        assert cond < 1e4
+        assert np.abs(ND.apply(fh, r) - zo).max() <= 1e-14 * max(cond, 10.0) * np.abs(zo).max()
 
 
 def test_disconnected_graph_expanded_and_factored(rng):

@@ -232,3 +232,26 @@ def test_amalgamated_factors_apply_identically(max_rows):
     out = np.empty_like(z)
     out[f.plan.perm] = z
     assert np.abs(out - ref).max() <= 1e-12 * np.abs(ref).max()
+
+
+def test_block_inverse_conditioning_guard(caplog):
+    """pack() measures cond_1(L11) of every block (the explicit inverses' error
+    grows like cond * eps): small on the beams (the reference's factors here:
+    ~10), and a graded SPD system is flagged."""
+    _, f = _factors((6, 6, 20), 64)
+    H = K.pack(f)
+    assert 1.0 <= H["cond_l11"] <= 20.0
+    # ill-conditioned: a graded SPD chain
+    n = 40
+    s = np.logspace(0, 30, n)
+    dense = np.diag(s * s)
+    for i in range(n - 1):  # D T D with T = tridiag(0.49, 1, 0.49) (SPD), D graded: L11 entries grow ~3^k
+        dense[i, i + 1] = dense[i + 1, i] = 0.49 * s[i] * s[i + 1]
+    rows, cols = np.nonzero(dense)
+    rp = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(np.bincount(rows, minlength=n), out=rp[1:])
+    a = CsrMatrix(n, n, rp, cols.astype(np.int64), dense[rows, cols])
+    plan = ND.nested_dissection(ND.graph_from_pattern(a), 64)
+    fi = ND.ldlt_factor(a, plan)
+    Hi = K.pack(fi)
+    assert Hi["cond_l11"] > K.COND_WARN
