@@ -250,6 +250,8 @@ typedef struct tsb_ldlt_desc {
     int32_t *d_ctl;               /* [4] tickets / exit counters (zeroed)          */
     int64_t *d_trace_lower;       /* optional [n_items_lower][8] item timeline     */
     int64_t *d_trace_upper;       /* optional [n_items_upper][8]                   */
+    double *d_rin;                /* scratch [n]: apply's input gathered through perm once, so
+                                     the lower sweep's items read it directly (NULL: gather per item) */
 } tsb_ldlt_desc;
 
 typedef struct tsb_ldlt *tsb_ldlt_t;

@@ -63,6 +63,8 @@ logger = logging.getLogger(__name__)
 # beams) and warns above COND_WARN, where the apply can drift from the
 # reference's by more than ~1e-8 relative.
 COND_WARN = 1e8
+# apply: gather r through perm once before the lower sweep instead of per item
+PERMUTE_ONCE = os.environ.get("TSB_PERMUTE_ONCE", "1") != "0"
 
 TILE = 32               # rows per tile (one per lane)
 ITEM_BYTES = 40 * 1024  # small-tile item budget: one TMA bulk copy (csrc kStage)
@@ -653,7 +655,7 @@ class DevicePanels:
                 "d": up(H["d"]), "perm": i32(H["perm"]), "ext_rows": i32(nz(H["ext_rows"])),
             }
             ntl, ntu = len(H["tiles_l"]), len(H["tiles_u"])
-            self.t.update(cbuf=z(H["ncbuf"], t.float64), x=z(n, t.float64), y=z(n, t.float64),
+            self.t.update(cbuf=z(H["ncbuf"], t.float64), x=z(n, t.float64), y=z(n, t.float64), rin=z(n, t.float64),
                           part=z(TILE * (H["npart_l"] + H["npart_u"]), t.float64),
                           cnt=z(3 * nb, t.int32), tcnt=z(ntl + ntu, t.int32), ctl=z(4, t.int32))
         self.n = n
@@ -679,6 +681,7 @@ class DevicePanels:
             d_ctl=tp("ctl"),
             d_trace_lower=_lib.ptr(self.trace_l) if trace else None,
             d_trace_upper=_lib.ptr(self.trace_u) if trace else None,
+            d_rin=tp("rin") if PERMUTE_ONCE else None,
         )
         if stream is not None:
             stream.synchronize()

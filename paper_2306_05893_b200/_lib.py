@@ -66,7 +66,7 @@ class LdltDesc(C.Structure):
         ("d_part_lower", c_vp), ("d_part_upper", c_vp), ("d_tcnt_lower", c_vp), ("d_tcnt_upper", c_vp),
         ("n_tiles_lower", c_i64), ("n_tiles_upper", c_i64), ("d_ext_rows", c_vp), ("n_ext", c_i64),
         ("d_ctl", c_vp),
-        ("d_trace_lower", c_vp), ("d_trace_upper", c_vp),
+        ("d_trace_lower", c_vp), ("d_trace_upper", c_vp), ("d_rin", c_vp),
     ]
 
 

@@ -66,6 +66,13 @@ __global__ void __launch_bounds__(kSweepBlock) upper_sweep(tsb_ldlt_desc D, Swee
     upper_sweep_body<TRACE>(D, A, smem, R);
 }
 
+__global__ void permute_kernel(int64_t n, const int32_t *__restrict__ perm, const double *__restrict__ r,
+                               double *__restrict__ out, const int32_t *done) {
+    if (done != nullptr && *((volatile const int32_t *)done)) return;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = __ldg(r + perm[i]);
+}
+
 static uint64_t g_serial = 0;
 static std::mutex g_serial_mu;
 
@@ -94,8 +101,16 @@ void ldlt_enqueue(tsb_ldlt_t h, int mode, const double *r, double *out, const in
     tsb_ldlt_desc &D = h->d;
     if (D.n == 0) return;
     const int grid = D.grid;
+    if (mode == 2 && D.d_rin != nullptr) {  // r through perm once: the sweep's items then read it directly
+        int g = (int)((D.n + 255) / 256);
+        if (g > kNumSM * 8) g = kNumSM * 8;
+        permute_kernel<<<g, 256, 0, st>>>(D.n, D.d_perm, r, D.d_rin, done);
+        TSB_LAUNCHED();
+    }
     if (mode == 0 || mode == 2) {
-        SweepArgs a{r, mode == 2 ? D.d_perm : nullptr, nullptr, mode == 2 ? D.d_y : out, nullptr, nullptr, done};
+        const bool pre = mode == 2 && D.d_rin != nullptr;
+        SweepArgs a{pre ? D.d_rin : r, (mode == 2 && !pre) ? D.d_perm : nullptr, nullptr, mode == 2 ? D.d_y : out,
+                    nullptr, nullptr, done};
         if (D.d_trace_lower)
             launch_coop(lower_sweep<true>, grid, sweep_smem_lower(D), st, D, a);
         else

@@ -195,12 +195,22 @@ pcg_persistent(PcgWork W, PcgArgs a, tsb_ldlt_desc D) {
         }
     }
     // preconditioner application z = M r and rz = r.z
-    SweepArgs lo_args{W.r, D.d_perm, nullptr, D.d_y, nullptr, nullptr, nullptr};
+    // LDL^T: r is gathered through perm once per apply into W.invdiag (unused by
+    // this kind) before the lower sweep, so the sweep's items read it directly
+    const bool pre_perm = KIND == TSB_PRECOND_LDLT && D.d_rin != nullptr;
+    SweepArgs lo_args{pre_perm ? W.invdiag : W.r, pre_perm ? nullptr : D.d_perm, nullptr, D.d_y, nullptr, nullptr,
+                      nullptr};
+    auto permute_r = [&]() {
+        if (!pre_perm) return;
+        for (int64_t i = gtid; i < n; i += gstride) W.invdiag[i] = __ldcg(W.r + D.d_perm[i]);
+        grid_sync(W.bar);
+    };
     SweepArgs up_args{D.d_y, nullptr, D.d_d, D.d_x, D.d_perm, W.z, nullptr};
     double rz = 0.0, beta = 0.0;
     if (!done) {
         double v = 0.0;
         if (KIND == TSB_PRECOND_LDLT) {
+            permute_r();
             lower_sweep_body<false>(D, lo_args, smem, ring);
             grid_sync(W.bar);
             upper_sweep_body<false>(D, up_args, smem, ring);
@@ -315,6 +325,7 @@ pcg_persistent(PcgWork W, PcgArgs a, tsb_ldlt_desc D) {
         } else if (KIND == TSB_PRECOND_JACOBI) {
             rzn = all_partials(W.part, 1, red, &bc);
         } else {
+            permute_r();
             lower_sweep_body<false>(D, lo_args, smem, ring);
             grid_sync(W.bar);
             upper_sweep_body<false>(D, up_args, smem, ring);
