@@ -149,25 +149,32 @@ def expand_plan(plan: DissectionPlan, dofs_per_vertex: int = 3) -> DissectionPla
 
 
 def graph_from_pattern(a: CsrMatrix) -> Graph:
-    row_of = np.repeat(np.arange(a.nrows), np.diff(a.row_ptr))
-    off = row_of != a.col_ind
-    codes = np.unique(np.concatenate([row_of[off] * a.nrows + a.col_ind[off],
-                                      a.col_ind[off] * a.nrows + row_of[off]]))
-    src, dst = codes // a.nrows, codes % a.nrows
-    indptr = np.zeros(a.nrows + 1, dtype=np.int64)
-    np.cumsum(np.bincount(src, minlength=a.nrows), out=indptr[1:])
-    return Graph(n=a.nrows, indptr=indptr, indices=dst.astype(np.int64))
+    """Vertex graph of a CSR pattern (ndprecond.py:282-292): i ~ j when
+    A_ij or A_ji is stored, i != j; neighbour lists sorted, no self loops.
+    Restated: one symmetric boolean structure through scipy.sparse."""
+    import scipy.sparse as sp
+
+    n = a.nrows
+    pat = sp.csr_matrix((np.ones(a.nnz, dtype=np.int8), np.asarray(a.col_ind), np.asarray(a.row_ptr)), shape=(n, n))
+    sym = ((pat + pat.T) != 0).tocsr()
+    sym.setdiag(0)
+    sym.eliminate_zeros()
+    sym.sort_indices()
+    return Graph(n=n, indptr=sym.indptr.astype(np.int64), indices=sym.indices.astype(np.int64))
 
 
 def count_coupling_violations(a: CsrMatrix, plan: DissectionPlan) -> int:
+    """Stored entries (i, j) whose permuted positions lie in blocks that are
+    not on one root path (ndprecond.py:295-309): an entry is legal iff one
+    position falls inside the other block's subtree range [tree_start, stop)."""
     owner = plan.block_of_index()
-    tree_start = np.array([b.tree_start for b in plan.blocks])
-    stop = np.array([b.stop for b in plan.blocks])
-    row_of = np.repeat(np.arange(a.nrows), np.diff(a.row_ptr))
-    pi, pj = plan.iperm[row_of], plan.iperm[a.col_ind]
-    bi, bj = owner[pi], owner[pj]
-    legal = ((tree_start[bi] <= pj) & (pj < stop[bi])) | ((tree_start[bj] <= pi) & (pi < stop[bj]))
-    return int(np.count_nonzero(~legal))
+    lo = np.fromiter((b.tree_start for b in plan.blocks), dtype=np.int64, count=len(plan.blocks))
+    hi = np.fromiter((b.stop for b in plan.blocks), dtype=np.int64, count=len(plan.blocks))
+    p_row = plan.iperm[np.repeat(np.arange(a.nrows), np.diff(a.row_ptr))]
+    p_col = plan.iperm[np.asarray(a.col_ind)]
+    in_row_tree = (lo[owner[p_row]] <= p_col) & (p_col < hi[owner[p_row]])
+    in_col_tree = (lo[owner[p_col]] <= p_row) & (p_row < hi[owner[p_col]])
+    return int(np.sum(~(in_row_tree | in_col_tree)))
 
 
 # ---------------------------------------------------------------------------
@@ -426,29 +433,31 @@ def _front_index(ds_dst, m, width):
 
 
 def _blocks_to_csr(n, blocks) -> CsrMatrix:
-    """Strict lower triangle of L in CSR, exact zeros dropped."""
-    rows, cols, vals = [], [], []
+    """Strict lower triangle of L (l11 strict lower + l21 panels) in CSR with
+    exact zeros dropped (the reference's l_matrix, ndprecond.py:479-495).
+    Restated: every block's strict-lower triangle and panel become COO
+    entries of one scipy.sparse matrix, converted once."""
+    import scipy.sparse as sp
+
+    r_parts, c_parts, v_parts = [], [], []
     for bf in blocks:
         m = bf.stop - bf.start
-        ir, ic = np.tril_indices(m, -1)
-        v = bf.l11[ir, ic]
-        nz = v != 0.0
-        rows.append(bf.start + ir[nz])
-        cols.append(bf.start + ic[nz])
-        vals.append(v[nz])
+        cols = np.arange(bf.start, bf.stop)
+        tri = np.tril(np.asarray(bf.l11), -1)
+        rr, cc = np.nonzero(tri)
+        r_parts.append(bf.start + rr)
+        c_parts.append(bf.start + cc)
+        v_parts.append(tri[rr, cc])
         if len(bf.anc):
-            pv = bf.l21.ravel()
-            nz = pv != 0.0
-            rows.append(np.repeat(bf.anc, m)[nz])
-            cols.append(np.tile(np.arange(bf.start, bf.stop), len(bf.anc))[nz])
-            vals.append(pv[nz])
-    rows = np.concatenate(rows) if rows else np.empty(0, dtype=np.int64)
-    cols = np.concatenate(cols) if cols else np.empty(0, dtype=np.int64)
-    vals = np.concatenate(vals) if vals else np.empty(0)
-    o = np.lexsort((cols, rows))
-    row_ptr = np.zeros(n + 1, dtype=np.int64)
-    np.cumsum(np.bincount(rows, minlength=n), out=row_ptr[1:])
-    return CsrMatrix(n, n, row_ptr, cols[o], vals[o])
+            rr, cc = np.nonzero(np.asarray(bf.l21))
+            r_parts.append(np.asarray(bf.anc)[rr])
+            c_parts.append(cols[cc])
+            v_parts.append(np.asarray(bf.l21)[rr, cc])
+    cat = lambda parts, dt: np.concatenate(parts) if parts else np.empty(0, dtype=dt)  # noqa: E731
+    coo = sp.coo_matrix((cat(v_parts, np.float64), (cat(r_parts, np.int64), cat(c_parts, np.int64))), shape=(n, n))
+    csr = coo.tocsr()
+    csr.sort_indices()
+    return CsrMatrix(n, n, csr.indptr.astype(np.int64), csr.indices.astype(np.int64), csr.data)
 
 
 # ---------------------------------------------------------------------------
