@@ -116,6 +116,9 @@ typedef struct tsb_asm_plan {
     double *d_work;             /* [48][m] scratch: [m][36] grads', f_e, K v_e; [m][12] F F^T, S (StVK) */
     int32_t *d_flags;           /* [4] device status words                   */
     const double *d_gab;        /* [m][10] rest-gradient products g_a.g_b (tsb_assembly_setup) */
+    const int32_t *d_blk_mirror;/* [nb][2] or NULL: block k is (I, J), I <= J, and also writes the
+                                   transposed block (J, I) at slot0 / rowlen d_blk_mirror[k]
+                                   (slot0 -1: diagonal block); d_blk then lists only I <= J */
 } tsb_asm_plan;
 
 enum { TSB_LAW_COROTATIONAL = 0, TSB_LAW_LINEAR = 1, TSB_LAW_STVK = 2 };

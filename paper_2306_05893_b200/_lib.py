@@ -43,6 +43,7 @@ class AsmPlan(C.Structure):
         ("d_rest", c_vp), ("d_mass_diag", c_vp), ("d_gravity", c_vp), ("d_fixed_dof", c_vp),
         ("d_blk", c_vp), ("d_blk_list", c_vp), ("d_node_ptr", c_vp), ("d_node_list", c_vp),
         ("d_fixed_slots", c_vp), ("d_work", c_vp), ("d_flags", c_vp), ("d_gab", c_vp),
+        ("d_blk_mirror", c_vp),
     ]
 
 

@@ -152,21 +152,41 @@ def _i32(a):
 BLK_WINDOW = int(os.environ.get("TSB_BLK_WINDOW", "2048"))
 
 
+MIRROR_BLOCKS = os.environ.get("TSB_MIRROR_BLOCKS", "1") != "0"
+
+
+def _mirror_work(pattern, n_nodes):
+    """Block gather work list using K_ba = K_ab^T: only blocks (I, J) with
+    I <= J are summed; each off-diagonal one also writes block (J, I) (same
+    contributing elements, same ascending order).  -> (work [nw][4], mirror
+    [nw][2] = slot0, row length of (J, I), or -1 for a diagonal block)."""
+    blk = np.asarray(pattern["blk"], dtype=np.int64)
+    row_ptr = np.asarray(pattern["row_ptr"], dtype=np.int64)
+    col_ind = np.asarray(pattern["col_ind"], dtype=np.int64)
+    bI = (np.searchsorted(row_ptr, blk[:, 0], side="right") - 1) // 3
+    bJ = col_ind[blk[:, 0]] // 3
+    key = bI * n_nodes + bJ  # CSR order: ascending
+    up = bI <= bJ
+    mk = np.searchsorted(key, bJ[up] * n_nodes + bI[up])
+    mirror = np.where((bI[up] < bJ[up])[:, None], blk[mk][:, :2], -1)
+    return blk[up], mirror
+
+
 def _warp_uniform_order(blk):
-    """Block gather work order: within windows of BLK_WINDOW consecutive CSR
-    blocks (about the same node rows, so the element scratch they read is
-    still shared through L2), blocks sorted by contribution count, heaviest
-    first -- a warp's 32 threads then loop over about the same number of
-    contributions instead of every warp waiting for its one diagonal block
-    (~4x the contributions of an off-diagonal one).  Each entry carries its own
-    CSR slot, so the order changes nothing in the sums."""
+    """Block gather work order (a permutation of the work list): within
+    windows of BLK_WINDOW consecutive CSR blocks (about the same node rows, so
+    the element scratch they read is still shared through L2), blocks sorted
+    by contribution count, heaviest first -- a warp's 32 threads then loop over
+    about the same number of contributions instead of every warp waiting for
+    its one diagonal block (~4x the contributions of an off-diagonal one).
+    Each entry carries its own CSR slot, so the order changes nothing in the
+    sums."""
     blk = np.asarray(blk)
     if BLK_WINDOW <= 0 or len(blk) == 0:
-        return blk
+        return np.arange(len(blk))
     cnt = blk[:, 3] - blk[:, 2]
-    order = np.concatenate([w0 + np.argsort(-cnt[w0:w0 + BLK_WINDOW], kind="stable")
-                            for w0 in range(0, len(blk), BLK_WINDOW)])
-    return blk[order]
+    return np.concatenate([w0 + np.argsort(-cnt[w0:w0 + BLK_WINDOW], kind="stable")
+                           for w0 in range(0, len(blk), BLK_WINDOW)])
 
 
 LAWS = {"corotational": 0, "linear": 1, "stvk": 2}  # tsb.h TSB_LAW_*
@@ -209,12 +229,17 @@ class AssemblyPlan:
         self.gab = t.empty(max(m, 1) * 10, dtype=t.float64, device=dev)  # g_a . g_b per tet (tsb_assembly_setup)
         self.flags = t.zeros(4, dtype=t.int32, device=dev)
         self.pattern = pattern
+        self.blk_mirror = None
         if pattern is not None:
-            self.blk = t.from_numpy(_i32(_warp_uniform_order(pattern["blk"]))).to(dev)
+            work, mirror = _mirror_work(pattern, N) if MIRROR_BLOCKS else (np.asarray(pattern["blk"]), None)
+            order = _warp_uniform_order(work)
+            self.blk = t.from_numpy(_i32(work[order])).to(dev)
+            if mirror is not None:
+                self.blk_mirror = t.from_numpy(_i32(mirror[order])).to(dev)
             self.blk_list = t.from_numpy(_i32(pattern["blk_list"])).to(dev)
             self.fixed_slots = t.from_numpy(_i32(pattern["fixed_diag_slots"])).to(dev)
             node_ptr, node_list = pattern["node_ptr"], pattern["node_list"]
-            nb, nnz, nfix = len(pattern["blk"]), len(pattern["col_ind"]), len(pattern["fixed_diag_slots"])
+            nb, nnz, nfix = len(self.blk), len(pattern["col_ind"]), len(pattern["fixed_diag_slots"])
         else:
             self.blk = self.blk_list = self.fixed_slots = None
             flat = el.ravel()
@@ -232,7 +257,7 @@ class AssemblyPlan:
             d_fixed_dof=P(self.fixed_dof), d_blk=P(self.blk), d_blk_list=P(self.blk_list),
             d_node_ptr=P(self.node_ptr), d_node_list=P(self.node_list),
             d_fixed_slots=P(self.fixed_slots), d_work=P(self.work), d_flags=P(self.flags),
-            d_gab=P(self.gab),
+            d_gab=P(self.gab), d_blk_mirror=P(self.blk_mirror),
         )
         import ctypes as C
 

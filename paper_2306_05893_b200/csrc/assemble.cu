@@ -330,6 +330,7 @@ __global__ void gab_kernel(int64_t m, const double *__restrict__ grads, double *
 
 template <bool STVK, int U>
 __device__ __forceinline__ void block_body(int64_t bi, int64_t nb, int64_t m, const int4 *__restrict__ blk,
+                                           const int2 *__restrict__ mirror,
                                            const int32_t *__restrict__ list, const double *__restrict__ work,
                                            const double *__restrict__ grads, const double *__restrict__ gab,
                                            const double *__restrict__ vol,
@@ -398,6 +399,15 @@ __device__ __forceinline__ void block_body(int64_t bi, int64_t nb, int64_t m, co
     for (int i = 0; i < 3; ++i)
 #pragma unroll
         for (int j = 0; j < 3; ++j) values[info.x + i * info.y + j] = acc[3 * i + j];
+    if (mirror != nullptr) {  // K_ba = K_ab^T (the element blocks are symmetric): block (J, I) from (I, J)
+        const int2 mb = __ldg(mirror + bi);
+        if (mb.x >= 0) {
+#pragma unroll
+            for (int i = 0; i < 3; ++i)
+#pragma unroll
+                for (int j = 0; j < 3; ++j) values[mb.x + j * mb.y + i] = acc[3 * i + j];
+        }
+    }
 }
 
 __device__ __forceinline__ void node_body(int64_t I, int64_t N, const int32_t *__restrict__ node_ptr,
@@ -460,7 +470,8 @@ __device__ __forceinline__ void node_body(int64_t I, int64_t N, const int32_t *_
 // of running after it.
 template <bool STVK, int U, int MINB>
 __global__ void __launch_bounds__(256, MINB)
-gather_kernel(int64_t nbc, int64_t nb, int64_t m, const int4 *__restrict__ blk, const int32_t *__restrict__ list,
+gather_kernel(int64_t nbc, int64_t nb, int64_t m, const int4 *__restrict__ blk, const int2 *__restrict__ mirror,
+              const int32_t *__restrict__ list,
               const double *__restrict__ work, const double *__restrict__ grads, const double *__restrict__ gab,
               const double *__restrict__ vol,
               const double *__restrict__ share, double lam, double mu, double cm, double ck,
@@ -489,8 +500,8 @@ gather_kernel(int64_t nbc, int64_t nb, int64_t m, const int4 *__restrict__ blk, 
         node_body(node_cta * (int64_t)blockDim.x + threadIdx.x, N, node_ptr, node_list, work, x, v, fext_state,
                   gravity, mass_diag, fixed, hb, alpha, f_int, kv, b, f_ext, flags);
     else
-        block_body<STVK, U>(blk_cta * (int64_t)blockDim.x + threadIdx.x, nb, m, blk, list, work, grads, gab, vol,
-                            share, lam, mu, cm, ck, values);
+        block_body<STVK, U>(blk_cta * (int64_t)blockDim.x + threadIdx.x, nb, m, blk, mirror, list, work, grads, gab,
+                            vol, share, lam, mu, cm, ck, values);
 }
 
 __global__ void __launch_bounds__(128)
@@ -587,7 +598,8 @@ extern "C" int tsb_assemble_corot(const tsb_asm_plan *p, const tsb_asm_coeffs *c
                 else if (variant == 4) kern = gather_kernel<false, 1, 8>;
             }
             kern<<<(unsigned)(nbc + nnc), 256, 0, s>>>(
-                nbc, p->n_blocks, p->n_elems, reinterpret_cast<const int4 *>(p->d_blk), p->d_blk_list, p->d_work,
+                nbc, p->n_blocks, p->n_elems, reinterpret_cast<const int4 *>(p->d_blk),
+                reinterpret_cast<const int2 *>(p->d_blk_mirror), p->d_blk_list, p->d_work,
                 p->d_grads, p->d_gab, p->d_vol, p->d_mass_share, c->lam, c->mu, c->cm, c->ck, d_values, p->n_nodes,
                 p->d_node_ptr, p->d_node_list, d_x, d_v, d_f_ext_state, p->d_gravity, p->d_mass_diag,
                 p->d_fixed_dof, c->h + c->rayleigh_stiffness, c->rayleigh_mass, d_f_int, d_kv, d_b, d_f_ext,
