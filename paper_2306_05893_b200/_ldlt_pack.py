@@ -599,7 +599,11 @@ def pack(factors, subset=None):
 
     max_w = max([1] + [(lambda w: w[1] - w[0])(window(up, i, it)) for up in (False, True)
                        for i in range(nb) for it in items[up][i]])
-    cat = lambda parts: np.concatenate(parts) if parts else np.zeros(2)  # noqa: E731
+    def cat(parts):  # one array per sweep; the parts are released as soon as they are copied
+        out = np.concatenate(parts) if parts else np.zeros(2)
+        parts.clear()
+        return out
+
     return {
         "n": n, "nb": nb, "blocks": blocks, "items_l": items_l, "items_u": items_u,
         "tiles_l": tables[False], "tiles_u": tables[True], "g": cat(data[False]), "gt": cat(data[True]),
@@ -642,7 +646,12 @@ class DevicePanels:
             self.trace_u = t.zeros((len(items_u), 8), dtype=t.int64, device="cuda")
         ctx = t.cuda.stream(stream) if stream is not None else _NullCtx()
         with ctx:
-            up = lambda a: t.from_numpy(np.ascontiguousarray(a)).pin_memory().to("cuda", non_blocking=True)  # noqa: E731
+            def up(a):  # small arrays through pinned memory; the factor images (GBs at 1M nodes) straight,
+                # without a second full-size pinned host copy
+                a = np.ascontiguousarray(a)
+                if a.nbytes > (1 << 30):
+                    return t.from_numpy(a).to("cuda")
+                return t.from_numpy(a).pin_memory().to("cuda", non_blocking=True)
             i32 = lambda a: up(np.asarray(a, dtype=np.int32))  # noqa: E731
             i64 = lambda a: up(np.asarray(a, dtype=np.int64))  # noqa: E731
             z = lambda k, dt: t.zeros(max(k, 1), dtype=dt, device="cuda")  # noqa: E731
@@ -658,6 +667,7 @@ class DevicePanels:
             self.t.update(cbuf=z(H["ncbuf"], t.float64), x=z(n, t.float64), y=z(n, t.float64), rin=z(n, t.float64),
                           part=z(TILE * (H["npart_l"] + H["npart_u"]), t.float64),
                           cnt=z(3 * nb, t.int32), tcnt=z(ntl + ntu, t.int32), ctl=z(4, t.int32))
+        H["g"] = H["gt"] = None  # the host copies of the factor images (GBs) are not needed any more
         self.n = n
         self.ncbuf, self.npart_l = int(H["ncbuf"]), int(H["npart_l"])
         self._multi = {}
