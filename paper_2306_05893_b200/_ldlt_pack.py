@@ -135,26 +135,43 @@ def row_ranges(m: int, na: int, upper: bool):
     return np.zeros(m + na, dtype=np.int64), np.minimum(r + 1, m)
 
 
+def tile_layout(m: int, na: int, upper: bool):
+    """Tiles of one block for one sweep: [(tl, npair, row0, nrows)] (a tile
+    covers the union [tl, th) of its rows' v-ranges, tl even)."""
+    lo, hi = row_ranges(m, na, upper)
+    nrows_all = len(lo)
+    tiles = []
+    for r0 in range(0, nrows_all, TILE):
+        r1 = min(r0 + TILE, nrows_all)
+        tl = int(lo[r0:r1].min()) & ~1
+        th = int(hi[r0:r1].max())
+        tiles.append((tl, max((th - tl + 1) // 2, 0), r0, r1 - r0))
+    return tiles
+
+
+def tile_data(G, tiles):
+    """The tiles' data (pair-major, lane-interleaved), concatenated in tile order."""
+    parts = []
+    for tl, npair, r0, nr in tiles:
+        d = np.zeros((TILE, 2 * npair))
+        w = min(2 * npair, G.shape[1] - tl)
+        if w > 0:
+            d[:nr, :w] = G[r0:r0 + nr, tl:tl + w]
+        parts.append(d.reshape(TILE, npair, 2).transpose(1, 0, 2).ravel())
+    return np.concatenate(parts) if parts else np.zeros(0)
+
+
 def tile_block(G, m: int, na: int, upper: bool):
     """Tiles of one block for one sweep -> (list of (tl, np, row0, nrows), data parts).
 
     G holds the sweep's rows: gfull() for the lower sweep, its transpose for
     the upper; None gives zero tiles (structure only, filled on the device by
     tsb_refactor_run)."""
-    lo, hi = row_ranges(m, na, upper)
-    nrows_all = len(lo)
-    tiles, parts = [], []
-    for r0 in range(0, nrows_all, TILE):
-        r1 = min(r0 + TILE, nrows_all)
-        tl = int(lo[r0:r1].min()) & ~1
-        th = int(hi[r0:r1].max())
-        npair = max((th - tl + 1) // 2, 0)
-        d = np.zeros((TILE, 2 * npair))
-        w = th - tl
-        if w > 0 and G is not None:
-            d[: r1 - r0, :w] = G[r0:r1, tl:th]
-        parts.append(d.reshape(TILE, npair, 2).transpose(1, 0, 2).ravel())
-        tiles.append((tl, npair, r0, r1 - r0))
+    tiles = tile_layout(m, na, upper)
+    parts = []
+    for tl, npair, r0, nr in tiles:
+        d = tile_data(G, [(tl, npair, r0, nr)]) if G is not None else np.zeros(TILE * 2 * npair)
+        parts.append(d)
     return tiles, parts
 
 
@@ -409,7 +426,7 @@ def _list_schedule(entries, cost, children, sweep):
     return out.reshape(-1, 4)
 
 
-def pack(factors, subset=None):
+def pack(factors, subset=None, sink=None, alloc=None):
     """Host arrays of the tiled block-inverse layout + item lists (pure NumPy).
 
     `subset` (block indices) packs one shard: ancestor rows outside the subset
@@ -450,39 +467,54 @@ def pack(factors, subset=None):
     ms_ = np.array([bf.stop - bf.start for bf in bfs], dtype=np.int64)
     na_ = np.array([len(bf.anc) for bf in bfs], dtype=np.int64)
 
-    # ---------------- tiles ----------------
+    # ---------------- tiles: layout pass ----------------
     tl_rows = {False: [], True: []}       # per sweep: global tile table rows
-    data = {False: [], True: []}
     pos = {False: 0, True: 0}
     blk_tiles = {False: [], True: []}     # per sweep, per block: (first tile id, [tiles])
     tile_blk = {False: [], True: []}      # per sweep: tile -> block
+    blk_off = {False: [], True: []}       # per sweep, per block: offset of its data
+    for i in range(nb):
+        for up in (False, True):
+            tiles = tile_layout(int(ms_[i]), int(na_[i]), up)
+            blk_tiles[up].append((len(tl_rows[up]), tiles))
+            tile_blk[up].extend([i] * len(tiles))
+            blk_off[up].append(pos[up])
+            for tl, npair, r0, nr in tiles:
+                tl_rows[up].append((pos[up], tl, npair, r0, nr))
+                pos[up] += TILE * 2 * npair
+    if alloc is not None:  # the caller's storage for the two images (e.g. HBM), before the data pass
+        alloc(pos[False], pos[True])
+    # ---------------- tiles: data pass ----------------
+    # block by block (block_matrix computed lazily, so the host holds one block's
+    # G at a time); sink(up, offset, data) receives each block's tiles -- the
+    # device image writes them straight into HBM, the default collects them
     from threadpoolctl import threadpool_limits
 
     values = all(getattr(bf, "l11", None) is not None for bf in bfs)  # else structure only (zero tiles)
-    big = ms_ * (ms_ + na_) > 1_000_000
-    mats = {}
-    if values:
-        with threadpool_limits(limits=1, user_api="blas"):  # small blocks: thread wake-ups cost more than the math
-            for i in np.flatnonzero(~big):
-                mats[i] = block_matrix(bfs[i])
-        for i in np.flatnonzero(big):
-            mats[i] = block_matrix(bfs[i])
+    data = {False: [], True: []}
+    if sink is None and values:
+        def sink(up, off, d):
+            data[up].append(d)
     cond_l11 = 1.0
-    for i, bf in enumerate(bfs):
-        if values:
-            linv_i = mats[i][0]
-            l11 = np.tril(np.asarray(bf.l11, dtype=np.float64), -1) + np.eye(len(linv_i))
-            c1 = float(np.abs(l11).sum(axis=0).max() * np.abs(linv_i).sum(axis=0).max()) if len(linv_i) else 1.0
-            cond_l11 = max(cond_l11, c1)
-        G = gfull(*mats.pop(i)) if values else None
-        for up in (False, True):
-            tiles, parts = tile_block(G.T if (up and G is not None) else G, int(ms_[i]), int(na_[i]), up)
-            blk_tiles[up].append((len(tl_rows[up]), tiles))
-            tile_blk[up].extend([i] * len(tiles))
-            for (tl, npair, r0, nr), p in zip(tiles, parts):
-                tl_rows[up].append((pos[up], tl, npair, r0, nr))
-                data[up].append(p)
-                pos[up] += len(p)
+    if values:
+        big = ms_ * (ms_ + na_) > 1_000_000
+        small_limiter = threadpool_limits(limits=1, user_api="blas")  # small blocks: thread wake-ups cost more
+        try:
+            for i, bf in enumerate(bfs):
+                if big[i]:
+                    small_limiter.restore_original_limits()
+                linv_i, mm_i = block_matrix(bf)
+                if big[i]:
+                    small_limiter = threadpool_limits(limits=1, user_api="blas")
+                l11 = np.tril(np.asarray(bf.l11, dtype=np.float64), -1) + np.eye(len(linv_i))
+                c1 = float(np.abs(l11).sum(axis=0).max() * np.abs(linv_i).sum(axis=0).max()) if len(linv_i) else 1.0
+                cond_l11 = max(cond_l11, c1)
+                G = gfull(linv_i, mm_i)
+                del l11, linv_i, mm_i
+                for up in (False, True):
+                    sink(up, blk_off[up][i], tile_data(G.T if up else G, blk_tiles[up][i][1]))
+        finally:
+            small_limiter.restore_original_limits()
     segs, groups_per_item = item_granularity(pos[False] * 8)
     tables = {}
     npart = {}
@@ -599,14 +631,18 @@ def pack(factors, subset=None):
 
     max_w = max([1] + [(lambda w: w[1] - w[0])(window(up, i, it)) for up in (False, True)
                        for i in range(nb) for it in items[up][i]])
-    def cat(parts):  # one array per sweep; the parts are released as soon as they are copied
-        out = np.concatenate(parts) if parts else np.zeros(2)
-        parts.clear()
+    def cat(up):  # one array per sweep (zeros: structure only; None: the sink holds the data)
+        if not values:
+            return np.zeros(max(pos[up], 2))
+        if not data[up]:
+            return None if pos[up] else np.zeros(2)
+        out = np.concatenate(data[up])
+        data[up].clear()
         return out
 
     return {
         "n": n, "nb": nb, "blocks": blocks, "items_l": items_l, "items_u": items_u,
-        "tiles_l": tables[False], "tiles_u": tables[True], "g": cat(data[False]), "gt": cat(data[True]),
+        "tiles_l": tables[False], "tiles_u": tables[True], "g": cat(False), "gt": cat(True),
         "anc": anc_all, "cslot": cslot, "cin_ptr": cin_ptr, "ncbuf": len(anc_all),
         "d": np.asarray(factors.d if factors.d is not None else np.zeros(n), dtype=np.float64), "perm": np.asarray(plan.perm, dtype=np.int64),
         "max_m": int(ms_.max()) if nb else 1, "max_v": int(max_w), "max_cb": max_cb, "cond_l11": cond_l11,
@@ -624,7 +660,19 @@ class DevicePanels:
         t = _lib.require_cuda()
         if merge is None:
             merge = MERGE_ROWS if subset is None else 0
-        H = pack(amalgamate(factors, merge) if merge else factors, subset)
+        dev_img = {}
+
+        def alloc(n_l, n_u):  # the factor images live only in HBM: each block's tiles are copied in directly
+            dev_img[False] = t.zeros(max(n_l, 2), dtype=t.float64, device="cuda")
+            dev_img[True] = t.zeros(max(n_u, 2), dtype=t.float64, device="cuda")
+
+        def sink(up, off, d):
+            if len(d):
+                dev_img[up][off:off + len(d)].copy_(t.from_numpy(d))
+
+        src = amalgamate(factors, merge) if merge else factors
+        values = all(getattr(bf, "l11", None) is not None for bf in src.blocks)
+        H = pack(src, subset, sink=sink if values else None, alloc=alloc if values else None)
         if force_mode is not None:  # testing: route every inner block through one input mode
             if force_mode != MODE_GATHER:
                 raise ValueError("only the item-gather mode can be forced (finaliser items are planned)")
@@ -659,7 +707,9 @@ class DevicePanels:
             raw = lambda a: up(nz(a).view(np.uint8))  # noqa: E731
             self.t = {
                 "blocks": raw(H["blocks"]), "items_l": up(nz(items_l.ravel())), "items_u": up(nz(items_u.ravel())),
-                "tiles_l": raw(H["tiles_l"]), "tiles_u": raw(H["tiles_u"]), "g": up(H["g"]), "gt": up(H["gt"]),
+                "tiles_l": raw(H["tiles_l"]), "tiles_u": raw(H["tiles_u"]),
+                "g": dev_img[False] if H["g"] is None else up(H["g"]),
+                "gt": dev_img[True] if H["gt"] is None else up(H["gt"]),
                 "anc": i32(nz(H["anc"])), "cslot": i32(nz(H["cslot"])), "cin_ptr": i64(H["cin_ptr"]),
                 "d": up(H["d"]), "perm": i32(H["perm"]), "ext_rows": i32(nz(H["ext_rows"])),
             }
