@@ -300,7 +300,13 @@ class LdlFactors:
 
     @property
     def fill_in(self) -> int:
-        return self.l_matrix.nnz
+        """nnz of the strict lower triangle of L, exact zeros dropped
+        (ndprecond.py:493-495) -- counted block by block, without
+        materialising l_matrix (~100 GB of COO at 1M nodes)."""
+        if self._l_matrix is not None:
+            return self._l_matrix.nnz
+        return int(sum(np.count_nonzero(np.tril(np.asarray(bf.l11), -1)) + np.count_nonzero(bf.l21)
+                       for bf in self.blocks))
 
     def device(self) -> "DeviceFactors":
         if self._device is None:

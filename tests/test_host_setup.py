@@ -223,3 +223,14 @@ def test_coupling_violations_zero_on_beam(golden):
     plan = ND.expand_plan(ND.nested_dissection(M.vertex_adjacency(mesh), 64))
     a = CsrMatrix(len(g["b"]), len(g["b"]), g["row_ptr"], g["col_ind"], g["values"])
     assert ND.count_coupling_violations(a, plan) == 0
+
+
+def test_fill_in_counts_without_materialising(golden):
+    """LdlFactors.fill_in (counted per block) equals the nnz of l_matrix."""
+    g = golden("ldlt_small")
+    mesh = clamped_beam(*map(int, g["dims"]))
+    plan = ND.expand_plan(ND.nested_dissection(M.vertex_adjacency(mesh), int(g["leaf"])))
+    a = CsrMatrix(len(g["b"]), len(g["b"]), g["row_ptr"], g["col_ind"], g["values"])
+    f = ND.ldlt_factor(a, plan, tile=16)
+    n0 = f.fill_in
+    assert n0 == f.l_matrix.nnz == int(g["f_fill"])
