@@ -668,7 +668,7 @@ def run_sharded(args, world, rank, local, dist):
 
     import torch
     import paper_2306_05893_b200 as P
-    from paper_2306_05893_b200 import krylov, shard as S
+    from paper_2306_05893_b200 import _lib, krylov, shard as S
     from paper_2306_05893_b200.integrator import BackwardEulerIntegrator, IntegratorConfig, SimState
 
     W = build_workload(args.workload)
@@ -718,14 +718,17 @@ def run_sharded(args, world, rank, local, dist):
     torch.cuda.synchronize()
     gc.disable()
     per = []
+    launches = 0
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
             flush()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            l0 = _lib.launch_count()
             e0.record()
             step()
             e1.record()
             e1.synchronize()
+            launches += _lib.launch_count() - l0 + dp.last_replayed  # eager + graph-replayed kernels
             per.append(e0.elapsed_time(e1))
     gc.enable()
     t_local = torch.tensor([sum(per)], dtype=torch.float64, device="cuda")
@@ -747,7 +750,7 @@ def run_sharded(args, world, rank, local, dist):
         "data": "synthetic", "config": cfgd, "iterations": it, "parity": parity,
         "shards": {"top_rows": int(len(sp.top_rows)), "load": [float(v) for v in sp.load],
                    "local_plan_s": t_plan},
-        "gpu_launches": None, "clocks": clk.summary(),
+        "gpu_launches": launches, "clocks": clk.summary(),
     }
     print(json.dumps(line))
     if dist:

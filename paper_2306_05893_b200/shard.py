@@ -666,6 +666,7 @@ class DistributedPcg:
         else:
             bd = b if L.is_tensor(b) else t.from_numpy(np.ascontiguousarray(b, dtype=np.float64)).cuda()
             L.check(self._lib.tsb_gather_rows(n, L.ptr(self.perm), L.ptr(bd), L.ptr(v["b"]), s), "gather")
+        l0, replays, captured = L.launch_count(), 0, 0
         v["r"].copy_(v["b"])
         v["x"].zero_()
         self._dot(v["b"], v["b"], 4)
@@ -685,10 +686,13 @@ class DistributedPcg:
             if use_graph:
                 key = (bnorm, tol, max_it)
                 if getattr(self, "_graph_key", None) != key:
+                    c0 = L.launch_count()
                     self._capture(bnorm, tol, max_it)
+                    captured = L.launch_count() - c0 - self._graph_kernels
                     self._graph_key = key
                 while True:
                     self._graph.replay()
+                    replays += 1
                     self.done_host.copy_(self.done, non_blocking=True)
                     t.cuda.current_stream().synchronize()
                     if int(self.done_host[0]):
@@ -706,6 +710,9 @@ class DistributedPcg:
         self._weighted_copy(v["x"], xw)
         self.allreduce(xw)
         L.check(self._lib.tsb_gather_rows(n, L.ptr(self.iperm), L.ptr(xw), L.ptr(x_out), s), "gather")
+        # libtsb kernels this solve ran: eager launches + the kernels of each graph replay
+        self.last_replayed = replays * getattr(self, "_graph_kernels", 0)
+        self.last_launches = L.launch_count() - l0 - captured + self.last_replayed
         return x_out, it, res, conv
 
     def _capture(self, bnorm, tol, max_it):
@@ -719,9 +726,11 @@ class DistributedPcg:
         t.cuda.current_stream().wait_stream(side)
         t.cuda.synchronize()
         self._graph = t.cuda.CUDAGraph()
+        k0 = self._L.launch_count()
         with t.cuda.graph(self._graph):
             for _ in range(self.GRAPH_ITERS):
                 self._iteration(bnorm, tol, max_it)
+        self._graph_kernels = self._L.launch_count() - k0  # libtsb kernels per replay
         t.cuda.synchronize()
         # capture does not execute: restore the state the warm-up pass advanced
         for dst, src in zip((self.done, self.it, self.res, self.sc,
