@@ -88,16 +88,18 @@ __device__ __forceinline__ void grid_sync(unsigned *bar) {
 }
 
 // Block partial -> part[kind][cta]; returns nothing (thread 0 writes).
+template <int NT>
 __device__ __forceinline__ void put_partial(double v, double *part, int kind, double *red) {
-    const double s = block_sum<kPcgBlock>(v, red);
+    const double s = block_sum<NT>(v, red);
     if (threadIdx.x == 0) part[kind * kMaxGrid + blockIdx.x] = s;
 }
 
 // Sum of all CTAs' partials in a fixed order (identical in every CTA).
+template <int NT>
 __device__ __forceinline__ double all_partials(const double *part, int kind, double *red, double *bc) {
     double acc = 0.0;
-    for (int i = threadIdx.x; i < (int)gridDim.x; i += kPcgBlock) acc += __ldcg(part + kind * kMaxGrid + i);
-    const double s = block_sum<kPcgBlock>(acc, red);
+    for (int i = threadIdx.x; i < (int)gridDim.x; i += NT) acc += __ldcg(part + kind * kMaxGrid + i);
+    const double s = block_sum<NT>(acc, red);
     if (threadIdx.x == 0) *bc = s;
     __syncthreads();
     const double out = *bc;
@@ -108,8 +110,11 @@ __device__ __forceinline__ double all_partials(const double *part, int kind, dou
 // MINB = resident CTAs per SM the register budget is sized for: LDL^T 2
 // (two 40 KB sweep stages per CTA in shared memory); Jacobi / identity 3 for small systems
 // (grid-barrier bound), 6 for large ones (the SpMV is gather-latency bound)
-template <int KIND, int MINB>
-__global__ void __launch_bounds__(kPcgBlock, MINB)
+// NT = threads per CTA: 256 with the sweep ring (the sweeps' warp roles); the
+// large Jacobi / identity solve runs the same warps per SM in fewer, larger
+// CTAs -- fewer arrivals per grid barrier, fewer partials per reduction.
+template <int KIND, int MINB, int NT = kPcgBlock>
+__global__ void __launch_bounds__(NT, MINB)
 pcg_persistent(PcgWork W, PcgArgs a, tsb_ldlt_desc D) {
     extern __shared__ __align__(128) double smem[];  // sweep staging (LDL^T)
     __shared__ double red[32];
@@ -117,7 +122,7 @@ pcg_persistent(PcgWork W, PcgArgs a, tsb_ldlt_desc D) {
     __shared__ SweepRing ring;
     const int tid = threadIdx.x;
     const int64_t n = W.n;
-    const int64_t gtid = (int64_t)blockIdx.x * kPcgBlock + tid, gstride = (int64_t)gridDim.x * kPcgBlock;
+    const int64_t gtid = (int64_t)blockIdx.x * NT + tid, gstride = (int64_t)gridDim.x * NT;
     const int lane8 = tid & 7;
     const unsigned gmask = 0xffu << ((tid & 31) & 24);
     const int64_t grp = gtid >> 3, ngrp = gstride >> 3;
@@ -169,11 +174,11 @@ pcg_persistent(PcgWork W, PcgArgs a, tsb_ldlt_desc D) {
             }
         }
     }
-    put_partial(bb, W.part, 0, red);
-    put_partial(rr, W.part, 1, red);
+    put_partial<NT>(bb, W.part, 0, red);
+    put_partial<NT>(rr, W.part, 1, red);
     grid_sync(W.bar);
-    const double bnorm = sqrt(all_partials(W.part, 0, red, &bc));
-    const double rr0 = all_partials(W.part, 1, red, &bc);
+    const double bnorm = sqrt(all_partials<NT>(W.part, 0, red, &bc));
+    const double rr0 = all_partials<NT>(W.part, 1, red, &bc);
     const int32_t status = *((volatile int32_t *)W.status);
     long long it = 0;
     double res = 0.0;
@@ -224,9 +229,9 @@ pcg_persistent(PcgWork W, PcgArgs a, tsb_ldlt_desc D) {
                 v += ri * zi;
             }
         }
-        put_partial(v, W.part, 2, red);
+        put_partial<NT>(v, W.part, 2, red);
         grid_sync(W.bar);
-        rz = all_partials(W.part, 2, red, &bc);
+        rz = all_partials<NT>(W.part, 2, red, &bc);
     }
     // ---- iterations (krylov.py:144-157) --------------------------------------
     long long ph[6] = {0, 0, 0, 0, 0, 0};
@@ -286,10 +291,10 @@ pcg_persistent(PcgWork W, PcgArgs a, tsb_ldlt_desc D) {
                 }
             }
         }
-        put_partial(v, W.part, 3, red);
+        put_partial<NT>(v, W.part, 3, red);
         lap(0);
         grid_sync(W.bar);
-        const double alpha = rz / all_partials(W.part, 3, red, &bc);
+        const double alpha = rz / all_partials<NT>(W.part, 3, red, &bc);
         lap(1);
         // P2: x, r updates, ||r||^2 (+ z, r.z for diagonal preconditioners)
         double vr = 0.0, vz = 0.0;
@@ -306,11 +311,11 @@ pcg_persistent(PcgWork W, PcgArgs a, tsb_ldlt_desc D) {
                 W.z[i] = ri;
             }
         }
-        put_partial(vr, W.part, 0, red);
-        if (KIND == TSB_PRECOND_JACOBI) put_partial(vz, W.part, 1, red);
+        put_partial<NT>(vr, W.part, 0, red);
+        if (KIND == TSB_PRECOND_JACOBI) put_partial<NT>(vz, W.part, 1, red);
         lap(2);
         grid_sync(W.bar);
-        const double rrn = all_partials(W.part, 0, red, &bc);
+        const double rrn = all_partials<NT>(W.part, 0, red, &bc);
         lap(3);
         ++it;
         res = sqrt(rrn) / bnorm;
@@ -323,7 +328,7 @@ pcg_persistent(PcgWork W, PcgArgs a, tsb_ldlt_desc D) {
         if (KIND == TSB_PRECOND_IDENTITY) {
             rzn = rrn;
         } else if (KIND == TSB_PRECOND_JACOBI) {
-            rzn = all_partials(W.part, 1, red, &bc);
+            rzn = all_partials<NT>(W.part, 1, red, &bc);
         } else {
             permute_r();
             lower_sweep_body<false>(D, lo_args, smem, ring);
@@ -332,9 +337,9 @@ pcg_persistent(PcgWork W, PcgArgs a, tsb_ldlt_desc D) {
             grid_sync(W.bar);
             double w2 = 0.0;
             for (int64_t i = gtid; i < n; i += gstride) w2 += __ldcg(W.r + i) * __ldcg(W.z + i);
-            put_partial(w2, W.part, 2, red);
+            put_partial<NT>(w2, W.part, 2, red);
             grid_sync(W.bar);
-            rzn = all_partials(W.part, 2, red, &bc);
+            rzn = all_partials<NT>(W.part, 2, red, &bc);
         }
         beta = rzn / rz;
         rz = rzn;
@@ -372,12 +377,12 @@ struct tsb_pcg {
 
 namespace tsb {
 
-template <int KIND, int MINB>
+template <int KIND, int MINB, int NT = kPcgBlock>
 static int occupancy_grid(size_t smem) {
-    auto k = pcg_persistent<KIND, MINB>;
+    auto k = pcg_persistent<KIND, MINB, NT>;
     allow_max_smem(k);
     int per_sm = 0, dev = 0, nsm = kNumSM;
-    TSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kPcgBlock, smem));
+    TSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, NT, smem));
     TSB_CUDA(cudaGetDevice(&dev));
     TSB_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
     if (per_sm < 1) throw Error(TSB_E_ARG, "pcg kernel does not fit on an SM");
@@ -389,13 +394,42 @@ static int occupancy_grid(size_t smem) {
     return g < kMaxGrid ? g : kMaxGrid;
 }
 
-template <int KIND, int MINB>
+template <int KIND, int MINB, int NT = kPcgBlock>
 static void launch(tsb_pcg *h, PcgArgs &a, tsb_ldlt_desc &D, int grid, size_t smem, cudaStream_t s) {
     if (KIND == TSB_PRECOND_LDLT) sync_pub_direct();
     void *args[] = {&h->W, &a, &D};
-    TSB_CUDA(cudaLaunchCooperativeKernel((const void *)pcg_persistent<KIND, MINB>, dim3(grid), dim3(kPcgBlock),
-                                         args, smem, s));
+    TSB_CUDA(cudaLaunchCooperativeKernel((const void *)pcg_persistent<KIND, MINB, NT>, dim3(grid), dim3(NT), args,
+                                         smem, s));
     count_launch();
+}
+
+// Large Jacobi / identity solves: 48 warps per SM as 6 x 256, 3 x 512 or
+// 2 x 768 threads (TSB_PCG_BIG_NT; the shape only changes barrier arrivals and
+// the partials' count).
+static int big_nt() {
+    static int nt = 0;
+    if (nt == 0) {
+        const char *e = getenv("TSB_PCG_BIG_NT");
+        const int v = e ? atoi(e) : 768;
+        nt = (v == 256 || v == 512 || v == 768) ? v : 768;
+    }
+    return nt;
+}
+template <int KIND>
+static int big_grid() {
+    switch (big_nt()) {
+        case 256: return occupancy_grid<KIND, 6, 256>(0);
+        case 512: return occupancy_grid<KIND, 3, 512>(0);
+        default: return occupancy_grid<KIND, 2, 768>(0);
+    }
+}
+template <int KIND>
+static void big_launch(tsb_pcg *h, PcgArgs &a, tsb_ldlt_desc &D, int grid, cudaStream_t s) {
+    switch (big_nt()) {
+        case 256: launch<KIND, 6, 256>(h, a, D, grid, 0, s); break;
+        case 512: launch<KIND, 3, 512>(h, a, D, grid, 0, s); break;
+        default: launch<KIND, 2, 768>(h, a, D, grid, 0, s); break;
+    }
 }
 
 }  // namespace tsb
@@ -433,9 +467,9 @@ extern "C" int tsb_pcg_create(int64_t n, tsb_pcg_t *out) {
         TSB_CUDA(cudaMemset(W.bar, 0, 256));
         TSB_CUDA(cudaMallocHost(&h->h_state, sizeof(PcgState)));
         h->big = n >= kFuseRows;
-        h->grid[TSB_PRECOND_IDENTITY] = h->big ? occupancy_grid<TSB_PRECOND_IDENTITY, 6>(0)
+        h->grid[TSB_PRECOND_IDENTITY] = h->big ? big_grid<TSB_PRECOND_IDENTITY>()
                                                : occupancy_grid<TSB_PRECOND_IDENTITY, 3>(0);
-        h->grid[TSB_PRECOND_JACOBI] = h->big ? occupancy_grid<TSB_PRECOND_JACOBI, 6>(0)
+        h->grid[TSB_PRECOND_JACOBI] = h->big ? big_grid<TSB_PRECOND_JACOBI>()
                                              : occupancy_grid<TSB_PRECOND_JACOBI, 3>(0);
         *out = h;
     });
@@ -501,12 +535,12 @@ extern "C" int tsb_pcg_solve(tsb_pcg_t h, int64_t nrows, const int32_t *d_row_pt
             launch<TSB_PRECOND_LDLT, 2>(h, a, D, h->grid[TSB_PRECOND_LDLT], sm, s);
         } else if (kind == TSB_PRECOND_JACOBI) {
             if (h->big)
-                launch<TSB_PRECOND_JACOBI, 6>(h, a, D, h->grid[TSB_PRECOND_JACOBI], 0, s);
+                big_launch<TSB_PRECOND_JACOBI>(h, a, D, h->grid[TSB_PRECOND_JACOBI], s);
             else
                 launch<TSB_PRECOND_JACOBI, 3>(h, a, D, h->grid[TSB_PRECOND_JACOBI], 0, s);
         } else {
             if (h->big)
-                launch<TSB_PRECOND_IDENTITY, 6>(h, a, D, h->grid[TSB_PRECOND_IDENTITY], 0, s);
+                big_launch<TSB_PRECOND_IDENTITY>(h, a, D, h->grid[TSB_PRECOND_IDENTITY], s);
             else
                 launch<TSB_PRECOND_IDENTITY, 3>(h, a, D, h->grid[TSB_PRECOND_IDENTITY], 0, s);
         }

@@ -2,7 +2,10 @@
 item, TMA groups per small-tile item): packs the bench workload's factors
 once per setting and times dev.run("apply") with CUDA events, L2 flushed.
 
-    python tools/item_tune.py [--workload cfg3] [--segs 1,2,4,8] [--groups 1,2,4]
+    python tools/item_tune.py [--workload cfg3] [--segs 1,2,4,8] [--groups 1,2,4] [--ratios 0,1]
+
+--ratios sweeps the lower input-mode threshold (K.GATHER_RATIO); the lower
+and upper sweeps are timed separately too.
 """
 import argparse
 import json
@@ -23,6 +26,7 @@ def main():
     ap.add_argument("--segs", default="1,2,4,8")
     ap.add_argument("--groups", default="1,2,4")
     ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--ratios", default="")
     args = ap.parse_args()
     import torch
 
@@ -32,25 +36,33 @@ def main():
     r = torch.randn(f.plan.n, dtype=torch.float64, device="cuda")
     z = torch.empty_like(r)
     out = []
-    for sg in map(int, args.segs.split(",")):
-        for gr in map(int, args.groups.split(",")):
-            K.SEGS_PER_ITEM, K.GROUPS_PER_ITEM = sg, min(gr, 4)  # overrides of item_granularity (csrc kGroupsPerItem)
-            dev = K.DevicePanels(f)
-            for _ in range(3):
-                dev.run("apply", r, z)
-            ts = []
-            for _ in range(args.reps):
-                flush()
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record()
-                dev.run("apply", r, z)
-                e1.record()
-                e1.synchronize()
-                ts.append(e0.elapsed_time(e1))
-            row = {"segs": sg, "groups": gr, "apply_ms": statistics.median(ts), "items": dev.n_items}
-            print(json.dumps(row), flush=True)
-            out.append(row)
-            del dev
+
+    def timed(dev, mode):
+        for _ in range(3):
+            dev.run(mode, r, z)
+        ts = []
+        for _ in range(args.reps):
+            flush()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            dev.run(mode, r, z)
+            e1.record()
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        return statistics.median(ts)
+
+    ratios = [float(v) for v in args.ratios.split(",")] if args.ratios else [None]
+    for ratio in ratios:
+        K.GATHER_RATIO = ratio
+        for sg in map(int, args.segs.split(",")):
+            for gr in map(int, args.groups.split(",")):
+                K.SEGS_PER_ITEM, K.GROUPS_PER_ITEM = sg, min(gr, 4)  # overrides of item_granularity (csrc kGroupsPerItem)
+                dev = K.DevicePanels(f)
+                row = {"segs": sg, "groups": gr, "ratio": ratio, "apply_ms": timed(dev, "apply"),
+                       "lower_ms": timed(dev, "lower"), "upper_ms": timed(dev, "upper"), "items": dev.n_items}
+                print(json.dumps(row), flush=True)
+                out.append(row)
+                del dev
     print(json.dumps({"workload": args.workload, "best": min(out, key=lambda x: x["apply_ms"])}))
 
 
