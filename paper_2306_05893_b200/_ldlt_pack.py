@@ -72,10 +72,12 @@ SEG_PAIRS = 80          # pairs per column segment of a large tile (80 * 32 * 16
 # item granularity by regime (tools/item_tune.py, B200): latency-bound factors
 # (stored lower tiles <= GATHER_BIG_BYTES) keep items short -- cfg2 apply
 # 0.168 ms at 2/2 vs 0.198 at 4/4 -- bandwidth-bound ones amortise the per-item
-# chain over more bytes -- cfg3 1.13 ms at 8/4 and 6/4 vs 1.16 at 4/4, 1.86 at 16/4
+# chain over more bytes -- cfg3 1.13 ms at 8/4 and 6/4 vs 1.16 at 4/4, 1.86 at 16/4;
+# 8/8 1.1316 vs 8/4 1.1377 (22,658 vs 25,270 lower items)
 SEGS_PER_ITEM = int(os.environ["TSB_SEGS_PER_ITEM"]) if "TSB_SEGS_PER_ITEM" in os.environ else None
-GROUPS_PER_ITEM = min(4, int(os.environ["TSB_GROUPS_PER_ITEM"])) if "TSB_GROUPS_PER_ITEM" in os.environ else None
-SEGS_SMALL, GROUPS_SMALL, SEGS_BIG, GROUPS_BIG = 2, 2, 8, 4
+MAX_GROUPS = 8          # csrc kGroupsPerItem (mailbox capacity: MAX_GROUPS x WARPS tiles)
+GROUPS_PER_ITEM = min(MAX_GROUPS, int(os.environ["TSB_GROUPS_PER_ITEM"])) if "TSB_GROUPS_PER_ITEM" in os.environ else None
+SEGS_SMALL, GROUPS_SMALL, SEGS_BIG, GROUPS_BIG = 2, 2, 8, 8
 WARPS = 7               # consumer warps per CTA (csrc kWarps): one small tile each
 MERGE_ROWS = 0          # default subtree amalgamation (rows); 0 = off
 CB_CAP = 1024           # contributions staged per piece when a block's items sum them (csrc max_cb)

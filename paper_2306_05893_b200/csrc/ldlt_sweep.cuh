@@ -34,7 +34,7 @@ constexpr int kStage = 5120;            // doubles per ring stage (40 KB; 2 stag
 constexpr int kStages = 2;
 constexpr int kSegPairs = 80;           // pairs per column segment of a large tile (40 KB)
 constexpr int kMaxV = 8192;             // largest item window staged in shared memory
-constexpr int kGroupsPerItem = 4;       // TMA groups (<= kWarps small tiles, <= 40 KB each) per small-tile item
+constexpr int kGroupsPerItem = 8;       // TMA groups (<= kWarps small tiles, <= 40 KB each) per small-tile item (max)
 constexpr int kMailTiles = kGroupsPerItem * kWarps;
 constexpr int kMaxItemRows = kMailTiles * kTile;
 

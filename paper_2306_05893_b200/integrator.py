@@ -284,11 +284,23 @@ class BackwardEulerIntegrator:
         ev = getattr(self, "_ev", None)
         if ev is None:
             ev = self._ev = [t.cuda.Event(enable_timing=True) for _ in range(3)]
+        ent = self._out_buffer(n) if host else None
+        try:
+            return self._step_body(state, solve, host, n, h, stage, ent, x0, v0, fe_state, dev_solve, ev)
+        except BaseException:
+            if ent is not None:
+                _release_buffer(ent)  # no result views were handed out
+            raise
+
+    def _step_body(self, state, solve, host, n, h, stage, ent, x0, v0, fe_state, dev_solve, ev):
+        t = _lib.torch()
+        cfg = self.config
         assembly_time = solve_time = 0.0
         rebuilt_any = False
         x_tr, v_tr = x0, v0
         fixed = self._plan.fixed_dof if self._plan is not None else None
-        for _ in range(cfg.newton_iterations):
+        side = None
+        for it_newton in range(cfg.newton_iterations):
             ev[0].record()
             d_out = stage["d_out"] if host else None
             a, b, f_int, f_ext, rebuilt = self._assemble_device(
@@ -296,6 +308,12 @@ class BackwardEulerIntegrator:
                                                                   d_out[5 * n:]))
             fixed = self._plan.fixed_dof
             ev[1].record()
+            if host and it_newton == cfg.newton_iterations - 1:
+                # b, f_int, f_ext are final: their D2H runs on a side stream under the solve
+                side = self._d2h_stream()
+                side.wait_event(ev[1])
+                with t.cuda.stream(side):
+                    ent[0][3 * n:].copy_(d_out[3 * n:], non_blocking=True)
             rebuilt_any = rebuilt_any or rebuilt
             accel, report = solve(a, b if dev_solve else b.cpu().numpy())
             ev[2].record()
@@ -311,7 +329,10 @@ class BackwardEulerIntegrator:
             P = _lib.ptr
             _lib.check(_lib.load().tsb_advance(n, P(d_acc), P(v0), P(x0), P(fixed), h, P(acc), P(v1),
                                                P(x1), P(self._plan.flags), _lib.stream_ptr()), "advance")
-            flags = self._plan.flags.cpu()  # one readback: model + accel flags
+            if host and it_newton == cfg.newton_iterations - 1:  # x1, v1, acc with the same wait
+                ent[0][:3 * n].copy_(d_out[:3 * n], non_blocking=True)
+                t.cuda.current_stream().wait_stream(side)
+            flags = self._plan.flags.cpu()  # one readback: model + accel flags (and the results' D2H)
             ev[2].synchronize()
             assembly_time += ev[0].elapsed_time(ev[1]) * 1e-3
             solve_time += ev[1].elapsed_time(ev[2]) * 1e-3
@@ -324,9 +345,6 @@ class BackwardEulerIntegrator:
                 raise StepError("solver produced non-finite accelerations", report)
             x_tr, v_tr = x1, v1
         if host:
-            ent = self._out_buffer(n)
-            ent[0].copy_(stage["d_out"], non_blocking=True)
-            t.cuda.current_stream().synchronize()
             o = ent[0].numpy()  # the six results are views of this pinned buffer, which is
             weakref.finalize(o, _release_buffer, ent)  # reused only once every view is gone
             part = lambda k: o[k * n:(k + 1) * n]  # noqa: E731
@@ -353,6 +371,12 @@ class BackwardEulerIntegrator:
                   "d_out": t.empty(6 * n, dtype=t.float64, device="cuda")}
             self._stage = st
             self._out_pool = []
+        return st
+
+    def _d2h_stream(self):
+        st = getattr(self, "_side", None)
+        if st is None:
+            st = self._side = _lib.torch().cuda.Stream()
         return st
 
     def _out_buffer(self, n):

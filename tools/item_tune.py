@@ -56,7 +56,7 @@ def main():
         K.GATHER_RATIO = ratio
         for sg in map(int, args.segs.split(",")):
             for gr in map(int, args.groups.split(",")):
-                K.SEGS_PER_ITEM, K.GROUPS_PER_ITEM = sg, min(gr, 4)  # overrides of item_granularity (csrc kGroupsPerItem)
+                K.SEGS_PER_ITEM, K.GROUPS_PER_ITEM = sg, min(gr, K.MAX_GROUPS)  # overrides of item_granularity (csrc kGroupsPerItem)
                 dev = K.DevicePanels(f)
                 row = {"segs": sg, "groups": gr, "ratio": ratio, "apply_ms": timed(dev, "apply"),
                        "lower_ms": timed(dev, "lower"), "upper_ms": timed(dev, "upper"), "items": dev.n_items}
