@@ -203,7 +203,9 @@ typedef struct tsb_ldlt_block {
                                        1 every item sums the contributions itself,
                                        2 nfin finaliser items form x_b once        */
     int32_t ncb;                    /* contributions into the block's rows         */
-    int32_t nfin, pad_;             /* finaliser items (mode 2)                     */
+    int32_t nfin;                   /* finaliser items (mode 2)                     */
+    int32_t nu_parent;              /* n_u of the parent (0 at a root): the upper
+                                       items' dependency target                    */
     int64_t anc_off;                /* offset of the block's anc rows in d_anc      */
     int64_t cb_off;                 /* first cbuf slot of the block's rows          */
 } tsb_ldlt_block;

@@ -93,7 +93,7 @@ GATHER_BIG_BYTES = 512 << 20  # stored lower tiles above this: bandwidth-bound r
 BLOCK_DTYPE = np.dtype([
     ("start", "<i4"), ("m", "<i4"), ("na", "<i4"), ("parent", "<i4"),
     ("target_l", "<i4"), ("n_u", "<i4"), ("mode", "<i4"), ("ncb", "<i4"),
-    ("nfin", "<i4"), ("pad_", "<i4"), ("anc_off", "<i8"), ("cb_off", "<i8"),
+    ("nfin", "<i4"), ("nu_parent", "<i4"), ("anc_off", "<i8"), ("cb_off", "<i8"),
 ])
 assert BLOCK_DTYPE.itemsize == 56
 FIN_CONTRIB = 4096      # contributions per finaliser item of a mode-2 block
@@ -621,6 +621,7 @@ def pack(factors, subset=None, sink=None, alloc=None):
     blocks["parent"] = parent
     blocks["target_l"] = target_l
     blocks["n_u"] = n_u
+    blocks["nu_parent"] = np.where(np.asarray(parent) >= 0, np.asarray(n_u)[np.maximum(np.asarray(parent), 0)], 0)
     blocks["mode"] = mode
     blocks["nfin"] = nfin
     blocks["ncb"] = blk_contrib

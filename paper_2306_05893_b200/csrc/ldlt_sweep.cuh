@@ -157,7 +157,8 @@ struct SweepArgs {
 // block, its tiles (small groups: up to kWarps; chunks: the tile) and its
 // vector window.
 struct MailEntry {
-    int32_t iid, w0, w1, pad_;
+    int32_t iid, w0, w1, dep_target;
+    const int32_t *dep;  // counter the item waits for (>= dep_target) or nullptr
     Item it;
     tsb_ldlt_block B;
     tsb_ldlt_tile T[kMailTiles];
@@ -270,19 +271,22 @@ __device__ __forceinline__ void stage_copy(double *dst, const double *src, int n
 // Strided per-consumer-thread loops with their global loads issued in batches
 // of 4 (the loads of one batch are independent; results land in shared memory).
 // dst[j] = f(j) for j = tid, tid + 224, ... < n
-template <class F>
+// j = tid, tid + NT, ... < n with U loads in flight per thread (consumer
+// threads [0, NT) take part)
+template <class F, int NT = kCThreads>
 __device__ __forceinline__ void batched(int n, F f) {
     constexpr int U = 4;
-    for (int j0 = threadIdx.x; j0 < n; j0 += U * kCThreads) {
+    if ((int)threadIdx.x >= NT) return;
+    for (int j0 = threadIdx.x; j0 < n; j0 += U * NT) {
         double t[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const int j = j0 + u * kCThreads;
+            const int j = j0 + u * NT;
             if (j < n) t[u] = f.load(j);
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const int j = j0 + u * kCThreads;
+            const int j = j0 + u * NT;
             if (j < n) f.store(j, t[u]);
         }
     }
@@ -373,9 +377,10 @@ __device__ __forceinline__ void wait_serving(SweepRing &R, uint64_t *bar, uint32
         if (live) live = serve_pubs(R, p);
 }
 
-__device__ __forceinline__ void sweep_producer(SweepRing &R, int32_t *ticket, int64_t n_items, const Item *items,
-                                               const tsb_ldlt_block *blocks, const tsb_ldlt_tile *tiles,
-                                               const double *base, double *stage, bool upper) {
+__device__ __forceinline__ void sweep_producer(SweepRing &R, const tsb_ldlt_desc &D, int32_t *ticket,
+                                               int64_t n_items, const Item *items, const tsb_ldlt_block *blocks,
+                                               const tsb_ldlt_tile *tiles, const double *base, double *stage,
+                                               bool upper) {
     if ((threadIdx.x & 31) != 0) return;
     uint32_t q = R.q_prod, k = R.k_prod, p = R.p_prod;
     bool live = true;
@@ -398,6 +403,23 @@ __device__ __forceinline__ void sweep_producer(SweepRing &R, int32_t *ticket, in
                 for (int t = it.t0; t < it.t1; ++t) M.T[t - it.t0] = t == it.t0 ? T0 : tiles[t];
             }
             if (it.seg >= 0) item_window(it, M.T, B.m + (upper ? B.na : 0), M.w0, M.w1);
+            // the item's dependency (the counter its consumers would spin on)
+            const int32_t *dep = nullptr;
+            int32_t tgt = 0;
+            if (upper) {  // -z_anc in the window: the parent's items (a parent outside the handle is solved before)
+                if (B.parent >= 0 && M.w1 > B.m) {
+                    dep = D.d_done_u + B.parent;
+                    tgt = B.nu_parent;
+                }
+            } else if (it.seg < 0 || B.mode == 1) {  // finaliser / items summing contributions: the children
+                dep = D.d_cnt_l + it.block;
+                tgt = B.target_l;
+            } else if (B.mode == 2) {  // x_b formed by the block's finalisers
+                dep = D.d_ready_l + it.block;
+                tgt = B.nfin;
+            }
+            M.dep = dep;
+            M.dep_target = tgt;
         } else if (k >= 2) {
             wait_serving(R, &R.taken[e], ((k >> 1) - 1) & 1u, p, live);
         }
@@ -431,6 +453,16 @@ __device__ __forceinline__ void sweep_producer(SweepRing &R, int32_t *ticket, in
     R.q_prod = q;
     R.k_prod = k;
     R.p_prod = p;
+}
+
+// Consumers: the item's dependency (computed by the producer into the mailbox)
+// is waited on by consumer thread kDepThread alone while the first kLoaders
+// threads fetch the item's input window -- the acquire round trip overlaps
+// those loads instead of following them.
+constexpr int kDepThread = kCThreads - 32;  // lane 0 of the last consumer warp (a warp of its own:
+constexpr int kLoaders = kCThreads - 32;    // its spin does not serialise a loading warp)
+__device__ __forceinline__ void dep_spin(const MailEntry &M) {
+    if (threadIdx.x == kDepThread && M.dep != nullptr) spin_until_geq(M.dep, M.dep_target);
 }
 
 // ---- consumer side ---------------------------------------------------------
@@ -679,7 +711,7 @@ __device__ __forceinline__ void lower_sweep_body(const tsb_ldlt_desc &D, const S
     double *stage = smem;
     const Item *items = reinterpret_cast<const Item *>(D.d_items_lower);
     if ((threadIdx.x >> 5) == kProducerWarp) {
-        sweep_producer(R, D.d_ctl, D.n_items_lower, items, D.d_blocks, D.d_tiles_lower, D.d_g, stage, false);
+        sweep_producer(R, D, D.d_ctl, D.n_items_lower, items, D.d_blocks, D.d_tiles_lower, D.d_g, stage, false);
         lower_exit(D);
         return;
     }
@@ -712,7 +744,7 @@ __device__ __forceinline__ void lower_sweep_body(const tsb_ldlt_desc &D, const S
             // [t0, t1), once the children are done; contributions staged piece
             // by piece in the item's ring stage, one thread per row sums in order
             double *scratch = ring_wait(R, q, stage);
-            if (tid == 0) spin_until_geq(D.d_cnt_l + it.block, B.target_l);
+            dep_spin(M);
             csync();
             trace(tbuf, iid, 1);
             int i0 = it.t0;
@@ -763,23 +795,20 @@ __device__ __forceinline__ void lower_sweep_body(const tsb_ldlt_desc &D, const S
                 __device__ double load(int j) const { return lower_input(A, s + j, r); }
                 __device__ void store(int j, double v) const { xs[j] = v; }
             };
+            dep_spin(M);  // the dependency thread, meanwhile the others fetch:
             if (B.mode != 2)  // mode 2: x_b comes from the finalisers
-                for (int j = 0; j < nr; ++j) batched(nw, In{A, xs + j * xstride, s + w0, j});
+                for (int j = 0; j < nr; ++j) batched<In, kLoaders>(nw, In{A, xs + j * xstride, s + w0, j});
         }
         if (tid < nr) xs[tid * xstride + nw] = 0.0;  // column pad of odd-width tiles
         const tsb_ldlt_tile &Tf = M.T[0], &Tb = M.T[it.seg ? 0 : it.t1 - 1 - it.t0];
         const int r_hi = Tb.row0 + Tb.nrows, mr0 = max(Tf.row0, m);
-        for (int j = mr0 + tid; j < r_hi; j += kCThreads) dsts[j - mr0] = __ldg(D.d_cslot + B.anc_off + (j - m));
-        int64_t cb0 = 0;
-        if (B.mode == 1) {
-            cb0 = __ldg(D.d_cin_ptr + s + w0);
-            for (int j = tid; j <= nw; j += kCThreads) offs[j] = (int32_t)(__ldg(D.d_cin_ptr + s + w0 + j) - cb0);
+        const int64_t cb0 = B.mode == 1 ? __ldg(D.d_cin_ptr + s + w0) : 0;
+        if (tid < kLoaders) {
+            for (int j = mr0 + tid; j < r_hi; j += kLoaders) dsts[j - mr0] = __ldg(D.d_cslot + B.anc_off + (j - m));
+            if (B.mode == 1)
+                for (int j = tid; j <= nw; j += kLoaders) offs[j] = (int32_t)(__ldg(D.d_cin_ptr + s + w0 + j) - cb0);
         }
-        if (tid == 0) {
-            if (B.mode == 1) spin_until_geq(D.d_cnt_l + it.block, B.target_l);
-            else if (B.mode == 2) spin_until_geq(D.d_ready_l + it.block, B.nfin);
-        }
-        csync();
+        csync();  // dependency met; the window's staged input / offsets / destinations
         trace(tbuf, iid, 1);
         // x_b = input - (contributions of the descendants) over the window
         if (B.mode == 1) {  // rows in pieces whose contributions fit the buffer, per right-hand side
@@ -865,7 +894,7 @@ __device__ __forceinline__ void upper_sweep_body(const tsb_ldlt_desc &D, const S
     double *stage = smem;
     const Item *items = reinterpret_cast<const Item *>(D.d_items_upper);
     if ((threadIdx.x >> 5) == kProducerWarp) {
-        sweep_producer(R, D.d_ctl + 2, D.n_items_upper, items, D.d_blocks, D.d_tiles_upper, D.d_gt, stage, true);
+        sweep_producer(R, D, D.d_ctl + 2, D.n_items_upper, items, D.d_blocks, D.d_tiles_upper, D.d_gt, stage, true);
         upper_exit(D);
         return;
     }
@@ -889,17 +918,18 @@ __device__ __forceinline__ void upper_sweep_body(const tsb_ldlt_desc &D, const S
         const int m = B.m, s = B.start, na = B.na;
         const int w0 = M.w0, w1 = M.w1;
         const int nw = w1 - w0;
-        for (int t = w0 + tid; t < min(w1, m); t += kCThreads) {  // w_b: produced before this sweep
-            double w = __ldcg(A.in + s + t);
-            if (A.dscale) w = w / A.dscale[s + t];
-            v[t - w0] = w;
-        }
+        dep_spin(M);  // -z_anc in the window: the parent's items; meanwhile the others fetch:
         const int k0 = max(w0, m) - m, k1 = w1 - m;  // ancestor entries in the window
-        for (int kk = k0 + tid; kk < k1; kk += kCThreads)  // rows parked in v until the wait is over
-            v[m + kk - w0] = __longlong_as_double((long long)__ldg(D.d_anc + B.anc_off + kk));
+        if (tid < kLoaders) {
+            for (int t = w0 + tid; t < min(w1, m); t += kLoaders) {  // w_b: produced before this sweep
+                double w = __ldcg(A.in + s + t);
+                if (A.dscale) w = w / A.dscale[s + t];
+                v[t - w0] = w;
+            }
+            for (int kk = k0 + tid; kk < k1; kk += kLoaders)  // rows parked in v until the wait is over
+                v[m + kk - w0] = __longlong_as_double((long long)__ldg(D.d_anc + B.anc_off + kk));
+        }
         if (tid == 0) v[nw] = 0.0;  // column pad of odd-width tiles
-        if (k1 > k0 && B.parent >= 0 && tid == 0)  // parent outside the handle (shard): solved before
-            spin_until_geq(D.d_done_u + B.parent, D.d_blocks[B.parent].n_u);
         csync();
         trace(tbuf, iid, 1);
         if (k1 > k0) {
