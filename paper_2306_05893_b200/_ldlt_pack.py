@@ -78,6 +78,7 @@ SEGS_PER_ITEM = int(os.environ["TSB_SEGS_PER_ITEM"]) if "TSB_SEGS_PER_ITEM" in o
 MAX_GROUPS = 8          # csrc kGroupsPerItem (mailbox capacity: MAX_GROUPS x WARPS tiles)
 GROUPS_PER_ITEM = min(MAX_GROUPS, int(os.environ["TSB_GROUPS_PER_ITEM"])) if "TSB_GROUPS_PER_ITEM" in os.environ else None
 SEGS_SMALL, GROUPS_SMALL, SEGS_BIG, GROUPS_BIG = 2, 2, 8, 8
+SEGS_LOWER = int(os.environ["TSB_SEGS_LOWER"]) if "TSB_SEGS_LOWER" in os.environ else None
 WARPS = 7               # consumer warps per CTA (csrc kWarps): one small tile each
 MERGE_ROWS = 0          # default subtree amalgamation (rows); 0 = off
 CB_CAP = 1024           # contributions staged per piece when a block's items sum them (csrc max_cb)
@@ -518,6 +519,7 @@ def pack(factors, subset=None, sink=None, alloc=None):
         finally:
             small_limiter.restore_original_limits()
     segs, groups_per_item = item_granularity(pos[False] * 8)
+    segs_l = SEGS_LOWER if SEGS_LOWER is not None else segs  # tuning override for the lower sweep alone
     tables = {}
     npart = {}
     for up in (False, True):
@@ -526,7 +528,7 @@ def pack(factors, subset=None, sink=None, alloc=None):
             arr = np.array(tl_rows[up], dtype=np.int64)
             t["off"], t["tl"], t["np"], t["row0"], t["nrows"] = arr.T
         big = t["np"].astype(np.int64) * TILE * 16 > ITEM_BYTES
-        t["nseg"] = np.where(big, [_nchunks(v, segs) for v in t["np"]], 0)  # chunk items (partial slots) per tile
+        t["nseg"] = np.where(big, [_nchunks(v, segs if up else segs_l) for v in t["np"]], 0)  # chunk items per tile
         part = np.zeros(len(t) + 1, dtype=np.int64)
         np.cumsum(t["nseg"], out=part[1:])
         t["part"] = part[:-1]
@@ -546,7 +548,8 @@ def pack(factors, subset=None, sink=None, alloc=None):
     ext_rows = np.unique(anc_all[owner[anc_all] < 0]) if len(anc_all) else np.zeros(0, dtype=np.int64)
 
     # ---------------- items + lower input modes ----------------
-    items = {up: [_items(blk_tiles[up][i][1], blk_tiles[up][i][0], segs, groups_per_item) for i in range(nb)]
+    items = {up: [_items(blk_tiles[up][i][1], blk_tiles[up][i][0], segs if up else segs_l, groups_per_item)
+                  for i in range(nb)]
              for up in (False, True)}
     nl = np.array([len(x) for x in items[False]], dtype=np.int64)
     n_u = np.array([len(x) for x in items[True]], dtype=np.int64)
