@@ -28,9 +28,12 @@ world_size > 1 tests (gloo); the device loop is `DistributedPcg`.
 
 from __future__ import annotations
 
+import logging
 from dataclasses import dataclass
 
 import numpy as np
+
+logger = logging.getLogger(__name__)
 
 
 def block_etree(factors):
@@ -635,6 +638,8 @@ class DistributedPcg:
     def _graph_ok(self):
         """CUDA-graph replay needs capturable exchanges: our peer kernels, NCCL,
         or none (one rank); a gloo process group runs the iterations eagerly."""
+        if getattr(self, "_graph_failed", False):
+            return False
         if self.world == 1 or self.peer is not None:
             return True
         import torch.distributed as dist
@@ -687,9 +692,16 @@ class DistributedPcg:
                 key = (bnorm, tol, max_it)
                 if getattr(self, "_graph_key", None) != key:
                     c0 = L.launch_count()
-                    self._capture(bnorm, tol, max_it)
-                    captured = L.launch_count() - c0 - self._graph_kernels
-                    self._graph_key = key
+                    try:
+                        self._capture(bnorm, tol, max_it)
+                    except RuntimeError as e:  # an exchange that cannot be captured: iterate eagerly
+                        logger.warning("sharded PCG: CUDA-graph capture failed (%s); eager iterations", e)
+                        self._graph_failed = True
+                        use_graph = False
+                    else:
+                        captured = L.launch_count() - c0 - self._graph_kernels
+                        self._graph_key = key
+            if use_graph:
                 while True:
                     self._graph.replay()
                     replays += 1
@@ -727,15 +739,17 @@ class DistributedPcg:
         t.cuda.synchronize()
         self._graph = t.cuda.CUDAGraph()
         k0 = self._L.launch_count()
-        with t.cuda.graph(self._graph):
-            for _ in range(self.GRAPH_ITERS):
-                self._iteration(bnorm, tol, max_it)
-        self._graph_kernels = self._L.launch_count() - k0  # libtsb kernels per replay
-        t.cuda.synchronize()
-        # capture does not execute: restore the state the warm-up pass advanced
-        for dst, src in zip((self.done, self.it, self.res, self.sc,
-                             *(self.v[k] for k in ("x", "r", "z", "p"))), saved):
-            dst.copy_(src)
+        try:
+            with t.cuda.graph(self._graph):
+                for _ in range(self.GRAPH_ITERS):
+                    self._iteration(bnorm, tol, max_it)
+            self._graph_kernels = self._L.launch_count() - k0  # libtsb kernels per replay
+        finally:
+            t.cuda.synchronize()
+            # capture does not execute: restore the state the warm-up pass advanced
+            for dst, src in zip((self.done, self.it, self.res, self.sc,
+                                 *(self.v[k] for k in ("x", "r", "z", "p"))), saved):
+                dst.copy_(src)
 
     def _weighted_copy(self, x, out):
         """out = x on the rows this rank contributes (owned, top on rank 0), else 0."""
