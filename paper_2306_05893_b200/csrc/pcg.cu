@@ -522,8 +522,9 @@ extern "C" int tsb_pcg_solve(tsb_pcg_t h, int64_t nrows, const int32_t *d_row_pt
         TSB_CUDA(cudaMemsetAsync(W.status, 0, 8, s));
         TSB_CUDA(cudaMemsetAsync(W.status + 2, 0xff, 8, s));
         // small systems are barrier-latency bound, large ones gather bound
-        PcgArgs a{d_row_ptr, d_col_ind, d_values, d_b, d_x0, d_inv_diag, d_x, tol, (long long)max_iterations,
-                  nrows < kFuseRows ? 1 : 0};
+        static const int fuse_env = getenv("TSB_PCG_FUSE_P") ? atoi(getenv("TSB_PCG_FUSE_P")) : -1;  // A/B switch
+        const int fuse = fuse_env >= 0 ? fuse_env : (nrows < kFuseRows ? 1 : 0);
+        PcgArgs a{d_row_ptr, d_col_ind, d_values, d_b, d_x0, d_inv_diag, d_x, tol, (long long)max_iterations, fuse};
         tsb_ldlt_desc D{};
         if (kind == TSB_PRECOND_LDLT) {
             D = ldlt_desc(ldlt);
