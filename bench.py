@@ -327,13 +327,20 @@ def time_async_device(W, steps, flush):
 
 
 def time_e2e(W, mode, steps):
-    """Same step through the reference-facing API with HOST (NumPy) state:
-    H2D of x, v, f_ext and D2H of the step's results inside the timed region."""
+    """Same step through the reference-facing API with HOST (NumPy) state in
+    pinned memory: H2D of x, v, f_ext and D2H of the step's results inside the
+    timed region."""
     import torch
     from paper_2306_05893_b200.integrator import SimState
 
-    st = W["state"].to_host()
-    host = SimState(st.positions, st.velocities, st.accelerations, st.f_int, st.f_ext, st.time)
+    st = W["state"]
+
+    def pinned(a):  # the step's inputs live in pinned host memory (straight DMA, as a time loop's results do)
+        t = a.detach().cpu() if torch.is_tensor(a) else torch.from_numpy(np.ascontiguousarray(a))
+        return t.pin_memory().numpy()
+
+    host = SimState(pinned(st.positions), pinned(st.velocities), pinned(st.accelerations), pinned(st.f_int),
+                    pinned(st.f_ext), st.time)
     solve = W["solvers"][mode]
     for _ in range(2):
         W["integ"].compute_step(host, solve)
