@@ -558,6 +558,15 @@ __device__ __forceinline__ void item_gemv(SweepRing &R, uint32_t &q, const Item 
     }
     red[warp * 32 + lane] = acc;
     csync();
+    if (T.nseg == 1) {  // the whole tile in this item: emit without the partials' round trip
+        if (threadIdx.x < 32) {
+            double a = 0.0;
+#pragma unroll
+            for (int w = 0; w < kWarps; ++w) a += red[w * 32 + threadIdx.x];
+            if ((int)threadIdx.x < T.nrows) emit(T.row0 + threadIdx.x, 0.0 + a);  // = the one-chunk sum below
+        }
+        return;
+    }
     if (threadIdx.x < 32) {
         double a = 0.0;
 #pragma unroll
@@ -676,6 +685,16 @@ __device__ __forceinline__ void item_gemv_multi(SweepRing &R, uint32_t &q, const
     }
     for (int j = 0; j < nr; ++j) red[(j * kWarps + warp) * 32 + lane] = acc[j];
     csync();
+    if (T.nseg == 1) {  // whole tile: emit directly (as item_gemv)
+        for (int idx = threadIdx.x; idx < 32 * nr; idx += kCThreads) {
+            const int j = idx >> 5, l = idx & 31;
+            double a = 0.0;
+#pragma unroll
+            for (int w = 0; w < kWarps; ++w) a += red[(j * kWarps + w) * 32 + l];
+            if (l < T.nrows) emit(T.row0 + l, j, 0.0 + a);
+        }
+        return;
+    }
     for (int idx = threadIdx.x; idx < 32 * nr; idx += kCThreads) {
         const int j = idx >> 5, l = idx & 31;
         double a = 0.0;
