@@ -79,7 +79,12 @@ MAX_GROUPS = 8          # csrc kGroupsPerItem (mailbox capacity: MAX_GROUPS x WA
 GROUPS_PER_ITEM = min(MAX_GROUPS, int(os.environ["TSB_GROUPS_PER_ITEM"])) if "TSB_GROUPS_PER_ITEM" in os.environ else None
 SEGS_SMALL, GROUPS_SMALL, SEGS_BIG, GROUPS_BIG = 2, 2, 8, 8
 SEGS_LOWER = int(os.environ["TSB_SEGS_LOWER"]) if "TSB_SEGS_LOWER" in os.environ else None
+WHOLE = 1 << 20         # Item.seg of a whole-tiles item (csrc kWhole)
+# one-chunk large tiles of a block grouped into whole-tiles items (no partial
+# slots, one dependency wait and publication for several tiles)
+WHOLE_ITEMS = os.environ.get("TSB_WHOLE_ITEMS", "1") != "0"
 WARPS = 7               # consumer warps per CTA (csrc kWarps): one small tile each
+MAIL_TILES = MAX_GROUPS * WARPS  # tiles one mailbox entry holds (csrc kMailTiles)
 MERGE_ROWS = 0          # default subtree amalgamation (rows); 0 = off
 CB_CAP = 1024           # contributions staged per piece when a block's items sum them (csrc max_cb)
 # lower input mode: a block's items sum their contributions themselves while the
@@ -283,14 +288,28 @@ def amalgamate(factors, max_rows: int):
 
 def _items(tiles_of_block, first_tile, segs, groups_per_item):
     """Group a block's tiles into items -> list of (t0, t1, seg) in global tile ids
-    (seg = 0: small tiles [t0, t1); seg = c + 1: chunk c of large tile t0, i.e.
-    its column segments [c t1, c t1 + t1), t1 = segs)."""
+    (seg = 0: small tiles [t0, t1); seg = WHOLE: whole large tiles [t0, t1) of
+    <= segs segments in all; seg = c + 1: chunk c of large tile t0, i.e. its
+    column segments [c t1, c t1 + t1), t1 = segs)."""
     out = []
     k = 0
     nt = len(tiles_of_block)
+
+    def nseg(k_):
+        return (int(tiles_of_block[k_][1]) + SEG_PAIRS - 1) // SEG_PAIRS
+
     while k < nt:
         npair = tiles_of_block[k][1]
         if npair * TILE * 16 > ITEM_BYTES:
+            if WHOLE_ITEMS and nseg(k) <= segs:  # consecutive one-chunk tiles: one item
+                k1, tot = k, 0
+                while (k1 < nt and k1 - k < MAIL_TILES and tiles_of_block[k1][1] * TILE * 16 > ITEM_BYTES
+                       and tot + nseg(k1) <= segs):
+                    tot += nseg(k1)
+                    k1 += 1
+                out.append((first_tile + k, first_tile + k1, WHOLE))
+                k = k1
+                continue
             for c in range(_nchunks(npair, segs)):
                 out.append((first_tile + k, segs, c + 1))
             k += 1
@@ -338,7 +357,7 @@ SCHED_WORKERS = 296     # resident CTAs the list schedule assumes (148 SMs x 2)
 
 def _window(T, lim, it):
     """v-columns [w0, w1) an item reads (csrc item_window); T = the sweep's tile table."""
-    if it[2] > 0:
+    if 0 < it[2] < WHOLE:
         p0, p1 = _chunk_pairs(T["np"][it[0]], it)
         w0 = int(T["tl"][it[0]]) + 2 * p0
         return w0, min(int(T["tl"][it[0]]) + 2 * p1, lim)
@@ -578,7 +597,7 @@ def pack(factors, subset=None, sink=None, alloc=None):
     def cost(up, it):  # us: item latency + streaming at ~24 GB/s per CTA (HBM shared by 296 CTAs)
         if it[2] < 0:
             return 2.5
-        if it[2] > 0:
+        if 0 < it[2] < WHOLE:
             p0, p1 = _chunk_pairs(tables[up]["np"][it[0]], it)
             return 3.0 + (p1 - p0) * TILE * 16 / 24e3
         return 3.0 + int(tables[up]["np"][it[0]:it[1]].sum()) * TILE * 16 / 24e3

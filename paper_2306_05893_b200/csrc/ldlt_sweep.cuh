@@ -38,6 +38,11 @@ constexpr int kGroupsPerItem = 8;       // TMA groups (<= kWarps small tiles, <=
 constexpr int kMailTiles = kGroupsPerItem * kWarps;
 constexpr int kMaxItemRows = kMailTiles * kTile;
 
+constexpr int kWhole = 1 << 20;  // Item.seg of a whole-tiles item (see below)
+
+// seg = kWhole: whole large tiles [t0, t1), each one chunk (<= t1 - t0 <= kMailTiles
+// tiles, their segments streamed one TMA each, every tile's rows emitted from the
+// warp reduction -- no partial slots);
 // seg = 0: small tiles [t0, t1), streamed as up to kGroupsPerItem TMA groups
 // (greedy: <= kWarps tiles and <= 40 KB per group); seg = c + 1 (chunk item of a large
 // tile): column segments [c*t1, min(c*t1 + t1, nsegs)) of tile t0, one TMA
@@ -339,8 +344,9 @@ __device__ __forceinline__ int group_end(const tsb_ldlt_tile *T, int nt, int g0)
 
 // v-columns [w0, w1) an item reads (lim = width of its vector: m or m + na);
 // T = the item's tiles.
+__device__ __forceinline__ bool is_chunk(const Item &it) { return it.seg > 0 && it.seg != kWhole; }
 __device__ __forceinline__ void item_window(const Item &it, const tsb_ldlt_tile *T, int lim, int &w0, int &w1) {
-    if (it.seg) {
+    if (is_chunk(it)) {
         int s0, s1;
         chunk_range(it, T[0], s0, s1);
         w0 = T[0].tl + 2 * s0 * kSegPairs;
@@ -397,9 +403,9 @@ __device__ __forceinline__ void sweep_producer(SweepRing &R, const tsb_ldlt_desc
             if (k >= 2) wait_serving(R, &R.taken[e], ((k >> 1) - 1) & 1u, p, live);
             M.it = it;
             M.B = B;
-            if (it.seg > 0) {
+            if (is_chunk(it)) {
                 M.T[0] = T0;
-            } else if (it.seg == 0) {
+            } else if (it.seg >= 0) {  // small groups / whole tiles: every tile
                 for (int t = it.t0; t < it.t1; ++t) M.T[t - it.t0] = t == it.t0 ? T0 : tiles[t];
             }
             if (it.seg >= 0) item_window(it, M.T, B.m + (upper ? B.na : 0), M.w0, M.w1);
@@ -429,7 +435,21 @@ __device__ __forceinline__ void sweep_producer(SweepRing &R, const tsb_ldlt_desc
         if (iid >= n_items) break;
         int s0 = 0, s1 = 1, g0 = 0;
         const int nt = it.t1 - it.t0;
-        if (it.seg > 0) chunk_range(it, T0, s0, s1);
+        if (is_chunk(it)) chunk_range(it, T0, s0, s1);
+        if (it.seg == kWhole) {  // every segment of every tile, in order
+            for (int t = 0; t < nt; ++t) {
+                const tsb_ldlt_tile &Tt = M.T[t];
+                const int ns = (Tt.np + kSegPairs - 1) / kSegPairs;
+                for (int sg = 0; sg < ns; ++sg, ++q) {
+                    const int st = q % kStages;
+                    if (q >= (uint32_t)kStages) wait_serving(R, &R.empty[st], ((q / kStages) - 1) & 1u, p, live);
+                    const int p0 = sg * kSegPairs, cnt = min(kSegPairs, Tt.np - p0);
+                    tma_load_1d(stage + st * kStage, base + Tt.off + (int64_t)p0 * (2 * kTile),
+                                (uint32_t)(cnt * 2 * kTile * 8), &R.full[st]);
+                }
+            }
+            continue;
+        }
         for (int sg = s0; it.seg == 0 ? g0 < nt : sg < s1; ++sg, ++q) {
             const int st = q % kStages;
             if (q >= (uint32_t)kStages) wait_serving(R, &R.empty[st], ((q / kStages) - 1) & 1u, p, live);
@@ -541,6 +561,30 @@ __device__ __forceinline__ void item_gemv(SweepRing &R, uint32_t &q, const Item 
             csync();
             ring_release(R, q);
             g0 = g1;
+        }
+        return;
+    }
+    if (it.seg == kWhole) {  // whole tiles, one after the other: segments split over the warps
+        const int nt = it.t1 - it.t0;
+        for (int t = 0; t < nt; ++t) {
+            const tsb_ldlt_tile T = tiles[t];
+            const int ns = (T.np + kSegPairs - 1) / kSegPairs;
+            double acc = 0.0;
+            for (int sg = 0; sg < ns; ++sg, ++q) {
+                const double *sd = ring_wait(R, q, stage);
+                const int p0 = sg * kSegPairs, cnt = min(kSegPairs, T.np - p0);
+                acc += tile_dot(sd, v + T.tl + 2 * p0, warp, cnt, kWarps, lane);
+                csync();
+                ring_release(R, q);
+            }
+            red[warp * 32 + lane] = acc;
+            csync();
+            if (threadIdx.x < 32) {  // the sum a one-chunk item of the tile emits
+                double a = 0.0;
+#pragma unroll
+                for (int w = 0; w < kWarps; ++w) a += red[w * 32 + threadIdx.x];
+                if ((int)threadIdx.x < T.nrows) emit(T.row0 + threadIdx.x, 0.0 + a);
+            }
         }
         return;
     }
@@ -664,6 +708,36 @@ __device__ __forceinline__ void item_gemv_multi(SweepRing &R, uint32_t &q, const
             csync();
             ring_release(R, q);
             g0 = g1;
+        }
+        return;
+    }
+    if (it.seg == kWhole) {  // as item_gemv
+        const int nt = it.t1 - it.t0;
+        for (int t = 0; t < nt; ++t) {
+            const tsb_ldlt_tile T = tiles[t];
+            const int ns = (T.np + kSegPairs - 1) / kSegPairs;
+            double acc[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[j] = 0.0;
+            for (int sg = 0; sg < ns; ++sg, ++q) {
+                const double *sd = ring_wait(R, q, stage);
+                const int p0 = sg * kSegPairs, cnt = min(kSegPairs, T.np - p0);
+                tile_dot_nr(nr, sd, v + T.tl + 2 * p0, vstride, warp, cnt, kWarps, lane, out);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc[j] += out[j];
+                csync();
+                ring_release(R, q);
+            }
+            for (int j = 0; j < nr; ++j) red[(j * kWarps + warp) * 32 + lane] = acc[j];
+            csync();
+            for (int idx = threadIdx.x; idx < 32 * nr; idx += kCThreads) {
+                const int j = idx >> 5, l = idx & 31;
+                double a = 0.0;
+#pragma unroll
+                for (int w = 0; w < kWarps; ++w) a += red[(j * kWarps + w) * 32 + l];
+                if (l < T.nrows) emit(T.row0 + l, j, 0.0 + a);
+            }
+            csync();  // red is rewritten by the next tile
         }
         return;
     }
@@ -819,7 +893,7 @@ __device__ __forceinline__ void lower_sweep_body(const tsb_ldlt_desc &D, const S
                 for (int j = 0; j < nr; ++j) batched<In, kLoaders>(nw, In{A, xs + j * xstride, s + w0, j});
         }
         if (tid < nr) xs[tid * xstride + nw] = 0.0;  // column pad of odd-width tiles
-        const tsb_ldlt_tile &Tf = M.T[0], &Tb = M.T[it.seg ? 0 : it.t1 - 1 - it.t0];
+        const tsb_ldlt_tile &Tf = M.T[0], &Tb = M.T[is_chunk(it) ? 0 : it.t1 - 1 - it.t0];
         const int r_hi = Tb.row0 + Tb.nrows, mr0 = max(Tf.row0, m);
         const int64_t cb0 = B.mode == 1 ? __ldg(D.d_cin_ptr + s + w0) : 0;
         if (tid < kLoaders) {

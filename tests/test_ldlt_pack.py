@@ -59,8 +59,10 @@ def emulate_lower(H, r):
         else:
             assert B["target_l"] == 0
             xs = r[s:s + m].copy()
-        for t in ([t0] if sg > 0 else range(t0, t1)):
-            if sg:  # segment item: the tile's rows are emitted by its last segment
+        for t in ([t0] if 0 < sg < K.WHOLE else range(t0, t1)):
+            if sg == K.WHOLE:  # whole-tiles item: each tile complete (one chunk)
+                segs[t] += H["tiles_l"]["nseg"][t]
+            elif sg:  # segment item: the tile's rows are emitted by its last segment
                 segs[t] += 1
                 if segs[t] < H["tiles_l"]["nseg"][t]:
                     continue
@@ -109,8 +111,10 @@ def emulate_upper(H, w, z=None):
             p = int(B["parent"])
             assert done[p] == blocks[p]["n_u"], "upper item dispatched before the parent's z"
         v = np.concatenate([w[s:s + m], -z[H["anc"][B["anc_off"]: B["anc_off"] + na]]])
-        for t in ([t0] if sg > 0 else range(t0, t1)):
-            if sg:
+        for t in ([t0] if 0 < sg < K.WHOLE else range(t0, t1)):
+            if sg == K.WHOLE:
+                segs[t] += H["tiles_u"]["nseg"][t]
+            elif sg:
                 segs[t] += 1
                 if segs[t] < H["tiles_u"]["nseg"][t]:
                     continue
