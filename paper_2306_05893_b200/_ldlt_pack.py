@@ -83,6 +83,7 @@ WHOLE = 1 << 20         # Item.seg of a whole-tiles item (csrc kWhole)
 # one-chunk large tiles of a block grouped into whole-tiles items (no partial
 # slots, one dependency wait and publication for several tiles)
 WHOLE_ITEMS = os.environ.get("TSB_WHOLE_ITEMS", "1") != "0"
+WHOLE_SEGS = int(os.environ["TSB_WHOLE_SEGS"]) if "TSB_WHOLE_SEGS" in os.environ else None  # segments per whole item
 WARPS = 7               # consumer warps per CTA (csrc kWarps): one small tile each
 MAIL_TILES = MAX_GROUPS * WARPS  # tiles one mailbox entry holds (csrc kMailTiles)
 MERGE_ROWS = 0          # default subtree amalgamation (rows); 0 = off
@@ -303,8 +304,9 @@ def _items(tiles_of_block, first_tile, segs, groups_per_item):
         if npair * TILE * 16 > ITEM_BYTES:
             if WHOLE_ITEMS and nseg(k) <= segs:  # consecutive one-chunk tiles: one item
                 k1, tot = k, 0
+                budget = WHOLE_SEGS if WHOLE_SEGS is not None else segs
                 while (k1 < nt and k1 - k < MAIL_TILES and tiles_of_block[k1][1] * TILE * 16 > ITEM_BYTES
-                       and tot + nseg(k1) <= segs):
+                       and nseg(k1) <= segs and (k1 == k or tot + nseg(k1) <= budget)):
                     tot += nseg(k1)
                     k1 += 1
                 out.append((first_tile + k, first_tile + k1, WHOLE))

@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--ratios", default="")
     ap.add_argument("--segs-lower", default="", help="lower-sweep segments per chunk (default: --segs)")
+    ap.add_argument("--whole", default="", help="segments per whole-tiles item (default: --segs)")
     args = ap.parse_args()
     import torch
 
@@ -54,14 +55,15 @@ def main():
 
     ratios = [float(v) for v in args.ratios.split(",")] if args.ratios else [None]
     lowers = [int(v) for v in args.segs_lower.split(",")] if args.segs_lower else [None]
-    for ratio, sl in [(r_, l_) for r_ in ratios for l_ in lowers]:
-        K.SEGS_LOWER = sl
+    wholes = [int(v) for v in args.whole.split(",")] if args.whole else [None]
+    for ratio, sl, wh in [(r_, l_, w_) for r_ in ratios for l_ in lowers for w_ in wholes]:
+        K.SEGS_LOWER, K.WHOLE_SEGS = sl, wh
         K.GATHER_RATIO = ratio
         for sg in map(int, args.segs.split(",")):
             for gr in map(int, args.groups.split(",")):
                 K.SEGS_PER_ITEM, K.GROUPS_PER_ITEM = sg, min(gr, K.MAX_GROUPS)  # overrides of item_granularity (csrc kGroupsPerItem)
                 dev = K.DevicePanels(f)
-                row = {"segs": sg, "segs_lower": sl, "groups": gr, "ratio": ratio, "apply_ms": timed(dev, "apply"),
+                row = {"segs": sg, "segs_lower": sl, "whole": wh, "groups": gr, "ratio": ratio, "apply_ms": timed(dev, "apply"),
                        "lower_ms": timed(dev, "lower"), "upper_ms": timed(dev, "upper"), "items": dev.n_items}
                 print(json.dumps(row), flush=True)
                 out.append(row)
