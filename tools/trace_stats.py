@@ -18,7 +18,9 @@ def main(path):
         take, ready, end, st, cp = [(tr[:, k] - t0) / 1e3 for k in (0, 1, 2, 4, 5)]
         seg = it[:, 3]
         print(nm, "items", len(tr), "wall %.1f us" % end.max())
-        for name, mask in (("chunk", seg > 0), ("small", seg == 0), ("fin", seg < 0)):
+        WHOLE = 1 << 20  # csrc kWhole: whole-tiles items
+        for name, mask in (("chunk", (seg > 0) & (seg != WHOLE)), ("whole", seg == WHOLE), ("small", seg == 0),
+                           ("fin", seg < 0)):
             if mask.sum() == 0:
                 continue
             if name == "fin":
