@@ -204,6 +204,54 @@ __global__ void __launch_bounds__(256, MINB) ks(int n, const int *__restrict__ r
     }
 }
 
+// SELL-32: a warp owns a slice of 32 consecutive rows stored column-major
+// (entry k of the slice's row i at base + k*32 + i; padded to the slice's
+// longest row), one lane per row: every value / column load is one coalesced
+// 256 / 128 B access.  Each lane keeps the 8 strided partial sums of its row
+// in registers, batch by batch of 8 terms, and sums exactly as reduceat
+// (rows of <= 129 entries).
+__global__ void __launch_bounds__(256, 4) ksell(int n, const long long *__restrict__ sbase,
+                                                const int *__restrict__ lens, const int *__restrict__ sc,
+                                                const double *__restrict__ sv, const double *__restrict__ x,
+                                                double *__restrict__ y) {
+    const int lane = threadIdx.x & 31;
+    const int nslices = (n + 31) / 32;
+    for (int sl = (blockIdx.x * 8 + (threadIdx.x >> 5)); sl < nslices; sl += gridDim.x * 8) {
+        const int row = sl * 32 + lane;
+        const long long b = sbase[sl];
+        const int len = row < n ? lens[row] : 0;
+        const double *vv = sv + b + lane;
+        const int *cc = sc + b + lane;
+        auto term = [&](int k) -> double { return mul(__ldg(vv + 32LL * k), __ldg(x + __ldg(cc + 32LL * k))); };
+        if (len <= 0) {
+            if (row < n) y[row] = 0.0;
+            continue;
+        }
+        const double p0 = term(0);
+        const int nn = len - 1, nfull = nn >> 3, tail = nn & 7;
+        double a0 = 0, a1 = 0, a2 = 0, a3 = 0, a4 = 0, a5 = 0, a6 = 0, a7 = 0;
+        for (int m = 0; m < nfull; ++m) {
+            const int k = 1 + 8 * m;
+            const double t0 = term(k), t1 = term(k + 1), t2 = term(k + 2), t3 = term(k + 3);
+            const double t4 = term(k + 4), t5 = term(k + 5), t6 = term(k + 6), t7 = term(k + 7);
+            if (m == 0) {
+                a0 = t0; a1 = t1; a2 = t2; a3 = t3; a4 = t4; a5 = t5; a6 = t6; a7 = t7;
+            } else {
+                a0 = add(a0, t0); a1 = add(a1, t1); a2 = add(a2, t2); a3 = add(a3, t3);
+                a4 = add(a4, t4); a5 = add(a5, t5); a6 = add(a6, t6); a7 = add(a7, t7);
+            }
+        }
+        double res = nfull > 0 ? add(add(add(a0, a1), add(a2, a3)), add(add(a4, a5), add(a6, a7))) : -0.0;
+        double tt[7];
+#pragma unroll
+        for (int u = 0; u < 7; ++u) tt[u] = u < tail ? term(1 + 8 * nfull + u) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 7; ++u)
+            if (u < tail) res = add(res, tt[u]);
+        y[row] = add(p0, res);
+    }
+}
+
 // V4: 4 lanes per row, two strided accumulators per lane (r_l, r_{l+4}), the
 // tail and the first product in lane 0 -- exact order, fewer shuffles.
 template <int MINB>
@@ -353,6 +401,45 @@ int main(int argc, char **argv) {
     run("ks rpw4 minb6", [&] { ks<4, 6, 336><<<148 * 6, 256>>>(n, drp, dci, dval, dx, dy); }, true);
     run("ks rpw8 minb5", [&] { ks<8, 5, 680><<<148 * 5, 256>>>(n, drp, dci, dval, dx, dy); }, true);
     run("ks rpw8 minb4", [&] { ks<8, 4, 680><<<148 * 4, 256>>>(n, drp, dci, dval, dx, dy); }, true);
+    {  // SELL-32 layout on the host
+        std::vector<int> hrp(n + 1), hci(nnz);
+        memcpy(hrp.data(), rp.data(), rp.size());
+        memcpy(hci.data(), ci.data(), ci.size());
+        const double *hv = reinterpret_cast<const double *>(val.data());
+        const int ns = (n + 31) / 32;
+        std::vector<long long> base(ns + 1, 0);
+        std::vector<int> lens(n);
+        for (int r = 0; r < n; ++r) lens[r] = hrp[r + 1] - hrp[r];
+        for (int s = 0; s < ns; ++s) {
+            int w = 0;
+            for (int r = s * 32; r < std::min(n, s * 32 + 32); ++r) w = std::max(w, lens[r]);
+            base[s + 1] = base[s] + 32LL * w;
+        }
+        std::vector<int> scol(base[ns], 0);
+        std::vector<double> sval(base[ns], 0.0);
+        for (int r = 0; r < n; ++r) {
+            const int s = r / 32, i = r % 32;
+            for (int k = 0; k < lens[r]; ++k) {
+                scol[base[s] + 32LL * k + i] = hci[hrp[r] + k];
+                sval[base[s] + 32LL * k + i] = hv[hrp[r] + k];
+            }
+        }
+        printf("SELL-32: %lld stored entries (%.2fx nnz)\n", base[ns], (double)base[ns] / nnz);
+        long long *dbase;
+        int *dlens, *dsc;
+        double *dsv;
+        CK(cudaMalloc(&dbase, 8L * (ns + 1)));
+        CK(cudaMalloc(&dlens, 4L * n));
+        CK(cudaMalloc(&dsc, 4L * base[ns]));
+        CK(cudaMalloc(&dsv, 8L * base[ns]));
+        CK(cudaMemcpy(dbase, base.data(), 8L * (ns + 1), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(dlens, lens.data(), 4L * n, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(dsc, scol.data(), 4L * base[ns], cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(dsv, sval.data(), 8L * base[ns], cudaMemcpyHostToDevice));
+        for (int g : {148 * 4, 148 * 8, 148 * 16})
+            run(g == 592 ? "sell32 grid 4/SM" : g == 1184 ? "sell32 grid 8/SM" : "sell32 grid 16/SM",
+                [&] { ksell<<<g, 256>>>(n, dbase, dlens, dsc, dsv, dx, dy); }, true);
+    }
     run("k4 exact minb8", [&] { k4<8><<<148 * 8, 256>>>(n, drp, dci, dval, dx, dy); }, true);
     run("k4 exact minb6", [&] { k4<6><<<148 * 6, 256>>>(n, drp, dci, dval, dx, dy); }, true);
     run("k4 exact minb4", [&] { k4<4><<<148 * 4, 256>>>(n, drp, dci, dval, dx, dy); }, true);
