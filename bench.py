@@ -922,7 +922,8 @@ def run_reference_batched(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--steps", type=int, default=None,
+                    help="timed steps (default 100; the reference arm's CPU samples default to 10)")
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--workload", default="cfg3", choices=sorted(WORKLOADS))
     ap.add_argument("--precond", default="ldlt", choices=["ldlt", "jacobi"])
@@ -937,6 +938,8 @@ def main():
                     help="all ranks on cuda:0 (gloo group + peer exchange): exercises the N > 1 path on one GPU")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.steps is None:  # defaults that finish within minutes on either arm
+        args.steps = 10 if args.impl == "reference" else 100
     if args.impl == "reference":
         return run_reference(args)
 
