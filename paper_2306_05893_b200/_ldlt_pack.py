@@ -96,6 +96,7 @@ CB_CAP = 1024           # contributions staged per piece when a block's items su
 # 1.82 ms (1) vs 1.70 (0).  TSB_GATHER_RATIO overrides.
 GATHER_RATIO = float(os.environ["TSB_GATHER_RATIO"]) if "TSB_GATHER_RATIO" in os.environ else None
 GATHER_BIG_BYTES = 512 << 20  # stored lower tiles above this: bandwidth-bound regime
+GATHER_FEW = int(os.environ.get("TSB_GATHER_FEW", "0"))  # tuning: small blocks with <= this many items gather
 
 BLOCK_DTYPE = np.dtype([
     ("start", "<i4"), ("m", "<i4"), ("na", "<i4"), ("parent", "<i4"),
@@ -586,6 +587,9 @@ def pack(factors, subset=None, sink=None, alloc=None):
     ratio = GATHER_RATIO if GATHER_RATIO is not None else (0.0 if pos[False] * 8 > GATHER_BIG_BYTES else 1.0)
     mode = np.where(target_l == 0, MODE_LEAF,
                     np.where(nl * blk_contrib <= ratio * gsize, MODE_GATHER, MODE_FIN))
+    if GATHER_FEW:  # blocks of <= GATHER_FEW items whose contributions one finaliser would sum: gather
+        few = (target_l > 0) & (nl <= GATHER_FEW) & (blk_contrib <= FIN_CONTRIB)
+        mode = np.where(few, MODE_GATHER, mode)
     nfin = np.where(mode == MODE_FIN,
                     np.minimum(np.minimum(32, (ms_ + 31) // 32), np.maximum(1, (blk_contrib + FIN_CONTRIB - 1) // FIN_CONTRIB)),
                     0)

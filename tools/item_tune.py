@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--ratios", default="")
     ap.add_argument("--segs-lower", default="", help="lower-sweep segments per chunk (default: --segs)")
     ap.add_argument("--whole", default="", help="segments per whole-tiles item (default: --segs)")
+    ap.add_argument("--few", default="", help="K.GATHER_FEW values")
     args = ap.parse_args()
     import torch
 
@@ -56,14 +57,15 @@ def main():
     ratios = [float(v) for v in args.ratios.split(",")] if args.ratios else [None]
     lowers = [int(v) for v in args.segs_lower.split(",")] if args.segs_lower else [None]
     wholes = [int(v) for v in args.whole.split(",")] if args.whole else [None]
-    for ratio, sl, wh in [(r_, l_, w_) for r_ in ratios for l_ in lowers for w_ in wholes]:
-        K.SEGS_LOWER, K.WHOLE_SEGS = sl, wh
+    fews = [int(v) for v in args.few.split(",")] if args.few else [K.GATHER_FEW]
+    for ratio, sl, wh, fw in [(r_, l_, w_, f_) for r_ in ratios for l_ in lowers for w_ in wholes for f_ in fews]:
+        K.SEGS_LOWER, K.WHOLE_SEGS, K.GATHER_FEW = sl, wh, fw
         K.GATHER_RATIO = ratio
         for sg in map(int, args.segs.split(",")):
             for gr in map(int, args.groups.split(",")):
                 K.SEGS_PER_ITEM, K.GROUPS_PER_ITEM = sg, min(gr, K.MAX_GROUPS)  # overrides of item_granularity (csrc kGroupsPerItem)
                 dev = K.DevicePanels(f)
-                row = {"segs": sg, "segs_lower": sl, "whole": wh, "groups": gr, "ratio": ratio, "apply_ms": timed(dev, "apply"),
+                row = {"segs": sg, "segs_lower": sl, "whole": wh, "few": fw, "groups": gr, "ratio": ratio, "apply_ms": timed(dev, "apply"),
                        "lower_ms": timed(dev, "lower"), "upper_ms": timed(dev, "upper"), "items": dev.n_items}
                 print(json.dumps(row), flush=True)
                 out.append(row)
