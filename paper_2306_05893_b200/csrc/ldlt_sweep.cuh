@@ -1008,7 +1008,7 @@ __device__ __forceinline__ void upper_sweep_body(const tsb_ldlt_desc &D, const S
         trace(tbuf, iid, 0);
         const Item it = M.it;
         const tsb_ldlt_block B = M.B;
-        const int m = B.m, s = B.start, na = B.na;
+        const int m = B.m, s = B.start;
         const int w0 = M.w0, w1 = M.w1;
         const int nw = w1 - w0;
         dep_spin(M);  // -z_anc in the window: the parent's items; meanwhile the others fetch:

@@ -65,6 +65,9 @@ struct PcgArgs {
 };
 
 constexpr int kPcgBlock = 256;
+#ifndef TSB_LDLT_RPG
+#define TSB_LDLT_RPG 2  // rows per 8-lane group in flight in the LDL^T kernel's SpMV (build-time A/B)
+#endif
 constexpr int64_t kFuseRows = 150000;
 constexpr int kMaxGrid = kNumSM * 8;
 
@@ -279,7 +282,7 @@ pcg_persistent(PcgWork W, PcgArgs a, tsb_ldlt_desc D) {
                 W.ap[row] = s;
                 v += __ldcg(pcur + row) * s;
             };
-            rows_exact<2>(grp, ngrp, n, a.rp, a.ci, a.val, xa, lane8, gmask, out);
+            rows_exact<TSB_LDLT_RPG>(grp, ngrp, n, a.rp, a.ci, a.val, xa, lane8, gmask, out);
         } else {
             XPlainCG xa{pcur};
             for (int64_t row = grp; row < n; row += ngrp) {
