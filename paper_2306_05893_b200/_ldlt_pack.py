@@ -87,7 +87,7 @@ WHOLE_SEGS = int(os.environ["TSB_WHOLE_SEGS"]) if "TSB_WHOLE_SEGS" in os.environ
 WARPS = 7               # consumer warps per CTA (csrc kWarps): one small tile each
 MAIL_TILES = MAX_GROUPS * WARPS  # tiles one mailbox entry holds (csrc kMailTiles)
 MERGE_ROWS = 0          # default subtree amalgamation (rows); 0 = off
-CB_CAP = 1024           # contributions staged per piece when a block's items sum them (csrc max_cb)
+CB_CAP = int(os.environ.get("TSB_CB_CAP", "1024"))  # contributions staged per piece when a block's items sum them (csrc max_cb)
 # lower input mode: a block's items sum their contributions themselves while the
 # redundant reads (items x contributions) stay below ratio x its factor entries,
 # else finaliser items form x_b once.  Latency-bound (small) factors favour the

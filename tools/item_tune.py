@@ -30,6 +30,7 @@ def main():
     ap.add_argument("--segs-lower", default="", help="lower-sweep segments per chunk (default: --segs)")
     ap.add_argument("--whole", default="", help="segments per whole-tiles item (default: --segs)")
     ap.add_argument("--few", default="", help="K.GATHER_FEW values")
+    ap.add_argument("--cbcap", type=int, default=None, help="K.CB_CAP (contribution staging; 0 = sum from L2)")
     args = ap.parse_args()
     import torch
 
@@ -54,6 +55,8 @@ def main():
             ts.append(e0.elapsed_time(e1))
         return statistics.median(ts)
 
+    if args.cbcap is not None:
+        K.CB_CAP = args.cbcap
     ratios = [float(v) for v in args.ratios.split(",")] if args.ratios else [None]
     lowers = [int(v) for v in args.segs_lower.split(",")] if args.segs_lower else [None]
     wholes = [int(v) for v in args.whole.split(",")] if args.whole else [None]
