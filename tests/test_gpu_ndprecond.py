@@ -112,3 +112,35 @@ def test_async_device_every_k_policy_and_staleness(rng):
     x, rep = krylov.pcg(a, rng.standard_normal(40), pre, krylov.SolverConfig(1e-9, 50))
     assert rep.converged and rep.iterations <= 2
     pre.close()
+
+
+@pytest.mark.parametrize("segs", [2, 8])
+def test_whole_tile_items_apply_identical(monkeypatch, segs):
+    """The sweeps with whole-tiles items (several one-chunk tiles per item,
+    each emitted from the warp reduction) give the apply of the chunk-item
+    packing bit for bit -- the per-tile sums are the same -- and match the
+    oracle."""
+    import torch
+
+    from conftest import clamped_beam
+    from paper_2306_05893_b200 import _ldlt_pack as K, mesh as M
+
+    mesh = clamped_beam(10, 10, 60)
+    rest = O.rest_data(mesh.nodes, mesh.elements, 1e5, 0.3, 1000.0)
+    out = O.assemble_system(mesh.nodes, mesh.elements, mesh.fixed_nodes, rest, mesh.nodes,
+                            np.zeros_like(mesh.nodes), np.zeros(mesh.ndof), 0.01, (0.0, -9.81, 0.0))
+    a = CsrMatrix(mesh.ndof, mesh.ndof, out["row_ptr"], out["col_ind"], out["values"])
+    f = ND.ldlt_factor(a, ND.expand_plan(ND.nested_dissection(M.vertex_adjacency(mesh), 64)))
+    monkeypatch.setattr(K, "SEGS_PER_ITEM", segs)
+    r = torch.from_numpy(np.random.default_rng(5).standard_normal(mesh.ndof)).cuda()
+    zs = []
+    for whole in (False, True):
+        monkeypatch.setattr(K, "WHOLE_ITEMS", whole)
+        dev = K.DevicePanels(f)
+        z = torch.empty_like(r)
+        dev.run("apply", r, z)
+        zs.append(z.cpu().numpy())
+        del dev
+    assert np.array_equal(zs[0], zs[1])
+    ref = O.apply(f, r.cpu().numpy())
+    assert np.abs(zs[1] - ref).max() <= 1e-12 * np.abs(ref).max()

@@ -259,3 +259,31 @@ def test_block_inverse_conditioning_guard(caplog):
     fi = ND.ldlt_factor(a, plan)
     Hi = K.pack(fi)
     assert Hi["cond_l11"] > K.COND_WARN
+
+
+@pytest.mark.parametrize("segs", [2, 8])
+def test_whole_tile_items(monkeypatch, segs):
+    """Whole-tiles items (seg == WHOLE): only large tiles of one chunk each,
+    consecutive in one block, <= segs segments and <= MAIL_TILES tiles in all;
+    every other large tile keeps its chunk items; the emulated sweeps still
+    reproduce the oracle."""
+    mesh, f = _factors((10, 10, 60), 64)
+    monkeypatch.setattr(K, "SEGS_PER_ITEM", segs)
+    H = K.pack(f)
+    for up, key, tkey in ((False, "items_l", "tiles_l"), (True, "items_u", "tiles_u")):
+        T = H[tkey]
+        big = T["np"].astype(np.int64) * K.TILE * 16 > K.ITEM_BYTES
+        nseg = (T["np"].astype(np.int64) + K.SEG_PAIRS - 1) // K.SEG_PAIRS
+        seen = np.zeros(len(T), dtype=bool)
+        for b, t0, t1, sg in H[key]:
+            if sg == K.WHOLE:
+                assert 0 < t1 - t0 <= K.MAIL_TILES and big[t0:t1].all() and (nseg[t0:t1] <= segs).all()
+                assert nseg[t0:t1].sum() <= segs or t1 - t0 == 1
+                assert not seen[t0:t1].any()
+                seen[t0:t1] = True
+            elif sg > 0:  # chunk item of a tile too wide for one chunk (or whole items off)
+                assert big[t0]
+        assert (seen == (big & (nseg <= segs))).all()  # every one-chunk large tile is in a whole item
+    r = np.random.default_rng(11).standard_normal(mesh.ndof)
+    assert np.abs(emulate_lower(H, r) - O.solve_lower(f, r)).max() <= 1e-12 * np.abs(O.solve_lower(f, r)).max()
+    assert np.abs(emulate_upper(H, r) - O.solve_upper(f, r)).max() <= 1e-12 * np.abs(O.solve_upper(f, r)).max()
